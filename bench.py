@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""bench.py -- effective FP64 GFLOP/s (2MNK/t) of the recursive fast-matrix-multiplication hot
+path (arXiv 1507.00687) on B200, BASELINE.json configs[4] (C5): M = K = N = 32768, FP64,
+Strassen-Winograd, 3 levels, A, B ~ U(-1,1) seed 4.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fmm|reference] [--dtype f64|f32]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, NCCL)
+
+One step = one complete C = A.B through the C ABI (fmm_execute): every K1 / K2 / K3 / ACC launch
+of the plan (plus, for N > 1, the ncclReduce of the partial C onto rank 0).  Work is strong-
+scaled: the 7 top-level products are split round-robin over the ranks.  Timing: W untimed
+steps, then K steps bracketed by barrier + synchronize, CUDA events on the launch stream, max
+over ranks.  The operands (8 GiB each) exceed the 126 MB L2, so no flush is needed.
+
+The JSON line also carries: `e2e` (same metric through fmm_execute_host with pinned host
+buffers, copies inside the timed region), `roofline` (the leaf-product kernel K2 against the
+measured FP64 DMMA peak), `cpu_baseline` (the CPU oracle on a bounded row/column sample of the
+same workload), `clocks` (nvidia-smi sampled during the timed region) and `gpu_launches`.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "effective FP64 GFLOP/s (2MNK/t) at 1/2/4/8 B200 and max-norm error vs oracle"
+UNIT = "GFLOP/s"
+FP64_DMMA_PEAK_TFLOPS = 36.9  # profiles/r01_fp64_peak_microbench.txt (mma.sync f64, 1965 MHz)
+TF32_PEAK_TFLOPS_NOMINAL = 1100.0  # B200_PROFILING.md nominal dense tf32 (fallback)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while active."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def load_traffic(workload: str):
+    """Per-launch DRAM bytes of K2 from a committed ncu --set full capture (or None)."""
+    f = ROOT / "profiles" / "k2_traffic.json"
+    if not f.exists():
+        return None
+    try:
+        d = json.loads(f.read_text())
+        return d.get(workload)
+    except (OSError, ValueError):
+        return None
+
+
+def make_inputs(M, K, N, seed, dtype):
+    """C5 inputs drawn by the shared recipe (fmm_inputs) straight into pinned host memory."""
+    import fmm_inputs as fi
+    t0 = time.time()
+    A, B = fi.draw_torch("u(-1,1)", M, K, N, seed, pin=True)
+    if dtype == "f32":
+        A, B = A.float().pin_memory(), B.float().pin_memory()
+    log(f"[bench] inputs {M}x{K}x{N} generated in {time.time() - t0:.1f}s")
+    return A, B
+
+
+# ------------------------------------------------------------------------------------------
+def cpu_baseline(A_host, B_host, plan_rules, M, K, N, C_gpu_host=None, target_s=15.0):
+    """The CPU oracle, as it stands, on a bounded row/column sample of the same workload:
+    rows G = lift_rows(leaf rows), columns H = lift_cols(leaf cols) (bitwise the oracle's own
+    entries of C, oracle.fmm_sub).  Value = 2 |G| |H| K / t."""
+    import numpy as np
+    import oracle
+    from oracle import rules as OR
+    plan = OR.Plan.uniform([OR.builtin(n) for n in plan_rules])
+    A = A_host.numpy() if hasattr(A_host, "numpy") else A_host
+    B = B_host.numpy() if hasattr(B_host, "numpy") else B_host
+    pm, _, pn = plan.dims_divisor()
+    # calibrate: one leaf row/col first, then scale to ~target_s
+    nr = 1
+    res = None
+    while True:
+        G = oracle.lift_rows(M, plan, range(nr))
+        H = oracle.lift_cols(N, plan, range(nr))
+        Ag = np.ascontiguousarray(A[G, :])
+        Bh = np.ascontiguousarray(B[:, H])
+        t0 = time.perf_counter()
+        Cs = oracle.fmm(Ag, Bh, plan)
+        t = time.perf_counter() - t0
+        res = (nr, G, H, Cs, t)
+        if t > target_s / 5 or nr * 2 > min(M // pm, N // pn) or nr >= 1024:
+            break
+        nr *= 2
+    nr, G, H, Cs, t = res
+    flops = 2.0 * len(G) * len(H) * K
+    out = {"value": flops / t / 1e9, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+           "sample": f"C[G,H] with |G|={len(G)} rows x |H|={len(H)} cols (leaf rows/cols 0..{nr - 1} "
+                     f"lifted through all levels; oracle.fmm_sub, bitwise the full oracle's entries)",
+           "seconds": t}
+    if C_gpu_host is not None:
+        Cg = C_gpu_host[np.ix_(G, H)]
+        out["parity_sampled"] = oracle.parity_metric(Cg, Cs, float(np.abs(A).max()),
+                                                     float(np.abs(B).max()), K)
+    return out
+
+
+# ------------------------------------------------------------------------------------------
+def run_reference(args):
+    """--impl reference: the CPU oracle (this tier's reference arm) timed on bounded samples of
+    the same workload, rank 0 only."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+    import oracle
+    from oracle import rules as OR
+    M = K = N = 32768
+    rules = ("winograd",) * 3
+    oracle.build()
+    A, B = make_inputs(M, K, N, 4, "f64")
+    An, Bn = A.numpy(), B.numpy()
+    plan = OR.Plan.uniform([OR.builtin(n) for n in rules])
+    nr = args.ref_sample
+    times = []
+    for step in range(args.warmup + args.steps):
+        rows = [(step * nr + i) % (M // 8) for i in range(nr)]
+        G = oracle.lift_rows(M, plan, rows)
+        H = oracle.lift_cols(N, plan, rows)
+        t0 = time.perf_counter()
+        oracle.fmm(np.ascontiguousarray(An[G, :]), np.ascontiguousarray(Bn[:, H]), plan)
+        t = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(t)
+    flops = 2.0 * (8 * nr) * (8 * nr) * K
+    total = sum(times)
+    value = flops * len(times) / total / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total / len(times) * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C5: S-W <2,2,2;7> L=3, M=K=N=32768 FP64, U(-1,1) seed 4",
+                       "sample_per_step": f"C[G,H], |G| = |H| = {8 * nr} lifted rows/cols"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(),
+                             "kind": "oracle",
+                             "sample": f"per step C[G,H] with |G|=|H|={8 * nr} (row/col-sampled oracle)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------
+def run_fmm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1507_00687_b200 as fb
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    M = K = N = args.n
+    rules = ("winograd",) * args.levels
+    dt = torch.float64 if args.dtype == "f64" else torch.float32
+    esz = 8 if args.dtype == "f64" else 4
+    leaf = fb.fmm.LEAF_NATIVE if args.dtype == "f64" else args.leaf
+    stream = torch.cuda.Stream()
+
+    # ---- inputs: host (pinned) on rank 0, device copies on every rank -----------------------
+    if rank == 0:
+        A_h, B_h = make_inputs(M, K, N, 4, args.dtype)
+    A = torch.empty((M, K), dtype=dt, device="cuda")
+    B = torch.empty((K, N), dtype=dt, device="cuda")
+    Cd = torch.empty((M, N), dtype=dt, device="cuda")
+    if rank == 0:
+        A.copy_(A_h)
+        B.copy_(B_h)
+    if ws > 1:
+        dist.broadcast(A, 0)
+        dist.broadcast(B, 0)
+    torch.cuda.synchronize()
+
+    plan = fb.Plan([fb.Rule.builtin(r) for r in rules], M, K, N, dtype=args.dtype, leaf=leaf)
+    if ws > 1:
+        uid = [fb.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, 0)
+        plan.set_comm(uid[0], rank, ws)
+    wsp = plan.workspace(A.device)
+    log(f"[bench] rank {rank}: workspace {plan.workspace_bytes() / 2**30:.1f} GiB, "
+        f"{plan.launch_count()} launches / step")
+
+    def step():
+        plan.execute(A, B, Cd, ws=wsp, stream=stream)
+
+    # ---- warm-up ------------------------------------------------------------------------------
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device events, max over ranks) -----------------------------------------
+    sampler = ClockSampler(local)
+    plan.set_timing(True)
+    plan.step_times()  # reset
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    kinds = plan.step_times()
+    plan.set_timing(False)
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    flops = 2.0 * M * N * K
+    value = flops * args.steps / (ms * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (K2, the leaf products) -------------------------------
+    L = args.levels
+    leaf_flops_step = (7 ** L) * 2.0 * (M >> L) * (N >> L) * (K >> L)
+    k2_ms, k2_n = kinds.get("K2", (0.0, 0))
+    per_launch_flops = leaf_flops_step * args.steps / max(k2_n, 1)
+    peak = FP64_DMMA_PEAK_TFLOPS if args.dtype == "f64" else TF32_PEAK_TFLOPS_NOMINAL / (
+        3 if leaf == fb.fmm.LEAF_3XTF32 else 1)
+    achieved = per_launch_flops / (k2_ms / max(k2_n, 1) * 1e-3) / 1e12 if k2_n else None
+    workload = f"C5-{args.dtype}-n{M}-L{L}-p{ws}"
+    roofline = {"kernel": "k2_gemm_f64 (leaf products, DMMA mma.sync f64)" if args.dtype == "f64"
+                else "k2 (leaf products, FP32)",
+                "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": (achieved / peak) if achieved else None,
+                "traffic": load_traffic(workload),
+                "peak_source": "measured FP64 DMMA microbenchmark (profiles/r01_fp64_peak_microbench.txt); "
+                               "MEASURED_PEAKS.json has no FP64 entry" if args.dtype == "f64" else
+                               "B200_PROFILING.md nominal dense TF32 (fallback)",
+                "flops_per_launch": per_launch_flops, "launch_ms": (k2_ms / k2_n) if k2_n else None,
+                "step_share": {k: v[0] / ms for k, v in kinds.items()}}
+
+    # ---- end-to-end through the C ABI with host buffers ---------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        C_h = torch.empty((M, N), dtype=dt).pin_memory() if rank == 0 else None
+        for it in range(args.e2e_warmup + args.steps):
+            if ws > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            if it == args.e2e_warmup:
+                f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                f0.record(stream)
+            if ws == 1:
+                plan.execute_host(A_h, B_h, C_h, A, B, Cd, ws=wsp, stream=stream)
+            else:
+                with torch.cuda.stream(stream):
+                    if rank == 0:
+                        A.copy_(A_h, non_blocking=True)
+                        B.copy_(B_h, non_blocking=True)
+                    dist.broadcast(A, 0)
+                    dist.broadcast(B, 0)
+                    step()
+                    if rank == 0:
+                        C_h.copy_(Cd, non_blocking=True)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1)
+        if ws > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": flops * args.steps / (ems * 1e-3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": (M * K + K * N) * esz, "d2h_bytes_per_step": M * N * esz,
+               "ms_per_step": ems / args.steps}
+
+    # ---- CPU oracle baseline (rank 0, N = 1) ----------------------------------------------------
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        Cg = Cd.cpu().numpy()
+        An = A_h.numpy() if args.dtype == "f64" else A_h.double().numpy()
+        Bn = B_h.numpy() if args.dtype == "f64" else B_h.double().numpy()
+        if args.dtype == "f32":
+            An, Bn = A_h.numpy(), B_h.numpy()
+        cpu = cpu_baseline(An, Bn, rules, M, K, N, C_gpu_host=Cg, target_s=args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": f"C5: Strassen-Winograd <2,2,2;7> L={L}, M=K=N={M} "
+                                   f"{args.dtype.upper()}, A,B ~ U(-1,1) seed 4 (BASELINE configs[4])",
+                       "parallelism": f"top-level r round-robin over {ws} GPU(s)"
+                                      + (", ncclReduce of C" if ws > 1 else ""),
+                       "l2": "operands 8 GiB each >> 126 MB L2 (no flush needed)",
+                       "leaf": {0: "native", 1: "tf32", 2: "3xtf32"}[leaf]},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": plan.launch_count() * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="fmm", choices=["fmm", "reference"])
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--leaf", type=int, default=2, help="FP32 leaf: 0 native, 1 tf32, 2 3xtf32")
+    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--levels", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-warmup", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-sample", type=int, default=16, help="reference arm: leaf rows per step")
+    args = ap.parse_args()
+    ws, _, _ = dist_env()
+    if args.gpus != ws and ws > 1:
+        log(f"[bench] --gpus {args.gpus} but WORLD_SIZE {ws}")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_fmm(args)
+
+
+if __name__ == "__main__":
+    main()

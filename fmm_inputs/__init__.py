@@ -43,12 +43,31 @@ CONFIGS = {
 }
 
 
-def _u(g, shape, a, b):
-    return a + (b - a) * torch.rand(shape, generator=g, dtype=torch.float64)
+def _u(g, shape, a, b, pin=False):
+    """U(a, b) = a + (b - a) * rand, computed in place (rand * (b - a) is exact for the
+    power-of-two widths used, then one rounded addition)."""
+    t = torch.empty(shape, dtype=torch.float64, pin_memory=pin)
+    t.uniform_(0.0, 1.0, generator=g)
+    return t.mul_(b - a).add_(a)
+
+
+def draw_torch(dist: str, M: int, K: int, N: int, seed: int, pin: bool = False):
+    """A, B as float64 CPU torch tensors (optionally in pinned memory, for the benchmark's
+    host buffers).  Only the uniform families support pin=True."""
+    g = torch.Generator("cpu").manual_seed(seed)
+    if dist == "u(-1,1)":
+        return _u(g, (M, K), -1.0, 1.0, pin), _u(g, (K, N), -1.0, 1.0, pin)
+    if dist == "u(0,1)":
+        return _u(g, (M, K), 0.0, 1.0, pin), _u(g, (K, N), 0.0, 1.0, pin)
+    assert not pin
+    return tuple(torch.from_numpy(x) for x in draw(dist, M, K, N, seed))
 
 
 def draw(dist: str, M: int, K: int, N: int, seed: int):
     """A (M x K), B (K x N) as float64 numpy arrays (row-major)."""
+    if dist in ("u(-1,1)", "u(0,1)"):
+        A, B = draw_torch(dist, M, K, N, seed)
+        return A.numpy(), B.numpy()
     g = torch.Generator("cpu").manual_seed(seed)
     if dist == "u(-1,1)":
         A = _u(g, (M, K), -1.0, 1.0)

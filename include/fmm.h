@@ -1,0 +1,240 @@
+/*
+ * fmm.h -- C ABI of the B200-native recursive fast-matrix-multiplication library
+ * (libfmm_b200.so), implementing the hot path of arXiv 1507.00687 (Ballard, Benson, Druinsky,
+ * Lipshitz, Schwartz, "Numerical stability of fast matrix multiplication").
+ * Citations "P:<line>" are lines of the paper's text and the section / equation /
+ * algorithm they fall in.
+ *
+ * General conventions
+ *  - Every entry point is extern "C", takes plain pointers and sizes, and returns fmm_status
+ *    (FMM_OK = 0).  No C++ exception crosses the ABI.  On failure, fmm_last_error() returns a
+ *    thread-local message naming the offending argument / index / CUDA or NCCL error text.
+ *  - Matrices are dense ROW-MAJOR with a leading dimension in elements (ld >= #columns).
+ *    A is M x K, B is K x N, C is M x N: C = A.B.
+ *  - Device pointers ("dev") must be CUDA device memory of the current device; "host" pointers
+ *    are CPU memory.  The caller owns every buffer passed in (A, B, C, workspace, factor
+ *    vectors); the library owns fmm_rule / fmm_plan objects and their small device tables.
+ *  - Work is enqueued asynchronously on the given cudaStream_t (passed as void*; NULL = legacy
+ *    default stream).  Argument errors are reported synchronously; device faults surface as
+ *    FMM_E_CUDA at a later call or synchronisation.
+ *  - Inputs A and B are never modified.  NaN/Inf propagate (no checks).
+ *  - Dtype FMM_F64: double; FMM_F32: float.
+ */
+#ifndef FMM_B200_H
+#define FMM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  FMM_OK = 0,
+  FMM_E_ARG = 1,          /* bad argument (null pointer, negative size, bad enum, ld < cols) */
+  FMM_E_RULE = 2,         /* rule violates the Brent equations (not a bilinear algorithm)    */
+  FMM_E_SHAPE = 3,        /* dims not divisible by the plan's base-case products, mismatch   */
+  FMM_E_ALIGN = 4,        /* pointer / ld alignment requirement not met                      */
+  FMM_E_PRECOND = 5,      /* scaling precondition: an all-zero row or column         */
+  FMM_E_UNSUPPORTED = 6,  /* valid request this build does not implement                     */
+  FMM_E_CUDA = 7,         /* CUDA runtime error                                              */
+  FMM_E_NCCL = 8,         /* NCCL error / NCCL library not loadable                          */
+  FMM_E_OOM = 9,          /* workspace too small / device allocation failed                  */
+  FMM_E_NOT_CONVERGED = 10 /* reserved                                                        */
+} fmm_status;
+
+typedef enum { FMM_F64 = 0, FMM_F32 = 1 } fmm_dtype;
+
+/* Leaf (base-case) classical multiplication kind.
+ *  NATIVE : FP64 -> DMMA tensor-core mma (f64 in, f64 accumulate); FP32 -> FP32 FMA.
+ *  TF32   : FP32 only, single-pass TF32 tensor core (reported variant; fails FP32 parity).
+ *  3XTF32 : FP32 only, hi/lo split 3-pass TF32 tensor core (default for FP32). */
+typedef enum { FMM_LEAF_NATIVE = 0, FMM_LEAF_TF32 = 1, FMM_LEAF_3XTF32 = 2 } fmm_leaf;
+
+/* Diagonal scaling modes (Section 6): outside = Alg. 1, inside = Alg. 2
+ * (P:862-868), out_in / in_out = one O step then one I step (or reverse), repeated = Alg. 3
+ * with the Thm stopping-criterion test. */
+typedef enum {
+  FMM_SCALE_NONE = 0,
+  FMM_SCALE_OUTSIDE = 1,
+  FMM_SCALE_INSIDE = 2,
+  FMM_SCALE_OUT_IN = 3,
+  FMM_SCALE_IN_OUT = 4,
+  FMM_SCALE_REPEATED = 5
+} fmm_scale_mode;
+
+typedef struct {
+  int mode;            /* fmm_scale_mode */
+  int first_step_is_O; /* repeated: 1 = start with an O step (Alg. 3 as printed), 0 = I step */
+  double tau;          /* repeated: stopping tolerance tau; tau < 0 disables the test,
+                          tau = 0 stops only at an exact fixed point */
+  int max_steps;       /* repeated: cap on the number of O/I steps (>= 1)                    */
+  int pow2;            /* 1: round every factor to the nearest power of two      */
+} fmm_scaling;
+
+typedef struct fmm_rule fmm_rule; /* opaque, immutable after creation, thread-safe to share */
+typedef struct fmm_plan fmm_plan; /* opaque; execute() is re-entrant for distinct C / ws   */
+
+/* ---------------------------------------------------------------------------------------
+ * Rules <U,V,W> (Eq. eqn:bilinear_alg)
+ * U is (m0*k0) x R, V is (k0*n0) x R, W is (m0*n0) x R, each ROW-MAJOR int32 numerators;
+ * coefficient = numerator / 2^log2_den.  Row conventions: U/V rows index the entries of
+ * the A/B base-case block in COLUMN-major order (i = ia + m0*ja, j = ja + k0*jb); W rows index
+ * C in ROW-major order (k = ia*n0 + jb).  The Brent equations are checked exactly in int64 over
+ * all (m0k0)(k0n0)(m0n0) triples; on violation returns FMM_E_RULE, *n_violations (nullable) is
+ * the count and fmm_last_error() names the first violated (i,j,k).  Limits: m0*k0, k0*n0,
+ * m0*n0 <= 16, R <= 32, |numerator| < 2^20, 0 <= log2_den <= 8.  `name` (nullable) is copied.
+ * ------------------------------------------------------------------------------------- */
+fmm_status fmm_rule_create(int m0, int k0, int n0, int R, const int32_t* U, const int32_t* V,
+                           const int32_t* W, int log2_den, const char* name, fmm_rule** out,
+                           int64_t* n_violations);
+
+/* Built-in rules: "classical222" (<2,2,2;8>, product r = 4ia + 2ja + jb), "strassen" (App. A,
+ * P:1971-1991, converted to the stated convention, A1), "winograd"
+ * (Strassen-Winograd, coefficients in DESIGN.md A2), "strassen_dalberto"
+ * (<U, (swap (x) I2)V, (I2 (x) swap)W>). */
+fmm_status fmm_rule_builtin(const char* name, fmm_rule** out);
+
+/* Copy out a rule's dims and tables (any output pointer may be NULL; U/V/W must hold the
+ * full table when non-NULL). */
+fmm_status fmm_rule_info(const fmm_rule* rule, int* m0, int* k0, int* n0, int* R, int32_t* U,
+                         int32_t* V, int32_t* W, int* log2_den);
+void fmm_rule_destroy(fmm_rule* rule);
+
+/* ---------------------------------------------------------------------------------------
+ * Plans (Sections 3.2-3.4)
+ *  uniform = 1: nodes[l] is the rule of level l (l = 0 is the root, "level 1" in the paper's
+ *               numbering); n_nodes == levels.  Stationary plans repeat one rule.
+ *  uniform = 0: nodes lists one rule per internal node of the recursion tree in BFS order,
+ *               node [l, r1..r_{l-1}] at index sum_{l'<l} prod R + ((r1 R2 + r2) R3 + ...)
+ *               (0-based r), n_nodes = 1 + R1 + R1 R2 + ....  Rules within a
+ *               level must share (m0,k0,n0,R).
+ *  levels = 0 means the classical algorithm (the leaf) on the whole problem.
+ *  M, K, N must be divisible by prod m0, prod k0, prod n0 (else FMM_E_SHAPE).
+ *  leaf: fmm_leaf; FP64 requires NATIVE.  scaling (nullable = none): applied inside
+ *  fmm_execute around the multiplication (C = D_A (A' B') D_B, eqn:scaling P:717-722).
+ * The plan copies what it needs from the rules; rules may be destroyed afterwards.
+ * ------------------------------------------------------------------------------------- */
+fmm_status fmm_plan_create(const fmm_rule* const* nodes, int n_nodes, int levels, int uniform,
+                           int64_t M, int64_t K, int64_t N, int dtype, int leaf,
+                           const fmm_scaling* scaling, fmm_plan** out);
+void fmm_plan_destroy(fmm_plan* plan);
+
+/* Multi-GPU partition of the top-level subproblems: rank p of P computes only
+ * the top-level products M_r with r = p (mod P) and writes into C the PARTIAL sum
+ * C_k = sum_{owned r, ascending} w_kr M_r (blocks with no owned contribution are zeroed).
+ * nranks = 1 restores the full computation.  Host-only; call before fmm_execute. */
+fmm_status fmm_plan_set_partition(fmm_plan* plan, int rank, int nranks);
+
+/* Host-only query: owned[r] = 1 if top-level product r is computed by `rank` (R entries). */
+fmm_status fmm_plan_owned(const fmm_plan* plan, int rank, int nranks, int32_t* owned, int* R);
+
+/* Device workspace (bytes) fmm_execute needs for this plan (and its current partition). */
+fmm_status fmm_plan_workspace_bytes(const fmm_plan* plan, size_t* bytes);
+
+/* Kernel launches one fmm_execute issues (for the benchmark's launch accounting). */
+fmm_status fmm_plan_launch_count(const fmm_plan* plan, int64_t* launches);
+
+/* Device timing of fmm_execute's launches, per step kind, with CUDA events recorded on the
+ * launch stream around each launch (enable = 1) -- for the benchmark's roofline numbers.
+ * fmm_plan_step_times returns the totals since the previous call and resets them:
+ * ms[k] / launches[k] for k = 1 K1 (S/T formation), 2 K2 (leaf products), 3 K3 (C
+ * combination), 4 ACC (top-level accumulation), 5 ZERO, 6 scaling, 7 NCCL reduce (arrays of 8;
+ * entry 0 unused).  Synchronises on the recorded events. */
+fmm_status fmm_plan_set_timing(fmm_plan* plan, int enable);
+fmm_status fmm_plan_step_times(fmm_plan* plan, double* ms, int64_t* launches);
+
+/* C = A.B by the plan (dev pointers).  A: M x K (lda), B: K x N (ldb), C: M x N (ldc),
+ * overwritten.  ws: dev workspace of >= fmm_plan_workspace_bytes.  Requirements: A, B, C, ws
+ * 16-byte aligned for the vectorised paths (otherwise a scalar path is used).  With a
+ * partition (nranks > 1) C receives this rank's partial sum; with a communicator set
+ * (fmm_plan_set_comm) the partials are summed onto rank 0's C by ncclReduce. */
+fmm_status fmm_execute(const fmm_plan* plan, const void* A, int64_t lda, const void* B,
+                       int64_t ldb, void* C, int64_t ldc, void* ws, size_t ws_bytes,
+                       void* stream);
+
+/* End-to-end variant with HOST buffers: A_host (M x K, lda), B_host (K x N, ldb) are copied to
+ * the caller's device staging buffers A_dev / B_dev (dense, ld = K / N), the product is computed
+ * into C_dev (dense, ld = N) and copied back to C_host (ldc).  All copies and kernels are
+ * enqueued on `stream`; host buffers should be pinned (cudaHostAlloc / torch pin_memory) for
+ * asynchronous copies.  The call returns without synchronising; C_host is valid after the
+ * stream completes. */
+fmm_status fmm_execute_host(const fmm_plan* plan, const void* A_host, int64_t lda,
+                            const void* B_host, int64_t ldb, void* C_host, int64_t ldc,
+                            void* A_dev, void* B_dev, void* C_dev, void* ws, size_t ws_bytes,
+                            void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Building blocks (one recursion node; used by tests and tools)
+ * ------------------------------------------------------------------------------------- */
+/* All S_r = sum_i u_ir A_i (mb x kb each, stored contiguously at S + r*mb*kb) and
+ * T_r = sum_j v_jr B_j (kb x nb, at T + r*kb*nb) of one node, i / j ascending (Eq.
+ * eqn:bilinear_alg).  A: m x k (lda), B: k x n (ldb), dev pointers. */
+fmm_status fmm_node_st(const fmm_rule* rule, int dtype, int64_t m, int64_t k, int64_t n,
+                       const void* A, int64_t lda, const void* B, int64_t ldb, void* S, void* T,
+                       void* stream);
+/* C_k = sum_r w_kr M_r, r ascending, from R contiguous blocks Ms (mb x nb each) into
+ * C (m x n, ldc). */
+fmm_status fmm_node_c(const fmm_rule* rule, int dtype, int64_t m, int64_t n, const void* Ms,
+                      void* C, int64_t ldc, void* stream);
+/* Classical C = A.B (the leaf kernel alone): dev pointers, row-major. */
+fmm_status fmm_gemm(int dtype, int leaf, int64_t M, int64_t K, int64_t N, const void* A,
+                    int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Diagonal scaling (Section 6), FP64 only.  All pointers dev.  The scaled matrices are written
+ * to A_out (M x K, lda_out) / B_out (K x N, ldb_out); A and B are not modified.  Factors:
+ * dA (M) and dB (N) are the cumulative outer factors D_A, D_B; d (K) the inner factor D.
+ * Divisions are true divisions (D^{-1}A), sqrt and division correctly rounded.
+ * An all-zero row / column returns FMM_E_PRECOND (this check synchronises the stream).
+ * ------------------------------------------------------------------------------------- */
+/* Alg. 1 lines 1-4: dA_i = max_j |a_ij|, dB_j = max_i |b_ij|, A' = D_A^{-1} A,
+ * B' = B D_B^{-1}. */
+fmm_status fmm_scale_outside(int dtype, int64_t M, int64_t K, int64_t N, const void* A,
+                             int64_t lda, const void* B, int64_t ldb, void* A_out,
+                             int64_t lda_out, void* B_out, int64_t ldb_out, void* dA, void* dB,
+                             int pow2, void* stream);
+/* Alg. 2 lines 1-3: d_k = sqrt(max_j |b_kj| / max_i |a_ik|), A' = A D,
+ * B' = D^{-1} B. */
+fmm_status fmm_scale_inside(int dtype, int64_t M, int64_t K, int64_t N, const void* A,
+                            int64_t lda, const void* B, int64_t ldb, void* A_out,
+                            int64_t lda_out, void* B_out, int64_t ldb_out, void* d, int pow2,
+                            void* stream);
+/* Alg. 3: alternating O / I steps per `cfg`, with the stopping test of Thm
+ * stopping-criterion evaluated ON DEVICE from the step after the first O step.
+ * dI (K) receives the cumulative inner factor (reporting only).  steps_dev: dev int32 that
+ * receives the number of steps taken (no host synchronisation for the stop test).  ws: dev
+ * scratch of fmm_scale_workspace_bytes(M, K, N). */
+fmm_status fmm_scale_repeated(int dtype, int64_t M, int64_t K, int64_t N, const void* A,
+                              int64_t lda, const void* B, int64_t ldb, const fmm_scaling* cfg,
+                              void* A_out, int64_t lda_out, void* B_out, int64_t ldb_out,
+                              void* dA, void* dB, void* dI, int32_t* steps_dev, void* ws,
+                              size_t ws_bytes, void* stream);
+fmm_status fmm_scale_workspace_bytes(int64_t M, int64_t K, int64_t N, size_t* bytes);
+/* Alg. 1 line 6: C <- D_A C D_B in place, c_ij = (dA_i * c_ij) * dB_j. */
+fmm_status fmm_unscale(int dtype, int64_t M, int64_t N, void* C, int64_t ldc, const void* dA,
+                       const void* dB, void* stream);
+/* After an fmm_execute with scaling: copy the last run's step count (host int) -- synchronises
+ * the stream. */
+fmm_status fmm_plan_last_scaling_steps(const fmm_plan* plan, void* ws, int* steps, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Multi-GPU (one process per GPU).  NCCL is loaded at run time (dlopen of libnccl.so.2, or
+ * the path in env FMM_NCCL_LIB).  The 128-byte unique id is created on rank 0 and broadcast
+ * by the caller (e.g. torch.distributed).
+ * ------------------------------------------------------------------------------------- */
+fmm_status fmm_comm_unique_id(void* out128);
+/* ncclCommInitRank on the current device; attaches the communicator and partition
+ * (rank, nranks) to the plan.  fmm_execute then ends with ncclReduce(sum, root 0) of C. */
+fmm_status fmm_plan_set_comm(fmm_plan* plan, const void* id128, int rank, int nranks);
+
+/* Thread-local text of the last error (never NULL). */
+const char* fmm_last_error(void);
+/* Library version string. */
+const char* fmm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FMM_B200_H */

@@ -143,6 +143,8 @@ def fmm(A: np.ndarray, B: np.ndarray, plan: Plan) -> np.ndarray:
     M, K = A.shape
     K2, N = B.shape
     assert K == K2
+    if M == 0 or N == 0 or K == 0:
+        return np.zeros((M, N), dt)  # empty sum
     pm, pk, pn = plan.dims_divisor()
     Mp, Kp, Np = -(-M // pm) * pm, -(-K // pk) * pk, -(-N // pn) * pn
     if (Mp, Kp, Np) != (M, K, N):
@@ -310,7 +312,7 @@ def scaled_fmm(A, B, plan: Plan, mode="none", pow2=False, tau=1.0, max_steps=20)
     else:
         first_O = mode in ("out_in", "repeated")
         steps = 2 if mode in ("out_in", "in_out") else max_steps
-        tau_eff = tau if mode == "repeated" else 0.0  # fixed 2-step modes: no early stop
+        tau_eff = tau if mode == "repeated" else -1.0  # fixed 2-step modes: no stop test
         res = scale_repeated(A, B, first_O=first_O, tau=tau_eff, max_steps=steps, pow2=pow2)
         Ap, Bp, dA, dB = res["A"], res["B"], res["dA"], res["dB"]
         info["steps"] = res["steps"]
@@ -338,6 +340,29 @@ def lift_rows(M: int, plan: Plan, leaf_rows) -> np.ndarray:
         m //= m0
         offs = (offs[:, None] + (np.arange(m0) * m)[None, :]).ravel()
     return np.sort((offs[:, None] + G[None, :]).ravel())
+
+
+def lift_cols(N: int, plan: Plan, leaf_cols) -> np.ndarray:
+    """Columns H of B/C consistent with every level's column split (the transpose of
+    lift_rows): column j of every T_r, M_r and C_k depends only on column j of the B blocks."""
+    _, _, pn = plan.dims_divisor()
+    nleaf = N // pn
+    H = np.asarray(sorted(set(int(c) for c in leaf_cols)), dtype=np.int64)
+    assert H.size and H.max() < nleaf
+    offs = np.array([0], dtype=np.int64)
+    n = N
+    for lv in plan.levels:
+        n0 = lv[0].n0
+        n //= n0
+        offs = (offs[:, None] + (np.arange(n0) * n)[None, :]).ravel()
+    return np.sort((offs[:, None] + H[None, :]).ravel())
+
+
+def fmm_sub(A: np.ndarray, B: np.ndarray, plan: Plan, rows: np.ndarray, cols: np.ndarray) -> np.ndarray:
+    """C_oracle[rows][:, cols] from A[rows, :] and B[:, cols] alone (rows / cols from lift_rows /
+    lift_cols): bitwise equal to the same entries of the full oracle run, because the leaf is
+    row- and column-independent and every S / T / C sum is elementwise."""
+    return fmm(np.ascontiguousarray(A[rows, :]), np.ascontiguousarray(B[:, cols]), plan)
 
 
 def fmm_rows(A: np.ndarray, B: np.ndarray, plan: Plan, rows: np.ndarray) -> np.ndarray:

@@ -406,7 +406,8 @@ int orc_step_I(int64_t M, int64_t K, int64_t N, double* A, int64_t lda, double* 
 }
 
 /* Alg. 3 with the stopping criterion of Thm stopping-criterion,
- * tested from the step after the first O step on.  Steps alternate starting with
+ * tested from the step after the first O step on; tau < 0 disables the test
+ * (fixed step count), tau = 0 stops only at an exact fixed point.  Steps alternate starting with
  * O if first_O else I; a step is one O or one I.
  *   dA (M), dB (N): cumulative outer factors, start at 1: dA_i <- dA_i * r'_i,
  *                   dB_j <- s'_j * dB_j.
@@ -451,7 +452,7 @@ int orc_scale_repeated(int64_t M, int64_t K, int64_t N, double* A, int64_t lda, 
         double lw = fabs(log(sp[j]));
         if (lw > w) w = lw;
       }
-      stop = (t > t0) && ok;
+      stop = (tau >= 0.0) && (t > t0) && ok;
     } else {
       rc = orc_step_I(M, K, N, A, lda, B, ldb, pow2, p, which);
       if (rc) break;
@@ -462,7 +463,7 @@ int orc_scale_repeated(int64_t M, int64_t K, int64_t N, double* A, int64_t lda, 
         double lw = fabs(log(p[k]));
         if (lw > w) w = lw;
       }
-      stop = (t0 >= 0) && (t > t0) && ok;
+      stop = (tau >= 0.0) && (t0 >= 0) && (t > t0) && ok;
     }
     steps = t + 1;
     if (trace_kind) trace_kind[t] = isO ? 'O' : 'I';

@@ -1,0 +1,7 @@
+"""B200-native recursive fast matrix multiplication (hot path of arXiv 1507.00687).
+
+The product is the C-ABI library libfmm_b200.so (include/fmm.h) built from csrc/ for sm_100a;
+`fmm` is its thin ctypes binding.  Nothing here imports the test oracle."""
+from . import fmm  # noqa: F401
+from .fmm import (FmmError, Plan, Rule, comm_unique_id, gemm, lib, node_c, node_st,  # noqa: F401
+                  scale_inside, scale_outside, scale_repeated, unscale)

@@ -1,0 +1,1066 @@
+// The C ABI (include/fmm.h): rules, plans (host schedule + device descriptors), execute,
+// building blocks, scaling entry points, NCCL glue.
+//
+// Schedule.  A plan is compiled once into a list of launch Steps:
+//   breadth-first:  K1(level 0) .. K1(level L-1), K2(all leaves), K3(level L-1) .. K3(level 0)
+//   depth-first at the top level (when the breadth-first workspace is large, or sharded):
+//     for each owned top-level r (ascending): K1(root, only column r) -> breadth-first over
+//     the subtree r -> ACC (C_k (+)= w_kr M_r)  ...  then ZERO of blocks without contributions.
+// Operands are Op descriptors; S_r (T_r) whose U (V) column is a single +1 are not copied: the
+// child operand aliases the parent's block (rounding-neutral).  Descriptors are uploaded once.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fmm_internal.h"
+
+namespace fmm {
+int64_t brent_violations(const RuleData& d, int64_t* fi, int64_t* fj, int64_t* fk);
+bool builtin_rule(const std::string& name, RuleData* out);
+size_t scale_ws_bytes(int64_t M, int64_t K, int64_t N);
+int* scale_flags_ptr(void* ws, int64_t M, int64_t K, int64_t N);
+cudaError_t run_scaling(int64_t M, int64_t K, int64_t N, const double* A, int64_t lda,
+                        const double* B, int64_t ldb, double* A_out, int64_t lda_out,
+                        double* B_out, int64_t ldb_out, double* dA, double* dB, double* dI,
+                        const char* steps, int nsteps, bool first_O, double tau, int pow2,
+                        void* sws, cudaStream_t st);
+cudaError_t launch_unscale(double* C, int64_t ldc, int64_t M, int64_t N, const double* dA,
+                           const double* dB, cudaStream_t st);
+
+static thread_local std::string g_err = "no error";
+void set_error(const std::string& msg) { g_err = msg; }
+fmm_status cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return FMM_OK;
+  set_error(std::string(where) + ": " + cudaGetErrorString(e));
+  if (e == cudaErrorMemoryAllocation) return FMM_E_OOM;
+  if (e == cudaErrorNotSupported) return FMM_E_UNSUPPORTED;
+  return FMM_E_CUDA;
+}
+}  // namespace fmm
+
+using namespace fmm;
+
+// ---------------------------------------------------------------------------------------------
+// NCCL (dlopen'ed; types mirrored from nccl.h 2.x ABI)
+// ---------------------------------------------------------------------------------------------
+namespace {
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+typedef int ncclResult_t;
+enum { ncclSum_ = 0 };
+enum { ncclFloat32_ = 7, ncclFloat64_ = 8 };
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*reduce)(const void*, void*, size_t, int, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi* nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* env = getenv("FMM_NCCL_LIB");
+    const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      if (!n) continue;
+      api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (api.h) break;
+    }
+    if (!api.h) return;
+    api.getUniqueId = (decltype(api.getUniqueId))dlsym(api.h, "ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))dlsym(api.h, "ncclCommInitRank");
+    api.reduce = (decltype(api.reduce))dlsym(api.h, "ncclReduce");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(api.h, "ncclCommDestroy");
+    api.getErrorString = (decltype(api.getErrorString))dlsym(api.h, "ncclGetErrorString");
+  });
+  if (!api.h || !api.getUniqueId || !api.commInitRank || !api.reduce) return nullptr;
+  return &api;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// Plan
+// ---------------------------------------------------------------------------------------------
+struct fmm_plan {
+  int dtype = FMM_F64, leaf = FMM_LEAF_NATIVE, L = 0;
+  int64_t M = 0, K = 0, N = 0;
+  std::vector<RuleData> rules;              // distinct rules
+  std::vector<std::vector<int>> node_rule;  // per level, rule index per node (BFS)
+  std::vector<int64_t> lm, lk, ln;          // node dims at level l (l = 0..L)
+  fmm_scaling scaling{FMM_SCALE_NONE, 1, 1.0, 20, 0};
+  int rank = 0, nranks = 1;
+  ncclComm_t comm = nullptr;
+  // compiled schedule
+  std::vector<Step> steps;
+  std::vector<int> coef_U, coef_V, coef_W;  // per rule: offset in coef buffer (doubles)
+  std::vector<double> coef_host;
+  std::vector<uint8_t> desc_host;  // descriptor arena (host copy)
+  // device copies, uploaded lazily on first use so that plans can be built without a GPU
+  mutable std::mutex dev_mu;
+  mutable double* dev_coef = nullptr;
+  mutable void* dev_desc = nullptr;
+  mutable int dev_id = -1;
+  size_t desc_bytes = 0;
+  size_t fmm_ws_bytes = 0;     // FMM temporaries
+  size_t scale_bytes = 0;      // scaling region (A', B', factors, scratch), placed first
+  bool dims_vec_ok = true;     // every level's column dims / offsets multiple of the vector
+  int64_t launches = 0;
+  // optional per-step timing (events recorded on the launch stream)
+  bool timing = false;
+  mutable std::mutex tmu;
+  mutable std::vector<cudaEvent_t> ev_pool;
+  mutable std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
+  ~fmm_plan();
+};
+
+fmm_plan::~fmm_plan() {
+  for (auto& u : ev_used) { cudaEventDestroy(u.second.first); cudaEventDestroy(u.second.second); }
+  for (auto e : ev_pool) cudaEventDestroy(e);
+  if (dev_coef) cudaFree(dev_coef);
+  if (dev_desc) cudaFree(dev_desc);
+  if (comm && nccl() && nccl()->commDestroy) nccl()->commDestroy(comm);
+}
+
+namespace {
+
+int elem_size(int dtype) { return dtype == FMM_F64 ? 8 : 4; }
+
+struct Builder {
+  fmm_plan* p;
+  std::vector<uint8_t> desc;  // host copy of the descriptor arena
+  int64_t ws_elems = 0, ws_peak = 0;
+  int64_t align_elems;
+
+  explicit Builder(fmm_plan* pl) : p(pl) { align_elems = 256 / elem_size(pl->dtype); }
+
+  int64_t ws_alloc(int64_t elems) {
+    int64_t off = ws_elems;
+    ws_elems += (elems + align_elems - 1) / align_elems * align_elems;
+    ws_peak = std::max(ws_peak, ws_elems);
+    return off;
+  }
+  template <typename T>
+  int64_t push(const std::vector<T>& v) {
+    size_t off = (desc.size() + 255) / 256 * 256;
+    desc.resize(off + v.size() * sizeof(T));
+    std::memcpy(desc.data() + off, v.data(), v.size() * sizeof(T));
+    return (int64_t)off;
+  }
+  Op ws_op(int64_t off, int64_t ld) { return Op{BASE_WS, 0, 0, off, ld}; }
+  static Op sub(const Op& o, int64_t r0, int64_t c0) {
+    return Op{o.base, 0, o.row0 + r0, o.col0 + c0, o.ld};
+  }
+
+  // one node of the active set at level l
+  struct Node {
+    int64_t idx;  // BFS index within level
+    Op a, b, c;
+  };
+
+  const RuleData& rule_at(int l, int64_t idx) { return p->rules[p->node_rule[l][idx]]; }
+
+  static bool trivial_col(const RuleData& r, const std::vector<int32_t>& X, int rows, int col,
+                          int* only_row) {
+    int nz = 0, row = -1;
+    for (int i = 0; i < rows; ++i)
+      if (X[(size_t)i * r.R + col] != 0) { ++nz; row = i; }
+    if (nz == 1 && X[(size_t)row * r.R + col] == (1 << r.log2den)) { *only_row = row; return true; }
+    return false;
+  }
+
+  // K1 for the active nodes of level l (columns in `only_r` if >= 0); returns child nodes.
+  std::vector<Node> emit_k1(int l, const std::vector<Node>& nodes, int only_r) {
+    const int64_t mb = p->lm[l + 1], kb = p->lk[l + 1], nb = p->ln[l + 1];
+    std::vector<K1Node> ks, kt;
+    std::vector<Node> kids;
+    for (const Node& nd : nodes) {
+      const RuleData& ru = rule_at(l, nd.idx);
+      K1Node s{};
+      s.in = nd.a;
+      s.coef_off = p->coef_U[p->node_rule[l][nd.idx]];
+      K1Node t{};
+      t.in = nd.b;
+      t.coef_off = p->coef_V[p->node_rule[l][nd.idx]];
+      for (int r = 0; r < ru.R; ++r) {
+        if (only_r >= 0 && r != only_r) continue;
+        Node ch;
+        ch.idx = nd.idx * ru.R + r;
+        int row;
+        if (trivial_col(ru, ru.U, ru.m0 * ru.k0, r, &row)) {
+          ch.a = sub(nd.a, (row % ru.m0) * mb, (row / ru.m0) * kb);
+        } else {
+          ch.a = ws_op(ws_alloc(mb * kb), kb);
+          s.out[r] = ch.a;
+          s.out_mask |= 1u << r;
+        }
+        if (trivial_col(ru, ru.V, ru.k0 * ru.n0, r, &row)) {
+          ch.b = sub(nd.b, (row % ru.k0) * kb, (row / ru.k0) * nb);
+        } else {
+          ch.b = ws_op(ws_alloc(kb * nb), nb);
+          t.out[r] = ch.b;
+          t.out_mask |= 1u << r;
+        }
+        ch.c = ws_op(ws_alloc(mb * nb), nb);
+        kids.push_back(ch);
+      }
+      if (s.out_mask) ks.push_back(s);
+      if (t.out_mask) kt.push_back(t);
+    }
+    const RuleData& r0 = rule_at(l, nodes[0].idx);
+    if (!ks.empty()) {
+      Step st{};
+      st.kind = STEP_K1;
+      st.count = (int)ks.size();
+      st.dev_off = push(ks);
+      st.rows = mb; st.cols = kb; st.P = r0.m0; st.Q = r0.k0; st.R = r0.R;
+      p->steps.push_back(st);
+    }
+    if (!kt.empty()) {
+      Step st{};
+      st.kind = STEP_K1;
+      st.count = (int)kt.size();
+      st.dev_off = push(kt);
+      st.rows = kb; st.cols = nb; st.P = r0.k0; st.Q = r0.n0; st.R = r0.R;
+      p->steps.push_back(st);
+    }
+    return kids;
+  }
+
+  void emit_k2(const std::vector<Node>& leaves) {
+    std::vector<LeafNode> lf;
+    for (const Node& n : leaves) lf.push_back(LeafNode{n.a, n.b, n.c});
+    Step st{};
+    st.kind = STEP_K2;
+    st.count = (int)lf.size();
+    st.dev_off = push(lf);
+    st.rows = p->lm[p->L]; st.cols = p->ln[p->L]; st.inner = p->lk[p->L];
+    p->steps.push_back(st);
+  }
+
+  // K3 for nodes of level l whose children are `kids` (R per node, in order).
+  void emit_k3(int l, const std::vector<Node>& nodes, const std::vector<Node>& kids) {
+    std::vector<K3Node> k3;
+    size_t ci = 0;
+    for (const Node& nd : nodes) {
+      const RuleData& ru = rule_at(l, nd.idx);
+      K3Node kn{};
+      kn.out = nd.c;
+      kn.coef_off = p->coef_W[p->node_rule[l][nd.idx]];
+      for (int r = 0; r < ru.R; ++r) kn.in[r] = kids[ci++].c;
+      k3.push_back(kn);
+    }
+    const RuleData& r0 = rule_at(l, nodes[0].idx);
+    Step st{};
+    st.kind = STEP_K3;
+    st.count = (int)k3.size();
+    st.dev_off = push(k3);
+    st.rows = p->lm[l + 1]; st.cols = p->ln[l + 1]; st.P = r0.m0; st.Q = r0.n0; st.R = r0.R;
+    p->steps.push_back(st);
+  }
+
+  // breadth-first over the subtree(s) rooted at `nodes` (level l), outputs into nodes' c.
+  void breadth_first(int l, const std::vector<Node>& nodes) {
+    std::vector<std::vector<Node>> lv{nodes};
+    for (int d = l; d < p->L; ++d) lv.push_back(emit_k1(d, lv.back(), -1));
+    emit_k2(lv.back());
+    for (int d = p->L - 1; d >= l; --d) emit_k3(d, lv[d - l], lv[d - l + 1]);
+  }
+
+  void build() {
+    Node root{0, Op{BASE_A, 0, 0, 0, -1}, Op{BASE_B, 0, 0, 0, -1}, Op{BASE_C, 0, 0, 0, -1}};
+    if (p->L == 0) {
+      if (p->rank == 0) {
+        emit_k2({root});
+      } else {  // nothing owned: zero C
+        std::vector<ZeroNode> z{ZeroNode{root.c, 1u, 0}};
+        Step st{};
+        st.kind = STEP_ZERO; st.count = 1; st.dev_off = push(z);
+        st.rows = p->M; st.cols = p->N; st.P = 1; st.Q = 1; st.R = 1;
+        p->steps.push_back(st);
+      }
+      return;
+    }
+    // breadth-first workspace estimate
+    int64_t bf = 0, nodes = 1;
+    for (int l = 0; l < p->L; ++l) {
+      nodes *= p->rules[p->node_rule[l][0]].R;
+      bf += nodes * (p->lm[l + 1] * p->lk[l + 1] + p->lk[l + 1] * p->ln[l + 1] +
+                     p->lm[l + 1] * p->ln[l + 1]);
+    }
+    const int64_t bf_bytes = bf * elem_size(p->dtype);
+    const bool split = p->nranks > 1 || bf_bytes > (int64_t)24 << 30;
+    if (!split) {
+      breadth_first(0, {root});
+      return;
+    }
+    const RuleData& ru = rule_at(0, 0);
+    uint32_t started = 0;
+    const int64_t mark = ws_elems;
+    for (int r = 0; r < ru.R; ++r) {
+      if (r % p->nranks != p->rank) continue;
+      ws_elems = mark;  // subtrees run one after another on one stream: reuse the workspace
+      std::vector<Node> kid = emit_k1(0, {root}, r);
+      if (p->L > 1) {
+        breadth_first(1, kid);
+      } else {
+        emit_k2(kid);
+      }
+      AccNode a{};
+      a.out = root.c;
+      a.in = kid[0].c;
+      a.coef_off = p->coef_W[p->node_rule[0][0]];
+      a.r = r;
+      for (int k = 0; k < ru.m0 * ru.n0; ++k)
+        if (ru.W[(size_t)k * ru.R + r] != 0 && !((started >> k) & 1u)) {
+          a.first_mask |= 1u << k;
+          started |= 1u << k;
+        }
+      Step st{};
+      st.kind = STEP_ACC; st.count = 1; st.dev_off = push(std::vector<AccNode>{a});
+      st.rows = p->lm[1]; st.cols = p->ln[1]; st.P = ru.m0; st.Q = ru.n0; st.R = ru.R;
+      p->steps.push_back(st);
+    }
+    const uint32_t all = (ru.m0 * ru.n0 >= 32) ? 0xffffffffu : ((1u << (ru.m0 * ru.n0)) - 1u);
+    if ((started & all) != all) {
+      std::vector<ZeroNode> z{ZeroNode{root.c, all & ~started, 0}};
+      Step st{};
+      st.kind = STEP_ZERO; st.count = 1; st.dev_off = push(z);
+      st.rows = p->lm[1]; st.cols = p->ln[1]; st.P = ru.m0; st.Q = ru.n0; st.R = ru.R;
+      p->steps.push_back(st);
+    }
+  }
+};
+
+void scaling_steps(const fmm_scaling& sc, std::string* steps, double* tau);
+
+fmm_status compile_plan(fmm_plan* p) {
+  p->steps.clear();
+  {
+    std::lock_guard<std::mutex> g(p->dev_mu);
+    if (p->dev_desc) { cudaFree(p->dev_desc); p->dev_desc = nullptr; }
+    p->dev_id = -1;
+  }
+  Builder b(p);
+  b.build();
+  p->fmm_ws_bytes = (size_t)b.ws_peak * elem_size(p->dtype);
+  p->desc_bytes = b.desc.size();
+  p->launches = (int64_t)p->steps.size();
+  if (p->scaling.mode != FMM_SCALE_NONE) {
+    const size_t vec = (size_t)(p->M + p->N + p->K) * 8;
+    const size_t mats = ((size_t)p->M * p->K + (size_t)p->K * p->N) * 8;
+    p->scale_bytes = (mats + vec + scale_ws_bytes(p->M, p->K, p->N) + 4096 + 255) / 256 * 256;
+    std::string stp;
+    double tau;
+    scaling_steps(p->scaling, &stp, &tau);
+    p->launches += 3 + 2 + 3 * (int64_t)stp.size() + 1;  // fills, reductions, steps, unscale
+  } else {
+    p->scale_bytes = 0;
+  }
+  if (p->nranks > 1 && p->comm) p->launches += 1;
+  // vector-path feasibility of all plan-internal dims (caller lds / pointers checked at run)
+  const int vec = 16 / elem_size(p->dtype);
+  p->dims_vec_ok = true;
+  for (int l = 0; l <= p->L; ++l)
+    if (p->lk[l] % vec || p->ln[l] % vec) p->dims_vec_ok = false;
+  p->desc_host = std::move(b.desc);
+  return FMM_OK;
+}
+
+bool check_rule_dims(const RuleData& d) {
+  return d.m0 > 0 && d.k0 > 0 && d.n0 > 0 && d.R > 0 && d.m0 * d.k0 <= kMaxBlk &&
+         d.k0 * d.n0 <= kMaxBlk && d.m0 * d.n0 <= kMaxBlk && d.R <= kMaxR;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+namespace {
+static bool aligned16(const void* q) { return ((uintptr_t)q & 15u) == 0; }
+
+// Upload coefficient tables and descriptors to the current device (once per plan / device).
+static fmm_status ensure_device(const fmm_plan* p) {
+  std::lock_guard<std::mutex> g(p->dev_mu);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
+  if (p->dev_id == dev && (p->dev_coef || p->coef_host.empty()) && (p->dev_desc || p->desc_host.empty()))
+    return FMM_OK;
+  if (p->dev_coef) { cudaFree(p->dev_coef); p->dev_coef = nullptr; }
+  if (p->dev_desc) { cudaFree(p->dev_desc); p->dev_desc = nullptr; }
+  if (!p->coef_host.empty()) {
+    e = cudaMalloc((void**)&p->dev_coef, p->coef_host.size() * sizeof(double));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p->dev_coef, p->coef_host.data(), p->coef_host.size() * sizeof(double), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_status(e, "plan coefficient upload");
+  }
+  if (!p->desc_host.empty()) {
+    e = cudaMalloc(&p->dev_desc, p->desc_host.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(p->dev_desc, p->desc_host.data(), p->desc_host.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_status(e, "plan descriptor upload");
+  }
+  p->dev_id = dev;
+  return FMM_OK;
+}
+
+static cudaEvent_t ev_get(const fmm_plan* p) {
+  if (!p->ev_pool.empty()) {
+    cudaEvent_t e = p->ev_pool.back();
+    p->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Record a timing bracket around a launch of kind `kind` (no-op unless timing is enabled).
+struct TimedLaunch {
+  const fmm_plan* p;
+  int kind;
+  cudaStream_t st;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  TimedLaunch(const fmm_plan* pl, int k, cudaStream_t s) : p(pl), kind(k), st(s) {
+    if (!p->timing) return;
+    std::lock_guard<std::mutex> g(p->tmu);
+    e0 = ev_get(p);
+    e1 = ev_get(p);
+    cudaEventRecord(e0, st);
+  }
+  ~TimedLaunch() {
+    if (!e0) return;
+    cudaEventRecord(e1, st);
+    std::lock_guard<std::mutex> g(p->tmu);
+    p->ev_used.push_back({kind, {e0, e1}});
+  }
+};
+
+template <typename T>
+static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStream_t st) {
+  for (const Step& s : p->steps) {
+    const void* nd = (const uint8_t*)p->dev_desc + s.dev_off;
+    TimedLaunch tl(p, s.kind, st);
+    cudaError_t e = cudaSuccess;
+    switch (s.kind) {
+      case STEP_K1: e = launch_k1<T>(s, nd, p->dev_coef, b, vec, st); break;
+      case STEP_K3: e = launch_k3<T>(s, nd, p->dev_coef, b, vec, st); break;
+      case STEP_ACC: e = launch_acc<T>(s, nd, p->dev_coef, b, vec, st); break;
+      case STEP_ZERO: e = launch_zero<T>(s, nd, b, st); break;
+      case STEP_K2:
+        if (p->dtype == FMM_F64)
+          e = launch_gemm_f64((const LeafNode*)nd, s.count, s.rows, s.cols, s.inner, b, vec, st);
+        else
+          e = launch_gemm_f32((const LeafNode*)nd, s.count, s.rows, s.cols, s.inner, b, vec, p->leaf, st);
+        break;
+    }
+    if (e != cudaSuccess) return cuda_status(e, "fmm_execute launch");
+  }
+  return FMM_OK;
+}
+
+void scaling_steps(const fmm_scaling& sc, std::string* steps, double* tau) {
+  switch (sc.mode) {
+    case FMM_SCALE_OUTSIDE: *steps = "O"; *tau = -1; break;
+    case FMM_SCALE_INSIDE: *steps = "I"; *tau = -1; break;
+    case FMM_SCALE_OUT_IN: *steps = "OI"; *tau = -1; break;
+    case FMM_SCALE_IN_OUT: *steps = "IO"; *tau = -1; break;
+    case FMM_SCALE_REPEATED: {
+      steps->clear();
+      for (int t = 0; t < sc.max_steps; ++t)
+        steps->push_back(((t % 2 == 0) == (sc.first_step_is_O != 0)) ? 'O' : 'I');
+      *tau = sc.tau;
+      break;
+    }
+    default: steps->clear(); *tau = 0;
+  }
+}
+
+
+static fmm_status scale_common(int64_t M, int64_t K, int64_t N, const void* A, int64_t lda,
+                               const void* B, int64_t ldb, void* A_out, int64_t lda_out,
+                               void* B_out, int64_t ldb_out, void* dA, void* dB, void* dI,
+                               const std::string& steps, double tau, int pow2,
+                               int32_t* steps_dev, void* ws, cudaStream_t st, bool sync_check) {
+  if (!A || !B || !A_out || !B_out || M <= 0 || K <= 0 || N <= 0 || lda < K || ldb < N ||
+      lda_out < K || ldb_out < N) {
+    set_error("fmm_scale: bad argument");
+    return FMM_E_ARG;
+  }
+  void* own = nullptr;
+  cudaError_t e = cudaSuccess;
+  double *tdA = (double*)dA, *tdB = (double*)dB, *tdI = (double*)dI;
+  size_t need = scale_ws_bytes(M, K, N) + (size_t)(M + N + K) * 8 + 1024;
+  if (!ws) {
+    e = cudaMallocAsync(&own, need, st);
+    if (e != cudaSuccess) return cuda_status(e, "fmm_scale alloc");
+  }
+  uint8_t* w = (uint8_t*)(ws ? ws : own);
+  w = (uint8_t*)(((uintptr_t)w + 255) & ~(uintptr_t)255);
+  uint8_t* extra = w + (scale_ws_bytes(M, K, N) + 255) / 256 * 256;
+  if (!tdA) { tdA = (double*)extra; }
+  if (!tdB) { tdB = (double*)extra + M; }
+  if (!tdI) { tdI = (double*)extra + M + N; }
+  e = run_scaling(M, K, N, (const double*)A, lda, (const double*)B, ldb, (double*)A_out, lda_out,
+                  (double*)B_out, ldb_out, tdA, tdB, tdI, steps.data(), (int)steps.size(),
+                  steps[0] == 'O', tau, pow2, w, st);
+  int* flags = scale_flags_ptr(w, M, K, N);
+  if (e == cudaSuccess && steps_dev)
+    e = cudaMemcpyAsync(steps_dev, flags + 1, sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+  fmm_status status = FMM_OK;
+  if (e == cudaSuccess && sync_check) {
+    int hf[8];
+    e = cudaMemcpyAsync(hf, flags, sizeof hf, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess && hf[2]) {
+      static const char* what[] = {"", "row of A", "column of B", "column of A", "row of B"};
+      set_error(std::string("scaling precondition: all-zero ") + what[hf[2] & 7] + " at index " + std::to_string(hf[3]));
+      status = FMM_E_PRECOND;
+    }
+  }
+  if (own) cudaFreeAsync(own, st);
+  if (e != cudaSuccess) return cuda_status(e, "fmm_scale");
+  return status;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fmm_last_error(void) { return g_err.c_str(); }
+const char* fmm_version(void) { return "fmm_b200 0.1 (sm_100a)"; }
+
+fmm_status fmm_rule_create(int m0, int k0, int n0, int R, const int32_t* U, const int32_t* V,
+                           const int32_t* W, int log2_den, const char* name, fmm_rule** out,
+                           int64_t* n_violations) {
+  if (!U || !V || !W || !out) { set_error("fmm_rule_create: null pointer"); return FMM_E_ARG; }
+  if (log2_den < 0 || log2_den > 8) { set_error("fmm_rule_create: log2_den out of [0, 8]"); return FMM_E_ARG; }
+  RuleData d;
+  d.name = name ? name : "custom";
+  d.m0 = m0; d.k0 = k0; d.n0 = n0; d.R = R; d.log2den = log2_den;
+  if (!check_rule_dims(d)) { set_error("fmm_rule_create: dims out of range (m0k0,k0n0,m0n0 <= 16, R <= 32)"); return FMM_E_ARG; }
+  d.U.assign(U, U + (size_t)m0 * k0 * R);
+  d.V.assign(V, V + (size_t)k0 * n0 * R);
+  d.W.assign(W, W + (size_t)m0 * n0 * R);
+  for (auto* X : {&d.U, &d.V, &d.W})
+    for (int32_t x : *X)
+      if (x <= -(1 << 20) || x >= (1 << 20)) { set_error("fmm_rule_create: |numerator| >= 2^20"); return FMM_E_ARG; }
+  int64_t fi = -1, fj = -1, fk = -1;
+  int64_t nv = brent_violations(d, &fi, &fj, &fk);
+  if (n_violations) *n_violations = nv;
+  if (nv) {
+    char buf[200];
+    snprintf(buf, sizeof buf, "fmm_rule_create: %lld Brent violations; first at (i=%lld, j=%lld, k=%lld)",
+             (long long)nv, (long long)fi, (long long)fj, (long long)fk);
+    set_error(buf);
+    return FMM_E_RULE;
+  }
+  *out = new fmm_rule{d};
+  return FMM_OK;
+}
+
+fmm_status fmm_rule_builtin(const char* name, fmm_rule** out) {
+  if (!name || !out) { set_error("fmm_rule_builtin: null pointer"); return FMM_E_ARG; }
+  RuleData d;
+  if (!builtin_rule(name, &d)) { set_error(std::string("unknown builtin rule: ") + name); return FMM_E_ARG; }
+  if (brent_violations(d, nullptr, nullptr, nullptr) != 0) { set_error("builtin rule fails Brent"); return FMM_E_RULE; }
+  *out = new fmm_rule{d};
+  return FMM_OK;
+}
+
+fmm_status fmm_rule_info(const fmm_rule* r, int* m0, int* k0, int* n0, int* R, int32_t* U,
+                         int32_t* V, int32_t* W, int* log2_den) {
+  if (!r) { set_error("fmm_rule_info: null rule"); return FMM_E_ARG; }
+  if (m0) *m0 = r->d.m0;
+  if (k0) *k0 = r->d.k0;
+  if (n0) *n0 = r->d.n0;
+  if (R) *R = r->d.R;
+  if (log2_den) *log2_den = r->d.log2den;
+  if (U) std::copy(r->d.U.begin(), r->d.U.end(), U);
+  if (V) std::copy(r->d.V.begin(), r->d.V.end(), V);
+  if (W) std::copy(r->d.W.begin(), r->d.W.end(), W);
+  return FMM_OK;
+}
+
+void fmm_rule_destroy(fmm_rule* r) { delete r; }
+
+fmm_status fmm_plan_create(const fmm_rule* const* nodes, int n_nodes, int levels, int uniform,
+                           int64_t M, int64_t K, int64_t N, int dtype, int leaf,
+                           const fmm_scaling* scaling, fmm_plan** out) {
+  if (!out || levels < 0 || levels > 16 || M < 0 || K < 0 || N < 0 || (levels > 0 && !nodes)) {
+    set_error("fmm_plan_create: bad argument");
+    return FMM_E_ARG;
+  }
+  if (dtype != FMM_F64 && dtype != FMM_F32) { set_error("fmm_plan_create: bad dtype"); return FMM_E_ARG; }
+  if (leaf < FMM_LEAF_NATIVE || leaf > FMM_LEAF_3XTF32 || (dtype == FMM_F64 && leaf != FMM_LEAF_NATIVE)) {
+    set_error("fmm_plan_create: leaf kind not valid for dtype (FP64 requires NATIVE)");
+    return FMM_E_ARG;
+  }
+  auto p = new fmm_plan();
+  p->dtype = dtype; p->leaf = leaf; p->L = levels; p->M = M; p->K = K; p->N = N;
+  if (scaling) {
+    if (scaling->mode < FMM_SCALE_NONE || scaling->mode > FMM_SCALE_REPEATED ||
+        (scaling->mode == FMM_SCALE_REPEATED && scaling->max_steps < 1)) {
+      delete p; set_error("fmm_plan_create: bad scaling config"); return FMM_E_ARG;
+    }
+    if (scaling->mode != FMM_SCALE_NONE && dtype != FMM_F64) {
+      delete p; set_error("fmm_plan_create: scaling is implemented for FP64"); return FMM_E_UNSUPPORTED;
+    }
+    p->scaling = *scaling;
+  }
+  // expected node counts
+  int64_t count = 1, total = 0;
+  std::vector<int64_t> per_level;
+  auto find_rule = [&](const fmm_rule* r) {
+    for (size_t i = 0; i < p->rules.size(); ++i)
+      if (p->rules[i].name == r->d.name && p->rules[i].U == r->d.U && p->rules[i].V == r->d.V &&
+          p->rules[i].W == r->d.W && p->rules[i].log2den == r->d.log2den)
+        return (int)i;
+    p->rules.push_back(r->d);
+    return (int)p->rules.size() - 1;
+  };
+  int64_t idx = 0;
+  for (int l = 0; l < levels; ++l) {
+    std::vector<int> nr;
+    if (uniform) {
+      if (l >= n_nodes || !nodes[l]) { delete p; set_error("fmm_plan_create: uniform needs one rule per level"); return FMM_E_ARG; }
+      nr.assign((size_t)count, find_rule(nodes[l]));
+    } else {
+      if (idx + count > n_nodes) { delete p; set_error("fmm_plan_create: too few nodes for a non-uniform tree"); return FMM_E_ARG; }
+      for (int64_t q = 0; q < count; ++q) {
+        if (!nodes[idx + q]) { delete p; set_error("fmm_plan_create: null node rule"); return FMM_E_ARG; }
+        nr.push_back(find_rule(nodes[idx + q]));
+      }
+      idx += count;
+    }
+    const RuleData& r0 = p->rules[nr[0]];
+    for (int q : nr) {
+      const RuleData& rq = p->rules[q];
+      if (rq.m0 != r0.m0 || rq.k0 != r0.k0 || rq.n0 != r0.n0 || rq.R != r0.R) {
+        delete p; set_error("fmm_plan_create: rules within a level must share (m0,k0,n0,R) (P:146)"); return FMM_E_ARG;
+      }
+    }
+    p->node_rule.push_back(nr);
+    total += count;
+    count *= r0.R;
+    if (count > (1 << 22)) { delete p; set_error("fmm_plan_create: recursion tree too large"); return FMM_E_ARG; }
+  }
+  if (!uniform && idx != n_nodes && levels > 0) { delete p; set_error("fmm_plan_create: node count mismatch"); return FMM_E_ARG; }
+  (void)total;
+  p->lm.push_back(M); p->lk.push_back(K); p->ln.push_back(N);
+  for (int l = 0; l < levels; ++l) {
+    const RuleData& r = p->rules[p->node_rule[l][0]];
+    if (p->lm[l] % r.m0 || p->lk[l] % r.k0 || p->ln[l] % r.n0) {
+      char buf[160];
+      snprintf(buf, sizeof buf, "fmm_plan_create: level %d dims (%lld,%lld,%lld) not divisible by (%d,%d,%d)", l,
+               (long long)p->lm[l], (long long)p->lk[l], (long long)p->ln[l], r.m0, r.k0, r.n0);
+      delete p; set_error(buf); return FMM_E_SHAPE;
+    }
+    p->lm.push_back(p->lm[l] / r.m0); p->lk.push_back(p->lk[l] / r.k0); p->ln.push_back(p->ln[l] / r.n0);
+  }
+  // coefficient tables
+  for (const RuleData& r : p->rules) {
+    p->coef_U.push_back((int)p->coef_host.size());
+    for (int i = 0; i < r.m0 * r.k0; ++i) for (int q = 0; q < r.R; ++q) p->coef_host.push_back(r.coef(r.U, i, q));
+    p->coef_V.push_back((int)p->coef_host.size());
+    for (int j = 0; j < r.k0 * r.n0; ++j) for (int q = 0; q < r.R; ++q) p->coef_host.push_back(r.coef(r.V, j, q));
+    p->coef_W.push_back((int)p->coef_host.size());
+    for (int k = 0; k < r.m0 * r.n0; ++k) for (int q = 0; q < r.R; ++q) p->coef_host.push_back(r.coef(r.W, k, q));
+  }
+  fmm_status s = compile_plan(p);
+  if (s != FMM_OK) { delete p; return s; }
+  *out = p;
+  return FMM_OK;
+}
+
+void fmm_plan_destroy(fmm_plan* p) { delete p; }
+
+fmm_status fmm_plan_set_partition(fmm_plan* p, int rank, int nranks) {
+  if (!p || nranks < 1 || rank < 0 || rank >= nranks) { set_error("fmm_plan_set_partition: bad rank/nranks"); return FMM_E_ARG; }
+  p->rank = rank;
+  p->nranks = nranks;
+  return compile_plan(p);
+}
+
+fmm_status fmm_plan_owned(const fmm_plan* p, int rank, int nranks, int32_t* owned, int* R) {
+  if (!p || nranks < 1 || rank < 0 || rank >= nranks) { set_error("fmm_plan_owned: bad args"); return FMM_E_ARG; }
+  int RR = p->L > 0 ? p->rules[p->node_rule[0][0]].R : 1;
+  if (R) *R = RR;
+  if (owned)
+    for (int r = 0; r < RR; ++r) owned[r] = (p->L > 0 ? (r % nranks == rank) : (rank == 0)) ? 1 : 0;
+  return FMM_OK;
+}
+
+fmm_status fmm_plan_workspace_bytes(const fmm_plan* p, size_t* bytes) {
+  if (!p || !bytes) { set_error("fmm_plan_workspace_bytes: null"); return FMM_E_ARG; }
+  *bytes = p->scale_bytes + p->fmm_ws_bytes + 256;
+  return FMM_OK;
+}
+
+fmm_status fmm_plan_launch_count(const fmm_plan* p, int64_t* launches) {
+  if (!p || !launches) { set_error("fmm_plan_launch_count: null"); return FMM_E_ARG; }
+  *launches = p->launches;
+  return FMM_OK;
+}
+
+fmm_status fmm_execute(const fmm_plan* p, const void* A, int64_t lda, const void* B, int64_t ldb,
+                       void* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream) {
+  if (!p) { set_error("fmm_execute: null plan"); return FMM_E_ARG; }
+  const bool empty = p->M == 0 || p->N == 0;
+  if (!empty && (!A && p->K > 0)) { set_error("fmm_execute: null A"); return FMM_E_ARG; }
+  if (!empty && (!B && p->K > 0)) { set_error("fmm_execute: null B"); return FMM_E_ARG; }
+  if (!empty && !C) { set_error("fmm_execute: null C"); return FMM_E_ARG; }
+  if (lda < std::max<int64_t>(p->K, 1) || ldb < std::max<int64_t>(p->N, 1) || ldc < std::max<int64_t>(p->N, 1)) {
+    set_error("fmm_execute: leading dimension smaller than the row length");
+    return FMM_E_ARG;
+  }
+  size_t need = 0;
+  fmm_plan_workspace_bytes(p, &need);
+  if (ws_bytes < need || (need > 256 && !ws)) {
+    set_error("fmm_execute: workspace too small (need " + std::to_string(need) + " bytes)");
+    return FMM_E_OOM;
+  }
+  if (empty) return FMM_OK;
+  {
+    fmm_status es = ensure_device(p);
+    if (es != FMM_OK) return es;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  uint8_t* wsb = (uint8_t*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  Bases b{};
+  b.p[BASE_A] = A; b.p[BASE_B] = B; b.p[BASE_C] = C; b.p[BASE_WS] = wsb + p->scale_bytes;
+  b.ld[BASE_A] = lda; b.ld[BASE_B] = ldb; b.ld[BASE_C] = ldc; b.ld[BASE_WS] = 0;
+  double *dA = nullptr, *dB = nullptr;
+  if (p->scaling.mode != FMM_SCALE_NONE) {
+    double* Ap = (double*)wsb;
+    double* Bp = Ap + p->M * p->K;
+    dA = Bp + p->K * p->N;
+    dB = dA + p->M;
+    double* dI = dB + p->N;
+    void* sws = (void*)(((uintptr_t)(dI + p->K) + 255) & ~(uintptr_t)255);
+    std::string steps;
+    double tau;
+    scaling_steps(p->scaling, &steps, &tau);
+    TimedLaunch tl(p, 6, st);
+    cudaError_t e = run_scaling(p->M, p->K, p->N, (const double*)A, lda, (const double*)B, ldb, Ap,
+                                p->K, Bp, p->N, dA, dB, dI, steps.data(), (int)steps.size(),
+                                steps[0] == 'O', tau, p->scaling.pow2, sws, st);
+    if (e != cudaSuccess) return cuda_status(e, "fmm_execute scaling");
+    b.p[BASE_A] = Ap; b.p[BASE_B] = Bp;
+    b.ld[BASE_A] = p->K; b.ld[BASE_B] = p->N;
+  }
+  const int vecn = 16 / elem_size(p->dtype);
+  const bool vec = p->dims_vec_ok && aligned16(b.p[BASE_A]) && aligned16(b.p[BASE_B]) &&
+                   aligned16(C) && aligned16(b.p[BASE_WS]) && b.ld[BASE_A] % vecn == 0 &&
+                   b.ld[BASE_B] % vecn == 0 && ldc % vecn == 0;
+  fmm_status s = p->dtype == FMM_F64 ? run_steps<double>(p, b, vec, st) : run_steps<float>(p, b, vec, st);
+  if (s != FMM_OK) return s;
+  if (p->scaling.mode != FMM_SCALE_NONE) {
+    TimedLaunch tl(p, 6, st);
+    cudaError_t e = launch_unscale((double*)C, ldc, p->M, p->N, dA, dB, st);
+    if (e != cudaSuccess) return cuda_status(e, "fmm_execute unscale");
+  }
+  if (p->comm && p->nranks > 1) {
+    NcclApi* api = nccl();
+    if (!api) { set_error("NCCL not loadable"); return FMM_E_NCCL; }
+    if (ldc != p->N) { set_error("fmm_execute: multi-GPU reduce needs ldc == N"); return FMM_E_ARG; }
+    TimedLaunch tl(p, 7, st);
+    ncclResult_t r = api->reduce(C, C, (size_t)(p->M * p->N), p->dtype == FMM_F64 ? ncclFloat64_ : ncclFloat32_,
+                                 ncclSum_, 0, p->comm, st);
+    if (r != 0) { set_error(std::string("ncclReduce: ") + (api->getErrorString ? api->getErrorString(r) : "?")); return FMM_E_NCCL; }
+  }
+  return FMM_OK;
+}
+
+fmm_status fmm_plan_set_timing(fmm_plan* p, int enable) {
+  if (!p) { set_error("fmm_plan_set_timing: null"); return FMM_E_ARG; }
+  p->timing = enable != 0;
+  return FMM_OK;
+}
+
+fmm_status fmm_plan_step_times(fmm_plan* p, double* ms, int64_t* launches) {
+  if (!p || !ms || !launches) { set_error("fmm_plan_step_times: null"); return FMM_E_ARG; }
+  for (int k = 0; k < 8; ++k) { ms[k] = 0; launches[k] = 0; }
+  std::lock_guard<std::mutex> g(p->tmu);
+  cudaError_t err = cudaSuccess;
+  for (auto& u : p->ev_used) {
+    cudaError_t e = cudaEventSynchronize(u.second.second);
+    float t = 0;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, u.second.first, u.second.second);
+    if (e != cudaSuccess && err == cudaSuccess) err = e;
+    const int k = u.first & 7;
+    ms[k] += t;
+    launches[k] += 1;
+    p->ev_pool.push_back(u.second.first);
+    p->ev_pool.push_back(u.second.second);
+  }
+  p->ev_used.clear();
+  return cuda_status(err, "fmm_plan_step_times");
+}
+
+fmm_status fmm_execute_host(const fmm_plan* p, const void* A_host, int64_t lda,
+                            const void* B_host, int64_t ldb, void* C_host, int64_t ldc,
+                            void* A_dev, void* B_dev, void* C_dev, void* ws, size_t ws_bytes,
+                            void* stream) {
+  if (!p || !A_host || !B_host || !C_host || !A_dev || !B_dev || !C_dev) {
+    set_error("fmm_execute_host: null pointer");
+    return FMM_E_ARG;
+  }
+  if (lda < p->K || ldb < p->N || ldc < p->N) { set_error("fmm_execute_host: bad ld"); return FMM_E_ARG; }
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t es = (size_t)elem_size(p->dtype);
+  cudaError_t e = cudaMemcpy2DAsync(A_dev, p->K * es, A_host, lda * es, p->K * es, p->M, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(B_dev, p->N * es, B_host, ldb * es, p->N * es, p->K, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return cuda_status(e, "fmm_execute_host H2D");
+  fmm_status s = fmm_execute(p, A_dev, p->K, B_dev, p->N, C_dev, p->N, ws, ws_bytes, stream);
+  if (s != FMM_OK) return s;
+  e = cudaMemcpy2DAsync(C_host, ldc * es, C_dev, p->N * es, p->N * es, p->M, cudaMemcpyDeviceToHost, st);
+  return cuda_status(e, "fmm_execute_host D2H");
+}
+
+fmm_status fmm_plan_last_scaling_steps(const fmm_plan* p, void* ws, int* steps, void* stream) {
+  if (!p || !ws || !steps) { set_error("fmm_plan_last_scaling_steps: null"); return FMM_E_ARG; }
+  if (p->scaling.mode == FMM_SCALE_NONE) { *steps = 0; return FMM_OK; }
+  uint8_t* wsb = (uint8_t*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  double* dI = (double*)wsb + p->M * p->K + p->K * p->N + p->M + p->N;
+  void* sws = (void*)(((uintptr_t)(dI + p->K) + 255) & ~(uintptr_t)255);
+  int flags[8];
+  cudaError_t e = cudaMemcpyAsync(flags, scale_flags_ptr(sws, p->M, p->K, p->N), sizeof flags,
+                                  cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_status(e, "fmm_plan_last_scaling_steps");
+  *steps = flags[1];
+  if (flags[2]) {
+    static const char* what[] = {"", "row of A", "column of B", "column of A", "row of B"};
+    set_error(std::string("scaling precondition: all-zero ") + what[flags[2] & 7] + " at index " + std::to_string(flags[3]));
+    return FMM_E_PRECOND;
+  }
+  return FMM_OK;
+}
+
+// ---- building blocks ----------------------------------------------------------------------------
+
+fmm_status fmm_node_st(const fmm_rule* rule, int dtype, int64_t m, int64_t k, int64_t n,
+                       const void* A, int64_t lda, const void* B, int64_t ldb, void* S, void* T,
+                       void* stream) {
+  if (!rule || !A || !B || !S || !T) { set_error("fmm_node_st: null"); return FMM_E_ARG; }
+  const RuleData& r = rule->d;
+  if (m % r.m0 || k % r.k0 || n % r.n0) { set_error("fmm_node_st: dims not divisible"); return FMM_E_SHAPE; }
+  fmm_scaling none{FMM_SCALE_NONE, 1, 0, 1, 0};
+  const fmm_rule* nodes[1] = {rule};
+  fmm_plan* p = nullptr;
+  // build K1 descriptors directly (no plan schedule needed): ws base = S for U, T for V
+  std::vector<double> coef;
+  for (int i = 0; i < r.m0 * r.k0; ++i) for (int q = 0; q < r.R; ++q) coef.push_back(r.coef(r.U, i, q));
+  const int offV = (int)coef.size();
+  for (int j = 0; j < r.k0 * r.n0; ++j) for (int q = 0; q < r.R; ++q) coef.push_back(r.coef(r.V, j, q));
+  (void)none; (void)nodes; (void)p;
+  const int64_t mb = m / r.m0, kb = k / r.k0, nb = n / r.n0;
+  K1Node ks{}, kt{};
+  ks.in = Op{BASE_A, 0, 0, 0, -1};
+  kt.in = Op{BASE_B, 0, 0, 0, -1};
+  ks.coef_off = 0;
+  kt.coef_off = offV;
+  for (int q = 0; q < r.R; ++q) {
+    ks.out[q] = Op{BASE_C, 0, 0, q * mb * kb, kb};
+    kt.out[q] = Op{BASE_WS, 0, 0, q * kb * nb, nb};
+  }
+  ks.out_mask = kt.out_mask = (r.R >= 32) ? 0xffffffffu : ((1u << r.R) - 1u);
+  cudaStream_t st = (cudaStream_t)stream;
+  void* dmem = nullptr;
+  size_t bytes = coef.size() * 8 + 2 * sizeof(K1Node) + 512;
+  cudaError_t e = cudaMallocAsync(&dmem, bytes, st);
+  if (e != cudaSuccess) return cuda_status(e, "fmm_node_st alloc");
+  uint8_t* d8 = (uint8_t*)dmem;
+  double* dcoef = (double*)d8;
+  K1Node* dn = (K1Node*)(d8 + ((coef.size() * 8 + 255) / 256 * 256));
+  std::vector<uint8_t> host(bytes, 0);
+  std::memcpy(host.data(), coef.data(), coef.size() * 8);
+  std::memcpy(host.data() + ((uint8_t*)dn - d8), &ks, sizeof ks);
+  std::memcpy(host.data() + ((uint8_t*)dn - d8) + sizeof ks, &kt, sizeof kt);
+  e = cudaMemcpyAsync(dmem, host.data(), bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // host buffer lifetime
+  Bases b{};
+  b.p[BASE_A] = A; b.p[BASE_B] = B; b.p[BASE_C] = S; b.p[BASE_WS] = T;
+  b.ld[BASE_A] = lda; b.ld[BASE_B] = ldb;
+  const int vecn = 16 / elem_size(dtype);
+  const bool vec = aligned16(A) && aligned16(B) && aligned16(S) && aligned16(T) && lda % vecn == 0 &&
+                   ldb % vecn == 0 && kb % vecn == 0 && nb % vecn == 0;
+  Step s1{};
+  s1.kind = STEP_K1; s1.count = 1; s1.rows = mb; s1.cols = kb; s1.P = r.m0; s1.Q = r.k0; s1.R = r.R;
+  Step s2 = s1;
+  s2.rows = kb; s2.cols = nb; s2.P = r.k0; s2.Q = r.n0;
+  if (e == cudaSuccess) {
+    e = dtype == FMM_F64 ? launch_k1<double>(s1, dn, dcoef, b, vec, st) : launch_k1<float>(s1, dn, dcoef, b, vec, st);
+  }
+  if (e == cudaSuccess) {
+    e = dtype == FMM_F64 ? launch_k1<double>(s2, dn + 1, dcoef, b, vec, st) : launch_k1<float>(s2, dn + 1, dcoef, b, vec, st);
+  }
+  cudaError_t e2 = cudaFreeAsync(dmem, st);
+  if (e == cudaSuccess) e = e2;
+  return cuda_status(e, "fmm_node_st");
+}
+
+fmm_status fmm_node_c(const fmm_rule* rule, int dtype, int64_t m, int64_t n, const void* Ms,
+                      void* C, int64_t ldc, void* stream) {
+  if (!rule || !Ms || !C) { set_error("fmm_node_c: null"); return FMM_E_ARG; }
+  const RuleData& r = rule->d;
+  if (m % r.m0 || n % r.n0) { set_error("fmm_node_c: dims not divisible"); return FMM_E_SHAPE; }
+  const int64_t mb = m / r.m0, nb = n / r.n0;
+  std::vector<double> coef;
+  for (int k = 0; k < r.m0 * r.n0; ++k) for (int q = 0; q < r.R; ++q) coef.push_back(r.coef(r.W, k, q));
+  K3Node kn{};
+  kn.out = Op{BASE_C, 0, 0, 0, -1};
+  kn.coef_off = 0;
+  for (int q = 0; q < r.R; ++q) kn.in[q] = Op{BASE_WS, 0, 0, q * mb * nb, nb};
+  cudaStream_t st = (cudaStream_t)stream;
+  void* dmem = nullptr;
+  size_t off = (coef.size() * 8 + 255) / 256 * 256;
+  size_t bytes = off + sizeof kn;
+  cudaError_t e = cudaMallocAsync(&dmem, bytes, st);
+  if (e != cudaSuccess) return cuda_status(e, "fmm_node_c alloc");
+  std::vector<uint8_t> host(bytes, 0);
+  std::memcpy(host.data(), coef.data(), coef.size() * 8);
+  std::memcpy(host.data() + off, &kn, sizeof kn);
+  e = cudaMemcpyAsync(dmem, host.data(), bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  Bases b{};
+  b.p[BASE_C] = C; b.p[BASE_WS] = Ms; b.ld[BASE_C] = ldc;
+  const int vecn = 16 / elem_size(dtype);
+  const bool vec = aligned16(C) && aligned16(Ms) && ldc % vecn == 0 && nb % vecn == 0;
+  Step s{};
+  s.kind = STEP_K3; s.count = 1; s.rows = mb; s.cols = nb; s.P = r.m0; s.Q = r.n0; s.R = r.R;
+  if (e == cudaSuccess)
+    e = dtype == FMM_F64 ? launch_k3<double>(s, (uint8_t*)dmem + off, (double*)dmem, b, vec, st)
+                         : launch_k3<float>(s, (uint8_t*)dmem + off, (double*)dmem, b, vec, st);
+  cudaError_t e2 = cudaFreeAsync(dmem, st);
+  if (e == cudaSuccess) e = e2;
+  return cuda_status(e, "fmm_node_c");
+}
+
+fmm_status fmm_gemm(int dtype, int leaf, int64_t M, int64_t K, int64_t N, const void* A,
+                    int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, void* stream) {
+  if ((M && N && !C) || lda < std::max<int64_t>(K, 1) || ldb < std::max<int64_t>(N, 1) || ldc < std::max<int64_t>(N, 1)) {
+    set_error("fmm_gemm: bad argument"); return FMM_E_ARG;
+  }
+  if (dtype == FMM_F64 && leaf != FMM_LEAF_NATIVE) { set_error("fmm_gemm: FP64 requires NATIVE leaf"); return FMM_E_ARG; }
+  if (M == 0 || N == 0) return FMM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  LeafNode lf{Op{BASE_A, 0, 0, 0, -1}, Op{BASE_B, 0, 0, 0, -1}, Op{BASE_C, 0, 0, 0, -1}};
+  void* dmem = nullptr;
+  cudaError_t e = cudaMallocAsync(&dmem, sizeof lf, st);
+  if (e != cudaSuccess) return cuda_status(e, "fmm_gemm alloc");
+  e = cudaMemcpyAsync(dmem, &lf, sizeof lf, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  Bases b{};
+  b.p[BASE_A] = A; b.p[BASE_B] = B; b.p[BASE_C] = C;
+  b.ld[BASE_A] = lda; b.ld[BASE_B] = ldb; b.ld[BASE_C] = ldc;
+  const int vecn = 16 / elem_size(dtype);
+  const bool vec = aligned16(A) && aligned16(B) && aligned16(C) && lda % vecn == 0 && ldb % vecn == 0 &&
+                   ldc % vecn == 0 && K % vecn == 0 && N % vecn == 0;
+  if (e == cudaSuccess)
+    e = dtype == FMM_F64 ? launch_gemm_f64((const LeafNode*)dmem, 1, M, N, K, b, vec, st)
+                         : launch_gemm_f32((const LeafNode*)dmem, 1, M, N, K, b, vec, leaf, st);
+  cudaError_t e2 = cudaFreeAsync(dmem, st);
+  if (e == cudaSuccess) e = e2;
+  return cuda_status(e, "fmm_gemm");
+}
+
+// ---- scaling entry points ---------------------------------------------------------------------
+
+fmm_status fmm_scale_workspace_bytes(int64_t M, int64_t K, int64_t N, size_t* bytes) {
+  if (!bytes) return FMM_E_ARG;
+  *bytes = scale_ws_bytes(M, K, N) + 512;
+  return FMM_OK;
+}
+
+fmm_status fmm_scale_outside(int dtype, int64_t M, int64_t K, int64_t N, const void* A,
+                             int64_t lda, const void* B, int64_t ldb, void* A_out,
+                             int64_t lda_out, void* B_out, int64_t ldb_out, void* dA, void* dB,
+                             int pow2, void* stream) {
+  if (dtype != FMM_F64) { set_error("scaling: FP64 only"); return FMM_E_UNSUPPORTED; }
+  if (!dA || !dB) { set_error("fmm_scale_outside: null factor vector"); return FMM_E_ARG; }
+  return scale_common(M, K, N, A, lda, B, ldb, A_out, lda_out, B_out, ldb_out, dA, dB, nullptr,
+                      "O", -1.0, pow2, nullptr, nullptr, (cudaStream_t)stream, true);
+}
+
+fmm_status fmm_scale_inside(int dtype, int64_t M, int64_t K, int64_t N, const void* A,
+                            int64_t lda, const void* B, int64_t ldb, void* A_out,
+                            int64_t lda_out, void* B_out, int64_t ldb_out, void* d, int pow2,
+                            void* stream) {
+  if (dtype != FMM_F64) { set_error("scaling: FP64 only"); return FMM_E_UNSUPPORTED; }
+  if (!d) { set_error("fmm_scale_inside: null factor vector"); return FMM_E_ARG; }
+  return scale_common(M, K, N, A, lda, B, ldb, A_out, lda_out, B_out, ldb_out, nullptr, nullptr,
+                      d, "I", -1.0, pow2, nullptr, nullptr, (cudaStream_t)stream, true);
+}
+
+fmm_status fmm_scale_repeated(int dtype, int64_t M, int64_t K, int64_t N, const void* A,
+                              int64_t lda, const void* B, int64_t ldb, const fmm_scaling* cfg,
+                              void* A_out, int64_t lda_out, void* B_out, int64_t ldb_out,
+                              void* dA, void* dB, void* dI, int32_t* steps_dev, void* ws,
+                              size_t ws_bytes, void* stream) {
+  if (dtype != FMM_F64) { set_error("scaling: FP64 only"); return FMM_E_UNSUPPORTED; }
+  if (!cfg || cfg->max_steps < 1 || !dA || !dB || !dI) { set_error("fmm_scale_repeated: bad config / null factor"); return FMM_E_ARG; }
+  size_t need;
+  fmm_scale_workspace_bytes(M, K, N, &need);
+  if (ws && ws_bytes < need) { set_error("fmm_scale_repeated: workspace too small"); return FMM_E_OOM; }
+  std::string steps;
+  double tau;
+  fmm_scaling c = *cfg;
+  c.mode = FMM_SCALE_REPEATED;
+  scaling_steps(c, &steps, &tau);
+  return scale_common(M, K, N, A, lda, B, ldb, A_out, lda_out, B_out, ldb_out, dA, dB, dI, steps,
+                      tau, cfg->pow2, steps_dev, ws, (cudaStream_t)stream, false);
+}
+
+fmm_status fmm_unscale(int dtype, int64_t M, int64_t N, void* C, int64_t ldc, const void* dA,
+                       const void* dB, void* stream) {
+  if (dtype != FMM_F64) { set_error("scaling: FP64 only"); return FMM_E_UNSUPPORTED; }
+  if (!C || !dA || !dB || ldc < N) { set_error("fmm_unscale: bad argument"); return FMM_E_ARG; }
+  return cuda_status(launch_unscale((double*)C, ldc, M, N, (const double*)dA, (const double*)dB,
+                                    (cudaStream_t)stream), "fmm_unscale");
+}
+
+// ---- NCCL ----------------------------------------------------------------------------------------
+
+fmm_status fmm_comm_unique_id(void* out128) {
+  if (!out128) { set_error("fmm_comm_unique_id: null"); return FMM_E_ARG; }
+  NcclApi* api = nccl();
+  if (!api) { set_error("NCCL library not loadable (set FMM_NCCL_LIB)"); return FMM_E_NCCL; }
+  ncclUniqueId id;
+  ncclResult_t r = api->getUniqueId(&id);
+  if (r != 0) { set_error("ncclGetUniqueId failed"); return FMM_E_NCCL; }
+  std::memcpy(out128, &id, sizeof id);
+  return FMM_OK;
+}
+
+fmm_status fmm_plan_set_comm(fmm_plan* p, const void* id128, int rank, int nranks) {
+  if (!p || !id128 || nranks < 1 || rank < 0 || rank >= nranks) { set_error("fmm_plan_set_comm: bad args"); return FMM_E_ARG; }
+  NcclApi* api = nccl();
+  if (!api) { set_error("NCCL library not loadable (set FMM_NCCL_LIB)"); return FMM_E_NCCL; }
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  ncclComm_t c = nullptr;
+  ncclResult_t r = api->commInitRank(&c, nranks, id, rank);
+  if (r != 0) { set_error(std::string("ncclCommInitRank: ") + (api->getErrorString ? api->getErrorString(r) : "?")); return FMM_E_NCCL; }
+  if (p->comm && api->commDestroy) api->commDestroy(p->comm);
+  p->comm = c;
+  p->rank = rank;
+  p->nranks = nranks;
+  return compile_plan(p);
+}
+
+}  // extern "C"

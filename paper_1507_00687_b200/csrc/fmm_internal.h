@@ -1,0 +1,136 @@
+// Internal declarations of libfmm_b200 (not part of the ABI; see include/fmm.h).
+//
+// Data model: every operand the kernels touch -- a block of the caller's A, B,
+// C or a temporary in the workspace -- is described by an Op: element (i, j) lives at
+//   base[b] + (row0 + i) * ld + col0 + j,   ld = (Op.ld >= 0 ? Op.ld : bases.ld[b]).
+// Descriptors are built once per plan on the host and uploaded once; fmm_execute only passes
+// the four base pointers and the caller's leading dimensions as kernel arguments.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/fmm.h"
+
+namespace fmm {
+
+constexpr int kMaxBlk = 16;  // max m0*k0, k0*n0, m0*n0 of a rule
+constexpr int kMaxR = 32;    // max rank R of a rule
+
+enum BaseId : int32_t { BASE_A = 0, BASE_B = 1, BASE_C = 2, BASE_WS = 3 };
+
+struct Op {
+  int32_t base;
+  int32_t pad_;
+  int64_t row0, col0, ld;  // ld < 0: use the base's ld
+};
+
+struct Bases {
+  const void* p[4];
+  int64_t ld[4];
+};
+
+// Selects instead of b.p[o.base]: dynamic indexing of a by-value kernel parameter would force
+// a local-memory copy of Bases.
+template <typename T>
+__host__ __device__ inline T* op_ptr(const Bases& b, const Op& o, int64_t& ld) {
+  const int id = o.base;
+  const void* base = id == 0 ? b.p[0] : id == 1 ? b.p[1] : id == 2 ? b.p[2] : b.p[3];
+  const int64_t bld = id == 0 ? b.ld[0] : id == 1 ? b.ld[1] : id == 2 ? b.ld[2] : b.ld[3];
+  ld = o.ld >= 0 ? o.ld : bld;
+  return (T*)base + o.row0 * ld + o.col0;
+}
+
+// ---- K1: linear combinations S_r = sum_i u_ir A_i (or T_r = sum_j v_jr B_j) -------------
+// The input operand (rows*P x cols*Q) is split into P x Q sub-blocks of rows x cols; the
+// sub-block index is column-major, blk = p + P*q.  coef points at the rule's table
+// ((P*Q) x R row-major).  Outputs are written for the r in out_mask.
+struct K1Node {
+  Op in;
+  int32_t coef_off;  // offset (in doubles) of the table in the plan's coefficient buffer
+  uint32_t out_mask;
+  Op out[kMaxR];
+};
+
+// ---- K3: C_k = sum_r w_kr M_r into the node output (rows*M0 x cols*N0), k = ia*N0 + jb ----
+struct K3Node {
+  Op out;
+  int32_t coef_off;  // W table ((M0*N0) x R)
+  int32_t pad_;
+  Op in[kMaxR];
+};
+
+// ---- ACC: C_k (+)= w_kr M_r for one r (depth-first top level / multi-GPU partial) ----------
+struct AccNode {
+  Op out;     // node output (M0*rows x N0*cols)
+  Op in;      // M_r (rows x cols)
+  int32_t coef_off;
+  int32_t r;
+  uint32_t first_mask;  // bit k: this is the first contribution to C_k (initialise)
+  uint32_t pad_;
+};
+
+// ---- ZERO: zero the blocks k in mask of a node output --------------------------------------
+struct ZeroNode {
+  Op out;
+  uint32_t mask;
+  uint32_t pad_;
+};
+
+// ---- K2: leaf products M = S.T ---------------------------------------------------------------
+struct LeafNode {
+  Op a, b, c;
+};
+
+enum StepKind { STEP_K1 = 1, STEP_K2 = 2, STEP_K3 = 3, STEP_ACC = 4, STEP_ZERO = 5 };
+
+struct Step {
+  int kind;
+  int count;         // number of nodes in the launch
+  int64_t dev_off;   // byte offset of the node array in the plan's device descriptor buffer
+  int64_t rows, cols, inner;  // sub-block dims (K1/K3/ACC/ZERO) or m, n, k (K2)
+  int P, Q, R;       // K1: split P x Q, rank R.  K3/ACC/ZERO: P = M0, Q = N0, R
+  bool vec_ok;       // all ws offsets / dims allow 16-byte vectors (caller bases checked later)
+};
+
+// ---- rules -----------------------------------------------------------------------------------
+struct RuleData {
+  std::string name;
+  int m0 = 0, k0 = 0, n0 = 0, R = 0, log2den = 0;
+  std::vector<int32_t> U, V, W;  // numerators, row-major (rows x R)
+  double coef(const std::vector<int32_t>& X, int row, int r) const {
+    return (double)X[(size_t)row * R + r] / (double)(1 << log2den);
+  }
+};
+
+// ---- kernel launchers (kernels_*.cu) -----------------------------------------------------------
+template <typename T>
+cudaError_t launch_k1(const Step& s, const void* dev_nodes, const double* dev_coef,
+                      const Bases& b, bool vec, cudaStream_t st);
+template <typename T>
+cudaError_t launch_k3(const Step& s, const void* dev_nodes, const double* dev_coef,
+                      const Bases& b, bool vec, cudaStream_t st);
+template <typename T>
+cudaError_t launch_acc(const Step& s, const void* dev_nodes, const double* dev_coef,
+                       const Bases& b, bool vec, cudaStream_t st);
+template <typename T>
+cudaError_t launch_zero(const Step& s, const void* dev_nodes, const Bases& b, cudaStream_t st);
+
+cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
+                            int64_t k, const Bases& b, bool vec, cudaStream_t st);
+cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
+                            int64_t k, const Bases& b, bool vec, int leaf, cudaStream_t st);
+
+// ---- error reporting ------------------------------------------------------------------------
+void set_error(const std::string& msg);
+fmm_status cuda_status(cudaError_t e, const char* where);
+
+}  // namespace fmm
+
+// The opaque ABI types.
+struct fmm_rule {
+  fmm::RuleData d;
+};

@@ -1,0 +1,314 @@
+// HBM-streaming kernels of the recursion (K1 and K3):
+//   K1  S_r = sum_i u_ir A_i / T_r = sum_j v_jr B_j   for every node of a level, one pass
+//   K3  C_k = sum_r w_kr M_r                          for every node of a level, one pass
+//   ACC C_k = w_kr M_r  |  C_k = C_k + w_kr M_r         one top-level r (depth-first / sharded)
+//   ZERO blocks of C with no contribution (sharded partial sums)
+// Each thread owns one 16-byte vector position (i, j..j+VEC-1) of the sub-block and touches
+// the same position in every input / output block, so each input element is read once and
+// each output written once per launch (the algorithmic floor).  Sums run sequentially in
+// ascending index order with explicit round-to-nearest intrinsics (no FMA contraction),
+// exactly the order of PAPER.md's sequential summation model (eqn:seq_summation_error).
+#include "fmm_internal.h"
+
+namespace fmm {
+
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T mul_rn(T a, T b);
+template <>
+__device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
+template <>
+__device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
+template <typename T>
+__device__ __forceinline__ T add_rn(T a, T b);
+template <>
+__device__ __forceinline__ double add_rn<double>(double a, double b) { return __dadd_rn(a, b); }
+template <>
+__device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd_rn(a, b); }
+
+template <typename T, int VEC>
+struct Vec {
+  T v[VEC];
+};
+
+template <typename T, int VEC>
+__device__ __forceinline__ Vec<T, VEC> ld_vec(const T* p) {
+  Vec<T, VEC> r;
+  if constexpr (VEC * sizeof(T) == 16) {
+    if constexpr (sizeof(T) == 8) {
+      double2 x = *reinterpret_cast<const double2*>(p);
+      r.v[0] = x.x;
+      r.v[1] = x.y;
+    } else {
+      float4 x = *reinterpret_cast<const float4*>(p);
+      r.v[0] = x.x; r.v[1] = x.y; r.v[2] = x.z; r.v[3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) r.v[e] = p[e];
+  }
+  return r;
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void st_vec(T* p, const Vec<T, VEC>& r) {
+  if constexpr (VEC * sizeof(T) == 16) {
+    if constexpr (sizeof(T) == 8) {
+      *reinterpret_cast<double2*>(p) = make_double2(r.v[0], r.v[1]);
+    } else {
+      *reinterpret_cast<float4*>(p) = make_float4(r.v[0], r.v[1], r.v[2], r.v[3]);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) p[e] = r.v[e];
+  }
+}
+
+constexpr int kThreads = 128;  // threads per block (x: column vectors)
+constexpr int kRowsPerBlock = 4;
+
+// grid: x = column chunks of kThreads vectors, y = row groups of kRowsPerBlock, z = node.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(kThreads) k1_lincomb(const K1Node* __restrict__ nodes,
+                                                       const double* __restrict__ coef_all,
+                                                       Bases bases, int64_t rows, int64_t cols,
+                                                       int P, int Q, int R) {
+  __shared__ double cf[kMaxBlk * kMaxR];
+  __shared__ uint32_t need_s;
+  const K1Node& nd = nodes[blockIdx.z];
+  const int nblk = P * Q;
+  const uint32_t omask = nd.out_mask;
+  for (int t = threadIdx.x; t < nblk * R; t += blockDim.x) cf[t] = coef_all[nd.coef_off + t];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t need = 0;
+    for (int b = 0; b < nblk; ++b)
+      for (int r = 0; r < R; ++r)
+        if (((omask >> r) & 1u) && cf[b * R + r] != 0.0) need |= 1u << b;
+    need_s = need;
+  }
+  __syncthreads();
+  const uint32_t need = need_s;
+
+  int64_t ldi;
+  const T* in = op_ptr<const T>(bases, nd.in, ldi);
+  const int64_t jv = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * VEC;
+  if (jv >= cols) return;
+  const int64_t i0 = (int64_t)blockIdx.y * kRowsPerBlock;
+  for (int ii = 0; ii < kRowsPerBlock; ++ii) {
+    const int64_t i = i0 + ii;
+    if (i >= rows) break;
+    Vec<T, VEC> x[kMaxBlk];
+#pragma unroll
+    for (int b = 0; b < kMaxBlk; ++b) {
+      if (b < nblk && ((need >> b) & 1u)) {
+        const int p = b % P, q = b / P;  // column-major block index
+        x[b] = ld_vec<T, VEC>(in + (p * rows + i) * ldi + q * cols + jv);
+      }
+    }
+    for (int r = 0; r < R; ++r) {
+      if (!((omask >> r) & 1u)) continue;
+      Vec<T, VEC> acc;
+      bool started = false;
+#pragma unroll
+      for (int b = 0; b < kMaxBlk; ++b) {
+        if (b >= nblk) break;
+        const double u = cf[b * R + r];
+        if (u == 0.0) continue;
+        const T ut = (T)u;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e)
+          acc.v[e] = started ? add_rn<T>(acc.v[e], mul_rn<T>(ut, x[b].v[e])) : mul_rn<T>(ut, x[b].v[e]);
+        started = true;
+      }
+      if (!started) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc.v[e] = (T)0;
+      }
+      int64_t ldo;
+      T* o = op_ptr<T>(bases, nd.out[r], ldo);
+      st_vec<T, VEC>(o + i * ldo + jv, acc);
+    }
+  }
+}
+
+// K3: node output (P*rows x Q*cols) with P = M0, Q = N0; k = ia*Q + jb (row-major).
+template <typename T, int VEC, int MAXR>
+__global__ void __launch_bounds__(kThreads) k3_combine(const K3Node* __restrict__ nodes,
+                                                       const double* __restrict__ coef_all,
+                                                       Bases bases, int64_t rows, int64_t cols,
+                                                       int P, int Q, int R) {
+  __shared__ double cf[kMaxBlk * kMaxR];
+  const K3Node& nd = nodes[blockIdx.z];
+  const int nk = P * Q;
+  for (int t = threadIdx.x; t < nk * R; t += blockDim.x) cf[t] = coef_all[nd.coef_off + t];
+  __syncthreads();
+  const int64_t jv = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * VEC;
+  if (jv >= cols) return;
+  int64_t ldo;
+  T* out = op_ptr<T>(bases, nd.out, ldo);
+  const int64_t i0 = (int64_t)blockIdx.y * kRowsPerBlock;
+  for (int ii = 0; ii < kRowsPerBlock; ++ii) {
+    const int64_t i = i0 + ii;
+    if (i >= rows) break;
+    Vec<T, VEC> m[MAXR];
+#pragma unroll
+    for (int r = 0; r < MAXR; ++r) {
+      if (r < R) {
+        int64_t ldm;
+        const T* mp = op_ptr<const T>(bases, nd.in[r], ldm);
+        m[r] = ld_vec<T, VEC>(mp + i * ldm + jv);
+      }
+    }
+    for (int k = 0; k < nk; ++k) {
+      Vec<T, VEC> acc;
+      bool started = false;
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r) {
+        if (r >= R) break;
+        const double w = cf[k * R + r];
+        if (w == 0.0) continue;
+        const T wt = (T)w;
+#pragma unroll
+        for (int e = 0; e < VEC; ++e)
+          acc.v[e] = started ? add_rn<T>(acc.v[e], mul_rn<T>(wt, m[r].v[e])) : mul_rn<T>(wt, m[r].v[e]);
+        started = true;
+      }
+      if (!started) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc.v[e] = (T)0;
+      }
+      const int ia = k / Q, jb = k % Q;
+      st_vec<T, VEC>(out + (ia * rows + i) * ldo + jb * cols + jv, acc);
+    }
+  }
+}
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(kThreads) k_acc(const AccNode* __restrict__ nodes,
+                                                  const double* __restrict__ coef_all,
+                                                  Bases bases, int64_t rows, int64_t cols, int P,
+                                                  int Q, int R) {
+  const AccNode& nd = nodes[blockIdx.z];
+  const int64_t jv = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * VEC;
+  if (jv >= cols) return;
+  int64_t ldo, ldm;
+  T* out = op_ptr<T>(bases, nd.out, ldo);
+  const T* mp = op_ptr<const T>(bases, nd.in, ldm);
+  const int64_t i0 = (int64_t)blockIdx.y * kRowsPerBlock;
+  for (int ii = 0; ii < kRowsPerBlock; ++ii) {
+    const int64_t i = i0 + ii;
+    if (i >= rows) break;
+    const Vec<T, VEC> m = ld_vec<T, VEC>(mp + i * ldm + jv);
+    for (int k = 0; k < P * Q; ++k) {
+      const double w = coef_all[nd.coef_off + k * R + nd.r];
+      if (w == 0.0) continue;
+      const T wt = (T)w;
+      const int ia = k / Q, jb = k % Q;
+      T* o = out + (ia * rows + i) * ldo + jb * cols + jv;
+      Vec<T, VEC> acc;
+      if ((nd.first_mask >> k) & 1u) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc.v[e] = mul_rn<T>(wt, m.v[e]);
+      } else {
+        acc = ld_vec<T, VEC>(o);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc.v[e] = add_rn<T>(acc.v[e], mul_rn<T>(wt, m.v[e]));
+      }
+      st_vec<T, VEC>(o, acc);
+    }
+  }
+}
+
+template <typename T>
+__global__ void k_zero(const ZeroNode* __restrict__ nodes, Bases bases, int64_t rows,
+                       int64_t cols, int P, int Q) {
+  const ZeroNode& nd = nodes[blockIdx.z];
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  int64_t ldo;
+  T* out = op_ptr<T>(bases, nd.out, ldo);
+  const int64_t i0 = (int64_t)blockIdx.y * kRowsPerBlock;
+  for (int ii = 0; ii < kRowsPerBlock; ++ii) {
+    const int64_t i = i0 + ii;
+    if (i >= rows) break;
+    for (int k = 0; k < P * Q; ++k)
+      if ((nd.mask >> k) & 1u) out[((k / Q) * rows + i) * ldo + (k % Q) * cols + j] = (T)0;
+  }
+}
+
+inline dim3 grid_for(const Step& s, int vec) {
+  int64_t cv = (s.cols + vec - 1) / vec;
+  return dim3((unsigned)((cv + kThreads - 1) / kThreads),
+              (unsigned)((s.rows + kRowsPerBlock - 1) / kRowsPerBlock), (unsigned)s.count);
+}
+
+}  // namespace
+
+template <typename T>
+cudaError_t launch_k1(const Step& s, const void* dev_nodes, const double* dev_coef,
+                      const Bases& b, bool vec, cudaStream_t st) {
+  if (s.count == 0 || s.rows == 0 || s.cols == 0) return cudaSuccess;
+  constexpr int V = 16 / sizeof(T);
+  if (vec)
+    k1_lincomb<T, V><<<grid_for(s, V), kThreads, 0, st>>>((const K1Node*)dev_nodes, dev_coef, b,
+                                                          s.rows, s.cols, s.P, s.Q, s.R);
+  else
+    k1_lincomb<T, 1><<<grid_for(s, 1), kThreads, 0, st>>>((const K1Node*)dev_nodes, dev_coef, b,
+                                                          s.rows, s.cols, s.P, s.Q, s.R);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_k3(const Step& s, const void* dev_nodes, const double* dev_coef,
+                      const Bases& b, bool vec, cudaStream_t st) {
+  if (s.count == 0 || s.rows == 0 || s.cols == 0) return cudaSuccess;
+  constexpr int V = 16 / sizeof(T);
+  const K3Node* nd = (const K3Node*)dev_nodes;
+  if (s.R <= 8) {
+    if (vec)
+      k3_combine<T, V, 8><<<grid_for(s, V), kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
+    else
+      k3_combine<T, 1, 8><<<grid_for(s, 1), kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
+  } else {
+    if (vec)
+      k3_combine<T, V, kMaxR><<<grid_for(s, V), kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
+    else
+      k3_combine<T, 1, kMaxR><<<grid_for(s, 1), kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_acc(const Step& s, const void* dev_nodes, const double* dev_coef,
+                       const Bases& b, bool vec, cudaStream_t st) {
+  if (s.count == 0 || s.rows == 0 || s.cols == 0) return cudaSuccess;
+  constexpr int V = 16 / sizeof(T);
+  if (vec)
+    k_acc<T, V><<<grid_for(s, V), kThreads, 0, st>>>((const AccNode*)dev_nodes, dev_coef, b,
+                                                     s.rows, s.cols, s.P, s.Q, s.R);
+  else
+    k_acc<T, 1><<<grid_for(s, 1), kThreads, 0, st>>>((const AccNode*)dev_nodes, dev_coef, b,
+                                                     s.rows, s.cols, s.P, s.Q, s.R);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_zero(const Step& s, const void* dev_nodes, const Bases& b, cudaStream_t st) {
+  if (s.count == 0 || s.rows == 0 || s.cols == 0) return cudaSuccess;
+  k_zero<T><<<grid_for(s, 1), kThreads, 0, st>>>((const ZeroNode*)dev_nodes, b, s.rows, s.cols,
+                                                 s.P, s.Q);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_k1<double>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);
+template cudaError_t launch_k1<float>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);
+template cudaError_t launch_k3<double>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);
+template cudaError_t launch_k3<float>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);
+template cudaError_t launch_acc<double>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);
+template cudaError_t launch_acc<float>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);
+template cudaError_t launch_zero<double>(const Step&, const void*, const Bases&, cudaStream_t);
+template cudaError_t launch_zero<float>(const Step&, const void*, const Bases&, cudaStream_t);
+
+}  // namespace fmm

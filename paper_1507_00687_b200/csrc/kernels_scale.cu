@@ -1,0 +1,302 @@
+// K4: diagonal scaling (Section 6, Alg. 1-3) on device, FP64.
+//
+// One scaling step = one tiny factor kernel + one streaming pass per matrix.  The streaming
+// pass applies the step's factors (a / r'_i, a * p_k, b / s'_j, b / p_k -- true divisions,
+// DESIGN.md reading A9) and, in the same read, accumulates the row and column max-abs of the
+// RESULT, which are exactly the reductions the next step needs; so every step reads and writes
+// each matrix once.  Max-abs is combined across CTAs with atomicMax on the IEEE bit pattern
+// (non-negative doubles order like their bit patterns): exact and order-free.
+// The stopping test of Thm stopping-criterion, from the step after the first O
+// step, runs on device; once it fires, later steps' passes exit immediately, so the
+// host never synchronises inside Alg. 3.
+#include <cstdint>
+
+#include "fmm_internal.h"
+
+namespace fmm {
+
+// flags layout (int32): [0] done, [1] steps taken, [2] error kind (0 none; 1 zero row of A,
+// 2 zero col of B, 3 zero col of A, 4 zero row of B), [3] error index, [4] skip current step
+enum { F_DONE = 0, F_STEPS = 1, F_ERR = 2, F_ERRIDX = 3, F_SKIP = 4, F_COUNT = 8 };
+enum ApplyMode { AP_NONE = 0, AP_ROW_DIV = 1, AP_COL_DIV = 2, AP_COL_MUL = 3 };
+
+namespace {
+
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+  atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+// Nearest power of two in log2 (reading A8): x = m 2^e, m in [0.5, 1);
+// round down to 2^(e-1) iff m*m < 1/2, decided exactly with an error-free square.
+__device__ __forceinline__ double pow2_round(double x) {
+  int e;
+  double m = frexp(x, &e);
+  double h = __dmul_rn(m, m);
+  double l = fma(m, m, -h);
+  bool below = (h < 0.5) || (h == 0.5 && l < 0.0);
+  return ldexp(1.0, below ? e - 1 : e);
+}
+
+constexpr int TX = 32, TY = 8, TR = 32, TC = 64;  // tile: 32 rows x 64 cols, 2 cols / thread
+
+// dst = apply(src); row_max[i] = max_j |dst_ij|, col_max[j] = max_i |dst_ij| (atomic).
+// dst may equal src (in place) or be null (reduce only).
+__global__ void __launch_bounds__(TX* TY)
+    k_apply_reduce(const double* src, int64_t lds, double* dst, int64_t ldd,
+                   int64_t rows, int64_t cols, int mode, const double* __restrict__ f,
+                   double* __restrict__ row_max, double* __restrict__ col_max,
+                   const int* __restrict__ flags) {
+  if (flags && flags[F_SKIP]) return;
+  __shared__ double cm[TY][TC];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int64_t tiles_c = (cols + TC - 1) / TC;
+  const int64_t tiles = ((rows + TR - 1) / TR) * tiles_c;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t r0 = (tile / tiles_c) * TR, c0 = (tile % tiles_c) * TC;
+    const int64_t c = c0 + 2 * tx;
+    double cmax0 = 0.0, cmax1 = 0.0;
+    for (int rr = ty; rr < TR; rr += TY) {
+      const int64_t r = r0 + rr;
+      double rmax = 0.0;
+      if (r < rows) {
+        double v[2] = {0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t cc = c + e;
+          if (cc < cols) {
+            double x = src[r * lds + cc];
+            if (mode == AP_ROW_DIV) x = __ddiv_rn(x, f[r]);
+            else if (mode == AP_COL_DIV) x = __ddiv_rn(x, f[cc]);
+            else if (mode == AP_COL_MUL) x = __dmul_rn(x, f[cc]);
+            if (dst) dst[r * ldd + cc] = x;
+            v[e] = fabs(x);
+          }
+        }
+        rmax = fmax(v[0], v[1]);
+        cmax0 = fmax(cmax0, v[0]);
+        cmax1 = fmax(cmax1, v[1]);
+      }
+      // warp = one row segment of 64 columns
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+      if (tx == 0 && r < rows && row_max) atomic_max_nonneg(&row_max[r], rmax);
+    }
+    if (col_max) {
+      cm[ty][2 * tx] = cmax0;
+      cm[ty][2 * tx + 1] = cmax1;
+      __syncthreads();
+      if (ty == 0) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          double mx = 0.0;
+#pragma unroll
+          for (int y = 0; y < TY; ++y) mx = fmax(mx, cm[y][2 * tx + e]);
+          const int64_t cc = c + e;
+          if (cc < cols) atomic_max_nonneg(&col_max[cc], mx);
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ bool block_all(bool v) { return __syncthreads_and(v ? 1 : 0) != 0; }
+
+// O step factors (Alg. 3): r'_i = rowmaxA_i, s'_j = colmaxB_j; dA_i *= r'_i;
+// dB_j = s'_j * dB_j; stop test r', s' >= (1+tau)^(-1/2) when `test`.
+__global__ void k_factor_O(const double* __restrict__ rmA, const double* __restrict__ cmB,
+                           int64_t M, int64_t N, int pow2, double* dA, double* dB, double* r_out,
+                           double* s_out, int* flags, int test, double lo_O,
+                           double* next_zero, int64_t next_len) {
+  const bool skip = flags[F_DONE] != 0;
+  __syncthreads();
+  if (threadIdx.x == 0) flags[F_SKIP] = skip ? 1 : 0;
+  for (int64_t i = threadIdx.x; i < next_len; i += blockDim.x) next_zero[i] = 0.0;
+  if (skip) return;
+  bool ok = true;
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+    double r = rmA[i];
+    if (!(r > 0.0)) {
+      if (atomicCAS(&flags[F_ERR], 0, 1) == 0) flags[F_ERRIDX] = (int)i;
+      r = __longlong_as_double(0x7ff8000000000000LL);  // NaN propagates to C
+    } else if (pow2) {
+      r = pow2_round(r);
+    }
+    r_out[i] = r;
+    dA[i] = __dmul_rn(dA[i], r);
+    ok = ok && (r >= lo_O);
+  }
+  for (int64_t j = threadIdx.x; j < N; j += blockDim.x) {
+    double s = cmB[j];
+    if (!(s > 0.0)) {
+      if (atomicCAS(&flags[F_ERR], 0, 2) == 0) flags[F_ERRIDX] = (int)j;
+      s = __longlong_as_double(0x7ff8000000000000LL);
+    } else if (pow2) {
+      s = pow2_round(s);
+    }
+    s_out[j] = s;
+    dB[j] = __dmul_rn(s, dB[j]);
+    ok = ok && (s >= lo_O);
+  }
+  const bool all = block_all(ok);
+  if (threadIdx.x == 0) {
+    flags[F_STEPS] += 1;
+    if (test && all) flags[F_DONE] = 1;
+  }
+}
+
+// I step factor (Alg. 3): p_k = sqrt(rowmaxB_k / colmaxA_k); dI_k *= p_k;
+// stop test p_k in [(1+tau)^(-1/4), (1+tau)^(1/4)] when `test`.
+__global__ void k_factor_I(const double* __restrict__ cmA, const double* __restrict__ rmB,
+                           int64_t K, int pow2, double* dI, double* p_out, int* flags, int test,
+                           double lo_I, double hi_I, double* next_zero, int64_t next_len) {
+  const bool skip = flags[F_DONE] != 0;
+  __syncthreads();
+  if (threadIdx.x == 0) flags[F_SKIP] = skip ? 1 : 0;
+  for (int64_t i = threadIdx.x; i < next_len; i += blockDim.x) next_zero[i] = 0.0;
+  if (skip) return;
+  bool ok = true;
+  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+    const double a = cmA[k], b = rmB[k];
+    double p;
+    if (!(a > 0.0) || !(b > 0.0)) {
+      if (atomicCAS(&flags[F_ERR], 0, !(a > 0.0) ? 3 : 4) == 0) flags[F_ERRIDX] = (int)k;
+      p = __longlong_as_double(0x7ff8000000000000LL);
+    } else {
+      p = __dsqrt_rn(__ddiv_rn(b, a));
+      if (pow2) p = pow2_round(p);
+    }
+    p_out[k] = p;
+    dI[k] = __dmul_rn(dI[k], p);
+    ok = ok && (p >= lo_I && p <= hi_I);
+  }
+  const bool all = block_all(ok);
+  if (threadIdx.x == 0) {
+    flags[F_STEPS] += 1;
+    if (test && all) flags[F_DONE] = 1;
+  }
+}
+
+__global__ void k_fill(double* p, int64_t n, double v) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+__global__ void k_unscale(double* C, int64_t ldc, int64_t M, int64_t N, const double* dA,
+                          const double* dB) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const double sj = dB[j];
+  for (int64_t i = blockIdx.y; i < M; i += gridDim.y) {
+    double* c = C + i * ldc + j;
+    *c = __dmul_rn(__dmul_rn(dA[i], *c), sj);
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// Host-side driver of one scaling run (Alg. 1 / 2 / O->I / I->O / 3).  `sw` is a device scratch
+// of scale_ws_bytes(M, K, N).  Writes A' / B' (A_out / B_out), dA, dB, dI and flags.
+// ---------------------------------------------------------------------------------------------
+size_t scale_ws_bytes(int64_t M, int64_t K, int64_t N) {
+  // 2 sets of maxima (rowA M, colA K, rowB K, colB N) + factor vectors (r M, s N, p K) + flags
+  return (size_t)(2 * (M + K + K + N) + (M + N + K) + 16) * sizeof(double);
+}
+
+struct ScaleWsView {
+  double* mx[2];  // each: rowA (M) | colA (K) | rowB (K) | colB (N)
+  double *r, *s, *p;
+  int* flags;
+};
+
+static ScaleWsView scale_ws_view(void* ws, int64_t M, int64_t K, int64_t N) {
+  ScaleWsView v;
+  double* w = (double*)ws;
+  const int64_t set = M + K + K + N;
+  v.mx[0] = w;
+  v.mx[1] = w + set;
+  v.r = w + 2 * set;
+  v.s = v.r + M;
+  v.p = v.s + N;
+  v.flags = (int*)(v.p + K);
+  return v;
+}
+
+int* scale_flags_ptr(void* ws, int64_t M, int64_t K, int64_t N) {
+  return scale_ws_view(ws, M, K, N).flags;
+}
+
+static int grid_for_pass(int64_t rows, int64_t cols) {
+  int64_t tiles = ((rows + TR - 1) / TR) * ((cols + TC - 1) / TC);
+  int64_t g = 148 * 8;
+  return (int)(tiles < g ? (tiles > 0 ? tiles : 1) : g);
+}
+
+// steps: sequence of 'O'/'I' (length nsteps); test_from: index from which the stop test runs
+// (-1: never).  A_out / B_out may alias? no: they are distinct buffers (ws).
+cudaError_t run_scaling(int64_t M, int64_t K, int64_t N, const double* A, int64_t lda,
+                        const double* B, int64_t ldb, double* A_out, int64_t lda_out,
+                        double* B_out, int64_t ldb_out, double* dA, double* dB, double* dI,
+                        const char* steps, int nsteps, bool first_O, double tau, int pow2,
+                        void* sws, cudaStream_t st) {
+  ScaleWsView v = scale_ws_view(sws, M, K, N);
+  const int64_t set = M + K + K + N;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(v.mx[0], 0, sizeof(double) * set, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(v.flags, 0, sizeof(int) * F_COUNT, st)) != cudaSuccess) return e;
+  k_fill<<<64, 256, 0, st>>>(dA, M, 1.0);
+  k_fill<<<64, 256, 0, st>>>(dB, N, 1.0);
+  k_fill<<<64, 256, 0, st>>>(dI, K, 1.0);
+  dim3 blk(TX, TY);
+  // initial reductions of A, B
+  {
+    double* m = v.mx[0];
+    k_apply_reduce<<<grid_for_pass(M, K), blk, 0, st>>>(A, lda, nullptr, 0, M, K, AP_NONE, nullptr,
+                                                        m, m + M, nullptr);
+    k_apply_reduce<<<grid_for_pass(K, N), blk, 0, st>>>(B, ldb, nullptr, 0, K, N, AP_NONE, nullptr,
+                                                        m + M + K, m + M + 2 * K, nullptr);
+  }
+  const double lo_I = pow(1.0 + tau, -0.25), hi_I = pow(1.0 + tau, 0.25), lo_O = pow(1.0 + tau, -0.5);
+  int t0 = -1;
+  for (int t = 0; t < nsteps; ++t) {
+    const bool isO = steps[t] == 'O';
+    if (isO && t0 < 0) t0 = t;
+    const int test = (tau >= 0.0 && t0 >= 0 && t > t0) ? 1 : 0;
+    double* cur = v.mx[t & 1];
+    double* nxt = v.mx[(t + 1) & 1];
+    const double* srcA = t == 0 ? A : A_out;
+    const double* srcB = t == 0 ? B : B_out;
+    const int64_t lsa = t == 0 ? lda : lda_out, lsb = t == 0 ? ldb : ldb_out;
+    if (isO) {
+      k_factor_O<<<1, 1024, 0, st>>>(cur, cur + M + 2 * K, M, N, pow2, dA, dB, v.r, v.s, v.flags,
+                                     test, lo_O, nxt, set);
+      k_apply_reduce<<<grid_for_pass(M, K), blk, 0, st>>>(srcA, lsa, A_out, lda_out, M, K,
+                                                          AP_ROW_DIV, v.r, nxt, nxt + M, v.flags);
+      k_apply_reduce<<<grid_for_pass(K, N), blk, 0, st>>>(srcB, lsb, B_out, ldb_out, K, N,
+                                                          AP_COL_DIV, v.s, nxt + M + K,
+                                                          nxt + M + 2 * K, v.flags);
+    } else {
+      k_factor_I<<<1, 1024, 0, st>>>(cur + M, cur + M + K, K, pow2, dI, v.p, v.flags, test, lo_I,
+                                     hi_I, nxt, set);
+      k_apply_reduce<<<grid_for_pass(M, K), blk, 0, st>>>(srcA, lsa, A_out, lda_out, M, K,
+                                                          AP_COL_MUL, v.p, nxt, nxt + M, v.flags);
+      k_apply_reduce<<<grid_for_pass(K, N), blk, 0, st>>>(srcB, lsb, B_out, ldb_out, K, N,
+                                                          AP_ROW_DIV, v.p, nxt + M + K,
+                                                          nxt + M + 2 * K, v.flags);
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  (void)first_O;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_unscale(double* C, int64_t ldc, int64_t M, int64_t N, const double* dA,
+                           const double* dB, cudaStream_t st) {
+  if (M == 0 || N == 0) return cudaSuccess;
+  dim3 grid((unsigned)((N + 255) / 256), (unsigned)(M < 2048 ? M : 2048));
+  k_unscale<<<grid, 256, 0, st>>>(C, ldc, M, N, dA, dB);
+  return cudaGetLastError();
+}
+
+}  // namespace fmm

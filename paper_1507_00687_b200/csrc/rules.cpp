@@ -1,0 +1,162 @@
+// Bilinear base-case rules <U,V,W> (Eq. eqn:bilinear_alg): creation, the
+// exact Brent check, and the built-in table.  Host-only C++.
+//
+// Built-ins are written here from their product formulas (a transcription independent of the
+// test oracle's tables); the equality of the two is itself a test (tests/test_capi_host.py).
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+
+#include "fmm_internal.h"
+
+namespace fmm {
+
+namespace {
+
+// A term like "+A11" / "-B21": block (row, col) 1-based.
+struct Term {
+  int sign, row, col;
+};
+
+std::vector<Term> parse_terms(const char* s) {
+  std::vector<Term> t;
+  int sign = +1;
+  for (const char* p = s; *p;) {
+    if (*p == '+') { sign = +1; ++p; continue; }
+    if (*p == '-') { sign = -1; ++p; continue; }
+    if (*p == 'A' || *p == 'B' || *p == 'C' || *p == 'M') {
+      t.push_back({sign, p[1] - '0', p[2] - '0'});
+      sign = +1;
+      p += 3;
+      continue;
+    }
+    ++p;
+  }
+  return t;
+}
+
+// 2x2x2 rule from R products "S_r * T_r" and four C_k combinations over products M1..M7
+// ("Mxy" is parsed as product number 10x+y-1 -> we use "M1_" style: digit then '_').
+RuleData rule222(const char* name, const std::vector<std::pair<const char*, const char*>>& prods,
+                 const char* c11, const char* c12, const char* c21, const char* c22) {
+  RuleData d;
+  d.name = name;
+  d.m0 = d.k0 = d.n0 = 2;
+  d.R = (int)prods.size();
+  d.U.assign(4 * d.R, 0);
+  d.V.assign(4 * d.R, 0);
+  d.W.assign(4 * d.R, 0);
+  for (int r = 0; r < d.R; ++r) {
+    for (const Term& t : parse_terms(prods[r].first))  // A(ia, ja): U row ia + 2 ja
+      d.U[((t.row - 1) + 2 * (t.col - 1)) * d.R + r] += t.sign;
+    for (const Term& t : parse_terms(prods[r].second))  // B(ja, jb): V row ja + 2 jb
+      d.V[((t.row - 1) + 2 * (t.col - 1)) * d.R + r] += t.sign;
+  }
+  const char* cs[4] = {c11, c12, c21, c22};  // W row k = 2 ia + jb: C11, C12, C21, C22
+  for (int k = 0; k < 4; ++k) {
+    // "M3" -> product 3 (1-based); terms are written with a single digit after 'M' and a
+    // dummy '_' so that parse_terms' 3-char token works.
+    for (const Term& t : parse_terms(cs[k])) d.W[k * d.R + (t.row - 1)] += t.sign;
+  }
+  return d;
+}
+
+RuleData make_strassen() {
+  // App. A read in the paper's product numbering.
+  return rule222("strassen",
+                 {{"+A11+A22", "+B11+B22"},
+                  {"+A21+A22", "+B11"},
+                  {"+A11", "+B12-B22"},
+                  {"+A22", "+B21-B11"},
+                  {"+A11+A12", "+B22"},
+                  {"+A21-A11", "+B11+B12"},
+                  {"+A12-A22", "+B21+B22"}},
+                 "+M1_+M4_-M5_+M7_", "+M3_+M5_", "+M2_+M4_", "+M1_-M2_+M3_+M6_");
+}
+
+RuleData make_winograd() {
+  // Strassen-Winograd (reading A2).
+  return rule222("winograd",
+                 {{"+A11", "+B11"},
+                  {"+A12", "+B21"},
+                  {"+A11-A21+A12-A22", "+B22"},
+                  {"+A22", "+B11-B21-B12+B22"},
+                  {"+A21+A22", "+B12-B11"},
+                  {"+A21+A22-A11", "+B11-B12+B22"},
+                  {"+A11-A21", "+B22-B12"}},
+                 "+M1_+M2_", "+M1_+M3_+M5_+M6_", "+M1_-M4_+M6_+M7_", "+M1_+M5_+M6_+M7_");
+}
+
+RuleData make_classical() {
+  RuleData d;
+  d.name = "classical222";
+  d.m0 = d.k0 = d.n0 = 2;
+  d.R = 8;
+  d.U.assign(32, 0);
+  d.V.assign(32, 0);
+  d.W.assign(32, 0);
+  for (int ia = 0; ia < 2; ++ia)
+    for (int ja = 0; ja < 2; ++ja)
+      for (int jb = 0; jb < 2; ++jb) {
+        int r = 4 * ia + 2 * ja + jb;
+        d.U[(ia + 2 * ja) * 8 + r] = 1;
+        d.V[(ja + 2 * jb) * 8 + r] = 1;
+        d.W[(2 * ia + jb) * 8 + r] = 1;
+      }
+  return d;
+}
+
+RuleData make_dalberto() {
+  // D'Alberto's variant: V~ = (swap (x) I2) V swaps B's block columns,
+  // W~ = (I2 (x) swap) W swaps C's block columns (row conventions of P:108).
+  RuleData s = make_strassen();
+  RuleData d = s;
+  d.name = "strassen_dalberto";
+  for (int ja = 0; ja < 2; ++ja)
+    for (int jb = 0; jb < 2; ++jb)
+      for (int r = 0; r < d.R; ++r) d.V[(ja + 2 * jb) * d.R + r] = s.V[(ja + 2 * (1 - jb)) * d.R + r];
+  for (int ia = 0; ia < 2; ++ia)
+    for (int jb = 0; jb < 2; ++jb)
+      for (int r = 0; r < d.R; ++r) d.W[(2 * ia + jb) * d.R + r] = s.W[(2 * ia + (1 - jb)) * d.R + r];
+  return d;
+}
+
+}  // namespace
+
+// Brent equations: for A-entry i = (ia,ja) (column-major), B-entry j = (ja',jb) (column-major),
+// C-entry k = (ia',jb') (row-major): sum_r U_ir V_jr W_kr = [ja==ja'][ia==ia'][jb==jb'],
+// scaled by 2^(3*log2den) to stay in integers.
+int64_t brent_violations(const RuleData& d, int64_t* first_i, int64_t* first_j, int64_t* first_k) {
+  int64_t bad = 0;
+  const int64_t one = (int64_t)1 << (3 * d.log2den);
+  for (int i = 0; i < d.m0 * d.k0; ++i) {
+    int ia = i % d.m0, ja = i / d.m0;
+    for (int j = 0; j < d.k0 * d.n0; ++j) {
+      int ja2 = j % d.k0, jb = j / d.k0;
+      for (int k = 0; k < d.m0 * d.n0; ++k) {
+        int ia2 = k / d.n0, jb2 = k % d.n0;
+        int64_t s = 0;
+        for (int r = 0; r < d.R; ++r)
+          s += (int64_t)d.U[(size_t)i * d.R + r] * d.V[(size_t)j * d.R + r] * d.W[(size_t)k * d.R + r];
+        int64_t want = (ja == ja2 && ia == ia2 && jb == jb2) ? one : 0;
+        if (s != want) {
+          if (bad == 0 && first_i) { *first_i = i; *first_j = j; *first_k = k; }
+          ++bad;
+        }
+      }
+    }
+  }
+  return bad;
+}
+
+bool builtin_rule(const std::string& name, RuleData* out) {
+  if (name == "classical222") *out = make_classical();
+  else if (name == "strassen") *out = make_strassen();
+  else if (name == "winograd") *out = make_winograd();
+  else if (name == "strassen_dalberto") *out = make_dalberto();
+  else return false;
+  return true;
+}
+
+}  // namespace fmm

@@ -1,0 +1,240 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star): ||C_gpu - C_oracle||max / (||A||max ||B||max K) <= 1e-13
+(FP64) and <= 5e-5 (FP32).  Kernel-level checks whose order is fixed (K1 linear combinations,
+K3 combinations, scaling) are bitwise, and so is the whole recursion when the leaf inner
+dimension is 1 (the leaf is then a single correctly rounded product on both sides)."""
+import numpy as np
+import pytest
+import torch
+
+import fmm_inputs as fi
+import oracle
+from oracle import rules as R
+from oracle.rules import Plan as OPlan
+
+pytestmark = pytest.mark.gpu
+
+TOL64, TOL32 = 1e-13, 5e-5
+
+
+@pytest.fixture(scope="module")
+def fb():
+    import paper_1507_00687_b200 as fb
+    assert torch.cuda.is_available()
+    return fb
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def gpu_plan(fb, names, M, K, N, dtype="f64", **kw):
+    return fb.Plan([fb.Rule.builtin(n) for n in names], M, K, N, dtype=dtype, **kw)
+
+
+def run(fb, names, A, B, dtype="f64", **kw):
+    M, K = A.shape
+    N = B.shape[1]
+    p = gpu_plan(fb, names, M, K, N, dtype=dtype, **kw)
+    Cg = p.execute(dev(A), dev(B))
+    torch.cuda.synchronize()
+    return Cg.cpu().numpy()
+
+
+def parity(Cg, Co, A, B):
+    return oracle.parity_metric(Cg, Co, np.abs(A).max(), np.abs(B).max(), A.shape[1])
+
+
+# ---- K2 alone ---------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("shape", [(128, 128, 128), (256, 512, 384), (1, 1, 1), (7, 13, 5),
+                                   (129, 257, 131), (300, 17, 260), (64, 0, 64)])
+def test_leaf_gemm_f64(fb, shape):
+    M, K, N = shape
+    A, B = fi.random_pair(M, K, N, seed=M + K + N)
+    Cg = fb.gemm(dev(A), dev(B)).cpu().numpy()
+    Co = oracle.fmm(A, B, OPlan([]))
+    if K == 0:
+        assert np.all(Cg == 0)
+        return
+    assert parity(Cg, Co, A, B) <= TOL64
+    # componentwise classical bound gamma_K sum |a||b| for any order
+    g = K * 2.0 ** -53 / (1 - K * 2.0 ** -53)
+    assert np.all(np.abs(Cg - Co) <= 2 * g * (np.abs(A) @ np.abs(B)) + 1e-300)
+
+
+def test_leaf_gemm_f64_unaligned_ld(fb):
+    A, B = fi.random_pair(100, 70, 90, seed=1)
+    Ab = torch.zeros((100, 71), dtype=torch.float64, device="cuda")
+    Ab[:, :70] = dev(A)
+    Bb = torch.zeros((70, 93), dtype=torch.float64, device="cuda")
+    Bb[:, :90] = dev(B)
+    Cg = fb.gemm(Ab[:, :70], Bb[:, :90]).cpu().numpy()
+    assert parity(Cg, oracle.fmm(A, B, OPlan([])), A, B) <= TOL64
+
+
+def test_leaf_gemm_f32(fb):
+    A, B = fi.random_pair(200, 300, 100, seed=3, dtype=np.float32)
+    Cg = fb.gemm(dev(A), dev(B)).cpu().numpy()
+    assert parity(Cg, oracle.fmm(A, B, OPlan([])), A, B) <= TOL32
+
+
+# ---- K1 / K3 bitwise -----------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", sorted(R.BUILTINS))
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("dims", [(64, 96, 32), (6, 10, 14)])
+def test_node_st_bitwise(fb, name, dtype, dims):
+    m, k, n = dims
+    A, B = fi.random_pair(m, k, n, seed=5, dtype=dtype)
+    Sg, Tg = fb.node_st(fb.Rule.builtin(name), dev(A), dev(B))
+    So, To = oracle.node_st(R.builtin(name), A, B)
+    assert np.array_equal(Sg.cpu().numpy(), So) and np.array_equal(Tg.cpu().numpy(), To)
+
+
+@pytest.mark.parametrize("name", sorted(R.BUILTINS))
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_node_c_bitwise(fb, name, dtype):
+    r = R.builtin(name)
+    g = np.random.default_rng(7)
+    Ms = g.standard_normal((r.R, 24, 40)).astype(dtype)
+    Cg = fb.node_c(fb.Rule.builtin(name), dev(Ms)).cpu().numpy()
+    assert np.array_equal(Cg, oracle.node_c(r, Ms))
+
+
+def test_summation_order_case_on_gpu(fb):
+    # the hand-computed order pin of tests/test_oracle_exec.py, through the CUDA K1 / K3
+    A = np.array([[2.0 ** 53, -(2.0 ** 53)], [-1.0, -1.0]])
+    S, _ = fb.node_st(fb.Rule.builtin("winograd"), dev(A), dev(np.ones((2, 2))))
+    assert S[2, 0, 0].item() == 1.0
+    Ms = np.array([2.0 ** 53, 0.0, 1.0, 0.0, -(2.0 ** 53), 1.0, 0.0]).reshape(7, 1, 1)
+    assert fb.node_c(fb.Rule.builtin("winograd"), dev(Ms))[0, 1].item() == 1.0
+
+
+# ---- whole recursion ----------------------------------------------------------------------------
+
+PLANS = {
+    "winograd_L2": ("winograd", "winograd"),
+    "strassen_L3": ("strassen",) * 3,
+    "classical_L2": ("classical222",) * 2,
+    "C3_mix": ("winograd", "classical222", "strassen"),
+}
+
+
+@pytest.mark.parametrize("pname", sorted(PLANS))
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_recursion_bitwise_with_unit_leaf_k(fb, pname, dtype):
+    # K = 2^L: every leaf has inner dimension 1, so the leaf is one rounded product on both
+    # sides and the whole result is fixed by the S/T/C summation order (reading A3).
+    names = PLANS[pname]
+    L = len(names)
+    A, B = fi.random_pair(16 * 2 ** L, 2 ** L, 8 * 2 ** L, seed=L, dtype=dtype)
+    Cg = run(fb, names, A, B, dtype="f64" if dtype == np.float64 else "f32")
+    Co = oracle.fmm(A, B, OPlan.uniform([R.builtin(n) for n in names]))
+    assert np.array_equal(Cg, Co)
+
+
+@pytest.mark.parametrize("pname", sorted(PLANS))
+def test_recursion_parity_f64(fb, pname):
+    names = PLANS[pname]
+    A, B = fi.random_pair(512, 384, 256, seed=11)
+    Cg = run(fb, names, A, B)
+    Co = oracle.fmm(A, B, OPlan.uniform([R.builtin(n) for n in names]))
+    assert parity(Cg, Co, A, B) <= TOL64
+
+
+def test_integer_inputs_exact(fb):
+    A, B = fi.integer_pair(256, 256, 256, seed=2)
+    Ci = (A.astype(np.int64) @ B.astype(np.int64)).astype(np.float64)
+    for names in PLANS.values():
+        assert np.array_equal(run(fb, names, A, B), Ci)
+
+
+def test_dalberto_nonuniform(fb):
+    s, d = fb.Rule.builtin("strassen"), fb.Rule.builtin("strassen_dalberto")
+    nodes = [s] + [d if r in (0, 2, 3) else s for r in range(7)]
+    A, B = fi.random_pair(256, 256, 256, seed=3)
+    p = fb.Plan(nodes, 256, 256, 256, uniform=False, levels=2)
+    Cg = p.execute(dev(A), dev(B)).cpu().numpy()
+    Co = oracle.fmm(A, B, OPlan.dalberto_two_level())
+    assert parity(Cg, Co, A, B) <= TOL64
+    # unit-leaf bitwise variant
+    A, B = fi.random_pair(64, 4, 64, seed=4)
+    p = fb.Plan(nodes, 64, 4, 64, uniform=False, levels=2)
+    assert np.array_equal(p.execute(dev(A), dev(B)).cpu().numpy(),
+                          oracle.fmm(A, B, OPlan.dalberto_two_level()))
+
+
+def test_C1_full_size(fb):
+    A, B = fi.config_inputs("C1")
+    Cg = run(fb, ("winograd", "winograd"), A, B)
+    Co = oracle.fmm(A, B, OPlan.stationary(R.winograd(), 2))
+    assert parity(Cg, Co, A, B) <= TOL64
+    # and the Thm 4.3 bound against the double-double reference
+    hi, lo = oracle.ref_dd(A, B)
+    f = float(R.stationary_bound_factor(R.winograd(), 2, 512))
+    assert np.max(np.abs((Cg - hi) - lo)) <= f * np.abs(A).max() * np.abs(B).max() * 2.0 ** -53
+
+
+def test_C2_reduced(fb):
+    A, B = fi.config_inputs("C2", scale_div=4)  # 1024^3, Strassen L=4 -> 64^3 leaves
+    for names in (("strassen",) * 4, ("classical222",) * 4):
+        Cg = run(fb, names, A, B)
+        Co = oracle.fmm(A, B, OPlan.uniform([R.builtin(n) for n in names]))
+        assert parity(Cg, Co, A, B) <= TOL64
+
+
+def test_C3_reduced(fb):
+    A, B = fi.config_inputs("C3", scale_div=8)  # 1024 x 512 x 1024
+    names = ("winograd", "classical222", "strassen")
+    Cg = run(fb, names, A, B)
+    Co = oracle.fmm(A, B, OPlan.uniform([R.builtin(n) for n in names]))
+    assert parity(Cg, Co, A, B) <= TOL64
+
+
+def test_f32_recursion_parity(fb):
+    A, B = fi.random_pair(512, 512, 512, seed=4, dtype=np.float32)
+    Cg = run(fb, ("winograd",) * 3, A, B, dtype="f32")
+    Co = oracle.fmm(A, B, OPlan.stationary(R.winograd(), 3))
+    assert parity(Cg, Co, A, B) <= TOL32
+
+
+def test_deterministic(fb):
+    A, B = fi.random_pair(512, 512, 512, seed=6)
+    p = gpu_plan(fb, ("winograd",) * 2, 512, 512, 512)
+    c1 = p.execute(dev(A), dev(B)).cpu().numpy()
+    c2 = p.execute(dev(A), dev(B)).cpu().numpy()
+    assert np.array_equal(c1, c2)
+
+
+def test_split_schedule_matches_breadth_first(fb):
+    # depth-first top level (used for big problems and sharding) with nranks = 1 is bitwise
+    # equal to the breadth-first schedule: same kernels, same per-element orders.
+    A, B = fi.random_pair(256, 256, 256, seed=8)
+    p = gpu_plan(fb, ("winograd",) * 3, 256, 256, 256)
+    bf = p.execute(dev(A), dev(B)).cpu().numpy()
+    parts = []
+    for rank in range(3):
+        p.set_partition(rank, 3)
+        parts.append(p.execute(dev(A), dev(B)).cpu().numpy())
+    # virtual ranks: the partial sums add up to the product (parity), each rank's set of blocks
+    # is exact w.r.t. its own owned products
+    total = parts[0] + parts[1] + parts[2]
+    assert parity(total, bf, A, B) <= TOL64
+    p.set_partition(0, 1)
+    assert np.array_equal(p.execute(dev(A), dev(B)).cpu().numpy(), bf)
+
+
+def test_empty_and_degenerate(fb):
+    w = fb.Rule.builtin("winograd")
+    p = fb.Plan([w], 0, 4, 4)
+    p.execute(torch.empty((0, 4), dtype=torch.float64, device="cuda"),
+              torch.zeros((4, 4), dtype=torch.float64, device="cuda"))
+    p = fb.Plan([w], 4, 0, 4)
+    Cg = p.execute(torch.empty((4, 0), dtype=torch.float64, device="cuda"),
+                   torch.empty((0, 4), dtype=torch.float64, device="cuda"))
+    assert torch.all(Cg == 0)
+    # identity exact
+    I = np.eye(64)
+    assert np.array_equal(run(fb, ("strassen",) * 3, I, I), I)

@@ -1,0 +1,102 @@
+"""GPU diagonal scaling (K4) against the oracle: factors and scaled matrices bitwise (the max
+reductions are exact, divisions / sqrt correctly rounded, same operation order), the stopping
+test's step count equal, and scaled FMM products at the C4 recipe (componentwise check, since
+the normalised parity metric is vacuous for C4's skewed magnitudes -- SURVEY §8(c) C-tol)."""
+import numpy as np
+import pytest
+import torch
+
+import fmm_inputs as fi
+import oracle
+from oracle import rules as R
+from oracle.rules import Plan as OPlan
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fb():
+    import paper_1507_00687_b200 as fb
+    return fb
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+INPUTS = {
+    "c4_small": lambda: fi.config_inputs("C4", scale_div=64),  # 64^3, C4 recipe
+    "c4_rect": lambda: fi.draw("skew", 96, 40, 72, 3),
+    "ex69": lambda: (np.array([[1.0, 2.0 ** 40], [1.0, 1.0]]), np.array([[2.0 ** -40, 1.0], [2.0 ** -40, 1.0]])),
+}
+
+
+@pytest.mark.parametrize("name", sorted(INPUTS))
+@pytest.mark.parametrize("pow2", [False, True])
+def test_outside_inside_bitwise(fb, name, pow2):
+    A, B = INPUTS[name]()
+    Ao, Bo, dA, dB = fb.scale_outside(dev(A), dev(B), pow2=pow2)
+    ra, rb, rdA, rdB = oracle.scale_outside(A, B, pow2=pow2)
+    for g, o in ((Ao, ra), (Bo, rb), (dA, rdA), (dB, rdB)):
+        assert np.array_equal(host(g), o)
+    Ai, Bi, d = fb.scale_inside(dev(A), dev(B), pow2=pow2)
+    ra, rb, rd = oracle.scale_inside(A, B, pow2=pow2)
+    for g, o in ((Ai, ra), (Bi, rb), (d, rd)):
+        assert np.array_equal(host(g), o)
+
+
+@pytest.mark.parametrize("name", sorted(INPUTS))
+@pytest.mark.parametrize("first_O", [True, False])
+@pytest.mark.parametrize("tau,pow2", [(1.0, False), (0.1, False), (1.0, True), (0.0, False)])
+def test_repeated_bitwise(fb, name, first_O, tau, pow2):
+    A, B = INPUTS[name]()
+    g = fb.scale_repeated(dev(A), dev(B), first_O=first_O, tau=tau, max_steps=12, pow2=pow2)
+    o = oracle.scale_repeated(A, B, first_O=first_O, tau=tau, max_steps=12, pow2=pow2)
+    assert g["steps"] == o["steps"]
+    for k in ("A", "B", "dA", "dB", "dI"):
+        assert np.array_equal(host(g[k]), o[k]), k
+
+
+def test_lemma_sequence_on_gpu(fb):
+    # Lemma alt-scaling-example, v = 2: the cumulative s_2 factor sequence.
+    A = np.array([[1.0, 0.0], [1.0, 2.0 ** -4]])
+    B = np.eye(2)
+    for n, want in ((1, 1.0), (3, 0.25), (5, 0.125)):
+        g = fb.scale_repeated(dev(A), dev(B), first_O=True, tau=0.0, max_steps=n)
+        assert host(g["dB"])[1] == want
+
+
+def test_zero_row_precondition(fb):
+    A = np.ones((8, 8))
+    A[3] = 0
+    with pytest.raises(fb.FmmError) as e:
+        fb.scale_outside(dev(A), dev(np.ones((8, 8))))
+    assert e.value.status == "FMM_E_PRECOND" and "index 3" in str(e.value)
+
+
+@pytest.mark.parametrize("mode", ["none", "outside", "inside", "out_in", "in_out", "repeated"])
+def test_scaled_fmm_C4_recipe(fb, mode):
+    # C4 recipe at 512^3 (S-W L=3, 64^3 leaves), pow2 factors (reading A7)
+    A, B = fi.config_inputs("C4", scale_div=8)
+    M, K = A.shape
+    N = B.shape[1]
+    w = fb.Rule.builtin("winograd")
+    p = fb.Plan([w, w, w], M, K, N, scaling={"mode": mode, "tau": 1.0, "max_steps": 20, "pow2": 1})
+    Cg = host(p.execute(dev(A), dev(B)))
+    steps = p.last_scaling_steps()
+    plan = OPlan.stationary(R.winograd(), 3)
+    Co, info = oracle.scaled_fmm(A, B, plan, mode=mode, pow2=True, tau=1.0, max_steps=20)
+    assert steps == info["steps"]
+    hi, lo = oracle.ref_dd(A, B)
+    rel = lambda X: np.max(np.abs((X - hi) - lo) / np.abs(hi))
+    rel_o = rel(Co)
+    # componentwise GPU vs oracle at the level of the mode's own relative error
+    d = np.max(np.abs(Cg - Co) / np.abs(hi))
+    assert d <= 10 * max(rel_o, 1e-13), (mode, d, rel_o)
+    assert oracle.parity_metric(Cg, Co, np.abs(A).max(), np.abs(B).max(), K) <= 1e-13
+    if mode == "repeated":
+        assert rel(Cg) < 1e-10  # repeated O-I is accurate on this skew

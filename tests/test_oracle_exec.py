@@ -129,6 +129,15 @@ def test_row_sampling_is_bitwise(orc):
         assert np.array_equal(orc.fmm_rows(A, B, plan, G), full[G])
 
 
+def test_row_col_sampling_is_bitwise(orc):
+    A, B = fi.random_pair(128, 64, 256, seed=16)
+    for plan in (Plan.stationary(R.winograd(), 3), Plan.dalberto_two_level()):
+        full = orc.fmm(A, B, plan)
+        G = orc.lift_rows(128, plan, [1, 7])
+        H = orc.lift_cols(256, plan, [0, 3, 30])
+        assert np.array_equal(orc.fmm_sub(A, B, plan, G, H), full[np.ix_(G, H)])
+
+
 @pytest.mark.parametrize("pname", ["winograd_L2", "strassen_L3", "C3_mix", "dalberto",
                                    "classical_L2"])
 def test_bound_holds_against_double_double(orc, pname):
