@@ -3,10 +3,11 @@
 // sm_100a's tcgen05.mma has no f64 kind; FP64 tensor math is the warp-level DMMA
 // (mma.sync .f64 -> SASS DMMA.8x8x4), measured at 36.9 TFLOP/s on this pool's B200s
 // (profiles/r01_fp64_peak_microbench.txt; DFMA reaches 33.7).  Design:
-//   * CTA tile 128 x 128 x 16, 8 warps (2 x 4), warp tile 64 x 32 = 4 x 4 m16n8k4 fragments,
-//     64 fp64 accumulators per thread;
-//   * 4-stage cp.async (16-byte, L2-only .cg) pipeline global -> shared; shared rows padded
-//     (+4 doubles) so the 8-byte fragment loads of each half-warp hit 16 distinct bank pairs;
+//   * CTA tile BM x BN x BK, warps arranged WARPS_M x WARPS_N, warp tile WTM x WTN made of
+//     (WTM/16) x (WTN/8) m16n8k4 fragments (4 fp64 accumulators each per thread);
+//   * STAGES-deep cp.async (16-byte, L2-only .cg) pipeline global -> shared; shared rows padded
+//     by 4 doubles (row pitch = 4 mod 16 doubles) so the 8-byte fragment loads of each
+//     half-warp hit 16 distinct bank pairs (ncu: 0 shared-memory bank conflicts);
 //   * batched over the leaves of a level by grid.y with per-leaf operand descriptors;
 //     grouped rasterisation (8 tile-rows) inside a leaf for L2 reuse;
 //   * ragged edges handled by zero-fill (src-size 0) loads and guarded stores; a scalar
@@ -14,6 +15,7 @@
 // The leaf's k-order is the tensor core's (reading A4): not the oracle's
 // sequential order, covered by the parity tolerance.
 #include <cstdint>
+#include <cstdlib>
 
 #include "fmm_internal.h"
 
@@ -21,12 +23,6 @@ namespace fmm {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 4, THREADS = 256;
-constexpr int A_LD = BK + 4;  // 20 doubles per smem row of the A tile
-constexpr int B_LD = BN + 4;  // 132 doubles per smem row of the B tile
-constexpr int A_STAGE = BM * A_LD;
-constexpr int B_STAGE = BK * B_LD;
-constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8;
 constexpr int GROUP_M = 8;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -55,65 +51,78 @@ __device__ __forceinline__ void dmma16n8k4(double (&c)[4], double a0, double a1,
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-template <bool VEC>
+template <int BM_, int BN_, int BK_, int STAGES_, int WARPS_M_, int WARPS_N_, int MINB_ = 1>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_, MINB = MINB_;
+  static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
+  static constexpr int THREADS = WARPS_M * WARPS_N * 32;
+  static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
+  static constexpr int MI = WTM / 16, NI = WTN / 8;
+  static constexpr int A_LD = BK + 4, B_LD = BN + 4;
+  static constexpr int A_STAGE = BM * A_LD, B_STAGE = BK * B_LD;
+  static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8;
+  static_assert(A_LD % 16 == 4 && B_LD % 16 == 4, "pitch must be 4 mod 16 doubles");
+  static_assert((BM * BK / 2) % THREADS == 0 && (BK * BN / 2) % THREADS == 0, "chunking");
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+};
+
+template <typename C, bool VEC>
 __device__ __forceinline__ void load_tiles(double* As, double* Bs, const double* A, int64_t lda,
                                            const double* B, int64_t ldb, int64_t m, int64_t n,
                                            int64_t k, int64_t m0, int64_t n0, int64_t k0,
                                            int tid) {
   if constexpr (VEC) {
-    // A tile: 128 rows x 16 doubles = 1024 chunks of 16 B
+    constexpr int ACH = C::BK / 2;  // 16-byte chunks per A-tile row
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      int c = tid + q * THREADS;
-      int row = c >> 3, cc = (c & 7) * 2;
+    for (int q = 0; q < C::BM * C::BK / 2 / C::THREADS; ++q) {
+      int c = tid + q * C::THREADS;
+      int row = c / ACH, cc = (c % ACH) * 2;
       int64_t gr = m0 + row, gc = k0 + cc;
       bool ok = gr < m && gc < k;
-      const double* src = ok ? A + gr * lda + gc : A;
-      cp16(smem_u32(As + row * A_LD + cc), src, ok);
+      cp16(smem_u32(As + row * C::A_LD + cc), ok ? A + gr * lda + gc : A, ok);
     }
-    // B tile: 16 rows x 128 doubles
+    constexpr int BCH = C::BN / 2;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      int c = tid + q * THREADS;
-      int row = c >> 6, cc = (c & 63) * 2;
+    for (int q = 0; q < C::BK * C::BN / 2 / C::THREADS; ++q) {
+      int c = tid + q * C::THREADS;
+      int row = c / BCH, cc = (c % BCH) * 2;
       int64_t gr = k0 + row, gc = n0 + cc;
       bool ok = gr < k && gc < n;
-      const double* src = ok ? B + gr * ldb + gc : B;
-      cp16(smem_u32(Bs + row * B_LD + cc), src, ok);
+      cp16(smem_u32(Bs + row * C::B_LD + cc), ok ? B + gr * ldb + gc : B, ok);
     }
   } else {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      int c = tid + q * THREADS;
-      int row = c >> 4, cc = c & 15;
+    for (int q = 0; q < C::BM * C::BK / C::THREADS; ++q) {
+      int c = tid + q * C::THREADS;
+      int row = c / C::BK, cc = c % C::BK;
       int64_t gr = m0 + row, gc = k0 + cc;
       bool ok = gr < m && gc < k;
-      cp8(smem_u32(As + row * A_LD + cc), ok ? A + gr * lda + gc : A, ok);
+      cp8(smem_u32(As + row * C::A_LD + cc), ok ? A + gr * lda + gc : A, ok);
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      int c = tid + q * THREADS;
-      int row = c >> 7, cc = c & 127;
+    for (int q = 0; q < C::BK * C::BN / C::THREADS; ++q) {
+      int c = tid + q * C::THREADS;
+      int row = c / C::BN, cc = c % C::BN;
       int64_t gr = k0 + row, gc = n0 + cc;
       bool ok = gr < k && gc < n;
-      cp8(smem_u32(Bs + row * B_LD + cc), ok ? B + gr * ldb + gc : B, ok);
+      cp8(smem_u32(Bs + row * C::B_LD + cc), ok ? B + gr * ldb + gc : B, ok);
     }
   }
 }
 
-template <bool VEC>
-__global__ void __launch_bounds__(THREADS, 1)
+template <typename C, bool VEC>
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
     k2_gemm_f64(const LeafNode* __restrict__ leaves, Bases bases, int64_t m, int64_t n,
                 int64_t k, int tiles_m, int tiles_n) {
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
-  double* Bs = smem + STAGES * A_STAGE;
+  double* Bs = smem + C::STAGES * C::A_STAGE;
 
   const LeafNode& lf = leaves[blockIdx.y];
   int64_t lda, ldb, ldc;
   const double* A = op_ptr<const double>(bases, lf.a, lda);
   const double* B = op_ptr<const double>(bases, lf.b, ldb);
-  double* C = op_ptr<double>(bases, lf.c, ldc);
+  double* Cp = op_ptr<double>(bases, lf.c, ldc);
 
   // grouped rasterisation
   const int tile = blockIdx.x;
@@ -123,73 +132,74 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int gsz = min(tiles_m - first_m, GROUP_M);
   const int tm = first_m + (tile % per_group) % gsz;
   const int tn = (tile % per_group) / gsz;
-  const int64_t m0 = (int64_t)tm * BM, n0 = (int64_t)tn * BN;
+  const int64_t m0 = (int64_t)tm * C::BM, n0 = (int64_t)tn * C::BN;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int g = lane >> 2, t = lane & 3;
 
-  double acc[4][4][4];
+  double acc[C::MI][C::NI][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < C::MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < C::NI; ++j)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
 
-  const int KT = (int)((k + BK - 1) / BK);
+  const int KT = (int)((k + C::BK - 1) / C::BK);
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < KT) load_tiles<VEC>(As + s * A_STAGE, Bs + s * B_STAGE, A, lda, B, ldb, m, n, k, m0,
-                                n0, (int64_t)s * BK, tid);
+  for (int s = 0; s < C::STAGES - 1; ++s) {
+    if (s < KT)
+      load_tiles<C, VEC>(As + s * C::A_STAGE, Bs + s * C::B_STAGE, A, lda, B, ldb, m, n, k, m0, n0,
+                         (int64_t)s * C::BK, tid);
     cp_commit();
   }
 
   for (int kt = 0; kt < KT; ++kt) {
-    cp_wait<STAGES - 2>();
+    cp_wait<C::STAGES - 2>();
     __syncthreads();
     {
-      int nk = kt + STAGES - 1;
+      int nk = kt + C::STAGES - 1;
       if (nk < KT) {
-        int slot = nk % STAGES;
-        load_tiles<VEC>(As + slot * A_STAGE, Bs + slot * B_STAGE, A, lda, B, ldb, m, n, k, m0,
-                        n0, (int64_t)nk * BK, tid);
+        int slot = nk % C::STAGES;
+        load_tiles<C, VEC>(As + slot * C::A_STAGE, Bs + slot * C::B_STAGE, A, lda, B, ldb, m, n, k,
+                           m0, n0, (int64_t)nk * C::BK, tid);
       }
       cp_commit();
     }
-    const int slot = kt % STAGES;
-    const double* as = As + slot * A_STAGE + (wm * 64 + g) * A_LD + t;
-    const double* bs = Bs + slot * B_STAGE + t * B_LD + wn * 32 + g;
+    const int slot = kt % C::STAGES;
+    const double* as = As + slot * C::A_STAGE + (wm * C::WTM + g) * C::A_LD + t;
+    const double* bs = Bs + slot * C::B_STAGE + t * C::B_LD + wn * C::WTN + g;
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[4][2], bf[4];
+    for (int kk = 0; kk < C::BK; kk += 4) {
+      double af[C::MI][2], bf[C::NI];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        af[i][0] = as[(i * 16) * A_LD + kk];
-        af[i][1] = as[(i * 16 + 8) * A_LD + kk];
+      for (int i = 0; i < C::MI; ++i) {
+        af[i][0] = as[(i * 16) * C::A_LD + kk];
+        af[i][1] = as[(i * 16 + 8) * C::A_LD + kk];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = bs[kk * B_LD + j * 8];
+      for (int j = 0; j < C::NI; ++j) bf[j] = bs[kk * C::B_LD + j * 8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < C::MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma16n8k4(acc[i][j], af[i][0], af[i][1], bf[j]);
+        for (int j = 0; j < C::NI; ++j) dmma16n8k4(acc[i][j], af[i][0], af[i][1], bf[j]);
     }
   }
   cp_wait<0>();
 
   // epilogue: c0,c1 at (row g, cols 2t, 2t+1); c2,c3 at row g+8
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < C::MI; ++i) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int64_t row = m0 + wm * 64 + i * 16 + g + h * 8;
+      const int64_t row = m0 + wm * C::WTM + i * 16 + g + h * 8;
       if (row >= m) continue;
-      double* crow = C + row * ldc;
+      double* crow = Cp + row * ldc;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int64_t col = n0 + wn * 32 + j * 8 + 2 * t;
+      for (int j = 0; j < C::NI; ++j) {
+        const int64_t col = n0 + wn * C::WTN + j * 8 + 2 * t;
         const double v0 = acc[i][j][2 * h], v1 = acc[i][j][2 * h + 1];
         if (VEC && col + 1 < n) {
           *reinterpret_cast<double2*>(crow + col) = make_double2(v0, v1);
@@ -202,26 +212,71 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+template <typename C>
+cudaError_t launch_cfg(const LeafNode* dev_leaves, int count, int64_t m, int64_t n, int64_t k,
+                       const Bases& b, bool vec, cudaStream_t st) {
+  const int tiles_m = (int)((m + C::BM - 1) / C::BM), tiles_n = (int)((n + C::BN - 1) / C::BN);
+  dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)count);
+  cudaError_t e;
+  if (vec) {
+    e = cudaFuncSetAttribute(k2_gemm_f64<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    k2_gemm_f64<C, true><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(dev_leaves, b, m, n, k, tiles_m,
+                                                                 tiles_n);
+  } else {
+    e = cudaFuncSetAttribute(k2_gemm_f64<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    k2_gemm_f64<C, false><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(dev_leaves, b, m, n, k, tiles_m,
+                                                                  tiles_n);
+  }
+  return cudaGetLastError();
+}
+
+// Variants (selected by env FMM_K2_VARIANT for experiments; default chosen from measurements,
+// profiles/r01_k2_variants.txt).
+using V1 = Cfg<128, 128, 16, 4, 2, 4>;  // 8 warps, 64 x 32 warp tiles
+using V2 = Cfg<128, 128, 32, 3, 2, 4>;  // BK = 32
+using V3 = Cfg<128, 128, 16, 4, 4, 4>;  // 16 warps, 32 x 32 warp tiles
+using V4 = Cfg<128, 128, 32, 3, 4, 4>;  // 16 warps, BK = 32
+using V5 = Cfg<64, 128, 16, 4, 2, 4, 2>;  // 8 warps, 32 x 32 warp tiles (2 CTAs / SM)
+using V6 = Cfg<64, 128, 16, 3, 2, 4, 2>;
+using V7 = Cfg<128, 64, 16, 3, 4, 2, 2>;
+using V8 = Cfg<64, 128, 32, 2, 2, 4, 2>;
+using V9 = Cfg<64, 64, 16, 4, 2, 2, 3>;   // 4 warps, 3 CTAs / SM
+using V10 = Cfg<64, 256, 16, 3, 2, 8, 1>; // 16 warps, 32 x 32 warp tiles
+using V11 = Cfg<64, 64, 16, 3, 2, 2, 4>;  // 4 warps, 4 CTAs / SM
+using V12 = Cfg<64, 64, 32, 2, 2, 2, 3>;
+
+int variant() {
+  static int v = [] {
+    const char* e = getenv("FMM_K2_VARIANT");
+    return e ? atoi(e) : 9;
+  }();
+  return v;
+}
+
 }  // namespace
 
 cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
                             int64_t k, const Bases& b, bool vec, cudaStream_t st) {
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
-  const int tiles_m = (int)((m + BM - 1) / BM), tiles_n = (int)((n + BN - 1) / BN);
-  dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)count);
-  cudaError_t e;
-  if (vec) {
-    e = cudaFuncSetAttribute(k2_gemm_f64<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    k2_gemm_f64<true><<<grid, THREADS, SMEM_BYTES, st>>>(dev_leaves, b, m, n, k, tiles_m, tiles_n);
-  } else {
-    e = cudaFuncSetAttribute(k2_gemm_f64<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    k2_gemm_f64<false><<<grid, THREADS, SMEM_BYTES, st>>>(dev_leaves, b, m, n, k, tiles_m, tiles_n);
+  switch (variant()) {
+    case 2: return launch_cfg<V2>(dev_leaves, count, m, n, k, b, vec, st);
+    case 3: return launch_cfg<V3>(dev_leaves, count, m, n, k, b, vec, st);
+    case 4: return launch_cfg<V4>(dev_leaves, count, m, n, k, b, vec, st);
+    case 5: return launch_cfg<V5>(dev_leaves, count, m, n, k, b, vec, st);
+    case 6: return launch_cfg<V6>(dev_leaves, count, m, n, k, b, vec, st);
+    case 7: return launch_cfg<V7>(dev_leaves, count, m, n, k, b, vec, st);
+    case 8: return launch_cfg<V8>(dev_leaves, count, m, n, k, b, vec, st);
+    case 9: return launch_cfg<V9>(dev_leaves, count, m, n, k, b, vec, st);
+    case 10: return launch_cfg<V10>(dev_leaves, count, m, n, k, b, vec, st);
+    case 11: return launch_cfg<V11>(dev_leaves, count, m, n, k, b, vec, st);
+    case 12: return launch_cfg<V12>(dev_leaves, count, m, n, k, b, vec, st);
+    case 1: return launch_cfg<V1>(dev_leaves, count, m, n, k, b, vec, st);
+    default: return launch_cfg<V9>(dev_leaves, count, m, n, k, b, vec, st);
   }
-  return cudaGetLastError();
 }
 
 }  // namespace fmm

@@ -65,11 +65,14 @@ __device__ __forceinline__ void st_vec(T* p, const Vec<T, VEC>& r) {
   }
 }
 
-constexpr int kThreads = 128;  // threads per block (x: column vectors)
+constexpr int kThreads = 256;  // threads per block (x: column vectors)
 constexpr int kRowsPerBlock = 4;
 
 // grid: x = column chunks of kThreads vectors, y = row groups of kRowsPerBlock, z = node.
-template <typename T, int VEC>
+// NBLK: compile-time bound on the number of input sub-blocks (4 for 2x2 rules) so that the
+// per-thread input registers stay small; two rows are loaded before either is combined, so
+// each thread keeps up to 2*NBLK 16-byte loads in flight.
+template <typename T, int VEC, int NBLK>
 __global__ void __launch_bounds__(kThreads) k1_lincomb(const K1Node* __restrict__ nodes,
                                                        const double* __restrict__ coef_all,
                                                        Bases bases, int64_t rows, int64_t cols,
@@ -96,39 +99,46 @@ __global__ void __launch_bounds__(kThreads) k1_lincomb(const K1Node* __restrict_
   const int64_t jv = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * VEC;
   if (jv >= cols) return;
   const int64_t i0 = (int64_t)blockIdx.y * kRowsPerBlock;
-  for (int ii = 0; ii < kRowsPerBlock; ++ii) {
-    const int64_t i = i0 + ii;
-    if (i >= rows) break;
-    Vec<T, VEC> x[kMaxBlk];
+  for (int ii = 0; ii < kRowsPerBlock; ii += 2) {
+    Vec<T, VEC> x[2][NBLK];
 #pragma unroll
-    for (int b = 0; b < kMaxBlk; ++b) {
-      if (b < nblk && ((need >> b) & 1u)) {
-        const int p = b % P, q = b / P;  // column-major block index
-        x[b] = ld_vec<T, VEC>(in + (p * rows + i) * ldi + q * cols + jv);
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = i0 + ii + h;
+#pragma unroll
+      for (int b = 0; b < NBLK; ++b) {
+        if (b < nblk && ((need >> b) & 1u) && i < rows) {
+          const int p = b % P, q = b / P;  // column-major block index
+          x[h][b] = ld_vec<T, VEC>(in + (p * rows + i) * ldi + q * cols + jv);
+        }
       }
     }
-    for (int r = 0; r < R; ++r) {
-      if (!((omask >> r) & 1u)) continue;
-      Vec<T, VEC> acc;
-      bool started = false;
 #pragma unroll
-      for (int b = 0; b < kMaxBlk; ++b) {
-        if (b >= nblk) break;
-        const double u = cf[b * R + r];
-        if (u == 0.0) continue;
-        const T ut = (T)u;
+    for (int h = 0; h < 2; ++h) {
+      const int64_t i = i0 + ii + h;
+      if (i >= rows) break;
+      for (int r = 0; r < R; ++r) {
+        if (!((omask >> r) & 1u)) continue;
+        Vec<T, VEC> acc;
+        bool started = false;
 #pragma unroll
-        for (int e = 0; e < VEC; ++e)
-          acc.v[e] = started ? add_rn<T>(acc.v[e], mul_rn<T>(ut, x[b].v[e])) : mul_rn<T>(ut, x[b].v[e]);
-        started = true;
+        for (int b = 0; b < NBLK; ++b) {
+          if (b >= nblk) break;
+          const double u = cf[b * R + r];
+          if (u == 0.0) continue;
+          const T ut = (T)u;
+#pragma unroll
+          for (int e = 0; e < VEC; ++e)
+            acc.v[e] = started ? add_rn<T>(acc.v[e], mul_rn<T>(ut, x[h][b].v[e])) : mul_rn<T>(ut, x[h][b].v[e]);
+          started = true;
+        }
+        if (!started) {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) acc.v[e] = (T)0;
+        }
+        int64_t ldo;
+        T* o = op_ptr<T>(bases, nd.out[r], ldo);
+        st_vec<T, VEC>(o + i * ldo + jv, acc);
       }
-      if (!started) {
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) acc.v[e] = (T)0;
-      }
-      int64_t ldo;
-      T* o = op_ptr<T>(bases, nd.out[r], ldo);
-      st_vec<T, VEC>(o + i * ldo + jv, acc);
     }
   }
 }
@@ -251,12 +261,18 @@ cudaError_t launch_k1(const Step& s, const void* dev_nodes, const double* dev_co
                       const Bases& b, bool vec, cudaStream_t st) {
   if (s.count == 0 || s.rows == 0 || s.cols == 0) return cudaSuccess;
   constexpr int V = 16 / sizeof(T);
-  if (vec)
-    k1_lincomb<T, V><<<grid_for(s, V), kThreads, 0, st>>>((const K1Node*)dev_nodes, dev_coef, b,
-                                                          s.rows, s.cols, s.P, s.Q, s.R);
-  else
-    k1_lincomb<T, 1><<<grid_for(s, 1), kThreads, 0, st>>>((const K1Node*)dev_nodes, dev_coef, b,
-                                                          s.rows, s.cols, s.P, s.Q, s.R);
+  const K1Node* nd = (const K1Node*)dev_nodes;
+  if (s.P * s.Q <= 4) {
+    if (vec)
+      k1_lincomb<T, V, 4><<<grid_for(s, V), kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
+    else
+      k1_lincomb<T, 1, 4><<<grid_for(s, 1), kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
+  } else {
+    if (vec)
+      k1_lincomb<T, V, kMaxBlk><<<grid_for(s, V), kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
+    else
+      k1_lincomb<T, 1, kMaxBlk><<<grid_for(s, 1), kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
+  }
   return cudaGetLastError();
 }
 
