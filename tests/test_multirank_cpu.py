@@ -1,0 +1,83 @@
+"""Multi-rank host logic on CPU (gloo, world size 2): the library's top-level partition
+(fmm_plan_owned) assigns every top-level product to exactly one rank, and the
+per-rank partial sums C^(p) = sum_{owned r} w_kr M_r (computed here with oracle building blocks)
+summed across ranks by a collective equal the full product within the parity tolerance."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import fmm_inputs as fi
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _partial_oracle(rank, nranks, owned, A, B):
+    import oracle
+    from oracle import rules as R
+    w = R.winograd()
+    S, T = oracle.node_st(w, A, B)
+    sub = R.Plan.stationary(w, 1)
+    mb, nb = A.shape[0] // 2, B.shape[1] // 2
+    Wf = w.as_float()[2]
+    C = np.zeros((A.shape[0], B.shape[1]))
+    started = [False] * 4
+    for r in owned:
+        Mr = oracle.fmm(S[r], T[r], sub)
+        for k in range(4):
+            if Wf[k, r] == 0:
+                continue
+            ia, jb = divmod(k, 2)
+            blk = C[ia * mb:(ia + 1) * mb, jb * nb:(jb + 1) * nb]
+            blk[...] = Wf[k, r] * Mr if not started[k] else blk + Wf[k, r] * Mr
+            started[k] = True
+    return C
+
+
+def _worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1507_00687_b200 as fb
+    w = fb.Rule.builtin("winograd")
+    plan = fb.Plan([w, w], 128, 128, 128)
+    owned = plan.owned(rank, world)
+    A, B = fi.random_pair(128, 128, 128, seed=21)
+    part = torch.from_numpy(_partial_oracle(rank, world, owned, A, B))
+    dist.all_reduce(part)  # the exchange step (NCCL reduce on GPUs)
+    counts = torch.zeros(7, dtype=torch.int64)
+    counts[owned] = 1
+    dist.all_reduce(counts)
+    if rank == 0:
+        out_q.put((part.numpy(), counts.numpy(), owned))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_two_rank_partition_and_reduce(world):
+    import oracle
+    from oracle import rules as R
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    total, counts, owned0 = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert counts.tolist() == [1] * 7  # every top-level product exactly once
+    assert owned0 == [0, 2, 4, 6]
+    A, B = fi.random_pair(128, 128, 128, seed=21)
+    full = oracle.fmm(A, B, R.Plan.stationary(R.winograd(), 2))
+    assert oracle.parity_metric(total, full, np.abs(A).max(), np.abs(B).max(), 128) <= 1e-13
