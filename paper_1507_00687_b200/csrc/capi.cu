@@ -247,6 +247,9 @@ struct Builder {
     st.count = (int)lf.size();
     st.dev_off = push(lf);
     st.rows = p->lm[p->L]; st.cols = p->ln[p->L]; st.inner = p->lk[p->L];
+    st.arena_off = -1;
+    if (p->dtype == FMM_F32 && p->leaf != FMM_LEAF_NATIVE)
+      st.arena_off = ws_alloc((int64_t)tf32_arena_floats(st.count, st.rows, st.cols, st.inner));
     p->steps.push_back(st);
   }
 
@@ -463,7 +466,8 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
         if (p->dtype == FMM_F64)
           e = launch_gemm_f64((const LeafNode*)nd, s.count, s.rows, s.cols, s.inner, b, vec, st);
         else
-          e = launch_gemm_f32((const LeafNode*)nd, s.count, s.rows, s.cols, s.inner, b, vec, p->leaf, st);
+          e = launch_gemm_f32((const LeafNode*)nd, s.count, s.rows, s.cols, s.inner, b, vec, p->leaf,
+                              s.arena_off >= 0 ? (float*)b.p[BASE_WS] + s.arena_off : nullptr, st);
         break;
     }
     if (e != cudaSuccess) return cuda_status(e, "fmm_execute launch");
@@ -961,7 +965,8 @@ fmm_status fmm_gemm(int dtype, int leaf, int64_t M, int64_t K, int64_t N, const 
   cudaStream_t st = (cudaStream_t)stream;
   LeafNode lf{Op{BASE_A, 0, 0, 0, -1}, Op{BASE_B, 0, 0, 0, -1}, Op{BASE_C, 0, 0, 0, -1}};
   void* dmem = nullptr;
-  cudaError_t e = cudaMallocAsync(&dmem, sizeof lf, st);
+  const size_t arena = (dtype == FMM_F32 && leaf != FMM_LEAF_NATIVE) ? tf32_arena_floats(1, M, N, K) * 4 : 0;
+  cudaError_t e = cudaMallocAsync(&dmem, 256 + arena, st);
   if (e != cudaSuccess) return cuda_status(e, "fmm_gemm alloc");
   e = cudaMemcpyAsync(dmem, &lf, sizeof lf, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -973,7 +978,8 @@ fmm_status fmm_gemm(int dtype, int leaf, int64_t M, int64_t K, int64_t N, const 
                    ldc % vecn == 0 && K % vecn == 0 && N % vecn == 0;
   if (e == cudaSuccess)
     e = dtype == FMM_F64 ? launch_gemm_f64((const LeafNode*)dmem, 1, M, N, K, b, vec, st)
-                         : launch_gemm_f32((const LeafNode*)dmem, 1, M, N, K, b, vec, leaf, st);
+                         : launch_gemm_f32((const LeafNode*)dmem, 1, M, N, K, b, vec, leaf,
+                                           arena ? (float*)((uint8_t*)dmem + 256) : nullptr, st);
   cudaError_t e2 = cudaFreeAsync(dmem, st);
   if (e == cudaSuccess) e = e2;
   return cuda_status(e, "fmm_gemm");

@@ -93,6 +93,7 @@ struct Step {
   int64_t dev_off;   // byte offset of the node array in the plan's device descriptor buffer
   int64_t rows, cols, inner;  // sub-block dims (K1/K3/ACC/ZERO) or m, n, k (K2)
   int P, Q, R;       // K1: split P x Q, rank R.  K3/ACC/ZERO: P = M0, Q = N0, R
+  int64_t arena_off; // K2 FP32 tensor-core leaves: offset (elements) of the hi/lo arena in ws
   bool vec_ok;       // all ws offsets / dims allow 16-byte vectors (caller bases checked later)
 };
 
@@ -122,7 +123,10 @@ cudaError_t launch_zero(const Step& s, const void* dev_nodes, const Bases& b, cu
 cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
                             int64_t k, const Bases& b, bool vec, cudaStream_t st);
 cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
-                            int64_t k, const Bases& b, bool vec, int leaf, cudaStream_t st);
+                            int64_t k, const Bases& b, bool vec, int leaf, float* arena,
+                            cudaStream_t st);
+// floats of workspace the tensor-core FP32 leaf needs for a batch (hi / lo operand arena)
+size_t tf32_arena_floats(int64_t count, int64_t m, int64_t n, int64_t k);
 
 // ---- error reporting ------------------------------------------------------------------------
 void set_error(const std::string& msg);

@@ -7,7 +7,8 @@
 namespace fmm {
 
 cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
-                             int64_t k, const Bases& b, int passes, cudaStream_t st);
+                             int64_t k, const Bases& b, int passes, float* arena,
+                             cudaStream_t st);
 
 namespace {
 
@@ -97,11 +98,12 @@ __global__ void __launch_bounds__(THREADS)
 }  // namespace
 
 cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
-                            int64_t k, const Bases& b, bool vec, int leaf, cudaStream_t st) {
+                            int64_t k, const Bases& b, bool vec, int leaf, float* arena,
+                            cudaStream_t st) {
   (void)vec;
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
   if (leaf == FMM_LEAF_TF32 || leaf == FMM_LEAF_3XTF32)
-    return launch_gemm_tf32(dev_leaves, count, m, n, k, b, leaf == FMM_LEAF_TF32 ? 1 : 3, st);
+    return launch_gemm_tf32(dev_leaves, count, m, n, k, b, leaf == FMM_LEAF_TF32 ? 1 : 3, arena, st);
   const int tiles_m = (int)((m + BM - 1) / BM), tiles_n = (int)((n + BN - 1) / BN);
   dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)count);
   k2_gemm_f32_simt<<<grid, THREADS, 0, st>>>(dev_leaves, b, m, n, k, tiles_n);

@@ -49,3 +49,21 @@ def test_c5_f64_sampled_parity_and_bound(c5):
     hi, lo = oracle.ref_dd(An, np.ascontiguousarray(Bn[:, H]), rows=G[:8])
     err = np.max(np.abs((Cg[:8] - hi) - lo))
     assert err <= f_fmm * amax * bmax * eps
+
+
+def test_c5_f32_3xtf32_sampled_parity(c5):
+    # the FP32 variant of C5 (FP64 draws cast to FP32), 3xTF32 tensor-core leaves
+    import paper_1507_00687_b200 as fb
+    A, B = c5
+    A32, B32 = A.float(), B.float()
+    w = fb.Rule.builtin("winograd")
+    plan = fb.Plan([w, w, w], N, N, N, dtype="f32", leaf=fb.fmm.LEAF_3XTF32)
+    Cd = plan.execute(A32.cuda(), B32.cuda())
+    torch.cuda.synchronize()
+    An, Bn = A32.numpy(), B32.numpy()
+    op = R.Plan.stationary(R.winograd(), 3)
+    G = oracle.lift_rows(N, op, [0, 4095])
+    H = oracle.lift_cols(N, op, [3, 2048])
+    Co = oracle.fmm_sub(An, Bn, op, G, H)
+    Cg = Cd[torch.from_numpy(G).cuda()][:, torch.from_numpy(H).cuda()].cpu().numpy()
+    assert oracle.parity_metric(Cg, Co, float(np.abs(An).max()), float(np.abs(Bn).max()), N) <= 5e-5

@@ -80,6 +80,36 @@ def test_leaf_gemm_f32(fb):
     assert parity(Cg, oracle.fmm(A, B, OPlan([])), A, B) <= TOL32
 
 
+@pytest.mark.parametrize("shape", [(128, 32, 256), (256, 512, 384), (200, 300, 100), (7, 5, 3),
+                                   (1024, 1024, 1024)])
+def test_leaf_gemm_tf32_tensor_core(fb, shape):
+    # tcgen05 kind::tf32 leaf: 3xTF32 must pass the FP32 parity tolerance against the FP32
+    # oracle leaf; single-pass TF32 is a labelled variant (error ~ 2^-11 per product).
+    M, K, N = shape
+    A, B = fi.random_pair(M, K, N, seed=K, dtype=np.float32)
+    Co = oracle.fmm(A, B, OPlan([]))
+    C3 = fb.gemm(dev(A), dev(B), leaf=fb.fmm.LEAF_3XTF32).cpu().numpy()
+    C1 = fb.gemm(dev(A), dev(B), leaf=fb.fmm.LEAF_TF32).cpu().numpy()
+    p3, p1 = parity(C3, Co, A, B), parity(C1, Co, A, B)
+    assert p3 <= TOL32
+    assert p3 < p1  # the lo terms are really applied
+    exact = A.astype(np.float64) @ B.astype(np.float64)
+    absab = np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64)
+    # 3xTF32 with FP32 tensor-core accumulation: componentwise within K * 2^-22 sum|a||b|
+    assert np.all(np.abs(C3 - exact) <= K * 2.0 ** -22 * absab + 1e-30)
+    assert np.all(np.abs(C1 - exact) <= K * 2.0 ** -9 * absab + 1e-30)
+
+
+@pytest.mark.parametrize("names", [("winograd", "winograd"), ("strassen",) * 3])
+def test_f32_recursion_3xtf32(fb, names):
+    A, B = fi.random_pair(512, 512, 512, seed=14, dtype=np.float32)
+    p = fb.Plan([fb.Rule.builtin(n) for n in names], 512, 512, 512, dtype="f32",
+                leaf=fb.fmm.LEAF_3XTF32)
+    Cg = p.execute(dev(A), dev(B)).cpu().numpy()
+    Co = oracle.fmm(A, B, OPlan.uniform([R.builtin(n) for n in names]))
+    assert parity(Cg, Co, A, B) <= TOL32
+
+
 # ---- K1 / K3 bitwise -----------------------------------------------------------------------------
 
 @pytest.mark.parametrize("name", sorted(R.BUILTINS))
