@@ -127,6 +127,12 @@ void fmm_plan_destroy(fmm_plan* plan);
  * nranks = 1 restores the full computation.  Host-only; call before fmm_execute. */
 fmm_status fmm_plan_set_partition(fmm_plan* plan, int rank, int nranks);
 
+/* Schedule control (host-only): 0 = automatic (breadth-first unless its workspace exceeds
+ * 24 GiB), 1 = breadth-first over all levels, 2 = depth-first over the top-level products
+ * (each subtree breadth-first, top-level accumulation r ascending).  Results are bitwise
+ * identical across schedules. */
+fmm_status fmm_plan_set_schedule(fmm_plan* plan, int schedule);
+
 /* Host-only query: owned[r] = 1 if top-level product r is computed by `rank` (R entries). */
 fmm_status fmm_plan_owned(const fmm_plan* plan, int rank, int nranks, int32_t* owned, int* R);
 

@@ -102,6 +102,7 @@ struct fmm_plan {
   std::vector<int64_t> lm, lk, ln;          // node dims at level l (l = 0..L)
   fmm_scaling scaling{FMM_SCALE_NONE, 1, 1.0, 20, 0};
   int rank = 0, nranks = 1;
+  int schedule = 0;  // 0 auto, 1 breadth-first, 2 depth-first top level
   ncclComm_t comm = nullptr;
   // compiled schedule
   std::vector<Step> steps;
@@ -118,6 +119,14 @@ struct fmm_plan {
   size_t scale_bytes = 0;      // scaling region (A', B', factors, scratch), placed first
   bool dims_vec_ok = true;     // every level's column dims / offsets multiple of the vector
   int64_t launches = 0;
+  // depth-first top level: steps [begin, end) of top-level product r (for host-copy overlap)
+  struct RGroup {
+    int r;
+    size_t begin, end;
+  };
+  std::vector<RGroup> groups;
+  mutable cudaStream_t copy_h2d = nullptr, copy_d2h = nullptr;
+  mutable int copy_dev = -1;
   // optional per-step timing (events recorded on the launch stream)
   bool timing = false;
   mutable std::mutex tmu;
@@ -127,6 +136,8 @@ struct fmm_plan {
 };
 
 fmm_plan::~fmm_plan() {
+  if (copy_h2d) cudaStreamDestroy(copy_h2d);
+  if (copy_d2h) cudaStreamDestroy(copy_d2h);
   for (auto& u : ev_used) { cudaEventDestroy(u.second.first); cudaEventDestroy(u.second.second); }
   for (auto e : ev_pool) cudaEventDestroy(e);
   if (dev_coef) cudaFree(dev_coef);
@@ -304,7 +315,8 @@ struct Builder {
                      p->lm[l + 1] * p->ln[l + 1]);
     }
     const int64_t bf_bytes = bf * elem_size(p->dtype);
-    const bool split = p->nranks > 1 || bf_bytes > (int64_t)24 << 30;
+    const bool split = p->schedule == 2 || p->nranks > 1 ||
+                       (p->schedule == 0 && bf_bytes > (int64_t)24 << 30);
     if (!split) {
       breadth_first(0, {root});
       return;
@@ -315,6 +327,7 @@ struct Builder {
     for (int r = 0; r < ru.R; ++r) {
       if (r % p->nranks != p->rank) continue;
       ws_elems = mark;  // subtrees run one after another on one stream: reuse the workspace
+      const size_t g0 = p->steps.size();
       std::vector<Node> kid = emit_k1(0, {root}, r);
       if (p->L > 1) {
         breadth_first(1, kid);
@@ -335,6 +348,7 @@ struct Builder {
       st.kind = STEP_ACC; st.count = 1; st.dev_off = push(std::vector<AccNode>{a});
       st.rows = p->lm[1]; st.cols = p->ln[1]; st.P = ru.m0; st.Q = ru.n0; st.R = ru.R;
       p->steps.push_back(st);
+      p->groups.push_back({r, g0, p->steps.size()});
     }
     const uint32_t all = (ru.m0 * ru.n0 >= 32) ? 0xffffffffu : ((1u << (ru.m0 * ru.n0)) - 1u);
     if ((started & all) != all) {
@@ -351,6 +365,7 @@ void scaling_steps(const fmm_scaling& sc, std::string* steps, double* tau);
 
 fmm_status compile_plan(fmm_plan* p) {
   p->steps.clear();
+  p->groups.clear();
   {
     std::lock_guard<std::mutex> g(p->dev_mu);
     if (p->dev_desc) { cudaFree(p->dev_desc); p->dev_desc = nullptr; }
@@ -452,8 +467,11 @@ struct TimedLaunch {
 };
 
 template <typename T>
-static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStream_t st) {
-  for (const Step& s : p->steps) {
+static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStream_t st,
+                            size_t i0 = 0, size_t i1 = (size_t)-1) {
+  if (i1 > p->steps.size()) i1 = p->steps.size();
+  for (size_t si = i0; si < i1; ++si) {
+    const Step& s = p->steps[si];
     const void* nd = (const uint8_t*)p->dev_desc + s.dev_off;
     TimedLaunch tl(p, s.kind, st);
     cudaError_t e = cudaSuccess;
@@ -698,6 +716,12 @@ fmm_status fmm_plan_set_partition(fmm_plan* p, int rank, int nranks) {
   return compile_plan(p);
 }
 
+fmm_status fmm_plan_set_schedule(fmm_plan* p, int schedule) {
+  if (!p || schedule < 0 || schedule > 2) { set_error("fmm_plan_set_schedule: bad args"); return FMM_E_ARG; }
+  p->schedule = schedule;
+  return compile_plan(p);
+}
+
 fmm_status fmm_plan_owned(const fmm_plan* p, int rank, int nranks, int32_t* owned, int* R) {
   if (!p || nranks < 1 || rank < 0 || rank >= nranks) { set_error("fmm_plan_owned: bad args"); return FMM_E_ARG; }
   int RR = p->L > 0 ? p->rules[p->node_rule[0][0]].R : 1;
@@ -814,6 +838,127 @@ fmm_status fmm_plan_step_times(fmm_plan* p, double* ms, int64_t* launches) {
   return cuda_status(err, "fmm_plan_step_times");
 }
 
+// Host-buffer execution with the copies overlapped with the compute (depth-first plans): the
+// top-level blocks of A and B are copied H2D on a copy stream in order of first use, each
+// top-level product r waits only for the blocks its K1 reads, and every block C_k is copied
+// D2H as soon as its last contribution (the last r with w_kr != 0) has been accumulated.
+static fmm_status execute_host_pipelined(const fmm_plan* p, const void* A_host, int64_t lda,
+                                         const void* B_host, int64_t ldb, void* C_host,
+                                         int64_t ldc, void* A_dev, void* B_dev, void* C_dev,
+                                         void* ws, size_t ws_bytes, cudaStream_t st) {
+  fmm_status fs = ensure_device(p);
+  if (fs != FMM_OK) return fs;
+  size_t need = 0;
+  fmm_plan_workspace_bytes(p, &need);
+  if (ws_bytes < need || !ws) { set_error("fmm_execute_host: workspace too small"); return FMM_E_OOM; }
+  cudaError_t e = cudaSuccess;
+  {
+    std::lock_guard<std::mutex> g(p->dev_mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (p->copy_dev != dev) {
+      if (p->copy_h2d) cudaStreamDestroy(p->copy_h2d);
+      if (p->copy_d2h) cudaStreamDestroy(p->copy_d2h);
+      e = cudaStreamCreateWithFlags(&p->copy_h2d, cudaStreamNonBlocking);
+      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->copy_d2h, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return cuda_status(e, "fmm_execute_host streams");
+      p->copy_dev = dev;
+    }
+  }
+  const RuleData& ru = p->rules[p->node_rule[0][0]];
+  const size_t es = (size_t)elem_size(p->dtype);
+  const int64_t mb = p->lm[1], kb = p->lk[1], nb = p->ln[1];
+  const int nA = ru.m0 * ru.k0, nB = ru.k0 * ru.n0, nC = ru.m0 * ru.n0;
+  std::vector<cudaEvent_t> evs;
+  auto mkev = [&](cudaEvent_t* ev) {
+    cudaError_t r = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (r == cudaSuccess) evs.push_back(*ev);
+    return r;
+  };
+  cudaEvent_t entry;
+  if ((e = mkev(&entry)) != cudaSuccess) return cuda_status(e, "event");
+  cudaEventRecord(entry, st);  // device buffers may still be in use by earlier work on st
+  cudaStreamWaitEvent(p->copy_h2d, entry, 0);
+  cudaStreamWaitEvent(p->copy_d2h, entry, 0);
+  std::vector<cudaEvent_t> evA(nA, nullptr), evB(nB, nullptr);
+  auto copyA = [&](int i) {
+    const int ia = i % ru.m0, ja = i / ru.m0;  // column-major block index
+    cudaMemcpy2DAsync((char*)A_dev + ((ia * mb) * p->K + ja * kb) * es, p->K * es,
+                      (const char*)A_host + ((ia * mb) * lda + ja * kb) * es, lda * es, kb * es, mb,
+                      cudaMemcpyHostToDevice, p->copy_h2d);
+    mkev(&evA[i]);
+    cudaEventRecord(evA[i], p->copy_h2d);
+  };
+  auto copyB = [&](int j) {
+    const int ja = j % ru.k0, jb = j / ru.k0;
+    cudaMemcpy2DAsync((char*)B_dev + ((ja * kb) * p->N + jb * nb) * es, p->N * es,
+                      (const char*)B_host + ((ja * kb) * ldb + jb * nb) * es, ldb * es, nb * es, kb,
+                      cudaMemcpyHostToDevice, p->copy_h2d);
+    mkev(&evB[j]);
+    cudaEventRecord(evB[j], p->copy_h2d);
+  };
+  for (const auto& g : p->groups) {
+    for (int i = 0; i < nA; ++i)
+      if (ru.U[(size_t)i * ru.R + g.r] != 0 && !evA[i]) copyA(i);
+    for (int j = 0; j < nB; ++j)
+      if (ru.V[(size_t)j * ru.R + g.r] != 0 && !evB[j]) copyB(j);
+  }
+  for (int i = 0; i < nA; ++i) if (!evA[i]) copyA(i);
+  for (int j = 0; j < nB; ++j) if (!evB[j]) copyB(j);
+  // last group contributing to each C block
+  std::vector<int> last(nC, -1);
+  for (size_t gi = 0; gi < p->groups.size(); ++gi)
+    for (int k = 0; k < nC; ++k)
+      if (ru.W[(size_t)k * ru.R + p->groups[gi].r] != 0) last[k] = (int)gi;
+  uint8_t* wsb = (uint8_t*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  Bases b{};
+  b.p[BASE_A] = A_dev; b.p[BASE_B] = B_dev; b.p[BASE_C] = C_dev; b.p[BASE_WS] = wsb + p->scale_bytes;
+  b.ld[BASE_A] = p->K; b.ld[BASE_B] = p->N; b.ld[BASE_C] = p->N; b.ld[BASE_WS] = 0;
+  const int vecn = 16 / elem_size(p->dtype);
+  const bool vec = p->dims_vec_ok && aligned16(A_dev) && aligned16(B_dev) && aligned16(C_dev) &&
+                   aligned16(b.p[BASE_WS]) && p->K % vecn == 0 && p->N % vecn == 0;
+  std::vector<bool> copied(nC, false);
+  auto copyC = [&](int k) {
+    cudaEvent_t ev;
+    mkev(&ev);
+    cudaEventRecord(ev, st);
+    cudaStreamWaitEvent(p->copy_d2h, ev, 0);
+    const int ia = k / ru.n0, jb = k % ru.n0;  // row-major block index
+    cudaMemcpy2DAsync((char*)C_host + ((ia * mb) * ldc + jb * nb) * es, ldc * es,
+                      (const char*)C_dev + ((ia * mb) * p->N + jb * nb) * es, p->N * es, nb * es, mb,
+                      cudaMemcpyDeviceToHost, p->copy_d2h);
+    copied[k] = true;
+  };
+  for (size_t gi = 0; gi < p->groups.size(); ++gi) {
+    const auto& g = p->groups[gi];
+    for (int i = 0; i < nA; ++i)
+      if (ru.U[(size_t)i * ru.R + g.r] != 0) cudaStreamWaitEvent(st, evA[i], 0);
+    for (int j = 0; j < nB; ++j)
+      if (ru.V[(size_t)j * ru.R + g.r] != 0) cudaStreamWaitEvent(st, evB[j], 0);
+    fs = p->dtype == FMM_F64 ? run_steps<double>(p, b, vec, st, g.begin, g.end)
+                             : run_steps<float>(p, b, vec, st, g.begin, g.end);
+    if (fs != FMM_OK) return fs;
+    for (int k = 0; k < nC; ++k)
+      if (last[k] == (int)gi) copyC(k);
+  }
+  const size_t tail0 = p->groups.empty() ? 0 : p->groups.back().end;
+  if (tail0 < p->steps.size()) {
+    for (int i = 0; i < nA; ++i) cudaStreamWaitEvent(st, evA[i], 0);
+    for (int j = 0; j < nB; ++j) cudaStreamWaitEvent(st, evB[j], 0);
+    fs = p->dtype == FMM_F64 ? run_steps<double>(p, b, vec, st, tail0) : run_steps<float>(p, b, vec, st, tail0);
+    if (fs != FMM_OK) return fs;
+  }
+  for (int k = 0; k < nC; ++k)
+    if (!copied[k]) copyC(k);
+  cudaEvent_t done;
+  mkev(&done);
+  cudaEventRecord(done, p->copy_d2h);
+  cudaStreamWaitEvent(st, done, 0);  // stream completion => C_host valid
+  e = cudaGetLastError();
+  for (cudaEvent_t ev : evs) cudaEventDestroy(ev);  // deferred until the events complete
+  return cuda_status(e, "fmm_execute_host");
+}
+
 fmm_status fmm_execute_host(const fmm_plan* p, const void* A_host, int64_t lda,
                             const void* B_host, int64_t ldb, void* C_host, int64_t ldc,
                             void* A_dev, void* B_dev, void* C_dev, void* ws, size_t ws_bytes,
@@ -824,6 +969,10 @@ fmm_status fmm_execute_host(const fmm_plan* p, const void* A_host, int64_t lda,
   }
   if (lda < p->K || ldb < p->N || ldc < p->N) { set_error("fmm_execute_host: bad ld"); return FMM_E_ARG; }
   cudaStream_t st = (cudaStream_t)stream;
+  if (!p->groups.empty() && p->scaling.mode == FMM_SCALE_NONE && !(p->comm && p->nranks > 1) &&
+      p->M > 0 && p->N > 0 && p->K > 0)
+    return execute_host_pipelined(p, A_host, lda, B_host, ldb, C_host, ldc, A_dev, B_dev, C_dev,
+                                  ws, ws_bytes, st);
   const size_t es = (size_t)elem_size(p->dtype);
   cudaError_t e = cudaMemcpy2DAsync(A_dev, p->K * es, A_host, lda * es, p->K * es, p->M, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess)

@@ -41,6 +41,7 @@ SIGNATURES = {
     "fmm_plan_create": (_I, [C.POINTER(_P), _I, _I, _I, _I64, _I64, _I64, _I, _I, C.POINTER(fmm_scaling), C.POINTER(_P)]),
     "fmm_plan_destroy": (None, [_P]),
     "fmm_plan_set_partition": (_I, [_P, _I, _I]),
+    "fmm_plan_set_schedule": (_I, [_P, _I]),
     "fmm_plan_owned": (_I, [_P, _I, _I, _P, C.POINTER(_I)]),
     "fmm_plan_workspace_bytes": (_I, [_P, C.POINTER(_SZ)]),
     "fmm_plan_launch_count": (_I, [_P, C.POINTER(_I64)]),
@@ -234,6 +235,11 @@ class Plan:
 
     def set_partition(self, rank: int, nranks: int):
         _call("fmm_plan_set_partition", self._h, rank, nranks)
+        self._ws = None
+
+    def set_schedule(self, schedule: str):
+        """'auto' | 'breadth' | 'depth' (top-level depth-first)."""
+        _call("fmm_plan_set_schedule", self._h, {"auto": 0, "breadth": 1, "depth": 2}[schedule])
         self._ws = None
 
     def owned(self, rank: int, nranks: int):

@@ -244,6 +244,9 @@ def test_split_schedule_matches_breadth_first(fb):
     A, B = fi.random_pair(256, 256, 256, seed=8)
     p = gpu_plan(fb, ("winograd",) * 3, 256, 256, 256)
     bf = p.execute(dev(A), dev(B)).cpu().numpy()
+    p.set_schedule("depth")
+    assert np.array_equal(p.execute(dev(A), dev(B)).cpu().numpy(), bf)
+    p.set_schedule("auto")
     parts = []
     for rank in range(3):
         p.set_partition(rank, 3)
@@ -268,3 +271,28 @@ def test_empty_and_degenerate(fb):
     # identity exact
     I = np.eye(64)
     assert np.array_equal(run(fb, ("strassen",) * 3, I, I), I)
+
+
+@pytest.mark.parametrize("schedule", ["breadth", "depth"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_execute_host_overlapped(fb, schedule, dtype):
+    # fmm_execute_host (pinned host buffers; the depth-first schedule overlaps block copies with
+    # the compute) returns exactly what fmm_execute returns on device buffers.
+    npdt = np.float64 if dtype == "f64" else np.float32
+    A, B = fi.random_pair(256, 512, 384, seed=31, dtype=npdt)
+    w = fb.Rule.builtin("winograd")
+    leaf = fb.fmm.LEAF_NATIVE if dtype == "f64" else fb.fmm.LEAF_3XTF32
+    p = fb.Plan([w, w], 256, 512, 384, dtype=dtype, leaf=leaf)
+    p.set_schedule(schedule)
+    Cd = p.execute(dev(A), dev(B)).cpu().numpy()
+    Ah = torch.from_numpy(A).pin_memory()
+    Bh = torch.from_numpy(B).pin_memory()
+    Ch = torch.full((256, 384), float("nan"), dtype=Ah.dtype).pin_memory()
+    Ad, Bd = torch.empty_like(Ah, device="cuda"), torch.empty_like(Bh, device="cuda")
+    Cdd = torch.empty((256, 384), dtype=Ah.dtype, device="cuda")
+    for _ in range(2):  # twice: buffers reused across calls
+        p.execute_host(Ah, Bh, Ch, Ad, Bd, Cdd)
+        torch.cuda.synchronize()
+        assert np.array_equal(Ch.numpy(), Cd)
+    Co = oracle.fmm(A, B, OPlan.stationary(R.winograd(), 2))
+    assert parity(Ch.numpy(), Co, A, B) <= (TOL64 if dtype == "f64" else TOL32)
