@@ -118,14 +118,21 @@ def load_traffic(workload: str):
         return None
 
 
-def make_inputs(M, K, N, seed, dtype):
-    """C5 inputs drawn by the shared recipe (fmm_inputs) straight into pinned host memory."""
+def make_inputs(cfg, dtype):
+    """Inputs of BASELINE config `cfg` drawn by the shared recipe (fmm_inputs) into pinned host
+    memory (uniform families straight into pinned buffers)."""
+    import torch
     import fmm_inputs as fi
+    c = fi.CONFIGS[cfg]
     t0 = time.time()
-    A, B = fi.draw_torch("u(-1,1)", M, K, N, seed, pin=True)
+    if c.dist in ("u(-1,1)", "u(0,1)"):
+        A, B = fi.draw_torch(c.dist, c.M, c.K, c.N, c.seed, pin=True)
+    else:
+        A, B = fi.draw_torch(c.dist, c.M, c.K, c.N, c.seed)
+        A, B = A.pin_memory(), B.pin_memory()
     if dtype == "f32":
         A, B = A.float().pin_memory(), B.float().pin_memory()
-    log(f"[bench] inputs {M}x{K}x{N} generated in {time.time() - t0:.1f}s")
+    log(f"[bench] {cfg} inputs {c.M}x{c.K}x{c.N} ({c.dist}, seed {c.seed}) in {time.time() - t0:.1f}s")
     return A, B
 
 
@@ -179,35 +186,40 @@ def run_reference(args):
     import numpy as np
     import oracle
     from oracle import rules as OR
-    M = K = N = 32768
-    rules = ("winograd",) * 3
+    import fmm_inputs as fi
+    c = fi.CONFIGS[args.config]
+    M, K, N = c.M, c.K, c.N
+    rules = c.rules
     oracle.build()
-    A, B = make_inputs(M, K, N, 4, "f64")
+    A, B = make_inputs(args.config, "f64")
     An, Bn = A.numpy(), B.numpy()
     plan = OR.Plan.uniform([OR.builtin(n) for n in rules])
     nr = args.ref_sample
     times = []
     for step in range(args.warmup + args.steps):
-        rows = [(step * nr + i) % (M // 8) for i in range(nr)]
+        pm, _, pn = plan.dims_divisor()
+        rows = [(step * nr + i) % (M // pm) for i in range(nr)]
+        cols = [(step * nr + i) % (N // pn) for i in range(nr)]
         G = oracle.lift_rows(M, plan, rows)
-        H = oracle.lift_cols(N, plan, rows)
+        H = oracle.lift_cols(N, plan, cols)
         t0 = time.perf_counter()
         oracle.fmm(np.ascontiguousarray(An[G, :]), np.ascontiguousarray(Bn[:, H]), plan)
         t = time.perf_counter() - t0
         if step >= args.warmup:
             times.append(t)
-    flops = 2.0 * (8 * nr) * (8 * nr) * K
+    flops = 2.0 * len(G) * len(H) * K
     total = sum(times)
     value = flops * len(times) / total / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
             "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total / len(times) * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C5: S-W <2,2,2;7> L=3, M=K=N=32768 FP64, U(-1,1) seed 4",
-                       "sample_per_step": f"C[G,H], |G| = |H| = {8 * nr} lifted rows/cols"},
+            "config": {"workload": f"{args.config}: {' / '.join(rules)}, M={M} K={K} N={N} FP64, "
+                                   f"{c.dist} seed {c.seed}",
+                       "sample_per_step": f"C[G,H], |G| = {len(G)}, |H| = {len(H)} lifted rows/cols"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.num_threads(),
                              "kind": "oracle",
-                             "sample": f"per step C[G,H] with |G|=|H|={8 * nr} (row/col-sampled oracle)"},
+                             "sample": f"per step C[G,H] with |G|={len(G)}, |H|={len(H)} (row/col-sampled oracle)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -224,8 +236,10 @@ def run_fmm(args):
     torch.cuda.set_device(local)
     if ws > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    M = K = N = args.n
-    rules = ("winograd",) * args.levels
+    import fmm_inputs as fi
+    cfgd = fi.CONFIGS[args.config]
+    M, K, N = cfgd.M, cfgd.K, cfgd.N
+    rules = cfgd.rules
     dt = torch.float64 if args.dtype == "f64" else torch.float32
     esz = 8 if args.dtype == "f64" else 4
     leaf = fb.fmm.LEAF_NATIVE if args.dtype == "f64" else args.leaf
@@ -233,7 +247,7 @@ def run_fmm(args):
 
     # ---- inputs: host (pinned) on rank 0, device copies on every rank -----------------------
     if rank == 0:
-        A_h, B_h = make_inputs(M, K, N, 4, args.dtype)
+        A_h, B_h = make_inputs(args.config, args.dtype)
     A = torch.empty((M, K), dtype=dt, device="cuda")
     B = torch.empty((K, N), dtype=dt, device="cuda")
     Cd = torch.empty((M, N), dtype=dt, device="cuda")
@@ -245,12 +259,19 @@ def run_fmm(args):
         dist.broadcast(B, 0)
     torch.cuda.synchronize()
 
-    plan = fb.Plan([fb.Rule.builtin(r) for r in rules], M, K, N, dtype=args.dtype, leaf=leaf)
+    scaling = None
+    if args.scaling != "none":
+        scaling = {"mode": args.scaling, "tau": 1.0, "max_steps": 20, "pow2": 1}
+    plan = fb.Plan([fb.Rule.builtin(r) for r in rules], M, K, N, dtype=args.dtype, leaf=leaf,
+                   scaling=scaling)
     if ws > 1:
         uid = [fb.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, 0)
         plan.set_comm(uid[0], rank, ws)
     wsp = plan.workspace(A.device)
+    use_graph = args.graph == "on" or (args.graph == "auto" and M * N * K <= 4096 ** 3 and ws == 1)
+    if use_graph:
+        plan.set_graph(True)
     log(f"[bench] rank {rank}: workspace {plan.workspace_bytes() / 2**30:.1f} GiB, "
         f"{plan.launch_count()} launches / step")
 
@@ -265,22 +286,37 @@ def run_fmm(args):
 
     # ---- timed region (device events, max over ranks) -----------------------------------------
     sampler = ClockSampler(local)
-    plan.set_timing(True)
+    plan.set_timing(not use_graph)
     plan.step_times()  # reset
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    small = (M * K + K * N + M * N) * esz < (512 << 20)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if small else None
     sampler.start()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step()
-    e1.record(stream)
-    torch.cuda.synchronize()
+    if not small:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+    else:  # operands fit in L2: flush L2 (256 MB write) between steps, outside the events
+        evs = []
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+            a, b2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step()
+            b2.record(stream)
+            evs.append((a, b2))
+        torch.cuda.synchronize()
+        ms = sum(a.elapsed_time(b2) for a, b2 in evs)
     if ws > 1:
         dist.barrier()
     clocks = sampler.stop()
-    ms = e0.elapsed_time(e1)
     kinds = plan.step_times()
     plan.set_timing(False)
     if ws > 1:
@@ -291,14 +327,28 @@ def run_fmm(args):
     value = flops * args.steps / (ms * 1e-3) / 1e9
 
     # ---- roofline of the dominant kernel (K2, the leaf products) -------------------------------
-    L = args.levels
-    leaf_flops_step = (7 ** L) * 2.0 * (M >> L) * (N >> L) * (K >> L)
+    L = len(rules)
+    nleaves = 1
+    for r in rules:
+        nleaves *= fb.Rule.builtin(r).info()["R"]
+    leaf_flops_step = nleaves * 2.0 * (M >> L) * (N >> L) * (K >> L)
+    if use_graph:  # per-kind events are not recorded under graph replay: time K2 alone after
+        plan.set_graph(False)
+        plan.set_timing(True)
+        plan.step_times()
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                step()
+        torch.cuda.synchronize()
+        kinds = plan.step_times()
+        plan.set_timing(False)
     k2_ms, k2_n = kinds.get("K2", (0.0, 0))
     per_launch_flops = leaf_flops_step * args.steps / max(k2_n, 1)
     peak = FP64_DMMA_PEAK_TFLOPS if args.dtype == "f64" else TF32_PEAK_TFLOPS_NOMINAL / (
         3 if leaf == fb.fmm.LEAF_3XTF32 else 1)
     achieved = per_launch_flops / (k2_ms / max(k2_n, 1) * 1e-3) / 1e12 if k2_n else None
-    workload = f"C5-{args.dtype}-n{M}-L{L}-p{ws}"
+    workload = f"{args.config}-{args.dtype}-n{M}-L{L}-p{ws}" if args.config == "C5" else \
+        f"{args.config}-{args.dtype}-p{ws}"
     roofline = {"kernel": "k2_gemm_f64 (leaf products, DMMA mma.sync f64)" if args.dtype == "f64"
                 else "k2 (leaf products, FP32)",
                 "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -308,7 +358,10 @@ def run_fmm(args):
                                "MEASURED_PEAKS.json has no FP64 entry" if args.dtype == "f64" else
                                "B200_PROFILING.md nominal dense TF32 (fallback)",
                 "flops_per_launch": per_launch_flops, "launch_ms": (k2_ms / k2_n) if k2_n else None,
-                "step_share": {k: v[0] / ms for k, v in kinds.items()}}
+                "step_share": {k: v[0] / max(sum(x[0] for x in kinds.values()), 1e-9)
+                               for k, v in kinds.items()},
+                "timing_note": "K2 launch times from CUDA events the library records on the launch "
+                               "stream" + (" (separate pass: graph replay in the timed region)" if use_graph else "")}
 
     # ---- end-to-end through the C ABI with host buffers ---------------------------------------
     e2e = None
@@ -354,21 +407,26 @@ def run_fmm(args):
         Bn = B_h.numpy() if args.dtype == "f64" else B_h.double().numpy()
         if args.dtype == "f32":
             An, Bn = A_h.numpy(), B_h.numpy()
-        cpu = cpu_baseline(An, Bn, rules, M, K, N, C_gpu_host=Cg, target_s=args.cpu_seconds)
+        cpu = cpu_baseline(An, Bn, rules, M, K, N, C_gpu_host=Cg if args.scaling == "none" else None,
+                           target_s=args.cpu_seconds)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": f"C5: Strassen-Winograd <2,2,2;7> L={L}, M=K=N={M} "
-                                   f"{args.dtype.upper()}, A,B ~ U(-1,1) seed 4 (BASELINE configs[4])",
+            "config": {"workload": f"{args.config}: {' / '.join(rules)} (root first), M={M} K={K} "
+                                   f"N={N} {args.dtype.upper()}, {cfgd.dist} seed {cfgd.seed} "
+                                   f"(BASELINE configs[{list(fi.CONFIGS).index(args.config) if args.config != 'C2c' else 1}])"
+                                   + (f", scaling {args.scaling} (pow2, tau=1)" if args.scaling != "none" else ""),
                        "parallelism": f"top-level r round-robin over {ws} GPU(s)"
                                       + (", ncclReduce of C" if ws > 1 else ""),
-                       "l2": "operands 8 GiB each >> 126 MB L2 (no flush needed)",
+                       "l2": ("operands %.1f GiB each > 126 MB L2 (no flush needed)" % (M * K * esz / 2**30))
+                  if not small else "L2 flushed (256 MB write) between timed steps, outside the events",
                        "leaf": {0: "native", 1: "tf32", 2: "3xtf32"}[leaf]},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": plan.launch_count() * args.steps,
+            "cuda_graph": use_graph,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -383,8 +441,12 @@ def main():
     ap.add_argument("--impl", default="fmm", choices=["fmm", "reference"])
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--leaf", type=int, default=2, help="FP32 leaf: 0 native, 1 tf32, 2 3xtf32")
-    ap.add_argument("--n", type=int, default=32768)
-    ap.add_argument("--levels", type=int, default=3)
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C2c", "C3", "C4", "C5"],
+                    help="BASELINE config (default C5: the throughput config the metric is quoted on)")
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="CUDA-graph replay of each step (auto: on for problems <= 4096^3)")
+    ap.add_argument("--scaling", default="none",
+                    choices=["none", "outside", "inside", "out_in", "in_out", "repeated"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-warmup", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -151,6 +151,12 @@ fmm_status fmm_plan_launch_count(const fmm_plan* plan, int64_t* launches);
 fmm_status fmm_plan_set_timing(fmm_plan* plan, int enable);
 fmm_status fmm_plan_step_times(fmm_plan* plan, double* ms, int64_t* launches);
 
+/* CUDA-graph replay (enable = 1): fmm_execute captures its launch sequence into a CUDA graph
+ * the first time it sees a given (A, B, C, ws, lda, ldb, ldc) and replays the graph on later
+ * calls with the same arguments -- for small, launch-bound problems.  Ignored while timing is
+ * enabled or a communicator is attached. */
+fmm_status fmm_plan_set_graph(fmm_plan* plan, int enable);
+
 /* C = A.B by the plan (dev pointers).  A: M x K (lda), B: K x N (ldb), C: M x N (ldc),
  * overwritten.  ws: dev workspace of >= fmm_plan_workspace_bytes.  Requirements: A, B, C, ws
  * 16-byte aligned for the vectorised paths (otherwise a scalar path is used).  With a

@@ -127,6 +127,15 @@ struct fmm_plan {
   std::vector<RGroup> groups;
   mutable cudaStream_t copy_h2d = nullptr, copy_d2h = nullptr;
   mutable int copy_dev = -1;
+  // optional CUDA-graph replay of fmm_execute
+  bool use_graph = false;
+  struct GraphEntry {
+    const void *A, *B, *C, *ws;
+    int64_t lda, ldb, ldc;
+    cudaGraphExec_t exec;
+  };
+  mutable std::vector<GraphEntry> graphs;
+  mutable std::mutex gmu;
   // optional per-step timing (events recorded on the launch stream)
   bool timing = false;
   mutable std::mutex tmu;
@@ -136,6 +145,7 @@ struct fmm_plan {
 };
 
 fmm_plan::~fmm_plan() {
+  for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
   if (copy_h2d) cudaStreamDestroy(copy_h2d);
   if (copy_d2h) cudaStreamDestroy(copy_d2h);
   for (auto& u : ev_used) { cudaEventDestroy(u.second.first); cudaEventDestroy(u.second.second); }
@@ -364,6 +374,11 @@ struct Builder {
 void scaling_steps(const fmm_scaling& sc, std::string* steps, double* tau);
 
 fmm_status compile_plan(fmm_plan* p) {
+  {
+    std::lock_guard<std::mutex> g(p->gmu);
+    for (auto& ge : p->graphs) cudaGraphExecDestroy(ge.exec);
+    p->graphs.clear();
+  }
   p->steps.clear();
   p->groups.clear();
   {
@@ -743,8 +758,59 @@ fmm_status fmm_plan_launch_count(const fmm_plan* p, int64_t* launches) {
   return FMM_OK;
 }
 
+static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, const void* B,
+                               int64_t ldb, void* C, int64_t ldc, void* ws, size_t ws_bytes,
+                               void* stream);
+
+fmm_status fmm_plan_set_graph(fmm_plan* p, int enable) {
+  if (!p) { set_error("fmm_plan_set_graph: null"); return FMM_E_ARG; }
+  p->use_graph = enable != 0;
+  return FMM_OK;
+}
+
 fmm_status fmm_execute(const fmm_plan* p, const void* A, int64_t lda, const void* B, int64_t ldb,
                        void* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream) {
+  if (!p || !p->use_graph || p->timing || (p->comm && p->nranks > 1))
+    return execute_impl(p, A, lda, B, ldb, C, ldc, ws, ws_bytes, stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  {
+    std::lock_guard<std::mutex> g(p->gmu);
+    for (const auto& ge : p->graphs)
+      if (ge.A == A && ge.B == B && ge.C == C && ge.ws == ws && ge.lda == lda && ge.ldb == ldb && ge.ldc == ldc)
+        return cuda_status(cudaGraphLaunch(ge.exec, st), "fmm_execute graph launch");
+  }
+  {
+    fmm_status es = ensure_device(p);  // uploads are not capturable
+    if (es != FMM_OK) return es;
+  }
+  cudaStream_t cap = st;
+  bool own = false;
+  if (cap == nullptr) {  // the legacy stream cannot be captured: capture on a private stream
+    if (cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking) != cudaSuccess) return FMM_E_CUDA;
+    own = true;
+  }
+  cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) { if (own) cudaStreamDestroy(cap); return cuda_status(e, "graph capture"); }
+  fmm_status s = execute_impl(p, A, lda, B, ldb, C, ldc, ws, ws_bytes, cap);
+  cudaGraph_t graph = nullptr;
+  e = cudaStreamEndCapture(cap, &graph);
+  if (own) cudaStreamDestroy(cap);
+  if (s != FMM_OK) { if (graph) cudaGraphDestroy(graph); return s; }
+  if (e != cudaSuccess) return cuda_status(e, "graph capture end");
+  cudaGraphExec_t exec = nullptr;
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return cuda_status(e, "graph instantiate");
+  {
+    std::lock_guard<std::mutex> g(p->gmu);
+    p->graphs.push_back({A, B, C, ws, lda, ldb, ldc, exec});
+  }
+  return cuda_status(cudaGraphLaunch(exec, st), "fmm_execute graph launch");
+}
+
+static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, const void* B,
+                               int64_t ldb, void* C, int64_t ldc, void* ws, size_t ws_bytes,
+                               void* stream) {
   if (!p) { set_error("fmm_execute: null plan"); return FMM_E_ARG; }
   const bool empty = p->M == 0 || p->N == 0;
   if (!empty && (!A && p->K > 0)) { set_error("fmm_execute: null A"); return FMM_E_ARG; }

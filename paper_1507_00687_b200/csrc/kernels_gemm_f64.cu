@@ -51,9 +51,14 @@ __device__ __forceinline__ void dmma16n8k4(double (&c)[4], double a0, double a1,
       : "d"(a0), "d"(a1), "d"(b0));
 }
 
-template <int BM_, int BN_, int BK_, int STAGES_, int WARPS_M_, int WARPS_N_, int MINB_ = 1>
+template <int BM_, int BN_, int BK_, int STAGES_, int WARPS_M_, int WARPS_N_, int MINB_ = 1,
+          bool PIPE_ = false>
 struct Cfg {
   static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_, MINB = MINB_;
+  // PIPE: fragments of the next k-slice (and of the next stage) are loaded into a second
+  // register set while the current slice's DMMAs issue; the stage barrier sits before the last
+  // slice of each stage instead of in front of the first.
+  static constexpr bool PIPE = PIPE_;
   static constexpr int WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
   static constexpr int THREADS = WARPS_M * WARPS_N * 32;
   static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
@@ -156,35 +161,86 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     cp_commit();
   }
 
-  for (int kt = 0; kt < KT; ++kt) {
+  if constexpr (!C::PIPE) {
+    for (int kt = 0; kt < KT; ++kt) {
+      cp_wait<C::STAGES - 2>();
+      __syncthreads();
+      {
+        int nk = kt + C::STAGES - 1;
+        if (nk < KT) {
+          int slot = nk % C::STAGES;
+          load_tiles<C, VEC>(As + slot * C::A_STAGE, Bs + slot * C::B_STAGE, A, lda, B, ldb, m, n, k,
+                             m0, n0, (int64_t)nk * C::BK, tid);
+        }
+        cp_commit();
+      }
+      const int slot = kt % C::STAGES;
+      const double* as = As + slot * C::A_STAGE + (wm * C::WTM + g) * C::A_LD + t;
+      const double* bs = Bs + slot * C::B_STAGE + t * C::B_LD + wn * C::WTN + g;
+  #pragma unroll
+      for (int kk = 0; kk < C::BK; kk += 4) {
+        double af[C::MI][2], bf[C::NI];
+  #pragma unroll
+        for (int i = 0; i < C::MI; ++i) {
+          af[i][0] = as[(i * 16) * C::A_LD + kk];
+          af[i][1] = as[(i * 16 + 8) * C::A_LD + kk];
+        }
+  #pragma unroll
+        for (int j = 0; j < C::NI; ++j) bf[j] = bs[kk * C::B_LD + j * 8];
+  #pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+  #pragma unroll
+          for (int j = 0; j < C::NI; ++j) dmma16n8k4(acc[i][j], af[i][0], af[i][1], bf[j]);
+      }
+    }
+  } else {
+    constexpr int KQ = C::BK / 4;
+    static_assert(KQ % 2 == 0, "even number of k-slices per stage");
+    double af[2][C::MI][2], bf[2][C::NI];
+    const int a_off = (wm * C::WTM + g) * C::A_LD + t, b_off = t * C::B_LD + wn * C::WTN + g;
+    auto load_frag = [&](int buf, int slot, int kk) {
+      const double* as = As + slot * C::A_STAGE + a_off;
+      const double* bs = Bs + slot * C::B_STAGE + b_off;
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i) {
+        af[buf][i][0] = as[(i * 16) * C::A_LD + kk];
+        af[buf][i][1] = as[(i * 16 + 8) * C::A_LD + kk];
+      }
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j) bf[buf][j] = bs[kk * C::B_LD + j * 8];
+    };
     cp_wait<C::STAGES - 2>();
     __syncthreads();
     {
-      int nk = kt + C::STAGES - 1;
-      if (nk < KT) {
-        int slot = nk % C::STAGES;
-        load_tiles<C, VEC>(As + slot * C::A_STAGE, Bs + slot * C::B_STAGE, A, lda, B, ldb, m, n, k,
-                           m0, n0, (int64_t)nk * C::BK, tid);
-      }
+      const int nk = C::STAGES - 1;
+      if (nk < KT)
+        load_tiles<C, VEC>(As + (nk % C::STAGES) * C::A_STAGE, Bs + (nk % C::STAGES) * C::B_STAGE,
+                           A, lda, B, ldb, m, n, k, m0, n0, (int64_t)nk * C::BK, tid);
       cp_commit();
     }
-    const int slot = kt % C::STAGES;
-    const double* as = As + slot * C::A_STAGE + (wm * C::WTM + g) * C::A_LD + t;
-    const double* bs = Bs + slot * C::B_STAGE + t * C::B_LD + wn * C::WTN + g;
+    if (KT > 0) load_frag(0, 0, 0);
+    for (int kt = 0; kt < KT; ++kt) {
+      const int slot = kt % C::STAGES;
 #pragma unroll
-    for (int kk = 0; kk < C::BK; kk += 4) {
-      double af[C::MI][2], bf[C::NI];
+      for (int q = 0; q < KQ; ++q) {
+        const int cur = q & 1;
+        if (q == KQ - 1) {
+          cp_wait<C::STAGES - 2>();
+          __syncthreads();  // every warp is done reading `slot` (its last slice is in registers)
+          const int nk = kt + C::STAGES;
+          if (nk < KT)
+            load_tiles<C, VEC>(As + (nk % C::STAGES) * C::A_STAGE, Bs + (nk % C::STAGES) * C::B_STAGE,
+                               A, lda, B, ldb, m, n, k, m0, n0, (int64_t)nk * C::BK, tid);
+          cp_commit();
+          if (kt + 1 < KT) load_frag(cur ^ 1, (kt + 1) % C::STAGES, 0);
+        } else {
+          load_frag(cur ^ 1, slot, (q + 1) * 4);
+        }
 #pragma unroll
-      for (int i = 0; i < C::MI; ++i) {
-        af[i][0] = as[(i * 16) * C::A_LD + kk];
-        af[i][1] = as[(i * 16 + 8) * C::A_LD + kk];
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j) dmma16n8k4(acc[i][j], af[cur][i][0], af[cur][i][1], bf[cur][j]);
       }
-#pragma unroll
-      for (int j = 0; j < C::NI; ++j) bf[j] = bs[kk * C::B_LD + j * 8];
-#pragma unroll
-      for (int i = 0; i < C::MI; ++i)
-#pragma unroll
-        for (int j = 0; j < C::NI; ++j) dmma16n8k4(acc[i][j], af[i][0], af[i][1], bf[j]);
     }
   }
   cp_wait<0>();
@@ -248,11 +304,18 @@ using V9 = Cfg<64, 64, 16, 4, 2, 2, 3>;   // 4 warps, 3 CTAs / SM
 using V10 = Cfg<64, 256, 16, 3, 2, 8, 1>; // 16 warps, 32 x 32 warp tiles
 using V11 = Cfg<64, 64, 16, 3, 2, 2, 4>;  // 4 warps, 4 CTAs / SM
 using V12 = Cfg<64, 64, 32, 2, 2, 2, 3>;
+using V13 = Cfg<64, 64, 16, 4, 2, 2, 3, true>;  // v9 + cross-stage fragment prefetch
+using V14 = Cfg<64, 64, 32, 2, 2, 2, 3, true>;
+using V15 = Cfg<64, 128, 16, 4, 2, 4, 2, true>;
+using V16 = Cfg<128, 128, 16, 4, 2, 4, 1, true>;
+using V17 = Cfg<128, 128, 32, 3, 2, 4, 1, true>;
+using V18 = Cfg<128, 128, 16, 3, 2, 4, 1, true>;
+using V20 = Cfg<128, 128, 16, 5, 2, 4, 1, true>;
 
 int variant() {
   static int v = [] {
     const char* e = getenv("FMM_K2_VARIANT");
-    return e ? atoi(e) : 9;
+    return e ? atoi(e) : 16;
   }();
   return v;
 }
@@ -274,8 +337,15 @@ cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, in
     case 10: return launch_cfg<V10>(dev_leaves, count, m, n, k, b, vec, st);
     case 11: return launch_cfg<V11>(dev_leaves, count, m, n, k, b, vec, st);
     case 12: return launch_cfg<V12>(dev_leaves, count, m, n, k, b, vec, st);
+    case 13: return launch_cfg<V13>(dev_leaves, count, m, n, k, b, vec, st);
+    case 14: return launch_cfg<V14>(dev_leaves, count, m, n, k, b, vec, st);
+    case 15: return launch_cfg<V15>(dev_leaves, count, m, n, k, b, vec, st);
+    case 16: return launch_cfg<V16>(dev_leaves, count, m, n, k, b, vec, st);
+    case 17: return launch_cfg<V17>(dev_leaves, count, m, n, k, b, vec, st);
+    case 18: return launch_cfg<V18>(dev_leaves, count, m, n, k, b, vec, st);
+    case 20: return launch_cfg<V20>(dev_leaves, count, m, n, k, b, vec, st);
     case 1: return launch_cfg<V1>(dev_leaves, count, m, n, k, b, vec, st);
-    default: return launch_cfg<V9>(dev_leaves, count, m, n, k, b, vec, st);
+    default: return launch_cfg<V16>(dev_leaves, count, m, n, k, b, vec, st);
   }
 }
 

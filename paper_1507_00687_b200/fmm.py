@@ -46,6 +46,7 @@ SIGNATURES = {
     "fmm_plan_workspace_bytes": (_I, [_P, C.POINTER(_SZ)]),
     "fmm_plan_launch_count": (_I, [_P, C.POINTER(_I64)]),
     "fmm_plan_set_timing": (_I, [_P, _I]),
+    "fmm_plan_set_graph": (_I, [_P, _I]),
     "fmm_plan_step_times": (_I, [_P, _P, _P]),
     "fmm_execute": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _SZ, _P]),
     "fmm_execute_host": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _SZ, _P]),
@@ -221,6 +222,10 @@ class Plan:
         return n.value
 
     STEP_KINDS = {1: "K1", 2: "K2", 3: "K3", 4: "ACC", 5: "ZERO", 6: "SCALE", 7: "REDUCE"}
+
+    def set_graph(self, enable: bool = True):
+        """Replay fmm_execute as a CUDA graph for repeated calls with the same buffers."""
+        _call("fmm_plan_set_graph", self._h, int(enable))
 
     def set_timing(self, enable: bool = True):
         _call("fmm_plan_set_timing", self._h, int(enable))

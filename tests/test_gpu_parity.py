@@ -296,3 +296,22 @@ def test_execute_host_overlapped(fb, schedule, dtype):
         assert np.array_equal(Ch.numpy(), Cd)
     Co = oracle.fmm(A, B, OPlan.stationary(R.winograd(), 2))
     assert parity(Ch.numpy(), Co, A, B) <= (TOL64 if dtype == "f64" else TOL32)
+
+
+def test_cuda_graph_replay(fb):
+    A, B = fi.random_pair(512, 512, 512, seed=40)
+    w = fb.Rule.builtin("winograd")
+    p = fb.Plan([w, w], 512, 512, 512)
+    ref = p.execute(dev(A), dev(B)).cpu().numpy()
+    p.set_graph(True)
+    Ad, Bd = dev(A), dev(B)
+    C1 = torch.empty((512, 512), dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        C1.zero_()
+        p.execute(Ad, Bd, C1)
+        torch.cuda.synchronize()
+        assert np.array_equal(C1.cpu().numpy(), ref)
+    C2 = torch.empty_like(C1)  # new buffers -> a second captured graph
+    p.execute(Ad, Bd, C2)
+    torch.cuda.synchronize()
+    assert np.array_equal(C2.cpu().numpy(), ref)
