@@ -71,13 +71,22 @@ constexpr int kRowsPerBlock = 4;
 // grid: x = column chunks of kThreads vectors, y = row groups of kRowsPerBlock, z = node.
 // NBLK: compile-time bound on the number of input sub-blocks (4 for 2x2 rules) so that the
 // per-thread input registers stay small; two rows are loaded before either is combined, so
-// each thread keeps up to 2*NBLK 16-byte loads in flight.
+// each thread keeps up to 2*NBLK 16-byte loads in flight.  Per block, thread 0 compiles the
+// node's outputs into shared memory once: the list of r to write, their base pointers, and per
+// r a 2-bit code per input block (0: absent, 1: +1, 2: -1, 3: general coefficient); the inner
+// loop then needs one broadcast shared load per output.  u*x with u = +-1 is exact, so adding
+// +-x is bitwise the oracle's  s + u*x.
 template <typename T, int VEC, int NBLK>
 __global__ void __launch_bounds__(kThreads) k1_lincomb(const K1Node* __restrict__ nodes,
                                                        const double* __restrict__ coef_all,
                                                        Bases bases, int64_t rows, int64_t cols,
                                                        int P, int Q, int R) {
   __shared__ double cf[kMaxBlk * kMaxR];
+  __shared__ T* optr[kMaxR];
+  __shared__ int64_t old[kMaxR];
+  __shared__ uint32_t code[kMaxR];
+  __shared__ int rlist[kMaxR];
+  __shared__ int nr_s;
   __shared__ uint32_t need_s;
   const K1Node& nd = nodes[blockIdx.z];
   const int nblk = P * Q;
@@ -86,13 +95,29 @@ __global__ void __launch_bounds__(kThreads) k1_lincomb(const K1Node* __restrict_
   __syncthreads();
   if (threadIdx.x == 0) {
     uint32_t need = 0;
-    for (int b = 0; b < nblk; ++b)
-      for (int r = 0; r < R; ++r)
-        if (((omask >> r) & 1u) && cf[b * R + r] != 0.0) need |= 1u << b;
+    int nr = 0;
+    for (int r = 0; r < R; ++r) {
+      if (!((omask >> r) & 1u)) continue;
+      uint32_t c = 0;
+      for (int b = 0; b < nblk; ++b) {
+        const double u = cf[b * R + r];
+        if (u == 0.0) continue;
+        need |= 1u << b;
+        c |= (u == 1.0 ? 1u : u == -1.0 ? 2u : 3u) << (2 * b);
+      }
+      int64_t ldo;
+      optr[nr] = op_ptr<T>(bases, nd.out[r], ldo);
+      old[nr] = ldo;
+      code[nr] = c;
+      rlist[nr] = r;
+      ++nr;
+    }
+    nr_s = nr;
     need_s = need;
   }
   __syncthreads();
   const uint32_t need = need_s;
+  const int nr = nr_s;
 
   int64_t ldi;
   const T* in = op_ptr<const T>(bases, nd.in, ldi);
@@ -116,28 +141,33 @@ __global__ void __launch_bounds__(kThreads) k1_lincomb(const K1Node* __restrict_
     for (int h = 0; h < 2; ++h) {
       const int64_t i = i0 + ii + h;
       if (i >= rows) break;
-      for (int r = 0; r < R; ++r) {
-        if (!((omask >> r) & 1u)) continue;
+      for (int o = 0; o < nr; ++o) {
+        const uint32_t c = code[o];
         Vec<T, VEC> acc;
         bool started = false;
 #pragma unroll
         for (int b = 0; b < NBLK; ++b) {
-          if (b >= nblk) break;
-          const double u = cf[b * R + r];
-          if (u == 0.0) continue;
-          const T ut = (T)u;
+          const uint32_t cb = (c >> (2 * b)) & 3u;
+          if (cb == 0u) continue;
+          if (cb == 3u) {  // general dyadic coefficient: s + u*x
+            const T ut = (T)cf[b * R + rlist[o]];
 #pragma unroll
-          for (int e = 0; e < VEC; ++e)
-            acc.v[e] = started ? add_rn<T>(acc.v[e], mul_rn<T>(ut, x[h][b].v[e])) : mul_rn<T>(ut, x[h][b].v[e]);
+            for (int e = 0; e < VEC; ++e)
+              acc.v[e] = started ? add_rn<T>(acc.v[e], mul_rn<T>(ut, x[h][b].v[e])) : mul_rn<T>(ut, x[h][b].v[e]);
+          } else if (cb == 1u) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) acc.v[e] = started ? add_rn<T>(acc.v[e], x[h][b].v[e]) : x[h][b].v[e];
+          } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) acc.v[e] = started ? add_rn<T>(acc.v[e], -x[h][b].v[e]) : -x[h][b].v[e];
+          }
           started = true;
         }
         if (!started) {
 #pragma unroll
           for (int e = 0; e < VEC; ++e) acc.v[e] = (T)0;
         }
-        int64_t ldo;
-        T* o = op_ptr<T>(bases, nd.out[r], ldo);
-        st_vec<T, VEC>(o + i * ldo + jv, acc);
+        st_vec<T, VEC>(optr[o] + i * old[o] + jv, acc);
       }
     }
   }
@@ -150,9 +180,16 @@ __global__ void __launch_bounds__(kThreads) k3_combine(const K3Node* __restrict_
                                                        Bases bases, int64_t rows, int64_t cols,
                                                        int P, int Q, int R) {
   __shared__ double cf[kMaxBlk * kMaxR];
+  __shared__ const T* iptr[kMaxR];
+  __shared__ int64_t ild[kMaxR];
   const K3Node& nd = nodes[blockIdx.z];
   const int nk = P * Q;
   for (int t = threadIdx.x; t < nk * R; t += blockDim.x) cf[t] = coef_all[nd.coef_off + t];
+  if (threadIdx.x < R) {
+    int64_t l;
+    iptr[threadIdx.x] = op_ptr<const T>(bases, nd.in[threadIdx.x], l);
+    ild[threadIdx.x] = l;
+  }
   __syncthreads();
   const int64_t jv = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * VEC;
   if (jv >= cols) return;
@@ -165,11 +202,7 @@ __global__ void __launch_bounds__(kThreads) k3_combine(const K3Node* __restrict_
     Vec<T, VEC> m[MAXR];
 #pragma unroll
     for (int r = 0; r < MAXR; ++r) {
-      if (r < R) {
-        int64_t ldm;
-        const T* mp = op_ptr<const T>(bases, nd.in[r], ldm);
-        m[r] = ld_vec<T, VEC>(mp + i * ldm + jv);
-      }
+      if (r < R) m[r] = ld_vec<T, VEC>(iptr[r] + i * ild[r] + jv);
     }
     for (int k = 0; k < nk; ++k) {
       Vec<T, VEC> acc;

@@ -315,3 +315,33 @@ def test_cuda_graph_replay(fb):
     p.execute(Ad, Bd, C2)
     torch.cuda.synchronize()
     assert np.array_equal(C2.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("dtype,leaf", [("f64", 0), ("f32", 0), ("f32", 2)])
+@pytest.mark.parametrize("dims", [(256, 128, 192), (200, 136, 72)])
+def test_no_out_of_bounds_writes(fb, dtype, leaf, dims):
+    # compute-sanitizer is closed on this pool: guard bands instead.  C has padding columns
+    # (ldc > N) and guard rows before / after; the workspace has guard bytes after its end.
+    # Nothing outside C[:, :N] and ws may change.
+    M, K, N = dims
+    L = 2 if all(d % 4 == 0 for d in dims) else 1
+    if any(d % (2 ** L) for d in dims):
+        pytest.skip("dims not divisible")
+    npdt = np.float64 if dtype == "f64" else np.float32
+    A, B = fi.random_pair(M, K, N, seed=50, dtype=npdt)
+    w = fb.Rule.builtin("winograd")
+    p = fb.Plan([w] * L, M, K, N, dtype=dtype, leaf=leaf)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    ldc = N + 6
+    big = torch.full((M + 8, ldc), 12345.0, dtype=tdt, device="cuda")
+    Cv = big[4:4 + M, :N]
+    nb = p.workspace_bytes()
+    wsb = torch.full((nb + 4096,), 0xA5, dtype=torch.uint8, device="cuda")
+    p.execute(dev(A), dev(B), Cv, ws=wsb[:nb])
+    torch.cuda.synchronize()
+    g = big.clone()
+    g[4:4 + M, :N] = 12345.0
+    assert torch.all(g == 12345.0), "write outside C[:, :N]"
+    assert torch.all(wsb[nb:] == 0xA5), "write past the workspace"
+    Co = oracle.fmm(A, B, OPlan.stationary(R.winograd(), L))
+    assert parity(Cv.cpu().numpy(), Co, A, B) <= (TOL64 if dtype == "f64" else TOL32)
