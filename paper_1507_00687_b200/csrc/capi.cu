@@ -499,7 +499,8 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
         if (p->dtype == FMM_F64)
           e = launch_gemm_f64((const LeafNode*)nd, s.count, s.rows, s.cols, s.inner, b, vec, st);
         else
-          e = launch_gemm_f32((const LeafNode*)nd, s.count, s.rows, s.cols, s.inner, b, vec, p->leaf,
+          e = launch_gemm_f32((const LeafNode*)nd, (const LeafNode*)(p->desc_host.data() + s.dev_off),
+                              s.count, s.rows, s.cols, s.inner, b, vec, p->leaf,
                               s.arena_off >= 0 ? (float*)b.p[BASE_WS] + s.arena_off : nullptr, st);
         break;
     }
@@ -1193,7 +1194,7 @@ fmm_status fmm_gemm(int dtype, int leaf, int64_t M, int64_t K, int64_t N, const 
                    ldc % vecn == 0 && K % vecn == 0 && N % vecn == 0;
   if (e == cudaSuccess)
     e = dtype == FMM_F64 ? launch_gemm_f64((const LeafNode*)dmem, 1, M, N, K, b, vec, st)
-                         : launch_gemm_f32((const LeafNode*)dmem, 1, M, N, K, b, vec, leaf,
+                         : launch_gemm_f32((const LeafNode*)dmem, &lf, 1, M, N, K, b, vec, leaf,
                                            arena ? (float*)((uint8_t*)dmem + 256) : nullptr, st);
   cudaError_t e2 = cudaFreeAsync(dmem, st);
   if (e == cudaSuccess) e = e2;

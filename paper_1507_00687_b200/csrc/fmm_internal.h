@@ -122,9 +122,9 @@ cudaError_t launch_zero(const Step& s, const void* dev_nodes, const Bases& b, cu
 
 cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
                             int64_t k, const Bases& b, bool vec, cudaStream_t st);
-cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
-                            int64_t k, const Bases& b, bool vec, int leaf, float* arena,
-                            cudaStream_t st);
+cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, const LeafNode* host_leaves, int count,
+                            int64_t m, int64_t n, int64_t k, const Bases& b, bool vec, int leaf,
+                            float* arena, cudaStream_t st);
 // floats of workspace the tensor-core FP32 leaf needs for a batch (hi / lo operand arena)
 size_t tf32_arena_floats(int64_t count, int64_t m, int64_t n, int64_t k);
 
