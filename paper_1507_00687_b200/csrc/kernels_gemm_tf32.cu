@@ -116,11 +116,35 @@ __device__ __forceinline__ void split2(float x, float& h, float& l) {
   }
 }
 
+// K-major UMMA descriptor for a BK-float-wide swizzled tile (BK = 32: SW128, BK = 16: SW64).
+template <int BK>
+__device__ __forceinline__ uint64_t desc_k(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((8 * BK * 4) >> 4) << 32;  // 8 rows x row bytes
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(BK == 32 ? 2 : 4) << 61;  // SWIZZLE_128B / SWIZZLE_64B
+  return d;
+}
+
+template <int BK, int STAGES>
+struct TCfg {
+  static constexpr int A_B = TBM * BK * 4, B_B = TBN * BK * 4;
+  static constexpr int STAGE = 2 * A_B + 2 * B_B;
+  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
+  static_assert(SMEM <= 227 * 1024, "smem");
+};
+
+template <int BK, int STAGES>
 __global__ void __launch_bounds__(256, 1)
     k2_tf32(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
             const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
             const LeafNode* __restrict__ leaves, Bases bases, int64_t m, int64_t n, int64_t kp,
             int tiles_n, int passes) {
+  using CF = TCfg<BK, STAGES>;
+  constexpr int TSTAGES = STAGES, TBK = BK, A_BYTES = CF::A_B, B_BYTES = CF::B_B,
+                STAGE_BYTES = CF::STAGE;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + TSTAGES * STAGE_BYTES);
@@ -184,9 +208,9 @@ __global__ void __launch_bounds__(256, 1)
         mbar_wait(su32(&bars[s]), ph);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         uint8_t* st = smem + s * STAGE_BYTES;
-        const uint64_t a_hi = desc_sw128(su32(st)), a_lo = desc_sw128(su32(st + A_BYTES));
-        const uint64_t b_hi = desc_sw128(su32(st + 2 * A_BYTES));
-        const uint64_t b_lo = desc_sw128(su32(st + 2 * A_BYTES + B_BYTES));
+        const uint64_t a_hi = desc_k<BK>(su32(st)), a_lo = desc_k<BK>(su32(st + A_BYTES));
+        const uint64_t b_hi = desc_k<BK>(su32(st + 2 * A_BYTES));
+        const uint64_t b_lo = desc_k<BK>(su32(st + 2 * A_BYTES + B_BYTES));
 #pragma unroll
         for (int kk = 0; kk < TBK / 8; ++kk) {
           const uint64_t off = (uint64_t)((kk * 32) >> 4);  // 8 tf32 = 32 bytes along K
@@ -525,15 +549,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 bool make_map(CUtensorMap* map, float* base, int64_t kp, int64_t rows, int64_t leaves,
-              int box_rows) {
+              int box_rows, int box_k = TBK) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {(cuuint64_t)kp, (cuuint64_t)rows, (cuuint64_t)leaves};
   cuuint64_t strides[2] = {(cuuint64_t)(kp * 4), (cuuint64_t)(kp * rows * 4)};
-  cuuint32_t box[3] = {(cuuint32_t)TBK, (cuuint32_t)box_rows, 1};
+  cuuint32_t box[3] = {(cuuint32_t)box_k, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  box_k == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -570,16 +595,32 @@ cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, i
     k_split_tf32<<<dim3((unsigned)(kp / 32), (unsigned)((n + 31) / 32), (unsigned)count), blk, 0, st>>>(
         dev_leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, 1);
   }
+  static const int cfg = [] {
+    const char* e = getenv("FMM_TF32_CFG");  // 0: BK 32 / 2 stages (default), 1: BK 16 / 4 stages
+    return e ? atoi(e) : 0;
+  }();
+  const int bk = cfg == 0 ? 32 : 16;
   CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
   const int64_t kpe = kp > 0 ? kp : TBK;
-  if (!make_map(&ma_hi, a_hi, kpe, m, count, TBM) || !make_map(&ma_lo, a_lo, kpe, m, count, TBM) ||
-      !make_map(&mb_hi, b_hi, kpe, n, count, TBN) || !make_map(&mb_lo, b_lo, kpe, n, count, TBN))
+  if (!make_map(&ma_hi, a_hi, kpe, m, count, TBM, bk) || !make_map(&ma_lo, a_lo, kpe, m, count, TBM, bk) ||
+      !make_map(&mb_hi, b_hi, kpe, n, count, TBN, bk) || !make_map(&mb_lo, b_lo, kpe, n, count, TBN, bk))
     return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(k2_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  if (e != cudaSuccess) return e;
   const int tiles_m = (int)((m + TBM - 1) / TBM), tiles_n = (int)((n + TBN - 1) / TBN);
-  k2_tf32<<<dim3((unsigned)(tiles_m * tiles_n), (unsigned)count), 256, SMEM_BYTES, st>>>(
-      ma_hi, ma_lo, mb_hi, mb_lo, dev_leaves, b, m, n, kp, tiles_n, passes);
+  const dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)count);
+  cudaError_t e;
+  if (cfg == 0) {
+    using CF = TCfg<32, 2>;
+    e = cudaFuncSetAttribute(k2_tf32<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
+    if (e != cudaSuccess) return e;
+    k2_tf32<32, 2><<<grid, 256, CF::SMEM, st>>>(ma_hi, ma_lo, mb_hi, mb_lo, dev_leaves, b, m, n, kp,
+                                                 tiles_n, passes);
+  } else {
+    using CF = TCfg<16, 4>;
+    e = cudaFuncSetAttribute(k2_tf32<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
+    if (e != cudaSuccess) return e;
+    k2_tf32<16, 4><<<grid, 256, CF::SMEM, st>>>(ma_hi, ma_lo, mb_hi, mb_lo, dev_leaves, b, m, n, kp,
+                                                 tiles_n, passes);
+  }
   return cudaGetLastError();
 }
 
