@@ -417,7 +417,7 @@ def run_fmm(args):
             "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": f"{args.config}: {' / '.join(rules)} (root first), M={M} K={K} "
                                    f"N={N} {args.dtype.upper()}, {cfgd.dist} seed {cfgd.seed} "
-                                   f"(BASELINE configs[{list(fi.CONFIGS).index(args.config) if args.config != 'C2c' else 1}])"
+                                   f"(BASELINE configs[{ {'C1': 0, 'C2': 1, 'C2c': 1, 'C3': 2, 'C4': 3, 'C5': 4}[args.config] }])"
                                    + (f", scaling {args.scaling} (pow2, tau=1)" if args.scaling != "none" else ""),
                        "parallelism": f"top-level r round-robin over {ws} GPU(s)"
                                       + (", ncclReduce of C" if ws > 1 else ""),
@@ -451,7 +451,8 @@ def main():
     ap.add_argument("--e2e-warmup", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-sample", type=int, default=16, help="reference arm: leaf rows per step")
+    ap.add_argument("--ref-sample", type=int, default=256,
+                    help="reference arm: leaf rows / cols per step (sample = 8x that per side at C5)")
     args = ap.parse_args()
     ws, _, _ = dist_env()
     if args.gpus != ws and ws > 1:

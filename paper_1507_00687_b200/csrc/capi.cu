@@ -127,6 +127,8 @@ struct fmm_plan {
   std::vector<RGroup> groups;
   mutable cudaStream_t copy_h2d = nullptr, copy_d2h = nullptr;
   mutable int copy_dev = -1;
+  // breadth-first plans: a depth-first twin used by fmm_execute_host to overlap the copies
+  mutable fmm_plan* df_twin = nullptr;
   // optional CUDA-graph replay of fmm_execute
   bool use_graph = false;
   struct GraphEntry {
@@ -145,6 +147,7 @@ struct fmm_plan {
 };
 
 fmm_plan::~fmm_plan() {
+  delete df_twin;
   for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
   if (copy_h2d) cudaStreamDestroy(copy_h2d);
   if (copy_d2h) cudaStreamDestroy(copy_d2h);
@@ -1026,6 +1029,22 @@ static fmm_status execute_host_pipelined(const fmm_plan* p, const void* A_host, 
   return cuda_status(e, "fmm_execute_host");
 }
 
+// The depth-first twin of a breadth-first plan (same rules, dims, dtype; bitwise-identical
+// results), built on first use.
+static const fmm_plan* depth_first_twin(const fmm_plan* p) {
+  std::lock_guard<std::mutex> g(p->dev_mu);
+  if (!p->df_twin) {
+    fmm_plan* t = new fmm_plan();
+    t->dtype = p->dtype; t->leaf = p->leaf; t->L = p->L; t->M = p->M; t->K = p->K; t->N = p->N;
+    t->rules = p->rules; t->node_rule = p->node_rule; t->lm = p->lm; t->lk = p->lk; t->ln = p->ln;
+    t->scaling = p->scaling; t->coef_U = p->coef_U; t->coef_V = p->coef_V; t->coef_W = p->coef_W;
+    t->coef_host = p->coef_host; t->schedule = 2;
+    if (compile_plan(t) != FMM_OK) { delete t; return nullptr; }
+    p->df_twin = t;
+  }
+  return p->df_twin;
+}
+
 fmm_status fmm_execute_host(const fmm_plan* p, const void* A_host, int64_t lda,
                             const void* B_host, int64_t ldb, void* C_host, int64_t ldc,
                             void* A_dev, void* B_dev, void* C_dev, void* ws, size_t ws_bytes,
@@ -1036,10 +1055,15 @@ fmm_status fmm_execute_host(const fmm_plan* p, const void* A_host, int64_t lda,
   }
   if (lda < p->K || ldb < p->N || ldc < p->N) { set_error("fmm_execute_host: bad ld"); return FMM_E_ARG; }
   cudaStream_t st = (cudaStream_t)stream;
-  if (!p->groups.empty() && p->scaling.mode == FMM_SCALE_NONE && !(p->comm && p->nranks > 1) &&
-      p->M > 0 && p->N > 0 && p->K > 0)
-    return execute_host_pipelined(p, A_host, lda, B_host, ldb, C_host, ldc, A_dev, B_dev, C_dev,
-                                  ws, ws_bytes, st);
+  if (p->L > 0 && p->scaling.mode == FMM_SCALE_NONE && !(p->comm && p->nranks > 1) && p->M > 0 &&
+      p->N > 0 && p->K > 0) {
+    const fmm_plan* q = p->groups.empty() ? depth_first_twin(p) : p;
+    size_t need = 0;
+    if (q) fmm_plan_workspace_bytes(q, &need);
+    if (q && !q->groups.empty() && ws && ws_bytes >= need)
+      return execute_host_pipelined(q, A_host, lda, B_host, ldb, C_host, ldc, A_dev, B_dev, C_dev,
+                                    ws, ws_bytes, st);
+  }
   const size_t es = (size_t)elem_size(p->dtype);
   cudaError_t e = cudaMemcpy2DAsync(A_dev, p->K * es, A_host, lda * es, p->K * es, p->M, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess)
