@@ -36,6 +36,20 @@ METRIC = "effective FP64 GFLOP/s (2MNK/t) at 1/2/4/8 B200 and max-norm error vs 
 UNIT = "GFLOP/s"
 FP64_DMMA_PEAK_TFLOPS = 36.9  # profiles/r01_fp64_peak_microbench.txt (mma.sync f64, 1965 MHz)
 TF32_PEAK_TFLOPS_NOMINAL = 1100.0  # B200_PROFILING.md nominal dense tf32 (fallback)
+BF16_PEAK_TFLOPS_NOMINAL = 2250.0  # B200_PROFILING.md nominal dense bf16
+
+
+def tf32_peak():
+    """TF32 tensor peak for the FP32 leaf: MEASURED_PEAKS.json's sustained bf16 figure (the
+    leaf runs inside a long step) x the guide's nominal tf32 / bf16 ratio; else the nominal."""
+    try:
+        mp = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        v = float(mp["bf16_tflops_sustained"])
+        return v * TF32_PEAK_TFLOPS_NOMINAL / BF16_PEAK_TFLOPS_NOMINAL, (
+            f"MEASURED_PEAKS.json bf16_tflops_sustained {v:g} x nominal tf32/bf16 "
+            f"{TF32_PEAK_TFLOPS_NOMINAL:g}/{BF16_PEAK_TFLOPS_NOMINAL:g}")
+    except (OSError, KeyError, ValueError):
+        return TF32_PEAK_TFLOPS_NOMINAL, "B200_PROFILING.md nominal dense TF32 (fallback)"
 
 
 def log(*a):
@@ -344,7 +358,8 @@ def run_fmm(args):
         plan.set_timing(False)
     k2_ms, k2_n = kinds.get("K2", (0.0, 0))
     per_launch_flops = leaf_flops_step * args.steps / max(k2_n, 1)
-    peak = FP64_DMMA_PEAK_TFLOPS if args.dtype == "f64" else TF32_PEAK_TFLOPS_NOMINAL / (
+    tf32, tf32_src = tf32_peak()
+    peak = FP64_DMMA_PEAK_TFLOPS if args.dtype == "f64" else tf32 / (
         3 if leaf == fb.fmm.LEAF_3XTF32 else 1)
     achieved = per_launch_flops / (k2_ms / max(k2_n, 1) * 1e-3) / 1e12 if k2_n else None
     workload = f"{args.config}-{args.dtype}-n{M}-L{L}-p{ws}" if args.config == "C5" else \
@@ -356,7 +371,8 @@ def run_fmm(args):
                 "traffic": load_traffic(workload),
                 "peak_source": "measured FP64 DMMA microbenchmark (profiles/r01_fp64_peak_microbench.txt); "
                                "MEASURED_PEAKS.json has no FP64 entry" if args.dtype == "f64" else
-                               "B200_PROFILING.md nominal dense TF32 (fallback)",
+                               tf32_src + (" / 3 (3xTF32: three MMA passes)"
+                                           if leaf == fb.fmm.LEAF_3XTF32 else ""),
                 "flops_per_launch": per_launch_flops, "launch_ms": (k2_ms / k2_n) if k2_n else None,
                 "step_share": {k: v[0] / max(sum(x[0] for x in kinds.values()), 1e-9)
                                for k, v in kinds.items()},

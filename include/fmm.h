@@ -133,6 +133,19 @@ fmm_status fmm_plan_set_partition(fmm_plan* plan, int rank, int nranks);
  * identical across schedules. */
 fmm_status fmm_plan_set_schedule(fmm_plan* plan, int schedule);
 
+/* Epilogue fusion of the accumulation step (host-only; north star item 3, Eq.
+ * eqn:recursive_alg P:116-125): the parents of the leaves compute C_k = sum_r w_kr M_r inside
+ * the leaf-product kernel -- one CTA runs the R leaf products of a parent at one output tile
+ * in ascending r and updates C_k after each (c = w*m first, then c = c + w*m), so M_r is never
+ * written to memory and the result is bitwise identical to the unfused K2 + K3 path.
+ * mode: 0 = off, 1 = on, 2 = automatic (default; on when parents x output tiles fill the GPU
+ * several times).  FP64 only (FP32 plans ignore it).  The environment variable FMM_FUSION
+ * (0/1/2) sets the default at fmm_plan_create. */
+fmm_status fmm_plan_set_fusion(fmm_plan* plan, int mode);
+
+/* Host-only query: number of fused leaf-product launches (K2F) in the compiled schedule. */
+fmm_status fmm_plan_fused_launches(const fmm_plan* plan, int64_t* n);
+
 /* Host-only query: owned[r] = 1 if top-level product r is computed by `rank` (R entries). */
 fmm_status fmm_plan_owned(const fmm_plan* plan, int rank, int nranks, int32_t* owned, int* R);
 

@@ -103,6 +103,7 @@ struct fmm_plan {
   fmm_scaling scaling{FMM_SCALE_NONE, 1, 1.0, 20, 0};
   int rank = 0, nranks = 1;
   int schedule = 0;  // 0 auto, 1 breadth-first, 2 depth-first top level
+  int fusion = 2;    // W-combination of the leaves' parents in the leaf GEMM epilogue: 0 off, 1 on, 2 auto
   ncclComm_t comm = nullptr;
   // compiled schedule
   std::vector<Step> steps;
@@ -206,7 +207,7 @@ struct Builder {
   }
 
   // K1 for the active nodes of level l (columns in `only_r` if >= 0); returns child nodes.
-  std::vector<Node> emit_k1(int l, const std::vector<Node>& nodes, int only_r) {
+  std::vector<Node> emit_k1(int l, const std::vector<Node>& nodes, int only_r, bool alloc_c = true) {
     const int64_t mb = p->lm[l + 1], kb = p->lk[l + 1], nb = p->ln[l + 1];
     std::vector<K1Node> ks, kt;
     std::vector<Node> kids;
@@ -237,9 +238,11 @@ struct Builder {
           t.out[r] = ch.b;
           t.out_mask |= 1u << r;
         }
-        ch.c = ws_op(ws_alloc(mb * nb), nb);
+        if (alloc_c) ch.c = ws_op(ws_alloc(mb * nb), nb);
         kids.push_back(ch);
       }
+      k1_compile(s, ru, ru.U, ru.m0 * ru.k0);
+      k1_compile(t, ru, ru.V, ru.k0 * ru.n0);
       if (s.out_mask) ks.push_back(s);
       if (t.out_mask) kt.push_back(t);
     }
@@ -277,6 +280,56 @@ struct Builder {
     p->steps.push_back(st);
   }
 
+  // Is the leaf-parent level fused (K2F) for `nparents` parents?  FP64 only; auto mode fuses
+  // when the fused grid (parents x 128x128 output tiles of a leaf) fills the GPU several times.
+  bool fuse_leaves(int64_t nparents) const {
+    if (p->dtype != FMM_F64 || p->fusion == 0) return false;
+    if (p->fusion == 1) return true;
+    const int64_t tiles = ((p->lm[p->L] + 127) / 128) * ((p->ln[p->L] + 127) / 128);
+    return nparents * tiles >= 4 * 148;
+  }
+
+  // K2F over parents at level l with their leaf children `kids` (R per parent, in order; or
+  // one child per parent, product `only_r`, when only_r >= 0).  `started` carries, per
+  // parent, the C blocks already initialised (depth-first top level).
+  void emit_k2f(int l, const std::vector<Node>& parents, const std::vector<Node>& kids, int only_r,
+                uint32_t* started_ext) {
+    std::vector<FusedNode> fz;
+    size_t ci = 0;
+    for (const Node& nd : parents) {
+      const RuleData& ru = rule_at(l, nd.idx);
+      FusedNode f{};
+      f.out = nd.c;
+      f.coef_off = p->coef_W[p->node_rule[l][nd.idx]];
+      uint32_t started = started_ext ? *started_ext : 0u;
+      for (int r = 0; r < ru.R; ++r) {
+        if (only_r >= 0 && r != only_r) continue;
+        const Node& ch = kids[ci++];
+        uint32_t wm = 0;
+        for (int k = 0; k < ru.m0 * ru.n0; ++k)
+          if (ru.W[(size_t)k * ru.R + r] != 0) wm |= 1u << k;
+        f.rlist[f.nr] = (uint8_t)r;
+        f.wmask[f.nr] = wm;
+        f.first[f.nr] = wm & ~started;
+        f.a[f.nr] = ch.a;
+        f.b[f.nr] = ch.b;
+        started |= wm;
+        ++f.nr;
+      }
+      if (started_ext) *started_ext = started;
+      fz.push_back(f);
+    }
+    const RuleData& r0 = rule_at(l, parents[0].idx);
+    Step st{};
+    st.kind = STEP_K2F;
+    st.count = (int)fz.size();
+    st.dev_off = push(fz);
+    st.rows = p->lm[p->L]; st.cols = p->ln[p->L]; st.inner = p->lk[p->L];
+    st.P = r0.m0; st.Q = r0.n0; st.R = r0.R;
+    st.arena_off = -1;
+    p->steps.push_back(st);
+  }
+
   // K3 for nodes of level l whose children are `kids` (R per node, in order).
   void emit_k3(int l, const std::vector<Node>& nodes, const std::vector<Node>& kids) {
     std::vector<K3Node> k3;
@@ -301,9 +354,17 @@ struct Builder {
   // breadth-first over the subtree(s) rooted at `nodes` (level l), outputs into nodes' c.
   void breadth_first(int l, const std::vector<Node>& nodes) {
     std::vector<std::vector<Node>> lv{nodes};
-    for (int d = l; d < p->L; ++d) lv.push_back(emit_k1(d, lv.back(), -1));
-    emit_k2(lv.back());
-    for (int d = p->L - 1; d >= l; --d) emit_k3(d, lv[d - l], lv[d - l + 1]);
+    for (int d = l; d < p->L - 1; ++d) lv.push_back(emit_k1(d, lv.back(), -1));
+    const bool fuse = fuse_leaves((int64_t)lv.back().size());
+    lv.push_back(emit_k1(p->L - 1, lv.back(), -1, !fuse));
+    int top = p->L - 1;
+    if (fuse) {
+      emit_k2f(p->L - 1, lv[p->L - 1 - l], lv.back(), -1, nullptr);
+      --top;
+    } else {
+      emit_k2(lv.back());
+    }
+    for (int d = top; d >= l; --d) emit_k3(d, lv[d - l], lv[d - l + 1]);
   }
 
   void build() {
@@ -341,7 +402,13 @@ struct Builder {
       if (r % p->nranks != p->rank) continue;
       ws_elems = mark;  // subtrees run one after another on one stream: reuse the workspace
       const size_t g0 = p->steps.size();
-      std::vector<Node> kid = emit_k1(0, {root}, r);
+      const bool fuse1 = p->L == 1 && fuse_leaves(1);
+      std::vector<Node> kid = emit_k1(0, {root}, r, !fuse1);
+      if (fuse1) {
+        emit_k2f(0, {root}, kid, r, &started);
+        p->groups.push_back({r, g0, p->steps.size()});
+        continue;
+      }
       if (p->L > 1) {
         breadth_first(1, kid);
       } else {
@@ -491,13 +558,17 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
   for (size_t si = i0; si < i1; ++si) {
     const Step& s = p->steps[si];
     const void* nd = (const uint8_t*)p->dev_desc + s.dev_off;
-    TimedLaunch tl(p, s.kind, st);
+    TimedLaunch tl(p, s.kind == STEP_K2F ? STEP_K2 : s.kind, st);
     cudaError_t e = cudaSuccess;
     switch (s.kind) {
       case STEP_K1: e = launch_k1<T>(s, nd, p->dev_coef, b, vec, st); break;
       case STEP_K3: e = launch_k3<T>(s, nd, p->dev_coef, b, vec, st); break;
       case STEP_ACC: e = launch_acc<T>(s, nd, p->dev_coef, b, vec, st); break;
       case STEP_ZERO: e = launch_zero<T>(s, nd, b, st); break;
+      case STEP_K2F:
+        e = launch_gemm_f64_fused((const FusedNode*)nd, s.count, s.rows, s.cols, s.inner,
+                                  p->dev_coef, s.P, s.Q, s.R, b, vec, st);
+        break;
       case STEP_K2:
         if (p->dtype == FMM_F64)
           e = launch_gemm_f64((const LeafNode*)nd, s.count, s.rows, s.cols, s.inner, b, vec, st);
@@ -651,6 +722,10 @@ fmm_status fmm_plan_create(const fmm_rule* const* nodes, int n_nodes, int levels
   }
   auto p = new fmm_plan();
   p->dtype = dtype; p->leaf = leaf; p->L = levels; p->M = M; p->K = K; p->N = N;
+  if (const char* fe = getenv("FMM_FUSION")) {
+    const int f = atoi(fe);
+    if (f >= 0 && f <= 2) p->fusion = f;
+  }
   if (scaling) {
     if (scaling->mode < FMM_SCALE_NONE || scaling->mode > FMM_SCALE_REPEATED ||
         (scaling->mode == FMM_SCALE_REPEATED && scaling->max_steps < 1)) {
@@ -739,6 +814,19 @@ fmm_status fmm_plan_set_schedule(fmm_plan* p, int schedule) {
   if (!p || schedule < 0 || schedule > 2) { set_error("fmm_plan_set_schedule: bad args"); return FMM_E_ARG; }
   p->schedule = schedule;
   return compile_plan(p);
+}
+
+fmm_status fmm_plan_set_fusion(fmm_plan* p, int mode) {
+  if (!p || mode < 0 || mode > 2) { set_error("fmm_plan_set_fusion: bad args"); return FMM_E_ARG; }
+  p->fusion = mode;
+  return compile_plan(p);
+}
+
+fmm_status fmm_plan_fused_launches(const fmm_plan* p, int64_t* n) {
+  if (!p || !n) { set_error("fmm_plan_fused_launches: null"); return FMM_E_ARG; }
+  *n = 0;
+  for (const Step& s : p->steps) *n += s.kind == STEP_K2F;
+  return FMM_OK;
 }
 
 fmm_status fmm_plan_owned(const fmm_plan* p, int rank, int nranks, int32_t* owned, int* R) {
@@ -1038,7 +1126,7 @@ static const fmm_plan* depth_first_twin(const fmm_plan* p) {
     t->dtype = p->dtype; t->leaf = p->leaf; t->L = p->L; t->M = p->M; t->K = p->K; t->N = p->N;
     t->rules = p->rules; t->node_rule = p->node_rule; t->lm = p->lm; t->lk = p->lk; t->ln = p->ln;
     t->scaling = p->scaling; t->coef_U = p->coef_U; t->coef_V = p->coef_V; t->coef_W = p->coef_W;
-    t->coef_host = p->coef_host; t->schedule = 2;
+    t->coef_host = p->coef_host; t->schedule = 2; t->fusion = p->fusion;
     if (compile_plan(t) != FMM_OK) { delete t; return nullptr; }
     p->df_twin = t;
   }
@@ -1123,6 +1211,8 @@ fmm_status fmm_node_st(const fmm_rule* rule, int dtype, int64_t m, int64_t k, in
     kt.out[q] = Op{BASE_WS, 0, 0, q * kb * nb, nb};
   }
   ks.out_mask = kt.out_mask = (r.R >= 32) ? 0xffffffffu : ((1u << r.R) - 1u);
+  k1_compile(ks, r, r.U, r.m0 * r.k0);
+  k1_compile(kt, r, r.V, r.k0 * r.n0);
   cudaStream_t st = (cudaStream_t)stream;
   void* dmem = nullptr;
   size_t bytes = coef.size() * 8 + 2 * sizeof(K1Node) + 512;

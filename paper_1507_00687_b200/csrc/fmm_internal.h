@@ -44,16 +44,53 @@ __host__ __device__ inline T* op_ptr(const Bases& b, const Op& o, int64_t& ld) {
   return (T*)base + o.row0 * ld + o.col0;
 }
 
+// ---- rules -----------------------------------------------------------------------------------
+struct RuleData {
+  std::string name;
+  int m0 = 0, k0 = 0, n0 = 0, R = 0, log2den = 0;
+  std::vector<int32_t> U, V, W;  // numerators, row-major (rows x R)
+  double coef(const std::vector<int32_t>& X, int row, int r) const {
+    return (double)X[(size_t)row * R + r] / (double)(1 << log2den);
+  }
+};
+
 // ---- K1: linear combinations S_r = sum_i u_ir A_i (or T_r = sum_j v_jr B_j) -------------
 // The input operand (rows*P x cols*Q) is split into P x Q sub-blocks of rows x cols; the
 // sub-block index is column-major, blk = p + P*q.  coef points at the rule's table
 // ((P*Q) x R row-major).  Outputs are written for the r in out_mask.
+// The output list is compiled on the host (k1_compile): nout outputs r = rlist[o], each with
+// a 2-bit code per input block (0 absent, 1 +1, 2 -1, 3 general coefficient from the table).
 struct K1Node {
   Op in;
   int32_t coef_off;  // offset (in doubles) of the table in the plan's coefficient buffer
   uint32_t out_mask;
+  int32_t nout;      // number of outputs written
+  uint32_t need;     // bit b: input block b is read
+  uint8_t rlist[kMaxR];
+  uint32_t code[kMaxR];
   Op out[kMaxR];
 };
+
+// Host: fill nout / rlist / code / need of a K1 node from its rule table X ((nblk) x R
+// numerators over 2^log2den, i.e. U or V) and the node's out_mask.
+inline void k1_compile(K1Node& n, const RuleData& ru, const std::vector<int32_t>& X, int nblk) {
+  n.nout = 0;
+  n.need = 0;
+  const int32_t one = 1 << ru.log2den;
+  for (int r = 0; r < ru.R; ++r) {
+    if (!((n.out_mask >> r) & 1u)) continue;
+    uint32_t c = 0;
+    for (int b = 0; b < nblk; ++b) {
+      const int32_t u = X[(size_t)b * ru.R + r];
+      if (u == 0) continue;
+      n.need |= 1u << b;
+      c |= (u == one ? 1u : u == -one ? 2u : 3u) << (2 * b);
+    }
+    n.rlist[n.nout] = (uint8_t)r;
+    n.code[n.nout] = c;
+    ++n.nout;
+  }
+}
 
 // ---- K3: C_k = sum_r w_kr M_r into the node output (rows*M0 x cols*N0), k = ia*N0 + jb ----
 struct K3Node {
@@ -85,7 +122,23 @@ struct LeafNode {
   Op a, b, c;
 };
 
-enum StepKind { STEP_K1 = 1, STEP_K2 = 2, STEP_K3 = 3, STEP_ACC = 4, STEP_ZERO = 5 };
+// ---- K2F: leaf products with the parent's W-combination fused into the epilogue ----------
+// One CTA computes one output tile position of the leaf products r = rlist[0..nr) of a parent
+// node in ascending order and, after each product, updates the parent's output blocks
+//   C_k = w_kr M_r (first contribution, bit k of first[i]) | C_k = C_k + w_kr M_r,
+// i.e. the K3 / ACC arithmetic in the same per-element order (bitwise identical), without
+// writing M_r to memory.
+struct FusedNode {
+  Op out;            // parent output (M0*m x N0*n)
+  int32_t coef_off;  // W table ((M0*N0) x R)
+  int32_t nr;
+  uint8_t rlist[kMaxR];
+  uint32_t wmask[kMaxR];  // bit k: w_kr != 0
+  uint32_t first[kMaxR];  // bit k: this product initialises C_k
+  Op a[kMaxR], b[kMaxR];  // leaf operands S_r, T_r (index i, not r)
+};
+
+enum StepKind { STEP_K1 = 1, STEP_K2 = 2, STEP_K3 = 3, STEP_ACC = 4, STEP_ZERO = 5, STEP_K2F = 8 };
 
 struct Step {
   int kind;
@@ -95,16 +148,6 @@ struct Step {
   int P, Q, R;       // K1: split P x Q, rank R.  K3/ACC/ZERO: P = M0, Q = N0, R
   int64_t arena_off; // K2 FP32 tensor-core leaves: offset (elements) of the hi/lo arena in ws
   bool vec_ok;       // all ws offsets / dims allow 16-byte vectors (caller bases checked later)
-};
-
-// ---- rules -----------------------------------------------------------------------------------
-struct RuleData {
-  std::string name;
-  int m0 = 0, k0 = 0, n0 = 0, R = 0, log2den = 0;
-  std::vector<int32_t> U, V, W;  // numerators, row-major (rows x R)
-  double coef(const std::vector<int32_t>& X, int row, int r) const {
-    return (double)X[(size_t)row * R + r] / (double)(1 << log2den);
-  }
 };
 
 // ---- kernel launchers (kernels_*.cu) -----------------------------------------------------------
@@ -122,6 +165,9 @@ cudaError_t launch_zero(const Step& s, const void* dev_nodes, const Bases& b, cu
 
 cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
                             int64_t k, const Bases& b, bool vec, cudaStream_t st);
+cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
+                                  int64_t k, const double* dev_coef, int P, int Q, int R,
+                                  const Bases& b, bool vec, cudaStream_t st);
 cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, const LeafNode* host_leaves, int count,
                             int64_t m, int64_t n, int64_t k, const Bases& b, bool vec, int leaf,
                             float* arena, cudaStream_t st);

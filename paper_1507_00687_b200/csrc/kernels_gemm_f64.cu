@@ -268,6 +268,224 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   }
 }
 
+// K2F: the leaf products r = rlist[0..nr) of one parent node (grid.y) at one output tile
+// position (grid.x), in ascending order, with the parent's W-combination in the epilogue
+// (FusedNode in fmm_internal.h).  The cp.async pipeline runs over the flattened (product,
+// k-tile) sequence, so the next product's first stages are in flight while the epilogue of the
+// previous one updates C_k.  Each thread owns the same fragment positions in every product,
+// so the read-modify-write chain of an element of C_k stays in one thread, in ascending r:
+//   c = w*m (first contribution)  |  c = c + w*m        (both rounded to nearest, no FMA)
+// exactly K3's sequence (k3_combine / k_acc), with M_r never written to memory.
+template <typename C, bool VEC>
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
+    k2f_gemm_f64(const FusedNode* __restrict__ nodes, const double* __restrict__ coef_all,
+                 Bases bases, int64_t m, int64_t n, int64_t k, int tiles_m, int tiles_n, int P,
+                 int Q, int R) {
+  static_assert(C::PIPE, "the fused kernel uses the PIPE mainloop");
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + C::STAGES * C::A_STAGE;
+  __shared__ const double* pa[kMaxR];
+  __shared__ const double* pb[kMaxR];
+  __shared__ int64_t la[kMaxR], lb[kMaxR];
+  __shared__ uint32_t wm_s[kMaxR], fm_s[kMaxR];
+  __shared__ int r_s[kMaxR];
+  __shared__ double wcf[kMaxBlk * kMaxR];
+
+  const FusedNode& nd = nodes[blockIdx.y];
+  const int nr = nd.nr;
+  const int tid = threadIdx.x;
+  if (tid < nr) {
+    int64_t l;
+    pa[tid] = op_ptr<const double>(bases, nd.a[tid], l);
+    la[tid] = l;
+    pb[tid] = op_ptr<const double>(bases, nd.b[tid], l);
+    lb[tid] = l;
+    wm_s[tid] = nd.wmask[tid];
+    fm_s[tid] = nd.first[tid];
+    r_s[tid] = nd.rlist[tid];
+  }
+  for (int t = tid; t < P * Q * R; t += C::THREADS) wcf[t] = coef_all[nd.coef_off + t];
+  __syncthreads();
+
+  const int tile = blockIdx.x;
+  const int per_group = GROUP_M * tiles_n;
+  const int group = tile / per_group;
+  const int first_m = group * GROUP_M;
+  const int gsz = min(tiles_m - first_m, GROUP_M);
+  const int tm = first_m + (tile % per_group) % gsz;
+  const int tn = (tile % per_group) / gsz;
+  const int64_t m0 = (int64_t)tm * C::BM, n0 = (int64_t)tn * C::BN;
+
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int g = lane >> 2, t = lane & 3;
+
+  double acc[C::MI][C::NI][4];
+#pragma unroll
+  for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+
+  const int KT = max(1, (int)((k + C::BK - 1) / C::BK));  // k = 0: one zero-filled tile
+  const int total = nr * KT;
+  // load stream over the flattened (product, k-tile) sequence, advanced incrementally
+  int l_kt = 0, l_ri = 0;
+  const double* lA = pa[0];
+  const double* lB = pb[0];
+  int64_t lla = la[0], llb = lb[0];
+  auto load_next = [&](int slot) {
+    load_tiles<C, VEC>(As + slot * C::A_STAGE, Bs + slot * C::B_STAGE, lA, lla, lB, llb, m, n, k,
+                       m0, n0, (int64_t)l_kt * C::BK, tid);
+    if (++l_kt == KT) {
+      l_kt = 0;
+      if (++l_ri < nr) {
+        lA = pa[l_ri]; lB = pb[l_ri]; lla = la[l_ri]; llb = lb[l_ri];
+      }
+    }
+  };
+  auto epilogue = [&](int ri) {
+    const uint32_t wmask = wm_s[ri], fmask = fm_s[ri];
+    const int r = r_s[ri];
+    int64_t ldo;
+    double* out = op_ptr<double>(bases, nd.out, ldo);
+    for (int kk = 0; kk < P * Q; ++kk) {  // kk = ia*Q + jb (row-major C blocks)
+      if (!((wmask >> kk) & 1u)) continue;
+      const double w = wcf[kk * R + r];
+      const bool first = (fmask >> kk) & 1u;
+      double* ob = out + (int64_t)(kk / Q) * m * ldo + (int64_t)(kk % Q) * n;
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i) {
+        double2 old[2][C::NI];
+        if (!first) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t row = m0 + wm * C::WTM + i * 16 + g + h * 8;
+#pragma unroll
+            for (int j = 0; j < C::NI; ++j) {
+              const int64_t col = n0 + wn * C::WTN + j * 8 + 2 * t;
+              old[h][j] = make_double2(0.0, 0.0);
+              if (row < m) {
+                const double* cp = ob + row * ldo + col;
+                if (VEC && col + 1 < n) old[h][j] = *reinterpret_cast<const double2*>(cp);
+                else {
+                  if (col < n) old[h][j].x = cp[0];
+                  if (col + 1 < n) old[h][j].y = cp[1];
+                }
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t row = m0 + wm * C::WTM + i * 16 + g + h * 8;
+          if (row >= m) continue;
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j) {
+            const int64_t col = n0 + wn * C::WTN + j * 8 + 2 * t;
+            double v0 = __dmul_rn(w, acc[i][j][2 * h]), v1 = __dmul_rn(w, acc[i][j][2 * h + 1]);
+            if (!first) {
+              v0 = __dadd_rn(old[h][j].x, v0);
+              v1 = __dadd_rn(old[h][j].y, v1);
+            }
+            double* cp = ob + row * ldo + col;
+            if (VEC && col + 1 < n) {
+              *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
+            } else {
+              if (col < n) cp[0] = v0;
+              if (col + 1 < n) cp[1] = v1;
+            }
+          }
+        }
+      }
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < C::STAGES - 1; ++s) {
+    if (s < total) load_next(s);
+    cp_commit();
+  }
+  constexpr int KQ = C::BK / 4;
+  static_assert(KQ % 2 == 0, "even number of k-slices per stage");
+  double af[2][C::MI][2], bf[2][C::NI];
+  const int a_off = (wm * C::WTM + g) * C::A_LD + t, b_off = t * C::B_LD + wn * C::WTN + g;
+  auto load_frag = [&](int buf, int slot, int kk) {
+    const double* as = As + slot * C::A_STAGE + a_off;
+    const double* bs = Bs + slot * C::B_STAGE + b_off;
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i) {
+      af[buf][i][0] = as[(i * 16) * C::A_LD + kk];
+      af[buf][i][1] = as[(i * 16 + 8) * C::A_LD + kk];
+    }
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) bf[buf][j] = bs[kk * C::B_LD + j * 8];
+  };
+  cp_wait<C::STAGES - 2>();
+  __syncthreads();
+  if (C::STAGES - 1 < total) load_next((C::STAGES - 1) % C::STAGES);
+  cp_commit();
+  load_frag(0, 0, 0);
+  int kt_in_r = 0, ri = 0;
+  for (int it = 0; it < total; ++it) {
+    const int slot = it % C::STAGES;
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+      const int cur = q & 1;
+      if (q == KQ - 1) {
+        cp_wait<C::STAGES - 2>();
+        __syncthreads();  // every warp is done reading `slot` (its last slice is in registers)
+        if (it + C::STAGES < total) load_next(slot);
+        cp_commit();
+        if (it + 1 < total) load_frag(cur ^ 1, (it + 1) % C::STAGES, 0);
+      } else {
+        load_frag(cur ^ 1, slot, (q + 1) * 4);
+      }
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) dmma16n8k4(acc[i][j], af[cur][i][0], af[cur][i][1], bf[cur][j]);
+    }
+    if (++kt_in_r == KT) {
+      epilogue(ri);
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+      kt_in_r = 0;
+      ++ri;
+    }
+  }
+  cp_wait<0>();
+}
+
+template <typename C>
+cudaError_t launch_fused_cfg(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
+                             int64_t k, const double* coef, int P, int Q, int R, const Bases& b,
+                             bool vec, cudaStream_t st) {
+  const int tiles_m = (int)((m + C::BM - 1) / C::BM), tiles_n = (int)((n + C::BN - 1) / C::BN);
+  dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)count);
+  cudaError_t e;
+  if (vec) {
+    e = cudaFuncSetAttribute(k2f_gemm_f64<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    k2f_gemm_f64<C, true><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(dev_nodes, coef, b, m, n, k,
+                                                                  tiles_m, tiles_n, P, Q, R);
+  } else {
+    e = cudaFuncSetAttribute(k2f_gemm_f64<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    k2f_gemm_f64<C, false><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(dev_nodes, coef, b, m, n, k,
+                                                                   tiles_m, tiles_n, P, Q, R);
+  }
+  return cudaGetLastError();
+}
+
 template <typename C>
 cudaError_t launch_cfg(const LeafNode* dev_leaves, int count, int64_t m, int64_t n, int64_t k,
                        const Bases& b, bool vec, cudaStream_t st) {
@@ -346,6 +564,27 @@ cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, in
     case 20: return launch_cfg<V20>(dev_leaves, count, m, n, k, b, vec, st);
     case 1: return launch_cfg<V1>(dev_leaves, count, m, n, k, b, vec, st);
     default: return launch_cfg<V16>(dev_leaves, count, m, n, k, b, vec, st);
+  }
+}
+
+namespace {
+int fused_variant() {
+  static int v = [] {
+    const char* e = getenv("FMM_K2F_VARIANT");
+    return e ? atoi(e) : 16;
+  }();
+  return v;
+}
+}  // namespace
+
+cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
+                                  int64_t k, const double* dev_coef, int P, int Q, int R,
+                                  const Bases& b, bool vec, cudaStream_t st) {
+  if (count == 0 || m == 0 || n == 0) return cudaSuccess;
+  switch (fused_variant()) {
+    case 13: return launch_fused_cfg<V13>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
+    case 15: return launch_fused_cfg<V15>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
+    default: return launch_fused_cfg<V16>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
   }
 }
 

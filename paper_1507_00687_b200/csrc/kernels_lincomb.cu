@@ -8,6 +8,8 @@
 // each output written once per launch (the algorithmic floor).  Sums run sequentially in
 // ascending index order with explicit round-to-nearest intrinsics (no FMA contraction),
 // exactly the order of PAPER.md's sequential summation model (eqn:seq_summation_error).
+#include <cstdlib>
+
 #include "fmm_internal.h"
 
 namespace fmm {
@@ -68,66 +70,47 @@ __device__ __forceinline__ void st_vec(T* p, const Vec<T, VEC>& r) {
 constexpr int kThreads = 256;  // threads per block (x: column vectors)
 constexpr int kRowsPerBlock = 4;
 
-// grid: x = column chunks of kThreads vectors, y = row groups of kRowsPerBlock, z = node.
+// K1 grid: x = column chunks of kThreads vectors, y = row groups of RPB rows, z = node.
 // NBLK: compile-time bound on the number of input sub-blocks (4 for 2x2 rules) so that the
-// per-thread input registers stay small; two rows are loaded before either is combined, so
-// each thread keeps up to 2*NBLK 16-byte loads in flight.  Per block, thread 0 compiles the
-// node's outputs into shared memory once: the list of r to write, their base pointers, and per
-// r a 2-bit code per input block (0: absent, 1: +1, 2: -1, 3: general coefficient); the inner
-// loop then needs one broadcast shared load per output.  u*x with u = +-1 is exact, so adding
-// +-x is bitwise the oracle's  s + u*x.
-template <typename T, int VEC, int NBLK>
+// per-thread input registers stay small; RIF rows are loaded before any is combined, so each
+// thread keeps up to RIF*NBLK 16-byte loads in flight.  The output list (which r, and per r a
+// 2-bit code per input block: 0 absent, 1 +1, 2 -1, 3 general coefficient) is compiled on the
+// host into the node descriptor (k1_compile); threads 0..nout-1 resolve the output pointers in
+// parallel, so the per-block setup is one shared-memory round trip.  u*x with u = +-1 is exact,
+// so adding +-x is bitwise the oracle's  s + u*x.
+template <typename T, int VEC, int NBLK, int RPB, int RIF>
 __global__ void __launch_bounds__(kThreads) k1_lincomb(const K1Node* __restrict__ nodes,
                                                        const double* __restrict__ coef_all,
                                                        Bases bases, int64_t rows, int64_t cols,
                                                        int P, int Q, int R) {
-  __shared__ double cf[kMaxBlk * kMaxR];
   __shared__ T* optr[kMaxR];
   __shared__ int64_t old[kMaxR];
   __shared__ uint32_t code[kMaxR];
   __shared__ int rlist[kMaxR];
-  __shared__ int nr_s;
-  __shared__ uint32_t need_s;
   const K1Node& nd = nodes[blockIdx.z];
   const int nblk = P * Q;
-  const uint32_t omask = nd.out_mask;
-  for (int t = threadIdx.x; t < nblk * R; t += blockDim.x) cf[t] = coef_all[nd.coef_off + t];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t need = 0;
-    int nr = 0;
-    for (int r = 0; r < R; ++r) {
-      if (!((omask >> r) & 1u)) continue;
-      uint32_t c = 0;
-      for (int b = 0; b < nblk; ++b) {
-        const double u = cf[b * R + r];
-        if (u == 0.0) continue;
-        need |= 1u << b;
-        c |= (u == 1.0 ? 1u : u == -1.0 ? 2u : 3u) << (2 * b);
-      }
-      int64_t ldo;
-      optr[nr] = op_ptr<T>(bases, nd.out[r], ldo);
-      old[nr] = ldo;
-      code[nr] = c;
-      rlist[nr] = r;
-      ++nr;
-    }
-    nr_s = nr;
-    need_s = need;
+  const int nout = nd.nout;
+  const uint32_t need = nd.need;
+  if (threadIdx.x < nout) {
+    const int r = nd.rlist[threadIdx.x];
+    int64_t ldo;
+    optr[threadIdx.x] = op_ptr<T>(bases, nd.out[r], ldo);
+    old[threadIdx.x] = ldo;
+    code[threadIdx.x] = nd.code[threadIdx.x];
+    rlist[threadIdx.x] = r;
   }
-  __syncthreads();
-  const uint32_t need = need_s;
-  const int nr = nr_s;
-
   int64_t ldi;
   const T* in = op_ptr<const T>(bases, nd.in, ldi);
+  __syncthreads();
+
   const int64_t jv = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * VEC;
   if (jv >= cols) return;
-  const int64_t i0 = (int64_t)blockIdx.y * kRowsPerBlock;
-  for (int ii = 0; ii < kRowsPerBlock; ii += 2) {
-    Vec<T, VEC> x[2][NBLK];
+  const int64_t i0 = (int64_t)blockIdx.y * RPB;
+#pragma unroll 1
+  for (int ii = 0; ii < RPB; ii += RIF) {
+    Vec<T, VEC> x[RIF][NBLK];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < RIF; ++h) {
       const int64_t i = i0 + ii + h;
 #pragma unroll
       for (int b = 0; b < NBLK; ++b) {
@@ -138,10 +121,11 @@ __global__ void __launch_bounds__(kThreads) k1_lincomb(const K1Node* __restrict_
       }
     }
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < RIF; ++h) {
       const int64_t i = i0 + ii + h;
       if (i >= rows) break;
-      for (int o = 0; o < nr; ++o) {
+#pragma unroll 1
+      for (int o = 0; o < nout; ++o) {
         const uint32_t c = code[o];
         Vec<T, VEC> acc;
         bool started = false;
@@ -150,7 +134,7 @@ __global__ void __launch_bounds__(kThreads) k1_lincomb(const K1Node* __restrict_
           const uint32_t cb = (c >> (2 * b)) & 3u;
           if (cb == 0u) continue;
           if (cb == 3u) {  // general dyadic coefficient: s + u*x
-            const T ut = (T)cf[b * R + rlist[o]];
+            const T ut = (T)coef_all[nd.coef_off + b * R + rlist[o]];
 #pragma unroll
             for (int e = 0; e < VEC; ++e)
               acc.v[e] = started ? add_rn<T>(acc.v[e], mul_rn<T>(ut, x[h][b].v[e])) : mul_rn<T>(ut, x[h][b].v[e]);
@@ -289,6 +273,36 @@ inline dim3 grid_for(const Step& s, int vec) {
 
 }  // namespace
 
+namespace {
+int k1_variant() {
+  static int v = [] {
+    const char* e = getenv("FMM_K1_VARIANT");
+    return e ? atoi(e) : 1;  // 4 rows per block, 2 in flight: 6.58 TB/s (tools/bench_passes.py)
+  }();
+  return v;
+}
+
+template <typename T, int VEC, int NBLK, int RPB, int RIF>
+void k1_go(const Step& s, const K1Node* nd, const double* dev_coef, const Bases& b, cudaStream_t st) {
+  const int64_t cv = (s.cols + VEC - 1) / VEC;
+  dim3 grid((unsigned)((cv + kThreads - 1) / kThreads), (unsigned)((s.rows + RPB - 1) / RPB),
+            (unsigned)s.count);
+  k1_lincomb<T, VEC, NBLK, RPB, RIF><<<grid, kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
+}
+
+template <typename T, int VEC, int NBLK>
+void k1_pick(const Step& s, const K1Node* nd, const double* dev_coef, const Bases& b, cudaStream_t st) {
+  switch (k1_variant()) {
+    case 2: k1_go<T, VEC, NBLK, 8, 2>(s, nd, dev_coef, b, st); break;
+    case 3: k1_go<T, VEC, NBLK, 16, 2>(s, nd, dev_coef, b, st); break;
+    case 4: k1_go<T, VEC, NBLK, 8, 4>(s, nd, dev_coef, b, st); break;
+    case 5: k1_go<T, VEC, NBLK, 16, 4>(s, nd, dev_coef, b, st); break;
+    case 6: k1_go<T, VEC, NBLK, 32, 2>(s, nd, dev_coef, b, st); break;
+    default: k1_go<T, VEC, NBLK, 4, 2>(s, nd, dev_coef, b, st); break;
+  }
+}
+}  // namespace
+
 template <typename T>
 cudaError_t launch_k1(const Step& s, const void* dev_nodes, const double* dev_coef,
                       const Bases& b, bool vec, cudaStream_t st) {
@@ -296,15 +310,11 @@ cudaError_t launch_k1(const Step& s, const void* dev_nodes, const double* dev_co
   constexpr int V = 16 / sizeof(T);
   const K1Node* nd = (const K1Node*)dev_nodes;
   if (s.P * s.Q <= 4) {
-    if (vec)
-      k1_lincomb<T, V, 4><<<grid_for(s, V), kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
-    else
-      k1_lincomb<T, 1, 4><<<grid_for(s, 1), kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
+    if (vec) k1_pick<T, V, 4>(s, nd, dev_coef, b, st);
+    else k1_pick<T, 1, 4>(s, nd, dev_coef, b, st);
   } else {
-    if (vec)
-      k1_lincomb<T, V, kMaxBlk><<<grid_for(s, V), kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
-    else
-      k1_lincomb<T, 1, kMaxBlk><<<grid_for(s, 1), kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
+    if (vec) k1_go<T, V, kMaxBlk, 4, 1>(s, nd, dev_coef, b, st);
+    else k1_go<T, 1, kMaxBlk, 4, 1>(s, nd, dev_coef, b, st);
   }
   return cudaGetLastError();
 }

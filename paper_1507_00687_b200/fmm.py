@@ -42,6 +42,8 @@ SIGNATURES = {
     "fmm_plan_destroy": (None, [_P]),
     "fmm_plan_set_partition": (_I, [_P, _I, _I]),
     "fmm_plan_set_schedule": (_I, [_P, _I]),
+    "fmm_plan_set_fusion": (_I, [_P, _I]),
+    "fmm_plan_fused_launches": (_I, [_P, C.POINTER(C.c_int64)]),
     "fmm_plan_owned": (_I, [_P, _I, _I, _P, C.POINTER(_I)]),
     "fmm_plan_workspace_bytes": (_I, [_P, C.POINTER(_SZ)]),
     "fmm_plan_launch_count": (_I, [_P, C.POINTER(_I64)]),
@@ -246,6 +248,16 @@ class Plan:
         """'auto' | 'breadth' | 'depth' (top-level depth-first)."""
         _call("fmm_plan_set_schedule", self._h, {"auto": 0, "breadth": 1, "depth": 2}[schedule])
         self._ws = None
+
+    def set_fusion(self, mode):
+        """Leaf-product epilogue fusion of the parents' W-combination: 'off' | 'on' | 'auto'."""
+        _call("fmm_plan_set_fusion", self._h, {"off": 0, "on": 1, "auto": 2}[mode])
+        self._ws = None
+
+    def fused_launches(self) -> int:
+        n = C.c_int64()
+        _call("fmm_plan_fused_launches", self._h, C.byref(n))
+        return n.value
 
     def owned(self, rank: int, nranks: int):
         import numpy as np

@@ -103,3 +103,23 @@ def test_nonuniform_plan_validation():
     c = fb.Rule.builtin("classical222")
     with pytest.raises(fb.FmmError):  # rank differs within a level
         fb.Plan([s] + [c] + [s] * 6, 256, 256, 256, uniform=False, levels=2)
+
+
+def test_fusion_auto_policy():
+    # auto: fuse the leaf-parent level when parents x 128^2 leaf tiles >= 4 x 148 (FP64 only)
+    w, s, c = (fb.Rule.builtin(n) for n in ("winograd", "strassen", "classical222"))
+    cases = [([w, w], (512,) * 3, 0),                 # C1: 7 parents x 1 tile
+             ([s] * 4, (4096,) * 3, 1),               # C2: 343 x 4
+             ([w, c, s], (8192, 4096, 8192), 1),     # C3: 56 x 64
+             ([w] * 3, (4096,) * 3, 1),               # C4: 49 x 16
+             ([w] * 3, (32768,) * 3, 7)]              # C5: depth-first, one per subtree
+    for rules, (M, K, N), want in cases:
+        p = fb.Plan(rules, M, K, N)
+        assert p.fused_launches() == want, (M, want)
+    p = fb.Plan([w] * 3, 4096, 4096, 4096)
+    ws_fused = p.workspace_bytes()
+    p.set_fusion("off")
+    assert p.fused_launches() == 0
+    assert p.workspace_bytes() > ws_fused  # leaf M_r buffers are not allocated when fused
+    p32 = fb.Plan([w] * 3, 4096, 4096, 4096, dtype="f32")
+    assert p32.fused_launches() == 0
