@@ -364,8 +364,10 @@ def run_fmm(args):
     achieved = per_launch_flops / (k2_ms / max(k2_n, 1) * 1e-3) / 1e12 if k2_n else None
     workload = f"{args.config}-{args.dtype}-n{M}-L{L}-p{ws}" if args.config == "C5" else \
         f"{args.config}-{args.dtype}-p{ws}"
-    roofline = {"kernel": "k2_gemm_f64 (leaf products, DMMA mma.sync f64)" if args.dtype == "f64"
-                else "k2 (leaf products, FP32)",
+    fused = plan.fused_launches() > 0
+    k2_name = ("k2f_gemm_f64 (leaf products on DMMA mma.sync f64 + the parents' W-combination "
+               "fused in the epilogue)" if fused else "k2_gemm_f64 (leaf products, DMMA mma.sync f64)")
+    roofline = {"kernel": k2_name if args.dtype == "f64" else "k2 (leaf products, FP32)",
                 "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None,
                 "traffic": load_traffic(workload),
@@ -439,7 +441,8 @@ def run_fmm(args):
                                       + (", ncclReduce of C" if ws > 1 else ""),
                        "l2": ("operands %.1f GiB each > 126 MB L2 (no flush needed)" % (M * K * esz / 2**30))
                   if not small else "L2 flushed (256 MB write) between timed steps, outside the events",
-                       "leaf": {0: "native", 1: "tf32", 2: "3xtf32"}[leaf]},
+                       "leaf": {0: "native", 1: "tf32", 2: "3xtf32"}[leaf],
+                       "k3_fused_in_leaf_epilogue": bool(fused)},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": plan.launch_count() * args.steps,
             "cuda_graph": use_graph,

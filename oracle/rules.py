@@ -158,6 +158,30 @@ def castrapel_gustafson(base: Rule, x: int, y: int, z: int) -> Rule:
     return make_rule(f"{base.name}_cg{x}{y}{z}", base.m0, base.k0, base.n0, U, V, W)
 
 
+def make_rule_labelled(name, m0, k0, n0, U, V, W, u_labels, v_labels, w_labels,
+                       u_den=1, v_den=1, w_den=1) -> Rule:
+    """A rule from tables whose rows are given in an arbitrary order: row p of U is the entry
+    u_labels[p] = (ia, ja) of A, row p of V is v_labels[p] = (ja, jb) of B, row p of W is
+    w_labels[p] = (ia, jb) of C; entries are divided by the *_den prefactors.  Rows are placed
+    in the stated convention: U row ia + m0*ja, V row ja + k0*jb, W row ia*n0 + jb.
+    Used for App. C's <4,4,2;26>, whose printed row order is not that
+    convention (reading A27)."""
+    R = len(U[0])
+
+    def place(X, labels, nrows, index, den):
+        out = [None] * nrows
+        for row, lab in zip(X, labels):
+            out[index(*lab)] = [Fraction(x, den) for x in row]
+        assert all(r is not None for r in out) and len(labels) == nrows, name
+        return out
+
+    Uo = place(U, u_labels, m0 * k0, lambda ia, ja: ia + m0 * ja, u_den)
+    Vo = place(V, v_labels, k0 * n0, lambda ja, jb: ja + k0 * jb, v_den)
+    Wo = place(W, w_labels, m0 * n0, lambda ia, jb: ia * n0 + jb, w_den)
+    assert all(len(r) == R for r in Uo + Vo + Wo)
+    return make_rule(name, m0, k0, n0, Uo, Vo, Wo)
+
+
 BUILTINS = {
     "classical222": classical222,
     "strassen": strassen,

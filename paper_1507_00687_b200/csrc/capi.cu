@@ -97,6 +97,12 @@ NcclApi* nccl() {
 struct fmm_plan {
   int dtype = FMM_F64, leaf = FMM_LEAF_NATIVE, L = 0;
   int64_t M = 0, K = 0, N = 0;
+  // zero padding: the recursion runs on Mp x Kp x Np, the smallest multiples of
+  // prod m0, prod k0, prod n0; A, B are copied into zero-padded workspace buffers and C is
+  // cropped back.  padded = false when the dims already divide.
+  int64_t Mp = 0, Kp = 0, Np = 0;
+  bool padded = false;
+  size_t pad_bytes = 0;
   std::vector<RuleData> rules;              // distinct rules
   std::vector<std::vector<int>> node_rule;  // per level, rule index per node (BFS)
   std::vector<int64_t> lm, lk, ln;          // node dims at level l (l = 0..L)
@@ -280,13 +286,19 @@ struct Builder {
     p->steps.push_back(st);
   }
 
-  // Is the leaf-parent level fused (K2F) for `nparents` parents?  FP64 only; auto mode fuses
-  // when the fused grid (parents x 128x128 output tiles of a leaf) fills the GPU several times.
+  // Is the leaf-parent level fused (K2F) for `nparents` parents?  FP64 only.  A fused CTA runs
+  // all R products of its parent, so the fused grid has R times fewer, R times longer CTAs
+  // than the unfused leaf GEMM; auto mode fuses when that grid (parents x 128x128 output tiles
+  // of a leaf, one CTA per SM) still fills the 148 SMs in >= 4 waves at >= 90 % wave
+  // efficiency (measured: profiles/r01_fusion.md).
   bool fuse_leaves(int64_t nparents) const {
     if (p->dtype != FMM_F64 || p->fusion == 0) return false;
     if (p->fusion == 1) return true;
+    constexpr int64_t kSMs = 148;
     const int64_t tiles = ((p->lm[p->L] + 127) / 128) * ((p->ln[p->L] + 127) / 128);
-    return nparents * tiles >= 4 * 148;
+    const int64_t units = nparents * tiles;
+    const int64_t waves = (units + kSMs - 1) / kSMs;
+    return waves >= 4 && units * 10 >= waves * kSMs * 9;
   }
 
   // K2F over parents at level l with their leaf children `kids` (R per parent, in order; or
@@ -376,7 +388,7 @@ struct Builder {
         std::vector<ZeroNode> z{ZeroNode{root.c, 1u, 0}};
         Step st{};
         st.kind = STEP_ZERO; st.count = 1; st.dev_off = push(z);
-        st.rows = p->M; st.cols = p->N; st.P = 1; st.Q = 1; st.R = 1;
+        st.rows = p->lm[0]; st.cols = p->ln[0]; st.P = 1; st.Q = 1; st.R = 1;
         p->steps.push_back(st);
       }
       return;
@@ -459,6 +471,13 @@ fmm_status compile_plan(fmm_plan* p) {
   Builder b(p);
   b.build();
   p->fmm_ws_bytes = (size_t)b.ws_peak * elem_size(p->dtype);
+  p->pad_bytes = 0;
+  if (p->padded) {
+    auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t es = (size_t)elem_size(p->dtype);
+    p->pad_bytes = al((size_t)p->Mp * p->Kp * es) + al((size_t)p->Kp * p->Np * es) +
+                   al((size_t)p->Mp * p->Np * es);
+  }
   p->desc_bytes = b.desc.size();
   p->launches = (int64_t)p->steps.size();
   if (p->scaling.mode != FMM_SCALE_NONE) {
@@ -473,6 +492,7 @@ fmm_status compile_plan(fmm_plan* p) {
     p->scale_bytes = 0;
   }
   if (p->nranks > 1 && p->comm) p->launches += 1;
+  if (p->padded) p->launches += 3;  // pad A, pad B, crop C
   // vector-path feasibility of all plan-internal dims (caller lds / pointers checked at run)
   const int vec = 16 / elem_size(p->dtype);
   p->dims_vec_ok = true;
@@ -775,15 +795,19 @@ fmm_status fmm_plan_create(const fmm_rule* const* nodes, int n_nodes, int levels
   }
   if (!uniform && idx != n_nodes && levels > 0) { delete p; set_error("fmm_plan_create: node count mismatch"); return FMM_E_ARG; }
   (void)total;
-  p->lm.push_back(M); p->lk.push_back(K); p->ln.push_back(N);
+  // pad_dims: smallest multiples of prod m0, prod k0, prod n0
+  int64_t pm = 1, pk = 1, pn = 1;
   for (int l = 0; l < levels; ++l) {
     const RuleData& r = p->rules[p->node_rule[l][0]];
-    if (p->lm[l] % r.m0 || p->lk[l] % r.k0 || p->ln[l] % r.n0) {
-      char buf[160];
-      snprintf(buf, sizeof buf, "fmm_plan_create: level %d dims (%lld,%lld,%lld) not divisible by (%d,%d,%d)", l,
-               (long long)p->lm[l], (long long)p->lk[l], (long long)p->ln[l], r.m0, r.k0, r.n0);
-      delete p; set_error(buf); return FMM_E_SHAPE;
-    }
+    pm *= r.m0; pk *= r.k0; pn *= r.n0;
+  }
+  p->Mp = (M + pm - 1) / pm * pm;
+  p->Kp = (K + pk - 1) / pk * pk;
+  p->Np = (N + pn - 1) / pn * pn;
+  p->padded = p->Mp != M || p->Kp != K || p->Np != N;
+  p->lm.push_back(p->Mp); p->lk.push_back(p->Kp); p->ln.push_back(p->Np);
+  for (int l = 0; l < levels; ++l) {
+    const RuleData& r = p->rules[p->node_rule[l][0]];
     p->lm.push_back(p->lm[l] / r.m0); p->lk.push_back(p->lk[l] / r.k0); p->ln.push_back(p->ln[l] / r.n0);
   }
   // coefficient tables
@@ -840,7 +864,7 @@ fmm_status fmm_plan_owned(const fmm_plan* p, int rank, int nranks, int32_t* owne
 
 fmm_status fmm_plan_workspace_bytes(const fmm_plan* p, size_t* bytes) {
   if (!p || !bytes) { set_error("fmm_plan_workspace_bytes: null"); return FMM_E_ARG; }
-  *bytes = p->scale_bytes + p->fmm_ws_bytes + 256;
+  *bytes = p->scale_bytes + p->pad_bytes + p->fmm_ws_bytes + 256;
   return FMM_OK;
 }
 
@@ -926,7 +950,8 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
   cudaStream_t st = (cudaStream_t)stream;
   uint8_t* wsb = (uint8_t*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
   Bases b{};
-  b.p[BASE_A] = A; b.p[BASE_B] = B; b.p[BASE_C] = C; b.p[BASE_WS] = wsb + p->scale_bytes;
+  b.p[BASE_A] = A; b.p[BASE_B] = B; b.p[BASE_C] = C;
+  b.p[BASE_WS] = wsb + p->scale_bytes + p->pad_bytes;
   b.ld[BASE_A] = lda; b.ld[BASE_B] = ldb; b.ld[BASE_C] = ldc; b.ld[BASE_WS] = 0;
   double *dA = nullptr, *dB = nullptr;
   if (p->scaling.mode != FMM_SCALE_NONE) {
@@ -947,12 +972,37 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
     b.p[BASE_A] = Ap; b.p[BASE_B] = Bp;
     b.ld[BASE_A] = p->K; b.ld[BASE_B] = p->N;
   }
+  if (p->padded) {  // zero-padded copies of A, B; the recursion writes a padded C
+    const size_t es = (size_t)elem_size(p->dtype);
+    auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+    uint8_t* pa = wsb + p->scale_bytes;
+    uint8_t* pb = pa + al((size_t)p->Mp * p->Kp * es);
+    uint8_t* pc = pb + al((size_t)p->Kp * p->Np * es);
+    TimedLaunch tl(p, STEP_K1, st);
+    cudaError_t e = p->dtype == FMM_F64
+        ? launch_pad_copy<double>((const double*)b.p[BASE_A], p->M, p->K, b.ld[BASE_A], (double*)pa, p->Mp, p->Kp, p->Kp, st)
+        : launch_pad_copy<float>((const float*)b.p[BASE_A], p->M, p->K, b.ld[BASE_A], (float*)pa, p->Mp, p->Kp, p->Kp, st);
+    if (e == cudaSuccess)
+      e = p->dtype == FMM_F64
+          ? launch_pad_copy<double>((const double*)b.p[BASE_B], p->K, p->N, b.ld[BASE_B], (double*)pb, p->Kp, p->Np, p->Np, st)
+          : launch_pad_copy<float>((const float*)b.p[BASE_B], p->K, p->N, b.ld[BASE_B], (float*)pb, p->Kp, p->Np, p->Np, st);
+    if (e != cudaSuccess) return cuda_status(e, "fmm_execute pad");
+    b.p[BASE_A] = pa; b.p[BASE_B] = pb; b.p[BASE_C] = pc;
+    b.ld[BASE_A] = p->Kp; b.ld[BASE_B] = p->Np; b.ld[BASE_C] = p->Np;
+  }
   const int vecn = 16 / elem_size(p->dtype);
   const bool vec = p->dims_vec_ok && aligned16(b.p[BASE_A]) && aligned16(b.p[BASE_B]) &&
-                   aligned16(C) && aligned16(b.p[BASE_WS]) && b.ld[BASE_A] % vecn == 0 &&
-                   b.ld[BASE_B] % vecn == 0 && ldc % vecn == 0;
+                   aligned16(b.p[BASE_C]) && aligned16(b.p[BASE_WS]) && b.ld[BASE_A] % vecn == 0 &&
+                   b.ld[BASE_B] % vecn == 0 && b.ld[BASE_C] % vecn == 0;
   fmm_status s = p->dtype == FMM_F64 ? run_steps<double>(p, b, vec, st) : run_steps<float>(p, b, vec, st);
   if (s != FMM_OK) return s;
+  if (p->padded) {  // crop
+    TimedLaunch tl(p, STEP_K3, st);
+    cudaError_t e = p->dtype == FMM_F64
+        ? launch_pad_copy<double>((const double*)b.p[BASE_C], p->M, p->N, p->Np, (double*)C, p->M, p->N, ldc, st)
+        : launch_pad_copy<float>((const float*)b.p[BASE_C], p->M, p->N, p->Np, (float*)C, p->M, p->N, ldc, st);
+    if (e != cudaSuccess) return cuda_status(e, "fmm_execute crop");
+  }
   if (p->scaling.mode != FMM_SCALE_NONE) {
     TimedLaunch tl(p, 6, st);
     cudaError_t e = launch_unscale((double*)C, ldc, p->M, p->N, dA, dB, st);
@@ -1124,6 +1174,7 @@ static const fmm_plan* depth_first_twin(const fmm_plan* p) {
   if (!p->df_twin) {
     fmm_plan* t = new fmm_plan();
     t->dtype = p->dtype; t->leaf = p->leaf; t->L = p->L; t->M = p->M; t->K = p->K; t->N = p->N;
+    t->Mp = p->Mp; t->Kp = p->Kp; t->Np = p->Np; t->padded = p->padded;
     t->rules = p->rules; t->node_rule = p->node_rule; t->lm = p->lm; t->lk = p->lk; t->ln = p->ln;
     t->scaling = p->scaling; t->coef_U = p->coef_U; t->coef_V = p->coef_V; t->coef_W = p->coef_W;
     t->coef_host = p->coef_host; t->schedule = 2; t->fusion = p->fusion;
@@ -1143,7 +1194,7 @@ fmm_status fmm_execute_host(const fmm_plan* p, const void* A_host, int64_t lda,
   }
   if (lda < p->K || ldb < p->N || ldc < p->N) { set_error("fmm_execute_host: bad ld"); return FMM_E_ARG; }
   cudaStream_t st = (cudaStream_t)stream;
-  if (p->L > 0 && p->scaling.mode == FMM_SCALE_NONE && !(p->comm && p->nranks > 1) && p->M > 0 &&
+  if (p->L > 0 && p->scaling.mode == FMM_SCALE_NONE && !(p->comm && p->nranks > 1) && !p->padded && p->M > 0 &&
       p->N > 0 && p->K > 0) {
     const fmm_plan* q = p->groups.empty() ? depth_first_twin(p) : p;
     size_t need = 0;

@@ -163,6 +163,12 @@ cudaError_t launch_acc(const Step& s, const void* dev_nodes, const double* dev_c
 template <typename T>
 cudaError_t launch_zero(const Step& s, const void* dev_nodes, const Bases& b, cudaStream_t st);
 
+// dst (rows_p x cols_p, ldd) = src (rows x cols, lds) zero-extended (rows <= rows_p, cols <=
+// cols_p): the zero padding / cropping of non-divisible dims
+template <typename T>
+cudaError_t launch_pad_copy(const T* src, int64_t rows, int64_t cols, int64_t lds, T* dst,
+                            int64_t rows_p, int64_t cols_p, int64_t ldd, cudaStream_t st);
+
 cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
                             int64_t k, const Bases& b, bool vec, cudaStream_t st);
 cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,

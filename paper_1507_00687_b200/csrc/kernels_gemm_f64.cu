@@ -14,6 +14,7 @@
 //     (8-byte) load path serves operands whose ld / offsets are not 16-byte aligned.
 // The leaf's k-order is the tensor core's (reading A4): not the oracle's
 // sequential order, covered by the parity tolerance.
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -276,7 +277,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
 // so the read-modify-write chain of an element of C_k stays in one thread, in ascending r:
 //   c = w*m (first contribution)  |  c = c + w*m        (both rounded to nearest, no FMA)
 // exactly K3's sequence (k3_combine / k_acc), with M_r never written to memory.
-template <typename C, bool VEC>
+__device__ __forceinline__ void red_add(double* p, double v) {
+  asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(p), "d"(v) : "memory");
+}
+
+template <typename C, bool VEC, bool RED, bool FLAT>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
     k2f_gemm_f64(const FusedNode* __restrict__ nodes, const double* __restrict__ coef_all,
                  Bases bases, int64_t m, int64_t n, int64_t k, int tiles_m, int tiles_n, int P,
@@ -331,7 +336,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
 
   const int KT = max(1, (int)((k + C::BK - 1) / C::BK));  // k = 0: one zero-filled tile
   const int total = nr * KT;
-  // load stream over the flattened (product, k-tile) sequence, advanced incrementally
+  // FLAT (any KT): one load stream over the flattened (product, k-tile) sequence, advanced
+  // incrementally.  !FLAT (KT >= STAGES): per-product loops whose operand pointers are loop
+  // invariant (the hot loop is the unfused kernel's); only the last STAGES k-tiles of a product
+  // load the next product's first tiles.
   int l_kt = 0, l_ri = 0;
   const double* lA = pa[0];
   const double* lB = pb[0];
@@ -356,6 +364,26 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       const double w = wcf[kk * R + r];
       const bool first = (fmask >> kk) & 1u;
       double* ob = out + (int64_t)(kk / Q) * m * ldo + (int64_t)(kk % Q) * n;
+      if (RED && !first) {
+        // c = c + w*m as L2 reductions (RED.ADD.F64, round to nearest): no load round trip.
+        // Only this thread updates these elements, and same-address operations of one thread
+        // are applied in program order, so the per-element sequence is K3's.
+#pragma unroll
+        for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int64_t row = m0 + wm * C::WTM + i * 16 + g + h * 8;
+            if (row >= m) continue;
+#pragma unroll
+            for (int j = 0; j < C::NI; ++j) {
+              const int64_t col = n0 + wn * C::WTN + j * 8 + 2 * t;
+              double* cp = ob + row * ldo + col;
+              if (col < n) red_add(cp, __dmul_rn(w, acc[i][j][2 * h]));
+              if (col + 1 < n) red_add(cp + 1, __dmul_rn(w, acc[i][j][2 * h + 1]));
+            }
+          }
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < C::MI; ++i) {
         double2 old[2][C::NI];
@@ -403,11 +431,6 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     }
   };
 
-#pragma unroll
-  for (int s = 0; s < C::STAGES - 1; ++s) {
-    if (s < total) load_next(s);
-    cp_commit();
-  }
   constexpr int KQ = C::BK / 4;
   static_assert(KQ % 2 == 0, "even number of k-slices per stage");
   double af[2][C::MI][2], bf[2][C::NI];
@@ -423,13 +446,17 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
 #pragma unroll
     for (int j = 0; j < C::NI; ++j) bf[buf][j] = bs[kk * C::B_LD + j * 8];
   };
-  cp_wait<C::STAGES - 2>();
-  __syncthreads();
-  if (C::STAGES - 1 < total) load_next((C::STAGES - 1) % C::STAGES);
-  cp_commit();
-  load_frag(0, 0, 0);
-  int kt_in_r = 0, ri = 0;
-  for (int it = 0; it < total; ++it) {
+  auto zero_acc = [&]() {
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+  };
+  // one k-tile (global index it, ring slot it % STAGES); `refill(slot)` issues the load of
+  // k-tile it + STAGES into the slot just consumed
+  auto ktile = [&](int it, auto&& refill) {
     const int slot = it % C::STAGES;
 #pragma unroll
     for (int q = 0; q < KQ; ++q) {
@@ -437,7 +464,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       if (q == KQ - 1) {
         cp_wait<C::STAGES - 2>();
         __syncthreads();  // every warp is done reading `slot` (its last slice is in registers)
-        if (it + C::STAGES < total) load_next(slot);
+        refill(slot);
         cp_commit();
         if (it + 1 < total) load_frag(cur ^ 1, (it + 1) % C::STAGES, 0);
       } else {
@@ -448,42 +475,113 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
 #pragma unroll
         for (int j = 0; j < C::NI; ++j) dmma16n8k4(acc[i][j], af[cur][i][0], af[cur][i][1], bf[cur][j]);
     }
-    if (++kt_in_r == KT) {
+  };
+
+  if constexpr (FLAT) {
+#pragma unroll
+    for (int s = 0; s < C::STAGES - 1; ++s) {
+      if (s < total) load_next(s);
+      cp_commit();
+    }
+    cp_wait<C::STAGES - 2>();
+    __syncthreads();
+    if (C::STAGES - 1 < total) load_next((C::STAGES - 1) % C::STAGES);
+    cp_commit();
+    load_frag(0, 0, 0);
+    int kt_in_r = 0, ri = 0;
+    for (int it = 0; it < total; ++it) {
+      ktile(it, [&](int slot) { if (it + C::STAGES < total) load_next(slot); });
+      if (++kt_in_r == KT) {
+        epilogue(ri);
+        zero_acc();
+        kt_in_r = 0;
+        ++ri;
+      }
+    }
+  } else {
+    // KT >= STAGES: the prologue only touches product 0
+    {
+      const double* A = pa[0];
+      const double* B = pb[0];
+      const int64_t lda = la[0], ldb = lb[0];
+#pragma unroll
+      for (int s = 0; s < C::STAGES - 1; ++s) {
+        load_tiles<C, VEC>(As + s * C::A_STAGE, Bs + s * C::B_STAGE, A, lda, B, ldb, m, n, k, m0,
+                           n0, (int64_t)s * C::BK, tid);
+        cp_commit();
+      }
+      cp_wait<C::STAGES - 2>();
+      __syncthreads();
+      load_tiles<C, VEC>(As + (C::STAGES - 1) * C::A_STAGE, Bs + (C::STAGES - 1) * C::B_STAGE, A,
+                         lda, B, ldb, m, n, k, m0, n0, (int64_t)(C::STAGES - 1) * C::BK, tid);
+      cp_commit();
+    }
+    load_frag(0, 0, 0);
+    int it = 0;
+    for (int ri = 0; ri < nr; ++ri) {
+      const double* A = pa[ri];
+      const double* B = pb[ri];
+      const int64_t lda = la[ri], ldb = lb[ri];
+      for (int kt = 0; kt < KT - C::STAGES; ++kt, ++it)
+        ktile(it, [&](int slot) {
+          load_tiles<C, VEC>(As + slot * C::A_STAGE, Bs + slot * C::B_STAGE, A, lda, B, ldb, m, n,
+                             k, m0, n0, (int64_t)(kt + C::STAGES) * C::BK, tid);
+        });
+      // last STAGES k-tiles: prefetch the next product's first STAGES k-tiles
+      const bool more = ri + 1 < nr;
+      const double* An = more ? pa[ri + 1] : A;
+      const double* Bn = more ? pb[ri + 1] : B;
+      const int64_t ldan = more ? la[ri + 1] : lda, ldbn = more ? lb[ri + 1] : ldb;
+      for (int j = 0; j < C::STAGES; ++j, ++it)
+        ktile(it, [&](int slot) {
+          if (more)
+            load_tiles<C, VEC>(As + slot * C::A_STAGE, Bs + slot * C::B_STAGE, An, ldan, Bn, ldbn,
+                               m, n, k, m0, n0, (int64_t)j * C::BK, tid);
+        });
       epilogue(ri);
-#pragma unroll
-      for (int i = 0; i < C::MI; ++i)
-#pragma unroll
-        for (int j = 0; j < C::NI; ++j)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
-      kt_in_r = 0;
-      ++ri;
+      zero_acc();
     }
   }
   cp_wait<0>();
+}
+
+template <typename C, bool VEC, bool RED>
+cudaError_t launch_fused_kernel(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
+                                int64_t k, const double* coef, int P, int Q, int R,
+                                const Bases& b, cudaStream_t st) {
+  const int tiles_m = (int)((m + C::BM - 1) / C::BM), tiles_n = (int)((n + C::BN - 1) / C::BN);
+  dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)count);
+  const int KT = (int)std::max<int64_t>(1, (k + C::BK - 1) / C::BK);
+  auto go = [&](auto kern) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         C::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, C::THREADS, C::SMEM_BYTES, st>>>(dev_nodes, coef, b, m, n, k, tiles_m, tiles_n, P,
+                                                  Q, R);
+    return cudaGetLastError();
+  };
+  if (KT >= C::STAGES) return go(k2f_gemm_f64<C, VEC, RED, false>);
+  return go(k2f_gemm_f64<C, VEC, RED, true>);
+}
+
+int fused_red() {
+  static int v = [] {
+    const char* e = getenv("FMM_K2F_RED");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
 }
 
 template <typename C>
 cudaError_t launch_fused_cfg(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                              int64_t k, const double* coef, int P, int Q, int R, const Bases& b,
                              bool vec, cudaStream_t st) {
-  const int tiles_m = (int)((m + C::BM - 1) / C::BM), tiles_n = (int)((n + C::BN - 1) / C::BN);
-  dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)count);
-  cudaError_t e;
-  if (vec) {
-    e = cudaFuncSetAttribute(k2f_gemm_f64<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    k2f_gemm_f64<C, true><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(dev_nodes, coef, b, m, n, k,
-                                                                  tiles_m, tiles_n, P, Q, R);
-  } else {
-    e = cudaFuncSetAttribute(k2f_gemm_f64<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    k2f_gemm_f64<C, false><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(dev_nodes, coef, b, m, n, k,
-                                                                   tiles_m, tiles_n, P, Q, R);
+  if (fused_red()) {
+    return vec ? launch_fused_kernel<C, true, true>(dev_nodes, count, m, n, k, coef, P, Q, R, b, st)
+               : launch_fused_kernel<C, false, true>(dev_nodes, count, m, n, k, coef, P, Q, R, b, st);
   }
-  return cudaGetLastError();
+  return vec ? launch_fused_kernel<C, true, false>(dev_nodes, count, m, n, k, coef, P, Q, R, b, st)
+             : launch_fused_kernel<C, false, false>(dev_nodes, count, m, n, k, coef, P, Q, R, b, st);
 }
 
 template <typename C>

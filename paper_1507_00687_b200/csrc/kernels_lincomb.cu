@@ -8,6 +8,7 @@
 // each output written once per launch (the algorithmic floor).  Sums run sequentially in
 // ascending index order with explicit round-to-nearest intrinsics (no FMA contraction),
 // exactly the order of PAPER.md's sequential summation model (eqn:seq_summation_error).
+#include <algorithm>
 #include <cstdlib>
 
 #include "fmm_internal.h"
@@ -361,6 +362,28 @@ cudaError_t launch_zero(const Step& s, const void* dev_nodes, const Bases& b, cu
   return cudaGetLastError();
 }
 
+namespace {
+template <typename T>
+__global__ void k_pad_copy(const T* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+                           T* __restrict__ dst, int64_t rows_p, int64_t cols_p, int64_t ldd) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols_p) return;
+  for (int64_t i = blockIdx.y; i < rows_p; i += gridDim.y)
+    dst[i * ldd + j] = (i < rows && j < cols) ? src[i * lds + j] : (T)0;
+}
+}  // namespace
+
+template <typename T>
+cudaError_t launch_pad_copy(const T* src, int64_t rows, int64_t cols, int64_t lds, T* dst,
+                            int64_t rows_p, int64_t cols_p, int64_t ldd, cudaStream_t st) {
+  if (rows_p == 0 || cols_p == 0) return cudaSuccess;
+  dim3 grid((unsigned)((cols_p + kThreads - 1) / kThreads), (unsigned)std::min<int64_t>(rows_p, 65535));
+  k_pad_copy<T><<<grid, kThreads, 0, st>>>(src, rows, cols, lds, dst, rows_p, cols_p, ldd);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_pad_copy<double>(const double*, int64_t, int64_t, int64_t, double*, int64_t, int64_t, int64_t, cudaStream_t);
+template cudaError_t launch_pad_copy<float>(const float*, int64_t, int64_t, int64_t, float*, int64_t, int64_t, int64_t, cudaStream_t);
 template cudaError_t launch_k1<double>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);
 template cudaError_t launch_k1<float>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);
 template cudaError_t launch_k3<double>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);

@@ -143,3 +143,48 @@ def test_winograd_derived_quantities():
     q = R.quantities(R.winograd())
     assert (q.nnz, q.Q, q.E) == (42, 10, 18)
     assert q.E > 12
+
+
+# ---- App. C <4,4,2;26> ------------------------------------------------------------
+# DESIGN.md reading A27: the printed rows are a relabelling of A's, B's and C's entries; these
+# labels (found by matching each row's Brent slice) make the printed table an exact algorithm.
+APP_C_LABELS = {
+    "U": [(0, 0), (2, 0), (1, 0), (3, 0), (0, 2), (2, 2), (1, 2), (3, 2),
+          (0, 1), (2, 1), (1, 1), (3, 1), (0, 3), (2, 3), (1, 3), (3, 3)],
+    "V": [(0, 0), (1, 0), (0, 1), (1, 1), (2, 0), (3, 0), (2, 1), (3, 1)],
+    "W": [(0, 0), (1, 0), (0, 1), (1, 1), (2, 0), (3, 0), (2, 1), (3, 1)],
+}
+
+
+def app_c_442():
+    g = read_golden_matrices("app_c_442.txt")
+    return R.make_rule_labelled("app_c_442", 4, 4, 2, g["U"], g["V"], g["W"],
+                                APP_C_LABELS["U"], APP_C_LABELS["V"], APP_C_LABELS["W"],
+                                u_den=2, v_den=2)
+
+
+def test_app_c_442_printed_order_is_not_the_stated_convention():
+    g = read_golden_matrices("app_c_442.txt")
+    half = lambda X: [[Fraction(x, 2) for x in r] for r in X]
+    printed = R.make_rule("printed442", 4, 4, 2, half(g["U"]), half(g["V"]), g["W"])
+    assert len(R.brent_violations(printed)) > 0
+
+
+def test_app_c_442_relabelled_is_exact_and_matches_table1():
+    rule = app_c_442()
+    assert R.brent_violations(rule) == []
+    q = R.quantities(rule)
+    # Table 1 row <4,4,2>: R 26, nnz 257, Q 22, E 89; Ex. better_emax: E = 89
+    assert (rule.R, q.nnz, q.Q, q.E) == (26, 257, 22, 89)
+    # U and V carry +-1/2 entries, so a, b (1-norms) differ from alpha, beta (counts)
+    assert q.a != q.alpha
+
+
+def test_app_c_442_transpose_via_vec_permutation_keeps_E():
+    # <P42 V, P44 U, P24 W> is a <2,4,4> algorithm with the same E; its cyclic
+    # rotation [[V, W, U]] is the <4,2,4> row of Table 1 (Q 23, E 92; A21).
+    rule = app_c_442()
+    rot = R.make_rule("rot424", 4, 2, 4, rule.V, rule.W, rule.U)
+    assert R.brent_violations(rot) == []
+    q = R.quantities(rot)
+    assert (q.nnz, q.Q, q.E) == (257, 23, 92)
