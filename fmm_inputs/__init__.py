@@ -89,6 +89,22 @@ def draw(dist: str, M: int, K: int, N: int, seed: int):
         d4 = torch.pow(10.0, _u(g, (N,), -8.0, 8.0))
         A = (d1[:, None] * G) * d2[None, :]
         B = (d3[:, None] * H) * d4[None, :]
+    elif dist in ("paper2", "paper3"):
+        # PAPER.md Sec. 6.5 distributions 2 and 3 (distribution 1 is "u(0,1)").
+        # All entries are drawn U(0,1) (A then B, row-major); the designated blocks are then
+        # multiplied by 1/N^2 or N^2 (U(0, c) = c U(0, 1)).  Halves are taken 0-based: rows
+        # i < N/2 (top), columns j >= N/2 (right) -- DESIGN.md reading A28.
+        assert M == K == N, "the paper's distributions are square"
+        A = _u(g, (M, K), 0.0, 1.0)
+        B = _u(g, (K, N), 0.0, 1.0)
+        h = N // 2
+        small, big = 1.0 / (N * N), float(N * N)
+        if dist == "paper2":  # A: right columns small; B: top rows small (models Ex. 5.2)
+            A[:, h:] *= small
+            B[:h, :] *= small
+        else:  # A: top-right block large; B: left columns small (models Ex. 6.9)
+            A[:h, h:] *= big
+            B[:, :h] *= small
     else:
         raise ValueError(dist)
     return A.numpy(), B.numpy()

@@ -146,6 +146,29 @@ fmm_status fmm_plan_set_fusion(fmm_plan* plan, int mode);
 /* Host-only query: number of fused leaf-product launches (K2F) in the compiled schedule. */
 fmm_status fmm_plan_fused_launches(const fmm_plan* plan, int64_t* n);
 
+/* ---------------------------------------------------------------------------------------
+ * Stability analysis (host-only; Section 4)
+ * fmm_rule_quantities: nnz of U, V, W; Q = max_k q_k with q_k = gamma_k + max_r (alpha_r +
+ *   beta_r) I(w_kr != 0) (Def. prefactor); E = max_k e_k with e_k = sum_r a_r b_r
+ *   |w_kr| (Def. stability), a / b the 1-norms of U / V columns (eqn:ab).
+ *   q, e (nullable) receive the m0*n0 vectors (k row-major).
+ * fmm_plan_stability: for the plan's recursion tree, xi = max_k xi_k (the largest intermediate
+ *   growth, simplified form P:455-463; = prod E for uniform plans) and delta = max_k delta_k
+ *   (the largest accumulation error, including the leaf term K / prod K0).
+ *   uniform_bound (nullable): the Thm non_stationary_analysis factor (K/prod K0 + sum Q)
+ *   (K/prod K0) prod E for uniform plans, NaN for non-uniform ones.
+ * fmm_choose_variants: a two-level non-uniform plan -- `root` at level 1 and, at each of its R
+ *   children, one of the n_variants rules (same (m0,k0,n0,R), e.g. the Castrapel-Gustafson
+ *   variants) -- minimising xi (P:465-475's D'Alberto / <3,2,3> examples do this by
+ *   hand).  choice[r] (R entries) receives the variant index of child r; exhaustive search
+ *   (lexicographically first minimum) when n_variants^R <= 2^24, else coordinate descent.
+ * ------------------------------------------------------------------------------------- */
+fmm_status fmm_rule_quantities(const fmm_rule* rule, int64_t* nnz, double* Q, double* E, double* q,
+                               double* e);
+fmm_status fmm_plan_stability(const fmm_plan* plan, double* xi, double* delta, double* uniform_bound);
+fmm_status fmm_choose_variants(const fmm_rule* root, const fmm_rule* const* variants, int n_variants,
+                               int32_t* choice, double* xi);
+
 /* Host-only query: owned[r] = 1 if top-level product r is computed by `rank` (R entries). */
 fmm_status fmm_plan_owned(const fmm_plan* plan, int rank, int nranks, int32_t* owned, int* R);
 

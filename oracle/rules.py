@@ -314,6 +314,76 @@ def xi_nonuniform(plan_rules: list) -> Fraction:
     return max(node_vec(0, 0))
 
 
+def xi_nonuniform_full(plan_rules: list) -> Fraction:
+    """xi = max_k xi_k by the unsimplified definition: for every root-to-leaf path
+    (r_1, ..., r_L), |prod_l W^{[l]}_{k_l r_l}| * sum_{i_1..i_L} |prod_l U^{[l]}_{i_l r_l}|
+    * sum_{j_1..j_L} |prod_l V^{[l]}_{j_l r_l}|, summed over paths; k = (k_1, ..., k_L)."""
+    L = len(plan_rules)
+    paths = [((), 0)]  # (r path, node index at the current level)
+    nodes_on_path = {(): []}
+    for level in range(L):
+        nxt = []
+        for path, idx in paths:
+            rule = plan_rules[level][idx]
+            for r in range(rule.R):
+                np_ = path + (r,)
+                nodes_on_path[np_] = nodes_on_path[path] + [rule]
+                nxt.append((np_, idx * rule.R + r))
+        paths = nxt
+    kdims = [len(plan_rules[l][0].W) for l in range(L)]
+    best = Fraction(0)
+    for ks in product(*[range(d) for d in kdims]):
+        total = Fraction(0)
+        for path, _ in paths:
+            rules_ = nodes_on_path[path]
+            w = Fraction(1)
+            for rule, k, r in zip(rules_, ks, path):
+                w *= abs(rule.W[k][r])
+            if w == 0:
+                continue
+            su = Fraction(0)
+            for iis in product(*[range(len(rule.U)) for rule in rules_]):
+                t = Fraction(1)
+                for rule, i, r in zip(rules_, iis, path):
+                    t *= abs(rule.U[i][r])
+                su += t
+            sv = Fraction(0)
+            for jjs in product(*[range(len(rule.V)) for rule in rules_]):
+                t = Fraction(1)
+                for rule, j, r in zip(rules_, jjs, path):
+                    t *= abs(rule.V[j][r])
+                sv += t
+            total += w * su * sv
+        best = max(best, total)
+    return best
+
+
+def delta_nonuniform(plan_rules: list, K: int) -> Fraction:
+    """Largest accumulation error delta = max_k delta_k^{[1]}, written out as the
+    paper's recursion: delta_k^{[1]} = K/prod K0 + gamma_{k1} + max_{r1} delta_k^{[2,r1]}
+    I(W_{k1 r1} != 0); inner levels gamma_{kl} + max_{rl} delta^{[l+1,..]}_k I(.); the last level
+    gamma_{kL} + max_{rL} chi_r I(W_{kL rL} != 0), chi_r = sum over the path of alpha + beta."""
+    L = len(plan_rules)
+    pk = 1
+    for lvl in plan_rules:
+        pk *= lvl[0].k0
+    kdims = [len(plan_rules[l][0].W) for l in range(L)]
+
+    def delta(level, idx, ks, chi):
+        rule = plan_rules[level][idx]
+        qq = quantities(rule)
+        k = ks[level]
+        terms = []
+        for r in range(rule.R):
+            if rule.W[k][r] == 0:
+                continue
+            c = chi + qq.alpha[r] + qq.beta[r]
+            terms.append(c if level == L - 1 else delta(level + 1, idx * rule.R + r, ks, c))
+        return qq.gamma[k] + (max(terms) if terms else 0)
+
+    return max(Fraction(K, pk) + delta(0, 0, ks, 0) for ks in product(*[range(d) for d in kdims]))
+
+
 # ---------------------------------------------------------------------------------------------
 # Plans
 # ---------------------------------------------------------------------------------------------

@@ -3,5 +3,6 @@
 The product is the C-ABI library libfmm_b200.so (include/fmm.h) built from csrc/ for sm_100a;
 `fmm` is its thin ctypes binding.  Nothing here imports the test oracle."""
 from . import fmm  # noqa: F401
-from .fmm import (FmmError, Plan, Rule, comm_unique_id, gemm, lib, node_c, node_st,  # noqa: F401
+from .fmm import (FmmError, Plan, Rule, choose_variants, comm_unique_id, gemm, lib, node_c,  # noqa: F401
+                  node_st,
                   scale_inside, scale_outside, scale_repeated, unscale)

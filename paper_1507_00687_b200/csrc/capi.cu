@@ -1421,6 +1421,165 @@ fmm_status fmm_unscale(int dtype, int64_t M, int64_t N, void* C, int64_t ldc, co
                                     (cudaStream_t)stream), "fmm_unscale");
 }
 
+// ---- stability analysis (Sec. 4) -----------------------------------
+
+fmm_status fmm_rule_quantities(const fmm_rule* r, int64_t* nnz, double* Q, double* E, double* q,
+                               double* e) {
+  if (!r) { set_error("fmm_rule_quantities: null rule"); return FMM_E_ARG; }
+  RuleQuantities x = rule_quantities(r->d);
+  if (nnz) *nnz = x.nnz;
+  if (Q) *Q = x.Q;
+  if (E) *E = x.E;
+  if (q) std::copy(x.q.begin(), x.q.end(), q);
+  if (e) std::copy(x.e.begin(), x.e.end(), e);
+  return FMM_OK;
+}
+
+namespace {
+// xi_k over the flattened k = (k_l, ..., k_L) of the subtree rooted at node idx of level l
+// (simplified form): sum_r |w_{k_l r}| a_r b_r * child_r[rest]
+std::vector<double> xi_vec(const fmm_plan* p, int l, int64_t idx) {
+  const RuleData& ru = p->rules[p->node_rule[l][idx]];
+  const RuleQuantities q = rule_quantities(ru);
+  const double den = (double)(1 << ru.log2den);
+  const int nw = ru.m0 * ru.n0;
+  if (l == p->L - 1) {
+    std::vector<double> v(nw, 0.0);
+    for (int k = 0; k < nw; ++k)
+      for (int r = 0; r < ru.R; ++r) v[k] += std::fabs(ru.W[(size_t)k * ru.R + r] / den) * q.a[r] * q.b[r];
+    return v;
+  }
+  std::vector<double> out;
+  std::vector<std::vector<double>> child(ru.R);
+  for (int r = 0; r < ru.R; ++r) child[r] = xi_vec(p, l + 1, idx * ru.R + r);
+  const size_t rest = child[0].size();
+  out.assign((size_t)nw * rest, 0.0);
+  for (int k = 0; k < nw; ++k)
+    for (int r = 0; r < ru.R; ++r) {
+      const double c = std::fabs(ru.W[(size_t)k * ru.R + r] / den) * q.a[r] * q.b[r];
+      if (c == 0) continue;
+      for (size_t t = 0; t < rest; ++t) out[(size_t)k * rest + t] += c * child[r][t];
+    }
+  return out;
+}
+
+// delta^{[l, r_1..r_{l-1}]}_k over the flattened k = (k_l, ..., k_L); chi carries
+// sum of alpha + beta along the path from the root (the S_r / T_r additions at the leaves).
+std::vector<double> delta_vec(const fmm_plan* p, int l, int64_t idx, double chi) {
+  const RuleData& ru = p->rules[p->node_rule[l][idx]];
+  const RuleQuantities q = rule_quantities(ru);
+  const int nw = ru.m0 * ru.n0;
+  if (l == p->L - 1) {
+    std::vector<double> v(nw, 0.0);
+    for (int k = 0; k < nw; ++k) {
+      double mx = 0;
+      for (int r = 0; r < ru.R; ++r)
+        if (ru.W[(size_t)k * ru.R + r] != 0) mx = std::max(mx, chi + q.alpha[r] + q.beta[r]);
+      v[k] = q.gamma[k] + mx;
+    }
+    return v;
+  }
+  std::vector<std::vector<double>> child(ru.R);
+  for (int r = 0; r < ru.R; ++r) child[r] = delta_vec(p, l + 1, idx * ru.R + r, chi + q.alpha[r] + q.beta[r]);
+  const size_t rest = child[0].size();
+  std::vector<double> out((size_t)nw * rest, 0.0);
+  for (int k = 0; k < nw; ++k)
+    for (size_t t = 0; t < rest; ++t) {
+      double mx = 0;
+      for (int r = 0; r < ru.R; ++r)
+        if (ru.W[(size_t)k * ru.R + r] != 0) mx = std::max(mx, child[r][t]);
+      out[(size_t)k * rest + t] = q.gamma[k] + mx;
+    }
+  return out;
+}
+}  // namespace
+
+fmm_status fmm_plan_stability(const fmm_plan* p, double* xi, double* delta, double* uniform_bound) {
+  if (!p) { set_error("fmm_plan_stability: null plan"); return FMM_E_ARG; }
+  const double kl = (double)p->lk[p->L];  // K / prod K0 (padded K)
+  double x = 1.0, d = kl * 1.0;
+  if (p->L > 0) {
+    std::vector<double> xv = xi_vec(p, 0, 0);
+    x = *std::max_element(xv.begin(), xv.end());
+    std::vector<double> dv = delta_vec(p, 0, 0, 0.0);
+    d = kl + *std::max_element(dv.begin(), dv.end());
+  }
+  if (xi) *xi = x;
+  if (delta) *delta = d;
+  if (uniform_bound) {  // Thm non_stationary_analysis, uniform plans only
+    bool uniform = true;
+    double sq = 0, pe = 1;
+    for (int l = 0; l < p->L; ++l) {
+      for (int r : p->node_rule[l]) uniform = uniform && r == p->node_rule[l][0];
+      const RuleQuantities q = rule_quantities(p->rules[p->node_rule[l][0]]);
+      sq += q.Q;
+      pe *= q.E;
+    }
+    *uniform_bound = uniform ? (kl + sq) * kl * pe : std::nan("");
+  }
+  return FMM_OK;
+}
+
+fmm_status fmm_choose_variants(const fmm_rule* root, const fmm_rule* const* variants, int n_variants,
+                               int32_t* choice, double* xi_out) {
+  if (!root || !variants || n_variants < 1 || !choice) { set_error("fmm_choose_variants: bad args"); return FMM_E_ARG; }
+  const RuleData& rr = root->d;
+  for (int v = 0; v < n_variants; ++v) {
+    const RuleData& vd = variants[v]->d;
+    if (vd.m0 != rr.m0 || vd.k0 != rr.k0 || vd.n0 != rr.n0 || vd.R != rr.R) {
+      set_error("fmm_choose_variants: variants must share the root's (m0,k0,n0,R) (P:146)");
+      return FMM_E_ARG;
+    }
+  }
+  // two-level xi_k = sum_{r1} c_{k1 r1} e^{[2, r1]}_{k2}, c = |w| a b of the root
+  const RuleQuantities qr = rule_quantities(rr);
+  const double den = (double)(1 << rr.log2den);
+  const int nw = rr.m0 * rr.n0, R = rr.R;
+  std::vector<std::vector<double>> ev(n_variants);
+  for (int v = 0; v < n_variants; ++v) ev[v] = rule_quantities(variants[v]->d).e;
+  std::vector<double> c((size_t)nw * R);
+  for (int k = 0; k < nw; ++k)
+    for (int r = 0; r < R; ++r) c[(size_t)k * R + r] = std::fabs(rr.W[(size_t)k * R + r] / den) * qr.a[r] * qr.b[r];
+  auto xi_of = [&](const std::vector<int>& ch) {
+    double best = 0;
+    for (int k1 = 0; k1 < nw; ++k1)
+      for (int k2 = 0; k2 < nw; ++k2) {
+        double s = 0;
+        for (int r = 0; r < R; ++r) s += c[(size_t)k1 * R + r] * ev[ch[r]][k2];
+        best = std::max(best, s);
+      }
+    return best;
+  };
+  std::vector<int> ch(R, 0), best_ch(R, 0);
+  double best = xi_of(ch);
+  double combos = std::pow((double)n_variants, (double)R);
+  if (combos <= (double)(1 << 24)) {  // exhaustive, lexicographic (first minimum wins)
+    for (int64_t id = 1; id < (int64_t)combos; ++id) {
+      int64_t x = id;
+      for (int r = R - 1; r >= 0; --r) { ch[r] = (int)(x % n_variants); x /= n_variants; }
+      const double v = xi_of(ch);
+      if (v < best) { best = v; best_ch = ch; }
+    }
+  } else {  // coordinate descent from all-variant-0 until no single change improves
+    bool improved = true;
+    ch = best_ch;
+    while (improved) {
+      improved = false;
+      for (int r = 0; r < R; ++r)
+        for (int v = 0; v < n_variants; ++v) {
+          std::vector<int> t = ch;
+          t[r] = v;
+          const double x = xi_of(t);
+          if (x < best) { best = x; ch = t; improved = true; }
+        }
+    }
+    best_ch = ch;
+  }
+  for (int r = 0; r < R; ++r) choice[r] = best_ch[r];
+  if (xi_out) *xi_out = best;
+  return FMM_OK;
+}
+
 // ---- NCCL ----------------------------------------------------------------------------------------
 
 fmm_status fmm_comm_unique_id(void* out128) {

@@ -54,6 +54,15 @@ struct RuleData {
   }
 };
 
+// Principal quantities of a rule (Sec. 4.1): alpha / beta (nonzeros of U / V
+// columns), gamma (nonzeros of W rows), a / b (1-norms of U / V columns), q_k, Q, e_k, E, nnz.
+struct RuleQuantities {
+  std::vector<double> alpha, beta, gamma, a, b, q, e;
+  double Q = 0, E = 0;
+  int64_t nnz = 0;
+};
+RuleQuantities rule_quantities(const RuleData& d);
+
 // ---- K1: linear combinations S_r = sum_i u_ir A_i (or T_r = sum_j v_jr B_j) -------------
 // The input operand (rows*P x cols*Q) is split into P x Q sub-blocks of rows x cols; the
 // sub-block index is column-major, blk = p + P*q.  coef points at the rule's table

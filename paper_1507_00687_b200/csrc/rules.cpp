@@ -3,6 +3,8 @@
 //
 // Built-ins are written here from their product formulas (a transcription independent of the
 // test oracle's tables); the equality of the two is itself a test (tests/test_capi_host.py).
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -157,6 +159,49 @@ bool builtin_rule(const std::string& name, RuleData* out) {
   else if (name == "strassen_dalberto") *out = make_dalberto();
   else return false;
   return true;
+}
+
+}  // namespace fmm
+
+// ---------------------------------------------------------------------------------------------
+// Stability analysis of rules and plans (Sec. 4).  Host-only, double
+// arithmetic (exact here: the quantities are sums / products of small dyadic numbers).
+// ---------------------------------------------------------------------------------------------
+namespace fmm {
+
+RuleQuantities rule_quantities(const RuleData& d) {
+  RuleQuantities q;
+  const double den = (double)(1 << d.log2den);
+  const int nu = d.m0 * d.k0, nv = d.k0 * d.n0, nw = d.m0 * d.n0;
+  q.alpha.assign(d.R, 0); q.beta.assign(d.R, 0); q.a.assign(d.R, 0); q.b.assign(d.R, 0);
+  q.gamma.assign(nw, 0); q.q.assign(nw, 0); q.e.assign(nw, 0);
+  q.nnz = 0;
+  for (int r = 0; r < d.R; ++r) {
+    for (int i = 0; i < nu; ++i) {  // eqn:abg, eqn:ab: nonzeros and 1-norms of U's column r
+      const int32_t u = d.U[(size_t)i * d.R + r];
+      if (u) { q.alpha[r] += 1; q.a[r] += std::fabs(u / den); ++q.nnz; }
+    }
+    for (int j = 0; j < nv; ++j) {
+      const int32_t v = d.V[(size_t)j * d.R + r];
+      if (v) { q.beta[r] += 1; q.b[r] += std::fabs(v / den); ++q.nnz; }
+    }
+  }
+  q.Q = 0; q.E = 0;
+  for (int k = 0; k < nw; ++k) {
+    double mx = 0;
+    for (int r = 0; r < d.R; ++r) {
+      const int32_t w = d.W[(size_t)k * d.R + r];
+      if (!w) continue;
+      q.gamma[k] += 1;
+      ++q.nnz;
+      mx = std::max(mx, q.alpha[r] + q.beta[r]);
+      q.e[k] += q.a[r] * q.b[r] * std::fabs(w / den);  // Def. stability (eqn:emax)
+    }
+    q.q[k] = q.gamma[k] + mx;  // Def. prefactor (eqn:qmax)
+    q.Q = std::max(q.Q, q.q[k]);
+    q.E = std::max(q.E, q.e[k]);
+  }
+  return q;
 }
 
 }  // namespace fmm

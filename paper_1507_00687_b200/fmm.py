@@ -43,6 +43,9 @@ SIGNATURES = {
     "fmm_plan_set_partition": (_I, [_P, _I, _I]),
     "fmm_plan_set_schedule": (_I, [_P, _I]),
     "fmm_plan_set_fusion": (_I, [_P, _I]),
+    "fmm_rule_quantities": (_I, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double), _P, _P]),
+    "fmm_plan_stability": (_I, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "fmm_choose_variants": (_I, [_P, _P, _I, _P, C.POINTER(C.c_double)]),
     "fmm_plan_fused_launches": (_I, [_P, C.POINTER(C.c_int64)]),
     "fmm_plan_owned": (_I, [_P, _I, _I, _P, C.POINTER(_I)]),
     "fmm_plan_workspace_bytes": (_I, [_P, C.POINTER(_SZ)]),
@@ -169,10 +172,33 @@ class Rule:
         return dict(m0=m0.value, k0=k0.value, n0=n0.value, R=R.value, U=U, V=V, W=W,
                     log2_den=den.value)
 
+    def quantities(self):
+        """nnz, Q, E, q (m0*n0), e (m0*n0) of the rule (Sec. 4.1)."""
+        import numpy as np
+        info = self.info()
+        nw = info["m0"] * info["n0"]
+        nnz, Q, E = C.c_int64(), C.c_double(), C.c_double()
+        q, e = np.zeros(nw), np.zeros(nw)
+        _call("fmm_rule_quantities", self._h, C.byref(nnz), C.byref(Q), C.byref(E), q.ctypes.data,
+              e.ctypes.data)
+        return dict(nnz=nnz.value, Q=Q.value, E=E.value, q=q, e=e)
+
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
             _lib.fmm_rule_destroy(self._h)
             self._h = None
+
+
+def choose_variants(root: "Rule", variants: Sequence["Rule"]):
+    """Two-level plan minimising xi: (choice per child r of the root, xi) (fmm_choose_variants)."""
+    import numpy as np
+    R = root.info()["R"]
+    arr = (C.c_void_p * len(variants))(*[v._h.value for v in variants])
+    ch = np.zeros(R, np.int32)
+    xi = C.c_double()
+    _call("fmm_choose_variants", root._h, C.cast(arr, C.c_void_p), len(variants), ch.ctypes.data,
+          C.byref(xi))
+    return [int(c) for c in ch], xi.value
 
 
 def _scaling(scaling) -> Optional[fmm_scaling]:
@@ -248,6 +274,12 @@ class Plan:
         """'auto' | 'breadth' | 'depth' (top-level depth-first)."""
         _call("fmm_plan_set_schedule", self._h, {"auto": 0, "breadth": 1, "depth": 2}[schedule])
         self._ws = None
+
+    def stability(self):
+        """{'xi', 'delta', 'uniform_bound'} of the plan's recursion tree (fmm_plan_stability)."""
+        xi, de, ub = C.c_double(), C.c_double(), C.c_double()
+        _call("fmm_plan_stability", self._h, C.byref(xi), C.byref(de), C.byref(ub))
+        return {"xi": xi.value, "delta": de.value, "uniform_bound": ub.value}
 
     def set_fusion(self, mode):
         """Leaf-product epilogue fusion of the parents' W-combination: 'off' | 'on' | 'auto'."""
