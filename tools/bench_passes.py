@@ -63,6 +63,24 @@ def main():
     r = run(p, A, B, C, a.reps)
     bytes_acc = (7 + 14 + 10) * q  # read M_r x7, write 14 (nnz W), read 10 (non-first)
     out["ACC"] = {"ms": r["ACC"][0], "GBps": bytes_acc / r["ACC"][0] / 1e6, "bytes": bytes_acc}
+    del A, B, C, p
+    # K4: repeated scaling without the stop test (steps fixed) on n/4 x n/4 x n/4 FP64:
+    # initial max reductions read A, B; every step reads + writes A and B once (apply fused with
+    # the next step's reductions); the unscale reads + writes C.
+    m4 = n // 4
+    steps = 10
+    A = torch.rand(m4, m4, dtype=torch.float64, device="cuda") + 0.5
+    B = torch.rand(m4, m4, dtype=torch.float64, device="cuda") + 0.5
+    C = torch.empty(m4, m4, dtype=torch.float64, device="cuda")
+    for pow2 in (0, 1):
+        p = fb.Plan([w], m4, m4, m4, scaling={"mode": "repeated", "tau": -1.0, "max_steps": steps,
+                                              "pow2": pow2})
+        r = run(p, A, B, C, a.reps)
+        mat = m4 * m4 * 8
+        bytes_k4 = 2 * mat + steps * 4 * mat + 2 * mat
+        out[f"K4_pow2_{pow2}"] = {"ms": r["SCALE"][0], "GBps": bytes_k4 / r["SCALE"][0] / 1e6,
+                                  "bytes": bytes_k4, "steps": steps}
+        del p
     print(json.dumps(out))
 
 
