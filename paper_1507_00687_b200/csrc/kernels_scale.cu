@@ -37,13 +37,40 @@ __device__ __forceinline__ double pow2_round(double x) {
   return ldexp(1.0, below ? e - 1 : e);
 }
 
-constexpr int TX = 32, TY = 8, TR = 32, TC = 64;  // tile: 32 rows x 64 cols, 2 cols / thread
+constexpr int TX = 32, TY = 8, TR = 64, TC = 64;  // tile: 64 rows x 64 cols, 2 cols / lane
+constexpr int RU = 4;                              // rows in flight per warp
+
+// x / f, correctly rounded.  When f is an exact power of two whose reciprocal is a normal
+// double (pow2 factors, reading A7), x * (1/f) is the same real number rounded
+// once, i.e. bitwise x / f, and avoids the FP64 division sequence.
+struct Divisor {
+  double f, inv;
+  bool pow2;
+  __device__ __forceinline__ explicit Divisor(double v) : f(v) {
+    const int64_t bits = __double_as_longlong(v);
+    const int ex = (int)((bits >> 52) & 0x7ff);
+    pow2 = (bits & 0x000fffffffffffffLL) == 0 && ex >= 2 && ex <= 2045 && v > 0.0;
+    inv = pow2 ? __longlong_as_double((int64_t)(2046 - ex) << 52) : 0.0;
+  }
+  __device__ __forceinline__ double div(double x) const { return pow2 ? __dmul_rn(x, inv) : __ddiv_rn(x, f); }
+};
+
+template <int MODE>
+__device__ __forceinline__ void apply2(double& x0, double& x1, const Divisor& fr, const Divisor& fc0,
+                                       const Divisor& fc1, double m0, double m1) {
+  if (MODE == AP_ROW_DIV) { x0 = fr.div(x0); x1 = fr.div(x1); }
+  else if (MODE == AP_COL_DIV) { x0 = fc0.div(x0); x1 = fc1.div(x1); }
+  else if (MODE == AP_COL_MUL) { x0 = __dmul_rn(x0, m0); x1 = __dmul_rn(x1, m1); }
+}
 
 // dst = apply(src); row_max[i] = max_j |dst_ij|, col_max[j] = max_i |dst_ij| (atomic).
-// dst may equal src (in place) or be null (reduce only).
+// dst may equal src (in place) or be null (reduce only).  Warp w of the block handles rows
+// w, w + TY, ... of a 64 x 64 tile, RU rows at a time (their loads issued together); lane l
+// owns columns 2l, 2l+1 (16-byte accesses when VEC).
+template <int MODE, bool VEC>
 __global__ void __launch_bounds__(TX* TY)
     k_apply_reduce(const double* src, int64_t lds, double* dst, int64_t ldd,
-                   int64_t rows, int64_t cols, int mode, const double* __restrict__ f,
+                   int64_t rows, int64_t cols, const double* __restrict__ f,
                    double* __restrict__ row_max, double* __restrict__ col_max,
                    const int* __restrict__ flags) {
   if (flags && flags[F_SKIP]) return;
@@ -54,32 +81,57 @@ __global__ void __launch_bounds__(TX* TY)
   for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int64_t r0 = (tile / tiles_c) * TR, c0 = (tile % tiles_c) * TC;
     const int64_t c = c0 + 2 * tx;
+    const bool ok0 = c < cols, ok1 = c + 1 < cols;
+    Divisor fc0(1.0), fc1(1.0);
+    double m0 = 1.0, m1 = 1.0;
+    if (MODE == AP_COL_DIV || MODE == AP_COL_MUL) {
+      const double a0 = ok0 ? f[c] : 1.0, a1 = ok1 ? f[c + 1] : 1.0;
+      if (MODE == AP_COL_DIV) { fc0 = Divisor(a0); fc1 = Divisor(a1); }
+      else { m0 = a0; m1 = a1; }
+    }
     double cmax0 = 0.0, cmax1 = 0.0;
-    for (int rr = ty; rr < TR; rr += TY) {
-      const int64_t r = r0 + rr;
-      double rmax = 0.0;
-      if (r < rows) {
-        double v[2] = {0.0, 0.0};
+#pragma unroll 1
+    for (int rb = ty; rb < TR; rb += TY * RU) {
+      double x[RU][2];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t cc = c + e;
-          if (cc < cols) {
-            double x = src[r * lds + cc];
-            if (mode == AP_ROW_DIV) x = __ddiv_rn(x, f[r]);
-            else if (mode == AP_COL_DIV) x = __ddiv_rn(x, f[cc]);
-            else if (mode == AP_COL_MUL) x = __dmul_rn(x, f[cc]);
-            if (dst) dst[r * ldd + cc] = x;
-            v[e] = fabs(x);
+      for (int u = 0; u < RU; ++u) {
+        const int64_t r = r0 + rb + u * TY;
+        x[u][0] = x[u][1] = 0.0;
+        if (r < rows) {
+          const double* sp = src + r * lds + c;
+          if (VEC && ok1) {
+            const double2 v = *reinterpret_cast<const double2*>(sp);
+            x[u][0] = v.x; x[u][1] = v.y;
+          } else {
+            if (ok0) x[u][0] = sp[0];
+            if (ok1) x[u][1] = sp[1];
           }
         }
-        rmax = fmax(v[0], v[1]);
-        cmax0 = fmax(cmax0, v[0]);
-        cmax1 = fmax(cmax1, v[1]);
       }
-      // warp = one row segment of 64 columns
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-      if (tx == 0 && r < rows && row_max) atomic_max_nonneg(&row_max[r], rmax);
+      for (int u = 0; u < RU; ++u) {
+        const int64_t r = r0 + rb + u * TY;
+        if (r >= rows) continue;  // warp-uniform
+        Divisor fr(1.0);
+        if (MODE == AP_ROW_DIV) fr = Divisor(f[r]);
+        double x0 = x[u][0], x1 = x[u][1];
+        apply2<MODE>(x0, x1, fr, fc0, fc1, m0, m1);
+        if (dst) {
+          double* dp = dst + r * ldd + c;
+          if (VEC && ok1) *reinterpret_cast<double2*>(dp) = make_double2(x0, x1);
+          else {
+            if (ok0) dp[0] = x0;
+            if (ok1) dp[1] = x1;
+          }
+        }
+        const double v0 = ok0 ? fabs(x0) : 0.0, v1 = ok1 ? fabs(x1) : 0.0;
+        double rmax = fmax(v0, v1);
+        cmax0 = fmax(cmax0, v0);
+        cmax1 = fmax(cmax1, v1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+        if (tx == 0 && row_max) atomic_max_nonneg(&row_max[r], rmax);
+      }
     }
     if (col_max) {
       cm[ty][2 * tx] = cmax0;
@@ -182,14 +234,23 @@ __global__ void k_fill(double* p, int64_t n, double v) {
     p[i] = v;
 }
 
+// C_ij = (dA_i C'_ij) dB_j (reading A9); VEC: two columns per thread, 16-byte accesses
+template <bool VEC>
 __global__ void k_unscale(double* C, int64_t ldc, int64_t M, int64_t N, const double* dA,
                           const double* dB) {
-  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * (VEC ? 2 : 1);
   if (j >= N) return;
-  const double sj = dB[j];
+  const bool two = VEC && j + 1 < N;
+  const double s0 = dB[j], s1 = two ? dB[j + 1] : 0.0;
   for (int64_t i = blockIdx.y; i < M; i += gridDim.y) {
     double* c = C + i * ldc + j;
-    *c = __dmul_rn(__dmul_rn(dA[i], *c), sj);
+    const double a = dA[i];
+    if (two) {
+      const double2 v = *reinterpret_cast<const double2*>(c);
+      *reinterpret_cast<double2*>(c) = make_double2(__dmul_rn(__dmul_rn(a, v.x), s0), __dmul_rn(__dmul_rn(a, v.y), s1));
+    } else {
+      *c = __dmul_rn(__dmul_rn(a, *c), s0);
+    }
   }
 }
 
@@ -233,6 +294,24 @@ static int grid_for_pass(int64_t rows, int64_t cols) {
   return (int)(tiles < g ? (tiles > 0 ? tiles : 1) : g);
 }
 
+// one streaming pass: dst = apply(src) with the row / column max-abs of the result
+static void apply_reduce(cudaStream_t st, int mode, const double* src, int64_t lds, double* dst,
+                         int64_t ldd, int64_t rows, int64_t cols, const double* f, double* row_max,
+                         double* col_max, const int* flags) {
+  const bool vec = ((uintptr_t)src % 16 == 0) && lds % 2 == 0 &&
+                   (!dst || (((uintptr_t)dst % 16 == 0) && ldd % 2 == 0));
+  dim3 blk(TX, TY);
+  const int g = grid_for_pass(rows, cols);
+#define FMM_AR(M, V) k_apply_reduce<M, V><<<g, blk, 0, st>>>(src, lds, dst, ldd, rows, cols, f, row_max, col_max, flags)
+  switch (mode) {
+    case AP_ROW_DIV: if (vec) FMM_AR(AP_ROW_DIV, true); else FMM_AR(AP_ROW_DIV, false); break;
+    case AP_COL_DIV: if (vec) FMM_AR(AP_COL_DIV, true); else FMM_AR(AP_COL_DIV, false); break;
+    case AP_COL_MUL: if (vec) FMM_AR(AP_COL_MUL, true); else FMM_AR(AP_COL_MUL, false); break;
+    default: if (vec) FMM_AR(AP_NONE, true); else FMM_AR(AP_NONE, false); break;
+  }
+#undef FMM_AR
+}
+
 // steps: sequence of 'O'/'I' (length nsteps); test_from: index from which the stop test runs
 // (-1: never).  A_out / B_out may alias? no: they are distinct buffers (ws).
 cudaError_t run_scaling(int64_t M, int64_t K, int64_t N, const double* A, int64_t lda,
@@ -248,14 +327,11 @@ cudaError_t run_scaling(int64_t M, int64_t K, int64_t N, const double* A, int64_
   k_fill<<<64, 256, 0, st>>>(dA, M, 1.0);
   k_fill<<<64, 256, 0, st>>>(dB, N, 1.0);
   k_fill<<<64, 256, 0, st>>>(dI, K, 1.0);
-  dim3 blk(TX, TY);
   // initial reductions of A, B
   {
     double* m = v.mx[0];
-    k_apply_reduce<<<grid_for_pass(M, K), blk, 0, st>>>(A, lda, nullptr, 0, M, K, AP_NONE, nullptr,
-                                                        m, m + M, nullptr);
-    k_apply_reduce<<<grid_for_pass(K, N), blk, 0, st>>>(B, ldb, nullptr, 0, K, N, AP_NONE, nullptr,
-                                                        m + M + K, m + M + 2 * K, nullptr);
+    apply_reduce(st, AP_NONE, A, lda, nullptr, 0, M, K, nullptr, m, m + M, nullptr);
+    apply_reduce(st, AP_NONE, B, ldb, nullptr, 0, K, N, nullptr, m + M + K, m + M + 2 * K, nullptr);
   }
   const double lo_I = pow(1.0 + tau, -0.25), hi_I = pow(1.0 + tau, 0.25), lo_O = pow(1.0 + tau, -0.5);
   int t0 = -1;
@@ -271,19 +347,15 @@ cudaError_t run_scaling(int64_t M, int64_t K, int64_t N, const double* A, int64_
     if (isO) {
       k_factor_O<<<1, 1024, 0, st>>>(cur, cur + M + 2 * K, M, N, pow2, dA, dB, v.r, v.s, v.flags,
                                      test, lo_O, nxt, set);
-      k_apply_reduce<<<grid_for_pass(M, K), blk, 0, st>>>(srcA, lsa, A_out, lda_out, M, K,
-                                                          AP_ROW_DIV, v.r, nxt, nxt + M, v.flags);
-      k_apply_reduce<<<grid_for_pass(K, N), blk, 0, st>>>(srcB, lsb, B_out, ldb_out, K, N,
-                                                          AP_COL_DIV, v.s, nxt + M + K,
-                                                          nxt + M + 2 * K, v.flags);
+      apply_reduce(st, AP_ROW_DIV, srcA, lsa, A_out, lda_out, M, K, v.r, nxt, nxt + M, v.flags);
+      apply_reduce(st, AP_COL_DIV, srcB, lsb, B_out, ldb_out, K, N, v.s, nxt + M + K,
+                   nxt + M + 2 * K, v.flags);
     } else {
       k_factor_I<<<1, 1024, 0, st>>>(cur + M, cur + M + K, K, pow2, dI, v.p, v.flags, test, lo_I,
                                      hi_I, nxt, set);
-      k_apply_reduce<<<grid_for_pass(M, K), blk, 0, st>>>(srcA, lsa, A_out, lda_out, M, K,
-                                                          AP_COL_MUL, v.p, nxt, nxt + M, v.flags);
-      k_apply_reduce<<<grid_for_pass(K, N), blk, 0, st>>>(srcB, lsb, B_out, ldb_out, K, N,
-                                                          AP_ROW_DIV, v.p, nxt + M + K,
-                                                          nxt + M + 2 * K, v.flags);
+      apply_reduce(st, AP_COL_MUL, srcA, lsa, A_out, lda_out, M, K, v.p, nxt, nxt + M, v.flags);
+      apply_reduce(st, AP_ROW_DIV, srcB, lsb, B_out, ldb_out, K, N, v.p, nxt + M + K,
+                   nxt + M + 2 * K, v.flags);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
@@ -294,8 +366,11 @@ cudaError_t run_scaling(int64_t M, int64_t K, int64_t N, const double* A, int64_
 cudaError_t launch_unscale(double* C, int64_t ldc, int64_t M, int64_t N, const double* dA,
                            const double* dB, cudaStream_t st) {
   if (M == 0 || N == 0) return cudaSuccess;
-  dim3 grid((unsigned)((N + 255) / 256), (unsigned)(M < 2048 ? M : 2048));
-  k_unscale<<<grid, 256, 0, st>>>(C, ldc, M, N, dA, dB);
+  const bool vec = ((uintptr_t)C % 16 == 0) && ldc % 2 == 0;
+  const int64_t per = vec ? 2 : 1;
+  dim3 grid((unsigned)((N + 256 * per - 1) / (256 * per)), (unsigned)(M < 2048 ? M : 2048));
+  if (vec) k_unscale<true><<<grid, 256, 0, st>>>(C, ldc, M, N, dA, dB);
+  else k_unscale<false><<<grid, 256, 0, st>>>(C, ldc, M, N, dA, dB);
   return cudaGetLastError();
 }
 

@@ -37,11 +37,19 @@ def main():
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--thin", type=int, default=256)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--only", default="", help="k4: only the scaling passes")
     a = ap.parse_args()
     n, t = a.n, a.thin
     w = fb.Rule.builtin("winograd")
     out = {"K1_variant": os.environ.get("FMM_K1_VARIANT", "default")}
     q = (n // 2) ** 2 * 8  # bytes of one quarter block of the big operand
+    if a.only != "k4":
+        passes_k1_k3(a, n, t, w, q, out)
+    k4(a, n, w, out)
+    print(json.dumps(out))
+
+
+def passes_k1_k3(a, n, t, w, q, out):
     # K1: A is n x n, B is n x t (S-W: all 4 A blocks needed, 4 non-trivial S; same for T)
     A = torch.rand(n, n, dtype=torch.float64, device="cuda")
     B = torch.rand(n, t, dtype=torch.float64, device="cuda")
@@ -56,6 +64,7 @@ def main():
     B = torch.rand(t, n, dtype=torch.float64, device="cuda")
     C = torch.empty(n, n, dtype=torch.float64, device="cuda")
     p = fb.Plan([w], n, t, n)
+    p.set_fusion("off")  # time the K3 pass itself
     r = run(p, A, B, C, a.reps)
     bytes_k3 = 11 * q
     out["K3"] = {"ms": r["K3"][0], "GBps": bytes_k3 / r["K3"][0] / 1e6, "bytes": bytes_k3}
@@ -63,11 +72,17 @@ def main():
     r = run(p, A, B, C, a.reps)
     bytes_acc = (7 + 14 + 10) * q  # read M_r x7, write 14 (nnz W), read 10 (non-first)
     out["ACC"] = {"ms": r["ACC"][0], "GBps": bytes_acc / r["ACC"][0] / 1e6, "bytes": bytes_acc}
-    del A, B, C, p
+
+
+def k4(a, n, w, out):
     # K4: repeated scaling without the stop test (steps fixed) on n/4 x n/4 x n/4 FP64:
     # initial max reductions read A, B; every step reads + writes A and B once (apply fused with
     # the next step's reductions); the unscale reads + writes C.
-    m4 = n // 4
+    for m4 in sorted({n // 4, n}):
+        k4_size(a, m4, w, out)
+
+
+def k4_size(a, m4, w, out):
     steps = 10
     A = torch.rand(m4, m4, dtype=torch.float64, device="cuda") + 0.5
     B = torch.rand(m4, m4, dtype=torch.float64, device="cuda") + 0.5
@@ -78,10 +93,9 @@ def main():
         r = run(p, A, B, C, a.reps)
         mat = m4 * m4 * 8
         bytes_k4 = 2 * mat + steps * 4 * mat + 2 * mat
-        out[f"K4_pow2_{pow2}"] = {"ms": r["SCALE"][0], "GBps": bytes_k4 / r["SCALE"][0] / 1e6,
+        out[f"K4_{m4}_pow2_{pow2}"] = {"ms": r["SCALE"][0], "GBps": bytes_k4 / r["SCALE"][0] / 1e6,
                                   "bytes": bytes_k4, "steps": steps}
         del p
-    print(json.dumps(out))
 
 
 if __name__ == "__main__":
