@@ -278,6 +278,8 @@ def run_fmm(args):
         scaling = {"mode": args.scaling, "tau": 1.0, "max_steps": 20, "pow2": 1}
     plan = fb.Plan([fb.Rule.builtin(r) for r in rules], M, K, N, dtype=args.dtype, leaf=leaf,
                    scaling=scaling)
+    if ws > 1 and args.shard_depth > 1:
+        plan.set_shard_depth(args.shard_depth)
     if ws > 1:
         uid = [fb.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, 0)
@@ -437,7 +439,8 @@ def run_fmm(args):
                                    f"N={N} {args.dtype.upper()}, {cfgd.dist} seed {cfgd.seed} "
                                    f"(BASELINE configs[{ {'C1': 0, 'C2': 1, 'C2c': 1, 'C3': 2, 'C4': 3, 'C5': 4}[args.config] }])"
                                    + (f", scaling {args.scaling} (pow2, tau=1)" if args.scaling != "none" else ""),
-                       "parallelism": f"top-level r round-robin over {ws} GPU(s)"
+                       "parallelism": (f"top-level r round-robin over {ws} GPU(s)" if args.shard_depth == 1
+                                       else f"depth-{args.shard_depth} paths round-robin over {ws} GPU(s)")
                                       + (", ncclReduce of C" if ws > 1 else ""),
                        "l2": ("operands %.1f GiB each > 126 MB L2 (no flush needed)" % (M * K * esz / 2**30))
                   if not small else "L2 flushed (256 MB write) between timed steps, outside the events",
@@ -466,6 +469,8 @@ def main():
                     help="CUDA-graph replay of each step (auto: on for problems <= 4096^3)")
     ap.add_argument("--scaling", default="none",
                     choices=["none", "outside", "inside", "out_in", "in_out", "repeated"])
+    ap.add_argument("--shard-depth", type=int, default=1,
+                    help="multi-GPU units = paths of the first d levels (fmm_plan_set_shard_depth)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-warmup", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -169,7 +169,18 @@ fmm_status fmm_plan_stability(const fmm_plan* plan, double* xi, double* delta, d
 fmm_status fmm_choose_variants(const fmm_rule* root, const fmm_rule* const* variants, int n_variants,
                                int32_t* choice, double* xi);
 
-/* Host-only query: owned[r] = 1 if top-level product r is computed by `rank` (R entries). */
+/* Finer multi-GPU sharding (host-only): the units of the partition are the paths
+ * (r_1, ..., r_d) of the first d = depth levels of the recursion tree (BFS order; d = 1, the
+ * default, is the top-level products), unit u going to rank u mod nranks.  A rank forms, depth-
+ * first, only the S / T it needs on the way to its units and accumulates the partial
+ * C = sum over its units of the W-weighted products (every level's W applied, r ascending);
+ * the ranks' partials sum to A.B (linearity of Eq. eqn:recursive_alg).  With R = 7, d = 2
+ * gives 49 units (98 / 94 / 88 % balance at 2 / 4 / 8 ranks), d = 3 gives 343 (99.7 % at 8).
+ * 1 <= depth <= levels. */
+fmm_status fmm_plan_set_shard_depth(fmm_plan* plan, int depth);
+
+/* Host-only query: owned[u] = 1 if shard unit u is computed by `rank`; *R receives the number
+ * of units (the top-level rank R at shard depth 1). */
 fmm_status fmm_plan_owned(const fmm_plan* plan, int rank, int nranks, int32_t* owned, int* R);
 
 /* Device workspace (bytes) fmm_execute needs for this plan (and its current partition). */

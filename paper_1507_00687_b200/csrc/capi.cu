@@ -110,6 +110,7 @@ struct fmm_plan {
   int rank = 0, nranks = 1;
   int schedule = 0;  // 0 auto, 1 breadth-first, 2 depth-first top level
   int fusion = 2;    // W-combination of the leaves' parents in the leaf GEMM epilogue: 0 off, 1 on, 2 auto
+  int shard_depth = 1;  // multi-GPU: units = paths of the first shard_depth levels, round-robin
   ncclComm_t comm = nullptr;
   // compiled schedule
   std::vector<Step> steps;
@@ -407,47 +408,71 @@ struct Builder {
       breadth_first(0, {root});
       return;
     }
-    const RuleData& ru = rule_at(0, 0);
+    depth_first(0, root, 0);
+  }
+
+  // Number of shard units below one node of level l (product of the ranks of levels l ..
+  // shard_depth - 1); units are the paths (r_1, ..., r_d) of the first d = shard_depth levels
+  // in BFS order, unit u belongs to rank u mod nranks.
+  int64_t unit_span(int l) const {
+    int64_t s = 1;
+    for (int q = l; q < p->shard_depth; ++q) s *= p->rules[p->node_rule[q][0]].R;
+    return s;
+  }
+  bool owns_subtree(int level, int64_t unit_prefix) const {
+    if (p->nranks == 1) return true;
+    const int64_t span = unit_span(level);  // units below this node
+    if (span >= p->nranks) return true;
+    const int64_t u0 = unit_prefix * span;
+    for (int64_t u = u0; u < u0 + span; ++u)
+      if (u % p->nranks == p->rank) return true;
+    return false;
+  }
+
+  // Depth-first over the products r of `node` (level l), accumulating C_k (+)= w_kr M_r into
+  // node.c in ascending r; recursion continues depth-first down to the shard depth, then each
+  // owned subtree runs breadth-first.  Children's workspace is reused across r (one stream).
+  void depth_first(int l, const Node& node, int64_t unit_prefix) {
+    const RuleData& ru = rule_at(l, node.idx);
     uint32_t started = 0;
     const int64_t mark = ws_elems;
+    const bool leaf_next = l + 1 == p->L;
     for (int r = 0; r < ru.R; ++r) {
-      if (r % p->nranks != p->rank) continue;
+      const int64_t unit = unit_prefix * ru.R + r;
+      if (!owns_subtree(l + 1, unit)) continue;
       ws_elems = mark;  // subtrees run one after another on one stream: reuse the workspace
       const size_t g0 = p->steps.size();
-      const bool fuse1 = p->L == 1 && fuse_leaves(1);
-      std::vector<Node> kid = emit_k1(0, {root}, r, !fuse1);
+      const bool fuse1 = leaf_next && fuse_leaves(1);
+      std::vector<Node> kid = emit_k1(l, {node}, r, !fuse1);
       if (fuse1) {
-        emit_k2f(0, {root}, kid, r, &started);
-        p->groups.push_back({r, g0, p->steps.size()});
-        continue;
-      }
-      if (p->L > 1) {
-        breadth_first(1, kid);
+        emit_k2f(l, {node}, kid, r, &started);
       } else {
-        emit_k2(kid);
+        if (leaf_next) emit_k2(kid);
+        else if (l + 1 < p->shard_depth && p->nranks > 1) depth_first(l + 1, kid[0], unit);
+        else breadth_first(l + 1, kid);
+        AccNode a{};
+        a.out = node.c;
+        a.in = kid[0].c;
+        a.coef_off = p->coef_W[p->node_rule[l][node.idx]];
+        a.r = r;
+        for (int k = 0; k < ru.m0 * ru.n0; ++k)
+          if (ru.W[(size_t)k * ru.R + r] != 0 && !((started >> k) & 1u)) {
+            a.first_mask |= 1u << k;
+            started |= 1u << k;
+          }
+        Step st{};
+        st.kind = STEP_ACC; st.count = 1; st.dev_off = push(std::vector<AccNode>{a});
+        st.rows = p->lm[l + 1]; st.cols = p->ln[l + 1]; st.P = ru.m0; st.Q = ru.n0; st.R = ru.R;
+        p->steps.push_back(st);
       }
-      AccNode a{};
-      a.out = root.c;
-      a.in = kid[0].c;
-      a.coef_off = p->coef_W[p->node_rule[0][0]];
-      a.r = r;
-      for (int k = 0; k < ru.m0 * ru.n0; ++k)
-        if (ru.W[(size_t)k * ru.R + r] != 0 && !((started >> k) & 1u)) {
-          a.first_mask |= 1u << k;
-          started |= 1u << k;
-        }
-      Step st{};
-      st.kind = STEP_ACC; st.count = 1; st.dev_off = push(std::vector<AccNode>{a});
-      st.rows = p->lm[1]; st.cols = p->ln[1]; st.P = ru.m0; st.Q = ru.n0; st.R = ru.R;
-      p->steps.push_back(st);
-      p->groups.push_back({r, g0, p->steps.size()});
+      if (l == 0) p->groups.push_back({r, g0, p->steps.size()});
     }
     const uint32_t all = (ru.m0 * ru.n0 >= 32) ? 0xffffffffu : ((1u << (ru.m0 * ru.n0)) - 1u);
     if ((started & all) != all) {
-      std::vector<ZeroNode> z{ZeroNode{root.c, all & ~started, 0}};
+      std::vector<ZeroNode> z{ZeroNode{node.c, all & ~started, 0}};
       Step st{};
       st.kind = STEP_ZERO; st.count = 1; st.dev_off = push(z);
-      st.rows = p->lm[1]; st.cols = p->ln[1]; st.P = ru.m0; st.Q = ru.n0; st.R = ru.R;
+      st.rows = p->lm[l + 1]; st.cols = p->ln[l + 1]; st.P = ru.m0; st.Q = ru.n0; st.R = ru.R;
       p->steps.push_back(st);
     }
   }
@@ -853,12 +878,22 @@ fmm_status fmm_plan_fused_launches(const fmm_plan* p, int64_t* n) {
   return FMM_OK;
 }
 
+fmm_status fmm_plan_set_shard_depth(fmm_plan* p, int depth) {
+  if (!p || depth < 1 || (p->L > 0 && depth > p->L)) { set_error("fmm_plan_set_shard_depth: depth must be in [1, L]"); return FMM_E_ARG; }
+  int64_t units = 1;
+  for (int l = 0; l < depth && l < p->L; ++l) units *= p->rules[p->node_rule[l][0]].R;
+  if (units > (1 << 20)) { set_error("fmm_plan_set_shard_depth: too many units"); return FMM_E_ARG; }
+  p->shard_depth = depth;
+  return compile_plan(p);
+}
+
 fmm_status fmm_plan_owned(const fmm_plan* p, int rank, int nranks, int32_t* owned, int* R) {
   if (!p || nranks < 1 || rank < 0 || rank >= nranks) { set_error("fmm_plan_owned: bad args"); return FMM_E_ARG; }
-  int RR = p->L > 0 ? p->rules[p->node_rule[0][0]].R : 1;
-  if (R) *R = RR;
+  int64_t units = 1;
+  for (int l = 0; l < p->shard_depth && l < p->L; ++l) units *= p->rules[p->node_rule[l][0]].R;
+  if (R) *R = (int)units;
   if (owned)
-    for (int r = 0; r < RR; ++r) owned[r] = (p->L > 0 ? (r % nranks == rank) : (rank == 0)) ? 1 : 0;
+    for (int64_t u = 0; u < units; ++u) owned[u] = (p->L > 0 ? (u % nranks == rank) : (rank == 0)) ? 1 : 0;
   return FMM_OK;
 }
 
@@ -1177,7 +1212,7 @@ static const fmm_plan* depth_first_twin(const fmm_plan* p) {
     t->Mp = p->Mp; t->Kp = p->Kp; t->Np = p->Np; t->padded = p->padded;
     t->rules = p->rules; t->node_rule = p->node_rule; t->lm = p->lm; t->lk = p->lk; t->ln = p->ln;
     t->scaling = p->scaling; t->coef_U = p->coef_U; t->coef_V = p->coef_V; t->coef_W = p->coef_W;
-    t->coef_host = p->coef_host; t->schedule = 2; t->fusion = p->fusion;
+    t->coef_host = p->coef_host; t->schedule = 2; t->fusion = p->fusion; t->shard_depth = p->shard_depth;
     if (compile_plan(t) != FMM_OK) { delete t; return nullptr; }
     p->df_twin = t;
   }

@@ -682,6 +682,9 @@ cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t
   switch (fused_variant()) {
     case 13: return launch_fused_cfg<V13>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
     case 15: return launch_fused_cfg<V15>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
+    case 17: return launch_fused_cfg<V17>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
+    case 18: return launch_fused_cfg<V18>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
+    case 20: return launch_fused_cfg<V20>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
     default: return launch_fused_cfg<V16>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
   }
 }

@@ -37,7 +37,7 @@ __device__ __forceinline__ double pow2_round(double x) {
   return ldexp(1.0, below ? e - 1 : e);
 }
 
-constexpr int TX = 32, TY = 8, TR = 64, TC = 64;  // tile: 64 rows x 64 cols, 2 cols / lane
+constexpr int TX = 32, TY = 8, TC = 64;  // 64-column strips, 2 columns per lane
 constexpr int RU = 4;                              // rows in flight per warp
 
 // x / f, correctly rounded.  When f is an exact power of two whose reciprocal is a normal
@@ -64,90 +64,88 @@ __device__ __forceinline__ void apply2(double& x0, double& x1, const Divisor& fr
 }
 
 // dst = apply(src); row_max[i] = max_j |dst_ij|, col_max[j] = max_i |dst_ij| (atomic).
-// dst may equal src (in place) or be null (reduce only).  Warp w of the block handles rows
-// w, w + TY, ... of a 64 x 64 tile, RU rows at a time (their loads issued together); lane l
-// owns columns 2l, 2l+1 (16-byte accesses when VEC).
+// dst may equal src (in place) or be null (reduce only).  Block (x, y) owns the 64-column strip
+// x and the row chunk y; warp w handles rows w, w + TY, ... of the chunk, RU rows at a time
+// (their loads issued together), lane l owns columns 2l, 2l+1 (16-byte accesses when VEC).
+// Column maxima stay in registers over the whole chunk: one shared-memory combine and one
+// atomic per column per block at the end, no block barrier inside the stream.
 template <int MODE, bool VEC>
-__global__ void __launch_bounds__(TX* TY)
+__global__ void __launch_bounds__(TX* TY, 4)
     k_apply_reduce(const double* src, int64_t lds, double* dst, int64_t ldd,
-                   int64_t rows, int64_t cols, const double* __restrict__ f,
+                   int64_t rows, int64_t cols, int64_t chunk, const double* __restrict__ f,
                    double* __restrict__ row_max, double* __restrict__ col_max,
                    const int* __restrict__ flags) {
   if (flags && flags[F_SKIP]) return;
   __shared__ double cm[TY][TC];
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int64_t tiles_c = (cols + TC - 1) / TC;
-  const int64_t tiles = ((rows + TR - 1) / TR) * tiles_c;
-  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const int64_t r0 = (tile / tiles_c) * TR, c0 = (tile % tiles_c) * TC;
-    const int64_t c = c0 + 2 * tx;
-    const bool ok0 = c < cols, ok1 = c + 1 < cols;
-    Divisor fc0(1.0), fc1(1.0);
-    double m0 = 1.0, m1 = 1.0;
-    if (MODE == AP_COL_DIV || MODE == AP_COL_MUL) {
-      const double a0 = ok0 ? f[c] : 1.0, a1 = ok1 ? f[c + 1] : 1.0;
-      if (MODE == AP_COL_DIV) { fc0 = Divisor(a0); fc1 = Divisor(a1); }
-      else { m0 = a0; m1 = a1; }
-    }
-    double cmax0 = 0.0, cmax1 = 0.0;
+  const int64_t c = (int64_t)blockIdx.x * TC + 2 * tx;
+  const int64_t rbeg = (int64_t)blockIdx.y * chunk;
+  const int64_t rend = rbeg + chunk < rows ? rbeg + chunk : rows;
+  const bool ok0 = c < cols, ok1 = c + 1 < cols;
+  Divisor fc0(1.0), fc1(1.0);
+  double m0 = 1.0, m1 = 1.0;
+  if (MODE == AP_COL_DIV || MODE == AP_COL_MUL) {
+    const double a0 = ok0 ? f[c] : 1.0, a1 = ok1 ? f[c + 1] : 1.0;
+    if (MODE == AP_COL_DIV) { fc0 = Divisor(a0); fc1 = Divisor(a1); }
+    else { m0 = a0; m1 = a1; }
+  }
+  double cmax0 = 0.0, cmax1 = 0.0;
 #pragma unroll 1
-    for (int rb = ty; rb < TR; rb += TY * RU) {
-      double x[RU][2];
+  for (int64_t rb = rbeg + ty; rb < rend; rb += TY * RU) {
+    double x[RU][2];
 #pragma unroll
-      for (int u = 0; u < RU; ++u) {
-        const int64_t r = r0 + rb + u * TY;
-        x[u][0] = x[u][1] = 0.0;
-        if (r < rows) {
-          const double* sp = src + r * lds + c;
-          if (VEC && ok1) {
-            const double2 v = *reinterpret_cast<const double2*>(sp);
-            x[u][0] = v.x; x[u][1] = v.y;
-          } else {
-            if (ok0) x[u][0] = sp[0];
-            if (ok1) x[u][1] = sp[1];
-          }
+    for (int u = 0; u < RU; ++u) {
+      const int64_t r = rb + u * TY;
+      x[u][0] = x[u][1] = 0.0;
+      if (r < rend) {
+        const double* sp = src + r * lds + c;
+        if (VEC && ok1) {
+          const double2 v = *reinterpret_cast<const double2*>(sp);
+          x[u][0] = v.x; x[u][1] = v.y;
+        } else {
+          if (ok0) x[u][0] = sp[0];
+          if (ok1) x[u][1] = sp[1];
         }
-      }
-#pragma unroll
-      for (int u = 0; u < RU; ++u) {
-        const int64_t r = r0 + rb + u * TY;
-        if (r >= rows) continue;  // warp-uniform
-        Divisor fr(1.0);
-        if (MODE == AP_ROW_DIV) fr = Divisor(f[r]);
-        double x0 = x[u][0], x1 = x[u][1];
-        apply2<MODE>(x0, x1, fr, fc0, fc1, m0, m1);
-        if (dst) {
-          double* dp = dst + r * ldd + c;
-          if (VEC && ok1) *reinterpret_cast<double2*>(dp) = make_double2(x0, x1);
-          else {
-            if (ok0) dp[0] = x0;
-            if (ok1) dp[1] = x1;
-          }
-        }
-        const double v0 = ok0 ? fabs(x0) : 0.0, v1 = ok1 ? fabs(x1) : 0.0;
-        double rmax = fmax(v0, v1);
-        cmax0 = fmax(cmax0, v0);
-        cmax1 = fmax(cmax1, v1);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-        if (tx == 0 && row_max) atomic_max_nonneg(&row_max[r], rmax);
       }
     }
-    if (col_max) {
-      cm[ty][2 * tx] = cmax0;
-      cm[ty][2 * tx + 1] = cmax1;
-      __syncthreads();
-      if (ty == 0) {
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          double mx = 0.0;
-#pragma unroll
-          for (int y = 0; y < TY; ++y) mx = fmax(mx, cm[y][2 * tx + e]);
-          const int64_t cc = c + e;
-          if (cc < cols) atomic_max_nonneg(&col_max[cc], mx);
+    for (int u = 0; u < RU; ++u) {
+      const int64_t r = rb + u * TY;
+      if (r >= rend) continue;  // warp-uniform
+      Divisor fr(1.0);
+      if (MODE == AP_ROW_DIV) fr = Divisor(f[r]);
+      double x0 = x[u][0], x1 = x[u][1];
+      apply2<MODE>(x0, x1, fr, fc0, fc1, m0, m1);
+      if (dst) {
+        double* dp = dst + r * ldd + c;
+        if (VEC && ok1) *reinterpret_cast<double2*>(dp) = make_double2(x0, x1);
+        else {
+          if (ok0) dp[0] = x0;
+          if (ok1) dp[1] = x1;
         }
       }
-      __syncthreads();
+      const double v0 = ok0 ? fabs(x0) : 0.0, v1 = ok1 ? fabs(x1) : 0.0;
+      double rmax = fmax(v0, v1);
+      cmax0 = fmax(cmax0, v0);
+      cmax1 = fmax(cmax1, v1);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+      if (tx == 0 && row_max) atomic_max_nonneg(&row_max[r], rmax);
+    }
+  }
+  if (col_max) {
+    cm[ty][2 * tx] = cmax0;
+    cm[ty][2 * tx + 1] = cmax1;
+    __syncthreads();
+    if (ty == 0) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        double mx = 0.0;
+#pragma unroll
+        for (int y = 0; y < TY; ++y) mx = fmax(mx, cm[y][2 * tx + e]);
+        const int64_t cc = c + e;
+        if (cc < cols) atomic_max_nonneg(&col_max[cc], mx);
+      }
     }
   }
 }
@@ -288,21 +286,22 @@ int* scale_flags_ptr(void* ws, int64_t M, int64_t K, int64_t N) {
   return scale_ws_view(ws, M, K, N).flags;
 }
 
-static int grid_for_pass(int64_t rows, int64_t cols) {
-  int64_t tiles = ((rows + TR - 1) / TR) * ((cols + TC - 1) / TC);
-  int64_t g = 148 * 8;
-  return (int)(tiles < g ? (tiles > 0 ? tiles : 1) : g);
-}
-
 // one streaming pass: dst = apply(src) with the row / column max-abs of the result
 static void apply_reduce(cudaStream_t st, int mode, const double* src, int64_t lds, double* dst,
                          int64_t ldd, int64_t rows, int64_t cols, const double* f, double* row_max,
                          double* col_max, const int* flags) {
   const bool vec = ((uintptr_t)src % 16 == 0) && lds % 2 == 0 &&
                    (!dst || (((uintptr_t)dst % 16 == 0) && ldd % 2 == 0));
+  if (rows == 0 || cols == 0) return;
   dim3 blk(TX, TY);
-  const int g = grid_for_pass(rows, cols);
-#define FMM_AR(M, V) k_apply_reduce<M, V><<<g, blk, 0, st>>>(src, lds, dst, ldd, rows, cols, f, row_max, col_max, flags)
+  // column strips x row chunks, ~8 blocks per SM, chunks a multiple of TY * RU rows
+  const int64_t strips = (cols + TC - 1) / TC;
+  int64_t nchunks = (148 * 8 + strips - 1) / strips;
+  int64_t chunk = (rows + nchunks - 1) / nchunks;
+  chunk = (chunk + TY * RU - 1) / (TY * RU) * (TY * RU);
+  nchunks = (rows + chunk - 1) / chunk;
+  dim3 g((unsigned)strips, (unsigned)nchunks);
+#define FMM_AR(M, V) k_apply_reduce<M, V><<<g, blk, 0, st>>>(src, lds, dst, ldd, rows, cols, chunk, f, row_max, col_max, flags)
   switch (mode) {
     case AP_ROW_DIV: if (vec) FMM_AR(AP_ROW_DIV, true); else FMM_AR(AP_ROW_DIV, false); break;
     case AP_COL_DIV: if (vec) FMM_AR(AP_COL_DIV, true); else FMM_AR(AP_COL_DIV, false); break;

@@ -43,6 +43,7 @@ SIGNATURES = {
     "fmm_plan_set_partition": (_I, [_P, _I, _I]),
     "fmm_plan_set_schedule": (_I, [_P, _I]),
     "fmm_plan_set_fusion": (_I, [_P, _I]),
+    "fmm_plan_set_shard_depth": (_I, [_P, _I]),
     "fmm_rule_quantities": (_I, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double), _P, _P]),
     "fmm_plan_stability": (_I, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "fmm_choose_variants": (_I, [_P, _P, _I, _P, C.POINTER(C.c_double)]),
@@ -290,6 +291,11 @@ class Plan:
         n = C.c_int64()
         _call("fmm_plan_fused_launches", self._h, C.byref(n))
         return n.value
+
+    def set_shard_depth(self, depth: int):
+        """Multi-GPU units = paths of the first `depth` levels (fmm_plan_set_shard_depth)."""
+        _call("fmm_plan_set_shard_depth", self._h, depth)
+        self._ws = None
 
     def owned(self, rank: int, nranks: int):
         import numpy as np

@@ -126,3 +126,16 @@ def test_fusion_auto_policy():
     assert p.workspace_bytes() > ws_fused  # leaf M_r buffers are not allocated when fused
     p32 = fb.Plan([w] * 3, 4096, 4096, 4096, dtype="f32")
     assert p32.fused_launches() == 0
+
+
+def test_shard_depth_units_and_balance():
+    # finer units improve the R = 7 balance cap 7 / (P ceil(7/P)) = 87.5 %
+    w = fb.Rule.builtin("winograd")
+    p = fb.Plan([w] * 3, 1024, 1024, 1024)
+    for depth, P, cap in ((1, 8, 7 / 8), (2, 4, 49 / (4 * 13)), (2, 2, 49 / 50), (3, 8, 343 / (8 * 43))):
+        p.set_shard_depth(depth)
+        owned = [p.owned(r, P) for r in range(P)]
+        assert sorted(u for o in owned for u in o) == list(range(7 ** depth))
+        assert abs(7 ** depth / (P * max(len(o) for o in owned)) - cap) < 1e-12
+    with pytest.raises(fb.FmmError):
+        p.set_shard_depth(4)

@@ -143,3 +143,24 @@ def test_fused_C2_full_size_equals_unfused(fb):
     Cf = exe(pa, A, B)
     Cu = exe(plan(fb, ("strassen",) * 4, 4096, 4096, 4096, "off"), A, B)
     assert np.array_equal(Cf, Cu)
+
+
+@pytest.mark.parametrize("depth,nranks", [(2, 2), (2, 4), (2, 8), (3, 8)])
+def test_shard_depth_virtual_ranks(fb, depth, nranks):
+    # finer sharding (units = paths of the first `depth` levels): the ranks' partial C sum to
+    # the product (parity), every unit is owned once, and rank partials are deterministic
+    A, B = fi.random_pair(256, 256, 256, seed=12)
+    names = ("winograd",) * 3
+    ref = exe(plan(fb, names, 256, 256, 256, "auto"), A, B)
+    total = np.zeros_like(ref)
+    units = []
+    for rank in range(nranks):
+        p = plan(fb, names, 256, 256, 256, "auto")
+        p.set_shard_depth(depth)
+        p.set_partition(rank, nranks)
+        units += p.owned(rank, nranks)
+        part = exe(p, A, B)
+        assert np.array_equal(part, exe(p, A, B))
+        total += part
+    assert sorted(units) == list(range(7 ** depth))
+    assert oracle.parity_metric(total, ref, np.abs(A).max(), np.abs(B).max(), 256) <= TOL64

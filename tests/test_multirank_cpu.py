@@ -44,6 +44,80 @@ def _partial_oracle(rank, nranks, owned, A, B):
     return C
 
 
+def _combine(rule, blocks_by_r, mb, nb):
+    """C = sum_r w_kr M_r over the given {r: M_r} in ascending r (oracle-side arithmetic)."""
+    Wf = rule.as_float()[2]
+    C = np.zeros((2 * mb, 2 * nb))
+    started = [False] * 4
+    for r in sorted(blocks_by_r):
+        for k in range(4):
+            if Wf[k, r] == 0:
+                continue
+            ia, jb = divmod(k, 2)
+            blk = C[ia * mb:(ia + 1) * mb, jb * nb:(jb + 1) * nb]
+            blk[...] = Wf[k, r] * blocks_by_r[r] if not started[k] else blk + Wf[k, r] * blocks_by_r[r]
+            started[k] = True
+    return C
+
+
+def _partial_oracle_depth2(owned_units, A, B):
+    """Partial C of a rank owning the depth-2 units u = 7 r1 + r2 of a 2-level S-W plan."""
+    import oracle
+    from oracle import rules as R
+    w = R.winograd()
+    leaf = R.Plan([])
+    S1, T1 = oracle.node_st(w, A, B)
+    m1 = {}
+    for r1 in range(7):
+        mine = [u % 7 for u in owned_units if u // 7 == r1]
+        if not mine:
+            continue
+        S2, T2 = oracle.node_st(w, S1[r1], T1[r1])
+        m2 = {r2: oracle.fmm(S2[r2], T2[r2], leaf) for r2 in mine}
+        m1[r1] = _combine(w, m2, A.shape[0] // 4, B.shape[1] // 4)
+    return _combine(w, m1, A.shape[0] // 2, B.shape[1] // 2)
+
+
+def _worker_depth2(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1507_00687_b200 as fb
+    w = fb.Rule.builtin("winograd")
+    plan = fb.Plan([w, w], 128, 128, 128)
+    plan.set_shard_depth(2)
+    owned = plan.owned(rank, world)
+    A, B = fi.random_pair(128, 128, 128, seed=22)
+    part = torch.from_numpy(_partial_oracle_depth2(owned, A, B))
+    dist.all_reduce(part)
+    counts = torch.zeros(49, dtype=torch.int64)
+    counts[owned] = 1
+    dist.all_reduce(counts)
+    if rank == 0:
+        out_q.put((part.numpy(), counts.numpy()))
+    dist.destroy_process_group()
+
+
+def test_two_rank_depth2_units_and_reduce():
+    # finer sharding (fmm_plan_set_shard_depth(2)): 49 units, every one owned once; the ranks'
+    # partial sums reduced by a collective equal the full product within the parity tolerance
+    import oracle
+    from oracle import rules as R
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_depth2, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    total, counts = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert counts.tolist() == [1] * 49
+    A, B = fi.random_pair(128, 128, 128, seed=22)
+    full = oracle.fmm(A, B, R.Plan.stationary(R.winograd(), 2))
+    assert oracle.parity_metric(total, full, np.abs(A).max(), np.abs(B).max(), 128) <= 1e-13
+
+
 def _worker(rank, world, port, out_q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
