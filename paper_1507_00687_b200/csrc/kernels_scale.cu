@@ -9,6 +9,7 @@
 // The stopping test of Thm stopping-criterion, from the step after the first O
 // step, runs on device; once it fires, later steps' passes exit immediately, so the
 // host never synchronises inside Alg. 3.
+#include <algorithm>
 #include <cstdint>
 
 #include "fmm_internal.h"
@@ -37,8 +38,10 @@ __device__ __forceinline__ double pow2_round(double x) {
   return ldexp(1.0, below ? e - 1 : e);
 }
 
-constexpr int TX = 32, TY = 8, TC = 64;  // 64-column strips, 2 columns per lane
-constexpr int RU = 4;                              // rows in flight per warp
+constexpr int TX = 32, TY = 8;
+constexpr int CPL = 4;         // columns per lane (two 16-byte accesses)
+constexpr int TC = TX * CPL;   // 128-column strips
+constexpr int RU = 2;          // rows in flight per warp
 
 // x / f, correctly rounded.  When f is an exact power of two whose reciprocal is a normal
 // double (pow2 factors, reading A7), x * (1/f) is the same real number rounded
@@ -52,23 +55,17 @@ struct Divisor {
     pow2 = (bits & 0x000fffffffffffffLL) == 0 && ex >= 2 && ex <= 2045 && v > 0.0;
     inv = pow2 ? __longlong_as_double((int64_t)(2046 - ex) << 52) : 0.0;
   }
+  __device__ __forceinline__ Divisor() : f(1.0), inv(1.0), pow2(true) {}
   __device__ __forceinline__ double div(double x) const { return pow2 ? __dmul_rn(x, inv) : __ddiv_rn(x, f); }
 };
 
-template <int MODE>
-__device__ __forceinline__ void apply2(double& x0, double& x1, const Divisor& fr, const Divisor& fc0,
-                                       const Divisor& fc1, double m0, double m1) {
-  if (MODE == AP_ROW_DIV) { x0 = fr.div(x0); x1 = fr.div(x1); }
-  else if (MODE == AP_COL_DIV) { x0 = fc0.div(x0); x1 = fc1.div(x1); }
-  else if (MODE == AP_COL_MUL) { x0 = __dmul_rn(x0, m0); x1 = __dmul_rn(x1, m1); }
-}
-
 // dst = apply(src); row_max[i] = max_j |dst_ij|, col_max[j] = max_i |dst_ij| (atomic).
-// dst may equal src (in place) or be null (reduce only).  Block (x, y) owns the 64-column strip
+// dst may equal src (in place) or be null (reduce only).  Block (x, y) owns the 128-column strip
 // x and the row chunk y; warp w handles rows w, w + TY, ... of the chunk, RU rows at a time
-// (their loads issued together), lane l owns columns 2l, 2l+1 (16-byte accesses when VEC).
-// Column maxima stay in registers over the whole chunk: one shared-memory combine and one
-// atomic per column per block at the end, no block barrier inside the stream.
+// (their loads issued together), lane l owns columns 2l, 2l+1 and 64+2l, 64+2l+1 (16-byte
+// accesses when VEC, each warp instruction covering 512 contiguous bytes).  Column maxima stay
+// in registers over the whole chunk: one shared-memory combine and one atomic per column per
+// block at the end, no block barrier inside the stream.
 template <int MODE, bool VEC>
 __global__ void __launch_bounds__(TX* TY, 4)
     k_apply_reduce(const double* src, int64_t lds, double* dst, int64_t ldd,
@@ -78,33 +75,50 @@ __global__ void __launch_bounds__(TX* TY, 4)
   if (flags && flags[F_SKIP]) return;
   __shared__ double cm[TY][TC];
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const int64_t c = (int64_t)blockIdx.x * TC + 2 * tx;
+  const int64_t cbase = (int64_t)blockIdx.x * TC + 2 * tx;
   const int64_t rbeg = (int64_t)blockIdx.y * chunk;
   const int64_t rend = rbeg + chunk < rows ? rbeg + chunk : rows;
-  const bool ok0 = c < cols, ok1 = c + 1 < cols;
-  Divisor fc0(1.0), fc1(1.0);
-  double m0 = 1.0, m1 = 1.0;
-  if (MODE == AP_COL_DIV || MODE == AP_COL_MUL) {
-    const double a0 = ok0 ? f[c] : 1.0, a1 = ok1 ? f[c + 1] : 1.0;
-    if (MODE == AP_COL_DIV) { fc0 = Divisor(a0); fc1 = Divisor(a1); }
-    else { m0 = a0; m1 = a1; }
+  int64_t cidx[CPL];
+  bool ok[CPL];
+#pragma unroll
+  for (int e = 0; e < CPL; ++e) {
+    cidx[e] = cbase + (e / 2) * (2 * TX) + (e & 1);
+    ok[e] = cidx[e] < cols;
   }
-  double cmax0 = 0.0, cmax1 = 0.0;
+  Divisor fcol[CPL];
+  double mcol[CPL];
+#pragma unroll
+  for (int e = 0; e < CPL; ++e) {
+    mcol[e] = 1.0;
+    if (MODE == AP_COL_DIV || MODE == AP_COL_MUL) {
+      const double v = ok[e] ? f[cidx[e]] : 1.0;
+      if (MODE == AP_COL_DIV) fcol[e] = Divisor(v);
+      else mcol[e] = v;
+    }
+  }
+  double cmax[CPL];
+#pragma unroll
+  for (int e = 0; e < CPL; ++e) cmax[e] = 0.0;
 #pragma unroll 1
   for (int64_t rb = rbeg + ty; rb < rend; rb += TY * RU) {
-    double x[RU][2];
+    double x[RU][CPL];
 #pragma unroll
     for (int u = 0; u < RU; ++u) {
       const int64_t r = rb + u * TY;
-      x[u][0] = x[u][1] = 0.0;
+#pragma unroll
+      for (int e = 0; e < CPL; ++e) x[u][e] = 0.0;
       if (r < rend) {
-        const double* sp = src + r * lds + c;
-        if (VEC && ok1) {
-          const double2 v = *reinterpret_cast<const double2*>(sp);
-          x[u][0] = v.x; x[u][1] = v.y;
-        } else {
-          if (ok0) x[u][0] = sp[0];
-          if (ok1) x[u][1] = sp[1];
+        const double* sp = src + r * lds;
+#pragma unroll
+        for (int h = 0; h < CPL / 2; ++h) {
+          const int64_t c0 = cidx[2 * h];
+          if (VEC && ok[2 * h + 1]) {
+            const double2 v = *reinterpret_cast<const double2*>(sp + c0);
+            x[u][2 * h] = v.x; x[u][2 * h + 1] = v.y;
+          } else {
+            if (ok[2 * h]) x[u][2 * h] = sp[c0];
+            if (ok[2 * h + 1]) x[u][2 * h + 1] = sp[c0 + 1];
+          }
         }
       }
     }
@@ -112,40 +126,48 @@ __global__ void __launch_bounds__(TX* TY, 4)
     for (int u = 0; u < RU; ++u) {
       const int64_t r = rb + u * TY;
       if (r >= rend) continue;  // warp-uniform
-      Divisor fr(1.0);
+      Divisor fr;
       if (MODE == AP_ROW_DIV) fr = Divisor(f[r]);
-      double x0 = x[u][0], x1 = x[u][1];
-      apply2<MODE>(x0, x1, fr, fc0, fc1, m0, m1);
+      double rmax = 0.0;
+#pragma unroll
+      for (int e = 0; e < CPL; ++e) {
+        double y = x[u][e];
+        if (MODE == AP_ROW_DIV) y = fr.div(y);
+        else if (MODE == AP_COL_DIV) y = fcol[e].div(y);
+        else if (MODE == AP_COL_MUL) y = __dmul_rn(y, mcol[e]);
+        x[u][e] = y;
+        const double v = ok[e] ? fabs(y) : 0.0;
+        rmax = fmax(rmax, v);
+        cmax[e] = fmax(cmax[e], v);
+      }
       if (dst) {
-        double* dp = dst + r * ldd + c;
-        if (VEC && ok1) *reinterpret_cast<double2*>(dp) = make_double2(x0, x1);
-        else {
-          if (ok0) dp[0] = x0;
-          if (ok1) dp[1] = x1;
+        double* dp = dst + r * ldd;
+#pragma unroll
+        for (int h = 0; h < CPL / 2; ++h) {
+          const int64_t c0 = cidx[2 * h];
+          if (VEC && ok[2 * h + 1]) {
+            *reinterpret_cast<double2*>(dp + c0) = make_double2(x[u][2 * h], x[u][2 * h + 1]);
+          } else {
+            if (ok[2 * h]) dp[c0] = x[u][2 * h];
+            if (ok[2 * h + 1]) dp[c0 + 1] = x[u][2 * h + 1];
+          }
         }
       }
-      const double v0 = ok0 ? fabs(x0) : 0.0, v1 = ok1 ? fabs(x1) : 0.0;
-      double rmax = fmax(v0, v1);
-      cmax0 = fmax(cmax0, v0);
-      cmax1 = fmax(cmax1, v1);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
       if (tx == 0 && row_max) atomic_max_nonneg(&row_max[r], rmax);
     }
   }
   if (col_max) {
-    cm[ty][2 * tx] = cmax0;
-    cm[ty][2 * tx + 1] = cmax1;
+#pragma unroll
+    for (int e = 0; e < CPL; ++e) cm[ty][(e / 2) * (2 * TX) + 2 * tx + (e & 1)] = cmax[e];
     __syncthreads();
-    if (ty == 0) {
+    for (int q = ty * TX + tx; q < TC; q += TX * TY) {
+      double mx = 0.0;
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        double mx = 0.0;
-#pragma unroll
-        for (int y = 0; y < TY; ++y) mx = fmax(mx, cm[y][2 * tx + e]);
-        const int64_t cc = c + e;
-        if (cc < cols) atomic_max_nonneg(&col_max[cc], mx);
-      }
+      for (int y = 0; y < TY; ++y) mx = fmax(mx, cm[y][q]);
+      const int64_t cc = (int64_t)blockIdx.x * TC + q;
+      if (cc < cols) atomic_max_nonneg(&col_max[cc], mx);
     }
   }
 }
@@ -294,9 +316,10 @@ static void apply_reduce(cudaStream_t st, int mode, const double* src, int64_t l
                    (!dst || (((uintptr_t)dst % 16 == 0) && ldd % 2 == 0));
   if (rows == 0 || cols == 0) return;
   dim3 blk(TX, TY);
-  // column strips x row chunks, ~8 blocks per SM, chunks a multiple of TY * RU rows
+  // column strips x row chunks: one wave of 4 resident blocks per SM, chunks a multiple of
+  // TY * RU rows
   const int64_t strips = (cols + TC - 1) / TC;
-  int64_t nchunks = (148 * 8 + strips - 1) / strips;
+  int64_t nchunks = std::max<int64_t>(1, (148 * 4) / strips);
   int64_t chunk = (rows + nchunks - 1) / nchunks;
   chunk = (chunk + TY * RU - 1) / (TY * RU) * (TY * RU);
   nchunks = (rows + chunk - 1) / chunk;
