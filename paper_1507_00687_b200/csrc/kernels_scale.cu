@@ -18,7 +18,9 @@ namespace fmm {
 
 // flags layout (int32): [0] done, [1] steps taken, [2] error kind (0 none; 1 zero row of A,
 // 2 zero col of B, 3 zero col of A, 4 zero row of B), [3] error index, [4] skip current step
-enum { F_DONE = 0, F_STEPS = 1, F_ERR = 2, F_ERRIDX = 3, F_SKIP = 4, F_COUNT = 8 };
+// [5] inexact: some factor of the current step has no exactly representable power-of-two
+// reciprocal (the multiply pass then yields to the dividing pass)
+enum { F_DONE = 0, F_STEPS = 1, F_ERR = 2, F_ERRIDX = 3, F_SKIP = 4, F_INEXACT = 5, F_COUNT = 8 };
 enum ApplyMode { AP_NONE = 0, AP_ROW_DIV = 1, AP_COL_DIV = 2, AP_COL_MUL = 3 };
 
 namespace {
@@ -71,8 +73,8 @@ __global__ void __launch_bounds__(TX* TY, 4)
     k_apply_reduce(const double* src, int64_t lds, double* dst, int64_t ldd,
                    int64_t rows, int64_t cols, int64_t chunk, const double* __restrict__ f,
                    double* __restrict__ row_max, double* __restrict__ col_max,
-                   const int* __restrict__ flags) {
-  if (flags && flags[F_SKIP]) return;
+                   const int* __restrict__ flags, int only_if_inexact) {
+  if (flags && (flags[F_SKIP] || (only_if_inexact && !flags[F_INEXACT]))) return;
   __shared__ double cm[TY][TC];
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int64_t cbase = (int64_t)blockIdx.x * TC + 2 * tx;
@@ -102,12 +104,15 @@ __global__ void __launch_bounds__(TX* TY, 4)
 #pragma unroll 1
   for (int64_t rb = rbeg + ty; rb < rend; rb += TY * RU) {
     double x[RU][CPL];
+    double frow[RU];
 #pragma unroll
     for (int u = 0; u < RU; ++u) {
       const int64_t r = rb + u * TY;
 #pragma unroll
       for (int e = 0; e < CPL; ++e) x[u][e] = 0.0;
+      frow[u] = 1.0;
       if (r < rend) {
+        if (MODE == AP_ROW_DIV) frow[u] = f[r];  // issued with the row's data loads
         const double* sp = src + r * lds;
 #pragma unroll
         for (int h = 0; h < CPL / 2; ++h) {
@@ -127,7 +132,7 @@ __global__ void __launch_bounds__(TX* TY, 4)
       const int64_t r = rb + u * TY;
       if (r >= rend) continue;  // warp-uniform
       Divisor fr;
-      if (MODE == AP_ROW_DIV) fr = Divisor(f[r]);
+      if (MODE == AP_ROW_DIV) fr = Divisor(frow[u]);
       double rmax = 0.0;
 #pragma unroll
       for (int e = 0; e < CPL; ++e) {
@@ -172,17 +177,137 @@ __global__ void __launch_bounds__(TX* TY, 4)
   }
 }
 
+// Multiply-only pass for power-of-two factors (pow2 = 1): the factor kernels store the exact
+// reciprocals 1/r, 1/s, 1/p (a power of two's reciprocal is a power of two, exact whenever it
+// is representable), so x / f = x * (1/f) bitwise and every apply is one multiplication.
+// MODE: AP_NONE (reduce only), AP_ROW_MUL (x * g_i), AP_COL_MUL (x * g_j).  Same block / warp
+// layout as k_apply_reduce with 8 columns per lane (256-column strips): half the per-element
+// cost of the row-max shuffles, 8 16-byte loads in flight per lane.  `need_exact`: return
+// unless every factor of this step had an exact reciprocal (flags[F_INEXACT] == 0).
+constexpr int CPL8 = 8, TC8 = TX * CPL8, RU8 = 2;
+enum { AP_ROW_MUL = 4 };
+
+template <int MODE>
+constexpr int mul_blocks_per_sm() { return MODE == AP_COL_MUL ? 2 : 3; }  // COL: 8 more factor registers
+
+template <int MODE, bool VEC>
+__global__ void __launch_bounds__(TX* TY, mul_blocks_per_sm<MODE>())
+    k_apply_reduce_mul(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+                       int64_t cols, int64_t chunk, const double* __restrict__ g,
+                       double* __restrict__ row_max, double* __restrict__ col_max,
+                       const int* __restrict__ flags, int need_exact) {
+  if (flags && (flags[F_SKIP] || (need_exact && flags[F_INEXACT]))) return;
+  __shared__ double cm[TY][TC8];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  // lane columns: cbase + off(e), off(e) = (e / 2) * 64 + (e & 1); valid iff off(e) < lim
+  const int64_t cbase = (int64_t)blockIdx.x * TC8 + 2 * tx;
+  const int64_t lim = cols - cbase;
+  const int64_t rbeg = (int64_t)blockIdx.y * chunk;
+  const int64_t rend = rbeg + chunk < rows ? rbeg + chunk : rows;
+  const bool full = lim >= (CPL8 / 2 - 1) * 2 * TX + 2;  // every lane column valid
+  double gc[CPL8], cmax[CPL8];
+#pragma unroll
+  for (int e = 0; e < CPL8; ++e) {
+    const int off = (e / 2) * (2 * TX) + (e & 1);
+    gc[e] = (MODE == AP_COL_MUL && off < lim) ? g[cbase + off] : 1.0;
+    cmax[e] = 0.0;
+  }
+#pragma unroll 1
+  for (int64_t rb = rbeg + ty; rb < rend; rb += TY * RU8) {
+    double x[RU8][CPL8];
+    double gr[RU8];
+#pragma unroll
+    for (int u = 0; u < RU8; ++u) {
+      const int64_t r = rb + u * TY;
+      gr[u] = 1.0;
+#pragma unroll
+      for (int e = 0; e < CPL8; ++e) x[u][e] = 0.0;
+      if (r < rend) {
+        if (MODE == AP_ROW_MUL) gr[u] = g[r];
+        const double* sp = src + r * lds + cbase;
+#pragma unroll
+        for (int h = 0; h < CPL8 / 2; ++h) {
+          const int off = h * (2 * TX);
+          if (VEC && (full || off + 1 < lim)) {
+            const double2 v = *reinterpret_cast<const double2*>(sp + off);
+            x[u][2 * h] = v.x; x[u][2 * h + 1] = v.y;
+          } else {
+            if (off < lim) x[u][2 * h] = sp[off];
+            if (off + 1 < lim) x[u][2 * h + 1] = sp[off + 1];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < RU8; ++u) {
+      const int64_t r = rb + u * TY;
+      if (r >= rend) continue;  // warp-uniform
+      double rmax = 0.0;
+#pragma unroll
+      for (int e = 0; e < CPL8; ++e) {
+        const int off = (e / 2) * (2 * TX) + (e & 1);
+        double y = x[u][e];
+        if (MODE == AP_ROW_MUL) y = __dmul_rn(y, gr[u]);
+        else if (MODE == AP_COL_MUL) y = __dmul_rn(y, gc[e]);
+        x[u][e] = y;
+        const double v = (full || off < lim) ? fabs(y) : 0.0;
+        rmax = fmax(rmax, v);
+        cmax[e] = fmax(cmax[e], v);
+      }
+      if (dst) {
+        double* dp = dst + r * ldd + cbase;
+#pragma unroll
+        for (int h = 0; h < CPL8 / 2; ++h) {
+          const int off = h * (2 * TX);
+          if (VEC && (full || off + 1 < lim)) {
+            *reinterpret_cast<double2*>(dp + off) = make_double2(x[u][2 * h], x[u][2 * h + 1]);
+          } else {
+            if (off < lim) dp[off] = x[u][2 * h];
+            if (off + 1 < lim) dp[off + 1] = x[u][2 * h + 1];
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+      if (tx == 0 && row_max) atomic_max_nonneg(&row_max[r], rmax);
+    }
+  }
+  if (col_max) {
+#pragma unroll
+    for (int e = 0; e < CPL8; ++e) cm[ty][(e / 2) * (2 * TX) + 2 * tx + (e & 1)] = cmax[e];
+    __syncthreads();
+    for (int q = ty * TX + tx; q < TC8; q += TX * TY) {
+      double mx = 0.0;
+#pragma unroll
+      for (int y = 0; y < TY; ++y) mx = fmax(mx, cm[y][q]);
+      const int64_t cc = (int64_t)blockIdx.x * TC8 + q;
+      if (cc < cols) atomic_max_nonneg(&col_max[cc], mx);
+    }
+  }
+}
+
+// exact reciprocal of a power-of-two factor (false if f is not a power of two whose reciprocal
+// is representable; then the dividing pass runs)
+__device__ __forceinline__ bool exact_recip(double f, double* inv) {
+  const int64_t bits = __double_as_longlong(f);
+  const int ex = (int)((bits >> 52) & 0x7ff);
+  if ((bits & 0x000fffffffffffffLL) != 0 || ex < 1 || ex > 2045 || !(f > 0.0)) return false;
+  *inv = __longlong_as_double((int64_t)(2046 - ex) << 52);
+  return true;
+}
+
 __device__ bool block_all(bool v) { return __syncthreads_and(v ? 1 : 0) != 0; }
 
 // O step factors (Alg. 3): r'_i = rowmaxA_i, s'_j = colmaxB_j; dA_i *= r'_i;
 // dB_j = s'_j * dB_j; stop test r', s' >= (1+tau)^(-1/2) when `test`.
 __global__ void k_factor_O(const double* __restrict__ rmA, const double* __restrict__ cmB,
                            int64_t M, int64_t N, int pow2, double* dA, double* dB, double* r_out,
-                           double* s_out, int* flags, int test, double lo_O,
-                           double* next_zero, int64_t next_len) {
+                           double* s_out, double* r_inv, double* s_inv, int* flags, int test,
+                           double lo_O, double* next_zero, int64_t next_len) {
   const bool skip = flags[F_DONE] != 0;
   __syncthreads();
-  if (threadIdx.x == 0) flags[F_SKIP] = skip ? 1 : 0;
+  if (threadIdx.x == 0) { flags[F_SKIP] = skip ? 1 : 0; flags[F_INEXACT] = 0; }
+  __syncthreads();
   for (int64_t i = threadIdx.x; i < next_len; i += blockDim.x) next_zero[i] = 0.0;
   if (skip) return;
   bool ok = true;
@@ -195,6 +320,7 @@ __global__ void k_factor_O(const double* __restrict__ rmA, const double* __restr
       r = pow2_round(r);
     }
     r_out[i] = r;
+    if (pow2 && !exact_recip(r, &r_inv[i])) flags[F_INEXACT] = 1;
     dA[i] = __dmul_rn(dA[i], r);
     ok = ok && (r >= lo_O);
   }
@@ -207,6 +333,7 @@ __global__ void k_factor_O(const double* __restrict__ rmA, const double* __restr
       s = pow2_round(s);
     }
     s_out[j] = s;
+    if (pow2 && !exact_recip(s, &s_inv[j])) flags[F_INEXACT] = 1;
     dB[j] = __dmul_rn(s, dB[j]);
     ok = ok && (s >= lo_O);
   }
@@ -220,11 +347,13 @@ __global__ void k_factor_O(const double* __restrict__ rmA, const double* __restr
 // I step factor (Alg. 3): p_k = sqrt(rowmaxB_k / colmaxA_k); dI_k *= p_k;
 // stop test p_k in [(1+tau)^(-1/4), (1+tau)^(1/4)] when `test`.
 __global__ void k_factor_I(const double* __restrict__ cmA, const double* __restrict__ rmB,
-                           int64_t K, int pow2, double* dI, double* p_out, int* flags, int test,
-                           double lo_I, double hi_I, double* next_zero, int64_t next_len) {
+                           int64_t K, int pow2, double* dI, double* p_out, double* p_inv,
+                           int* flags, int test, double lo_I, double hi_I, double* next_zero,
+                           int64_t next_len) {
   const bool skip = flags[F_DONE] != 0;
   __syncthreads();
-  if (threadIdx.x == 0) flags[F_SKIP] = skip ? 1 : 0;
+  if (threadIdx.x == 0) { flags[F_SKIP] = skip ? 1 : 0; flags[F_INEXACT] = 0; }
+  __syncthreads();
   for (int64_t i = threadIdx.x; i < next_len; i += blockDim.x) next_zero[i] = 0.0;
   if (skip) return;
   bool ok = true;
@@ -239,6 +368,7 @@ __global__ void k_factor_I(const double* __restrict__ cmA, const double* __restr
       if (pow2) p = pow2_round(p);
     }
     p_out[k] = p;
+    if (pow2 && !exact_recip(p, &p_inv[k])) flags[F_INEXACT] = 1;
     dI[k] = __dmul_rn(dI[k], p);
     ok = ok && (p >= lo_I && p <= hi_I);
   }
@@ -282,12 +412,14 @@ __global__ void k_unscale(double* C, int64_t ldc, int64_t M, int64_t N, const do
 // ---------------------------------------------------------------------------------------------
 size_t scale_ws_bytes(int64_t M, int64_t K, int64_t N) {
   // 2 sets of maxima (rowA M, colA K, rowB K, colB N) + factor vectors (r M, s N, p K) + flags
-  return (size_t)(2 * (M + K + K + N) + (M + N + K) + 16) * sizeof(double);
+  // + exact reciprocals (r M, s N, p K) of power-of-two factors
+  return (size_t)(2 * (M + K + K + N) + 2 * (M + N + K) + 16) * sizeof(double);
 }
 
 struct ScaleWsView {
   double* mx[2];  // each: rowA (M) | colA (K) | rowB (K) | colB (N)
   double *r, *s, *p;
+  double *ri, *si, *pi;
   int* flags;
 };
 
@@ -300,7 +432,10 @@ static ScaleWsView scale_ws_view(void* ws, int64_t M, int64_t K, int64_t N) {
   v.r = w + 2 * set;
   v.s = v.r + M;
   v.p = v.s + N;
-  v.flags = (int*)(v.p + K);
+  v.ri = v.p + K;
+  v.si = v.ri + M;
+  v.pi = v.si + N;
+  v.flags = (int*)(v.pi + K);
   return v;
 }
 
@@ -308,28 +443,54 @@ int* scale_flags_ptr(void* ws, int64_t M, int64_t K, int64_t N) {
   return scale_ws_view(ws, M, K, N).flags;
 }
 
-// one streaming pass: dst = apply(src) with the row / column max-abs of the result
+static void grid_dims(int64_t rows, int64_t cols, int tc, int ru, int per_sm, dim3* g, int64_t* chunk) {
+  // column strips x row chunks: one wave of per_sm resident blocks per SM, chunks a multiple
+  // of TY * ru rows
+  const int64_t strips = (cols + tc - 1) / tc;
+  int64_t nchunks = std::max<int64_t>(1, (148 * per_sm) / strips);
+  int64_t ch = (rows + nchunks - 1) / nchunks;
+  ch = (ch + TY * ru - 1) / (TY * ru) * (TY * ru);
+  nchunks = (rows + ch - 1) / ch;
+  *g = dim3((unsigned)strips, (unsigned)nchunks);
+  *chunk = ch;
+}
+
+// one streaming pass: dst = apply(src) with the row / column max-abs of the result.
+// mode AP_ROW_DIV / AP_COL_DIV divide by f; with pow2 factors (finv != null) the multiply pass
+// by the exact reciprocals runs instead, and the dividing pass only if some reciprocal was
+// inexact (both check flags on device).
 static void apply_reduce(cudaStream_t st, int mode, const double* src, int64_t lds, double* dst,
-                         int64_t ldd, int64_t rows, int64_t cols, const double* f, double* row_max,
-                         double* col_max, const int* flags) {
+                         int64_t ldd, int64_t rows, int64_t cols, const double* f,
+                         const double* finv, double* row_max, double* col_max, const int* flags) {
+  if (rows == 0 || cols == 0) return;
   const bool vec = ((uintptr_t)src % 16 == 0) && lds % 2 == 0 &&
                    (!dst || (((uintptr_t)dst % 16 == 0) && ldd % 2 == 0));
-  if (rows == 0 || cols == 0) return;
   dim3 blk(TX, TY);
-  // column strips x row chunks: one wave of 4 resident blocks per SM, chunks a multiple of
-  // TY * RU rows
-  const int64_t strips = (cols + TC - 1) / TC;
-  int64_t nchunks = std::max<int64_t>(1, (148 * 4) / strips);
-  int64_t chunk = (rows + nchunks - 1) / nchunks;
-  chunk = (chunk + TY * RU - 1) / (TY * RU) * (TY * RU);
-  nchunks = (rows + chunk - 1) / chunk;
-  dim3 g((unsigned)strips, (unsigned)nchunks);
-#define FMM_AR(M, V) k_apply_reduce<M, V><<<g, blk, 0, st>>>(src, lds, dst, ldd, rows, cols, chunk, f, row_max, col_max, flags)
+  dim3 g;
+  int64_t chunk;
+  const bool mul = mode == AP_NONE || mode == AP_COL_MUL || finv != nullptr;
+  if (mul) {
+    const int mm = mode == AP_ROW_DIV ? AP_ROW_MUL : mode == AP_COL_DIV ? AP_COL_MUL : mode;
+    const double* gv = (mode == AP_ROW_DIV || mode == AP_COL_DIV) ? finv : f;
+    const int need_exact = (mode == AP_ROW_DIV || mode == AP_COL_DIV) ? 1 : 0;
+    grid_dims(rows, cols, TC8, RU8, mm == AP_COL_MUL ? 2 : 3, &g, &chunk);
+#define FMM_ARM(M, V) k_apply_reduce_mul<M, V><<<g, blk, 0, st>>>(src, lds, dst, ldd, rows, cols, chunk, gv, row_max, col_max, flags, need_exact)
+    switch (mm) {
+      case AP_ROW_MUL: if (vec) FMM_ARM(AP_ROW_MUL, true); else FMM_ARM(AP_ROW_MUL, false); break;
+      case AP_COL_MUL: if (vec) FMM_ARM(AP_COL_MUL, true); else FMM_ARM(AP_COL_MUL, false); break;
+      default: if (vec) FMM_ARM(AP_NONE, true); else FMM_ARM(AP_NONE, false); break;
+    }
+#undef FMM_ARM
+    if (!need_exact) return;
+  }
+  // dividing pass (pow2 = 0, or the fallback when a reciprocal was inexact)
+  const int only_if_inexact = mul ? 1 : 0;
+  grid_dims(rows, cols, TC, RU, 4, &g, &chunk);
+#define FMM_AR(M, V) k_apply_reduce<M, V><<<g, blk, 0, st>>>(src, lds, dst, ldd, rows, cols, chunk, f, row_max, col_max, flags, only_if_inexact)
   switch (mode) {
     case AP_ROW_DIV: if (vec) FMM_AR(AP_ROW_DIV, true); else FMM_AR(AP_ROW_DIV, false); break;
     case AP_COL_DIV: if (vec) FMM_AR(AP_COL_DIV, true); else FMM_AR(AP_COL_DIV, false); break;
-    case AP_COL_MUL: if (vec) FMM_AR(AP_COL_MUL, true); else FMM_AR(AP_COL_MUL, false); break;
-    default: if (vec) FMM_AR(AP_NONE, true); else FMM_AR(AP_NONE, false); break;
+    default: break;
   }
 #undef FMM_AR
 }
@@ -352,8 +513,8 @@ cudaError_t run_scaling(int64_t M, int64_t K, int64_t N, const double* A, int64_
   // initial reductions of A, B
   {
     double* m = v.mx[0];
-    apply_reduce(st, AP_NONE, A, lda, nullptr, 0, M, K, nullptr, m, m + M, nullptr);
-    apply_reduce(st, AP_NONE, B, ldb, nullptr, 0, K, N, nullptr, m + M + K, m + M + 2 * K, nullptr);
+    apply_reduce(st, AP_NONE, A, lda, nullptr, 0, M, K, nullptr, nullptr, m, m + M, nullptr);
+    apply_reduce(st, AP_NONE, B, ldb, nullptr, 0, K, N, nullptr, nullptr, m + M + K, m + M + 2 * K, nullptr);
   }
   const double lo_I = pow(1.0 + tau, -0.25), hi_I = pow(1.0 + tau, 0.25), lo_O = pow(1.0 + tau, -0.5);
   int t0 = -1;
@@ -367,16 +528,16 @@ cudaError_t run_scaling(int64_t M, int64_t K, int64_t N, const double* A, int64_
     const double* srcB = t == 0 ? B : B_out;
     const int64_t lsa = t == 0 ? lda : lda_out, lsb = t == 0 ? ldb : ldb_out;
     if (isO) {
-      k_factor_O<<<1, 1024, 0, st>>>(cur, cur + M + 2 * K, M, N, pow2, dA, dB, v.r, v.s, v.flags,
+      k_factor_O<<<1, 1024, 0, st>>>(cur, cur + M + 2 * K, M, N, pow2, dA, dB, v.r, v.s, v.ri, v.si, v.flags,
                                      test, lo_O, nxt, set);
-      apply_reduce(st, AP_ROW_DIV, srcA, lsa, A_out, lda_out, M, K, v.r, nxt, nxt + M, v.flags);
-      apply_reduce(st, AP_COL_DIV, srcB, lsb, B_out, ldb_out, K, N, v.s, nxt + M + K,
+      apply_reduce(st, AP_ROW_DIV, srcA, lsa, A_out, lda_out, M, K, v.r, pow2 ? v.ri : nullptr, nxt, nxt + M, v.flags);
+      apply_reduce(st, AP_COL_DIV, srcB, lsb, B_out, ldb_out, K, N, v.s, pow2 ? v.si : nullptr, nxt + M + K,
                    nxt + M + 2 * K, v.flags);
     } else {
-      k_factor_I<<<1, 1024, 0, st>>>(cur + M, cur + M + K, K, pow2, dI, v.p, v.flags, test, lo_I,
+      k_factor_I<<<1, 1024, 0, st>>>(cur + M, cur + M + K, K, pow2, dI, v.p, v.pi, v.flags, test, lo_I,
                                      hi_I, nxt, set);
-      apply_reduce(st, AP_COL_MUL, srcA, lsa, A_out, lda_out, M, K, v.p, nxt, nxt + M, v.flags);
-      apply_reduce(st, AP_ROW_DIV, srcB, lsb, B_out, ldb_out, K, N, v.p, nxt + M + K,
+      apply_reduce(st, AP_COL_MUL, srcA, lsa, A_out, lda_out, M, K, v.p, nullptr, nxt, nxt + M, v.flags);
+      apply_reduce(st, AP_ROW_DIV, srcB, lsb, B_out, ldb_out, K, N, v.p, pow2 ? v.pi : nullptr, nxt + M + K,
                    nxt + M + 2 * K, v.flags);
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return e;

@@ -100,3 +100,28 @@ def test_scaled_fmm_C4_recipe(fb, mode):
     assert oracle.parity_metric(Cg, Co, np.abs(A).max(), np.abs(B).max(), K) <= 1e-13
     if mode == "repeated":
         assert rel(Cg) < 1e-10  # repeated O-I is accurate on this skew
+
+
+@pytest.mark.parametrize("pow2", [True, False])
+def test_extreme_magnitudes_bitwise(fb, pow2):
+    # rows / columns near the top and bottom of the FP64 range: the power-of-two factors 2^1023
+    # and subnormal powers of two have no normal reciprocal, so the library falls back from
+    # the multiply-by-reciprocal pass to true division (flags[F_INEXACT]); results stay bitwise
+    # the oracle's (reading A9)
+    g = np.random.default_rng(3)
+    A = g.uniform(0.5, 1.0, (64, 96))
+    B = g.uniform(0.5, 1.0, (96, 80))
+    A[5] *= 1.5e308
+    A[7] *= 2.0 ** -1060            # subnormal row
+    B[:, 3] *= 1.2e308
+    B[:, 9] *= 2.0 ** -1065
+    for first_O in (True, False):
+        gg = fb.scale_repeated(dev(A), dev(B), first_O=first_O, tau=1.0, max_steps=6, pow2=pow2)
+        o = oracle.scale_repeated(A, B, first_O=first_O, tau=1.0, max_steps=6, pow2=pow2)
+        assert gg["steps"] == o["steps"]
+        for k in ("A", "B", "dA", "dB", "dI"):
+            assert np.array_equal(host(gg[k]), o[k]), k
+    Ao, Bo, dA, dB = fb.scale_outside(dev(A), dev(B), pow2=pow2)
+    ra, rb, rdA, rdB = oracle.scale_outside(A, B, pow2=pow2)
+    for x, y in ((Ao, ra), (Bo, rb), (dA, rdA), (dB, rdB)):
+        assert np.array_equal(host(x), y)
