@@ -111,6 +111,7 @@ struct fmm_plan {
   int schedule = 0;  // 0 auto, 1 breadth-first, 2 depth-first top level
   int fusion = 2;    // W-combination of the leaves' parents in the leaf GEMM epilogue: 0 off, 1 on, 2 auto
   int shard_depth = 1;  // multi-GPU: units = paths of the first shard_depth levels, round-robin
+  bool persistent = true;  // fused leaves as the persistent stream-K kernel (K2P) where eligible
   ncclComm_t comm = nullptr;
   // compiled schedule
   std::vector<Step> steps;
@@ -167,6 +168,8 @@ fmm_plan::~fmm_plan() {
 }
 
 namespace {
+
+constexpr int kPersistCtas = 148;  // B200 SMs: one persistent K2P CTA per SM
 
 int elem_size(int dtype) { return dtype == FMM_F64 ? 8 : 4; }
 
@@ -298,6 +301,10 @@ struct Builder {
     constexpr int64_t kSMs = 148;
     const int64_t tiles = ((p->lm[p->L] + 127) / 128) * ((p->ln[p->L] + 127) / 128);
     const int64_t units = nparents * tiles;
+    // the persistent stream-K form (K2P) balances any unit count: fuse when the product-tiles
+    // fill the SMs at least once
+    if (p->persistent && (p->lk[p->L] + 15) / 16 >= persistent_min_kt())
+      return units * p->rules[p->node_rule[p->L - 1][0]].R >= kSMs;
     const int64_t waves = (units + kSMs - 1) / kSMs;
     return waves >= 4 && units * 10 >= waves * kSMs * 9;
   }
@@ -339,7 +346,13 @@ struct Builder {
     st.dev_off = push(fz);
     st.rows = p->lm[p->L]; st.cols = p->ln[p->L]; st.inner = p->lk[p->L];
     st.P = r0.m0; st.Q = r0.n0; st.R = r0.R;
+    st.nr = fz[0].nr;
     st.arena_off = -1;
+    // persistent hybrid data-parallel / stream-K form (K2P) when the leaf has >= STAGES k-tiles
+    if (p->persistent && (st.inner + 15) / 16 >= persistent_min_kt()) {
+      st.persist = kPersistCtas;
+      st.arena_off = ws_alloc((int64_t)((persistent_scratch_bytes(kPersistCtas, st.nr) + 7) / 8));
+    }
     p->steps.push_back(st);
   }
 
@@ -596,6 +609,14 @@ struct TimedLaunch {
   }
 };
 
+// SMs of the current device (the persistent kernel needs one co-resident CTA per SM)
+static int device_sms() {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  return n;
+}
+
 template <typename T>
 static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStream_t st,
                             size_t i0 = 0, size_t i1 = (size_t)-1) {
@@ -611,8 +632,16 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
       case STEP_ACC: e = launch_acc<T>(s, nd, p->dev_coef, b, vec, st); break;
       case STEP_ZERO: e = launch_zero<T>(s, nd, b, st); break;
       case STEP_K2F:
-        e = launch_gemm_f64_fused((const FusedNode*)nd, s.count, s.rows, s.cols, s.inner,
-                                  p->dev_coef, s.P, s.Q, s.R, b, vec, st);
+        if (s.persist && s.persist <= device_sms()) {
+          double* scr = (double*)b.p[BASE_WS] + s.arena_off;
+          int* flg = (int*)(scr + (size_t)s.persist * s.nr * 128 * 128);
+          e = launch_gemm_f64_persistent((const FusedNode*)nd, s.count, s.rows, s.cols, s.inner,
+                                         p->dev_coef, s.P, s.Q, s.R, s.nr, s.persist, scr, flg, b,
+                                         vec, st);
+        } else {
+          e = launch_gemm_f64_fused((const FusedNode*)nd, s.count, s.rows, s.cols, s.inner,
+                                    p->dev_coef, s.P, s.Q, s.R, b, vec, st);
+        }
         break;
       case STEP_K2:
         if (p->dtype == FMM_F64)
@@ -767,6 +796,7 @@ fmm_status fmm_plan_create(const fmm_rule* const* nodes, int n_nodes, int levels
   }
   auto p = new fmm_plan();
   p->dtype = dtype; p->leaf = leaf; p->L = levels; p->M = M; p->K = K; p->N = N;
+  if (const char* pe = getenv("FMM_K2P")) p->persistent = atoi(pe) != 0;
   if (const char* fe = getenv("FMM_FUSION")) {
     const int f = atoi(fe);
     if (f >= 0 && f <= 2) p->fusion = f;
@@ -1213,6 +1243,7 @@ static const fmm_plan* depth_first_twin(const fmm_plan* p) {
     t->rules = p->rules; t->node_rule = p->node_rule; t->lm = p->lm; t->lk = p->lk; t->ln = p->ln;
     t->scaling = p->scaling; t->coef_U = p->coef_U; t->coef_V = p->coef_V; t->coef_W = p->coef_W;
     t->coef_host = p->coef_host; t->schedule = 2; t->fusion = p->fusion; t->shard_depth = p->shard_depth;
+    t->persistent = p->persistent;
     if (compile_plan(t) != FMM_OK) { delete t; return nullptr; }
     p->df_twin = t;
   }

@@ -155,8 +155,11 @@ struct Step {
   int64_t dev_off;   // byte offset of the node array in the plan's device descriptor buffer
   int64_t rows, cols, inner;  // sub-block dims (K1/K3/ACC/ZERO) or m, n, k (K2)
   int P, Q, R;       // K1: split P x Q, rank R.  K3/ACC/ZERO: P = M0, Q = N0, R
-  int64_t arena_off; // K2 FP32 tensor-core leaves: offset (elements) of the hi/lo arena in ws
+  int64_t arena_off; // K2 FP32 tensor-core leaves: offset (elements) of the hi/lo arena in ws;
+                     // K2F persistent (K2P): offset of the scratch tiles + flags in ws
   bool vec_ok;       // all ws offsets / dims allow 16-byte vectors (caller bases checked later)
+  int nr = 0;        // K2F: products per node (uniform)
+  int persist = 0;   // K2F: run as the persistent stream-K kernel with this many CTAs (0: grid)
 };
 
 // ---- kernel launchers (kernels_*.cu) -----------------------------------------------------------
@@ -183,6 +186,15 @@ cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, in
 cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                   int64_t k, const double* dev_coef, int P, int Q, int R,
                                   const Bases& b, bool vec, cudaStream_t st);
+// K2P: persistent hybrid data-parallel / stream-K form of K2F (one CTA per SM, `ctas` CTAs;
+// every node has NR products).  scratch / flags: persistent_scratch_bytes(ctas, NR) of
+// workspace (flags zeroed by the launcher).  Needs ceil(k / BK) >= persistent_min_kt().
+cudaError_t launch_gemm_f64_persistent(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
+                                       int64_t k, const double* dev_coef, int P, int Q, int R,
+                                       int NR, int ctas, double* scratch, int* flags,
+                                       const Bases& b, bool vec, cudaStream_t st);
+size_t persistent_scratch_bytes(int ctas, int NR);
+int persistent_min_kt();
 cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, const LeafNode* host_leaves, int count,
                             int64_t m, int64_t n, int64_t k, const Bases& b, bool vec, int leaf,
                             float* arena, cudaStream_t st);

@@ -545,6 +545,281 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   cp_wait<0>();
 }
 
+// K2P: the fused leaf products (K2F) as a persistent, hybrid data-parallel / stream-K kernel.
+// A unit is (parent, 128x128 output tile) with NR products; T = units x NR product-tiles.
+// Grid = one CTA per SM (G).  Units 0 .. G*floor(U/G)-1 go data-parallel (CTA c: units
+// c, c+G, ...: concurrent CTAs work on neighbouring tiles, as in K2F); the remaining U mod G
+// units' product-tiles are split evenly across the G CTAs in contiguous ranges (stream-K), so
+// every CTA does the same number of product-tiles to within one.  A unit whose products span
+// several CTAs is finished by its OWNER (the CTA holding its product 0): the other CTAs compute
+// their products of it FIRST (before their data-parallel units) into a scratch slot and raise a
+// flag; the owner, after its own products of that unit (its last work), waits for the flags and
+// applies the scratch products in ascending r with the same epilogue -- so every element of C_k
+// still sees c = w*m, c = c + w*m in ascending r (bitwise K2F / K3), and owners only ever wait
+// for work that was scheduled first (no deadlock with G co-resident CTAs).
+template <typename C, bool VEC>
+__global__ void __launch_bounds__(C::THREADS, 1)
+    k2p_gemm_f64(const FusedNode* __restrict__ nodes, const double* __restrict__ coef_all,
+                 Bases bases, int64_t m, int64_t n, int64_t k, int tiles_m, int tiles_n, int P,
+                 int Q, int R, int NR, int64_t U, double* __restrict__ scratch,
+                 int* __restrict__ flags) {
+  static_assert(C::PIPE, "the fused kernel uses the PIPE mainloop");
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + C::STAGES * C::A_STAGE;
+  __shared__ int flag_ok;
+
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int g = lane >> 2, t = lane & 3;
+  const int tiles = tiles_m * tiles_n;
+
+  // ---- this CTA's work list (constants kept in shared memory: registers go to the mainloop) -
+  __shared__ int64_t wl[6];  // dp_units, n_dp, T_tail, s0, n_lead, n_own_tail
+  if (tid == 0) {
+    const int64_t dp = (U / G) * G, tt = (U - dp) * NR;
+    const int64_t a0 = (int64_t)cta * tt / G, a1 = (int64_t)(cta + 1) * tt / G;
+    const int64_t lead_max = NR - a0 % NR;
+    const int64_t nl = (a0 % NR) ? (lead_max < a1 - a0 ? lead_max : a1 - a0) : 0;  // non-owner
+    wl[0] = dp; wl[1] = U / G; wl[2] = tt; wl[3] = a0; wl[4] = nl; wl[5] = (a1 - a0) - nl;
+  }
+  __syncthreads();
+#define dp_units wl[0]
+#define n_dp wl[1]
+#define T_tail wl[2]
+#define s0 wl[3]
+#define n_lead wl[4]
+#define n_own_tail wl[5]
+  const int64_t n_items = n_lead + n_dp * NR + n_own_tail;
+  // item i -> (unit, product index ri, role): 0 lead (scratch), 1 owned
+  auto item = [&](int64_t i, int64_t& u, int& ri, int& lead) {
+    if (i < n_lead) {
+      u = dp_units + s0 / NR; ri = (int)(s0 % NR) + (int)i; lead = 1;
+    } else if (i < n_lead + n_dp * NR) {
+      const int64_t j = i - n_lead;
+      u = cta + (j / NR) * G; ri = (int)(j % NR); lead = 0;
+    } else {
+      const int64_t q = s0 + n_lead + (i - n_lead - n_dp * NR);
+      u = dp_units + q / NR; ri = (int)(q % NR); lead = 0;
+    }
+  };
+  auto tile_coords = [&](int64_t u, int64_t& m0, int64_t& n0, const FusedNode*& nd) {
+    nd = nodes + u / tiles;
+    const int tile = (int)(u % tiles);
+    const int per_group = GROUP_M * tiles_n;
+    const int group = tile / per_group;
+    const int first_m = group * GROUP_M;
+    const int gsz = min(tiles_m - first_m, GROUP_M);
+    m0 = (int64_t)(first_m + (tile % per_group) % gsz) * C::BM;
+    n0 = (int64_t)((tile % per_group) / gsz) * C::BN;
+  };
+  // operands of item i with the tile offset folded in: A + m0 lda, B + n0, remaining rows /
+  // columns mr = m - m0, nr = n - n0 (32-bit: leaf dims and leading dimensions < 2^31)
+  struct Opnd {
+    const double* A;
+    const double* B;
+    int lda, ldb, mr, nr;
+  };
+  auto operands = [&](int64_t i) {
+    Opnd o;
+    int64_t u, m0, n0, la, lb;
+    int ri, lead;
+    item(i, u, ri, lead);
+    const FusedNode* nd;
+    tile_coords(u, m0, n0, nd);
+    o.A = op_ptr<const double>(bases, nd->a[ri], la) + m0 * la;
+    o.B = op_ptr<const double>(bases, nd->b[ri], lb) + n0;
+    o.lda = (int)la; o.ldb = (int)lb; o.mr = (int)(m - m0); o.nr = (int)(n - n0);
+    return o;
+  };
+  // scratch slot of stream-K product-tile q held by a non-owner CTA: (cta(q), position)
+  auto slot_of = [&](int64_t q) {
+    int64_t c = q * G / T_tail;
+    while (c + 1 < G && (c + 1) * T_tail / G <= q) ++c;
+    while (c > 0 && c * T_tail / G > q) --c;
+    return c * NR + (q - c * T_tail / G);
+  };
+
+  double acc[C::MI][C::NI][4];
+  auto zero_acc = [&]() {
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+  };
+  zero_acc();
+  if (n_items == 0) return;
+
+  // W-combination of product ri of node nd at tile (m0, n0) from acc (K2F's RED epilogue)
+  auto epilogue = [&](const FusedNode* nd, int ri, int64_t m0, int64_t n0) {
+    const uint32_t wmask = nd->wmask[ri], fmask = nd->first[ri];
+    const int r = nd->rlist[ri];
+    int64_t ldo;
+    double* out = op_ptr<double>(bases, nd->out, ldo);
+    for (int kk = 0; kk < P * Q; ++kk) {  // kk = ia*Q + jb (row-major C blocks)
+      if (!((wmask >> kk) & 1u)) continue;
+      const double w = coef_all[nd->coef_off + kk * R + r];
+      const bool first = (fmask >> kk) & 1u;
+      double* ob = out + (int64_t)(kk / Q) * m * ldo + (int64_t)(kk % Q) * n;
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t row = m0 + wm * C::WTM + i * 16 + g + h * 8;
+          if (row >= m) continue;
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j) {
+            const int64_t col = n0 + wn * C::WTN + j * 8 + 2 * t;
+            double* cp = ob + row * ldo + col;
+            const double v0 = __dmul_rn(w, acc[i][j][2 * h]), v1 = __dmul_rn(w, acc[i][j][2 * h + 1]);
+            if (first) {
+              if (VEC && col + 1 < n) {
+                *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
+              } else {
+                if (col < n) cp[0] = v0;
+                if (col + 1 < n) cp[1] = v1;
+              }
+            } else {
+              if (col < n) red_add(cp, v0);
+              if (col + 1 < n) red_add(cp + 1, v1);
+            }
+          }
+        }
+    }
+  };
+  constexpr int NACC = C::MI * C::NI * 4;
+  auto store_scratch = [&](int64_t slot) {  // layout [slot][acc index][thread]: coalesced
+    double* sp = scratch + slot * NACC * C::THREADS + tid;
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) sp[((i * C::NI + j) * 4 + e) * C::THREADS] = acc[i][j][e];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicExch(&flags[slot], 1);
+  };
+  auto load_scratch = [&](int64_t slot) {
+    if (tid == 0) {
+      unsigned ns = 32;
+      while (atomicAdd(&flags[slot], 0) == 0) { __nanosleep(ns); if (ns < 1024) ns *= 2; }
+      __threadfence();
+      flag_ok = 1;
+    }
+    __syncthreads();
+    const double* sp = scratch + slot * NACC * C::THREADS + tid;
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[i][j][e] = __ldcg(sp + ((i * C::NI + j) * 4 + e) * C::THREADS);
+  };
+
+  const int KT = (int)((k + C::BK - 1) / C::BK);  // >= STAGES (host-checked)
+  const int64_t total = n_items * KT;
+  constexpr int KQ = C::BK / 4;
+  static_assert(KQ % 2 == 0, "even number of k-slices per stage");
+  double af[2][C::MI][2], bf[2][C::NI];
+  const int a_off = (wm * C::WTM + g) * C::A_LD + t, b_off = t * C::B_LD + wn * C::WTN + g;
+  auto load_frag = [&](int buf, int slot, int kk) {
+    const double* as = As + slot * C::A_STAGE + a_off;
+    const double* bs = Bs + slot * C::B_STAGE + b_off;
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i) {
+      af[buf][i][0] = as[(i * 16) * C::A_LD + kk];
+      af[buf][i][1] = as[(i * 16 + 8) * C::A_LD + kk];
+    }
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) bf[buf][j] = bs[kk * C::B_LD + j * 8];
+  };
+  auto ktile = [&](int64_t it, auto&& refill) {
+    const int slot = (int)(it % C::STAGES);
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+      const int cur = q & 1;
+      if (q == KQ - 1) {
+        cp_wait<C::STAGES - 2>();
+        __syncthreads();
+        refill(slot);
+        cp_commit();
+        if (it + 1 < total) load_frag(cur ^ 1, (int)((it + 1) % C::STAGES), 0);
+      } else {
+        load_frag(cur ^ 1, slot, (q + 1) * 4);
+      }
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) dmma16n8k4(acc[i][j], af[cur][i][0], af[cur][i][1], bf[cur][j]);
+    }
+  };
+
+  {  // prologue: the first STAGES k-tiles of item 0
+    const Opnd o = operands(0);
+#pragma unroll
+    for (int s = 0; s < C::STAGES - 1; ++s) {
+      load_tiles<C, VEC>(As + s * C::A_STAGE, Bs + s * C::B_STAGE, o.A, o.lda, o.B, o.ldb, o.mr, o.nr,
+                         k, 0, 0, (int64_t)s * C::BK, tid);
+      cp_commit();
+    }
+    cp_wait<C::STAGES - 2>();
+    __syncthreads();
+    load_tiles<C, VEC>(As + (C::STAGES - 1) * C::A_STAGE, Bs + (C::STAGES - 1) * C::B_STAGE, o.A,
+                       o.lda, o.B, o.ldb, o.mr, o.nr, k, 0, 0, (int64_t)(C::STAGES - 1) * C::BK, tid);
+    cp_commit();
+  }
+  load_frag(0, 0, 0);
+  int64_t it = 0;
+  for (int64_t i = 0; i < n_items; ++i) {
+    const Opnd o = operands(i);
+    for (int kt = 0; kt < KT - C::STAGES; ++kt, ++it)
+      ktile(it, [&](int slot) {
+        load_tiles<C, VEC>(As + slot * C::A_STAGE, Bs + slot * C::B_STAGE, o.A, o.lda, o.B, o.ldb,
+                           o.mr, o.nr, k, 0, 0, (int64_t)(kt + C::STAGES) * C::BK, tid);
+      });
+    const bool more = i + 1 < n_items;
+    const Opnd on = more ? operands(i + 1) : o;
+    for (int j = 0; j < C::STAGES; ++j, ++it)
+      ktile(it, [&](int slot) {
+        if (more)
+          load_tiles<C, VEC>(As + slot * C::A_STAGE, Bs + slot * C::B_STAGE, on.A, on.lda, on.B,
+                             on.ldb, on.mr, on.nr, k, 0, 0, (int64_t)j * C::BK, tid);
+      });
+    int64_t u;
+    int ri, lead;
+    item(i, u, ri, lead);
+    if (lead) {
+      store_scratch((int64_t)cta * NR + i);
+    } else {
+      const FusedNode* nd;
+      int64_t m0, n0;
+      tile_coords(u, m0, n0, nd);
+      epilogue(nd, ri, m0, n0);
+      if (i == n_items - 1 && n_own_tail > 0 && ri + 1 < NR) {
+        // owner fix-up: the unit's remaining products come from later CTAs' scratch
+        const int64_t qbase = (u - dp_units) * NR;
+        for (int r2 = ri + 1; r2 < NR; ++r2) {
+          load_scratch(slot_of(qbase + r2));
+          epilogue(nd, r2, m0, n0);
+        }
+      }
+    }
+    zero_acc();
+  }
+  cp_wait<0>();
+#undef dp_units
+#undef n_dp
+#undef T_tail
+#undef s0
+#undef n_lead
+#undef n_own_tail
+}
+
 template <typename C, bool VEC, bool RED>
 cudaError_t launch_fused_kernel(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                 int64_t k, const double* coef, int P, int Q, int R,
@@ -664,6 +939,34 @@ cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, in
     default: return launch_cfg<V16>(dev_leaves, count, m, n, k, b, vec, st);
   }
 }
+
+cudaError_t launch_gemm_f64_persistent(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
+                                       int64_t k, const double* dev_coef, int P, int Q, int R,
+                                       int NR, int ctas, double* scratch, int* flags,
+                                       const Bases& b, bool vec, cudaStream_t st) {
+  using Cf = V16;
+  if (count == 0 || m == 0 || n == 0) return cudaSuccess;
+  const int tiles_m = (int)((m + Cf::BM - 1) / Cf::BM), tiles_n = (int)((n + Cf::BN - 1) / Cf::BN);
+  const int64_t U = (int64_t)count * tiles_m * tiles_n;
+  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)ctas * NR, st);
+  if (e != cudaSuccess) return e;
+  auto go = [&](auto kern) {
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          Cf::SMEM_BYTES);
+    if (e2 != cudaSuccess) return e2;
+    kern<<<ctas, Cf::THREADS, Cf::SMEM_BYTES, st>>>(dev_nodes, dev_coef, b, m, n, k, tiles_m, tiles_n,
+                                                    P, Q, R, NR, U, scratch, flags);
+    return cudaGetLastError();
+  };
+  return vec ? go(k2p_gemm_f64<Cf, true>) : go(k2p_gemm_f64<Cf, false>);
+}
+
+size_t persistent_scratch_bytes(int ctas, int NR) {
+  using Cf = V16;
+  return (size_t)ctas * NR * (size_t)(Cf::BM * Cf::BN) * sizeof(double) + (size_t)ctas * NR * sizeof(int) + 512;
+}
+
+int persistent_min_kt() { return V16::STAGES; }
 
 namespace {
 int fused_variant() {

@@ -164,3 +164,20 @@ def test_shard_depth_virtual_ranks(fb, depth, nranks):
         total += part
     assert sorted(units) == list(range(7 ** depth))
     assert oracle.parity_metric(total, ref, np.abs(A).max(), np.abs(B).max(), 256) <= TOL64
+
+
+@pytest.mark.parametrize("dims,names", [((2048, 2048, 2048), ("strassen",) * 3),
+                                        ((1536, 1024, 1280), ("winograd", "classical222")),
+                                        ((2 * 1000, 2 * 200, 2 * 600), ("winograd",))])
+def test_persistent_stream_k_equals_unfused(fb, dims, names):
+    # the persistent hybrid data-parallel / stream-K form (K2P): units split across CTAs are
+    # finished by their owner from the other CTAs' scratch in ascending r -- bitwise the
+    # unfused K2 + K3 (includes ragged tiles: 1000 / 600 are not multiples of 128)
+    M, K, N = dims
+    A, B = fi.random_pair(M, K, N, seed=M // 7)
+    pf = plan(fb, names, M, K, N, "on")
+    assert pf.fused_launches() >= 1
+    Cf = exe(pf, A, B)
+    Cu = exe(plan(fb, names, M, K, N, "off"), A, B)
+    assert np.array_equal(Cf, Cu)
+    assert np.array_equal(Cf, exe(pf, A, B))  # deterministic across runs

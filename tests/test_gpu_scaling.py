@@ -111,7 +111,7 @@ def test_extreme_magnitudes_bitwise(fb, pow2):
     g = np.random.default_rng(3)
     A = g.uniform(0.5, 1.0, (64, 96))
     B = g.uniform(0.5, 1.0, (96, 80))
-    A[5] *= 1.5e308
+    A[5] *= 1.2e308                 # rounds to 2^1023: reciprocal subnormal
     A[7] *= 2.0 ** -1060            # subnormal row
     B[:, 3] *= 1.2e308
     B[:, 9] *= 2.0 ** -1065
