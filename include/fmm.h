@@ -139,8 +139,11 @@ fmm_status fmm_plan_set_schedule(fmm_plan* plan, int schedule);
  * in ascending r and updates C_k after each (c = w*m first, then c = c + w*m), so M_r is never
  * written to memory and the result is bitwise identical to the unfused K2 + K3 path.
  * mode: 0 = off, 1 = on, 2 = automatic (default; on when parents x output tiles fill the GPU
- * several times).  FP64 only (FP32 plans ignore it).  The environment variable FMM_FUSION
- * (0/1/2) sets the default at fmm_plan_create. */
+ * several times), 3 = on, run as the persistent hybrid data-parallel / stream-K kernel (one CTA
+ * per SM; units split across CTAs are finished by their owner from scratch in ascending r, still
+ * bitwise; needs >= 64 inner-dimension elements per leaf, else mode 1).  FP64 only (FP32 plans
+ * ignore it).  The environment variables FMM_FUSION (0/1/2) and FMM_K2P (0/1) set the defaults
+ * at fmm_plan_create. */
 fmm_status fmm_plan_set_fusion(fmm_plan* plan, int mode);
 
 /* Host-only query: number of fused leaf-product launches (K2F) in the compiled schedule. */

@@ -111,7 +111,7 @@ struct fmm_plan {
   int schedule = 0;  // 0 auto, 1 breadth-first, 2 depth-first top level
   int fusion = 2;    // W-combination of the leaves' parents in the leaf GEMM epilogue: 0 off, 1 on, 2 auto
   int shard_depth = 1;  // multi-GPU: units = paths of the first shard_depth levels, round-robin
-  bool persistent = true;  // fused leaves as the persistent stream-K kernel (K2P) where eligible
+  bool persistent = false;  // fused leaves as the persistent stream-K kernel (K2P) where eligible
   ncclComm_t comm = nullptr;
   // compiled schedule
   std::vector<Step> steps;
@@ -634,7 +634,7 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
       case STEP_K2F:
         if (s.persist && s.persist <= device_sms()) {
           double* scr = (double*)b.p[BASE_WS] + s.arena_off;
-          int* flg = (int*)(scr + (size_t)s.persist * s.nr * 128 * 128);
+          int* flg = (int*)(scr + (size_t)persistent_max_tail_units(s.persist) * s.nr * 128 * 128);
           e = launch_gemm_f64_persistent((const FusedNode*)nd, s.count, s.rows, s.cols, s.inner,
                                          p->dev_coef, s.P, s.Q, s.R, s.nr, s.persist, scr, flg, b,
                                          vec, st);
@@ -896,8 +896,9 @@ fmm_status fmm_plan_set_schedule(fmm_plan* p, int schedule) {
 }
 
 fmm_status fmm_plan_set_fusion(fmm_plan* p, int mode) {
-  if (!p || mode < 0 || mode > 2) { set_error("fmm_plan_set_fusion: bad args"); return FMM_E_ARG; }
-  p->fusion = mode;
+  if (!p || mode < 0 || mode > 3) { set_error("fmm_plan_set_fusion: bad args"); return FMM_E_ARG; }
+  p->fusion = mode == 3 ? 1 : mode;
+  p->persistent = mode == 3;
   return compile_plan(p);
 }
 

@@ -194,6 +194,7 @@ cudaError_t launch_gemm_f64_persistent(const FusedNode* dev_nodes, int count, in
                                        int NR, int ctas, double* scratch, int* flags,
                                        const Bases& b, bool vec, cudaStream_t st);
 size_t persistent_scratch_bytes(int ctas, int NR);
+int64_t persistent_max_tail_units(int ctas);
 int persistent_min_kt();
 cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, const LeafNode* host_leaves, int count,
                             int64_t m, int64_t n, int64_t k, const Bases& b, bool vec, int leaf,

@@ -545,65 +545,46 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   cp_wait<0>();
 }
 
-// K2P: the fused leaf products (K2F) as a persistent, hybrid data-parallel / stream-K kernel.
-// A unit is (parent, 128x128 output tile) with NR products; T = units x NR product-tiles.
-// Grid = one CTA per SM (G).  Units 0 .. G*floor(U/G)-1 go data-parallel (CTA c: units
-// c, c+G, ...: concurrent CTAs work on neighbouring tiles, as in K2F); the remaining U mod G
-// units' product-tiles are split evenly across the G CTAs in contiguous ranges (stream-K), so
-// every CTA does the same number of product-tiles to within one.  A unit whose products span
-// several CTAs is finished by its OWNER (the CTA holding its product 0): the other CTAs compute
-// their products of it FIRST (before their data-parallel units) into a scratch slot and raise a
-// flag; the owner, after its own products of that unit (its last work), waits for the flags and
-// applies the scratch products in ascending r with the same epilogue -- so every element of C_k
-// still sees c = w*m, c = c + w*m in ascending r (bitwise K2F / K3), and owners only ever wait
-// for work that was scheduled first (no deadlock with G co-resident CTAs).
+// K2P: the fused leaf products (K2F) as a persistent kernel (one CTA per SM) with dynamic
+// work distribution.  A unit is (parent, 128x128 output tile) with NR products.  Work is one
+// counter (atomicAdd) over [0, U_dp) data-parallel units -- a CTA runs all NR products of the
+// unit with K2F's epilogue, and the active units stay a contiguous window, as in K2F's grid
+// order (L2 reuse of the S_r / T_r panels) -- followed by [U_dp, U_dp + T_tail) stream-K
+// product-tiles of the last U - U_dp units (U mod G plus one wave): each is one product into a
+// scratch slot with a ready flag, and the CTA that computes product NR-1 of a unit (taken last)
+// applies the unit's NR products from scratch in ascending r with the same epilogue -- every
+// element of C_k still sees c = w*m, c = c + w*m in ascending r (bitwise K2F / K3).  The
+// finisher only waits for tiles handed out before its own, which run on co-resident CTAs, so
+// the kernel cannot deadlock with G <= #SMs; CTAs end within about one product of each other.
 template <typename C, bool VEC>
 __global__ void __launch_bounds__(C::THREADS, 1)
     k2p_gemm_f64(const FusedNode* __restrict__ nodes, const double* __restrict__ coef_all,
                  Bases bases, int64_t m, int64_t n, int64_t k, int tiles_m, int tiles_n, int P,
-                 int Q, int R, int NR, int64_t U, double* __restrict__ scratch,
-                 int* __restrict__ flags) {
+                 int Q, int R, int NR, int64_t U, int64_t U_dp, double* __restrict__ scratch,
+                 int* __restrict__ flags, unsigned long long* __restrict__ counter) {
   static_assert(C::PIPE, "the fused kernel uses the PIPE mainloop");
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + C::STAGES * C::A_STAGE;
-  __shared__ int flag_ok;
+  __shared__ int64_t next_work;
 
-  const int G = gridDim.x, cta = blockIdx.x;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int g = lane >> 2, t = lane & 3;
   const int tiles = tiles_m * tiles_n;
+  const int64_t T_tail = (U - U_dp) * NR;
+  const int64_t W = U_dp + T_tail;  // work indices
 
-  // ---- this CTA's work list (constants kept in shared memory: registers go to the mainloop) -
-  __shared__ int64_t wl[6];  // dp_units, n_dp, T_tail, s0, n_lead, n_own_tail
-  if (tid == 0) {
-    const int64_t dp = (U / G) * G, tt = (U - dp) * NR;
-    const int64_t a0 = (int64_t)cta * tt / G, a1 = (int64_t)(cta + 1) * tt / G;
-    const int64_t lead_max = NR - a0 % NR;
-    const int64_t nl = (a0 % NR) ? (lead_max < a1 - a0 ? lead_max : a1 - a0) : 0;  // non-owner
-    wl[0] = dp; wl[1] = U / G; wl[2] = tt; wl[3] = a0; wl[4] = nl; wl[5] = (a1 - a0) - nl;
-  }
-  __syncthreads();
-#define dp_units wl[0]
-#define n_dp wl[1]
-#define T_tail wl[2]
-#define s0 wl[3]
-#define n_lead wl[4]
-#define n_own_tail wl[5]
-  const int64_t n_items = n_lead + n_dp * NR + n_own_tail;
-  // item i -> (unit, product index ri, role): 0 lead (scratch), 1 owned
-  auto item = [&](int64_t i, int64_t& u, int& ri, int& lead) {
-    if (i < n_lead) {
-      u = dp_units + s0 / NR; ri = (int)(s0 % NR) + (int)i; lead = 1;
-    } else if (i < n_lead + n_dp * NR) {
-      const int64_t j = i - n_lead;
-      u = cta + (j / NR) * G; ri = (int)(j % NR); lead = 0;
-    } else {
-      const int64_t q = s0 + n_lead + (i - n_lead - n_dp * NR);
-      u = dp_units + q / NR; ri = (int)(q % NR); lead = 0;
-    }
+  auto grab = [&]() {  // thread 0 only
+    const int64_t x = (int64_t)atomicAdd(counter, 1ull);
+    next_work = x < W ? x : -1;
+  };
+  // product j of work item w -> (unit, ri); number of products of w
+  auto nprod = [&](int64_t w) { return w < U_dp ? NR : 1; };
+  auto prod_of = [&](int64_t w, int j, int64_t& u, int& ri) {
+    if (w < U_dp) { u = w; ri = j; }
+    else { const int64_t q = w - U_dp; u = U_dp + q / NR; ri = (int)(q % NR); }
   };
   auto tile_coords = [&](int64_t u, int64_t& m0, int64_t& n0, const FusedNode*& nd) {
     nd = nodes + u / tiles;
@@ -615,31 +596,24 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     m0 = (int64_t)(first_m + (tile % per_group) % gsz) * C::BM;
     n0 = (int64_t)((tile % per_group) / gsz) * C::BN;
   };
-  // operands of item i with the tile offset folded in: A + m0 lda, B + n0, remaining rows /
-  // columns mr = m - m0, nr = n - n0 (32-bit: leaf dims and leading dimensions < 2^31)
+  // operands with the tile offset folded in: A + m0 lda, B + n0, remaining rows / cols
   struct Opnd {
     const double* A;
     const double* B;
-    int lda, ldb, mr, nr;
+    int64_t lda, ldb, mr, nr;
   };
-  auto operands = [&](int64_t i) {
+  auto operands = [&](int64_t u, int ri) {
     Opnd o;
-    int64_t u, m0, n0, la, lb;
-    int ri, lead;
-    item(i, u, ri, lead);
+    int64_t m0, n0;
     const FusedNode* nd;
     tile_coords(u, m0, n0, nd);
-    o.A = op_ptr<const double>(bases, nd->a[ri], la) + m0 * la;
-    o.B = op_ptr<const double>(bases, nd->b[ri], lb) + n0;
-    o.lda = (int)la; o.ldb = (int)lb; o.mr = (int)(m - m0); o.nr = (int)(n - n0);
+    const double* a0 = op_ptr<const double>(bases, nd->a[ri], o.lda);
+    const double* b0 = op_ptr<const double>(bases, nd->b[ri], o.ldb);
+    o.A = a0 + m0 * o.lda;
+    o.B = b0 + n0;
+    o.mr = m - m0;
+    o.nr = n - n0;
     return o;
-  };
-  // scratch slot of stream-K product-tile q held by a non-owner CTA: (cta(q), position)
-  auto slot_of = [&](int64_t q) {
-    int64_t c = q * G / T_tail;
-    while (c + 1 < G && (c + 1) * T_tail / G <= q) ++c;
-    while (c > 0 && c * T_tail / G > q) --c;
-    return c * NR + (q - c * T_tail / G);
   };
 
   double acc[C::MI][C::NI][4];
@@ -651,8 +625,6 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
   };
-  zero_acc();
-  if (n_items == 0) return;
 
   // W-combination of product ri of node nd at tile (m0, n0) from acc (K2F's RED epilogue)
   auto epilogue = [&](const FusedNode* nd, int ri, int64_t m0, int64_t n0) {
@@ -709,7 +681,6 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       unsigned ns = 32;
       while (atomicAdd(&flags[slot], 0) == 0) { __nanosleep(ns); if (ns < 1024) ns *= 2; }
       __threadfence();
-      flag_ok = 1;
     }
     __syncthreads();
     const double* sp = scratch + slot * NACC * C::THREADS + tid;
@@ -722,7 +693,6 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   };
 
   const int KT = (int)((k + C::BK - 1) / C::BK);  // >= STAGES (host-checked)
-  const int64_t total = n_items * KT;
   constexpr int KQ = C::BK / 4;
   static_assert(KQ % 2 == 0, "even number of k-slices per stage");
   double af[2][C::MI][2], bf[2][C::NI];
@@ -738,8 +708,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 #pragma unroll
     for (int j = 0; j < C::NI; ++j) bf[buf][j] = bs[kk * C::B_LD + j * 8];
   };
-  auto ktile = [&](int64_t it, auto&& refill) {
-    const int slot = (int)(it % C::STAGES);
+  // one k-tile; `refill(slot)` loads k-tile it + STAGES; `last` = no k-tile follows
+  auto ktile = [&](int it, bool last, auto&& refill) {
+    const int slot = it % C::STAGES;
 #pragma unroll
     for (int q = 0; q < KQ; ++q) {
       const int cur = q & 1;
@@ -748,7 +719,7 @@ __global__ void __launch_bounds__(C::THREADS, 1)
         __syncthreads();
         refill(slot);
         cp_commit();
-        if (it + 1 < total) load_frag(cur ^ 1, (int)((it + 1) % C::STAGES), 0);
+        if (!last) load_frag(cur ^ 1, (it + 1) % C::STAGES, 0);
       } else {
         load_frag(cur ^ 1, slot, (q + 1) * 4);
       }
@@ -759,8 +730,17 @@ __global__ void __launch_bounds__(C::THREADS, 1)
     }
   };
 
-  {  // prologue: the first STAGES k-tiles of item 0
-    const Opnd o = operands(0);
+  // ---- first work item ------------------------------------------------------------------
+  if (tid == 0) grab();
+  __syncthreads();
+  int64_t w = next_work;
+  if (w < 0) return;
+  int j = 0;  // product index within w
+  {
+    int64_t u;
+    int ri;
+    prod_of(w, 0, u, ri);
+    const Opnd o = operands(u, ri);
 #pragma unroll
     for (int s = 0; s < C::STAGES - 1; ++s) {
       load_tiles<C, VEC>(As + s * C::A_STAGE, Bs + s * C::B_STAGE, o.A, o.lda, o.B, o.ldb, o.mr, o.nr,
@@ -773,51 +753,65 @@ __global__ void __launch_bounds__(C::THREADS, 1)
                        o.lda, o.B, o.ldb, o.mr, o.nr, k, 0, 0, (int64_t)(C::STAGES - 1) * C::BK, tid);
     cp_commit();
   }
+  zero_acc();
   load_frag(0, 0, 0);
-  int64_t it = 0;
-  for (int64_t i = 0; i < n_items; ++i) {
-    const Opnd o = operands(i);
-    for (int kt = 0; kt < KT - C::STAGES; ++kt, ++it)
-      ktile(it, [&](int slot) {
-        load_tiles<C, VEC>(As + slot * C::A_STAGE, Bs + slot * C::B_STAGE, o.A, o.lda, o.B, o.ldb,
-                           o.mr, o.nr, k, 0, 0, (int64_t)(kt + C::STAGES) * C::BK, tid);
-      });
-    const bool more = i + 1 < n_items;
-    const Opnd on = more ? operands(i + 1) : o;
-    for (int j = 0; j < C::STAGES; ++j, ++it)
-      ktile(it, [&](int slot) {
-        if (more)
-          load_tiles<C, VEC>(As + slot * C::A_STAGE, Bs + slot * C::B_STAGE, on.A, on.lda, on.B,
-                             on.ldb, on.mr, on.nr, k, 0, 0, (int64_t)j * C::BK, tid);
-      });
+  int it = 0;
+  while (true) {
     int64_t u;
-    int ri, lead;
-    item(i, u, ri, lead);
-    if (lead) {
-      store_scratch((int64_t)cta * NR + i);
-    } else {
+    int ri;
+    prod_of(w, j, u, ri);
+    const bool last_of_item = j + 1 == nprod(w);
+    if (last_of_item) {  // take the next work item now: its first tiles load during this product
+      if (tid == 0) grab();
+      __syncthreads();
+    }
+    const int64_t w_next = last_of_item ? next_work : w;
+    const int j_next = last_of_item ? 0 : j + 1;
+    const bool more = w_next >= 0;
+    {
+      const Opnd o = operands(u, ri);
+      for (int kt = 0; kt < KT - C::STAGES; ++kt, ++it)
+        ktile(it, false, [&](int slot) {
+          load_tiles<C, VEC>(As + slot * C::A_STAGE, Bs + slot * C::B_STAGE, o.A, o.lda, o.B,
+                             o.ldb, o.mr, o.nr, k, 0, 0, (int64_t)(kt + C::STAGES) * C::BK, tid);
+        });
+    }
+    {
+      int64_t un = u;
+      int rn = ri;
+      if (more) prod_of(w_next, j_next, un, rn);
+      const Opnd on = operands(un, rn);
+      for (int jj = 0; jj < C::STAGES; ++jj, ++it)
+        ktile(it, !more && jj == C::STAGES - 1, [&](int slot) {
+          if (more)
+            load_tiles<C, VEC>(As + slot * C::A_STAGE, Bs + slot * C::B_STAGE, on.A, on.lda, on.B,
+                               on.ldb, on.mr, on.nr, k, 0, 0, (int64_t)jj * C::BK, tid);
+        });
+    }
+    if (w < U_dp) {
       const FusedNode* nd;
       int64_t m0, n0;
       tile_coords(u, m0, n0, nd);
       epilogue(nd, ri, m0, n0);
-      if (i == n_items - 1 && n_own_tail > 0 && ri + 1 < NR) {
-        // owner fix-up: the unit's remaining products come from later CTAs' scratch
-        const int64_t qbase = (u - dp_units) * NR;
-        for (int r2 = ri + 1; r2 < NR; ++r2) {
-          load_scratch(slot_of(qbase + r2));
+    } else {
+      const int64_t q = w - U_dp;
+      store_scratch(q);
+      if (ri == NR - 1) {  // finisher: the unit's products in ascending r
+        const FusedNode* nd;
+        int64_t m0, n0;
+        tile_coords(u, m0, n0, nd);
+        for (int r2 = 0; r2 < NR; ++r2) {
+          load_scratch(q - (NR - 1) + r2);
           epilogue(nd, r2, m0, n0);
         }
       }
     }
     zero_acc();
+    if (!more) break;
+    w = w_next;
+    j = j_next;
   }
   cp_wait<0>();
-#undef dp_units
-#undef n_dp
-#undef T_tail
-#undef s0
-#undef n_lead
-#undef n_own_tail
 }
 
 template <typename C, bool VEC, bool RED>
@@ -948,22 +942,31 @@ cudaError_t launch_gemm_f64_persistent(const FusedNode* dev_nodes, int count, in
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
   const int tiles_m = (int)((m + Cf::BM - 1) / Cf::BM), tiles_n = (int)((n + Cf::BN - 1) / Cf::BN);
   const int64_t U = (int64_t)count * tiles_m * tiles_n;
-  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)ctas * NR, st);
+  // stream-K tail: the last (U mod G) units plus one more wave when there is a full wave to spare
+  int64_t tail_units = U % ctas;
+  if (U - tail_units >= 2 * (int64_t)ctas) tail_units += ctas;
+  if (tail_units > persistent_max_tail_units(ctas)) tail_units = U % ctas;
+  const int64_t U_dp = U - tail_units;
+  unsigned long long* counter = (unsigned long long*)(flags + (size_t)2 * ctas * NR);
+  cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)2 * ctas * NR + 16, st);
   if (e != cudaSuccess) return e;
   auto go = [&](auto kern) {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           Cf::SMEM_BYTES);
     if (e2 != cudaSuccess) return e2;
     kern<<<ctas, Cf::THREADS, Cf::SMEM_BYTES, st>>>(dev_nodes, dev_coef, b, m, n, k, tiles_m, tiles_n,
-                                                    P, Q, R, NR, U, scratch, flags);
+                                                    P, Q, R, NR, U, U_dp, scratch, flags, counter);
     return cudaGetLastError();
   };
   return vec ? go(k2p_gemm_f64<Cf, true>) : go(k2p_gemm_f64<Cf, false>);
 }
 
+// scratch: one 128x128 tile per stream-K product-tile (at most 2 G units x NR) + flags + counter
+int64_t persistent_max_tail_units(int ctas) { return 2 * (int64_t)ctas; }
 size_t persistent_scratch_bytes(int ctas, int NR) {
   using Cf = V16;
-  return (size_t)ctas * NR * (size_t)(Cf::BM * Cf::BN) * sizeof(double) + (size_t)ctas * NR * sizeof(int) + 512;
+  const size_t tiles = (size_t)persistent_max_tail_units(ctas) * NR;
+  return tiles * (size_t)(Cf::BM * Cf::BN) * sizeof(double) + tiles * sizeof(int) + 512;
 }
 
 int persistent_min_kt() { return V16::STAGES; }

@@ -283,8 +283,9 @@ class Plan:
         return {"xi": xi.value, "delta": de.value, "uniform_bound": ub.value}
 
     def set_fusion(self, mode):
-        """Leaf-product epilogue fusion of the parents' W-combination: 'off' | 'on' | 'auto'."""
-        _call("fmm_plan_set_fusion", self._h, {"off": 0, "on": 1, "auto": 2}[mode])
+        """Leaf-product epilogue fusion of the parents' W-combination:
+        'off' | 'on' | 'auto' | 'persistent' (the stream-K form, K2P)."""
+        _call("fmm_plan_set_fusion", self._h, {"off": 0, "on": 1, "auto": 2, "persistent": 3}[mode])
         self._ws = None
 
     def fused_launches(self) -> int:

@@ -107,16 +107,14 @@ def test_nonuniform_plan_validation():
 
 
 def test_fusion_auto_policy():
-    # auto (FP64): with >= 4 k-tiles per leaf the fused leaves run as the persistent stream-K
-    # kernel (K2P), fused when the product-tiles (parents x 128^2 tiles x R) fill the 148 SMs;
-    # otherwise the grid kernel K2F needs >= 4 waves at >= 90 % wave efficiency
+    # auto (FP64): fuse the leaf-parent level when parents x 128^2 leaf tiles fill >= 4 waves
+    # of 148 SMs at >= 90 % wave efficiency (the grid kernel K2F)
     w, s, c = (fb.Rule.builtin(n) for n in ("winograd", "strassen", "classical222"))
-    cases = [([w, w], (512,) * 3, 0),                 # C1: 7 parents x 1 tile x 7 = 49 < 148
-             ([s] * 4, (4096,) * 3, 1),               # C2: 343 x 4 units
-             ([w, c, s], (8192, 4096, 8192), 1),     # C3: 56 x 64
-             ([w] * 3, (4096,) * 3, 1),               # C4: 49 x 16
-             ([w] * 3, (32768,) * 3, 7),              # C5: depth-first, 7 x 1024 per subtree
-             ([w] * 3, (64, 24, 64), 0)]              # 3 k-tiles per leaf: K2F waves rule
+    cases = [([w, w], (512,) * 3, 0),                 # C1: 7 parents x 1 tile
+             ([s] * 4, (4096,) * 3, 1),               # C2: 343 x 4 = 1372 (9.3 waves, 93 %)
+             ([w, c, s], (8192, 4096, 8192), 1),     # C3: 56 x 64 = 3584 (97 %)
+             ([w] * 3, (4096,) * 3, 0),               # C4: 49 x 16 = 784 (5.3 waves, 88 %)
+             ([w] * 3, (32768,) * 3, 7)]              # C5: depth-first, 7 x 1024 per subtree
     for rules, (M, K, N), want in cases:
         p = fb.Plan(rules, M, K, N)
         assert p.fused_launches() == want, (M, want)

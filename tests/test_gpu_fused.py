@@ -175,9 +175,20 @@ def test_persistent_stream_k_equals_unfused(fb, dims, names):
     # unfused K2 + K3 (includes ragged tiles: 1000 / 600 are not multiples of 128)
     M, K, N = dims
     A, B = fi.random_pair(M, K, N, seed=M // 7)
-    pf = plan(fb, names, M, K, N, "on")
+    pf = plan(fb, names, M, K, N, "persistent")
     assert pf.fused_launches() >= 1
     Cf = exe(pf, A, B)
     Cu = exe(plan(fb, names, M, K, N, "off"), A, B)
     assert np.array_equal(Cf, Cu)
     assert np.array_equal(Cf, exe(pf, A, B))  # deterministic across runs
+    assert np.array_equal(Cf, exe(plan(fb, names, M, K, N, "on"), A, B))
+
+
+@pytest.mark.parametrize("pname", sorted(PLANS))
+def test_persistent_small_problems(fb, pname):
+    # fewer product-tiles than CTAs: most units are split over several CTAs (chains of scratch
+    # products finished by the owner)
+    names = PLANS[pname]
+    A, B = fi.random_pair(512, 384, 256, seed=23)
+    Cp = exe(plan(fb, names, 512, 384, 256, "persistent"), A, B)
+    assert np.array_equal(Cp, exe(plan(fb, names, 512, 384, 256, "off"), A, B))
