@@ -910,6 +910,12 @@ int variant() {
 cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
                             int64_t k, const Bases& b, bool vec, cudaStream_t st) {
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
+  // small batches (fewer 128x128 tiles than two per SM, e.g. C1: 49 leaves of 128^2): 64x64
+  // tiles at 3 CTAs per SM give 4x the CTAs (profiles/r01_k2_variants.md: V13 is within 1 % of
+  // V16 on large problems)
+  const int64_t t128 = ((m + 127) / 128) * ((n + 127) / 128) * (int64_t)count;
+  if (!getenv("FMM_K2_VARIANT") && t128 < 2 * 148)
+    return launch_cfg<V13>(dev_leaves, count, m, n, k, b, vec, st);
   switch (variant()) {
     case 2: return launch_cfg<V2>(dev_leaves, count, m, n, k, b, vec, st);
     case 3: return launch_cfg<V3>(dev_leaves, count, m, n, k, b, vec, st);
