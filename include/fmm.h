@@ -146,6 +146,14 @@ fmm_status fmm_plan_set_schedule(fmm_plan* plan, int schedule);
  * at fmm_plan_create. */
 fmm_status fmm_plan_set_fusion(fmm_plan* plan, int mode);
 
+/* Operand fusion (host-only): in a fused leaf level, every S_r / T_r whose
+ * U / V column has at most two nonzero +-1 entries (Strassen, classical: all; S-W: 5 of 7 per
+ * operand) is not written by K1: the fused leaf kernel loads the parent blocks' tiles and
+ * combines them in shared memory with K1's sequential sum (bitwise identical results).  Saves
+ * the leaf level's S / T writes and reads.  FP64, leaf inner dimension >= 48; default off (the
+ * environment variable FMM_OPF=1 turns it on at fmm_plan_create). */
+fmm_status fmm_plan_set_operand_fusion(fmm_plan* plan, int enable);
+
 /* Host-only query: number of fused leaf-product launches (K2F) in the compiled schedule. */
 fmm_status fmm_plan_fused_launches(const fmm_plan* plan, int64_t* n);
 

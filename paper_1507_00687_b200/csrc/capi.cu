@@ -112,6 +112,7 @@ struct fmm_plan {
   int fusion = 2;    // W-combination of the leaves' parents in the leaf GEMM epilogue: 0 off, 1 on, 2 auto
   int shard_depth = 1;  // multi-GPU: units = paths of the first shard_depth levels, round-robin
   bool persistent = false;  // fused leaves as the persistent stream-K kernel (K2P) where eligible
+  bool operand_fusion = false;  // S_r / T_r with <= 2 +-1 terms formed inside the fused leaf kernel
   ncclComm_t comm = nullptr;
   // compiled schedule
   std::vector<Step> steps;
@@ -203,6 +204,10 @@ struct Builder {
   struct Node {
     int64_t idx;  // BFS index within level
     Op a, b, c;
+    // operand fusion: S = sa0 a + sa1 a2 (na sources), T = sb0 b + sb1 b2 (nb sources)
+    Op a2{}, b2{};
+    int8_t sa0 = 1, sa1 = 1, sb0 = 1, sb1 = 1;
+    uint8_t na = 1, nb = 1;
   };
 
   const RuleData& rule_at(int l, int64_t idx) { return p->rules[p->node_rule[l][idx]]; }
@@ -217,7 +222,27 @@ struct Builder {
   }
 
   // K1 for the active nodes of level l (columns in `only_r` if >= 0); returns child nodes.
-  std::vector<Node> emit_k1(int l, const std::vector<Node>& nodes, int only_r, bool alloc_c = true) {
+  // A U / V column with at most two nonzero +-1 entries (operand fusion candidate): rows
+  // (ascending) and signs.
+  static bool small_col(const RuleData& r, const std::vector<int32_t>& X, int rows, int col,
+                        int* i0, int* s0, int* i1, int* s1, int* cnt) {
+    *cnt = 0;
+    const int32_t one = 1 << r.log2den;
+    for (int i = 0; i < rows; ++i) {
+      const int32_t x = X[(size_t)i * r.R + col];
+      if (x == 0) continue;
+      if (x != one && x != -one) return false;
+      if (*cnt == 0) { *i0 = i; *s0 = x > 0 ? 1 : -1; }
+      else if (*cnt == 1) { *i1 = i; *s1 = x > 0 ? 1 : -1; }
+      if (++*cnt > 2) return false;
+    }
+    return *cnt >= 1;
+  }
+
+  // opf: leave S_r / T_r whose column has <= 2 nonzero +-1 entries unformed; the fused leaf
+  // kernel combines the parent's blocks while staging its tiles (same sequential sum).
+  std::vector<Node> emit_k1(int l, const std::vector<Node>& nodes, int only_r, bool alloc_c = true,
+                            bool opf = false) {
     const int64_t mb = p->lm[l + 1], kb = p->lk[l + 1], nb = p->ln[l + 1];
     std::vector<K1Node> ks, kt;
     std::vector<Node> kids;
@@ -233,9 +258,14 @@ struct Builder {
         if (only_r >= 0 && r != only_r) continue;
         Node ch;
         ch.idx = nd.idx * ru.R + r;
-        int row;
+        int row, i0 = 0, i1 = 0, s0 = 1, s1 = 1, cnt = 0;
         if (trivial_col(ru, ru.U, ru.m0 * ru.k0, r, &row)) {
           ch.a = sub(nd.a, (row % ru.m0) * mb, (row / ru.m0) * kb);
+        } else if (opf && small_col(ru, ru.U, ru.m0 * ru.k0, r, &i0, &s0, &i1, &s1, &cnt)) {
+          ch.a = sub(nd.a, (i0 % ru.m0) * mb, (i0 / ru.m0) * kb);
+          ch.sa0 = (int8_t)s0;
+          ch.na = (uint8_t)cnt;
+          if (cnt == 2) { ch.a2 = sub(nd.a, (i1 % ru.m0) * mb, (i1 / ru.m0) * kb); ch.sa1 = (int8_t)s1; }
         } else {
           ch.a = ws_op(ws_alloc(mb * kb), kb);
           s.out[r] = ch.a;
@@ -243,6 +273,11 @@ struct Builder {
         }
         if (trivial_col(ru, ru.V, ru.k0 * ru.n0, r, &row)) {
           ch.b = sub(nd.b, (row % ru.k0) * kb, (row / ru.k0) * nb);
+        } else if (opf && small_col(ru, ru.V, ru.k0 * ru.n0, r, &i0, &s0, &i1, &s1, &cnt)) {
+          ch.b = sub(nd.b, (i0 % ru.k0) * kb, (i0 / ru.k0) * nb);
+          ch.sb0 = (int8_t)s0;
+          ch.nb = (uint8_t)cnt;
+          if (cnt == 2) { ch.b2 = sub(nd.b, (i1 % ru.k0) * kb, (i1 / ru.k0) * nb); ch.sb1 = (int8_t)s1; }
         } else {
           ch.b = ws_op(ws_alloc(kb * nb), nb);
           t.out[r] = ch.b;
@@ -295,6 +330,9 @@ struct Builder {
   // than the unfused leaf GEMM; auto mode fuses when that grid (parents x 128x128 output tiles
   // of a leaf, one CTA per SM) still fills the 148 SMs in >= 4 waves at >= 90 % wave
   // efficiency (measured: profiles/r01_fusion.md).
+  // operand fusion in the fused leaf kernel (FP64, leaf inner dimension >= STAGES k-tiles)
+  bool opf_on() const { return p->operand_fusion && p->dtype == FMM_F64 && (p->lk[p->L] + 15) / 16 >= 3; }
+
   bool fuse_leaves(int64_t nparents) const {
     if (p->dtype != FMM_F64 || p->fusion == 0) return false;
     if (p->fusion == 1) return true;
@@ -333,6 +371,11 @@ struct Builder {
         f.first[f.nr] = wm & ~started;
         f.a[f.nr] = ch.a;
         f.b[f.nr] = ch.b;
+        f.a2[f.nr] = ch.a2;
+        f.b2[f.nr] = ch.b2;
+        f.sa[f.nr][0] = ch.sa0; f.sa[f.nr][1] = ch.sa1;
+        f.sb[f.nr][0] = ch.sb0; f.sb[f.nr][1] = ch.sb1;
+        f.na[f.nr] = ch.na; f.nb[f.nr] = ch.nb;
         started |= wm;
         ++f.nr;
       }
@@ -347,9 +390,10 @@ struct Builder {
     st.rows = p->lm[p->L]; st.cols = p->ln[p->L]; st.inner = p->lk[p->L];
     st.P = r0.m0; st.Q = r0.n0; st.R = r0.R;
     st.nr = fz[0].nr;
+    st.opf = opf_on() ? 1 : 0;
     st.arena_off = -1;
     // persistent hybrid data-parallel / stream-K form (K2P) when the leaf has >= STAGES k-tiles
-    if (p->persistent && (st.inner + 15) / 16 >= persistent_min_kt()) {
+    if (p->persistent && !st.opf && (st.inner + 15) / 16 >= persistent_min_kt()) {
       st.persist = kPersistCtas;
       st.arena_off = ws_alloc((int64_t)((persistent_scratch_bytes(kPersistCtas, st.nr) + 7) / 8));
     }
@@ -382,7 +426,7 @@ struct Builder {
     std::vector<std::vector<Node>> lv{nodes};
     for (int d = l; d < p->L - 1; ++d) lv.push_back(emit_k1(d, lv.back(), -1));
     const bool fuse = fuse_leaves((int64_t)lv.back().size());
-    lv.push_back(emit_k1(p->L - 1, lv.back(), -1, !fuse));
+    lv.push_back(emit_k1(p->L - 1, lv.back(), -1, !fuse, fuse && opf_on()));
     int top = p->L - 1;
     if (fuse) {
       emit_k2f(p->L - 1, lv[p->L - 1 - l], lv.back(), -1, nullptr);
@@ -456,7 +500,7 @@ struct Builder {
       ws_elems = mark;  // subtrees run one after another on one stream: reuse the workspace
       const size_t g0 = p->steps.size();
       const bool fuse1 = leaf_next && fuse_leaves(1);
-      std::vector<Node> kid = emit_k1(l, {node}, r, !fuse1);
+      std::vector<Node> kid = emit_k1(l, {node}, r, !fuse1, fuse1 && opf_on());
       if (fuse1) {
         emit_k2f(l, {node}, kid, r, &started);
       } else {
@@ -640,7 +684,7 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
                                          vec, st);
         } else {
           e = launch_gemm_f64_fused((const FusedNode*)nd, s.count, s.rows, s.cols, s.inner,
-                                    p->dev_coef, s.P, s.Q, s.R, b, vec, st);
+                                    p->dev_coef, s.P, s.Q, s.R, b, vec, st, s.opf != 0);
         }
         break;
       case STEP_K2:
@@ -797,6 +841,7 @@ fmm_status fmm_plan_create(const fmm_rule* const* nodes, int n_nodes, int levels
   auto p = new fmm_plan();
   p->dtype = dtype; p->leaf = leaf; p->L = levels; p->M = M; p->K = K; p->N = N;
   if (const char* pe = getenv("FMM_K2P")) p->persistent = atoi(pe) != 0;
+  if (const char* oe = getenv("FMM_OPF")) p->operand_fusion = atoi(oe) != 0;
   if (const char* fe = getenv("FMM_FUSION")) {
     const int f = atoi(fe);
     if (f >= 0 && f <= 2) p->fusion = f;
@@ -899,6 +944,12 @@ fmm_status fmm_plan_set_fusion(fmm_plan* p, int mode) {
   if (!p || mode < 0 || mode > 3) { set_error("fmm_plan_set_fusion: bad args"); return FMM_E_ARG; }
   p->fusion = mode == 3 ? 1 : mode;
   p->persistent = mode == 3;
+  return compile_plan(p);
+}
+
+fmm_status fmm_plan_set_operand_fusion(fmm_plan* p, int enable) {
+  if (!p) { set_error("fmm_plan_set_operand_fusion: null"); return FMM_E_ARG; }
+  p->operand_fusion = enable != 0;
   return compile_plan(p);
 }
 
@@ -1245,6 +1296,7 @@ static const fmm_plan* depth_first_twin(const fmm_plan* p) {
     t->scaling = p->scaling; t->coef_U = p->coef_U; t->coef_V = p->coef_V; t->coef_W = p->coef_W;
     t->coef_host = p->coef_host; t->schedule = 2; t->fusion = p->fusion; t->shard_depth = p->shard_depth;
     t->persistent = p->persistent;
+    t->operand_fusion = p->operand_fusion;
     if (compile_plan(t) != FMM_OK) { delete t; return nullptr; }
     p->df_twin = t;
   }

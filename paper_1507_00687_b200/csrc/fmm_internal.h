@@ -145,6 +145,11 @@ struct FusedNode {
   uint32_t wmask[kMaxR];  // bit k: w_kr != 0
   uint32_t first[kMaxR];  // bit k: this product initialises C_k
   Op a[kMaxR], b[kMaxR];  // leaf operands S_r, T_r (index i, not r)
+  // operand fusion (fmm_plan_set_operand_fusion): S_i = sa[i][0] a[i] + sa[i][1] a2[i] formed
+  // while staging tiles (na[i] = 1 or 2 sources, signs +-1), likewise T_i from b / b2
+  Op a2[kMaxR], b2[kMaxR];
+  int8_t sa[kMaxR][2], sb[kMaxR][2];
+  uint8_t na[kMaxR], nb[kMaxR];
 };
 
 enum StepKind { STEP_K1 = 1, STEP_K2 = 2, STEP_K3 = 3, STEP_ACC = 4, STEP_ZERO = 5, STEP_K2F = 8 };
@@ -159,6 +164,7 @@ struct Step {
                      // K2F persistent (K2P): offset of the scratch tiles + flags in ws
   bool vec_ok;       // all ws offsets / dims allow 16-byte vectors (caller bases checked later)
   int nr = 0;        // K2F: products per node (uniform)
+  int opf = 0;       // K2F: operands formed in the kernel from up to two sources (na / nb)
   int persist = 0;   // K2F: run as the persistent stream-K kernel with this many CTAs (0: grid)
 };
 
@@ -185,7 +191,7 @@ cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, in
                             int64_t k, const Bases& b, bool vec, cudaStream_t st);
 cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                   int64_t k, const double* dev_coef, int P, int Q, int R,
-                                  const Bases& b, bool vec, cudaStream_t st);
+                                  const Bases& b, bool vec, cudaStream_t st, bool opf = false);
 // K2P: persistent hybrid data-parallel / stream-K form of K2F (one CTA per SM, `ctas` CTAs;
 // every node has NR products).  scratch / flags: persistent_scratch_bytes(ctas, NR) of
 // workspace (flags zeroed by the launcher).  Needs ceil(k / BK) >= persistent_min_kt().

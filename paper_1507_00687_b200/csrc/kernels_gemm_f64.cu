@@ -545,6 +545,294 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   cp_wait<0>();
 }
 
+// K2O: K2F with operand fusion.  A product's S_i = sa0 X + sa1 Y is not
+// materialised by K1: the kernel loads the tiles of both parent blocks X, Y (cp.async into two
+// slots of the stage) and, once the stage has landed, combines them in place in shared memory
+// -- v = sa0*x (exact negation), v = v + sa1*y (one rounding): K1's sequential sum, bitwise --
+// before the stage's fragments are read.  Same for T_i.  A stage holds two A and two B slots,
+// so the pipeline has 3 stages (221 KB).  Products whose operand is a single +1 source skip the
+// combine; products with wider sums use their materialised S / T as a single source.
+template <typename C, bool VEC>
+__device__ __forceinline__ void load_a_tile(double* As, const double* A, int64_t lda, int64_t m,
+                                            int64_t k, int64_t m0, int64_t k0, int tid) {
+  if constexpr (VEC) {
+    constexpr int ACH = C::BK / 2;
+#pragma unroll
+    for (int q = 0; q < C::BM * C::BK / 2 / C::THREADS; ++q) {
+      int c = tid + q * C::THREADS;
+      int row = c / ACH, cc = (c % ACH) * 2;
+      int64_t gr = m0 + row, gc = k0 + cc;
+      bool ok = gr < m && gc < k;
+      cp16(smem_u32(As + row * C::A_LD + cc), ok ? A + gr * lda + gc : A, ok);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < C::BM * C::BK / C::THREADS; ++q) {
+      int c = tid + q * C::THREADS;
+      int row = c / C::BK, cc = c % C::BK;
+      int64_t gr = m0 + row, gc = k0 + cc;
+      bool ok = gr < m && gc < k;
+      cp8(smem_u32(As + row * C::A_LD + cc), ok ? A + gr * lda + gc : A, ok);
+    }
+  }
+}
+template <typename C, bool VEC>
+__device__ __forceinline__ void load_b_tile(double* Bs, const double* B, int64_t ldb, int64_t n,
+                                            int64_t k, int64_t n0, int64_t k0, int tid) {
+  if constexpr (VEC) {
+    constexpr int BCH = C::BN / 2;
+#pragma unroll
+    for (int q = 0; q < C::BK * C::BN / 2 / C::THREADS; ++q) {
+      int c = tid + q * C::THREADS;
+      int row = c / BCH, cc = (c % BCH) * 2;
+      int64_t gr = k0 + row, gc = n0 + cc;
+      bool ok = gr < k && gc < n;
+      cp16(smem_u32(Bs + row * C::B_LD + cc), ok ? B + gr * ldb + gc : B, ok);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < C::BK * C::BN / C::THREADS; ++q) {
+      int c = tid + q * C::THREADS;
+      int row = c / C::BN, cc = c % C::BN;
+      int64_t gr = k0 + row, gc = n0 + cc;
+      bool ok = gr < k && gc < n;
+      cp8(smem_u32(Bs + row * C::B_LD + cc), ok ? B + gr * ldb + gc : B, ok);
+    }
+  }
+}
+
+template <typename C, bool VEC>
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
+    k2o_gemm_f64(const FusedNode* __restrict__ nodes, const double* __restrict__ coef_all,
+                 Bases bases, int64_t m, int64_t n, int64_t k, int tiles_m, int tiles_n, int P,
+                 int Q, int R) {
+  static_assert(C::PIPE && C::STAGES == 3, "operand fusion: PIPE mainloop, 3 stages");
+  constexpr int ASZ = 2 * C::A_STAGE, BSZ = 2 * C::B_STAGE;  // two source slots per stage
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;
+  double* Bs = smem + C::STAGES * ASZ;
+  __shared__ const double* pa[kMaxR];
+  __shared__ const double* pb[kMaxR];
+  __shared__ const double* pa2[kMaxR];
+  __shared__ const double* pb2[kMaxR];
+  __shared__ int64_t la[kMaxR], lb[kMaxR], la2[kMaxR], lb2[kMaxR];
+  __shared__ uint32_t wm_s[kMaxR], fm_s[kMaxR];
+  __shared__ int r_s[kMaxR];
+  __shared__ int8_t na_s[kMaxR], nb_s[kMaxR], sa_s[kMaxR][2], sb_s[kMaxR][2];
+  __shared__ double wcf[kMaxBlk * kMaxR];
+
+  const FusedNode& nd = nodes[blockIdx.y];
+  const int nr = nd.nr;
+  const int tid = threadIdx.x;
+  if (tid < nr) {
+    int64_t l;
+    pa[tid] = op_ptr<const double>(bases, nd.a[tid], l);
+    la[tid] = l;
+    pb[tid] = op_ptr<const double>(bases, nd.b[tid], l);
+    lb[tid] = l;
+    na_s[tid] = (int8_t)nd.na[tid];
+    nb_s[tid] = (int8_t)nd.nb[tid];
+    sa_s[tid][0] = nd.sa[tid][0]; sa_s[tid][1] = nd.sa[tid][1];
+    sb_s[tid][0] = nd.sb[tid][0]; sb_s[tid][1] = nd.sb[tid][1];
+    pa2[tid] = nd.na[tid] == 2 ? op_ptr<const double>(bases, nd.a2[tid], l) : nullptr;
+    la2[tid] = nd.na[tid] == 2 ? l : 0;
+    pb2[tid] = nd.nb[tid] == 2 ? op_ptr<const double>(bases, nd.b2[tid], l) : nullptr;
+    lb2[tid] = nd.nb[tid] == 2 ? l : 0;
+    wm_s[tid] = nd.wmask[tid];
+    fm_s[tid] = nd.first[tid];
+    r_s[tid] = nd.rlist[tid];
+  }
+  for (int t = tid; t < P * Q * R; t += C::THREADS) wcf[t] = coef_all[nd.coef_off + t];
+  __syncthreads();
+
+  const int tile = blockIdx.x;
+  const int per_group = GROUP_M * tiles_n;
+  const int group = tile / per_group;
+  const int first_m = group * GROUP_M;
+  const int gsz = min(tiles_m - first_m, GROUP_M);
+  const int tm = first_m + (tile % per_group) % gsz;
+  const int tn = (tile % per_group) / gsz;
+  const int64_t m0 = (int64_t)tm * C::BM, n0 = (int64_t)tn * C::BN;
+
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int g = lane >> 2, t = lane & 3;
+
+  double acc[C::MI][C::NI][4];
+  auto zero_acc = [&]() {
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int j = 0; j < C::NI; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[i][j][e] = 0.0;
+  };
+  zero_acc();
+  const int KT = (int)((k + C::BK - 1) / C::BK);  // >= STAGES (host-checked)
+  const int total = nr * KT;
+
+  // all source tiles of product ri at k-tile kt into stage `slot`
+  auto load_stage = [&](int slot, int ri, int kt) {
+    const int64_t k0 = (int64_t)kt * C::BK;
+    load_a_tile<C, VEC>(As + slot * ASZ, pa[ri], la[ri], m, k, m0, k0, tid);
+    if (na_s[ri] == 2) load_a_tile<C, VEC>(As + slot * ASZ + C::A_STAGE, pa2[ri], la2[ri], m, k, m0, k0, tid);
+    load_b_tile<C, VEC>(Bs + slot * BSZ, pb[ri], lb[ri], n, k, n0, k0, tid);
+    if (nb_s[ri] == 2) load_b_tile<C, VEC>(Bs + slot * BSZ + C::B_STAGE, pb2[ri], lb2[ri], n, k, n0, k0, tid);
+  };
+  // combine the sources of stage `slot` (product ri) in place: K1's sequential sum
+  auto combine = [&](int slot, int ri) {
+    const int na = na_s[ri], nbq = nb_s[ri];
+    const double a0 = sa_s[ri][0], a1 = sa_s[ri][1], b0 = sb_s[ri][0], b1 = sb_s[ri][1];
+    if (na == 2 || a0 < 0) {
+      double* x = As + slot * ASZ;
+      const double* y = x + C::A_STAGE;
+#pragma unroll
+      for (int q = 0; q < C::BM * C::BK / 2 / C::THREADS; ++q) {
+        const int c = tid + q * C::THREADS;
+        const int off = (c / (C::BK / 2)) * C::A_LD + (c % (C::BK / 2)) * 2;
+        double2 v = *reinterpret_cast<double2*>(x + off);
+        v.x = a0 < 0 ? -v.x : v.x;
+        v.y = a0 < 0 ? -v.y : v.y;
+        if (na == 2) {
+          const double2 w = *reinterpret_cast<const double2*>(y + off);
+          v.x = __dadd_rn(v.x, a1 < 0 ? -w.x : w.x);
+          v.y = __dadd_rn(v.y, a1 < 0 ? -w.y : w.y);
+        }
+        *reinterpret_cast<double2*>(x + off) = v;
+      }
+    }
+    if (nbq == 2 || b0 < 0) {
+      double* x = Bs + slot * BSZ;
+      const double* y = x + C::B_STAGE;
+#pragma unroll
+      for (int q = 0; q < C::BK * C::BN / 2 / C::THREADS; ++q) {
+        const int c = tid + q * C::THREADS;
+        const int off = (c / (C::BN / 2)) * C::B_LD + (c % (C::BN / 2)) * 2;
+        double2 v = *reinterpret_cast<double2*>(x + off);
+        v.x = b0 < 0 ? -v.x : v.x;
+        v.y = b0 < 0 ? -v.y : v.y;
+        if (nbq == 2) {
+          const double2 w = *reinterpret_cast<const double2*>(y + off);
+          v.x = __dadd_rn(v.x, b1 < 0 ? -w.x : w.x);
+          v.y = __dadd_rn(v.y, b1 < 0 ? -w.y : w.y);
+        }
+        *reinterpret_cast<double2*>(x + off) = v;
+      }
+    }
+  };
+  auto needs_combine = [&](int ri) {
+    return na_s[ri] == 2 || nb_s[ri] == 2 || sa_s[ri][0] < 0 || sb_s[ri][0] < 0;
+  };
+
+  auto epilogue = [&](int ri) {
+    const uint32_t wmask = wm_s[ri], fmask = fm_s[ri];
+    const int r = r_s[ri];
+    int64_t ldo;
+    double* out = op_ptr<double>(bases, nd.out, ldo);
+    for (int kk = 0; kk < P * Q; ++kk) {
+      if (!((wmask >> kk) & 1u)) continue;
+      const double w = wcf[kk * R + r];
+      const bool first = (fmask >> kk) & 1u;
+      double* ob = out + (int64_t)(kk / Q) * m * ldo + (int64_t)(kk % Q) * n;
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int64_t row = m0 + wm * C::WTM + i * 16 + g + h * 8;
+          if (row >= m) continue;
+#pragma unroll
+          for (int j = 0; j < C::NI; ++j) {
+            const int64_t col = n0 + wn * C::WTN + j * 8 + 2 * t;
+            double* cp = ob + row * ldo + col;
+            const double v0 = __dmul_rn(w, acc[i][j][2 * h]), v1 = __dmul_rn(w, acc[i][j][2 * h + 1]);
+            if (first) {
+              if (VEC && col + 1 < n) {
+                *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
+              } else {
+                if (col < n) cp[0] = v0;
+                if (col + 1 < n) cp[1] = v1;
+              }
+            } else {
+              if (col < n) red_add(cp, v0);
+              if (col + 1 < n) red_add(cp + 1, v1);
+            }
+          }
+        }
+    }
+  };
+
+  constexpr int KQ = C::BK / 4;
+  double af[2][C::MI][2], bf[2][C::NI];
+  const int a_off = (wm * C::WTM + g) * C::A_LD + t, b_off = t * C::B_LD + wn * C::WTN + g;
+  auto load_frag = [&](int buf, int slot, int kk) {
+    const double* as = As + slot * ASZ + a_off;
+    const double* bs = Bs + slot * BSZ + b_off;
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i) {
+      af[buf][i][0] = as[(i * 16) * C::A_LD + kk];
+      af[buf][i][1] = as[(i * 16 + 8) * C::A_LD + kk];
+    }
+#pragma unroll
+    for (int j = 0; j < C::NI; ++j) bf[buf][j] = bs[kk * C::B_LD + j * 8];
+  };
+  // one k-tile: before the next stage's first fragments are read, its sources are combined
+  auto ktile = [&](int it, auto&& refill) {
+    const int slot = it % C::STAGES;
+#pragma unroll
+    for (int q = 0; q < KQ; ++q) {
+      const int cur = q & 1;
+      if (q == KQ - 1) {
+        cp_wait<C::STAGES - 2>();
+        __syncthreads();
+        refill(slot);
+        cp_commit();
+        if (it + 1 < total) {
+          const int rn = (it + 1) / KT;
+          if (needs_combine(rn)) {
+            combine((it + 1) % C::STAGES, rn);
+            __syncthreads();
+          }
+          load_frag(cur ^ 1, (it + 1) % C::STAGES, 0);
+        }
+      } else {
+        load_frag(cur ^ 1, slot, (q + 1) * 4);
+      }
+#pragma unroll
+      for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) dmma16n8k4(acc[i][j], af[cur][i][0], af[cur][i][1], bf[cur][j]);
+    }
+  };
+
+#pragma unroll
+  for (int s = 0; s < C::STAGES - 1; ++s) {
+    load_stage(s, 0, s);
+    cp_commit();
+  }
+  cp_wait<C::STAGES - 2>();
+  __syncthreads();
+  load_stage(C::STAGES - 1, 0, C::STAGES - 1);
+  cp_commit();
+  if (needs_combine(0)) {
+    combine(0, 0);
+    __syncthreads();
+  }
+  load_frag(0, 0, 0);
+  int it = 0;
+  for (int ri = 0; ri < nr; ++ri) {
+    for (int kt = 0; kt < KT - C::STAGES; ++kt, ++it)
+      ktile(it, [&](int slot) { load_stage(slot, ri, kt + C::STAGES); });
+    const bool more = ri + 1 < nr;
+    for (int j = 0; j < C::STAGES; ++j, ++it)
+      ktile(it, [&](int slot) {
+        if (more) load_stage(slot, ri + 1, j);
+      });
+    epilogue(ri);
+    zero_acc();
+  }
+  cp_wait<0>();
+}
+
 // K2P: the fused leaf products (K2F) as a persistent kernel (one CTA per SM) with dynamic
 // work distribution.  A unit is (parent, 128x128 output tile) with NR products.  Work is one
 // counter (atomicAdd) over [0, U_dp) data-parallel units -- a CTA runs all NR products of the
@@ -987,10 +1275,24 @@ int fused_variant() {
 }
 }  // namespace
 
+using VO = Cfg<128, 128, 16, 3, 2, 4, 1, true>;  // operand-fused K2O: 3 stages x (2 A + 2 B slots)
+
 cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                   int64_t k, const double* dev_coef, int P, int Q, int R,
-                                  const Bases& b, bool vec, cudaStream_t st) {
+                                  const Bases& b, bool vec, cudaStream_t st, bool opf) {
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
+  if (opf) {
+    const int tiles_m = (int)((m + VO::BM - 1) / VO::BM), tiles_n = (int)((n + VO::BN - 1) / VO::BN);
+    constexpr int smem = VO::STAGES * 2 * (VO::A_STAGE + VO::B_STAGE) * 8;
+    auto go = [&](auto kern) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e != cudaSuccess) return e;
+      kern<<<dim3((unsigned)(tiles_m * tiles_n), (unsigned)count), VO::THREADS, smem, st>>>(
+          dev_nodes, dev_coef, b, m, n, k, tiles_m, tiles_n, P, Q, R);
+      return cudaGetLastError();
+    };
+    return vec ? go(k2o_gemm_f64<VO, true>) : go(k2o_gemm_f64<VO, false>);
+  }
   switch (fused_variant()) {
     case 13: return launch_fused_cfg<V13>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
     case 15: return launch_fused_cfg<V15>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);

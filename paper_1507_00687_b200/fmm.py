@@ -44,6 +44,7 @@ SIGNATURES = {
     "fmm_plan_set_schedule": (_I, [_P, _I]),
     "fmm_plan_set_fusion": (_I, [_P, _I]),
     "fmm_plan_set_shard_depth": (_I, [_P, _I]),
+    "fmm_plan_set_operand_fusion": (_I, [_P, _I]),
     "fmm_rule_quantities": (_I, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double), _P, _P]),
     "fmm_plan_stability": (_I, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "fmm_choose_variants": (_I, [_P, _P, _I, _P, C.POINTER(C.c_double)]),
@@ -286,6 +287,11 @@ class Plan:
         """Leaf-product epilogue fusion of the parents' W-combination:
         'off' | 'on' | 'auto' | 'persistent' (the stream-K form, K2P)."""
         _call("fmm_plan_set_fusion", self._h, {"off": 0, "on": 1, "auto": 2, "persistent": 3}[mode])
+        self._ws = None
+
+    def set_operand_fusion(self, enable: bool = True):
+        """Form S_r / T_r with <= 2 +-1 terms inside the fused leaf kernel (no K1 writes)."""
+        _call("fmm_plan_set_operand_fusion", self._h, int(enable))
         self._ws = None
 
     def fused_launches(self) -> int:

@@ -139,3 +139,14 @@ def test_shard_depth_units_and_balance():
         assert abs(7 ** depth / (P * max(len(o) for o in owned)) - cap) < 1e-12
     with pytest.raises(fb.FmmError):
         p.set_shard_depth(4)
+
+
+def test_operand_fusion_skips_leaf_level_formation():
+    # Strassen: every U / V column has <= 2 +-1 entries, so the leaf level's K1 writes nothing
+    s = fb.Rule.builtin("strassen")
+    p = fb.Plan([s] * 3, 2048, 2048, 2048)
+    p.set_fusion("on")
+    n0, w0 = p.launch_count(), p.workspace_bytes()
+    p.set_operand_fusion(True)
+    assert p.launch_count() == n0 - 2  # no leaf-level K1 for S or T
+    assert p.workspace_bytes() < w0

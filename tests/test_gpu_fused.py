@@ -192,3 +192,26 @@ def test_persistent_small_problems(fb, pname):
     A, B = fi.random_pair(512, 384, 256, seed=23)
     Cp = exe(plan(fb, names, 512, 384, 256, "persistent"), A, B)
     assert np.array_equal(Cp, exe(plan(fb, names, 512, 384, 256, "off"), A, B))
+
+
+@pytest.mark.parametrize("pname", sorted(PLANS))
+@pytest.mark.parametrize("dims", [(512, 384, 256), (4 * 75, 4 * 33, 4 * 41)])
+def test_operand_fusion_bitwise(fb, pname, dims):
+    # S_r / T_r with <= 2 +-1 terms combined in shared memory while staging (K2O): bitwise the
+    # unfused path (K1's sequential sum); odd leaf dims exercise the 8-byte path
+    names = PLANS[pname]
+    M, K, N = dims
+    A, B = fi.random_pair(M, K, N, seed=M + 3)
+    po = plan(fb, names, M, K, N, "on")
+    po.set_operand_fusion(True)
+    Co = exe(po, A, B)
+    assert np.array_equal(Co, exe(plan(fb, names, M, K, N, "off"), A, B))
+
+
+def test_operand_fusion_C2_full_size(fb):
+    A, B = fi.config_inputs("C2")
+    po = plan(fb, ("strassen",) * 4, 4096, 4096, 4096, "auto")
+    po.set_operand_fusion(True)
+    pu = plan(fb, ("strassen",) * 4, 4096, 4096, 4096, "off")
+    assert po.workspace_bytes() < pu.workspace_bytes()
+    assert np.array_equal(exe(po, A, B), exe(pu, A, B))
