@@ -113,6 +113,7 @@ struct fmm_plan {
   int shard_depth = 1;  // multi-GPU: units = paths of the first shard_depth levels, round-robin
   bool persistent = false;  // fused leaves as the persistent stream-K kernel (K2P) where eligible
   bool operand_fusion = false;  // S_r / T_r with <= 2 +-1 terms formed inside the fused leaf kernel
+  bool split_chains = true;     // fused units' product chains split over CTAs (turnstiles)
   ncclComm_t comm = nullptr;
   // compiled schedule
   std::vector<Step> steps;
@@ -326,16 +327,65 @@ struct Builder {
   }
 
   // Is the leaf-parent level fused (K2F) for `nparents` parents?  FP64 only.  A fused CTA runs
-  // all R products of its parent, so the fused grid has R times fewer, R times longer CTAs
-  // than the unfused leaf GEMM; auto mode fuses when that grid (parents x 128x128 output tiles
-  // of a leaf, one CTA per SM) still fills the 148 SMs in >= 4 waves at >= 90 % wave
-  // efficiency (measured: profiles/r01_fusion.md).
+  // all R products of its parent's tile (or a chunk of them, chains split with turnstiles), so
+  // the fused grid has up to R times fewer, longer CTAs than the unfused leaf GEMM; auto mode
+  // fuses when that grid (parents x 128x128 output tiles of a leaf, one CTA per SM) fills the
+  // 148 SMs in >= 4 waves at >= 90 % wave efficiency, or when a chain split brings the
+  // simulated efficiency to >= 93 % (measured: profiles/r01_fusion_variants.md).
   // operand fusion in the fused leaf kernel (FP64, leaf inner dimension >= STAGES k-tiles)
   bool opf_on() const { return p->operand_fusion && p->dtype == FMM_F64 && (p->lk[p->L] + 15) / 16 >= 3; }
+
+  // Simulated makespan (in product durations) of the fused grid when each unit's R-product
+  // chain is split into groups of `chunk` products, dispatched group-major onto kSMs SMs in
+  // order (one CTA per SM), each item costing its products plus a pipeline fill of
+  // STAGES / KT products; group g of a unit cannot finish before group g-1 of that unit.
+  static double fused_makespan(int64_t units, int R, int chunk, int KT) {
+    constexpr int kSMs = 148;
+    const int groups = (R + chunk - 1) / chunk;
+    const double fill = 4.0 / std::max(KT, 1);
+    std::vector<double> sm(kSMs, 0.0), prev(units, 0.0);
+    double span = 0;
+    for (int g = 0; g < groups; ++g) {
+      const int np = std::min(R, (g + 1) * chunk) - g * chunk;
+      for (int64_t u = 0; u < units; ++u) {
+        auto it = std::min_element(sm.begin(), sm.end());
+        const double start = *it;
+        const double fin = std::max(start + np + fill, g ? prev[u] + 0.1 : 0.0);
+        *it = fin;
+        prev[u] = fin;
+        span = std::max(span, fin);
+      }
+    }
+    return span;
+  }
+  // best chain split for a fused leaf level (chunk = R: no split); efficiency out
+  static int best_chunk(int64_t units, int R, int KT, double* eff) {
+    int best = R;
+    double best_span = fused_makespan(units, R, R, KT);
+    if (KT >= 4 && units <= (1 << 16)) {
+      for (int groups = 2; groups <= 3; ++groups) {
+        const int c = (R + groups - 1) / groups;
+        const double sp = fused_makespan(units, R, c, KT);
+        if (sp < best_span * 0.995) { best_span = sp; best = c; }
+      }
+    }
+    if (eff) *eff = (double)units * R / (148.0 * best_span);
+    return best;
+  }
 
   bool fuse_leaves(int64_t nparents) const {
     if (p->dtype != FMM_F64 || p->fusion == 0) return false;
     if (p->fusion == 1) return true;
+    {  // chain splitting (turnstiles) smooths the wave quantisation of R-product units
+      const int64_t tiles = ((p->lm[p->L] + 127) / 128) * ((p->ln[p->L] + 127) / 128);
+      const int R = p->rules[p->node_rule[p->L - 1][0]].R;
+      const int KT = (int)((p->lk[p->L] + 15) / 16);
+      double eff = 0;
+      if (p->split_chains && KT >= 4 && nparents * tiles >= 148 && nparents * tiles * R >= 4 * 148) {
+        best_chunk(nparents * tiles, R, KT, &eff);
+        if (eff >= 0.93) return true;
+      }
+    }
     constexpr int64_t kSMs = 148;
     const int64_t tiles = ((p->lm[p->L] + 127) / 128) * ((p->ln[p->L] + 127) / 128);
     const int64_t units = nparents * tiles;
@@ -393,6 +443,15 @@ struct Builder {
     st.opf = opf_on() ? 1 : 0;
     st.arena_off = -1;
     // persistent hybrid data-parallel / stream-K form (K2P) when the leaf has >= STAGES k-tiles
+    // chain split with per-unit turnstiles (breadth-first levels: every parent has all R products)
+    if (p->split_chains && fz.size() > 0 && fz[0].nr == r0.R && (st.inner + 15) / 16 >= 4) {
+      const int64_t tiles = ((st.rows + 127) / 128) * ((st.cols + 127) / 128);
+      const int c = best_chunk((int64_t)st.count * tiles, r0.R, (int)((st.inner + 15) / 16), nullptr);
+      if (c < r0.R) {
+        st.chunk = c;
+        st.turn_off = ws_alloc((st.count * tiles + 1) / 2 + 1);  // ints, in 8-byte elements
+      }
+    }
     if (p->persistent && !st.opf && (st.inner + 15) / 16 >= persistent_min_kt()) {
       st.persist = kPersistCtas;
       st.arena_off = ws_alloc((int64_t)((persistent_scratch_bytes(kPersistCtas, st.nr) + 7) / 8));
@@ -684,7 +743,9 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
                                          vec, st);
         } else {
           e = launch_gemm_f64_fused((const FusedNode*)nd, s.count, s.rows, s.cols, s.inner,
-                                    p->dev_coef, s.P, s.Q, s.R, b, vec, st, s.opf != 0);
+                                    p->dev_coef, s.P, s.Q, s.R, b, vec, st, s.opf != 0, s.nr,
+                                    s.chunk,
+                                    s.turn_off >= 0 ? (int*)((double*)b.p[BASE_WS] + s.turn_off) : nullptr);
         }
         break;
       case STEP_K2:
@@ -842,6 +903,7 @@ fmm_status fmm_plan_create(const fmm_rule* const* nodes, int n_nodes, int levels
   p->dtype = dtype; p->leaf = leaf; p->L = levels; p->M = M; p->K = K; p->N = N;
   if (const char* pe = getenv("FMM_K2P")) p->persistent = atoi(pe) != 0;
   if (const char* oe = getenv("FMM_OPF")) p->operand_fusion = atoi(oe) != 0;
+  if (const char* ce = getenv("FMM_SPLIT")) p->split_chains = atoi(ce) != 0;
   if (const char* fe = getenv("FMM_FUSION")) {
     const int f = atoi(fe);
     if (f >= 0 && f <= 2) p->fusion = f;
@@ -1297,6 +1359,7 @@ static const fmm_plan* depth_first_twin(const fmm_plan* p) {
     t->coef_host = p->coef_host; t->schedule = 2; t->fusion = p->fusion; t->shard_depth = p->shard_depth;
     t->persistent = p->persistent;
     t->operand_fusion = p->operand_fusion;
+    t->split_chains = p->split_chains;
     if (compile_plan(t) != FMM_OK) { delete t; return nullptr; }
     p->df_twin = t;
   }

@@ -165,6 +165,9 @@ struct Step {
   bool vec_ok;       // all ws offsets / dims allow 16-byte vectors (caller bases checked later)
   int nr = 0;        // K2F: products per node (uniform)
   int opf = 0;       // K2F: operands formed in the kernel from up to two sources (na / nb)
+  int chunk = 0;     // K2F: products per CTA when a unit's chain is split (0: whole chain);
+                     // turnstiles (one int per unit) at ws offset turn_off (bytes)
+  int64_t turn_off = -1;
   int persist = 0;   // K2F: run as the persistent stream-K kernel with this many CTAs (0: grid)
 };
 
@@ -191,7 +194,8 @@ cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, in
                             int64_t k, const Bases& b, bool vec, cudaStream_t st);
 cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                   int64_t k, const double* dev_coef, int P, int Q, int R,
-                                  const Bases& b, bool vec, cudaStream_t st, bool opf = false);
+                                  const Bases& b, bool vec, cudaStream_t st, bool opf = false,
+                                  int nr = 0, int chunk = 0, int* turn = nullptr);
 // K2P: persistent hybrid data-parallel / stream-K form of K2F (one CTA per SM, `ctas` CTAs;
 // every node has NR products).  scratch / flags: persistent_scratch_bytes(ctas, NR) of
 // workspace (flags zeroed by the launcher).  Needs ceil(k / BK) >= persistent_min_kt().

@@ -285,7 +285,7 @@ template <typename C, bool VEC, bool RED, bool FLAT>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
     k2f_gemm_f64(const FusedNode* __restrict__ nodes, const double* __restrict__ coef_all,
                  Bases bases, int64_t m, int64_t n, int64_t k, int tiles_m, int tiles_n, int P,
-                 int Q, int R) {
+                 int Q, int R, int count, int chunk, int* __restrict__ turn) {
   static_assert(C::PIPE, "the fused kernel uses the PIPE mainloop");
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
@@ -297,18 +297,25 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   __shared__ int r_s[kMaxR];
   __shared__ double wcf[kMaxBlk * kMaxR];
 
-  const FusedNode& nd = nodes[blockIdx.y];
-  const int nr = nd.nr;
+  // product chain split (chunk < nr): grid.y = group * count + parent, groups dispatched in
+  // order; group g runs products [g*chunk, (g+1)*chunk) of its unit after group g-1 released
+  // the unit's turnstile (so every C_k element still sees ascending r)
+  const int parent = blockIdx.y % count, grp = blockIdx.y / count;
+  const FusedNode& nd = nodes[parent];
+  const int nr_all = nd.nr;
+  const int r_begin = grp * chunk;
+  const int nr = min(nr_all, r_begin + chunk) - r_begin;  // products of this CTA
   const int tid = threadIdx.x;
   if (tid < nr) {
+    const int q = r_begin + tid;
     int64_t l;
-    pa[tid] = op_ptr<const double>(bases, nd.a[tid], l);
+    pa[tid] = op_ptr<const double>(bases, nd.a[q], l);
     la[tid] = l;
-    pb[tid] = op_ptr<const double>(bases, nd.b[tid], l);
+    pb[tid] = op_ptr<const double>(bases, nd.b[q], l);
     lb[tid] = l;
-    wm_s[tid] = nd.wmask[tid];
-    fm_s[tid] = nd.first[tid];
-    r_s[tid] = nd.rlist[tid];
+    wm_s[tid] = nd.wmask[q];
+    fm_s[tid] = nd.first[q];
+    r_s[tid] = nd.rlist[q];
   }
   for (int t = tid; t < P * Q * R; t += C::THREADS) wcf[t] = coef_all[nd.coef_off + t];
   __syncthreads();
@@ -353,6 +360,27 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
         lA = pa[l_ri]; lB = pb[l_ri]; lla = la[l_ri]; llb = lb[l_ri];
       }
     }
+  };
+  int* my_turn = turn ? turn + (int64_t)parent * gridDim.x + blockIdx.x : nullptr;
+  auto turn_wait = [&]() {  // before this CTA's first epilogue: group grp-1 is done with the unit
+    if (grp == 0 || !my_turn) return;
+    if (tid == 0) {
+      unsigned ns = 64;
+      long long spins = 0;
+      while (atomicAdd(my_turn, 0) < grp) {
+        __nanosleep(ns);
+        if (ns < 2048) ns *= 2;
+        if (++spins > (1ll << 24)) __trap();  // > ~30 s: fail loudly instead of hanging
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  };
+  auto turn_release = [&]() {  // after the last epilogue: hand the unit to group grp+1
+    if (!my_turn || r_begin + nr >= nr_all) return;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicExch(my_turn, grp + 1);
   };
   auto epilogue = [&](int ri) {
     const uint32_t wmask = wm_s[ri], fmask = fm_s[ri];
@@ -492,7 +520,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     for (int it = 0; it < total; ++it) {
       ktile(it, [&](int slot) { if (it + C::STAGES < total) load_next(slot); });
       if (++kt_in_r == KT) {
+        if (ri == 0) turn_wait();
         epilogue(ri);
+        if (ri == nr - 1) turn_release();
         zero_acc();
         kt_in_r = 0;
         ++ri;
@@ -538,7 +568,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
             load_tiles<C, VEC>(As + slot * C::A_STAGE, Bs + slot * C::B_STAGE, An, ldan, Bn, ldbn,
                                m, n, k, m0, n0, (int64_t)j * C::BK, tid);
         });
+      if (ri == 0) turn_wait();
       epilogue(ri);
+      if (ri == nr - 1) turn_release();
       zero_acc();
     }
   }
@@ -967,7 +999,12 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   auto load_scratch = [&](int64_t slot) {
     if (tid == 0) {
       unsigned ns = 32;
-      while (atomicAdd(&flags[slot], 0) == 0) { __nanosleep(ns); if (ns < 1024) ns *= 2; }
+      long long spins = 0;
+      while (atomicAdd(&flags[slot], 0) == 0) {
+        __nanosleep(ns);
+        if (ns < 1024) ns *= 2;
+        if (++spins > (1ll << 25)) __trap();  // > ~30 s: fail loudly instead of hanging
+      }
       __threadfence();
     }
     __syncthreads();
@@ -1105,16 +1142,22 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 template <typename C, bool VEC, bool RED>
 cudaError_t launch_fused_kernel(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                 int64_t k, const double* coef, int P, int Q, int R,
-                                const Bases& b, cudaStream_t st) {
+                                const Bases& b, cudaStream_t st, int nr, int chunk, int* turn) {
   const int tiles_m = (int)((m + C::BM - 1) / C::BM), tiles_n = (int)((n + C::BN - 1) / C::BN);
-  dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)count);
   const int KT = (int)std::max<int64_t>(1, (k + C::BK - 1) / C::BK);
+  if (chunk <= 0 || chunk >= nr || KT < C::STAGES || !turn) chunk = nr;  // no split
+  const int groups = (nr + chunk - 1) / chunk;
+  if (groups > 1) {
+    cudaError_t e = cudaMemsetAsync(turn, 0, sizeof(int) * (size_t)count * tiles_m * tiles_n, st);
+    if (e != cudaSuccess) return e;
+  }
+  dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)(count * groups));
   auto go = [&](auto kern) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     kern<<<grid, C::THREADS, C::SMEM_BYTES, st>>>(dev_nodes, coef, b, m, n, k, tiles_m, tiles_n, P,
-                                                  Q, R);
+                                                  Q, R, count, chunk, groups > 1 ? turn : nullptr);
     return cudaGetLastError();
   };
   if (KT >= C::STAGES) return go(k2f_gemm_f64<C, VEC, RED, false>);
@@ -1132,13 +1175,13 @@ int fused_red() {
 template <typename C>
 cudaError_t launch_fused_cfg(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                              int64_t k, const double* coef, int P, int Q, int R, const Bases& b,
-                             bool vec, cudaStream_t st) {
+                             bool vec, cudaStream_t st, int nr, int chunk, int* turn) {
   if (fused_red()) {
-    return vec ? launch_fused_kernel<C, true, true>(dev_nodes, count, m, n, k, coef, P, Q, R, b, st)
-               : launch_fused_kernel<C, false, true>(dev_nodes, count, m, n, k, coef, P, Q, R, b, st);
+    return vec ? launch_fused_kernel<C, true, true>(dev_nodes, count, m, n, k, coef, P, Q, R, b, st, nr, chunk, turn)
+               : launch_fused_kernel<C, false, true>(dev_nodes, count, m, n, k, coef, P, Q, R, b, st, nr, chunk, turn);
   }
-  return vec ? launch_fused_kernel<C, true, false>(dev_nodes, count, m, n, k, coef, P, Q, R, b, st)
-             : launch_fused_kernel<C, false, false>(dev_nodes, count, m, n, k, coef, P, Q, R, b, st);
+  return vec ? launch_fused_kernel<C, true, false>(dev_nodes, count, m, n, k, coef, P, Q, R, b, st, nr, chunk, turn)
+             : launch_fused_kernel<C, false, false>(dev_nodes, count, m, n, k, coef, P, Q, R, b, st, nr, chunk, turn);
 }
 
 template <typename C>
@@ -1279,7 +1322,8 @@ using VO = Cfg<128, 128, 16, 3, 2, 4, 1, true>;  // operand-fused K2O: 3 stages 
 
 cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                   int64_t k, const double* dev_coef, int P, int Q, int R,
-                                  const Bases& b, bool vec, cudaStream_t st, bool opf) {
+                                  const Bases& b, bool vec, cudaStream_t st, bool opf, int nr,
+                                  int chunk, int* turn) {
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
   if (opf) {
     const int tiles_m = (int)((m + VO::BM - 1) / VO::BM), tiles_n = (int)((n + VO::BN - 1) / VO::BN);
@@ -1294,12 +1338,12 @@ cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t
     return vec ? go(k2o_gemm_f64<VO, true>) : go(k2o_gemm_f64<VO, false>);
   }
   switch (fused_variant()) {
-    case 13: return launch_fused_cfg<V13>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
-    case 15: return launch_fused_cfg<V15>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
-    case 17: return launch_fused_cfg<V17>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
-    case 18: return launch_fused_cfg<V18>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
-    case 20: return launch_fused_cfg<V20>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
-    default: return launch_fused_cfg<V16>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st);
+    case 13: return launch_fused_cfg<V13>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st, nr, chunk, turn);
+    case 15: return launch_fused_cfg<V15>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st, nr, chunk, turn);
+    case 17: return launch_fused_cfg<V17>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st, nr, chunk, turn);
+    case 18: return launch_fused_cfg<V18>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st, nr, chunk, turn);
+    case 20: return launch_fused_cfg<V20>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st, nr, chunk, turn);
+    default: return launch_fused_cfg<V16>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st, nr, chunk, turn);
   }
 }
 

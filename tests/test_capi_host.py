@@ -113,7 +113,7 @@ def test_fusion_auto_policy():
     cases = [([w, w], (512,) * 3, 0),                 # C1: 7 parents x 1 tile
              ([s] * 4, (4096,) * 3, 1),               # C2: 343 x 4 = 1372 (9.3 waves, 93 %)
              ([w, c, s], (8192, 4096, 8192), 1),     # C3: 56 x 64 = 3584 (97 %)
-             ([w] * 3, (4096,) * 3, 0),               # C4: 49 x 16 = 784 (5.3 waves, 88 %)
+             ([w] * 3, (4096,) * 3, 1),               # C4: 49 x 16 = 784: chains split in 2 (turnstiles)
              ([w] * 3, (32768,) * 3, 7)]              # C5: depth-first, 7 x 1024 per subtree
     for rules, (M, K, N), want in cases:
         p = fb.Plan(rules, M, K, N)

@@ -215,3 +215,17 @@ def test_operand_fusion_C2_full_size(fb):
     pu = plan(fb, ("strassen",) * 4, 4096, 4096, 4096, "off")
     assert po.workspace_bytes() < pu.workspace_bytes()
     assert np.array_equal(exe(po, A, B), exe(pu, A, B))
+
+
+@pytest.mark.parametrize("dims,names", [((2048, 2048, 2048), ("winograd",) * 3),   # chunks 4 + 3
+                                        ((3072, 3072, 3072), ("winograd",) * 2)])  # chunks 3 + 3 + 1
+def test_split_chains_equal_unfused(fb, dims, names):
+    # units whose R-product chain is split over 2-3 CTAs ordered by per-unit turnstiles (the
+    # split is chosen by the plan's makespan model): bitwise the unfused K2 + K3, deterministic
+    M, K, N = dims
+    A, B = fi.random_pair(M, K, N, seed=K // 64)
+    pa = plan(fb, names, M, K, N, "on")
+    assert pa.fused_launches() == 1
+    Cf = exe(pa, A, B)
+    assert np.array_equal(Cf, exe(plan(fb, names, M, K, N, "off"), A, B))
+    assert np.array_equal(Cf, exe(pa, A, B))
