@@ -251,9 +251,11 @@ struct Builder {
       const RuleData& ru = rule_at(l, nd.idx);
       K1Node s{};
       s.in = nd.a;
+      s.rows = mb; s.cols = kb; s.P = ru.m0; s.Q = ru.k0;
       s.coef_off = p->coef_U[p->node_rule[l][nd.idx]];
       K1Node t{};
       t.in = nd.b;
+      t.rows = kb; t.cols = nb; t.P = ru.k0; t.Q = ru.n0;
       t.coef_off = p->coef_V[p->node_rule[l][nd.idx]];
       for (int r = 0; r < ru.R; ++r) {
         if (only_r >= 0 && r != only_r) continue;
@@ -292,21 +294,19 @@ struct Builder {
       if (s.out_mask) ks.push_back(s);
       if (t.out_mask) kt.push_back(t);
     }
+    // every S_r and T_r of the level in one launch (per-node dims in the descriptors)
     const RuleData& r0 = rule_at(l, nodes[0].idx);
-    if (!ks.empty()) {
+    std::vector<K1Node> all = ks;
+    all.insert(all.end(), kt.begin(), kt.end());
+    if (!all.empty()) {
       Step st{};
       st.kind = STEP_K1;
-      st.count = (int)ks.size();
-      st.dev_off = push(ks);
-      st.rows = mb; st.cols = kb; st.P = r0.m0; st.Q = r0.k0; st.R = r0.R;
-      p->steps.push_back(st);
-    }
-    if (!kt.empty()) {
-      Step st{};
-      st.kind = STEP_K1;
-      st.count = (int)kt.size();
-      st.dev_off = push(kt);
-      st.rows = kb; st.cols = nb; st.P = r0.k0; st.Q = r0.n0; st.R = r0.R;
+      st.count = (int)all.size();
+      st.dev_off = push(all);
+      st.rows = ks.empty() ? kb : kt.empty() ? mb : std::max(mb, kb);
+      st.cols = ks.empty() ? nb : kt.empty() ? kb : std::max(kb, nb);
+      const int blk = std::max(ks.empty() ? 0 : r0.m0 * r0.k0, kt.empty() ? 0 : r0.k0 * r0.n0);
+      st.P = blk; st.Q = 1; st.R = r0.R;  // P * Q: max input sub-blocks of a node
       p->steps.push_back(st);
     }
     return kids;
@@ -1437,6 +1437,8 @@ fmm_status fmm_node_st(const fmm_rule* rule, int dtype, int64_t m, int64_t k, in
   K1Node ks{}, kt{};
   ks.in = Op{BASE_A, 0, 0, 0, -1};
   kt.in = Op{BASE_B, 0, 0, 0, -1};
+  ks.rows = m / r.m0; ks.cols = k / r.k0; ks.P = r.m0; ks.Q = r.k0;
+  kt.rows = k / r.k0; kt.cols = n / r.n0; kt.P = r.k0; kt.Q = r.n0;
   ks.coef_off = 0;
   kt.coef_off = offV;
   for (int q = 0; q < r.R; ++q) {
@@ -1467,9 +1469,9 @@ fmm_status fmm_node_st(const fmm_rule* rule, int dtype, int64_t m, int64_t k, in
   const bool vec = aligned16(A) && aligned16(B) && aligned16(S) && aligned16(T) && lda % vecn == 0 &&
                    ldb % vecn == 0 && kb % vecn == 0 && nb % vecn == 0;
   Step s1{};
-  s1.kind = STEP_K1; s1.count = 1; s1.rows = mb; s1.cols = kb; s1.P = r.m0; s1.Q = r.k0; s1.R = r.R;
+  s1.kind = STEP_K1; s1.count = 1; s1.rows = mb; s1.cols = kb; s1.P = r.m0 * r.k0; s1.Q = 1; s1.R = r.R;
   Step s2 = s1;
-  s2.rows = kb; s2.cols = nb; s2.P = r.k0; s2.Q = r.n0;
+  s2.rows = kb; s2.cols = nb; s2.P = r.k0 * r.n0;
   if (e == cudaSuccess) {
     e = dtype == FMM_F64 ? launch_k1<double>(s1, dn, dcoef, b, vec, st) : launch_k1<float>(s1, dn, dcoef, b, vec, st);
   }

@@ -71,6 +71,8 @@ RuleQuantities rule_quantities(const RuleData& d);
 // a 2-bit code per input block (0 absent, 1 +1, 2 -1, 3 general coefficient from the table).
 struct K1Node {
   Op in;
+  int64_t rows, cols;  // sub-block dims of this node's split (S: mb x kb, T: kb x nb)
+  int32_t P, Q;        // split P x Q (S: m0 x k0, T: k0 x n0)
   int32_t coef_off;  // offset (in doubles) of the table in the plan's coefficient buffer
   uint32_t out_mask;
   int32_t nout;      // number of outputs written

@@ -89,6 +89,12 @@ __global__ void __launch_bounds__(kThreads) k1_lincomb(const K1Node* __restrict_
   __shared__ uint32_t code[kMaxR];
   __shared__ int rlist[kMaxR];
   const K1Node& nd = nodes[blockIdx.z];
+  // per-node split (S and T nodes of a level share one launch; the grid covers the largest)
+  P = nd.P;
+  Q = nd.Q;
+  rows = nd.rows;
+  cols = nd.cols;
+  if ((int64_t)blockIdx.y * RPB >= rows || (int64_t)blockIdx.x * kThreads * VEC >= cols) return;
   const int nblk = P * Q;
   const int nout = nd.nout;
   const uint32_t need = nd.need;

@@ -79,7 +79,7 @@ def test_plan_shape_errors_and_workspace():
     # breadth-first: level 1: 4 S + 4 T + 7 M blocks of 256^2; level 2: 28 + 28 + 49 of 128^2
     exp = (4 + 4 + 7) * 256 * 256 * 8 + (28 + 28 + 49) * 128 * 128 * 8
     assert exp <= ws <= exp + 1 << 16
-    assert p.launch_count() == 2 + 2 + 1 + 2  # K1 x2 levels x (S, T), K2, K3 x2
+    assert p.launch_count() == 2 + 1 + 2  # K1 x2 levels (S and T in one launch), K2, K3 x2
 
 
 def test_partition_ownership():
@@ -148,5 +148,5 @@ def test_operand_fusion_skips_leaf_level_formation():
     p.set_fusion("on")
     n0, w0 = p.launch_count(), p.workspace_bytes()
     p.set_operand_fusion(True)
-    assert p.launch_count() == n0 - 2  # no leaf-level K1 for S or T
+    assert p.launch_count() == n0 - 1  # no leaf-level K1 (S and T) launch
     assert p.workspace_bytes() < w0
