@@ -282,6 +282,16 @@ fmm_status fmm_scale_repeated(int dtype, int64_t M, int64_t K, int64_t N, const 
                               void* dA, void* dB, void* dI, int32_t* steps_dev, void* ws,
                               size_t ws_bytes, void* stream);
 fmm_status fmm_scale_workspace_bytes(int64_t M, int64_t K, int64_t N, size_t* bytes);
+/* Apply given diagonal factors (eqn:scaling): A' = D_A^-1 A D, B' = D^-1 B D_B^-1,
+ * computed as a'_ik = (a_ik / dA_i) * d_k and b'_kj = (b_kj / d_k) / dB_j (each operation
+ * correctly rounded; exact for power-of-two factors, so applying the cumulative factors of
+ * fmm_scale_repeated with pow2 = 1 reproduces its A', B' bitwise).  dA (M), d (K), dB (N): device
+ * vectors; A_out / B_out: caller device buffers (may not alias A / B).  FP64 only. */
+fmm_status fmm_scale_apply(int dtype, int64_t M, int64_t K, int64_t N, const void* A, int64_t lda,
+                           const void* B, int64_t ldb, const void* dA, const void* d,
+                           const void* dB, void* A_out, int64_t lda_out, void* B_out,
+                           int64_t ldb_out, void* stream);
+
 /* Alg. 1 line 6: C <- D_A C D_B in place, c_ij = (dA_i * c_ij) * dB_j. */
 fmm_status fmm_unscale(int dtype, int64_t M, int64_t N, void* C, int64_t ldc, const void* dA,
                        const void* dB, void* stream);

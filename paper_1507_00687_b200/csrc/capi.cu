@@ -33,6 +33,10 @@ cudaError_t run_scaling(int64_t M, int64_t K, int64_t N, const double* A, int64_
                         void* sws, cudaStream_t st);
 cudaError_t launch_unscale(double* C, int64_t ldc, int64_t M, int64_t N, const double* dA,
                            const double* dB, cudaStream_t st);
+cudaError_t launch_scale_apply(int64_t M, int64_t K, int64_t N, const double* A, int64_t lda,
+                               const double* B, int64_t ldb, const double* dA, const double* d,
+                               const double* dB, double* A_out, int64_t lda_out, double* B_out,
+                               int64_t ldb_out, cudaStream_t st);
 
 static thread_local std::string g_err = "no error";
 void set_error(const std::string& msg) { g_err = msg; }
@@ -1595,6 +1599,22 @@ fmm_status fmm_scale_repeated(int dtype, int64_t M, int64_t K, int64_t N, const 
   scaling_steps(c, &steps, &tau);
   return scale_common(M, K, N, A, lda, B, ldb, A_out, lda_out, B_out, ldb_out, dA, dB, dI, steps,
                       tau, cfg->pow2, steps_dev, ws, (cudaStream_t)stream, false);
+}
+
+fmm_status fmm_scale_apply(int dtype, int64_t M, int64_t K, int64_t N, const void* A, int64_t lda,
+                           const void* B, int64_t ldb, const void* dA, const void* d,
+                           const void* dB, void* A_out, int64_t lda_out, void* B_out,
+                           int64_t ldb_out, void* stream) {
+  if (dtype != FMM_F64) { set_error("scaling: FP64 only"); return FMM_E_UNSUPPORTED; }
+  if (!A || !B || !dA || !d || !dB || !A_out || !B_out || M < 0 || K < 0 || N < 0 || lda < K ||
+      ldb < N || lda_out < K || ldb_out < N) {
+    set_error("fmm_scale_apply: bad argument");
+    return FMM_E_ARG;
+  }
+  return cuda_status(launch_scale_apply(M, K, N, (const double*)A, lda, (const double*)B, ldb,
+                                        (const double*)dA, (const double*)d, (const double*)dB,
+                                        (double*)A_out, lda_out, (double*)B_out, ldb_out,
+                                        (cudaStream_t)stream), "fmm_scale_apply");
 }
 
 fmm_status fmm_unscale(int dtype, int64_t M, int64_t N, void* C, int64_t ldc, const void* dA,

@@ -546,6 +546,36 @@ cudaError_t run_scaling(int64_t M, int64_t K, int64_t N, const double* A, int64_
   return cudaGetLastError();
 }
 
+// Apply given factors: A' = (a_ik / dA_i) * d_k, B' = (b_kj / d_k) / dB_j (each operation
+// correctly rounded; exact for power-of-two factors).  One streaming pass per matrix.
+__global__ void k_scale_apply_rows_cols(const double* __restrict__ X, int64_t ldx, double* __restrict__ Y,
+                                        int64_t ldy, int64_t rows, int64_t cols,
+                                        const double* __restrict__ rdiv, const double* __restrict__ cmul,
+                                        const double* __restrict__ cdiv) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  const double cm = cmul ? cmul[j] : 1.0, cd = cdiv ? cdiv[j] : 1.0;
+  for (int64_t i = blockIdx.y; i < rows; i += gridDim.y) {
+    double x = __ddiv_rn(X[i * ldx + j], rdiv[i]);
+    if (cmul) x = __dmul_rn(x, cm);
+    if (cdiv) x = __ddiv_rn(x, cd);
+    Y[i * ldy + j] = x;
+  }
+}
+
+cudaError_t launch_scale_apply(int64_t M, int64_t K, int64_t N, const double* A, int64_t lda,
+                               const double* B, int64_t ldb, const double* dA, const double* d,
+                               const double* dB, double* A_out, int64_t lda_out, double* B_out,
+                               int64_t ldb_out, cudaStream_t st) {
+  if (M > 0 && K > 0)
+    k_scale_apply_rows_cols<<<dim3((unsigned)((K + 255) / 256), (unsigned)(M < 4096 ? M : 4096)), 256, 0, st>>>(
+        A, lda, A_out, lda_out, M, K, dA, d, nullptr);
+  if (K > 0 && N > 0)
+    k_scale_apply_rows_cols<<<dim3((unsigned)((N + 255) / 256), (unsigned)(K < 4096 ? K : 4096)), 256, 0, st>>>(
+        B, ldb, B_out, ldb_out, K, N, d, nullptr, dB);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_unscale(double* C, int64_t ldc, int64_t M, int64_t N, const double* dA,
                            const double* dB, cudaStream_t st) {
   if (M == 0 || N == 0) return cudaSuccess;

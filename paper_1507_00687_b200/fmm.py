@@ -45,6 +45,7 @@ SIGNATURES = {
     "fmm_plan_set_fusion": (_I, [_P, _I]),
     "fmm_plan_set_shard_depth": (_I, [_P, _I]),
     "fmm_plan_set_operand_fusion": (_I, [_P, _I]),
+    "fmm_scale_apply": (_I, [_I, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _I64, _P, _I64, _P]),
     "fmm_rule_quantities": (_I, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double), _P, _P]),
     "fmm_plan_stability": (_I, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "fmm_choose_variants": (_I, [_P, _P, _I, _P, C.POINTER(C.c_double)]),
@@ -451,6 +452,20 @@ def scale_repeated(A, B, first_O=True, tau=1.0, max_steps=20, pow2=False, stream
           C.c_void_p(dB.data_ptr()), C.c_void_p(dI.data_ptr()), C.c_void_p(steps.data_ptr()),
           C.c_void_p(ws.data_ptr()), nb.value, _stream(stream))
     return dict(A=Ao, B=Bo, dA=dA, dB=dB, dI=dI, steps=int(steps.item()))
+
+
+def scale_apply(A, B, dA, d, dB, stream=None):
+    """A' = D_A^-1 A D, B' = D^-1 B D_B^-1 for given factor vectors (fmm_scale_apply)."""
+    import torch
+    M, K = A.shape
+    N = B.shape[1]
+    Ao, Bo = torch.empty_like(A), torch.empty_like(B)
+    a, lda = _mat(A, "A")
+    b, ldb = _mat(B, "B")
+    _call("fmm_scale_apply", F64, M, K, N, a, lda, b, ldb, C.c_void_p(dA.data_ptr()),
+          C.c_void_p(d.data_ptr()), C.c_void_p(dB.data_ptr()), C.c_void_p(Ao.data_ptr()), K,
+          C.c_void_p(Bo.data_ptr()), N, _stream(stream))
+    return Ao, Bo
 
 
 def unscale(Cm, dA, dB, stream=None):

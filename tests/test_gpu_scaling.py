@@ -125,3 +125,18 @@ def test_extreme_magnitudes_bitwise(fb, pow2):
     ra, rb, rdA, rdB = oracle.scale_outside(A, B, pow2=pow2)
     for x, y in ((Ao, ra), (Bo, rb), (dA, rdA), (dB, rdB)):
         assert np.array_equal(host(x), y)
+
+
+def test_scale_apply_definition_and_roundtrip(fb):
+    # fmm_scale_apply: a' = (a / dA_i) * d_k, b' = (b / d_k) / dB_j, each correctly rounded --
+    # bitwise numpy's IEEE operations; with the cumulative pow2 factors of Alg. 3 it reproduces
+    # the scaled matrices of fmm_scale_repeated exactly (eqn:scaling)
+    A, B = fi.draw("skew", 96, 40, 72, 3)
+    g = np.random.default_rng(1)
+    dA, d, dB = g.uniform(0.5, 3, 96), g.uniform(0.5, 3, 40), g.uniform(0.5, 3, 72)
+    Ao, Bo = fb.scale_apply(dev(A), dev(B), dev(dA), dev(d), dev(dB))
+    assert np.array_equal(host(Ao), (A / dA[:, None]) * d[None, :])
+    assert np.array_equal(host(Bo), (B / d[:, None]) / dB[None, :])
+    r = fb.scale_repeated(dev(A), dev(B), first_O=True, tau=1.0, max_steps=12, pow2=True)
+    Ao, Bo = fb.scale_apply(dev(A), dev(B), r["dA"], r["dI"], r["dB"])
+    assert np.array_equal(host(Ao), host(r["A"])) and np.array_equal(host(Bo), host(r["B"]))
