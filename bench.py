@@ -369,7 +369,9 @@ def run_fmm(args):
     fused = plan.fused_launches() > 0
     k2_name = ("k2f_gemm_f64 (leaf products on DMMA mma.sync f64 + the parents' W-combination "
                "fused in the epilogue)" if fused else "k2_gemm_f64 (leaf products, DMMA mma.sync f64)")
-    roofline = {"kernel": k2_name if args.dtype == "f64" else "k2 (leaf products, FP32)",
+    k2_name32 = ("k2f_tf32 (3xTF32 leaf products on tcgen05 + the parents' W-combination in a TMEM "
+                 "double-buffered epilogue)" if fused else "k2_tf32 (3xTF32 leaf products on tcgen05)")
+    roofline = {"kernel": k2_name if args.dtype == "f64" else k2_name32,
                 "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None,
                 "traffic": load_traffic(workload),

@@ -378,8 +378,15 @@ struct Builder {
   }
 
   bool fuse_leaves(int64_t nparents) const {
-    if (p->dtype != FMM_F64 || p->fusion == 0) return false;
+    const bool tc32 = p->dtype == FMM_F32 && p->leaf != FMM_LEAF_NATIVE;  // tcgen05 FP32 leaves
+    if ((p->dtype != FMM_F64 && !tc32) || p->fusion == 0) return false;
     if (p->fusion == 1) return true;
+    if (tc32) {  // k2f_tf32: 128 x 256 tiles, whole chains, >= 4 waves at >= 90 %
+      constexpr int64_t kSMs = 148;
+      const int64_t units = nparents * ((p->lm[p->L] + 127) / 128) * ((p->ln[p->L] + 255) / 256);
+      const int64_t waves = (units + kSMs - 1) / kSMs;
+      return waves >= 4 && units * 10 >= waves * kSMs * 9;
+    }
     {  // chain splitting (turnstiles) smooths the wave quantisation of R-product units
       const int64_t tiles = ((p->lm[p->L] + 127) / 128) * ((p->ln[p->L] + 127) / 128);
       const int R = p->rules[p->node_rule[p->L - 1][0]].R;
@@ -446,6 +453,15 @@ struct Builder {
     st.nr = fz[0].nr;
     st.opf = opf_on() ? 1 : 0;
     st.arena_off = -1;
+    if (p->dtype == FMM_F32) {  // tensor-core FP32 leaves: split list (parent-major) + hi/lo arena
+      std::vector<LeafNode> sl;
+      for (const FusedNode& f : fz)
+        for (int i = 0; i < f.nr; ++i) sl.push_back(LeafNode{f.a[i], f.b[i], Op{}});
+      st.dev_off2 = push(sl);
+      st.arena_off = ws_alloc((int64_t)tf32_arena_floats((int64_t)sl.size(), st.rows, st.cols, st.inner));
+      p->steps.push_back(st);
+      return;
+    }
     // persistent hybrid data-parallel / stream-K form (K2P) when the leaf has >= STAGES k-tiles
     // chain split with per-unit turnstiles (breadth-first levels: every parent has all R products)
     if (p->split_chains && fz.size() > 0 && fz[0].nr == r0.R && (st.inner + 15) / 16 >= 4) {
@@ -739,7 +755,12 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
       case STEP_ACC: e = launch_acc<T>(s, nd, p->dev_coef, b, vec, st); break;
       case STEP_ZERO: e = launch_zero<T>(s, nd, b, st); break;
       case STEP_K2F:
-        if (s.persist && s.persist <= device_sms()) {
+        if (p->dtype == FMM_F32) {
+          e = launch_gemm_tf32_fused((const FusedNode*)nd, (const LeafNode*)((const uint8_t*)p->dev_desc + s.dev_off2),
+                                     s.count, s.nr, s.rows, s.cols, s.inner, p->dev_coef, s.P, s.Q,
+                                     s.R, b, p->leaf == FMM_LEAF_TF32 ? 1 : 3,
+                                     (float*)b.p[BASE_WS] + s.arena_off, st);
+        } else if (s.persist && s.persist <= device_sms()) {
           double* scr = (double*)b.p[BASE_WS] + s.arena_off;
           int* flg = (int*)(scr + (size_t)persistent_max_tail_units(s.persist) * s.nr * 128 * 128);
           e = launch_gemm_f64_persistent((const FusedNode*)nd, s.count, s.rows, s.cols, s.inner,

@@ -166,6 +166,7 @@ struct Step {
                      // K2F persistent (K2P): offset of the scratch tiles + flags in ws
   bool vec_ok;       // all ws offsets / dims allow 16-byte vectors (caller bases checked later)
   int nr = 0;        // K2F: products per node (uniform)
+  int64_t dev_off2 = -1;  // K2F FP32: LeafNode list (parent-major) for the hi / lo split
   int opf = 0;       // K2F: operands formed in the kernel from up to two sources (na / nb)
   int chunk = 0;     // K2F: products per CTA when a unit's chain is split (0: whole chain);
                      // turnstiles (one int per unit) at ws offset turn_off (bytes)
@@ -206,6 +207,11 @@ cudaError_t launch_gemm_f64_persistent(const FusedNode* dev_nodes, int count, in
                                        int NR, int ctas, double* scratch, int* flags,
                                        const Bases& b, bool vec, cudaStream_t st);
 size_t persistent_scratch_bytes(int ctas, int NR);
+// K2F for the FP32 tensor-core leaves (3xTF32 / TF32 on tcgen05, TMEM double-buffered)
+cudaError_t launch_gemm_tf32_fused(const FusedNode* dev_nodes, const LeafNode* dev_split_leaves,
+                                   int count, int nr, int64_t m, int64_t n, int64_t k,
+                                   const double* dev_coef, int P, int Q, int R, const Bases& b,
+                                   int passes, float* arena, cudaStream_t st);
 int64_t persistent_max_tail_units(int ctas);
 int persistent_min_kt();
 cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, const LeafNode* host_leaves, int count,

@@ -281,6 +281,199 @@ __global__ void __launch_bounds__(256, 1)
                  "r"(TMEM_COLS));
 }
 
+// K2F for the FP32 tensor-core leaves: one CTA per (128 x 256 output tile, parent node) runs the
+// parent's nr leaf products in ascending r.  TMEM holds TWO 128 x 256 FP32 accumulators (512
+// columns): the single MMA-issuing thread writes product r into buffer r & 1 while warps 4-7
+// drain product r-1 from the other buffer and apply the parent's W-combination -- C_k = w*m for
+// the first contribution, else C_k = C_k + w*m (FP32, round to nearest, plain load / store by
+// the thread owning the row) -- K3's per-element sequence, bitwise, with M_r never written and
+// the epilogue overlapped with the next product's MMAs.  Barriers: full / empty per smem stage
+// (TMA <-> MMA, as in k2_tf32), acc_full / acc_empty per TMEM buffer (MMA <-> epilogue; the
+// epilogue's 128 threads arrive on acc_empty).  Operands: the per-launch hi / lo arena of
+// k_split_tf32 with leaf index parent * nr + r.
+template <int BK, int STAGES>
+__global__ void __launch_bounds__(256, 1)
+    k2f_tf32(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
+             const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
+             const FusedNode* __restrict__ nodes, const double* __restrict__ coef_all, Bases bases,
+             int64_t m, int64_t n, int64_t kp, int tiles_n, int passes, int P, int Q, int R) {
+  using CF = TCfg<BK, STAGES>;
+  constexpr int TSTAGES = STAGES, TBK = BK, A_BYTES = CF::A_B, B_BYTES = CF::B_B,
+                STAGE_BYTES = CF::STAGE;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = (uint64_t*)(smem + TSTAGES * STAGE_BYTES);
+  // bars: [0,S) full, [S,2S) empty, [2S,2S+2) acc_full, [2S+2,2S+4) acc_empty; then TMEM base
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * TSTAGES + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int parent = blockIdx.y;
+  const FusedNode& nd = nodes[parent];
+  const int nr = nd.nr;
+  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
+  const int m0 = tm * TBM, n0 = tn * TBN;
+  const int KT = (int)(kp / TBK);
+
+  if (warp == 0 && lane == 0) {
+    for (int s2 = 0; s2 < TSTAGES; ++s2) {
+      mbar_init(su32(&bars[s2]), 1);
+      mbar_init(su32(&bars[TSTAGES + s2]), 1);
+    }
+    for (int b2 = 0; b2 < 2; ++b2) {
+      mbar_init(su32(&bars[2 * TSTAGES + b2]), 1);        // acc_full: one tcgen05.commit
+      mbar_init(su32(&bars[2 * TSTAGES + 2 + b2]), 128);  // acc_empty: the 128 epilogue threads
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     su32(tmem_slot)),
+                 "r"(2 * TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer over all (product, k-tile) ----
+      int it = 0;
+      for (int ri = 0; ri < nr; ++ri) {
+        const int leaf = parent * nr + ri;
+        for (int kt = 0; kt < KT; ++kt, ++it) {
+          const int s2 = it % TSTAGES;
+          const uint32_t ph = (uint32_t)(it / TSTAGES) & 1u;
+          mbar_wait(su32(&bars[TSTAGES + s2]), ph ^ 1u);
+          uint8_t* st = smem + s2 * STAGE_BYTES;
+          const uint32_t full = su32(&bars[s2]);
+          const int kc = kt * TBK;
+          if (passes == 3) {
+            mbar_expect_tx(full, STAGE_BYTES);
+            tma_load_3d(su32(st), &ta_hi, kc, m0, leaf, full);
+            tma_load_3d(su32(st + A_BYTES), &ta_lo, kc, m0, leaf, full);
+            tma_load_3d(su32(st + 2 * A_BYTES), &tb_hi, kc, n0, leaf, full);
+            tma_load_3d(su32(st + 2 * A_BYTES + B_BYTES), &tb_lo, kc, n0, leaf, full);
+          } else {
+            mbar_expect_tx(full, A_BYTES + B_BYTES);
+            tma_load_3d(su32(st), &ta_hi, kc, m0, leaf, full);
+            tma_load_3d(su32(st + 2 * A_BYTES), &tb_hi, kc, n0, leaf, full);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer ----
+      int it = 0;
+      for (int ri = 0; ri < nr; ++ri) {
+        const int buf = ri & 1;
+        if (ri >= 2) {  // the epilogue has drained this buffer (product ri - 2)
+          mbar_wait(su32(&bars[2 * TSTAGES + 2 + buf]), (uint32_t)((ri / 2 - 1) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        }
+        const uint32_t acc = tmem + (uint32_t)(buf * TMEM_COLS);
+        for (int kt = 0; kt < KT; ++kt, ++it) {
+          const int s2 = it % TSTAGES;
+          const uint32_t ph = (uint32_t)(it / TSTAGES) & 1u;
+          mbar_wait(su32(&bars[s2]), ph);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          uint8_t* st = smem + s2 * STAGE_BYTES;
+          const uint64_t a_hi = desc_k<BK>(su32(st)), a_lo = desc_k<BK>(su32(st + A_BYTES));
+          const uint64_t b_hi = desc_k<BK>(su32(st + 2 * A_BYTES));
+          const uint64_t b_lo = desc_k<BK>(su32(st + 2 * A_BYTES + B_BYTES));
+#pragma unroll
+          for (int kk = 0; kk < TBK / 8; ++kk) {
+            const uint64_t off = (uint64_t)((kk * 32) >> 4);
+            const uint32_t first = (kt == 0 && kk == 0) ? 0u : 1u;
+            if (passes == 3) {
+              mma_tf32(acc, a_lo + off, b_hi + off, first);
+              mma_tf32(acc, a_hi + off, b_lo + off, 1u);
+              mma_tf32(acc, a_hi + off, b_hi + off, 1u);
+            } else {
+              mma_tf32(acc, a_hi + off, b_hi + off, first);
+            }
+          }
+          mma_commit(su32(&bars[TSTAGES + s2]));
+        }
+        mma_commit(su32(&bars[2 * TSTAGES + buf]));  // product ri complete in buffer buf
+      }
+    }
+  } else if (warp >= 4) {  // ---- epilogue: TMEM -> registers -> W-combination ----
+    const int q = warp & 3;
+    const int64_t row = m0 + q * 32 + lane;
+    int64_t ldo;
+    float* out = op_ptr<float>(bases, nd.out, ldo);
+    for (int ri = 0; ri < nr; ++ri) {
+      const int buf = ri & 1;
+      mbar_wait(su32(&bars[2 * TSTAGES + buf]), (uint32_t)((ri / 2) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const uint32_t wmask = nd.wmask[ri], fmask = nd.first[ri];
+      const int r = nd.rlist[ri];
+#pragma unroll 1
+      for (int cb = 0; cb < TBN / 32; ++cb) {
+        uint32_t v[32];
+        const uint32_t taddr =
+            tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * TMEM_COLS + cb * 32);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+              "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (KT == 0) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = 0u;
+        }
+        if (row >= m) continue;
+        const int64_t cbase = n0 + cb * 32;
+        for (int kk = 0; kk < P * Q; ++kk) {  // kk = ia*Q + jb (row-major C blocks)
+          if (!((wmask >> kk) & 1u)) continue;
+          const float w = (float)coef_all[nd.coef_off + kk * R + r];
+          const bool first = (fmask >> kk) & 1u;
+          float* crow = out + ((int64_t)(kk / Q) * m + row) * ldo + (int64_t)(kk % Q) * n + cbase;
+          const bool vec = ((((uintptr_t)crow) & 15u) == 0) && (cbase + 32 <= n);
+          if (vec) {
+#pragma unroll
+            for (int e = 0; e < 32; e += 4) {
+              float4 c4;
+              const float y0 = __fmul_rn(w, __uint_as_float(v[e])), y1 = __fmul_rn(w, __uint_as_float(v[e + 1]));
+              const float y2 = __fmul_rn(w, __uint_as_float(v[e + 2])), y3 = __fmul_rn(w, __uint_as_float(v[e + 3]));
+              if (first) {
+                c4 = make_float4(y0, y1, y2, y3);
+              } else {
+                c4 = *reinterpret_cast<const float4*>(crow + e);
+                c4.x = __fadd_rn(c4.x, y0); c4.y = __fadd_rn(c4.y, y1);
+                c4.z = __fadd_rn(c4.z, y2); c4.w = __fadd_rn(c4.w, y3);
+              }
+              *reinterpret_cast<float4*>(crow + e) = c4;
+            }
+          } else {
+            for (int e = 0; e < 32; ++e) {
+              if (cbase + e >= n) break;
+              const float y = __fmul_rn(w, __uint_as_float(v[e]));
+              crow[e] = first ? y : __fadd_rn(crow[e], y);
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&bars[2 * TSTAGES + 2 + buf]))
+                   : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                 "r"(2 * TMEM_COLS));
+}
+
 // S (m x k, via the leaf's a operand) -> hi, lo (m x kp); T (k x n) -> hi^T, lo^T (n x kp).
 // grid: x = kp / 32, y = ceil(rows / 32), z = leaf; block 32 x 8.
 __global__ void k_split_tf32(const LeafNode* __restrict__ leaves, Bases bases, int64_t m,
@@ -621,6 +814,41 @@ cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, i
     k2_tf32<16, 4><<<grid, 256, CF::SMEM, st>>>(ma_hi, ma_lo, mb_hi, mb_lo, dev_leaves, b, m, n, kp,
                                                  tiles_n, passes);
   }
+  return cudaGetLastError();
+}
+
+// Fused FP32 tensor-core leaves: split every (parent, product) leaf of the launch into the hi /
+// lo arena (leaf index parent * nr + r), then k2f_tf32.
+cudaError_t launch_gemm_tf32_fused(const FusedNode* dev_nodes, const LeafNode* dev_split_leaves,
+                                   int count, int nr, int64_t m, int64_t n, int64_t k,
+                                   const double* dev_coef, int P, int Q, int R, const Bases& b,
+                                   int passes, float* arena, cudaStream_t st) {
+  if (count == 0 || m == 0 || n == 0) return cudaSuccess;
+  if (!arena) return cudaErrorInvalidValue;
+  const int leaves = count * nr;
+  const int64_t kp = (k + TBK - 1) / TBK * TBK;
+  float* a_hi = arena;
+  float* a_lo = a_hi + (size_t)leaves * m * kp;
+  float* b_hi = a_lo + (size_t)leaves * m * kp;
+  float* b_lo = b_hi + (size_t)leaves * n * kp;
+  if (kp > 0) {
+    dim3 blk(32, 8);
+    k_split_tf32<<<dim3((unsigned)(kp / 32), (unsigned)((m + 31) / 32), (unsigned)leaves), blk, 0, st>>>(
+        dev_split_leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, 0);
+    k_split_tf32<<<dim3((unsigned)(kp / 32), (unsigned)((n + 31) / 32), (unsigned)leaves), blk, 0, st>>>(
+        dev_split_leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, 1);
+  }
+  CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
+  const int64_t kpe = kp > 0 ? kp : TBK;
+  if (!make_map(&ma_hi, a_hi, kpe, m, leaves, TBM, 32) || !make_map(&ma_lo, a_lo, kpe, m, leaves, TBM, 32) ||
+      !make_map(&mb_hi, b_hi, kpe, n, leaves, TBN, 32) || !make_map(&mb_lo, b_lo, kpe, n, leaves, TBN, 32))
+    return cudaErrorInvalidValue;
+  const int tiles_m = (int)((m + TBM - 1) / TBM), tiles_n = (int)((n + TBN - 1) / TBN);
+  using CF = TCfg<32, 2>;
+  cudaError_t e = cudaFuncSetAttribute(k2f_tf32<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
+  if (e != cudaSuccess) return e;
+  k2f_tf32<32, 2><<<dim3((unsigned)(tiles_m * tiles_n), (unsigned)count), 256, CF::SMEM, st>>>(
+      ma_hi, ma_lo, mb_hi, mb_lo, dev_nodes, dev_coef, b, m, n, kp, tiles_n, passes, P, Q, R);
   return cudaGetLastError();
 }
 
