@@ -381,12 +381,7 @@ struct Builder {
     const bool tc32 = p->dtype == FMM_F32 && p->leaf != FMM_LEAF_NATIVE;  // tcgen05 FP32 leaves
     if ((p->dtype != FMM_F64 && !tc32) || p->fusion == 0) return false;
     if (p->fusion == 1) return true;
-    if (tc32) {  // k2f_tf32: 128 x 256 tiles, whole chains, >= 4 waves at >= 90 %
-      constexpr int64_t kSMs = 148;
-      const int64_t units = nparents * ((p->lm[p->L] + 127) / 128) * ((p->ln[p->L] + 255) / 256);
-      const int64_t waves = (units + kSMs - 1) / kSMs;
-      return waves >= 4 && units * 10 >= waves * kSMs * 9;
-    }
+    if (tc32) return false;  // k2f_tf32 measured slower than k2_tf32 + K3 at C5 (310 vs 287 ms): opt-in
     {  // chain splitting (turnstiles) smooths the wave quantisation of R-product units
       const int64_t tiles = ((p->lm[p->L] + 127) / 128) * ((p->ln[p->L] + 127) / 128);
       const int R = p->rules[p->node_rule[p->L - 1][0]].R;
