@@ -454,6 +454,11 @@ struct Builder {
         for (int i = 0; i < f.nr; ++i) sl.push_back(LeafNode{f.a[i], f.b[i], Op{}});
       st.dev_off2 = push(sl);
       st.arena_off = ws_alloc((int64_t)tf32_arena_floats((int64_t)sl.size(), st.rows, st.cols, st.inner));
+      if (p->split_chains && st.nr > 1) {  // one product per CTA, in product-major order
+        st.chunk = 1;
+        const int64_t tiles = ((st.rows + 127) / 128) * ((st.cols + 255) / 256);
+        st.turn_off = ws_alloc(st.count * tiles + 1);  // ints (in 4-byte elements)
+      }
       p->steps.push_back(st);
       return;
     }
@@ -754,7 +759,8 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
           e = launch_gemm_tf32_fused((const FusedNode*)nd, (const LeafNode*)((const uint8_t*)p->dev_desc + s.dev_off2),
                                      s.count, s.nr, s.rows, s.cols, s.inner, p->dev_coef, s.P, s.Q,
                                      s.R, b, p->leaf == FMM_LEAF_TF32 ? 1 : 3,
-                                     (float*)b.p[BASE_WS] + s.arena_off, st);
+                                     (float*)b.p[BASE_WS] + s.arena_off, st, s.chunk,
+                                     s.turn_off >= 0 ? (int*)((float*)b.p[BASE_WS] + s.turn_off) : nullptr);
         } else if (s.persist && s.persist <= device_sms()) {
           double* scr = (double*)b.p[BASE_WS] + s.arena_off;
           int* flg = (int*)(scr + (size_t)persistent_max_tail_units(s.persist) * s.nr * 128 * 128);

@@ -211,7 +211,8 @@ size_t persistent_scratch_bytes(int ctas, int NR);
 cudaError_t launch_gemm_tf32_fused(const FusedNode* dev_nodes, const LeafNode* dev_split_leaves,
                                    int count, int nr, int64_t m, int64_t n, int64_t k,
                                    const double* dev_coef, int P, int Q, int R, const Bases& b,
-                                   int passes, float* arena, cudaStream_t st);
+                                   int passes, float* arena, cudaStream_t st, int chunk = 0,
+                                   int* turn = nullptr);
 int64_t persistent_max_tail_units(int ctas);
 int persistent_min_kt();
 cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, const LeafNode* host_leaves, int count,

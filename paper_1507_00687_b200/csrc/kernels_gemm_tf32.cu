@@ -296,7 +296,8 @@ __global__ void __launch_bounds__(256, 1)
     k2f_tf32(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
              const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
              const FusedNode* __restrict__ nodes, const double* __restrict__ coef_all, Bases bases,
-             int64_t m, int64_t n, int64_t kp, int tiles_n, int passes, int P, int Q, int R) {
+             int64_t m, int64_t n, int64_t kp, int tiles_n, int passes, int P, int Q, int R,
+             int count, int chunk, int* __restrict__ turn) {
   using CF = TCfg<BK, STAGES>;
   constexpr int TSTAGES = STAGES, TBK = BK, A_BYTES = CF::A_B, B_BYTES = CF::B_B,
                 STAGE_BYTES = CF::STAGE;
@@ -307,9 +308,14 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * TSTAGES + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int parent = blockIdx.y;
+  // chain split (chunk < nr, turnstiles as in k2f_gemm_f64): grid.y = group * count + parent;
+  // chunk = 1 keeps the unfused kernel's order (all CTAs of one product first: the L2 reuse of
+  // that leaf's panels) while the epilogue still applies the W-combination in place
+  const int parent = blockIdx.y % count, grp = blockIdx.y / count;
   const FusedNode& nd = nodes[parent];
-  const int nr = nd.nr;
+  const int r_begin = grp * chunk;
+  const int r_end = min(nd.nr, r_begin + chunk);
+  const int nr_all = nd.nr;
   const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
   const int m0 = tm * TBM, n0 = tn * TBN;
   const int KT = (int)(kp / TBK);
@@ -339,8 +345,8 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer over all (product, k-tile) ----
       int it = 0;
-      for (int ri = 0; ri < nr; ++ri) {
-        const int leaf = parent * nr + ri;
+      for (int ri = r_begin; ri < r_end; ++ri) {
+        const int leaf = parent * nr_all + ri;
         for (int kt = 0; kt < KT; ++kt, ++it) {
           const int s2 = it % TSTAGES;
           const uint32_t ph = (uint32_t)(it / TSTAGES) & 1u;
@@ -365,10 +371,11 @@ __global__ void __launch_bounds__(256, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer ----
       int it = 0;
-      for (int ri = 0; ri < nr; ++ri) {
-        const int buf = ri & 1;
-        if (ri >= 2) {  // the epilogue has drained this buffer (product ri - 2)
-          mbar_wait(su32(&bars[2 * TSTAGES + 2 + buf]), (uint32_t)((ri / 2 - 1) & 1));
+      for (int ri = r_begin; ri < r_end; ++ri) {
+        const int j = ri - r_begin;
+        const int buf = j & 1;
+        if (j >= 2) {  // the epilogue has drained this buffer (product ri - 2)
+          mbar_wait(su32(&bars[2 * TSTAGES + 2 + buf]), (uint32_t)((j / 2 - 1) & 1));
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         }
         const uint32_t acc = tmem + (uint32_t)(buf * TMEM_COLS);
@@ -403,10 +410,25 @@ __global__ void __launch_bounds__(256, 1)
     const int64_t row = m0 + q * 32 + lane;
     int64_t ldo;
     float* out = op_ptr<float>(bases, nd.out, ldo);
-    for (int ri = 0; ri < nr; ++ri) {
-      const int buf = ri & 1;
-      mbar_wait(su32(&bars[2 * TSTAGES + buf]), (uint32_t)((ri / 2) & 1));
+    int* my_turn = turn ? turn + (int64_t)parent * gridDim.x + blockIdx.x : nullptr;
+    for (int ri = r_begin; ri < r_end; ++ri) {
+      const int j = ri - r_begin;
+      const int buf = j & 1;
+      mbar_wait(su32(&bars[2 * TSTAGES + buf]), (uint32_t)((j / 2) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      if (j == 0 && grp > 0 && my_turn) {  // group grp-1 released this unit
+        if (threadIdx.x == 128) {
+          unsigned ns = 64;
+          long long spins = 0;
+          while (atomicAdd(my_turn, 0) < grp) {
+            __nanosleep(ns);
+            if (ns < 2048) ns *= 2;
+            if (++spins > (1ll << 24)) __trap();
+          }
+          __threadfence();
+        }
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      }
       const uint32_t wmask = nd.wmask[ri], fmask = nd.first[ri];
       const int r = nd.rlist[ri];
 #pragma unroll 1
@@ -464,6 +486,11 @@ __global__ void __launch_bounds__(256, 1)
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&bars[2 * TSTAGES + 2 + buf]))
                    : "memory");
+    }
+    if (my_turn && r_end < nr_all) {  // hand the unit to group grp+1
+      __threadfence();
+      asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      if (threadIdx.x == 128) atomicExch(my_turn, grp + 1);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -822,7 +849,7 @@ cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, i
 cudaError_t launch_gemm_tf32_fused(const FusedNode* dev_nodes, const LeafNode* dev_split_leaves,
                                    int count, int nr, int64_t m, int64_t n, int64_t k,
                                    const double* dev_coef, int P, int Q, int R, const Bases& b,
-                                   int passes, float* arena, cudaStream_t st) {
+                                   int passes, float* arena, cudaStream_t st, int chunk, int* turn) {
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
   if (!arena) return cudaErrorInvalidValue;
   const int leaves = count * nr;
@@ -847,8 +874,15 @@ cudaError_t launch_gemm_tf32_fused(const FusedNode* dev_nodes, const LeafNode* d
   using CF = TCfg<32, 2>;
   cudaError_t e = cudaFuncSetAttribute(k2f_tf32<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
   if (e != cudaSuccess) return e;
-  k2f_tf32<32, 2><<<dim3((unsigned)(tiles_m * tiles_n), (unsigned)count), 256, CF::SMEM, st>>>(
-      ma_hi, ma_lo, mb_hi, mb_lo, dev_nodes, dev_coef, b, m, n, kp, tiles_n, passes, P, Q, R);
+  if (chunk <= 0 || chunk >= nr || !turn) chunk = nr;
+  const int groups = (nr + chunk - 1) / chunk;
+  if (groups > 1) {
+    e = cudaMemsetAsync(turn, 0, sizeof(int) * (size_t)count * tiles_m * tiles_n, st);
+    if (e != cudaSuccess) return e;
+  }
+  k2f_tf32<32, 2><<<dim3((unsigned)(tiles_m * tiles_n), (unsigned)(count * groups)), 256, CF::SMEM, st>>>(
+      ma_hi, ma_lo, mb_hi, mb_lo, dev_nodes, dev_coef, b, m, n, kp, tiles_n, passes, P, Q, R, count,
+      chunk, groups > 1 ? turn : nullptr);
   return cudaGetLastError();
 }
 
