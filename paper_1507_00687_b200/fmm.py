@@ -373,6 +373,34 @@ def gemm(A, B, leaf=LEAF_NATIVE, C_out=None, stream=None):
     return C_out
 
 
+_PLAN_CACHE = {}
+
+
+def matmul(A, B, rules=("winograd",) * 3, scaling=None, leaf=None, C_out=None, stream=None):
+    """C = A @ B by recursive fast matrix multiplication: `rules` is one built-in rule name (or
+    Rule) per level, root first; `scaling` None / 'outside' / 'inside' / 'out_in' /
+    'in_out' / 'repeated' or a dict (fmm_scaling fields), FP64 only.  Plans are cached per
+    (rules, dims, dtype, leaf, scaling, device).  A, B: row-major CUDA tensors (float64 or
+    float32; FP32 defaults to the 3xTF32 tensor-core leaf)."""
+    import torch
+    if A.dtype != B.dtype or A.dtype not in (torch.float64, torch.float32):
+        raise ValueError("A and B must both be float64 or float32")
+    dtype = "f64" if A.dtype == torch.float64 else "f32"
+    if leaf is None:
+        leaf = LEAF_NATIVE if dtype == "f64" else LEAF_3XTF32
+    M, K = A.shape
+    N = B.shape[1]
+    rl = tuple(r if isinstance(r, Rule) else Rule.builtin(r) for r in rules)
+    sc = scaling if (scaling is None or isinstance(scaling, dict)) else {"mode": scaling, "pow2": 1}
+    key = (tuple(r.name for r in rl), M, K, N, dtype, leaf,
+           tuple(sorted(sc.items())) if sc else None, A.device.index)
+    plan = _PLAN_CACHE.get(key)
+    if plan is None:
+        plan = Plan(list(rl), M, K, N, dtype=dtype, leaf=leaf, scaling=sc)
+        _PLAN_CACHE[key] = plan
+    return plan.execute(A, B, C_out=C_out, stream=stream)
+
+
 def node_st(rule: Rule, A, B, stream=None):
     """All S_r, T_r of one node (R x mb x kb, R x kb x nb)."""
     import torch

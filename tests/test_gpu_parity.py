@@ -345,3 +345,22 @@ def test_no_out_of_bounds_writes(fb, dtype, leaf, dims):
     assert torch.all(wsb[nb:] == 0xA5), "write past the workspace"
     Co = oracle.fmm(A, B, OPlan.stationary(R.winograd(), L))
     assert parity(Cv.cpu().numpy(), Co, A, B) <= (TOL64 if dtype == "f64" else TOL32)
+
+
+def test_matmul_convenience_api(fb):
+    # fb.matmul: cached plans; FP64 parity, FP32 (3xTF32) parity, scaling, padding
+    A, B = fi.random_pair(300, 260, 200, seed=61)
+    C1 = fb.matmul(dev(A), dev(B), rules=("strassen", "winograd")).cpu().numpy()
+    Co = oracle.fmm(A, B, OPlan.uniform([R.strassen(), R.winograd()]))
+    assert parity(C1, Co, A, B) <= TOL64
+    C2 = fb.matmul(dev(A), dev(B), rules=("strassen", "winograd")).cpu().numpy()
+    assert np.array_equal(C1, C2) and len(fb.fmm._PLAN_CACHE) >= 1
+    A32, B32 = A.astype(np.float32), B.astype(np.float32)
+    C3 = fb.matmul(dev(A32), dev(B32), rules=("winograd",) * 2).cpu().numpy()
+    assert parity(C3, oracle.fmm(A32, B32, OPlan.stationary(R.winograd(), 2)), A32, B32) <= TOL32
+    As, Bs = fi.draw("skew", 128, 64, 96, 3)
+    Cs = fb.matmul(dev(As), dev(Bs), rules=("winograd",) * 2, scaling="repeated").cpu().numpy()
+    Cso, _ = oracle.scaled_fmm(As, Bs, OPlan.stationary(R.winograd(), 2), mode="repeated", pow2=True)
+    hi, lo = oracle.ref_dd(As, Bs)
+    rel = lambda X: np.max(np.abs((X - hi) - lo) / np.abs(hi))
+    assert rel(Cs) <= 10 * max(rel(Cso), 1e-15)
