@@ -364,6 +364,13 @@ struct Builder {
   }
   // best chain split for a fused leaf level (chunk = R: no split); efficiency out
   static int best_chunk(int64_t units, int R, int KT, double* eff) {
+    if (const char* ce = getenv("FMM_CHUNK")) {  // experiments: force the split
+      const int c = atoi(ce);
+      if (c >= 1 && c <= R) {
+        if (eff) *eff = 1.0;
+        return c;
+      }
+    }
     int best = R;
     double best_span = fused_makespan(units, R, R, KT);
     if (KT >= 4 && units <= (1 << 16)) {
@@ -740,48 +747,77 @@ static int device_sms() {
   return n;
 }
 
+// Launch one step (or one node-chunk of it: grid.y / grid.z carry the node count, limited to
+// 65535, so steps with more nodes -- deep recursions, 7^6 = 117649 leaves -- run in chunks).
+// `c0` = first node of the chunk: descriptor arrays, the FP32 split list and the turnstiles
+// are offset accordingly; the FP32 hi / lo arena is reused by consecutive chunks.
+template <typename T>
+static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, const Bases& b,
+                               bool vec, cudaStream_t st) {
+  size_t node_bytes = 0;
+  switch (s.kind) {
+    case STEP_K1: node_bytes = sizeof(K1Node); break;
+    case STEP_K3: node_bytes = sizeof(K3Node); break;
+    case STEP_ACC: node_bytes = sizeof(AccNode); break;
+    case STEP_ZERO: node_bytes = sizeof(ZeroNode); break;
+    case STEP_K2: node_bytes = sizeof(LeafNode); break;
+    case STEP_K2F: node_bytes = sizeof(FusedNode); break;
+  }
+  const void* nd = (const uint8_t*)p->dev_desc + s.dev_off + c0 * node_bytes;
+  const int64_t tiles_f = p->dtype == FMM_F32 ? ((s.rows + 127) / 128) * ((s.cols + 255) / 256)
+                                              : ((s.rows + 127) / 128) * ((s.cols + 127) / 128);
+  switch (s.kind) {
+    case STEP_K1: return launch_k1<T>(s, nd, p->dev_coef, b, vec, st);
+    case STEP_K3: return launch_k3<T>(s, nd, p->dev_coef, b, vec, st);
+    case STEP_ACC: return launch_acc<T>(s, nd, p->dev_coef, b, vec, st);
+    case STEP_ZERO: return launch_zero<T>(s, nd, b, st);
+    case STEP_K2F:
+      if (p->dtype == FMM_F32) {
+        int* turn = s.turn_off >= 0 ? (int*)((float*)b.p[BASE_WS] + s.turn_off) + c0 * tiles_f : nullptr;
+        return launch_gemm_tf32_fused(
+            (const FusedNode*)nd,
+            (const LeafNode*)((const uint8_t*)p->dev_desc + s.dev_off2) + c0 * s.nr, s.count, s.nr,
+            s.rows, s.cols, s.inner, p->dev_coef, s.P, s.Q, s.R, b, p->leaf == FMM_LEAF_TF32 ? 1 : 3,
+            (float*)b.p[BASE_WS] + s.arena_off, st, s.chunk, turn);
+      }
+      if (s.persist && s.persist <= device_sms()) {
+        double* scr = (double*)b.p[BASE_WS] + s.arena_off;
+        int* flg = (int*)(scr + (size_t)persistent_max_tail_units(s.persist) * s.nr * 128 * 128);
+        return launch_gemm_f64_persistent((const FusedNode*)nd, s.count, s.rows, s.cols, s.inner,
+                                          p->dev_coef, s.P, s.Q, s.R, s.nr, s.persist, scr, flg, b,
+                                          vec, st);
+      }
+      return launch_gemm_f64_fused(
+          (const FusedNode*)nd, s.count, s.rows, s.cols, s.inner, p->dev_coef, s.P, s.Q, s.R, b, vec,
+          st, s.opf != 0, s.nr, s.chunk,
+          s.turn_off >= 0 ? (int*)((double*)b.p[BASE_WS] + s.turn_off) + c0 * tiles_f : nullptr);
+    case STEP_K2:
+      if (p->dtype == FMM_F64)
+        return launch_gemm_f64((const LeafNode*)nd, s.count, s.rows, s.cols, s.inner, b, vec, st);
+      return launch_gemm_f32((const LeafNode*)nd,
+                             (const LeafNode*)(p->desc_host.data() + s.dev_off) + c0, s.count,
+                             s.rows, s.cols, s.inner, b, vec, p->leaf,
+                             s.arena_off >= 0 ? (float*)b.p[BASE_WS] + s.arena_off : nullptr, st);
+  }
+  return cudaSuccess;
+}
+
 template <typename T>
 static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStream_t st,
                             size_t i0 = 0, size_t i1 = (size_t)-1) {
+  constexpr int64_t kMaxNodes = 32768;  // per launch (grid.y / grid.z <= 65535)
   if (i1 > p->steps.size()) i1 = p->steps.size();
   for (size_t si = i0; si < i1; ++si) {
     const Step& s = p->steps[si];
-    const void* nd = (const uint8_t*)p->dev_desc + s.dev_off;
     TimedLaunch tl(p, s.kind == STEP_K2F ? STEP_K2 : s.kind, st);
     cudaError_t e = cudaSuccess;
-    switch (s.kind) {
-      case STEP_K1: e = launch_k1<T>(s, nd, p->dev_coef, b, vec, st); break;
-      case STEP_K3: e = launch_k3<T>(s, nd, p->dev_coef, b, vec, st); break;
-      case STEP_ACC: e = launch_acc<T>(s, nd, p->dev_coef, b, vec, st); break;
-      case STEP_ZERO: e = launch_zero<T>(s, nd, b, st); break;
-      case STEP_K2F:
-        if (p->dtype == FMM_F32) {
-          e = launch_gemm_tf32_fused((const FusedNode*)nd, (const LeafNode*)((const uint8_t*)p->dev_desc + s.dev_off2),
-                                     s.count, s.nr, s.rows, s.cols, s.inner, p->dev_coef, s.P, s.Q,
-                                     s.R, b, p->leaf == FMM_LEAF_TF32 ? 1 : 3,
-                                     (float*)b.p[BASE_WS] + s.arena_off, st, s.chunk,
-                                     s.turn_off >= 0 ? (int*)((float*)b.p[BASE_WS] + s.turn_off) : nullptr);
-        } else if (s.persist && s.persist <= device_sms()) {
-          double* scr = (double*)b.p[BASE_WS] + s.arena_off;
-          int* flg = (int*)(scr + (size_t)persistent_max_tail_units(s.persist) * s.nr * 128 * 128);
-          e = launch_gemm_f64_persistent((const FusedNode*)nd, s.count, s.rows, s.cols, s.inner,
-                                         p->dev_coef, s.P, s.Q, s.R, s.nr, s.persist, scr, flg, b,
-                                         vec, st);
-        } else {
-          e = launch_gemm_f64_fused((const FusedNode*)nd, s.count, s.rows, s.cols, s.inner,
-                                    p->dev_coef, s.P, s.Q, s.R, b, vec, st, s.opf != 0, s.nr,
-                                    s.chunk,
-                                    s.turn_off >= 0 ? (int*)((double*)b.p[BASE_WS] + s.turn_off) : nullptr);
-        }
-        break;
-      case STEP_K2:
-        if (p->dtype == FMM_F64)
-          e = launch_gemm_f64((const LeafNode*)nd, s.count, s.rows, s.cols, s.inner, b, vec, st);
-        else
-          e = launch_gemm_f32((const LeafNode*)nd, (const LeafNode*)(p->desc_host.data() + s.dev_off),
-                              s.count, s.rows, s.cols, s.inner, b, vec, p->leaf,
-                              s.arena_off >= 0 ? (float*)b.p[BASE_WS] + s.arena_off : nullptr, st);
-        break;
+    int64_t maxn = kMaxNodes;
+    if (s.kind == STEP_K2F && s.chunk > 0 && s.nr > s.chunk)  // grid.y = groups x nodes
+      maxn = std::min<int64_t>(maxn, 65535 / ((s.nr + s.chunk - 1) / s.chunk));
+    for (int64_t c0 = 0; c0 < s.count && e == cudaSuccess; c0 += maxn) {
+      Step sub = s;
+      sub.count = (int)std::min<int64_t>(maxn, s.count - c0);
+      e = launch_step<T>(p, sub, c0, b, vec, st);
     }
     if (e != cudaSuccess) return cuda_status(e, "fmm_execute launch");
   }

@@ -25,6 +25,7 @@ namespace fmm {
 namespace {
 
 constexpr int GROUP_M = 8;
+__device__ int g_group_m_f = 8;  // K2F rasterisation group (FMM_K2F_GROUP_M, experiments)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -321,10 +322,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   __syncthreads();
 
   const int tile = blockIdx.x;
-  const int per_group = GROUP_M * tiles_n;
+  const int gm = g_group_m_f;
+  const int per_group = gm * tiles_n;
   const int group = tile / per_group;
-  const int first_m = group * GROUP_M;
-  const int gsz = min(tiles_m - first_m, GROUP_M);
+  const int first_m = group * gm;
+  const int gsz = min(tiles_m - first_m, gm);
   const int tm = first_m + (tile % per_group) % gsz;
   const int tn = (tile % per_group) / gsz;
   const int64_t m0 = (int64_t)tm * C::BM, n0 = (int64_t)tn * C::BN;
@@ -1139,11 +1141,22 @@ __global__ void __launch_bounds__(C::THREADS, 1)
   cp_wait<0>();
 }
 
+void fused_group_m_init() {
+  static bool once = false;
+  if (once) return;
+  once = true;
+  if (const char* e = getenv("FMM_K2F_GROUP_M")) {
+    const int v = atoi(e);
+    if (v >= 1) cudaMemcpyToSymbol(g_group_m_f, &v, sizeof(int));
+  }
+}
+
 template <typename C, bool VEC, bool RED>
 cudaError_t launch_fused_kernel(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                 int64_t k, const double* coef, int P, int Q, int R,
                                 const Bases& b, cudaStream_t st, int nr, int chunk, int* turn) {
   const int tiles_m = (int)((m + C::BM - 1) / C::BM), tiles_n = (int)((n + C::BN - 1) / C::BN);
+  fused_group_m_init();
   const int KT = (int)std::max<int64_t>(1, (k + C::BK - 1) / C::BK);
   if (chunk <= 0 || chunk >= nr || KT < C::STAGES || !turn) chunk = nr;  // no split
   const int groups = (nr + chunk - 1) / chunk;

@@ -364,3 +364,18 @@ def test_matmul_convenience_api(fb):
     hi, lo = oracle.ref_dd(As, Bs)
     rel = lambda X: np.max(np.abs((X - hi) - lo) / np.abs(hi))
     assert rel(Cs) <= 10 * max(rel(Cso), 1e-15)
+
+
+@pytest.mark.parametrize("fusion", ["off", "on"])
+def test_deep_recursion_node_chunks(fb, fusion):
+    # Strassen L = 6 on 128^3: 7^6 = 117649 leaves of 2 x 2 x 2 -- more nodes than a grid
+    # dimension holds (65535), so the steps launch in node chunks (P:111-129 allows any depth)
+    A, B = fi.random_pair(128, 128, 128, seed=66)
+    p = fb.Plan([fb.Rule.builtin("strassen")] * 6, 128, 128, 128)
+    p.set_fusion(fusion)
+    Cg = p.execute(dev(A), dev(B)).cpu().numpy()
+    Co = oracle.fmm(A, B, OPlan.stationary(R.strassen(), 6))
+    assert parity(Cg, Co, A, B) <= TOL64
+    Ai, Bi = fi.integer_pair(128, 128, 128, seed=3, lo=-2, hi=2)
+    Ci = (Ai.astype(np.int64) @ Bi.astype(np.int64)).astype(np.float64)
+    assert np.array_equal(p.execute(dev(Ai), dev(Bi)).cpu().numpy(), Ci)
