@@ -302,8 +302,15 @@ struct Builder {
     const RuleData& r0 = rule_at(l, nodes[0].idx);
     std::vector<K1Node> all = ks;
     all.insert(all.end(), kt.begin(), kt.end());
+    int64_t items = 0;  // TMA-staged K1 work items: 4 rows x 4 KB column chunks per node
+    const int64_t cw = 4096 / elem_size(p->dtype);
+    for (K1Node& kn : all) {
+      kn.item0 = items;
+      items += ((kn.rows + 3) / 4) * ((kn.cols + cw - 1) / cw);
+    }
     if (!all.empty()) {
       Step st{};
+      st.items = items;
       st.kind = STEP_K1;
       st.count = (int)all.size();
       st.dev_off = push(all);
@@ -817,6 +824,7 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
     for (int64_t c0 = 0; c0 < s.count && e == cudaSuccess; c0 += maxn) {
       Step sub = s;
       sub.count = (int)std::min<int64_t>(maxn, s.count - c0);
+      if (sub.count != s.count) sub.items = 0;  // item prefixes span the whole step
       e = launch_step<T>(p, sub, c0, b, vec, st);
     }
     if (e != cudaSuccess) return cuda_status(e, "fmm_execute launch");

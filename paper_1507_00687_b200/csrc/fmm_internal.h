@@ -71,6 +71,7 @@ RuleQuantities rule_quantities(const RuleData& d);
 // a 2-bit code per input block (0 absent, 1 +1, 2 -1, 3 general coefficient from the table).
 struct K1Node {
   Op in;
+  int64_t item0;       // TMA-staged K1: first work item of this node (prefix over the launch)
   int64_t rows, cols;  // sub-block dims of this node's split (S: mb x kb, T: kb x nb)
   int32_t P, Q;        // split P x Q (S: m0 x k0, T: k0 x n0)
   int32_t coef_off;  // offset (in doubles) of the table in the plan's coefficient buffer
@@ -167,6 +168,7 @@ struct Step {
   bool vec_ok;       // all ws offsets / dims allow 16-byte vectors (caller bases checked later)
   int nr = 0;        // K2F: products per node (uniform)
   int64_t dev_off2 = -1;  // K2F FP32: LeafNode list (parent-major) for the hi / lo split
+  int64_t items = 0;      // K1 TMA-staged variant: work items (4 rows x 4 KB) of the launch
   int opf = 0;       // K2F: operands formed in the kernel from up to two sources (na / nb)
   int chunk = 0;     // K2F: products per CTA when a unit's chain is split (0: whole chain);
                      // turnstiles (one int per unit) at ws offset turn_off (bytes)

@@ -37,7 +37,7 @@ def main():
     ap.add_argument("--n", type=int, default=16384)
     ap.add_argument("--thin", type=int, default=256)
     ap.add_argument("--reps", type=int, default=5)
-    ap.add_argument("--only", default="", help="k4: only the scaling passes")
+    ap.add_argument("--only", default="", help="k4: only the scaling passes; k1: no scaling passes")
     a = ap.parse_args()
     n, t = a.n, a.thin
     w = fb.Rule.builtin("winograd")
@@ -45,7 +45,8 @@ def main():
     q = (n // 2) ** 2 * 8  # bytes of one quarter block of the big operand
     if a.only != "k4":
         passes_k1_k3(a, n, t, w, q, out)
-    k4(a, n, w, out)
+    if a.only != "k1":
+        k4(a, n, w, out)
     print(json.dumps(out))
 
 
