@@ -96,6 +96,13 @@ fmm_status fmm_rule_create(int m0, int k0, int n0, int R, const int32_t* U, cons
  * (<U, (swap (x) I2)V, (I2 (x) swap)W>). */
 fmm_status fmm_rule_builtin(const char* name, fmm_rule** out);
 
+/* Rule transformations (App. A-C); the result is validated
+ * (Brent) and returned as a new rule (caller destroys).  kind 1: cyclic rotation [[W,U,V]], a
+ * <n0,m0,k0> algorithm; kind 2: [[V,W,U]], <k0,n0,m0>; kind 3: transposition (C^T = B^T A^T,
+ * vec-permuted rows), <n0,k0,m0>.  Rotations and transposition keep R and nnz; Q / E of the
+ * rotations are those of the rotated tables (App. A: Strassen's three rotations share Q and E). */
+fmm_status fmm_rule_transform(const fmm_rule* rule, int kind, fmm_rule** out);
+
 /* Copy out a rule's dims and tables (any output pointer may be NULL; U/V/W must hold the
  * full table when non-NULL). */
 fmm_status fmm_rule_info(const fmm_rule* rule, int* m0, int* k0, int* n0, int* R, int32_t* U,

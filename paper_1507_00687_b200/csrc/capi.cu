@@ -23,6 +23,7 @@
 
 namespace fmm {
 int64_t brent_violations(const RuleData& d, int64_t* fi, int64_t* fj, int64_t* fk);
+bool transform_rule(const RuleData& d, int kind, RuleData* out);
 bool builtin_rule(const std::string& name, RuleData* out);
 size_t scale_ws_bytes(int64_t M, int64_t K, int64_t N);
 int* scale_flags_ptr(void* ws, int64_t M, int64_t K, int64_t N);
@@ -956,6 +957,20 @@ fmm_status fmm_rule_info(const fmm_rule* r, int* m0, int* k0, int* n0, int* R, i
 }
 
 void fmm_rule_destroy(fmm_rule* r) { delete r; }
+
+fmm_status fmm_rule_transform(const fmm_rule* r, int kind, fmm_rule** out) {
+  if (!r || !out) { set_error("fmm_rule_transform: null"); return FMM_E_ARG; }
+  RuleData d;
+  if (!transform_rule(r->d, kind, &d)) { set_error("fmm_rule_transform: kind must be 1, 2 or 3"); return FMM_E_ARG; }
+  if (!check_rule_dims(d)) { set_error("fmm_rule_transform: result dims out of range"); return FMM_E_ARG; }
+  int64_t fi = -1, fj = -1, fk = -1;
+  if (brent_violations(d, &fi, &fj, &fk) != 0) {
+    set_error("fmm_rule_transform: result violates the Brent equations");
+    return FMM_E_RULE;
+  }
+  *out = new fmm_rule{d};
+  return FMM_OK;
+}
 
 fmm_status fmm_plan_create(const fmm_rule* const* nodes, int n_nodes, int levels, int uniform,
                            int64_t M, int64_t K, int64_t N, int dtype, int leaf,

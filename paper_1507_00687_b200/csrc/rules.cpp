@@ -205,3 +205,55 @@ RuleQuantities rule_quantities(const RuleData& d) {
 }
 
 }  // namespace fmm
+
+// ---------------------------------------------------------------------------------------------
+// Rule transformations (App. A-C): cyclic rotations and transposition.  With the stated row
+// conventions (U / V column-major, W row-major) the rotation [[W,U,V]] is literally a
+// <n0,m0,k0> algorithm and [[V,W,U]] a <k0,n0,m0> one (the row numbers coincide: a row-major
+// index of an m x n matrix is the column-major index of its transpose).
+// Transposition C^T = B^T A^T gives <n0,k0,m0> = [[P V, P U, P W]] with vec-permutations:
+//   U'[jb + n0*ja] = V[ja + k0*jb],  V'[ja + k0*ia] = U[ia + m0*ja],  W'[jb*m0 + ia] = W[ia*n0 + jb].
+// ---------------------------------------------------------------------------------------------
+namespace fmm {
+
+bool transform_rule(const RuleData& d, int kind, RuleData* out) {
+  RuleData o;
+  o.R = d.R;
+  o.log2den = d.log2den;
+  const int R = d.R;
+  auto rows = [&](const std::vector<int32_t>& X) { return (int)(X.size() / R); };
+  (void)rows;
+  if (kind == 1) {  // [[W, U, V]]: <n0, m0, k0>
+    o.name = d.name + "_rot";
+    o.m0 = d.n0; o.k0 = d.m0; o.n0 = d.k0;
+    o.U = d.W; o.V = d.U; o.W = d.V;
+  } else if (kind == 2) {  // [[V, W, U]]: <k0, n0, m0>
+    o.name = d.name + "_rot2";
+    o.m0 = d.k0; o.k0 = d.n0; o.n0 = d.m0;
+    o.U = d.V; o.V = d.W; o.W = d.U;
+  } else if (kind == 3) {  // transpose: <n0, k0, m0>
+    o.name = d.name + "_T";
+    o.m0 = d.n0; o.k0 = d.k0; o.n0 = d.m0;
+    o.U.assign((size_t)d.n0 * d.k0 * R, 0);
+    o.V.assign((size_t)d.k0 * d.m0 * R, 0);
+    o.W.assign((size_t)d.m0 * d.n0 * R, 0);
+    for (int ja = 0; ja < d.k0; ++ja)
+      for (int jb = 0; jb < d.n0; ++jb)
+        for (int r = 0; r < R; ++r)
+          o.U[((size_t)jb + (size_t)d.n0 * ja) * R + r] = d.V[((size_t)ja + (size_t)d.k0 * jb) * R + r];
+    for (int ia = 0; ia < d.m0; ++ia)
+      for (int ja = 0; ja < d.k0; ++ja)
+        for (int r = 0; r < R; ++r)
+          o.V[((size_t)ja + (size_t)d.k0 * ia) * R + r] = d.U[((size_t)ia + (size_t)d.m0 * ja) * R + r];
+    for (int ia = 0; ia < d.m0; ++ia)
+      for (int jb = 0; jb < d.n0; ++jb)
+        for (int r = 0; r < R; ++r)
+          o.W[((size_t)jb * d.m0 + ia) * R + r] = d.W[((size_t)ia * d.n0 + jb) * R + r];
+  } else {
+    return false;
+  }
+  *out = o;
+  return true;
+}
+
+}  // namespace fmm

@@ -44,6 +44,7 @@ SIGNATURES = {
     "fmm_plan_set_schedule": (_I, [_P, _I]),
     "fmm_plan_set_fusion": (_I, [_P, _I]),
     "fmm_plan_set_shard_depth": (_I, [_P, _I]),
+    "fmm_rule_transform": (_I, [_P, _I, C.POINTER(_P)]),
     "fmm_plan_set_operand_fusion": (_I, [_P, _I]),
     "fmm_scale_apply": (_I, [_I, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _I64, _P, _I64, _P]),
     "fmm_rule_quantities": (_I, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double), _P, _P]),
@@ -174,6 +175,14 @@ class Rule:
               W.ctypes.data, None)
         return dict(m0=m0.value, k0=k0.value, n0=n0.value, R=R.value, U=U, V=V, W=W,
                     log2_den=den.value)
+
+    def transform(self, kind: str) -> "Rule":
+        """'rotate' ([[W,U,V]]: <n0,m0,k0>), 'rotate2' ([[V,W,U]]: <k0,n0,m0>) or 'transpose'
+        (<n0,k0,m0>), validated (fmm_rule_transform)."""
+        h = C.c_void_p()
+        _call("fmm_rule_transform", self._h, {"rotate": 1, "rotate2": 2, "transpose": 3}[kind],
+              C.byref(h))
+        return Rule(h.value, f"{self.name}_{kind}")
 
     def quantities(self):
         """nnz, Q, E, q (m0*n0), e (m0*n0) of the rule (Sec. 4.1)."""

@@ -113,3 +113,24 @@ def test_castrapel_gustafson_nonuniform_plan(fb):
                 assert oracle.parity_metric(Cg, Co, np.abs(A).max(), np.abs(B).max(), K) <= TOL64
             else:
                 assert np.array_equal(Cg, Co)
+
+
+@pytest.mark.parametrize("kind", ["rotate", "rotate2"])
+def test_rotated_323_through_the_abi(fb, kind):
+    # App. B rotations: [[W,U,V]] is <3,3,2>, [[V,W,U]] is <2,3,3>; the GPU rule
+    # comes from fmm_rule_transform, the oracle's is built independently from App. B's tables
+    b = app_b_323()
+    if kind == "rotate":
+        orule = R.make_rule("rot", 3, 3, 2, b.W, b.U, b.V)
+    else:
+        orule = R.make_rule("rot2", 2, 3, 3, b.V, b.W, b.U)
+    grule = to_gpu_rule(fb, b).transform(kind)
+    gi = grule.info()
+    assert (gi["m0"], gi["k0"], gi["n0"]) == (orule.m0, orule.k0, orule.n0)
+    M, K, N = orule.m0 * 40, orule.k0 * 36, orule.n0 * 44
+    A, B = fi.random_pair(M, K, N, seed=9)
+    p = fb.Plan([grule, fb.Rule.builtin("strassen")], 2 * M, 2 * K, 2 * N)
+    A2, B2 = fi.random_pair(2 * M, 2 * K, 2 * N, seed=10)
+    Cg = p.execute(dev(A2), dev(B2)).cpu().numpy()
+    Co = oracle.fmm(A2, B2, OPlan.uniform([orule, R.strassen()]))
+    assert oracle.parity_metric(Cg, Co, np.abs(A2).max(), np.abs(B2).max(), 2 * K) <= TOL64

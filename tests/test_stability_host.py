@@ -105,3 +105,27 @@ def test_choose_variants_is_the_brute_force_minimum():
     choice, xi = fb.choose_variants(to_gpu_rule(fb, w), [to_gpu_rule(fb, v) for v in cg])
     assert R.xi_nonuniform([[w], [cg[c] for c in choice]]) == xi
     assert xi <= R.quantities(w).E ** 2
+
+
+def test_rule_transforms_validate_and_match_table1():
+    # App. A: Strassen's rotations share Q, E; App. B: [[W,U,V]] is the <3,3,2> row of
+    # Table 1 (nnz 94, Q 11, E 23); App. C: transposition keeps E = 89, the
+    # rotations give (26, 102) and the <4,2,4> row (23, 92) (reading A21)
+    s = fb.Rule.builtin("strassen")
+    for kind in ("rotate", "rotate2", "transpose"):
+        q = s.transform(kind).quantities()
+        assert (q["Q"], q["E"]) == (8, 12)
+    b = to_gpu_rule(fb, app_b_323())
+    r1 = b.transform("rotate")
+    assert (r1.info()["m0"], r1.info()["k0"], r1.info()["n0"]) == (3, 3, 2)
+    q = r1.quantities()
+    assert (q["nnz"], q["Q"], q["E"]) == (94, 11, 23)
+    c = to_gpu_rule(fb, app_c_442())
+    assert c.transform("transpose").quantities()["E"] == 89
+    q1, q2 = c.transform("rotate").quantities(), c.transform("rotate2").quantities()
+    assert (q1["Q"], q1["E"]) == (26, 102) and (q2["Q"], q2["E"]) == (23, 92)
+    # transposition is an involution up to the table itself
+    t2 = c.transform("transpose").transform("transpose").info()
+    ci = c.info()
+    for key in ("U", "V", "W"):
+        assert np.array_equal(t2[key], ci[key])
