@@ -10,7 +10,7 @@ namespace fmm {
 
 cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
                              int64_t k, const Bases& b, int passes, float* arena,
-                             cudaStream_t st);
+                             cudaStream_t st, const LeafNode* host_leaves);
 cudaError_t launch_gemm_tf32_v2(const LeafNode* dev_leaves, const LeafNode* host_leaves,
                                 int count, int64_t m, int64_t n, int64_t k, const Bases& b,
                                 int passes, float* arena, cudaStream_t st);
@@ -127,7 +127,7 @@ cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, const LeafNode* host_lea
     static const bool use_v2 = getenv("FMM_TF32_V2") != nullptr;
     if (use_v2 && tma_ok(host_leaves, count, b))
       return launch_gemm_tf32_v2(dev_leaves, host_leaves, count, m, n, k, b, passes, arena, st);
-    return launch_gemm_tf32(dev_leaves, count, m, n, k, b, passes, arena, st);
+    return launch_gemm_tf32(dev_leaves, count, m, n, k, b, passes, arena, st, host_leaves);
   }
   const int tiles_m = (int)((m + BM - 1) / BM), tiles_n = (int)((n + BN - 1) / BN);
   dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)count);

@@ -574,7 +574,6 @@ __device__ __forceinline__ void mma_tf32_v2(uint32_t tmem_d, uint64_t a, uint64_
 // SWIZZLE_128B_BASE32B = 1, TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): k-rows of 128 B (32 floats
 // of N), 4-row core groups (SBO = 512 B), 32-float MN chunks 4 KB apart (LBO = 4096 B).
 __device__ int g_mn_lbo = 4096, g_mn_sbo = 512, g_mn_layout = 1;
-__device__ int g_dbg = 0;
 __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
@@ -722,18 +721,6 @@ __global__ void __launch_bounds__(256, 1)
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  if (g_dbg && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
-    const LeafNode& lf = leaves[0];
-    int64_t ldc;
-    float* Cp = op_ptr<float>(bases, lf.c, ldc);
-    const float* sa = (const float*)smem;
-    const float* sb = (const float*)(smem + 2 * A_BYTES);
-    for (int e = 0; e < 16; ++e) Cp[(m - 1) * ldc + e] = sa[e];
-    for (int e = 0; e < 16; ++e) Cp[(m - 1) * ldc + 16 + e] = sb[e];
-    Cp[(m - 1) * ldc + 32] = (float)KT;
-    Cp[(m - 1) * ldc + 33] = (float)passes;
-    Cp[(m - 1) * ldc + 34] = (float)tmem;
-  }
   if (warp == 2)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
                  "r"(TMEM_COLS));
@@ -753,6 +740,98 @@ __global__ void k_split_lo(const LeafNode* __restrict__ leaves, Bases bases, int
       out[r * ldo + c] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
     }
   }
+}
+
+// Vectorised hi / lo split (same elementwise split2 as k_split_tf32, so bitwise the same arena):
+// A side: 16-byte loads / stores, one float4 per thread, rows grid-strided.
+// B side: 64 x 64 tiles of T (k x n) staged through shared memory, 16-byte loads along n and
+// 16-byte stores along k of the transposed (n x kp) outputs.
+// Requires: leaf operands 16-byte aligned with ld % 4 == 0, k % 4 == 0 (checked by the caller).
+__global__ void k_split_a_vec(const LeafNode* __restrict__ leaves, Bases bases, int64_t m,
+                              int64_t k, int64_t kp, float* __restrict__ a_hi,
+                              float* __restrict__ a_lo) {
+  const LeafNode& lf = leaves[blockIdx.z];
+  int64_t lda;
+  const float* A = op_ptr<const float>(bases, lf.a, lda);
+  const size_t base = (size_t)blockIdx.z * (size_t)(m * kp);
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (c >= kp) return;
+  for (int64_t r = blockIdx.y; r < m; r += gridDim.y) {
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c < k) x = *reinterpret_cast<const float4*>(A + r * lda + c);
+    float4 h, l;
+    split2(x.x, h.x, l.x); split2(x.y, h.y, l.y); split2(x.z, h.z, l.z); split2(x.w, h.w, l.w);
+    *reinterpret_cast<float4*>(a_hi + base + r * kp + c) = h;
+    *reinterpret_cast<float4*>(a_lo + base + r * kp + c) = l;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_split_b_vec(const LeafNode* __restrict__ leaves, Bases bases,
+                                                     int64_t n, int64_t k, int64_t kp,
+                                                     float* __restrict__ b_hi, float* __restrict__ b_lo) {
+  __shared__ float tile[64][65];
+  const LeafNode& lf = leaves[blockIdx.z];
+  int64_t ldb;
+  const float* B = op_ptr<const float>(bases, lf.b, ldb);
+  const size_t base = (size_t)blockIdx.z * (size_t)(n * kp);
+  const int64_t k0 = (int64_t)blockIdx.x * 64, n0 = (int64_t)blockIdx.y * 64;
+  const int tid = threadIdx.x;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // 64 rows (k) x 16 float4 (n)
+    const int idx = tid + q * 256;
+    const int rr = idx >> 4, cc = (idx & 15) * 4;
+    const int64_t kk = k0 + rr, nn = n0 + cc;
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (kk < k) {
+      if (nn + 3 < n) x = *reinterpret_cast<const float4*>(B + kk * ldb + nn);
+      else {
+        if (nn < n) x.x = B[kk * ldb + nn];
+        if (nn + 1 < n) x.y = B[kk * ldb + nn + 1];
+        if (nn + 2 < n) x.z = B[kk * ldb + nn + 2];
+      }
+    }
+    tile[rr][cc] = x.x; tile[rr][cc + 1] = x.y; tile[rr][cc + 2] = x.z; tile[rr][cc + 3] = x.w;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {  // 64 rows (n) x 16 float4 (k) of the transposed tile
+    const int idx = tid + q * 256;
+    const int rr = idx >> 4, cc = (idx & 15) * 4;
+    const int64_t nn = n0 + rr, kk = k0 + cc;
+    if (nn >= n || kk >= kp) continue;
+    float4 h, l;
+    split2(tile[cc][rr], h.x, l.x);
+    split2(tile[cc + 1][rr], h.y, l.y);
+    split2(tile[cc + 2][rr], h.z, l.z);
+    split2(tile[cc + 3][rr], h.w, l.w);
+    *reinterpret_cast<float4*>(b_hi + base + nn * kp + kk) = h;
+    *reinterpret_cast<float4*>(b_lo + base + nn * kp + kk) = l;
+  }
+}
+
+// Split launcher: vectorised kernels when every leaf operand allows 16-byte access.
+void launch_split(const LeafNode* dev_leaves, const LeafNode* host_leaves, int count, const Bases& b,
+                  int64_t m, int64_t n, int64_t k, int64_t kp, float* a_hi, float* a_lo, float* b_hi,
+                  float* b_lo, cudaStream_t st) {
+  bool vec = host_leaves != nullptr && k % 4 == 0 && n % 4 == 0;
+  for (int i = 0; vec && i < count; ++i) {
+    int64_t lda, ldb;
+    const float* A = op_ptr<const float>(b, host_leaves[i].a, lda);
+    const float* B = op_ptr<const float>(b, host_leaves[i].b, ldb);
+    vec = !((((uintptr_t)A) & 15u) || (((uintptr_t)B) & 15u) || (lda & 3) || (ldb & 3));
+  }
+  if (vec) {
+    k_split_a_vec<<<dim3((unsigned)((kp / 4 + 255) / 256), (unsigned)(m < 8192 ? m : 8192), (unsigned)count), 256, 0, st>>>(
+        dev_leaves, b, m, k, kp, a_hi, a_lo);
+    k_split_b_vec<<<dim3((unsigned)((kp + 63) / 64), (unsigned)((n + 63) / 64), (unsigned)count), 256, 0, st>>>(
+        dev_leaves, b, n, k, kp, b_hi, b_lo);
+    return;
+  }
+  dim3 blk(32, 8);
+  k_split_tf32<<<dim3((unsigned)(kp / 32), (unsigned)((m + 31) / 32), (unsigned)count), blk, 0, st>>>(
+      dev_leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, 0);
+  k_split_tf32<<<dim3((unsigned)(kp / 32), (unsigned)((n + 31) / 32), (unsigned)count), blk, 0, st>>>(
+      dev_leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, 1);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -792,7 +871,7 @@ size_t tf32_arena_floats(int64_t count, int64_t m, int64_t n, int64_t k) {
 
 cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
                              int64_t k, const Bases& b, int passes, float* arena,
-                             cudaStream_t st) {
+                             cudaStream_t st, const LeafNode* host_leaves) {
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
   {
     static int mode = -1;
@@ -808,13 +887,7 @@ cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, i
   float* a_lo = a_hi + (size_t)count * m * kp;
   float* b_hi = a_lo + (size_t)count * m * kp;
   float* b_lo = b_hi + (size_t)count * n * kp;
-  if (kp > 0) {
-    dim3 blk(32, 8);
-    k_split_tf32<<<dim3((unsigned)(kp / 32), (unsigned)((m + 31) / 32), (unsigned)count), blk, 0, st>>>(
-        dev_leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, 0);
-    k_split_tf32<<<dim3((unsigned)(kp / 32), (unsigned)((n + 31) / 32), (unsigned)count), blk, 0, st>>>(
-        dev_leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, 1);
-  }
+  if (kp > 0) launch_split(dev_leaves, host_leaves, count, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, st);
   static const int cfg = [] {
     const char* e = getenv("FMM_TF32_CFG");  // 0: BK 32 / 2 stages (default), 1: BK 16 / 4 stages
     return e ? atoi(e) : 0;
@@ -858,13 +931,7 @@ cudaError_t launch_gemm_tf32_fused(const FusedNode* dev_nodes, const LeafNode* d
   float* a_lo = a_hi + (size_t)leaves * m * kp;
   float* b_hi = a_lo + (size_t)leaves * m * kp;
   float* b_lo = b_hi + (size_t)leaves * n * kp;
-  if (kp > 0) {
-    dim3 blk(32, 8);
-    k_split_tf32<<<dim3((unsigned)(kp / 32), (unsigned)((m + 31) / 32), (unsigned)leaves), blk, 0, st>>>(
-        dev_split_leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, 0);
-    k_split_tf32<<<dim3((unsigned)(kp / 32), (unsigned)((n + 31) / 32), (unsigned)leaves), blk, 0, st>>>(
-        dev_split_leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, 1);
-  }
+  if (kp > 0) launch_split(dev_split_leaves, nullptr, leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, st);
   CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
   const int64_t kpe = kp > 0 ? kp : TBK;
   if (!make_map(&ma_hi, a_hi, kpe, m, leaves, TBM, 32) || !make_map(&ma_lo, a_lo, kpe, m, leaves, TBM, 32) ||
@@ -909,7 +976,6 @@ cudaError_t launch_gemm_tf32_v2(const LeafNode* dev_leaves, const LeafNode* host
       const char* s2 = getenv("FMM_MN_SBO");
       if (l) { int v = atoi(l); cudaMemcpyToSymbol(g_mn_lbo, &v, sizeof(int)); }
       if (s2) { int v = atoi(s2); cudaMemcpyToSymbol(g_mn_sbo, &v, sizeof(int)); }
-      if (getenv("FMM_TF32_DEBUG")) { int v = 1; cudaMemcpyToSymbol(g_dbg, &v, sizeof(int)); }
       if (const char* lt = getenv("FMM_MN_LAYOUT")) { int v = atoi(lt); cudaMemcpyToSymbol(g_mn_layout, &v, sizeof(int)); }
     }
   }
