@@ -1509,15 +1509,11 @@ fmm_status fmm_node_st(const fmm_rule* rule, int dtype, int64_t m, int64_t k, in
   if (!rule || !A || !B || !S || !T) { set_error("fmm_node_st: null"); return FMM_E_ARG; }
   const RuleData& r = rule->d;
   if (m % r.m0 || k % r.k0 || n % r.n0) { set_error("fmm_node_st: dims not divisible"); return FMM_E_SHAPE; }
-  fmm_scaling none{FMM_SCALE_NONE, 1, 0, 1, 0};
-  const fmm_rule* nodes[1] = {rule};
-  fmm_plan* p = nullptr;
   // build K1 descriptors directly (no plan schedule needed): ws base = S for U, T for V
   std::vector<double> coef;
   for (int i = 0; i < r.m0 * r.k0; ++i) for (int q = 0; q < r.R; ++q) coef.push_back(r.coef(r.U, i, q));
   const int offV = (int)coef.size();
   for (int j = 0; j < r.k0 * r.n0; ++j) for (int q = 0; q < r.R; ++q) coef.push_back(r.coef(r.V, j, q));
-  (void)none; (void)nodes; (void)p;
   const int64_t mb = m / r.m0, kb = k / r.k0, nb = n / r.n0;
   K1Node ks{}, kt{};
   ks.in = Op{BASE_A, 0, 0, 0, -1};

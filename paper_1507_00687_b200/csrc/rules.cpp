@@ -221,8 +221,6 @@ bool transform_rule(const RuleData& d, int kind, RuleData* out) {
   o.R = d.R;
   o.log2den = d.log2den;
   const int R = d.R;
-  auto rows = [&](const std::vector<int32_t>& X) { return (int)(X.size() / R); };
-  (void)rows;
   if (kind == 1) {  // [[W, U, V]]: <n0, m0, k0>
     o.name = d.name + "_rot";
     o.m0 = d.n0; o.k0 = d.m0; o.n0 = d.k0;
