@@ -191,6 +191,39 @@ def cpu_baseline(A_host, B_host, plan_rules, M, K, N, C_gpu_host=None, target_s=
 
 
 # ------------------------------------------------------------------------------------------
+def pass_bytes(rule_infos, M, K, N, esz, fused_leaf_level):
+    """Algorithmic HBM bytes of the add passes of a uniform plan: per level, K1
+    reads each node's A / B block once and writes the non-trivial S_r / T_r (a column with a
+    single +1 is an alias); K3 reads the R child products and writes the node's output; with
+    the leaf-parent level fused, that level only writes its output once."""
+    def nontrivial(X, R):
+        """(number of non-trivial columns, number of blocks they read)"""
+        cnt, used = 0, set()
+        for r in range(R):
+            col = [X[i][r] for i in range(len(X))]
+            nz = [c for c in col if c != 0]
+            if not (len(nz) == 1 and nz[0] == 1):
+                cnt += 1
+                used |= {i for i in range(len(X)) if X[i][r] != 0}
+        return cnt, len(used)
+    total, nodes = 0, 1
+    m, k, n = M, K, N
+    L = len(rule_infos)
+    for l, ri in enumerate(rule_infos):
+        R, m0, k0, n0 = ri["R"], ri["m0"], ri["k0"], ri["n0"]
+        mb, kb, nb = m // m0, k // k0, n // n0
+        (nsa, ua), (nsb, ub) = nontrivial(ri["U"], R), nontrivial(ri["V"], R)
+        total += nodes * ((ua + nsa) * mb * kb + (ub + nsb) * kb * nb) * esz  # K1
+        if l == L - 1 and fused_leaf_level:
+            total += nodes * m * n * esz  # fused W-combination: the output written once
+        else:
+            total += nodes * (R * mb * nb + m * n) * esz  # K3: read R products, write the output
+        nodes *= R
+        m, k, n = mb, kb, nb
+    return total
+
+
+# ------------------------------------------------------------------------------------------
 def run_reference(args):
     """--impl reference: the CPU oracle (this tier's reference arm) timed on bounded samples of
     the same workload, rank 0 only."""
@@ -385,6 +418,22 @@ def run_fmm(args):
                 "timing_note": "K2 launch times from CUDA events the library records on the launch "
                                "stream" + (" (separate pass: graph replay in the timed region)" if use_graph else "")}
 
+    # ---- whole-step roofline: leaf flops at the tensor peak + algorithmic pass bytes at the
+    #      measured copy bandwidth (SURVEY §8(d) "pipeline roofline") ---------------------------
+    hbm = 6543.4
+    try:
+        hbm = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        pass
+    pbytes = pass_bytes([fb.Rule.builtin(r).info() for r in rules], M, K, N, esz, fused) if ws == 1 else None
+    pipeline = None
+    if pbytes is not None and args.scaling == "none":
+        t_roof = leaf_flops_step / (peak * 1e12) + pbytes / (hbm * 1e9)
+        pipeline = {"t_roof_ms": t_roof * 1e3, "frac": t_roof * 1e3 / (ms / args.steps),
+                    "leaf_flops": leaf_flops_step, "pass_bytes": pbytes,
+                    "note": "leaf flops / leaf-kernel peak + algorithmic K1 / K3 bytes / measured "
+                            "copy bandwidth (MEASURED_PEAKS.json hbm_gbs); frac = t_roof / t"}
+
     # ---- end-to-end through the C ABI with host buffers ---------------------------------------
     e2e = None
     if not args.no_e2e:
@@ -448,7 +497,8 @@ def run_fmm(args):
                   if not small else "L2 flushed (256 MB write) between timed steps, outside the events",
                        "leaf": {0: "native", 1: "tf32", 2: "3xtf32"}[leaf],
                        "k3_fused_in_leaf_epilogue": bool(fused)},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "roofline": roofline, "pipeline_roofline": pipeline, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": clocks,
             "gpu_launches": plan.launch_count() * args.steps,
             "cuda_graph": use_graph,
         }

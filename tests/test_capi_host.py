@@ -150,3 +150,17 @@ def test_operand_fusion_skips_leaf_level_formation():
     p.set_operand_fusion(True)
     assert p.launch_count() == n0 - 1  # no leaf-level K1 (S and T) launch
     assert p.workspace_bytes() < w0
+
+
+def test_bench_pass_byte_model():
+    # bench.py's pipeline roofline counts the algorithmic pass bytes: one S-W
+    # level on n^3: K1 reads the 4 quarter blocks of A and B and writes 4 non-trivial S and T;
+    # K3 reads 7 products and writes 4 quarters; a fused leaf level writes its output only;
+    # classical levels form nothing (all operands are aliases)
+    import bench
+    w = fb.Rule.builtin("winograd").info()
+    c = fb.Rule.builtin("classical222").info()
+    n, q = 1024, (512 * 512) * 8
+    assert bench.pass_bytes([w], n, n, n, 8, False) == (4 + 4) * q * 2 + (7 + 4) * q
+    assert bench.pass_bytes([w], n, n, n, 8, True) == (4 + 4) * q * 2 + 4 * q
+    assert bench.pass_bytes([c], n, n, n, 8, False) == (8 + 4) * q
