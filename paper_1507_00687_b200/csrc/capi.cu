@@ -177,6 +177,7 @@ fmm_plan::~fmm_plan() {
 namespace {
 
 constexpr int kPersistCtas = 148;  // B200 SMs: one persistent K2P CTA per SM
+constexpr int64_t kK2fSmallK = 1024;  // leaf inner dimension up to which K2F uses 64 x 64 tiles
 
 int elem_size(int dtype) { return dtype == FMM_F64 ? 8 : 4; }
 
@@ -351,8 +352,7 @@ struct Builder {
   // chain is split into groups of `chunk` products, dispatched group-major onto kSMs SMs in
   // order (one CTA per SM), each item costing its products plus a pipeline fill of
   // STAGES / KT products; group g of a unit cannot finish before group g-1 of that unit.
-  static double fused_makespan(int64_t units, int R, int chunk, int KT) {
-    constexpr int kSMs = 148;
+  static double fused_makespan(int64_t units, int R, int chunk, int KT, int kSMs) {
     const int groups = (R + chunk - 1) / chunk;
     const double fill = 4.0 / std::max(KT, 1);
     std::vector<double> sm(kSMs, 0.0), prev(units, 0.0);
@@ -371,7 +371,7 @@ struct Builder {
     return span;
   }
   // best chain split for a fused leaf level (chunk = R: no split); efficiency out
-  static int best_chunk(int64_t units, int R, int KT, double* eff) {
+  static int best_chunk(int64_t units, int R, int KT, int slots, double* eff) {
     if (const char* ce = getenv("FMM_CHUNK")) {  // experiments: force the split
       const int c = atoi(ce);
       if (c >= 1 && c <= R) {
@@ -380,16 +380,27 @@ struct Builder {
       }
     }
     int best = R;
-    double best_span = fused_makespan(units, R, R, KT);
+    double best_span = fused_makespan(units, R, R, KT, slots);
     if (KT >= 4 && units <= (1 << 16)) {
       for (int groups = 2; groups <= 3; ++groups) {
         const int c = (R + groups - 1) / groups;
-        const double sp = fused_makespan(units, R, c, KT);
+        const double sp = fused_makespan(units, R, c, KT, slots);
         if (sp < best_span * 0.995) { best_span = sp; best = c; }
       }
     }
-    if (eff) *eff = (double)units * R / (148.0 * best_span);
+    if (eff) *eff = (double)units * R / ((double)slots * best_span);
     return best;
+  }
+
+  // K2F tile configuration for this plan's leaves: the 64 x 64 tile kernel (v13, 3 CTAs per
+  // SM, so one CTA's epilogue overlaps two others' mainloops) for short leaf inner dimensions,
+  // the 128 x 128 kernel (v16, one CTA per SM) otherwise (profiles/r01_fusion_variants.md).
+  int k2f_cfg() const {
+    if (const char* e = getenv("FMM_K2F_VARIANT")) return atoi(e);
+    return p->lk[p->L] <= kK2fSmallK ? 13 : 16;
+  }
+  int k2f_tile() const { return k2f_cfg() == 13 ? 64 : 128; }
+  int k2f_slots() const { return k2f_cfg() == 13 ? 3 * 148 : 148;
   }
 
   bool fuse_leaves(int64_t nparents) const {
@@ -398,12 +409,14 @@ struct Builder {
     if (p->fusion == 1) return true;
     if (tc32) return false;  // k2f_tf32 measured slower than k2_tf32 + K3 at C5 (310 vs 287 ms): opt-in
     {  // chain splitting (turnstiles) smooths the wave quantisation of R-product units
-      const int64_t tiles = ((p->lm[p->L] + 127) / 128) * ((p->ln[p->L] + 127) / 128);
+      const int ts = k2f_tile();
+      const int64_t tiles = ((p->lm[p->L] + ts - 1) / ts) * ((p->ln[p->L] + ts - 1) / ts);
       const int R = p->rules[p->node_rule[p->L - 1][0]].R;
       const int KT = (int)((p->lk[p->L] + 15) / 16);
+      const int slots = k2f_slots();
       double eff = 0;
-      if (p->split_chains && KT >= 4 && nparents * tiles >= 148 && nparents * tiles * R >= 4 * 148) {
-        best_chunk(nparents * tiles, R, KT, &eff);
+      if (p->split_chains && KT >= 4 && nparents * tiles >= slots && nparents * tiles * R >= 4 * slots) {
+        best_chunk(nparents * tiles, R, KT, slots, &eff);
         if (eff >= 0.93) return true;
       }
     }
@@ -479,9 +492,12 @@ struct Builder {
     }
     // persistent hybrid data-parallel / stream-K form (K2P) when the leaf has >= STAGES k-tiles
     // chain split with per-unit turnstiles (breadth-first levels: every parent has all R products)
+    st.k2f_cfg = k2f_cfg();
     if (p->split_chains && fz.size() > 0 && fz[0].nr == r0.R && (st.inner + 15) / 16 >= 4) {
-      const int64_t tiles = ((st.rows + 127) / 128) * ((st.cols + 127) / 128);
-      const int c = best_chunk((int64_t)st.count * tiles, r0.R, (int)((st.inner + 15) / 16), nullptr);
+      const int ts = k2f_tile();
+      const int64_t tiles = ((st.rows + ts - 1) / ts) * ((st.cols + ts - 1) / ts);
+      const int c = best_chunk((int64_t)st.count * tiles, r0.R, (int)((st.inner + 15) / 16),
+                               k2f_slots(), nullptr);
       if (c < r0.R) {
         st.chunk = c;
         st.turn_off = ws_alloc((st.count * tiles + 1) / 2 + 1);  // ints, in 8-byte elements
@@ -772,8 +788,9 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
     case STEP_K2F: node_bytes = sizeof(FusedNode); break;
   }
   const void* nd = (const uint8_t*)p->dev_desc + s.dev_off + c0 * node_bytes;
+  const int ts = s.k2f_cfg == 13 ? 64 : 128;
   const int64_t tiles_f = p->dtype == FMM_F32 ? ((s.rows + 127) / 128) * ((s.cols + 255) / 256)
-                                              : ((s.rows + 127) / 128) * ((s.cols + 127) / 128);
+                                              : ((s.rows + ts - 1) / ts) * ((s.cols + ts - 1) / ts);
   switch (s.kind) {
     case STEP_K1: return launch_k1<T>(s, nd, p->dev_coef, b, vec, st);
     case STEP_K3: return launch_k3<T>(s, nd, p->dev_coef, b, vec, st);
@@ -798,7 +815,8 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
       return launch_gemm_f64_fused(
           (const FusedNode*)nd, s.count, s.rows, s.cols, s.inner, p->dev_coef, s.P, s.Q, s.R, b, vec,
           st, s.opf != 0, s.nr, s.chunk,
-          s.turn_off >= 0 ? (int*)((double*)b.p[BASE_WS] + s.turn_off) + c0 * tiles_f : nullptr);
+          s.turn_off >= 0 ? (int*)((double*)b.p[BASE_WS] + s.turn_off) + c0 * tiles_f : nullptr,
+          s.k2f_cfg);
     case STEP_K2:
       if (p->dtype == FMM_F64)
         return launch_gemm_f64((const LeafNode*)nd, s.count, s.rows, s.cols, s.inner, b, vec, st);

@@ -170,6 +170,7 @@ struct Step {
   int64_t dev_off2 = -1;  // K2F FP32: LeafNode list (parent-major) for the hi / lo split
   int64_t items = 0;      // K1 TMA-staged variant: work items (4 rows x 4 KB) of the launch
   int opf = 0;       // K2F: operands formed in the kernel from up to two sources (na / nb)
+  int k2f_cfg = 16;  // K2F tile configuration (16: 128 x 128 / 1 CTA per SM, 13: 64 x 64 / 3)
   int chunk = 0;     // K2F: products per CTA when a unit's chain is split (0: whole chain);
                      // turnstiles (one int per unit) at ws offset turn_off (bytes)
   int64_t turn_off = -1;
@@ -200,7 +201,7 @@ cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, in
 cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                   int64_t k, const double* dev_coef, int P, int Q, int R,
                                   const Bases& b, bool vec, cudaStream_t st, bool opf = false,
-                                  int nr = 0, int chunk = 0, int* turn = nullptr);
+                                  int nr = 0, int chunk = 0, int* turn = nullptr, int cfg = 16);
 // K2P: persistent hybrid data-parallel / stream-K form of K2F (one CTA per SM, `ctas` CTAs;
 // every node has NR products).  scratch / flags: persistent_scratch_bytes(ctas, NR) of
 // workspace (flags zeroed by the launcher).  Needs ceil(k / BK) >= persistent_min_kt().

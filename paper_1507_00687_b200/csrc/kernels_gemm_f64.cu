@@ -1336,7 +1336,7 @@ using VO = Cfg<128, 128, 16, 3, 2, 4, 1, true>;  // operand-fused K2O: 3 stages 
 cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                   int64_t k, const double* dev_coef, int P, int Q, int R,
                                   const Bases& b, bool vec, cudaStream_t st, bool opf, int nr,
-                                  int chunk, int* turn) {
+                                  int chunk, int* turn, int cfg) {
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
   if (opf) {
     const int tiles_m = (int)((m + VO::BM - 1) / VO::BM), tiles_n = (int)((n + VO::BN - 1) / VO::BN);
@@ -1350,7 +1350,7 @@ cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t
     };
     return vec ? go(k2o_gemm_f64<VO, true>) : go(k2o_gemm_f64<VO, false>);
   }
-  switch (fused_variant()) {
+  switch (getenv("FMM_K2F_VARIANT") ? fused_variant() : cfg) {
     case 13: return launch_fused_cfg<V13>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st, nr, chunk, turn);
     case 15: return launch_fused_cfg<V15>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st, nr, chunk, turn);
     case 17: return launch_fused_cfg<V17>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st, nr, chunk, turn);
