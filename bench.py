@@ -313,6 +313,8 @@ def run_fmm(args):
                    scaling=scaling)
     if ws > 1 and args.shard_depth > 1:
         plan.set_shard_depth(args.shard_depth)
+    if ws > 1 and args.comm != "reduce":
+        plan.set_comm_mode(args.comm)
     if ws > 1:
         uid = [fb.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, 0)
@@ -492,7 +494,7 @@ def run_fmm(args):
                                    + (f", scaling {args.scaling} (pow2, tau=1)" if args.scaling != "none" else ""),
                        "parallelism": (f"top-level r round-robin over {ws} GPU(s)" if args.shard_depth == 1
                                        else f"depth-{args.shard_depth} paths round-robin over {ws} GPU(s)")
-                                      + (", ncclReduce of C" if ws > 1 else ""),
+                                      + (f", {args.comm} of C" if ws > 1 else ""),
                        "l2": ("operands %.1f GiB each > 126 MB L2 (no flush needed)" % (M * K * esz / 2**30))
                   if not small else "L2 flushed (256 MB write) between timed steps, outside the events",
                        "leaf": {0: "native", 1: "tf32", 2: "3xtf32"}[leaf],
@@ -523,6 +525,8 @@ def main():
                     choices=["none", "outside", "inside", "out_in", "in_out", "repeated"])
     ap.add_argument("--shard-depth", type=int, default=1,
                     help="multi-GPU units = paths of the first d levels (fmm_plan_set_shard_depth)")
+    ap.add_argument("--comm", default="reduce", choices=["reduce", "allreduce", "reduce_scatter"],
+                    help="multi-GPU exchange of the partial C (fmm_plan_set_comm_mode)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-warmup", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -197,6 +197,14 @@ fmm_status fmm_choose_variants(const fmm_rule* root, const fmm_rule* const* vari
  * 1 <= depth <= levels. */
 fmm_status fmm_plan_set_shard_depth(fmm_plan* plan, int depth);
 
+/* The multi-GPU exchange after the ranks' partial products (host-only; default 0):
+ * 0 = ncclReduce(sum) onto rank 0 (C valid on rank 0);
+ * 1 = ncclAllReduce(sum) (C valid on every rank);
+ * 2 = ncclReduceScatter(sum), in place: rank r's C holds the finished rows
+ *     [r M / P, (r + 1) M / P) (M divisible by P, else FMM_E_SHAPE) -- a distributed C at
+ *     1 / P of the reduce's per-rank output traffic. */
+fmm_status fmm_plan_set_comm_mode(fmm_plan* plan, int mode);
+
 /* Host-only query: owned[u] = 1 if shard unit u is computed by `rank`; *R receives the number
  * of units (the top-level rank R at shard depth 1). */
 fmm_status fmm_plan_owned(const fmm_plan* plan, int rank, int nranks, int32_t* owned, int* R);

@@ -69,6 +69,8 @@ struct NcclApi {
   ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*reduce)(const void*, void*, size_t, int, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allreduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*reduce_scatter)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
 };
@@ -88,6 +90,8 @@ NcclApi* nccl() {
     api.getUniqueId = (decltype(api.getUniqueId))dlsym(api.h, "ncclGetUniqueId");
     api.commInitRank = (decltype(api.commInitRank))dlsym(api.h, "ncclCommInitRank");
     api.reduce = (decltype(api.reduce))dlsym(api.h, "ncclReduce");
+    api.allreduce = (decltype(api.allreduce))dlsym(api.h, "ncclAllReduce");
+    api.reduce_scatter = (decltype(api.reduce_scatter))dlsym(api.h, "ncclReduceScatter");
     api.commDestroy = (decltype(api.commDestroy))dlsym(api.h, "ncclCommDestroy");
     api.getErrorString = (decltype(api.getErrorString))dlsym(api.h, "ncclGetErrorString");
   });
@@ -116,6 +120,7 @@ struct fmm_plan {
   int schedule = 0;  // 0 auto, 1 breadth-first, 2 depth-first top level
   int fusion = 2;    // W-combination of the leaves' parents in the leaf GEMM epilogue: 0 off, 1 on, 2 auto
   int shard_depth = 1;  // multi-GPU: units = paths of the first shard_depth levels, round-robin
+  int comm_mode = 0;    // multi-GPU exchange: 0 reduce to rank 0, 1 all-reduce, 2 reduce-scatter
   bool persistent = false;  // fused leaves as the persistent stream-K kernel (K2P) where eligible
   bool operand_fusion = false;  // S_r / T_r with <= 2 +-1 terms formed inside the fused leaf kernel
   bool split_chains = true;     // fused units' product chains split over CTAs (turnstiles)
@@ -1125,6 +1130,12 @@ fmm_status fmm_plan_fused_launches(const fmm_plan* p, int64_t* n) {
   return FMM_OK;
 }
 
+fmm_status fmm_plan_set_comm_mode(fmm_plan* p, int mode) {
+  if (!p || mode < 0 || mode > 2) { set_error("fmm_plan_set_comm_mode: mode must be 0, 1 or 2"); return FMM_E_ARG; }
+  p->comm_mode = mode;
+  return FMM_OK;
+}
+
 fmm_status fmm_plan_set_shard_depth(fmm_plan* p, int depth) {
   if (!p || depth < 1 || (p->L > 0 && depth > p->L)) { set_error("fmm_plan_set_shard_depth: depth must be in [1, L]"); return FMM_E_ARG; }
   int64_t units = 1;
@@ -1295,9 +1306,23 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
     if (!api) { set_error("NCCL not loadable"); return FMM_E_NCCL; }
     if (ldc != p->N) { set_error("fmm_execute: multi-GPU reduce needs ldc == N"); return FMM_E_ARG; }
     TimedLaunch tl(p, 7, st);
-    ncclResult_t r = api->reduce(C, C, (size_t)(p->M * p->N), p->dtype == FMM_F64 ? ncclFloat64_ : ncclFloat32_,
-                                 ncclSum_, 0, p->comm, st);
-    if (r != 0) { set_error(std::string("ncclReduce: ") + (api->getErrorString ? api->getErrorString(r) : "?")); return FMM_E_NCCL; }
+    const int dt = p->dtype == FMM_F64 ? ncclFloat64_ : ncclFloat32_;
+    const size_t total = (size_t)(p->M * p->N);
+    ncclResult_t r = 0;
+    const char* what = "ncclReduce";
+    if (p->comm_mode == 1) {  // every rank gets C
+      what = "ncclAllReduce";
+      r = api->allreduce ? api->allreduce(C, C, total, dt, ncclSum_, p->comm, st) : 1;
+    } else if (p->comm_mode == 2) {  // rank r gets rows [r M/P, (r+1) M/P) of C, in place
+      what = "ncclReduceScatter";
+      if (p->M % p->nranks) { set_error("fmm_execute: reduce-scatter needs M divisible by the ranks"); return FMM_E_SHAPE; }
+      const size_t cnt = total / (size_t)p->nranks;
+      const size_t es = (size_t)elem_size(p->dtype);
+      r = api->reduce_scatter ? api->reduce_scatter(C, (uint8_t*)C + (size_t)p->rank * cnt * es, cnt, dt, ncclSum_, p->comm, st) : 1;
+    } else {  // C on rank 0
+      r = api->reduce(C, C, total, dt, ncclSum_, 0, p->comm, st);
+    }
+    if (r != 0) { set_error(std::string(what) + ": " + (api->getErrorString ? api->getErrorString(r) : "?")); return FMM_E_NCCL; }
   }
   return FMM_OK;
 }

@@ -44,6 +44,7 @@ SIGNATURES = {
     "fmm_plan_set_schedule": (_I, [_P, _I]),
     "fmm_plan_set_fusion": (_I, [_P, _I]),
     "fmm_plan_set_shard_depth": (_I, [_P, _I]),
+    "fmm_plan_set_comm_mode": (_I, [_P, _I]),
     "fmm_rule_transform": (_I, [_P, _I, C.POINTER(_P)]),
     "fmm_plan_set_operand_fusion": (_I, [_P, _I]),
     "fmm_scale_apply": (_I, [_I, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _I64, _P, _I64, _P]),
@@ -308,6 +309,10 @@ class Plan:
         n = C.c_int64()
         _call("fmm_plan_fused_launches", self._h, C.byref(n))
         return n.value
+
+    def set_comm_mode(self, mode: str):
+        """Multi-GPU exchange: 'reduce' (C on rank 0), 'allreduce', 'reduce_scatter' (rows)."""
+        _call("fmm_plan_set_comm_mode", self._h, {"reduce": 0, "allreduce": 1, "reduce_scatter": 2}[mode])
 
     def set_shard_depth(self, depth: int):
         """Multi-GPU units = paths of the first `depth` levels (fmm_plan_set_shard_depth)."""

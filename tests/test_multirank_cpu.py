@@ -155,3 +155,41 @@ def test_two_rank_partition_and_reduce(world):
     A, B = fi.random_pair(128, 128, 128, seed=21)
     full = oracle.fmm(A, B, R.Plan.stationary(R.winograd(), 2))
     assert oracle.parity_metric(total, full, np.abs(A).max(), np.abs(B).max(), 128) <= 1e-13
+
+
+def _worker_rs(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1507_00687_b200 as fb
+    w = fb.Rule.builtin("winograd")
+    plan = fb.Plan([w, w], 128, 128, 128)
+    plan.set_comm_mode("reduce_scatter")  # host-only setting; the exchange below mirrors it
+    owned = plan.owned(rank, world)
+    A, B = fi.random_pair(128, 128, 128, seed=21)
+    part = torch.from_numpy(_partial_oracle(rank, world, owned, A, B))
+    rows = 128 // world
+    mine = torch.empty((rows, 128), dtype=part.dtype)
+    dist.reduce_scatter_tensor(mine, part)  # rank r receives rows [r M/P, (r+1) M/P)
+    out_q.put((rank, mine.numpy()))
+    dist.destroy_process_group()
+
+
+def test_two_rank_reduce_scatter_rows():
+    # comm mode 2 (fmm_plan_set_comm_mode): the ranks' partials reduce-scattered by rows give
+    # the product's row blocks (within the parity tolerance of the full oracle product)
+    import oracle
+    from oracle import rules as R
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_rs, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    A, B = fi.random_pair(128, 128, 128, seed=21)
+    full = oracle.fmm(A, B, R.Plan.stationary(R.winograd(), 2))
+    C = np.vstack([got[0], got[1]])
+    assert oracle.parity_metric(C, full, np.abs(A).max(), np.abs(B).max(), 128) <= 1e-13
