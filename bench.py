@@ -68,6 +68,8 @@ class ClockSampler:
         self.index = index
         self.proc = None
         self.lines = []
+        self.stamps = []
+        self.first = 0
 
     def start(self):
         try:
@@ -83,10 +85,23 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+            self.stamps.append(time.monotonic())
 
-    def stop(self):
+    def wait_first(self, timeout=3.0):
+        """Block until nvidia-smi has produced its first line (it takes ~0.1-0.3 s to start)."""
+        t = time.monotonic()
+        while self.proc is not None and not self.lines and time.monotonic() - t < timeout:
+            time.sleep(0.01)
+
+    def mark(self):
+        """Index of the next sample: samples from here on were taken after this call."""
+        return len(self.lines)
+
+    def stop(self, first=None):
         if self.proc is None:
             return None
+        if first is not None:
+            self.first = first
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -94,7 +109,7 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[self.first:]:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
@@ -345,6 +360,8 @@ def run_fmm(args):
     small = (M * K + K * N + M * N) * esz < (512 << 20)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if small else None
     sampler.start()
+    sampler.wait_first()
+    first = sampler.mark()
     if not small:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -365,11 +382,31 @@ def run_fmm(args):
             evs.append((a, b2))
         torch.cuda.synchronize()
         ms = sum(a.elapsed_time(b2) for a, b2 in evs)
-    if ws > 1:
-        dist.barrier()
-    clocks = sampler.stop()
     kinds = plan.step_times()
     plan.set_timing(False)
+    # A timed region shorter than the 200 ms sampling period may see no sample: keep the GPU on
+    # the same (untimed) steps until one arrives, and say so in the clocks record.
+    extra = 0
+    t_ext = time.monotonic()
+    while True:
+        need = sampler.proc is not None and sampler.mark() == first and time.monotonic() - t_ext < 2.0
+        if ws > 1:  # the step may hold a collective: every rank runs the same number of extras
+            f = torch.tensor([1.0 if need else 0.0], device="cuda")
+            dist.all_reduce(f, op=dist.ReduceOp.MAX)
+            need = f.item() > 0
+        if not need:
+            break
+        with torch.cuda.stream(stream):
+            if flush is not None:
+                flush.fill_(1)
+            step()
+        torch.cuda.synchronize()
+        extra += 1
+    if ws > 1:
+        dist.barrier()
+    clocks = sampler.stop(first)
+    if clocks is not None:
+        clocks["untimed_steps_after"] = extra
     if ws > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
