@@ -206,35 +206,79 @@ def cpu_baseline(A_host, B_host, plan_rules, M, K, N, C_gpu_host=None, target_s=
 
 
 # ------------------------------------------------------------------------------------------
-def pass_bytes(rule_infos, M, K, N, esz, fused_leaf_level):
+def pass_bytes(rule_infos, M, K, N, esz, fused_leaf_level, two_level=True):
     """Algorithmic HBM bytes of the add passes of a uniform plan: per level, K1
     reads each node's A / B block once and writes the non-trivial S_r / T_r (a column with a
-    single +1 is an alias); K3 reads the R child products and writes the node's output; with
-    the leaf-parent level fused, that level only writes its output once."""
-    def nontrivial(X, R):
+    single +1 is an alias); with two levels per pass (K1X2, levels paired from the bottom where
+    both split <= 4 blocks) a pass reads the sub-blocks its formed grandchildren use once and
+    writes only the grandchildren (all but the products trivial at both levels); K3 reads the R
+    child products and writes the node's output; with the leaf-parent level fused, that level
+    only writes its output once."""
+    def col(X, r):
+        return [i for i in range(len(X)) if X[i][r] != 0]
+
+    def trivial(X, r):
+        nz = col(X, r)
+        return len(nz) == 1 and X[nz[0]][r] == 1
+
+    def one_level(X, R):
         """(number of non-trivial columns, number of blocks they read)"""
         cnt, used = 0, set()
         for r in range(R):
-            col = [X[i][r] for i in range(len(X))]
-            nz = [c for c in col if c != 0]
-            if not (len(nz) == 1 and nz[0] == 1):
+            if not trivial(X, r):
                 cnt += 1
-                used |= {i for i in range(len(X)) if X[i][r] != 0}
+                used |= set(col(X, r))
         return cnt, len(used)
-    total, nodes = 0, 1
-    m, k, n = M, K, N
+
+    def two_levels(X1, R1, X2, R2):
+        """(formed grandchildren, sub-blocks (i1, i2) read) of a K1X2 node"""
+        formed, need = 0, set()
+        for r1 in range(R1):
+            need2 = set()
+            for r2 in range(R2):
+                if trivial(X1, r1) and trivial(X2, r2):
+                    continue
+                formed += 1
+                need2 |= set(col(X2, r2))
+            need |= {(i1, i2) for i1 in col(X1, r1) for i2 in need2}
+        return formed, len(need)
+
     L = len(rule_infos)
-    for l, ri in enumerate(rule_infos):
-        R, m0, k0, n0 = ri["R"], ri["m0"], ri["k0"], ri["n0"]
-        mb, kb, nb = m // m0, k // k0, n // n0
-        (nsa, ua), (nsb, ub) = nontrivial(ri["U"], R), nontrivial(ri["V"], R)
-        total += nodes * ((ua + nsa) * mb * kb + (ub + nsb) * kb * nb) * esz  # K1
-        if l == L - 1 and fused_leaf_level:
-            total += nodes * m * n * esz  # fused W-combination: the output written once
+    dims = [(M, K, N)]
+    for ri in rule_infos:
+        m, k, n = dims[-1]
+        dims.append((m // ri["m0"], k // ri["k0"], n // ri["n0"]))
+    nodes = [1]
+    for ri in rule_infos:
+        nodes.append(nodes[-1] * ri["R"])
+    small = [ri["m0"] * ri["k0"] <= 4 and ri["k0"] * ri["n0"] <= 4 for ri in rule_infos]
+    pair = [False] * (L + 1)
+    if two_level:
+        for e in range(L - 2, -1, -2):
+            pair[e] = small[e] and small[e + 1] and rule_infos[e]["R"] * rule_infos[e + 1]["R"] <= 64
+    total = 0
+    l = 0
+    while l < L:  # K1
+        ri = rule_infos[l]
+        if pair[l]:
+            r2 = rule_infos[l + 1]
+            mb, kb, nb = dims[l + 2]
+            fa, na = two_levels(ri["U"], ri["R"], r2["U"], r2["R"])
+            fb_, nb_ = two_levels(ri["V"], ri["R"], r2["V"], r2["R"])
+            total += nodes[l] * ((na + fa) * mb * kb + (nb_ + fb_) * kb * nb) * esz
+            l += 2
         else:
-            total += nodes * (R * mb * nb + m * n) * esz  # K3: read R products, write the output
-        nodes *= R
-        m, k, n = mb, kb, nb
+            mb, kb, nb = dims[l + 1]
+            (nsa, ua), (nsb, ub) = one_level(ri["U"], ri["R"]), one_level(ri["V"], ri["R"])
+            total += nodes[l] * ((ua + nsa) * mb * kb + (ub + nsb) * kb * nb) * esz
+            l += 1
+    for l, ri in enumerate(rule_infos):  # K3 / fused epilogue
+        m, _, n = dims[l]
+        mb, _, nb = dims[l + 1]
+        if l == L - 1 and fused_leaf_level:
+            total += nodes[l] * m * n * esz  # fused W-combination: the output written once
+        else:
+            total += nodes[l] * (ri["R"] * mb * nb + m * n) * esz  # K3: read R products, write the output
     return total
 
 
@@ -464,7 +508,8 @@ def run_fmm(args):
         hbm = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
     except (OSError, KeyError, ValueError):
         pass
-    pbytes = pass_bytes([fb.Rule.builtin(r).info() for r in rules], M, K, N, esz, fused) if ws == 1 else None
+    pbytes = (pass_bytes([fb.Rule.builtin(r).info() for r in rules], M, K, N, esz, fused,
+                         os.environ.get("FMM_K1X2", "1") != "0") if ws == 1 else None)
     pipeline = None
     if pbytes is not None and args.scaling == "none":
         t_roof = leaf_flops_step / (peak * 1e12) + pbytes / (hbm * 1e9)

@@ -161,6 +161,17 @@ fmm_status fmm_plan_set_fusion(fmm_plan* plan, int mode);
  * environment variable FMM_OPF=1 turns it on at fmm_plan_create). */
 fmm_status fmm_plan_set_operand_fusion(fmm_plan* plan, int enable);
 
+/* S / T formation levels per pass (host-only; north star item 1, P:104-105 applied twice).
+ * levels = 2 (default): where two consecutive recursion levels d, d+1 split 2x2-or-smaller
+ * blocks and every child of a level-d node uses one rule (R1 * R2 <= 64), one K1X2 launch forms
+ * the level-(d+2) operands S_{r1 r2} = sum_i2 u2_{i2 r2} (sum_i1 u1_{i1 r1} A[i1][i2]) directly
+ * from the level-d operand, in registers, in the order of two one-level passes (bitwise
+ * identical); the level-(d+1) S_{r1} / T_{r1} are never written (less HBM traffic and
+ * workspace).  Levels pair from the bottom: (L-2, L-1), (L-4, L-3), ...  levels = 1: one K1 pass
+ * per level.  FMM_E_ARG for other values.  The environment variable FMM_K1X2=0 sets 1 at
+ * fmm_plan_create. */
+fmm_status fmm_plan_set_k1_levels(fmm_plan* plan, int levels);
+
 /* Host-only query: number of fused leaf-product launches (K2F) in the compiled schedule. */
 fmm_status fmm_plan_fused_launches(const fmm_plan* plan, int64_t* n);
 

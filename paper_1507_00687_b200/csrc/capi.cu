@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "fmm_internal.h"
+#include "builtin_tables.h"
 
 namespace fmm {
 int64_t brent_violations(const RuleData& d, int64_t* fi, int64_t* fj, int64_t* fk);
@@ -124,6 +125,7 @@ struct fmm_plan {
   bool persistent = false;  // fused leaves as the persistent stream-K kernel (K2P) where eligible
   bool operand_fusion = false;  // S_r / T_r with <= 2 +-1 terms formed inside the fused leaf kernel
   bool split_chains = true;     // fused units' product chains split over CTAs (turnstiles)
+  bool k1_two_level = true;     // S / T of two recursion levels formed in one pass (K1X2)
   ncclComm_t comm = nullptr;
   // compiled schedule
   std::vector<Step> steps;
@@ -195,8 +197,13 @@ struct Builder {
   explicit Builder(fmm_plan* pl) : p(pl) { align_elems = 256 / elem_size(pl->dtype); }
 
   int64_t ws_alloc(int64_t elems) {
+    static const int64_t skew = [] {  // experiments: extra bytes between workspace blocks
+      const char* e = getenv("FMM_WS_SKEW");
+      return e ? (int64_t)atoll(e) : (int64_t)0;
+    }();
     int64_t off = ws_elems;
     ws_elems += (elems + align_elems - 1) / align_elems * align_elems;
+    if (skew > 0) ws_elems += (skew / elem_size(p->dtype) + align_elems - 1) / align_elems * align_elems;
     ws_peak = std::max(ws_peak, ws_elems);
     return off;
   }
@@ -328,6 +335,107 @@ struct Builder {
       p->steps.push_back(st);
     }
     return kids;
+  }
+
+  // Built-in rule id of a rule (builtin_tables.h) if its U and V tables are exactly one of
+  // them, else kBuiltinNone.
+  static int builtin_id(const RuleData& r) {
+    if (r.m0 != 2 || r.k0 != 2 || r.n0 != 2 || r.log2den != 0) return kBuiltinNone;
+    for (int id = 0; id < 3; ++id) {
+      if (builtin_R(id) != r.R) continue;
+      bool eq = true;
+      for (int b = 0; b < 4 && eq; ++b)
+        for (int q = 0; q < r.R && eq; ++q)
+          eq = r.U[(size_t)b * r.R + q] == builtin_coef(id, 0, b, q) &&
+               r.V[(size_t)b * r.R + q] == builtin_coef(id, 1, b, q);
+      if (eq) return id;
+    }
+    return kBuiltinNone;
+  }
+
+  // K1X2 rule pair (1 + 3 * id_d + id_{d+1}) of levels (d, d+1) for `nodes` (level d), or 0:
+  // every node of level d and every child use one built-in rule per level.
+  int k1x2_pair(int d, const std::vector<Node>& nodes) {
+    if (!p->k1_two_level || d + 2 > p->L || nodes.empty()) return 0;
+    const int rule1 = p->node_rule[d][nodes[0].idx];
+    const int ra = builtin_id(p->rules[rule1]);
+    if (ra == kBuiltinNone) return 0;
+    const int R1 = p->rules[rule1].R;
+    const int rule2 = p->node_rule[d + 1][nodes[0].idx * R1];
+    const int rb = builtin_id(p->rules[rule2]);
+    if (rb == kBuiltinNone) return 0;
+    for (const Node& nd : nodes) {
+      if (p->node_rule[d][nd.idx] != rule1) return 0;
+      for (int r = 0; r < R1; ++r)
+        if (p->node_rule[d + 1][nd.idx * R1 + r] != rule2) return 0;
+    }
+    return 1 + 3 * ra + rb;
+  }
+
+  // Levels d and d+1 of S / T formation in one K1X2 launch.  Returns the children (level d+1:
+  // products M_{r1}, only c allocated -- their S / T are never formed) and the grandchildren
+  // (level d+2, operands formed or views, c allocated if alloc_c), both in BFS order.  The
+  // formed outputs are listed r1-major, r2 ascending: the kernel's compile-time order.
+  std::pair<std::vector<Node>, std::vector<Node>> emit_k1x2(int d, const std::vector<Node>& nodes,
+                                                            int pair, bool alloc_c) {
+    const int ra = (pair - 1) / 3, rb = (pair - 1) % 3;
+    const int64_t mb1 = p->lm[d + 1], kb1 = p->lk[d + 1], nb1 = p->ln[d + 1];
+    const int64_t mb = p->lm[d + 2], kb = p->lk[d + 2], nb = p->ln[d + 2];
+    const int R1 = builtin_R(ra), R2 = builtin_R(rb);
+    std::vector<K1x2Node> ks, kt;
+    std::vector<Node> kids, grand;
+    for (const Node& nd : nodes) {
+      K1x2Node s{}, t{};
+      s.in = nd.a; s.rows = mb; s.cols = kb; s.tv = 0;
+      t.in = nd.b; t.rows = kb; t.cols = nb; t.tv = 1;
+      for (int r1 = 0; r1 < R1; ++r1) {
+        Node ch;
+        ch.idx = nd.idx * R1 + r1;
+        ch.a = Op{}; ch.b = Op{};  // not formed
+        ch.c = ws_op(ws_alloc(mb1 * nb1), nb1);
+        kids.push_back(ch);
+        for (int r2 = 0; r2 < R2; ++r2) {
+          Node g;
+          g.idx = ch.idx * R2 + r2;
+          if (builtin_trivial(ra, 0, r1) && builtin_trivial(rb, 0, r2)) {  // a view of one block
+            int b1 = 0, b2 = 0;
+            while (builtin_coef(ra, 0, b1, r1) == 0) ++b1;
+            while (builtin_coef(rb, 0, b2, r2) == 0) ++b2;
+            g.a = sub(sub(nd.a, (b1 % 2) * mb1, (b1 / 2) * kb1), (b2 % 2) * mb, (b2 / 2) * kb);
+          } else {
+            g.a = ws_op(ws_alloc(mb * kb), kb);
+            s.out[s.nout++] = g.a;
+          }
+          if (builtin_trivial(ra, 1, r1) && builtin_trivial(rb, 1, r2)) {
+            int b1 = 0, b2 = 0;
+            while (builtin_coef(ra, 1, b1, r1) == 0) ++b1;
+            while (builtin_coef(rb, 1, b2, r2) == 0) ++b2;
+            g.b = sub(sub(nd.b, (b1 % 2) * kb1, (b1 / 2) * nb1), (b2 % 2) * kb, (b2 / 2) * nb);
+          } else {
+            g.b = ws_op(ws_alloc(kb * nb), nb);
+            t.out[t.nout++] = g.b;
+          }
+          if (alloc_c) g.c = ws_op(ws_alloc(mb * nb), nb);
+          grand.push_back(g);
+        }
+      }
+      if (s.nout) ks.push_back(s);
+      if (t.nout) kt.push_back(t);
+    }
+    std::vector<K1x2Node> all = ks;
+    all.insert(all.end(), kt.begin(), kt.end());
+    if (!all.empty()) {
+      Step st{};
+      st.kind = STEP_K1;
+      st.x2 = pair;
+      st.count = (int)all.size();
+      st.dev_off = push(all);
+      st.rows = ks.empty() ? kb : kt.empty() ? mb : std::max(mb, kb);
+      st.cols = ks.empty() ? nb : kt.empty() ? kb : std::max(kb, nb);
+      st.P = 4; st.Q = 1; st.R = R1;
+      p->steps.push_back(st);
+    }
+    return {kids, grand};
   }
 
   void emit_k2(const std::vector<Node>& leaves) {
@@ -539,9 +647,28 @@ struct Builder {
   // breadth-first over the subtree(s) rooted at `nodes` (level l), outputs into nodes' c.
   void breadth_first(int l, const std::vector<Node>& nodes) {
     std::vector<std::vector<Node>> lv{nodes};
-    for (int d = l; d < p->L - 1; ++d) lv.push_back(emit_k1(d, lv.back(), -1));
-    const bool fuse = fuse_leaves((int64_t)lv.back().size());
-    lv.push_back(emit_k1(p->L - 1, lv.back(), -1, !fuse, fuse && opf_on()));
+    int64_t npar = (int64_t)nodes.size();  // parents of the leaves (R uniform per level)
+    for (int d = l; d < p->L - 1; ++d) npar *= p->rules[p->node_rule[d][0]].R;
+    const bool fuse = fuse_leaves(npar);
+    const bool opf = fuse && opf_on();
+    // two levels per K1 pass (K1X2), paired from the bottom: (L-2, L-1), (L-4, L-3), ...
+    // (with operand fusion the last level stays a one-level pass)
+    const int ptop = opf ? p->L - 1 : p->L;
+    std::vector<bool> pair_at(p->L + 1, false);
+    for (int e = ptop - 2; e >= l; e -= 2) pair_at[e] = true;
+    for (int d = l; d < p->L;) {
+      const int pr = pair_at[d] ? k1x2_pair(d, lv.back()) : 0;
+      if (pr) {
+        auto kg = emit_k1x2(d, lv.back(), pr, !(d + 2 == p->L && fuse));
+        lv.push_back(kg.first);
+        lv.push_back(kg.second);
+        d += 2;
+      } else {
+        const bool last = d == p->L - 1;
+        lv.push_back(emit_k1(d, lv.back(), -1, !(last && fuse), last && opf));
+        d += 1;
+      }
+    }
     int top = p->L - 1;
     if (fuse) {
       emit_k2f(p->L - 1, lv[p->L - 1 - l], lv.back(), -1, nullptr);
@@ -785,7 +912,7 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
                                bool vec, cudaStream_t st) {
   size_t node_bytes = 0;
   switch (s.kind) {
-    case STEP_K1: node_bytes = sizeof(K1Node); break;
+    case STEP_K1: node_bytes = s.x2 ? sizeof(K1x2Node) : sizeof(K1Node); break;
     case STEP_K3: node_bytes = sizeof(K3Node); break;
     case STEP_ACC: node_bytes = sizeof(AccNode); break;
     case STEP_ZERO: node_bytes = sizeof(ZeroNode); break;
@@ -1012,6 +1139,7 @@ fmm_status fmm_plan_create(const fmm_rule* const* nodes, int n_nodes, int levels
   if (const char* pe = getenv("FMM_K2P")) p->persistent = atoi(pe) != 0;
   if (const char* oe = getenv("FMM_OPF")) p->operand_fusion = atoi(oe) != 0;
   if (const char* ce = getenv("FMM_SPLIT")) p->split_chains = atoi(ce) != 0;
+  if (const char* xe = getenv("FMM_K1X2")) p->k1_two_level = atoi(xe) != 0;
   if (const char* fe = getenv("FMM_FUSION")) {
     const int f = atoi(fe);
     if (f >= 0 && f <= 2) p->fusion = f;
@@ -1114,6 +1242,12 @@ fmm_status fmm_plan_set_fusion(fmm_plan* p, int mode) {
   if (!p || mode < 0 || mode > 3) { set_error("fmm_plan_set_fusion: bad args"); return FMM_E_ARG; }
   p->fusion = mode == 3 ? 1 : mode;
   p->persistent = mode == 3;
+  return compile_plan(p);
+}
+
+fmm_status fmm_plan_set_k1_levels(fmm_plan* p, int levels) {
+  if (!p || levels < 1 || levels > 2) { set_error("fmm_plan_set_k1_levels: levels must be 1 or 2"); return FMM_E_ARG; }
+  p->k1_two_level = levels == 2;
   return compile_plan(p);
 }
 

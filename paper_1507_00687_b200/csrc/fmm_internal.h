@@ -104,6 +104,26 @@ inline void k1_compile(K1Node& n, const RuleData& ru, const std::vector<int32_t>
   }
 }
 
+// ---- K1X2: two recursion levels of S (or T) formation in one HBM pass -------------------
+// A node of level d (rule 1: 2 x 2 blocks, table X1 = U or V, rank R1) whose children all use
+// rule 2 (2 x 2, X2, R2).  The grandchild operands
+//   S_{r1 r2} = sum_{i2} x2_{i2 r2} S_{r1}[i2],   S_{r1}[i2] = sum_{i1} x1_{i1 r1} A[i1][i2]
+// (P:104-105 applied at level d, then at level d+1 to the blocks of S_{r1}) are evaluated per
+// element in registers, in the order of the two one-level passes (so bitwise equal to them),
+// without writing the level-(d+1) operands S_{r1}.  Input block i1 = p1 + 2 q1 (column-major,
+// P:108), its sub-block i2 = p2 + 2 q2: rows (2 p1 + p2) rows + i, cols (2 q1 + q2) cols + j.
+// The rule pair is a kernel template (built-in rules, builtin_tables.h), so the output list --
+// every (r1, r2) except those whose columns are a single +1 at both levels (views), r1-major --
+// is known at compile time; the descriptor carries only the output pointers.
+constexpr int kMaxX2 = 64;  // max formed grandchildren of a node (R1 * R2)
+struct K1x2Node {
+  Op in;
+  int64_t rows, cols;  // grandchild block dims (outputs are workspace blocks with ld = cols)
+  int32_t tv;          // 0: S (U tables, A side), 1: T (V tables, B side)
+  int32_t nout;        // formed grandchildren (checked against the kernel's list)
+  Op out[kMaxX2];
+};
+
 // ---- K3: C_k = sum_r w_kr M_r into the node output (rows*M0 x cols*N0), k = ia*N0 + jb ----
 struct K3Node {
   Op out;
@@ -175,6 +195,8 @@ struct Step {
                      // turnstiles (one int per unit) at ws offset turn_off (bytes)
   int64_t turn_off = -1;
   int persist = 0;   // K2F: run as the persistent stream-K kernel with this many CTAs (0: grid)
+  int x2 = 0;        // K1: 0 one level (K1Node); else K1x2Node with rule pair (x2 - 1) / 3,
+                     // (x2 - 1) % 3 (builtin_tables.h ids)
 };
 
 // ---- kernel launchers (kernels_*.cu) -----------------------------------------------------------

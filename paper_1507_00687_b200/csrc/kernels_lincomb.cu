@@ -10,8 +10,10 @@
 // exactly the order of PAPER.md's sequential summation model (eqn:seq_summation_error).
 #include <algorithm>
 #include <cstdlib>
+#include <utility>
 
 #include "fmm_internal.h"
+#include "builtin_tables.h"
 
 namespace fmm {
 
@@ -161,6 +163,187 @@ __global__ void __launch_bounds__(kThreads) k1_lincomb(const K1Node* __restrict_
         st_vec<T, VEC>(optr[o] + i * old[o] + jv, acc);
       }
     }
+  }
+}
+
+// One term of a sequential linear combination s = u_0 x_0 (+ u_1 x_1 ...) in K1's order: code
+// cb (1 +1, 2 -1, 3 general dyadic coefficient *u); the first term initialises.
+template <typename T, int VEC>
+__device__ __forceinline__ void lc_term(Vec<T, VEC>& acc, bool& started, uint32_t cb,
+                                        const Vec<T, VEC>& x, const double* u) {
+  if (cb == 0u) return;
+  if (cb == 3u) {
+    const T ut = (T)*u;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e)
+      acc.v[e] = started ? add_rn<T>(acc.v[e], mul_rn<T>(ut, x.v[e])) : mul_rn<T>(ut, x.v[e]);
+  } else if (cb == 1u) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) acc.v[e] = started ? add_rn<T>(acc.v[e], x.v[e]) : x.v[e];
+  } else {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) acc.v[e] = started ? add_rn<T>(acc.v[e], -x.v[e]) : -x.v[e];
+  }
+  started = true;
+}
+
+constexpr int kThreadsX2 = 128;
+
+// Compile-time output structure of a K1X2 rule pair (RA at level d, RB at level d+1, table TV).
+template <int RA, int RB, int TV>
+struct X2Pair {
+  static constexpr int R1 = builtin_R(RA), R2 = builtin_R(RB);
+  static constexpr bool formed(int r1, int r2) {
+    return !(builtin_trivial(RA, TV, r1) && builtin_trivial(RB, TV, r2));
+  }
+  static constexpr bool need2(int r1, int b2) {  // S_{r1}[b2] used by a formed output
+    for (int r2 = 0; r2 < R2; ++r2)
+      if (formed(r1, r2) && builtin_coef(RB, TV, b2, r2) != 0) return true;
+    return false;
+  }
+  static constexpr bool need(int b1, int b2) {  // input sub-block (b1, b2) read
+    for (int r1 = 0; r1 < R1; ++r1)
+      if (builtin_coef(RA, TV, b1, r1) != 0 && need2(r1, b2)) return true;
+    return false;
+  }
+  static constexpr int nout() {
+    int n = 0;
+    for (int r1 = 0; r1 < R1; ++r1)
+      for (int r2 = 0; r2 < R2; ++r2) n += formed(r1, r2);
+    return n;
+  }
+  static constexpr uint32_t code(int id, int b, int r) {
+    return builtin_coef(id, TV, b, r) == 1 ? 1u : builtin_coef(id, TV, b, r) == -1 ? 2u : 0u;
+  }
+  static constexpr bool first(int id, int b, int r) {  // first nonzero term of column r
+    for (int q = 0; q < b; ++q)
+      if (builtin_coef(id, TV, q, r) != 0) return false;
+    return true;
+  }
+  static constexpr int oidx(int r1, int r2) {  // position in the r1-major list of formed outputs
+    int n = 0;
+    for (int a = 0; a < R1; ++a)
+      for (int c = 0; c < R2; ++c) {
+        if (a == r1 && c == r2) return n;
+        n += formed(a, c);
+      }
+    return n;
+  }
+};
+
+// Compile-time loop: f(std::integral_constant<int, 0>) ... f(integral_constant<int, N-1>), so
+// the K1X2 structure predicates below are constant expressions (if constexpr), not run-time
+// table lookups.
+template <typename F, int... I>
+__device__ __forceinline__ void static_for_impl(F&& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+template <int N, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+  static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+// One term s (+)= u x of a sequential sum with a compile-time code (1: +1, 2: -1).
+template <uint32_t CB, typename T, int VEC>
+__device__ __forceinline__ void lc_fixed(Vec<T, VEC>& acc, bool first, const Vec<T, VEC>& x) {
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    const T v = CB == 1u ? x.v[e] : -x.v[e];
+    acc.v[e] = first ? v : add_rn<T>(acc.v[e], v);
+  }
+}
+
+// One grandchild row position of a K1X2 node: load the needed input elements once, then per r1
+// form S_{r1}[i2] (level d) and every formed S_{r1 r2} (level d+1) from them, ascending
+// block order in both sums (the one-level K1's order).  All codes are constants, so the body is
+// only the loads, the adds and the stores.
+template <typename T, int VEC, int RA, int RB, int TV>
+__device__ __forceinline__ void k1x2_row(const T* __restrict__ in, int64_t ldi, int64_t rows,
+                                         int64_t cols, int64_t i, int64_t jv, T* const* optr) {
+  using X = X2Pair<RA, RB, TV>;
+  Vec<T, VEC> x[4][4];  // x[i2][i1]
+  static_for<4>([&](auto b1) {
+    static_for<4>([&](auto b2) {
+      if constexpr (X::need(b1, b2)) {
+        constexpr int p1 = b1 % 2, q1 = b1 / 2, p2 = b2 % 2, q2 = b2 / 2;
+        x[b2][b1] = ld_vec<T, VEC>(in + ((2 * p1 + p2) * rows + i) * ldi + (2 * q1 + q2) * cols + jv);
+      }
+    });
+  });
+  const int64_t off = i * cols + jv;
+  static_for<X::R1>([&](auto r1) {
+    Vec<T, VEC> y[4];
+    static_for<4>([&](auto b2) {
+      if constexpr (X::need2(r1, b2)) {
+        static_for<4>([&](auto b1) {
+          if constexpr (X::code(RA, b1, r1) != 0u)
+            lc_fixed<X::code(RA, b1, r1)>(y[b2], X::first(RA, b1, r1), x[b2][b1]);
+        });
+      }
+    });
+    static_for<X::R2>([&](auto r2) {
+      if constexpr (X::formed(r1, r2)) {
+        Vec<T, VEC> acc;
+        static_for<4>([&](auto b2) {
+          if constexpr (X::code(RB, b2, r2) != 0u)
+            lc_fixed<X::code(RB, b2, r2)>(acc, X::first(RB, b2, r2), y[b2]);
+        });
+        st_vec<T, VEC>(optr[X::oidx(r1, r2)] + off, acc);
+      }
+    });
+  });
+}
+
+// K1X2 launch: grid x = column chunks of kThreadsX2 vectors, y = row groups of RPB grandchild
+// rows, z = node (S nodes use the U tables, T nodes the V tables).
+template <typename T, int VEC, int RPB, int RA, int RB>
+__global__ void __launch_bounds__(kThreadsX2) k1x2_lincomb(const K1x2Node* __restrict__ nodes,
+                                                            Bases bases) {
+  __shared__ T* optr[kMaxX2];
+  const K1x2Node& nd = nodes[blockIdx.z];
+  const int64_t rows = nd.rows, cols = nd.cols;
+  if ((int64_t)blockIdx.y * RPB >= rows || (int64_t)blockIdx.x * kThreadsX2 * VEC >= cols) return;
+  if (threadIdx.x < nd.nout) {
+    int64_t ldo;
+    optr[threadIdx.x] = op_ptr<T>(bases, nd.out[threadIdx.x], ldo);
+  }
+  int64_t ldi;
+  const T* in = op_ptr<const T>(bases, nd.in, ldi);
+  const int tv = nd.tv;
+  __syncthreads();
+  const int64_t jv = ((int64_t)blockIdx.x * kThreadsX2 + threadIdx.x) * VEC;
+  if (jv >= cols) return;
+  const int64_t i0 = (int64_t)blockIdx.y * RPB;
+#pragma unroll 1
+  for (int ii = 0; ii < RPB; ++ii) {
+    const int64_t i = i0 + ii;
+    if (i >= rows) break;
+    if (tv) k1x2_row<T, VEC, RA, RB, 1>(in, ldi, rows, cols, i, jv, optr);
+    else k1x2_row<T, VEC, RA, RB, 0>(in, ldi, rows, cols, i, jv, optr);
+  }
+}
+
+template <typename T, int VEC, int RA, int RB>
+void k1x2_go(const Step& s, const K1x2Node* nd, const Bases& b, cudaStream_t st) {
+  constexpr int RPB = 4;
+  const int64_t cv = (s.cols + VEC - 1) / VEC;
+  dim3 grid((unsigned)((cv + kThreadsX2 - 1) / kThreadsX2), (unsigned)((s.rows + RPB - 1) / RPB),
+            (unsigned)s.count);
+  k1x2_lincomb<T, VEC, RPB, RA, RB><<<grid, kThreadsX2, 0, st>>>(nd, b);
+}
+
+template <typename T, int VEC>
+void k1x2_pick(const Step& s, const K1x2Node* nd, const Bases& b, cudaStream_t st) {
+  switch (s.x2 - 1) {
+    case 0: k1x2_go<T, VEC, 0, 0>(s, nd, b, st); break;
+    case 1: k1x2_go<T, VEC, 0, 1>(s, nd, b, st); break;
+    case 2: k1x2_go<T, VEC, 0, 2>(s, nd, b, st); break;
+    case 3: k1x2_go<T, VEC, 1, 0>(s, nd, b, st); break;
+    case 4: k1x2_go<T, VEC, 1, 1>(s, nd, b, st); break;
+    case 5: k1x2_go<T, VEC, 1, 2>(s, nd, b, st); break;
+    case 6: k1x2_go<T, VEC, 2, 0>(s, nd, b, st); break;
+    case 7: k1x2_go<T, VEC, 2, 1>(s, nd, b, st); break;
+    default: k1x2_go<T, VEC, 2, 2>(s, nd, b, st); break;
   }
 }
 
@@ -482,6 +665,11 @@ cudaError_t launch_k1(const Step& s, const void* dev_nodes, const double* dev_co
                       const Bases& b, bool vec, cudaStream_t st) {
   if (s.count == 0 || s.rows == 0 || s.cols == 0) return cudaSuccess;
   constexpr int V = 16 / sizeof(T);
+  if (s.x2) {
+    if (vec) k1x2_pick<T, V>(s, (const K1x2Node*)dev_nodes, b, st);
+    else k1x2_pick<T, 1>(s, (const K1x2Node*)dev_nodes, b, st);
+    return cudaGetLastError();
+  }
   const K1Node* nd = (const K1Node*)dev_nodes;
   if (vec && s.P * s.Q <= 4 && s.items > 0 && k1_tma_enabled()) {
     const size_t smem = (size_t)2 * TK_NBLK * TK_ROWS * TK_BYTES;

@@ -76,10 +76,19 @@ def test_plan_shape_errors_and_workspace():
     assert pp.launch_count() == p.launch_count() + 3  # pad A, pad B, crop C
     assert pp.workspace_bytes() == p.workspace_bytes() + 3 * 512 * 512 * 8
     ws = p.workspace_bytes()
-    # breadth-first: level 1: 4 S + 4 T + 7 M blocks of 256^2; level 2: 28 + 28 + 49 of 128^2
+    # breadth-first, two levels per K1 pass (default): level 1: 7 M blocks of 256^2 (its S / T
+    # are never formed); level 2: 40 S + 40 T (49 minus the 3 x 3 products whose U / V columns
+    # are trivial at both levels: views of A, B) + 49 M of 128^2
+    exp = 7 * 256 * 256 * 8 + (40 + 40 + 49) * 128 * 128 * 8
+    assert exp <= ws <= exp + (1 << 16)
+    assert p.launch_count() == 1 + 1 + 2  # one K1X2 (S and T of both levels), K2, K3 x2
+    # one level per pass: level 1: 4 S + 4 T + 7 M of 256^2; level 2: 28 + 28 + 49 of 128^2
+    p.set_k1_levels(1)
     exp = (4 + 4 + 7) * 256 * 256 * 8 + (28 + 28 + 49) * 128 * 128 * 8
-    assert exp <= ws <= exp + 1 << 16
+    assert exp <= p.workspace_bytes() <= exp + (1 << 16)
     assert p.launch_count() == 2 + 1 + 2  # K1 x2 levels (S and T in one launch), K2, K3 x2
+    with pytest.raises(fb.FmmError):
+        p.set_k1_levels(3)
 
 
 def test_partition_ownership():
