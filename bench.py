@@ -206,7 +206,8 @@ def cpu_baseline(A_host, B_host, plan_rules, M, K, N, C_gpu_host=None, target_s=
 
 
 # ------------------------------------------------------------------------------------------
-def pass_bytes(rule_infos, M, K, N, esz, fused_leaf_level, two_level=True):
+def pass_bytes(rule_infos, M, K, N, esz, fused_leaf_level, two_level=True, two_level_k3=True,
+               depth_first_top=False):
     """Algorithmic HBM bytes of the add passes of a uniform plan: per level, K1
     reads each node's A / B block once and writes the non-trivial S_r / T_r (a column with a
     single +1 is an alias); with two levels per pass (K1X2, levels paired from the bottom where
@@ -272,13 +273,27 @@ def pass_bytes(rule_infos, M, K, N, esz, fused_leaf_level, two_level=True):
             (nsa, ua), (nsb, ub) = one_level(ri["U"], ri["R"]), one_level(ri["V"], ri["R"])
             total += nodes[l] * ((ua + nsa) * mb * kb + (ub + nsb) * kb * nb) * esz
             l += 1
-    for l, ri in enumerate(rule_infos):  # K3 / fused epilogue
+    # K3 / fused epilogue; two levels per K3 pass (K3X2) paired from the bottom of the unfused
+    # levels (not the depth-first top level, whose W-combination is the per-r ACC pass)
+    top = L - 2 if fused_leaf_level else L - 1
+    if fused_leaf_level:
+        m, _, n = dims[L - 1]
+        total += nodes[L - 1] * m * n * esz  # fused W-combination: the output written once
+    l = top
+    first = 1 if depth_first_top else 0
+    while l >= 0:
+        ri = rule_infos[l]
         m, _, n = dims[l]
-        mb, _, nb = dims[l + 1]
-        if l == L - 1 and fused_leaf_level:
-            total += nodes[l] * m * n * esz  # fused W-combination: the output written once
+        if (two_level_k3 and l - 1 >= first and small[l - 1] and small[l]
+                and rule_infos[l - 1]["R"] * ri["R"] <= 64):
+            mg, _, ng = dims[l + 1]  # grandchildren of level l - 1
+            pm, _, pn = dims[l - 1]
+            total += nodes[l - 1] * (rule_infos[l - 1]["R"] * ri["R"] * mg * ng + pm * pn) * esz
+            l -= 2
         else:
+            mb, _, nb = dims[l + 1]
             total += nodes[l] * (ri["R"] * mb * nb + m * n) * esz  # K3: read R products, write the output
+            l -= 1
     return total
 
 
@@ -509,7 +524,8 @@ def run_fmm(args):
     except (OSError, KeyError, ValueError):
         pass
     pbytes = (pass_bytes([fb.Rule.builtin(r).info() for r in rules], M, K, N, esz, fused,
-                         os.environ.get("FMM_K1X2", "1") != "0") if ws == 1 else None)
+                         os.environ.get("FMM_K1X2", "1") != "0", os.environ.get("FMM_K3X2", "1") != "0",
+                         "ACC" in kinds) if ws == 1 else None)
     pipeline = None
     if pbytes is not None and args.scaling == "none":
         t_roof = leaf_flops_step / (peak * 1e12) + pbytes / (hbm * 1e9)

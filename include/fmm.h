@@ -163,7 +163,8 @@ fmm_status fmm_plan_set_operand_fusion(fmm_plan* plan, int enable);
 
 /* S / T formation levels per pass (host-only; north star item 1, P:104-105 applied twice).
  * levels = 2 (default): where two consecutive recursion levels d, d+1 split 2x2-or-smaller
- * blocks and every child of a level-d node uses one rule (R1 * R2 <= 64), one K1X2 launch forms
+ * blocks with built-in rules (Strassen, Strassen-Winograd, classical: tables equal to the built-in
+ * ones) and every child of a level-d node uses one rule, one K1X2 launch forms
  * the level-(d+2) operands S_{r1 r2} = sum_i2 u2_{i2 r2} (sum_i1 u1_{i1 r1} A[i1][i2]) directly
  * from the level-d operand, in registers, in the order of two one-level passes (bitwise
  * identical); the level-(d+1) S_{r1} / T_{r1} are never written (less HBM traffic and
@@ -171,6 +172,16 @@ fmm_status fmm_plan_set_operand_fusion(fmm_plan* plan, int enable);
  * per level.  FMM_E_ARG for other values.  The environment variable FMM_K1X2=0 sets 1 at
  * fmm_plan_create. */
 fmm_status fmm_plan_set_k1_levels(fmm_plan* plan, int levels);
+
+/* W-combination levels per pass (host-only; north star item 3, P:119 applied twice).
+ * levels = 2 (default): where a level d and its children use built-in 2x2x2 rules (Strassen,
+ * Strassen-Winograd, classical: U, V and W tables equal to the built-in ones), one K3X2 launch
+ * computes C[k1][k2] = sum_r1 w1_{k1 r1} (sum_r2 w2_{k2 r2} M_{r1 r2}) from the level-(d+2)
+ * products into the level-d outputs, in registers, in K3's order (bitwise identical to two
+ * K3 passes); the level-(d+1) outputs are never written.  Levels pair from the bottom of the
+ * unfused K3 levels.  levels = 1: one K3 pass per level.  FMM_E_ARG for other values.  The
+ * environment variable FMM_K3X2=0 sets 1 at fmm_plan_create. */
+fmm_status fmm_plan_set_k3_levels(fmm_plan* plan, int levels);
 
 /* Host-only query: number of fused leaf-product launches (K2F) in the compiled schedule. */
 fmm_status fmm_plan_fused_launches(const fmm_plan* plan, int64_t* n);

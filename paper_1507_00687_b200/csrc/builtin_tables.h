@@ -1,4 +1,4 @@
-// Compile-time U / V tables of the three built-in 2x2x2 rules, for the K1X2 kernels that are
+// Compile-time U / V / W tables of the three built-in 2x2x2 rules, for the K1X2 / K3X2 kernels that are
 // specialised per (level-d rule, level-(d+1) rule) pair (kernels_lincomb.cu).  Block index
 // b = ia + 2 ja (column-major), product r in the paper's numbering: Strassen App. A
 // (P:1971-1991), Strassen-Winograd (reading A2), classical r = 4 ia + 2 ja
@@ -34,6 +34,21 @@ __host__ __device__ constexpr int builtin_coef(int id, int tv, int b, int r) {
   }
   if (id == kBuiltinStrassen) return tv == 0 ? su[b][r] : sv[b][r];
   return tv == 0 ? wu[b][r] : wv[b][r];
+}
+
+// coefficient of product r in output block k = 2 ia + jb (row-major) of W
+__host__ __device__ constexpr int builtin_w(int id, int k, int r) {
+  // Strassen: C11 = M1+M4-M5+M7, C12 = M3+M5, C21 = M2+M4, C22 = M1-M2+M3+M6
+  const int8_t sw[4][7] = {{1, 0, 0, 1, -1, 0, 1}, {0, 0, 1, 0, 1, 0, 0}, {0, 1, 0, 1, 0, 0, 0},
+                           {1, -1, 1, 0, 0, 1, 0}};
+  // Strassen-Winograd: C11 = M1+M2, C12 = M1+M3+M5+M6, C21 = M1-M4+M6+M7, C22 = M1+M5+M6+M7
+  const int8_t ww[4][7] = {{1, 1, 0, 0, 0, 0, 0}, {1, 0, 1, 0, 1, 1, 0}, {1, 0, 0, -1, 0, 1, 1},
+                           {1, 0, 0, 0, 1, 1, 1}};
+  if (id == kBuiltinClassical) {
+    const int ia = r / 4, jb = r % 2;
+    return k == 2 * ia + jb ? 1 : 0;
+  }
+  return id == kBuiltinStrassen ? sw[k][r] : ww[k][r];
 }
 
 // column r is a single +1 (the product's operand is a view of one block)

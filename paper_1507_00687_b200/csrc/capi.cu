@@ -126,6 +126,7 @@ struct fmm_plan {
   bool operand_fusion = false;  // S_r / T_r with <= 2 +-1 terms formed inside the fused leaf kernel
   bool split_chains = true;     // fused units' product chains split over CTAs (turnstiles)
   bool k1_two_level = true;     // S / T of two recursion levels formed in one pass (K1X2)
+  bool k3_two_level = true;     // W-combination of two recursion levels in one pass (K3X2)
   ncclComm_t comm = nullptr;
   // compiled schedule
   std::vector<Step> steps;
@@ -337,7 +338,7 @@ struct Builder {
     return kids;
   }
 
-  // Built-in rule id of a rule (builtin_tables.h) if its U and V tables are exactly one of
+  // Built-in rule id of a rule (builtin_tables.h) if its U, V and W tables are exactly one of
   // them, else kBuiltinNone.
   static int builtin_id(const RuleData& r) {
     if (r.m0 != 2 || r.k0 != 2 || r.n0 != 2 || r.log2den != 0) return kBuiltinNone;
@@ -347,7 +348,8 @@ struct Builder {
       for (int b = 0; b < 4 && eq; ++b)
         for (int q = 0; q < r.R && eq; ++q)
           eq = r.U[(size_t)b * r.R + q] == builtin_coef(id, 0, b, q) &&
-               r.V[(size_t)b * r.R + q] == builtin_coef(id, 1, b, q);
+               r.V[(size_t)b * r.R + q] == builtin_coef(id, 1, b, q) &&
+               r.W[(size_t)b * r.R + q] == builtin_w(id, b, q);
       if (eq) return id;
     }
     return kBuiltinNone;
@@ -356,7 +358,7 @@ struct Builder {
   // K1X2 rule pair (1 + 3 * id_d + id_{d+1}) of levels (d, d+1) for `nodes` (level d), or 0:
   // every node of level d and every child use one built-in rule per level.
   int k1x2_pair(int d, const std::vector<Node>& nodes) {
-    if (!p->k1_two_level || d + 2 > p->L || nodes.empty()) return 0;
+    if (d + 2 > p->L || nodes.empty()) return 0;
     const int rule1 = p->node_rule[d][nodes[0].idx];
     const int ra = builtin_id(p->rules[rule1]);
     if (ra == kBuiltinNone) return 0;
@@ -644,6 +646,44 @@ struct Builder {
     p->steps.push_back(st);
   }
 
+  // K3X2: levels d and d+1 of the W-combination in one pass, from the grandchildren's products
+  // (level d+2 c blocks) straight into the level-d nodes' outputs.
+  void emit_k3x2(int d, const std::vector<Node>& nodes, const std::vector<Node>& grand, int pair) {
+    const int ra = (pair - 1) / 3, rb = (pair - 1) % 3;
+    const int n = builtin_R(ra) * builtin_R(rb);
+    std::vector<K3x2Node> k3;
+    size_t gi = 0;
+    for (const Node& nd : nodes) {
+      K3x2Node kn{};
+      kn.out = nd.c;
+      kn.rows = p->lm[d + 2]; kn.cols = p->ln[d + 2];
+      for (int q = 0; q < n; ++q) kn.in[q] = grand[gi++].c;
+      k3.push_back(kn);
+    }
+    Step st{};
+    st.kind = STEP_K3;
+    st.x2 = pair;
+    st.count = (int)k3.size();
+    st.dev_off = push(k3);
+    st.rows = p->lm[d + 2]; st.cols = p->ln[d + 2]; st.P = 2; st.Q = 2; st.R = builtin_R(ra);
+    p->steps.push_back(st);
+  }
+
+  // W-combination levels top .. l (bottom-up); two levels per pass (K3X2) paired from the
+  // bottom where the rules allow.  lv[q] = the nodes of level l + q.
+  void emit_k3_levels(int l, int top, const std::vector<std::vector<Node>>& lv) {
+    for (int d = top; d >= l;) {
+      const int pr = p->k3_two_level && d - 1 >= l ? k1x2_pair(d - 1, lv[d - 1 - l]) : 0;
+      if (pr) {
+        emit_k3x2(d - 1, lv[d - 1 - l], lv[d + 1 - l], pr);
+        d -= 2;
+      } else {
+        emit_k3(d, lv[d - l], lv[d - l + 1]);
+        d -= 1;
+      }
+    }
+  }
+
   // breadth-first over the subtree(s) rooted at `nodes` (level l), outputs into nodes' c.
   void breadth_first(int l, const std::vector<Node>& nodes) {
     std::vector<std::vector<Node>> lv{nodes};
@@ -657,7 +697,7 @@ struct Builder {
     std::vector<bool> pair_at(p->L + 1, false);
     for (int e = ptop - 2; e >= l; e -= 2) pair_at[e] = true;
     for (int d = l; d < p->L;) {
-      const int pr = pair_at[d] ? k1x2_pair(d, lv.back()) : 0;
+      const int pr = pair_at[d] && p->k1_two_level ? k1x2_pair(d, lv.back()) : 0;
       if (pr) {
         auto kg = emit_k1x2(d, lv.back(), pr, !(d + 2 == p->L && fuse));
         lv.push_back(kg.first);
@@ -676,7 +716,7 @@ struct Builder {
     } else {
       emit_k2(lv.back());
     }
-    for (int d = top; d >= l; --d) emit_k3(d, lv[d - l], lv[d - l + 1]);
+    emit_k3_levels(l, top, lv);
   }
 
   void build() {
@@ -913,7 +953,7 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
   size_t node_bytes = 0;
   switch (s.kind) {
     case STEP_K1: node_bytes = s.x2 ? sizeof(K1x2Node) : sizeof(K1Node); break;
-    case STEP_K3: node_bytes = sizeof(K3Node); break;
+    case STEP_K3: node_bytes = s.x2 ? sizeof(K3x2Node) : sizeof(K3Node); break;
     case STEP_ACC: node_bytes = sizeof(AccNode); break;
     case STEP_ZERO: node_bytes = sizeof(ZeroNode); break;
     case STEP_K2: node_bytes = sizeof(LeafNode); break;
@@ -1140,6 +1180,7 @@ fmm_status fmm_plan_create(const fmm_rule* const* nodes, int n_nodes, int levels
   if (const char* oe = getenv("FMM_OPF")) p->operand_fusion = atoi(oe) != 0;
   if (const char* ce = getenv("FMM_SPLIT")) p->split_chains = atoi(ce) != 0;
   if (const char* xe = getenv("FMM_K1X2")) p->k1_two_level = atoi(xe) != 0;
+  if (const char* xe = getenv("FMM_K3X2")) p->k3_two_level = atoi(xe) != 0;
   if (const char* fe = getenv("FMM_FUSION")) {
     const int f = atoi(fe);
     if (f >= 0 && f <= 2) p->fusion = f;
@@ -1248,6 +1289,12 @@ fmm_status fmm_plan_set_fusion(fmm_plan* p, int mode) {
 fmm_status fmm_plan_set_k1_levels(fmm_plan* p, int levels) {
   if (!p || levels < 1 || levels > 2) { set_error("fmm_plan_set_k1_levels: levels must be 1 or 2"); return FMM_E_ARG; }
   p->k1_two_level = levels == 2;
+  return compile_plan(p);
+}
+
+fmm_status fmm_plan_set_k3_levels(fmm_plan* p, int levels) {
+  if (!p || levels < 1 || levels > 2) { set_error("fmm_plan_set_k3_levels: levels must be 1 or 2"); return FMM_E_ARG; }
+  p->k3_two_level = levels == 2;
   return compile_plan(p);
 }
 

@@ -124,6 +124,19 @@ struct K1x2Node {
   Op out[kMaxX2];
 };
 
+// ---- K3X2: two levels of the W-combination in one pass --------------------------------------
+// For a node of level d (built-in rule 1, R1) whose children all use built-in rule 2 (R2):
+//   C[k1][k2] = sum_{r1} w1_{k1 r1} C_{r1}[k2],   C_{r1}[k2] = sum_{r2} w2_{k2 r2} M_{r1 r2}
+// (P:119 at levels d+1 and d), per element in registers in K3's order (ascending r, first term
+// initialises), so bitwise equal to two K3 passes; the children's outputs C_{r1} are never
+// written.  Output block k1 = 2 ia1 + jb1 (row-major), its sub-block k2 = 2 ia2 + jb2:
+// rows (2 ia1 + ia2) rows + i, cols (2 jb1 + jb2) cols + j of the node output.
+struct K3x2Node {
+  Op out;
+  int64_t rows, cols;  // grandchild block dims (inputs are workspace blocks with ld = cols)
+  Op in[kMaxX2];       // M_{r1 r2}, index r1 * R2 + r2
+};
+
 // ---- K3: C_k = sum_r w_kr M_r into the node output (rows*M0 x cols*N0), k = ia*N0 + jb ----
 struct K3Node {
   Op out;
@@ -195,8 +208,8 @@ struct Step {
                      // turnstiles (one int per unit) at ws offset turn_off (bytes)
   int64_t turn_off = -1;
   int persist = 0;   // K2F: run as the persistent stream-K kernel with this many CTAs (0: grid)
-  int x2 = 0;        // K1: 0 one level (K1Node); else K1x2Node with rule pair (x2 - 1) / 3,
-                     // (x2 - 1) % 3 (builtin_tables.h ids)
+  int x2 = 0;        // K1 / K3: 0 one level (K1Node / K3Node); else K1x2Node / K3x2Node with
+                     // rule pair (x2 - 1) / 3, (x2 - 1) % 3 (builtin_tables.h ids)
 };
 
 // ---- kernel launchers (kernels_*.cu) -----------------------------------------------------------

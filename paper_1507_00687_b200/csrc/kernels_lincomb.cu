@@ -323,13 +323,35 @@ __global__ void __launch_bounds__(kThreadsX2) k1x2_lincomb(const K1x2Node* __res
   }
 }
 
-template <typename T, int VEC, int RA, int RB>
-void k1x2_go(const Step& s, const K1x2Node* nd, const Bases& b, cudaStream_t st) {
-  constexpr int RPB = 4;
+// rows per CTA of the two-level passes (tools/bench_k1x2.py sweep: 1 fastest, 0.654 vs 0.688 ms
+// with 4 at C2, 25.8 vs 26.7 ms at C5)
+int k1x2_rpb() {
+  static int v = [] {
+    const char* e = getenv("FMM_K1X2_RPB");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+int k3x2_rpb() {
+  static int v = [] {
+    const char* e = getenv("FMM_K3X2_RPB");
+    return e ? atoi(e) : 4;  // K3X2: 4 rows per CTA (C2 0.223 vs 0.248 ms with 1, C4 0.090 vs 0.103)
+  }();
+  return v;
+}
+
+template <typename T, int VEC, int RA, int RB, int RPB>
+void k1x2_go_rpb(const Step& s, const K1x2Node* nd, const Bases& b, cudaStream_t st) {
   const int64_t cv = (s.cols + VEC - 1) / VEC;
   dim3 grid((unsigned)((cv + kThreadsX2 - 1) / kThreadsX2), (unsigned)((s.rows + RPB - 1) / RPB),
             (unsigned)s.count);
   k1x2_lincomb<T, VEC, RPB, RA, RB><<<grid, kThreadsX2, 0, st>>>(nd, b);
+}
+
+template <typename T, int VEC, int RA, int RB>
+void k1x2_go(const Step& s, const K1x2Node* nd, const Bases& b, cudaStream_t st) {
+  if (k1x2_rpb() == 4) k1x2_go_rpb<T, VEC, RA, RB, 4>(s, nd, b, st);
+  else k1x2_go_rpb<T, VEC, RA, RB, 1>(s, nd, b, st);
 }
 
 template <typename T, int VEC>
@@ -344,6 +366,119 @@ void k1x2_pick(const Step& s, const K1x2Node* nd, const Bases& b, cudaStream_t s
     case 6: k1x2_go<T, VEC, 2, 0>(s, nd, b, st); break;
     case 7: k1x2_go<T, VEC, 2, 1>(s, nd, b, st); break;
     default: k1x2_go<T, VEC, 2, 2>(s, nd, b, st); break;
+  }
+}
+
+// Compile-time structure of a K3X2 rule pair (RA at level d, RB at level d+1).
+template <int RA, int RB>
+struct W2Pair {
+  static constexpr int R1 = builtin_R(RA), R2 = builtin_R(RB);
+  static constexpr uint32_t code(int id, int k, int r) {
+    return builtin_w(id, k, r) == 1 ? 1u : builtin_w(id, k, r) == -1 ? 2u : 0u;
+  }
+  static constexpr bool first(int id, int k, int r) {  // first nonzero term of row k
+    for (int q = 0; q < r; ++q)
+      if (builtin_w(id, k, q) != 0) return false;
+    return true;
+  }
+  static constexpr bool used(int id, int r) {
+    for (int k = 0; k < 4; ++k)
+      if (builtin_w(id, k, r) != 0) return true;
+    return false;
+  }
+};
+
+// One grandchild row position of a K3X2 node: per r1 (ascending) form C_{r1}[k2] from the
+// M_{r1 r2} (level d+1, ascending r2) and accumulate w1_{k1 r1} C_{r1}[k2] into the 16 outputs
+// (level d); then store them.
+template <typename T, int VEC, int RA, int RB>
+__device__ __forceinline__ void k3x2_row(const T* const* iptr, T* __restrict__ out, int64_t ldo,
+                                         int64_t rows, int64_t cols, int64_t i, int64_t jv) {
+  using X = W2Pair<RA, RB>;
+  const int64_t off = i * cols + jv;
+  Vec<T, VEC> acc[4][4];  // [k1][k2]
+  static_for<X::R1>([&](auto r1) {
+    if constexpr (X::used(RA, r1)) {
+      Vec<T, VEC> y[4];
+      static_for<X::R2>([&](auto r2) {
+        if constexpr (X::used(RB, r2)) {
+          const Vec<T, VEC> m = ld_vec<T, VEC>(iptr[r1 * X::R2 + r2] + off);
+          static_for<4>([&](auto k2) {
+            if constexpr (X::code(RB, k2, r2) != 0u)
+              lc_fixed<X::code(RB, k2, r2)>(y[k2], X::first(RB, k2, r2), m);
+          });
+        }
+      });
+      static_for<4>([&](auto k1) {
+        if constexpr (X::code(RA, k1, r1) != 0u) {
+          static_for<4>([&](auto k2) {
+            lc_fixed<X::code(RA, k1, r1)>(acc[k1][k2], X::first(RA, k1, r1), y[k2]);
+          });
+        }
+      });
+    }
+  });
+  static_for<4>([&](auto k1) {
+    static_for<4>([&](auto k2) {
+      constexpr int ia = 2 * (k1 / 2) + k2 / 2, jb = 2 * (k1 % 2) + k2 % 2;
+      st_vec<T, VEC>(out + (ia * rows + i) * ldo + jb * cols + jv, acc[k1][k2]);
+    });
+  });
+}
+
+// K3X2 launch: grid x = column chunks of kThreadsX2 vectors, y = row groups of RPB, z = node.
+template <typename T, int VEC, int RPB, int RA, int RB>
+__global__ void __launch_bounds__(kThreadsX2) k3x2_combine(const K3x2Node* __restrict__ nodes,
+                                                            Bases bases) {
+  constexpr int NIN = builtin_R(RA) * builtin_R(RB);
+  __shared__ const T* iptr[NIN];
+  const K3x2Node& nd = nodes[blockIdx.z];
+  const int64_t rows = nd.rows, cols = nd.cols;
+  if ((int64_t)blockIdx.y * RPB >= rows || (int64_t)blockIdx.x * kThreadsX2 * VEC >= cols) return;
+  if (threadIdx.x < NIN) {
+    int64_t l;
+    iptr[threadIdx.x] = op_ptr<const T>(bases, nd.in[threadIdx.x], l);
+  }
+  int64_t ldo;
+  T* out = op_ptr<T>(bases, nd.out, ldo);
+  __syncthreads();
+  const int64_t jv = ((int64_t)blockIdx.x * kThreadsX2 + threadIdx.x) * VEC;
+  if (jv >= cols) return;
+  const int64_t i0 = (int64_t)blockIdx.y * RPB;
+#pragma unroll 1
+  for (int ii = 0; ii < RPB; ++ii) {
+    const int64_t i = i0 + ii;
+    if (i >= rows) break;
+    k3x2_row<T, VEC, RA, RB>(iptr, out, ldo, rows, cols, i, jv);
+  }
+}
+
+template <typename T, int VEC, int RA, int RB, int RPB>
+void k3x2_go_rpb(const Step& s, const K3x2Node* nd, const Bases& b, cudaStream_t st) {
+  const int64_t cv = (s.cols + VEC - 1) / VEC;
+  dim3 grid((unsigned)((cv + kThreadsX2 - 1) / kThreadsX2), (unsigned)((s.rows + RPB - 1) / RPB),
+            (unsigned)s.count);
+  k3x2_combine<T, VEC, RPB, RA, RB><<<grid, kThreadsX2, 0, st>>>(nd, b);
+}
+
+template <typename T, int VEC, int RA, int RB>
+void k3x2_go(const Step& s, const K3x2Node* nd, const Bases& b, cudaStream_t st) {
+  if (k3x2_rpb() == 4) k3x2_go_rpb<T, VEC, RA, RB, 4>(s, nd, b, st);
+  else k3x2_go_rpb<T, VEC, RA, RB, 1>(s, nd, b, st);
+}
+
+template <typename T, int VEC>
+void k3x2_pick(const Step& s, const K3x2Node* nd, const Bases& b, cudaStream_t st) {
+  switch (s.x2 - 1) {
+    case 0: k3x2_go<T, VEC, 0, 0>(s, nd, b, st); break;
+    case 1: k3x2_go<T, VEC, 0, 1>(s, nd, b, st); break;
+    case 2: k3x2_go<T, VEC, 0, 2>(s, nd, b, st); break;
+    case 3: k3x2_go<T, VEC, 1, 0>(s, nd, b, st); break;
+    case 4: k3x2_go<T, VEC, 1, 1>(s, nd, b, st); break;
+    case 5: k3x2_go<T, VEC, 1, 2>(s, nd, b, st); break;
+    case 6: k3x2_go<T, VEC, 2, 0>(s, nd, b, st); break;
+    case 7: k3x2_go<T, VEC, 2, 1>(s, nd, b, st); break;
+    default: k3x2_go<T, VEC, 2, 2>(s, nd, b, st); break;
   }
 }
 
@@ -694,6 +829,11 @@ cudaError_t launch_k3(const Step& s, const void* dev_nodes, const double* dev_co
                       const Bases& b, bool vec, cudaStream_t st) {
   if (s.count == 0 || s.rows == 0 || s.cols == 0) return cudaSuccess;
   constexpr int V = 16 / sizeof(T);
+  if (s.x2) {
+    if (vec) k3x2_pick<T, V>(s, (const K3x2Node*)dev_nodes, b, st);
+    else k3x2_pick<T, 1>(s, (const K3x2Node*)dev_nodes, b, st);
+    return cudaGetLastError();
+  }
   const K3Node* nd = (const K3Node*)dev_nodes;
   if (s.R <= 8) {
     if (vec)

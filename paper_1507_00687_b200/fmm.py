@@ -48,6 +48,7 @@ SIGNATURES = {
     "fmm_rule_transform": (_I, [_P, _I, C.POINTER(_P)]),
     "fmm_plan_set_operand_fusion": (_I, [_P, _I]),
     "fmm_plan_set_k1_levels": (_I, [_P, _I]),
+    "fmm_plan_set_k3_levels": (_I, [_P, _I]),
     "fmm_scale_apply": (_I, [_I, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _I64, _P, _I64, _P]),
     "fmm_rule_quantities": (_I, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double), _P, _P]),
     "fmm_plan_stability": (_I, [_P, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]),
@@ -309,6 +310,11 @@ class Plan:
     def set_k1_levels(self, levels: int = 2):
         """S / T formation: 2 = two recursion levels per K1 pass (K1X2, default), 1 = one."""
         _call("fmm_plan_set_k1_levels", self._h, int(levels))
+        self._ws = None
+
+    def set_k3_levels(self, levels: int = 2):
+        """W-combination: 2 = two recursion levels per K3 pass (K3X2, default), 1 = one."""
+        _call("fmm_plan_set_k3_levels", self._h, int(levels))
         self._ws = None
 
     def fused_launches(self) -> int:

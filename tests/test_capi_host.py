@@ -81,7 +81,11 @@ def test_plan_shape_errors_and_workspace():
     # are trivial at both levels: views of A, B) + 49 M of 128^2
     exp = 7 * 256 * 256 * 8 + (40 + 40 + 49) * 128 * 128 * 8
     assert exp <= ws <= exp + (1 << 16)
-    assert p.launch_count() == 1 + 1 + 2  # one K1X2 (S and T of both levels), K2, K3 x2
+    assert p.launch_count() == 1 + 1 + 1  # one K1X2 (S and T of both levels), K2, one K3X2
+    p.set_k3_levels(1)
+    assert p.launch_count() == 1 + 1 + 2  # K3 one level per pass
+    with pytest.raises(fb.FmmError):
+        p.set_k3_levels(0)
     # one level per pass: level 1: 4 S + 4 T + 7 M of 256^2; level 2: 28 + 28 + 49 of 128^2
     p.set_k1_levels(1)
     exp = (4 + 4 + 7) * 256 * 256 * 8 + (28 + 28 + 49) * 128 * 128 * 8

@@ -1,10 +1,12 @@
-"""GPU: two recursion levels of S / T formation in one pass (K1X2, fmm_plan_set_k1_levels).
+"""GPU: two recursion levels per pass -- S / T formation (K1X2, fmm_plan_set_k1_levels) and the
+W-combination (K3X2, fmm_plan_set_k3_levels).
 
-K1X2 evaluates S_{r1 r2} = sum_i2 u2_{i2 r2} (sum_i1 u1_{i1 r1} A[i1][i2]) in registers in the
-order of two one-level passes (Eq. eqn:recursive_alg P:116-125 applied at two consecutive
-levels; sequential summation P:241-246, reading A3), so plans with one and two levels
-per pass must agree BITWISE, and with unit leaf inner dimension (every leaf product one
-multiplication) both must equal the oracle bitwise."""
+K1X2 evaluates S_{r1 r2} = sum_i2 u2_{i2 r2} (sum_i1 u1_{i1 r1} A[i1][i2]) and K3X2
+C[k1][k2] = sum_r1 w1_{k1 r1} (sum_r2 w2_{k2 r2} M_{r1 r2}) in registers in the order of two
+one-level passes (Eq. eqn:recursive_alg P:116-125 applied at two consecutive levels; sequential
+summation P:241-246, reading A3), so plans with one and two levels per pass must agree
+BITWISE, and with unit leaf inner dimension (every leaf product one multiplication) both must
+equal the oracle bitwise."""
 import numpy as np
 import pytest
 import torch
@@ -41,12 +43,13 @@ def dev(x):
     return torch.from_numpy(np.ascontiguousarray(x)).cuda()
 
 
-def run(fb, names, A, B, levels, dtype="f64", fusion="auto", schedule="auto", leaf=None):
+def run(fb, names, A, B, levels, dtype="f64", fusion="auto", schedule="auto", leaf=None, k3=None):
     M, K = A.shape
     N = B.shape[1]
     kw = {} if leaf is None else {"leaf": leaf}
     p = fb.Plan([fb.Rule.builtin(n) for n in names], M, K, N, dtype=dtype, **kw)
     p.set_k1_levels(levels)
+    p.set_k3_levels(levels if k3 is None else k3)
     p.set_fusion(fusion)
     p.set_schedule(schedule)
     C = p.execute(dev(A), dev(B))
@@ -84,6 +87,19 @@ def test_two_level_equals_one_level_bitwise(fb, pname, schedule):
     assert oracle.parity_metric(C2, Co, np.abs(A).max(), np.abs(B).max(), K) <= TOL64
 
 
+@pytest.mark.parametrize("pname", ["strassen_L4", "C3_mix", "mix_pairs"])
+@pytest.mark.parametrize("fusion", ["off", "auto"])
+def test_k1_k3_levels_independent_bitwise(fb, pname, fusion):
+    # every combination of one / two levels per K1 and K3 pass gives the same bits
+    names = PLANS[pname]
+    L = len(names)
+    M, K, N = 2 ** L * 21, 2 ** L * 12, 2 ** L * 18
+    A, B = fi.random_pair(M, K, N, seed=3 * L)
+    outs = [run(fb, names, A, B, k1, fusion=fusion, k3=k3)[0] for k1 in (1, 2) for k3 in (1, 2)]
+    for C in outs[1:]:
+        assert np.array_equal(outs[0], C)
+
+
 @pytest.mark.parametrize("dims", [(509, 383, 257), (250, 130, 66), (64, 64, 63)])
 def test_padded_and_unvectorised(fb, dims):
     # zero padding of non-divisible dims, and odd K / N (scalar path)
@@ -117,6 +133,7 @@ def test_partition_partials(fb):
             for levels in (1, 2):
                 p = fb.Plan([fb.Rule.builtin(n) for n in names], 512, 256, 384)
                 p.set_k1_levels(levels)
+                p.set_k3_levels(levels)
                 p.set_partition(rank, nranks)
                 outs.append(p.execute(dev(A), dev(B)).cpu().numpy())
             assert np.array_equal(outs[0], outs[1])
@@ -135,6 +152,7 @@ def test_ineligible_rules_fall_back(fb):
     for levels in (1, 2):
         p = fb.Plan([w, b], M, K, N)
         p.set_k1_levels(levels)
+        p.set_k3_levels(levels)
         counts.append(p.launch_count())
         outs.append(p.execute(dev(A), dev(B)).cpu().numpy())
     assert counts[0] == counts[1]

@@ -1,9 +1,9 @@
-"""K1 microbenchmark (not the bench): the S / T formation passes of a plan timed alone (CUDA
-events the library records per launch kind), with one or two recursion levels per pass, reported
-as algorithmic GB/s (bench.pass_bytes' K1 part: needed input blocks read once, formed outputs
-written once) against the measured copy bandwidth.
+"""K1 / K3 microbenchmark (not the bench): the S / T formation and W-combination passes of a plan
+timed alone (CUDA events the library records per launch kind), with one or two recursion levels
+per pass (K1 reported as algorithmic GB/s: bench.pass_bytes' K1 part, needed input blocks read
+once, formed outputs written once, against the measured copy bandwidth; K3 as time).
 
-    python tools/bench_k1x2.py [--configs C2,C4,C5] [--reps 5]      (FMM_K1X2_VARIANT selects the kernel)
+    python tools/bench_k1x2.py [--configs C2,C4,C5] [--reps 5]   (FMM_K1X2_RPB / FMM_K3X2_RPB: rows per CTA)
 """
 import argparse
 import json
@@ -21,7 +21,7 @@ import paper_1507_00687_b200 as fb  # noqa: E402
 
 
 def k1_bytes(infos, M, K, N, esz, two):
-    tot = bench.pass_bytes(infos, M, K, N, esz, False, two)
+    tot = bench.pass_bytes(infos, M, K, N, esz, False, two, False)  # K3 one level: subtracted below
     k3, nodes, m, n = 0, 1, M, N
     for r in infos:
         mb, nb = m // r["m0"], n // r["n0"]
@@ -47,6 +47,7 @@ def main():
         for levels in (1, 2):
             p = fb.Plan([fb.Rule.builtin(r) for r in c.rules], M, K, N)
             p.set_k1_levels(levels)
+            p.set_k3_levels(levels)
             ws = p.workspace()
             for _ in range(2):
                 p.execute(A, B, Cm, ws=ws)
@@ -60,7 +61,9 @@ def main():
             ms = t["K1"][0] / a.reps
             nb = k1_bytes(infos, M, K, N, 8, levels == 2)
             out[f"{cfg}_L{levels}"] = {"k1_ms": ms, "k1_GB": nb / 1e9, "GBps": nb / ms / 1e6,
-                                       "launches": t["K1"][1] // a.reps}
+                                       "launches": t["K1"][1] // a.reps,
+                                       "k3_ms": t.get("K3", (0.0, 0))[0] / a.reps,
+                                       "k3_launches": t.get("K3", (0.0, 0))[1] // a.reps}
             del ws, p
             torch.cuda.empty_cache()
         del A, B, Cm
