@@ -12,7 +12,7 @@ scaled: the 7 top-level products are split round-robin over the ranks.  Timing: 
 steps, then K steps bracketed by barrier + synchronize, CUDA events on the launch stream, max
 over ranks.  The operands (8 GiB each) exceed the 126 MB L2, so no flush is needed.
 
-The JSON line also carries: `e2e` (same metric through fmm_execute_host with pinned host
+The JSON line also carries: `e2e` (same metric through fmm_execute_host_batch with pinned host
 buffers, copies inside the timed region), `roofline` (the leaf-product kernel K2 against the
 measured FP64 DMMA peak), `cpu_baseline` (the CPU oracle on a bounded row/column sample of the
 same workload), `clocks` (nvidia-smi sampled during the timed region) and `gpu_launches`.
@@ -535,38 +535,69 @@ def run_fmm(args):
                             "copy bandwidth (MEASURED_PEAKS.json hbm_gbs); frac = t_roof / t"}
 
     # ---- end-to-end through the C ABI with host buffers ---------------------------------------
+    # value: K problems through fmm_execute_host_batch (pinned host A, B in, C out every problem;
+    # two device buffer sets, so problem i's input copies overlap problem i - 1's compute and its
+    # C copy-out problem i + 1's).  serial: one fmm_execute_host call per problem, synchronised
+    # in between (no cross-problem overlap).  Multi-rank: rank 0 copies in, broadcasts, and
+    # copies the reduced C out, every step.
     e2e = None
     if not args.no_e2e:
         C_h = torch.empty((M, N), dtype=dt).pin_memory() if rank == 0 else None
-        for it in range(args.e2e_warmup + args.steps):
-            if ws > 1:
-                dist.barrier()
+
+        def e2e_serial(nsteps, warm):
+            for it in range(warm + nsteps):
+                if ws > 1:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                if it == warm:
+                    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    f0.record(stream)
+                if ws == 1:
+                    plan.execute_host(A_h, B_h, C_h, A, B, Cd, ws=wsp, stream=stream)
+                else:
+                    with torch.cuda.stream(stream):
+                        if rank == 0:
+                            A.copy_(A_h, non_blocking=True)
+                            B.copy_(B_h, non_blocking=True)
+                        dist.broadcast(A, 0)
+                        dist.broadcast(B, 0)
+                        step()
+                        if rank == 0:
+                            C_h.copy_(Cd, non_blocking=True)
+            f1.record(stream)
             torch.cuda.synchronize()
-            if it == args.e2e_warmup:
-                f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                f0.record(stream)
-            if ws == 1:
-                plan.execute_host(A_h, B_h, C_h, A, B, Cd, ws=wsp, stream=stream)
-            else:
-                with torch.cuda.stream(stream):
-                    if rank == 0:
-                        A.copy_(A_h, non_blocking=True)
-                        B.copy_(B_h, non_blocking=True)
-                    dist.broadcast(A, 0)
-                    dist.broadcast(B, 0)
-                    step()
-                    if rank == 0:
-                        C_h.copy_(Cd, non_blocking=True)
-        f1.record(stream)
-        torch.cuda.synchronize()
-        ems = f0.elapsed_time(f1)
-        if ws > 1:
-            t = torch.tensor([ems], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+            return f0.elapsed_time(f1)
+
+        def max_ranks(v):
+            if ws > 1:
+                t = torch.tensor([v], dtype=torch.float64, device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                v = float(t.item())
+            return v
+
+        sms = max_ranks(e2e_serial(args.steps, args.e2e_warmup))
+        ems, how = sms, "one fmm_execute_host call per problem, synchronised in between"
+        if ws == 1:
+            A2, B2, C2 = torch.empty_like(A), torch.empty_like(B), torch.empty_like(Cd)
+            devs = ([A, A2], [B, B2], [Cd, C2])
+            W = max(args.e2e_warmup, 2)
+            plan.execute_host_batch([A_h] * W, [B_h] * W, [C_h] * W, *devs, ws=wsp, stream=stream)
+            torch.cuda.synchronize()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            plan.execute_host_batch([A_h] * args.steps, [B_h] * args.steps, [C_h] * args.steps,
+                                    *devs, ws=wsp, stream=stream)
+            f1.record(stream)
+            torch.cuda.synchronize()
+            ems = f0.elapsed_time(f1)
+            how = ("K problems through one fmm_execute_host_batch call (2 device buffer sets: "
+                   "copies of neighbouring problems overlap compute)")
+            del A2, B2, C2
         e2e = {"value": flops * args.steps / (ems * 1e-3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": (M * K + K * N) * esz, "d2h_bytes_per_step": M * N * esz,
-               "ms_per_step": ems / args.steps}
+               "ms_per_step": ems / args.steps, "how": how,
+               "serial": {"value": flops * args.steps / (sms * 1e-3) / 1e9,
+                          "ms_per_step": sms / args.steps}}
 
     # ---- CPU oracle baseline (rank 0, N = 1) ----------------------------------------------------
     cpu = None
@@ -610,7 +641,7 @@ def run_fmm(args):
 def main():
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fmm", choices=["fmm", "reference"])
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])

@@ -272,6 +272,25 @@ fmm_status fmm_execute_host(const fmm_plan* plan, const void* A_host, int64_t ld
                             void* A_dev, void* B_dev, void* C_dev, void* ws, size_t ws_bytes,
                             void* stream);
 
+/* A stream of `count` independent products C_i = A_i.B_i with HOST buffers (serving-style
+ * batch), each as fmm_execute_host, pipelined across problems: problem i is staged in device
+ * buffer set i mod nbuf (A_devs / B_devs / C_devs: nbuf dense device buffers each, ld = K / N /
+ * N) and its input copies wait only for the compute of problem i - nbuf (the last reader of that
+ * set), so with nbuf = 2 they stream in while problem i - 1 computes, and problem i - 1's C
+ * copy-out overlaps problem i's compute.  Compute runs on `stream` in order (one workspace).
+ * A_hosts / B_hosts / C_hosts: arrays of count host pointers (pinned for asynchronous copies;
+ * C_hosts may repeat a buffer -- its copies are ordered).  Plans outside the per-block copy
+ * pipeline (L = 0, scaling, zero padding, communicator) copy whole operands on the copy streams
+ * around fmm_execute (still overlapped across problems); nbuf = 1 runs the problems one after
+ * another.
+ * Returns without synchronising; every C_host is valid after the stream completes.  FMM_E_ARG
+ * for null pointers, count < 0, nbuf < 1 or bad ld. */
+fmm_status fmm_execute_host_batch(const fmm_plan* plan, int count, const void* const* A_hosts,
+                                  int64_t lda, const void* const* B_hosts, int64_t ldb,
+                                  void* const* C_hosts, int64_t ldc, void* const* A_devs,
+                                  void* const* B_devs, void* const* C_devs, int nbuf, void* ws,
+                                  size_t ws_bytes, void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * Building blocks (one recursion node; used by tests and tools)
  * ------------------------------------------------------------------------------------- */

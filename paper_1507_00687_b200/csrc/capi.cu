@@ -1538,29 +1538,39 @@ fmm_status fmm_plan_step_times(fmm_plan* p, double* ms, int64_t* launches) {
 // top-level blocks of A and B are copied H2D on a copy stream in order of first use, each
 // top-level product r waits only for the blocks its K1 reads, and every block C_k is copied
 // D2H as soon as its last contribution (the last r with w_kr != 0) has been accumulated.
+// The plan's two copy streams (host-to-device, device-to-host) on the current device.
+static fmm_status ensure_copy_streams(const fmm_plan* p) {
+  std::lock_guard<std::mutex> g(p->dev_mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (p->copy_dev != dev) {
+    if (p->copy_h2d) cudaStreamDestroy(p->copy_h2d);
+    if (p->copy_d2h) cudaStreamDestroy(p->copy_d2h);
+    cudaError_t e = cudaStreamCreateWithFlags(&p->copy_h2d, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->copy_d2h, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_status(e, "fmm_execute_host streams");
+    p->copy_dev = dev;
+  }
+  return FMM_OK;
+}
+
+// gate: if non-null, the copies into A_dev / B_dev wait for this event instead of for all
+// earlier work on st (fmm_execute_host_batch: the compute that last read this buffer set).
+// join: st waits for the C_host copies at the end.  done_out: if non-null, receives an event
+// recorded after the last C_host copy (the caller destroys it).
 static fmm_status execute_host_pipelined(const fmm_plan* p, const void* A_host, int64_t lda,
                                          const void* B_host, int64_t ldb, void* C_host,
                                          int64_t ldc, void* A_dev, void* B_dev, void* C_dev,
-                                         void* ws, size_t ws_bytes, cudaStream_t st) {
+                                         void* ws, size_t ws_bytes, cudaStream_t st,
+                                         cudaEvent_t gate = nullptr, bool join = true,
+                                         cudaEvent_t* done_out = nullptr) {
   fmm_status fs = ensure_device(p);
   if (fs != FMM_OK) return fs;
   size_t need = 0;
   fmm_plan_workspace_bytes(p, &need);
   if (ws_bytes < need || !ws) { set_error("fmm_execute_host: workspace too small"); return FMM_E_OOM; }
   cudaError_t e = cudaSuccess;
-  {
-    std::lock_guard<std::mutex> g(p->dev_mu);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (p->copy_dev != dev) {
-      if (p->copy_h2d) cudaStreamDestroy(p->copy_h2d);
-      if (p->copy_d2h) cudaStreamDestroy(p->copy_d2h);
-      e = cudaStreamCreateWithFlags(&p->copy_h2d, cudaStreamNonBlocking);
-      if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->copy_d2h, cudaStreamNonBlocking);
-      if (e != cudaSuccess) return cuda_status(e, "fmm_execute_host streams");
-      p->copy_dev = dev;
-    }
-  }
+  if ((fs = ensure_copy_streams(p)) != FMM_OK) return fs;
   const RuleData& ru = p->rules[p->node_rule[0][0]];
   const size_t es = (size_t)elem_size(p->dtype);
   const int64_t mb = p->lm[1], kb = p->lk[1], nb = p->ln[1];
@@ -1571,11 +1581,12 @@ static fmm_status execute_host_pipelined(const fmm_plan* p, const void* A_host, 
     if (r == cudaSuccess) evs.push_back(*ev);
     return r;
   };
-  cudaEvent_t entry;
-  if ((e = mkev(&entry)) != cudaSuccess) return cuda_status(e, "event");
-  cudaEventRecord(entry, st);  // device buffers may still be in use by earlier work on st
+  cudaEvent_t entry = gate;
+  if (!entry) {
+    if ((e = mkev(&entry)) != cudaSuccess) return cuda_status(e, "event");
+    cudaEventRecord(entry, st);  // device buffers may still be in use by earlier work on st
+  }
   cudaStreamWaitEvent(p->copy_h2d, entry, 0);
-  cudaStreamWaitEvent(p->copy_d2h, entry, 0);
   std::vector<cudaEvent_t> evA(nA, nullptr), evB(nB, nullptr);
   auto copyA = [&](int i) {
     const int ia = i % ru.m0, ja = i / ru.m0;  // column-major block index
@@ -1647,9 +1658,15 @@ static fmm_status execute_host_pipelined(const fmm_plan* p, const void* A_host, 
   for (int k = 0; k < nC; ++k)
     if (!copied[k]) copyC(k);
   cudaEvent_t done;
-  mkev(&done);
+  if (done_out) {
+    if ((e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming)) != cudaSuccess)
+      return cuda_status(e, "event");
+    *done_out = done;
+  } else {
+    mkev(&done);
+  }
   cudaEventRecord(done, p->copy_d2h);
-  cudaStreamWaitEvent(st, done, 0);  // stream completion => C_host valid
+  if (join) cudaStreamWaitEvent(st, done, 0);  // stream completion => C_host valid
   e = cudaGetLastError();
   for (cudaEvent_t ev : evs) cudaEventDestroy(ev);  // deferred until the events complete
   return cuda_status(e, "fmm_execute_host");
@@ -1669,10 +1686,24 @@ static const fmm_plan* depth_first_twin(const fmm_plan* p) {
     t->persistent = p->persistent;
     t->operand_fusion = p->operand_fusion;
     t->split_chains = p->split_chains;
+    t->k1_two_level = p->k1_two_level;
+    t->k3_two_level = p->k3_two_level;
     if (compile_plan(t) != FMM_OK) { delete t; return nullptr; }
     p->df_twin = t;
   }
   return p->df_twin;
+}
+
+// The plan whose top-level groups drive the host-copy pipeline (the plan itself if depth-first
+// at the top, else its depth-first twin), or null where the pipeline does not apply.
+static const fmm_plan* host_pipeline_plan(const fmm_plan* p, const void* ws, size_t ws_bytes) {
+  if (!(p->L > 0 && p->scaling.mode == FMM_SCALE_NONE && !(p->comm && p->nranks > 1) &&
+        !p->padded && p->M > 0 && p->N > 0 && p->K > 0))
+    return nullptr;
+  const fmm_plan* q = p->groups.empty() ? depth_first_twin(p) : p;
+  size_t need = 0;
+  if (q) fmm_plan_workspace_bytes(q, &need);
+  return q && !q->groups.empty() && ws && ws_bytes >= need ? q : nullptr;
 }
 
 fmm_status fmm_execute_host(const fmm_plan* p, const void* A_host, int64_t lda,
@@ -1685,15 +1716,9 @@ fmm_status fmm_execute_host(const fmm_plan* p, const void* A_host, int64_t lda,
   }
   if (lda < p->K || ldb < p->N || ldc < p->N) { set_error("fmm_execute_host: bad ld"); return FMM_E_ARG; }
   cudaStream_t st = (cudaStream_t)stream;
-  if (p->L > 0 && p->scaling.mode == FMM_SCALE_NONE && !(p->comm && p->nranks > 1) && !p->padded && p->M > 0 &&
-      p->N > 0 && p->K > 0) {
-    const fmm_plan* q = p->groups.empty() ? depth_first_twin(p) : p;
-    size_t need = 0;
-    if (q) fmm_plan_workspace_bytes(q, &need);
-    if (q && !q->groups.empty() && ws && ws_bytes >= need)
-      return execute_host_pipelined(q, A_host, lda, B_host, ldb, C_host, ldc, A_dev, B_dev, C_dev,
-                                    ws, ws_bytes, st);
-  }
+  if (const fmm_plan* q = host_pipeline_plan(p, ws, ws_bytes))
+    return execute_host_pipelined(q, A_host, lda, B_host, ldb, C_host, ldc, A_dev, B_dev, C_dev,
+                                  ws, ws_bytes, st);
   const size_t es = (size_t)elem_size(p->dtype);
   cudaError_t e = cudaMemcpy2DAsync(A_dev, p->K * es, A_host, lda * es, p->K * es, p->M, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess)
@@ -1703,6 +1728,91 @@ fmm_status fmm_execute_host(const fmm_plan* p, const void* A_host, int64_t lda,
   if (s != FMM_OK) return s;
   e = cudaMemcpy2DAsync(C_host, ldc * es, C_dev, p->N * es, p->N * es, p->M, cudaMemcpyDeviceToHost, st);
   return cuda_status(e, "fmm_execute_host D2H");
+}
+
+fmm_status fmm_execute_host_batch(const fmm_plan* p, int count, const void* const* A_hosts,
+                                  int64_t lda, const void* const* B_hosts, int64_t ldb,
+                                  void* const* C_hosts, int64_t ldc, void* const* A_devs,
+                                  void* const* B_devs, void* const* C_devs, int nbuf, void* ws,
+                                  size_t ws_bytes, void* stream) {
+  if (!p || count < 0 || nbuf < 1 || !A_hosts || !B_hosts || !C_hosts || !A_devs || !B_devs || !C_devs) {
+    set_error("fmm_execute_host_batch: bad arguments");
+    return FMM_E_ARG;
+  }
+  for (int i = 0; i < count; ++i)
+    if (!A_hosts[i] || !B_hosts[i] || !C_hosts[i]) { set_error("fmm_execute_host_batch: null host pointer"); return FMM_E_ARG; }
+  for (int s = 0; s < nbuf; ++s)
+    if (!A_devs[s] || !B_devs[s] || !C_devs[s]) { set_error("fmm_execute_host_batch: null device pointer"); return FMM_E_ARG; }
+  if (lda < p->K || ldb < p->N || ldc < p->N) { set_error("fmm_execute_host_batch: bad ld"); return FMM_E_ARG; }
+  cudaStream_t st = (cudaStream_t)stream;
+  const fmm_plan* q = host_pipeline_plan(p, ws, ws_bytes);
+  if (nbuf == 1) {  // no cross-problem overlap: one problem after the other
+    for (int i = 0; i < count; ++i) {
+      const int s = i % nbuf;
+      fmm_status fs = fmm_execute_host(p, A_hosts[i], lda, B_hosts[i], ldb, C_hosts[i], ldc,
+                                       A_devs[s], B_devs[s], C_devs[s], ws, ws_bytes, stream);
+      if (fs != FMM_OK) return fs;
+    }
+    return FMM_OK;
+  }
+  // Problem i uses buffer set i mod nbuf.  Its input copies wait only for the compute of problem
+  // i - nbuf (the last reader of that set), so they stream in while problem i - 1 computes; its
+  // compute waits for problem i - nbuf's C copy-out (the same C buffer).  One compute stream, so
+  // the workspace is reused safely.
+  std::vector<cudaEvent_t> cdone(count, nullptr), ddone(count, nullptr);
+  cudaEvent_t entry = nullptr;
+  cudaError_t e = cudaEventCreateWithFlags(&entry, cudaEventDisableTiming);
+  if (e != cudaSuccess) return cuda_status(e, "fmm_execute_host_batch event");
+  cudaEventRecord(entry, st);
+  fmm_status fs = FMM_OK;
+  for (int i = 0; i < count && fs == FMM_OK; ++i) {
+    const int s = i % nbuf;
+    if (i >= nbuf) cudaStreamWaitEvent(st, ddone[i - nbuf], 0);
+    cudaEvent_t gate = i >= nbuf ? cdone[i - nbuf] : entry;
+    if (q) {
+      fs = execute_host_pipelined(q, A_hosts[i], lda, B_hosts[i], ldb, C_hosts[i], ldc, A_devs[s],
+                                  B_devs[s], C_devs[s], ws, ws_bytes, st, gate, false, &ddone[i]);
+    } else {  // whole-operand copies on the copy streams around an ordinary fmm_execute
+      fs = ensure_copy_streams(p);
+      const size_t es = (size_t)elem_size(p->dtype);
+      cudaEvent_t in = nullptr, out = nullptr;
+      if (fs == FMM_OK && ((e = cudaEventCreateWithFlags(&in, cudaEventDisableTiming)) != cudaSuccess ||
+                           (e = cudaEventCreateWithFlags(&out, cudaEventDisableTiming)) != cudaSuccess ||
+                           (e = cudaEventCreateWithFlags(&ddone[i], cudaEventDisableTiming)) != cudaSuccess))
+        fs = cuda_status(e, "fmm_execute_host_batch event");
+      if (fs == FMM_OK) {
+        cudaStreamWaitEvent(p->copy_h2d, gate, 0);
+        cudaMemcpy2DAsync(A_devs[s], p->K * es, A_hosts[i], lda * es, p->K * es, p->M, cudaMemcpyHostToDevice, p->copy_h2d);
+        cudaMemcpy2DAsync(B_devs[s], p->N * es, B_hosts[i], ldb * es, p->N * es, p->K, cudaMemcpyHostToDevice, p->copy_h2d);
+        cudaEventRecord(in, p->copy_h2d);
+        cudaStreamWaitEvent(st, in, 0);
+        fs = fmm_execute(p, A_devs[s], p->K, B_devs[s], p->N, C_devs[s], p->N, ws, ws_bytes, stream);
+      }
+      if (fs == FMM_OK) {
+        cudaEventRecord(out, st);
+        cudaStreamWaitEvent(p->copy_d2h, out, 0);
+        cudaMemcpy2DAsync(C_hosts[i], ldc * es, C_devs[s], p->N * es, p->N * es, p->M, cudaMemcpyDeviceToHost, p->copy_d2h);
+        cudaEventRecord(ddone[i], p->copy_d2h);
+      }
+      if (in) cudaEventDestroy(in);
+      if (out) cudaEventDestroy(out);
+    }
+    if (fs != FMM_OK) break;
+    if ((e = cudaEventCreateWithFlags(&cdone[i], cudaEventDisableTiming)) != cudaSuccess) {
+      fs = cuda_status(e, "fmm_execute_host_batch event");
+      break;
+    }
+    cudaEventRecord(cdone[i], st);
+  }
+  for (int i = 0; i < count; ++i)
+    if (ddone[i]) cudaStreamWaitEvent(st, ddone[i], 0);  // stream completion => all C_host valid
+  for (int i = 0; i < count; ++i) {
+    if (cdone[i]) cudaEventDestroy(cdone[i]);
+    if (ddone[i]) cudaEventDestroy(ddone[i]);
+  }
+  cudaEventDestroy(entry);
+  if (fs != FMM_OK) return fs;
+  return cuda_status(cudaGetLastError(), "fmm_execute_host_batch");
 }
 
 fmm_status fmm_plan_last_scaling_steps(const fmm_plan* p, void* ws, int* steps, void* stream) {

@@ -62,6 +62,7 @@ SIGNATURES = {
     "fmm_plan_step_times": (_I, [_P, _P, _P]),
     "fmm_execute": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _SZ, _P]),
     "fmm_execute_host": (_I, [_P, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _SZ, _P]),
+    "fmm_execute_host_batch": (_I, [_P, _I, _P, _I64, _P, _I64, _P, _I64, _P, _P, _P, _I, _P, _SZ, _P]),
     "fmm_node_st": (_I, [_P, _I, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _P]),
     "fmm_node_c": (_I, [_P, _I, _I64, _I64, _P, _P, _I64, _P]),
     "fmm_gemm": (_I, [_I, _I, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _I64, _P]),
@@ -375,6 +376,24 @@ class Plan:
               C.c_void_p(B_dev.data_ptr()), C.c_void_p(C_dev.data_ptr()),
               C.c_void_p(ws.data_ptr()), ws.numel() * ws.element_size(), _stream(stream))
         return C_host
+
+    def execute_host_batch(self, A_hosts, B_hosts, C_hosts, A_devs, B_devs, C_devs, ws=None,
+                           stream=None):
+        """A stream of products C_i = A_i B_i with host (pinned) buffers, pipelined across
+        problems over the device buffer sets A_devs / B_devs / C_devs (problem i uses set
+        i mod len(A_devs)); returns without synchronising."""
+        n, nbuf = len(A_hosts), len(A_devs)
+        if n == 0:
+            return C_hosts
+        if not (len(B_hosts) == len(C_hosts) == n and len(B_devs) == len(C_devs) == nbuf):
+            raise ValueError("execute_host_batch: list lengths differ")
+        ws = self.workspace(A_devs[0].device) if ws is None else ws
+        arr = lambda ts: (C.c_void_p * max(len(ts), 1))(*[t.data_ptr() for t in ts])
+        _call("fmm_execute_host_batch", self._h, n, arr(A_hosts), A_hosts[0].stride(0),
+              arr(B_hosts), B_hosts[0].stride(0), arr(C_hosts), C_hosts[0].stride(0),
+              arr(A_devs), arr(B_devs), arr(C_devs), nbuf, C.c_void_p(ws.data_ptr()),
+              ws.numel() * ws.element_size(), _stream(stream))
+        return C_hosts
 
     def last_scaling_steps(self, ws=None, stream=None) -> int:
         ws = self._ws if ws is None else ws

@@ -1,6 +1,7 @@
 """Host-side (no GPU) checks of the C-ABI library: it loads, exports every symbol include/fmm.h
 declares, its rule tables / Brent check / plan logic behave, and its built-in rules equal the
 oracle's independently written tables."""
+import ctypes
 import re
 
 import numpy as np
@@ -177,3 +178,20 @@ def test_bench_pass_byte_model():
     assert bench.pass_bytes([w], n, n, n, 8, False) == (4 + 4) * q * 2 + (7 + 4) * q
     assert bench.pass_bytes([w], n, n, n, 8, True) == (4 + 4) * q * 2 + 4 * q
     assert bench.pass_bytes([c], n, n, n, 8, False) == (8 + 4) * q
+
+
+def test_execute_host_batch_argument_errors():
+    # checked before any CUDA call: null arrays, nbuf < 1, count < 0, ld < cols
+    lib = fb.lib()
+    w = fb.Rule.builtin("winograd")
+    p = fb.Plan([w], 64, 64, 64)
+    P = ctypes.c_void_p
+    one = (P * 1)(P(16))
+    args = lambda count, nbuf, ld: (p._h, count, one, ld, one, ld, one, ld, one, one, one, nbuf,
+                                    None, ctypes.c_size_t(0), None)
+    assert lib.fmm_execute_host_batch(*args(1, 0, 64)) == 1   # nbuf < 1
+    assert lib.fmm_execute_host_batch(*args(-1, 1, 64)) == 1  # count < 0
+    assert lib.fmm_execute_host_batch(*args(1, 1, 32)) == 1   # ld < cols
+    assert lib.fmm_execute_host_batch(p._h, 1, None, 64, one, 64, one, 64, one, one, one, 1,
+                                      None, ctypes.c_size_t(0), None) == 1
+    assert b"fmm_execute_host_batch" in lib.fmm_last_error()

@@ -379,3 +379,32 @@ def test_deep_recursion_node_chunks(fb, fusion):
     Ai, Bi = fi.integer_pair(128, 128, 128, seed=3, lo=-2, hi=2)
     Ci = (Ai.astype(np.int64) @ Bi.astype(np.int64)).astype(np.float64)
     assert np.array_equal(p.execute(dev(Ai), dev(Bi)).cpu().numpy(), Ci)
+
+
+@pytest.mark.parametrize("nbuf", [1, 2, 3])
+@pytest.mark.parametrize("shape,scaling", [((256, 512, 384), None), ((250, 130, 66), None),
+                                           ((256, 256, 256), "repeated")])
+def test_execute_host_batch(fb, nbuf, shape, scaling):
+    # fmm_execute_host_batch: a stream of different problems, pipelined over nbuf device buffer
+    # sets, each result exactly fmm_execute's (the padded and the scaled plans take the
+    # whole-operand copy path)
+    M, K, N = shape
+    w = fb.Rule.builtin("winograd")
+    p = fb.Plan([w, w], M, K, N, scaling=scaling)
+    n = 5
+    pairs = [fi.random_pair(M, K, N, seed=100 + i) for i in range(n)]
+    want = [p.execute(dev(A), dev(B)).cpu().numpy() for A, B in pairs]
+    Ah = [torch.from_numpy(A).pin_memory() for A, _ in pairs]
+    Bh = [torch.from_numpy(B).pin_memory() for _, B in pairs]
+    Ch = [torch.full((M, N), float("nan"), dtype=torch.float64).pin_memory() for _ in range(n)]
+    Ad = [torch.empty((M, K), dtype=torch.float64, device="cuda") for _ in range(nbuf)]
+    Bd = [torch.empty((K, N), dtype=torch.float64, device="cuda") for _ in range(nbuf)]
+    Cd = [torch.empty((M, N), dtype=torch.float64, device="cuda") for _ in range(nbuf)]
+    for _ in range(2):  # twice: buffers and events reused across calls
+        for c in Ch:
+            c.fill_(float("nan"))
+        p.execute_host_batch(Ah, Bh, Ch, Ad, Bd, Cd)
+        torch.cuda.synchronize()
+        for c, w_ in zip(Ch, want):
+            assert np.array_equal(c.numpy(), w_)
+    p.execute_host_batch([], [], [], Ad, Bd, Cd)  # empty batch
