@@ -512,7 +512,12 @@ struct Builder {
   // the 128 x 128 kernel (v16, one CTA per SM) otherwise (profiles/r01_fusion_variants.md).
   int k2f_cfg() const {
     if (const char* e = getenv("FMM_K2F_VARIANT")) return atoi(e);
-    return p->lk[p->L] <= kK2fSmallK ? 13 : 16;
+    if (p->lk[p->L] > kK2fSmallK) return 16;
+    for (int ri : p->node_rule[p->L - 1]) {  // v13 holds the tables of 2x2 rules with R <= 8
+      const RuleData& r = p->rules[ri];
+      if (r.R > 8 || r.m0 * r.n0 > 4) return 16;
+    }
+    return 13;
   }
   int k2f_tile() const { return k2f_cfg() == 13 ? 64 : 128; }
   int k2f_slots() const { return k2f_cfg() == 13 ? 3 * 148 : 148;

@@ -22,6 +22,18 @@
 
 namespace fmm {
 
+// Dynamic shared memory above 48 KB, and the largest shared-memory carve-out: without the
+// carve-out hint the driver sized the 64 x 64 kernels' L1/shared split at 168 KB, which fits
+// only 2 of their 74 KB CTAs per SM instead of 3 (ncu "Block Limit Shared Mem").
+template <typename K>
+static cudaError_t set_smem(K* kern, int bytes) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             (int)cudaSharedmemCarveoutMaxShared);
+  return e;
+}
+
 namespace {
 
 constexpr int GROUP_M = 8;
@@ -291,12 +303,16 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
   double* Bs = smem + C::STAGES * C::A_STAGE;
-  __shared__ const double* pa[kMaxR];
-  __shared__ const double* pb[kMaxR];
-  __shared__ int64_t la[kMaxR], lb[kMaxR];
-  __shared__ uint32_t wm_s[kMaxR], fm_s[kMaxR];
-  __shared__ int r_s[kMaxR];
-  __shared__ double wcf[kMaxBlk * kMaxR];
+  // per-CTA product tables: the 64 x 64 configuration sizes them for 2x2 rules with R <= 8
+  // (the host selects it only for those) so that 3 CTAs fit an SM's 228 KB of shared memory
+  constexpr bool SMALL = C::BM * C::BN <= 64 * 64;
+  constexpr int CAPR = SMALL ? 8 : kMaxR, CAPW = SMALL ? 4 * 8 : kMaxBlk * kMaxR;
+  __shared__ const double* pa[CAPR];
+  __shared__ const double* pb[CAPR];
+  __shared__ int64_t la[CAPR], lb[CAPR];
+  __shared__ uint32_t wm_s[CAPR], fm_s[CAPR];
+  __shared__ int r_s[CAPR];
+  __shared__ double wcf[CAPW];
 
   // product chain split (chunk < nr): grid.y = group * count + parent, groups dispatched in
   // order; group g runs products [g*chunk, (g+1)*chunk) of its unit after group g-1 released
@@ -1166,8 +1182,7 @@ cudaError_t launch_fused_kernel(const FusedNode* dev_nodes, int count, int64_t m
   }
   dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)(count * groups));
   auto go = [&](auto kern) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::SMEM_BYTES);
+    cudaError_t e = set_smem(kern, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     kern<<<grid, C::THREADS, C::SMEM_BYTES, st>>>(dev_nodes, coef, b, m, n, k, tiles_m, tiles_n, P,
                                                   Q, R, count, chunk, groups > 1 ? turn : nullptr);
@@ -1204,14 +1219,12 @@ cudaError_t launch_cfg(const LeafNode* dev_leaves, int count, int64_t m, int64_t
   dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)count);
   cudaError_t e;
   if (vec) {
-    e = cudaFuncSetAttribute(k2_gemm_f64<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::SMEM_BYTES);
+    e = set_smem(k2_gemm_f64<C, true>, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     k2_gemm_f64<C, true><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(dev_leaves, b, m, n, k, tiles_m,
                                                                  tiles_n);
   } else {
-    e = cudaFuncSetAttribute(k2_gemm_f64<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::SMEM_BYTES);
+    e = set_smem(k2_gemm_f64<C, false>, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     k2_gemm_f64<C, false><<<grid, C::THREADS, C::SMEM_BYTES, st>>>(dev_leaves, b, m, n, k, tiles_m,
                                                                   tiles_n);
@@ -1301,8 +1314,7 @@ cudaError_t launch_gemm_f64_persistent(const FusedNode* dev_nodes, int count, in
   cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)2 * ctas * NR + 16, st);
   if (e != cudaSuccess) return e;
   auto go = [&](auto kern) {
-    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          Cf::SMEM_BYTES);
+    cudaError_t e2 = set_smem(kern, Cf::SMEM_BYTES);
     if (e2 != cudaSuccess) return e2;
     kern<<<ctas, Cf::THREADS, Cf::SMEM_BYTES, st>>>(dev_nodes, dev_coef, b, m, n, k, tiles_m, tiles_n,
                                                     P, Q, R, NR, U, U_dp, scratch, flags, counter);
@@ -1342,7 +1354,7 @@ cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t
     const int tiles_m = (int)((m + VO::BM - 1) / VO::BM), tiles_n = (int)((n + VO::BN - 1) / VO::BN);
     constexpr int smem = VO::STAGES * 2 * (VO::A_STAGE + VO::B_STAGE) * 8;
     auto go = [&](auto kern) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      cudaError_t e = set_smem(kern, smem);
       if (e != cudaSuccess) return e;
       kern<<<dim3((unsigned)(tiles_m * tiles_n), (unsigned)count), VO::THREADS, smem, st>>>(
           dev_nodes, dev_coef, b, m, n, k, tiles_m, tiles_n, P, Q, R);
@@ -1350,7 +1362,9 @@ cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t
     };
     return vec ? go(k2o_gemm_f64<VO, true>) : go(k2o_gemm_f64<VO, false>);
   }
-  switch (getenv("FMM_K2F_VARIANT") ? fused_variant() : cfg) {
+  int v = getenv("FMM_K2F_VARIANT") ? fused_variant() : cfg;
+  if (v == 13 && (R > 8 || P * Q > 4)) v = 16;  // v13's product tables hold 2x2 rules, R <= 8
+  switch (v) {
     case 13: return launch_fused_cfg<V13>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st, nr, chunk, turn);
     case 15: return launch_fused_cfg<V15>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st, nr, chunk, turn);
     case 17: return launch_fused_cfg<V17>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, vec, st, nr, chunk, turn);
