@@ -135,9 +135,13 @@ void fmm_plan_destroy(fmm_plan* plan);
 fmm_status fmm_plan_set_partition(fmm_plan* plan, int rank, int nranks);
 
 /* Schedule control (host-only): 0 = automatic (breadth-first unless its workspace exceeds
- * 24 GiB), 1 = breadth-first over all levels, 2 = depth-first over the top-level products
- * (each subtree breadth-first, top-level accumulation r ascending).  Results are bitwise
- * identical across schedules. */
+ * 24 GiB, then 3 on one rank if its workspace stays within 64 GiB, else 2), 1 = breadth-first
+ * over all levels, 2 = depth-first over the top-level products (each subtree breadth-first,
+ * top-level accumulation r ascending, per r), 3 = hybrid: the root's S_r / T_r of all r in one
+ * pass, the subtrees one after another, the root's (and level 1's, as one K3X2 pass)
+ * W-combination at the end (single rank; falls back to 2 above 64 GiB of workspace).  Results
+ * are bitwise identical across schedules.  FMM_E_ARG outside 0..3; the environment variable
+ * FMM_HYBRID=0 makes 0 choose 2 instead of 3. */
 fmm_status fmm_plan_set_schedule(fmm_plan* plan, int schedule);
 
 /* Epilogue fusion of the accumulation step (host-only; north star item 3, Eq.

@@ -185,6 +185,7 @@ fmm_plan::~fmm_plan() {
 namespace {
 
 constexpr int kPersistCtas = 148;  // B200 SMs: one persistent K2P CTA per SM
+constexpr size_t kHybridMaxWs = (size_t)64 << 30;  // hybrid top-level schedule: workspace cap
 constexpr int64_t kK2fSmallK = 1024;  // leaf inner dimension up to which K2F uses 64 x 64 tiles
 
 int elem_size(int dtype) { return dtype == FMM_F64 ? 8 : 4; }
@@ -676,9 +677,10 @@ struct Builder {
 
   // W-combination levels top .. l (bottom-up); two levels per pass (K3X2) paired from the
   // bottom where the rules allow.  lv[q] = the nodes of level l + q.
-  void emit_k3_levels(int l, int top, const std::vector<std::vector<Node>>& lv) {
-    for (int d = top; d >= l;) {
-      const int pr = p->k3_two_level && d - 1 >= l ? k1x2_pair(d - 1, lv[d - 1 - l]) : 0;
+  void emit_k3_levels(int l, int top, const std::vector<std::vector<Node>>& lv, int stop = -1) {
+    if (stop < l) stop = l;  // levels below `stop` are combined by the caller
+    for (int d = top; d >= stop;) {
+      const int pr = p->k3_two_level && d - 1 >= stop ? k1x2_pair(d - 1, lv[d - 1 - l]) : 0;
       if (pr) {
         emit_k3x2(d - 1, lv[d - 1 - l], lv[d + 1 - l], pr);
         d -= 2;
@@ -690,7 +692,11 @@ struct Builder {
   }
 
   // breadth-first over the subtree(s) rooted at `nodes` (level l), outputs into nodes' c.
-  void breadth_first(int l, const std::vector<Node>& nodes) {
+  // kid_c: if given, the outputs of the level-(l+1) nodes (persistent blocks of the caller);
+  // k3_stop: W-combination levels below it are left to the caller.  Returns the level-(l+1)
+  // nodes.
+  std::vector<Node> breadth_first(int l, const std::vector<Node>& nodes,
+                                  const std::vector<Op>* kid_c = nullptr, int k3_stop = -1) {
     std::vector<std::vector<Node>> lv{nodes};
     int64_t npar = (int64_t)nodes.size();  // parents of the leaves (R uniform per level)
     for (int d = l; d < p->L - 1; ++d) npar *= p->rules[p->node_rule[d][0]].R;
@@ -713,6 +719,8 @@ struct Builder {
         lv.push_back(emit_k1(d, lv.back(), -1, !(last && fuse), last && opf));
         d += 1;
       }
+      if (kid_c && lv.size() == (pr ? 3u : 2u))  // the first pass created level l + 1
+        for (size_t i = 0; i < lv[1].size(); ++i) lv[1][i].c = (*kid_c)[i];
     }
     int top = p->L - 1;
     if (fuse) {
@@ -721,7 +729,8 @@ struct Builder {
     } else {
       emit_k2(lv.back());
     }
-    emit_k3_levels(l, top, lv);
+    emit_k3_levels(l, top, lv, k3_stop);
+    return lv[1];
   }
 
   void build() {
@@ -746,13 +755,61 @@ struct Builder {
                      p->lm[l + 1] * p->ln[l + 1]);
     }
     const int64_t bf_bytes = bf * elem_size(p->dtype);
-    const bool split = p->schedule == 2 || p->nranks > 1 ||
+    const bool split = p->schedule >= 2 || p->nranks > 1 ||
                        (p->schedule == 0 && bf_bytes > (int64_t)24 << 30);
     if (!split) {
       breadth_first(0, {root});
       return;
     }
+    if ((p->schedule == 3 || (p->schedule == 0 && hybrid_on())) && p->nranks == 1 && p->L >= 2) {
+      const size_t s0 = p->steps.size(), d0 = desc.size();
+      hybrid(root);
+      if (ws_peak * elem_size(p->dtype) <= kHybridMaxWs) return;
+      p->steps.resize(s0);  // too much workspace: per-r depth-first instead
+      desc.resize(d0);
+      ws_elems = ws_peak = 0;
+    }
     depth_first(0, root, 0);
+  }
+
+  static bool hybrid_on() {
+    const char* e = getenv("FMM_HYBRID");
+    return !e || atoi(e) != 0;
+  }
+
+  // Single-rank plans too large for breadth-first (C5): the root's S_r / T_r for every r in one
+  // K1 pass (A and B read once, instead of once per r), then each top-level subtree's levels
+  // 1 .. L-1 one after another (their scratch workspace reused across r), then the root's
+  // W-combination -- together with level 1's, as one K3X2 pass from the level-2 products, where
+  // the rules pair -- at the end, instead of a per-r ACC read-modify-write of C.  The
+  // summation order of every C element is unchanged (ascending r at each level): bitwise the
+  // per-r depth-first schedule.  No top-level groups: fmm_execute_host uses the depth-first twin.
+  void hybrid(const Node& root) {
+    const RuleData& ru = rule_at(0, 0);
+    // K3X2 (0, 1) reads the level-2 outputs, so level 1 must not be the leaf parents' level
+    // (whose W-combination the leaf kernel may fuse into the level-1 outputs): L >= 3
+    const int pair = p->k3_two_level && p->L >= 3 ? k1x2_pair(0, {root}) : 0;
+    std::vector<Node> kids = emit_k1(0, {root}, -1, /*alloc_c=*/pair == 0);
+    std::vector<Op> c2;  // persistent level-2 outputs (pair): the K3X2 inputs
+    int R2 = 0;
+    if (pair) {
+      R2 = builtin_R((pair - 1) % 3);
+      for (int q = 0; q < ru.R * R2; ++q) c2.push_back(ws_op(ws_alloc(p->lm[2] * p->ln[2]), p->ln[2]));
+    }
+    const int64_t mark = ws_elems;
+    std::vector<Node> level2;
+    for (int r = 0; r < ru.R; ++r) {
+      ws_elems = mark;  // subtrees run one after another on one stream
+      if (pair) {
+        std::vector<Op> kc(c2.begin() + (size_t)r * R2, c2.begin() + (size_t)(r + 1) * R2);
+        std::vector<Node> l2 = breadth_first(1, {kids[r]}, &kc, 2);
+        level2.insert(level2.end(), l2.begin(), l2.end());
+      } else {
+        breadth_first(1, {kids[r]});
+      }
+    }
+    if (pair) emit_k3x2(0, {root}, level2, pair);
+    else emit_k3(0, {root}, kids);
   }
 
   // Number of shard units below one node of level l (product of the ranks of levels l ..
@@ -1279,7 +1336,7 @@ fmm_status fmm_plan_set_partition(fmm_plan* p, int rank, int nranks) {
 }
 
 fmm_status fmm_plan_set_schedule(fmm_plan* p, int schedule) {
-  if (!p || schedule < 0 || schedule > 2) { set_error("fmm_plan_set_schedule: bad args"); return FMM_E_ARG; }
+  if (!p || schedule < 0 || schedule > 3) { set_error("fmm_plan_set_schedule: bad args"); return FMM_E_ARG; }
   p->schedule = schedule;
   return compile_plan(p);
 }

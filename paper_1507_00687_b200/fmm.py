@@ -287,8 +287,10 @@ class Plan:
         self._ws = None
 
     def set_schedule(self, schedule: str):
-        """'auto' | 'breadth' | 'depth' (top-level depth-first)."""
-        _call("fmm_plan_set_schedule", self._h, {"auto": 0, "breadth": 1, "depth": 2}[schedule])
+        """'auto' | 'breadth' | 'depth' (top-level depth-first, per-r accumulation) | 'hybrid'
+        (root S / T at once, subtrees in turn, root combination at the end)."""
+        _call("fmm_plan_set_schedule", self._h,
+              {"auto": 0, "breadth": 1, "depth": 2, "hybrid": 3}[schedule])
         self._ws = None
 
     def stability(self):

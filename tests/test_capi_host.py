@@ -195,3 +195,21 @@ def test_execute_host_batch_argument_errors():
     assert lib.fmm_execute_host_batch(p._h, 1, None, 64, one, 64, one, 64, one, one, one, 1,
                                       None, ctypes.c_size_t(0), None) == 1
     assert b"fmm_execute_host_batch" in lib.fmm_last_error()
+
+
+def test_hybrid_schedule_structure():
+    # hybrid (schedule 3): one root K1, per top-level r a K1X2 (levels 1-2) and a K2F, one
+    # K3X2 (levels 0-1) at the end; auto picks it for single-rank plans whose breadth-first
+    # workspace exceeds 24 GiB (C5), and depth-first when partitioned
+    w = fb.Rule.builtin("winograd")
+    p = fb.Plan([w] * 3, 1024, 1024, 1024)
+    p.set_fusion("on")
+    p.set_schedule("hybrid")
+    assert p.launch_count() == 1 + 7 * 2 + 1
+    big = fb.Plan([w] * 3, 32768, 32768, 32768)
+    assert big.launch_count() == 1 + 7 * 2 + 1
+    assert big.workspace_bytes() <= 64 << 30
+    big.set_partition(0, 2)
+    assert big.launch_count() != 1 + 7 * 2 + 1
+    with pytest.raises(fb.FmmError):
+        fb.fmm._call("fmm_plan_set_schedule", p._h, 4)

@@ -52,7 +52,7 @@ def exe(p, A, B):
 
 
 @pytest.mark.parametrize("pname", sorted(PLANS))
-@pytest.mark.parametrize("schedule", ["breadth", "depth"])
+@pytest.mark.parametrize("schedule", ["breadth", "depth", "hybrid"])
 def test_fused_equals_unfused_bitwise(fb, pname, schedule):
     names = PLANS[pname]
     A, B = fi.random_pair(512, 384, 256, seed=21)
@@ -256,7 +256,8 @@ def test_fused_tf32_equals_unfused(fb, leaf, pname, dims):
 def test_fused_tf32_depth_first_and_partition(fb):
     A, B = fi.random_pair(512, 512, 512, seed=7, dtype=np.float32)
     ref = None
-    for sched, part in (("breadth", None), ("depth", None), ("auto", (0, 2)), ("auto", (1, 2))):
+    for sched, part in (("breadth", None), ("depth", None), ("hybrid", None), ("auto", (0, 2)),
+                        ("auto", (1, 2))):
         p = fb.Plan([fb.Rule.builtin("winograd")] * 2, 512, 512, 512, dtype="f32",
                     leaf=fb.fmm.LEAF_3XTF32)
         p.set_fusion("on")

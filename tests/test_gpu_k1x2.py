@@ -72,7 +72,7 @@ def test_unit_leaf_equals_oracle_bitwise(fb, pname):
 
 
 @pytest.mark.parametrize("pname", sorted(PLANS))
-@pytest.mark.parametrize("schedule", ["breadth", "depth"])
+@pytest.mark.parametrize("schedule", ["breadth", "depth", "hybrid"])
 def test_two_level_equals_one_level_bitwise(fb, pname, schedule):
     names = PLANS[pname]
     L = len(names)

@@ -246,6 +246,8 @@ def test_split_schedule_matches_breadth_first(fb):
     bf = p.execute(dev(A), dev(B)).cpu().numpy()
     p.set_schedule("depth")
     assert np.array_equal(p.execute(dev(A), dev(B)).cpu().numpy(), bf)
+    p.set_schedule("hybrid")  # root S / T at once, root (+ level 1) combination at the end
+    assert np.array_equal(p.execute(dev(A), dev(B)).cpu().numpy(), bf)
     p.set_schedule("auto")
     parts = []
     for rank in range(3):
@@ -273,7 +275,7 @@ def test_empty_and_degenerate(fb):
     assert np.array_equal(run(fb, ("strassen",) * 3, I, I), I)
 
 
-@pytest.mark.parametrize("schedule", ["breadth", "depth"])
+@pytest.mark.parametrize("schedule", ["breadth", "depth", "hybrid"])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_execute_host_overlapped(fb, schedule, dtype):
     # fmm_execute_host (pinned host buffers; the depth-first schedule overlaps block copies with
