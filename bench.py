@@ -385,6 +385,9 @@ def run_fmm(args):
         scaling = {"mode": args.scaling, "tau": 1.0, "max_steps": 20, "pow2": 1}
     plan = fb.Plan([fb.Rule.builtin(r) for r in rules], M, K, N, dtype=args.dtype, leaf=leaf,
                    scaling=scaling)
+    if args.shard_depth <= 0:  # auto: 49 depth-2 units balance 2 and 4 ranks (98 / 94 % vs
+        # 87.5 % with the 7 top-level products); 8 ranks gain nothing from depth 2 (7 / 6.125)
+        args.shard_depth = 2 if ws in (2, 4) else 1
     if ws > 1 and args.shard_depth > 1:
         plan.set_shard_depth(args.shard_depth)
     if ws > 1 and args.comm != "reduce":
@@ -621,7 +624,7 @@ def run_fmm(args):
                                    f"N={N} {args.dtype.upper()}, {cfgd.dist} seed {cfgd.seed} "
                                    f"(BASELINE configs[{ {'C1': 0, 'C2': 1, 'C2c': 1, 'C3': 2, 'C4': 3, 'C5': 4}[args.config] }])"
                                    + (f", scaling {args.scaling} (pow2, tau=1)" if args.scaling != "none" else ""),
-                       "parallelism": (f"top-level r round-robin over {ws} GPU(s)" if args.shard_depth == 1
+                       "parallelism": (f"top-level r round-robin over {ws} GPU(s)" if args.shard_depth <= 1
                                        else f"depth-{args.shard_depth} paths round-robin over {ws} GPU(s)")
                                       + (f", {args.comm} of C" if ws > 1 else ""),
                        "l2": ("operands %.1f GiB each > 126 MB L2 (no flush needed)" % (M * K * esz / 2**30))
@@ -652,8 +655,9 @@ def main():
                     help="CUDA-graph replay of each step (auto: on for problems <= 4096^3)")
     ap.add_argument("--scaling", default="none",
                     choices=["none", "outside", "inside", "out_in", "in_out", "repeated"])
-    ap.add_argument("--shard-depth", type=int, default=1,
-                    help="multi-GPU units = paths of the first d levels (fmm_plan_set_shard_depth)")
+    ap.add_argument("--shard-depth", type=int, default=0,
+                    help="multi-GPU units = paths of the first d levels (fmm_plan_set_shard_depth); "
+                         "0 = auto (2 for 2 or 4 ranks, else 1)")
     ap.add_argument("--comm", default="reduce", choices=["reduce", "allreduce", "reduce_scatter"],
                     help="multi-GPU exchange of the partial C (fmm_plan_set_comm_mode)")
     ap.add_argument("--no-e2e", action="store_true")
