@@ -164,6 +164,20 @@ def test_ineligible_rules_fall_back(fb):
     assert p.launch_count() == n2 + 1
 
 
+@pytest.mark.parametrize("names", [("strassen",) * 4, ("winograd", "classical222", "strassen"),
+                                   ("classical222", "winograd", "winograd")])
+def test_hybrid_schedule_bitwise(fb, names):
+    # hybrid top level (root S / T at once, subtrees in turn, root + level-1 combination as one
+    # K3X2 at the end) against breadth-first, fused and unfused
+    L = len(names)
+    M, K, N = 2 ** L * 24, 2 ** L * 10, 2 ** L * 16
+    A, B = fi.random_pair(M, K, N, seed=L + 40)
+    for fusion in ("off", "on"):
+        Cb, _ = run(fb, names, A, B, 2, fusion=fusion, schedule="breadth")
+        Ch, _ = run(fb, names, A, B, 2, fusion=fusion, schedule="hybrid")
+        assert np.array_equal(Cb, Ch)
+
+
 def test_workspace_smaller(fb):
     w = fb.Rule.builtin("winograd")
     p = fb.Plan([w] * 3, 4096, 4096, 4096)

@@ -105,9 +105,10 @@ def test_castrapel_gustafson_nonuniform_plan(fb):
     for (M, K, N), check in (((256, 192, 128), "parity"), ((64, 4, 32), "bitwise")):
         A, B = fi.random_pair(M, K, N, seed=K)
         Co = oracle.fmm(A, B, oplan)
-        for fusion in ("off", "on"):
+        for fusion, sched in (("off", "auto"), ("on", "auto"), ("on", "hybrid"), ("off", "depth")):
             p = fb.Plan(nodes, M, K, N, uniform=False, levels=2)
             p.set_fusion(fusion)
+            p.set_schedule(sched)
             Cg = p.execute(dev(A), dev(B)).cpu().numpy()
             if check == "parity":
                 assert oracle.parity_metric(Cg, Co, np.abs(A).max(), np.abs(B).max(), K) <= TOL64
