@@ -199,13 +199,8 @@ struct Builder {
   explicit Builder(fmm_plan* pl) : p(pl) { align_elems = 256 / elem_size(pl->dtype); }
 
   int64_t ws_alloc(int64_t elems) {
-    static const int64_t skew = [] {  // experiments: extra bytes between workspace blocks
-      const char* e = getenv("FMM_WS_SKEW");
-      return e ? (int64_t)atoll(e) : (int64_t)0;
-    }();
     int64_t off = ws_elems;
     ws_elems += (elems + align_elems - 1) / align_elems * align_elems;
-    if (skew > 0) ws_elems += (skew / elem_size(p->dtype) + align_elems - 1) / align_elems * align_elems;
     ws_peak = std::max(ws_peak, ws_elems);
     return off;
   }
