@@ -39,6 +39,8 @@ def test_padded_parity(fb, dims, names, fusion):
     assert Cg.shape == (M, N)
     Co = oracle.fmm(A, B, OPlan.uniform([R.builtin(n) for n in names]))
     assert oracle.parity_metric(Cg, Co, np.abs(A).max(), np.abs(B).max(), K) <= TOL64
+    p.set_schedule("hybrid")  # padding wraps any schedule
+    assert np.array_equal(p.execute(dev(A), dev(B)).cpu().numpy(), Cg)
 
 
 @pytest.mark.parametrize("fusion", ["off", "on"])

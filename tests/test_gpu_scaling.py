@@ -100,6 +100,10 @@ def test_scaled_fmm_C4_recipe(fb, mode):
     assert oracle.parity_metric(Cg, Co, np.abs(A).max(), np.abs(B).max(), K) <= 1e-13
     if mode == "repeated":
         assert rel(Cg) < 1e-10  # repeated O-I is accurate on this skew
+    # the scaling wraps any schedule: depth-first and hybrid top levels give the same bits
+    for sched in ("depth", "hybrid"):
+        p.set_schedule(sched)
+        assert np.array_equal(host(p.execute(dev(A), dev(B))), Cg), sched
 
 
 @pytest.mark.parametrize("pow2", [True, False])
