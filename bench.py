@@ -386,8 +386,9 @@ def run_fmm(args):
     plan = fb.Plan([fb.Rule.builtin(r) for r in rules], M, K, N, dtype=args.dtype, leaf=leaf,
                    scaling=scaling)
     if args.shard_depth <= 0:  # auto: 49 depth-2 units balance 2 and 4 ranks (98 / 94 % vs
-        # 87.5 % with the 7 top-level products); 8 ranks gain nothing from depth 2 (7 / 6.125)
-        args.shard_depth = 2 if ws in (2, 4) else 1
+        # 87.5 % with the 7 top-level products); 8 ranks gain nothing from depth 2 (7 / 6.125);
+        # the fused NVLink combine works on the top-level products (depth 1)
+        args.shard_depth = 2 if ws in (2, 4) and args.comm != "p2p" else 1
     if ws > 1 and args.shard_depth > 1:
         plan.set_shard_depth(args.shard_depth)
     if ws > 1 and args.comm != "reduce":
@@ -396,6 +397,10 @@ def run_fmm(args):
         uid = [fb.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, 0)
         plan.set_comm(uid[0], rank, ws)
+        if args.comm == "p2p":  # symmetric product buffers, CUDA IPC handles exchanged
+            handles = [None] * ws
+            dist.all_gather_object(handles, plan.sym_alloc())
+            plan.set_peer_handles(handles)
     wsp = plan.workspace(A.device)
     use_graph = args.graph == "on" or (args.graph == "auto" and M * N * K <= 4096 ** 3 and ws == 1)
     if use_graph:
@@ -545,7 +550,11 @@ def run_fmm(args):
     # copies the reduced C out, every step.
     e2e = None
     if not args.no_e2e:
-        C_h = torch.empty((M, N), dtype=dt).pin_memory() if rank == 0 else None
+        # distributed C (reduce_scatter, p2p): every rank copies out its own rows
+        dist_c = ws > 1 and args.comm in ("reduce_scatter", "p2p")
+        r0, r1 = (M * rank // ws, M * (rank + 1) // ws) if dist_c else (0, M)
+        C_h = (torch.empty((r1 - r0, N), dtype=dt).pin_memory() if (rank == 0 or dist_c)
+               else None)
 
         def e2e_serial(nsteps, warm):
             for it in range(warm + nsteps):
@@ -565,8 +574,8 @@ def run_fmm(args):
                         dist.broadcast(A, 0)
                         dist.broadcast(B, 0)
                         step()
-                        if rank == 0:
-                            C_h.copy_(Cd, non_blocking=True)
+                        if rank == 0 or dist_c:
+                            C_h.copy_(Cd[r0:r1], non_blocking=True)
             f1.record(stream)
             torch.cuda.synchronize()
             return f0.elapsed_time(f1)
@@ -658,8 +667,9 @@ def main():
     ap.add_argument("--shard-depth", type=int, default=0,
                     help="multi-GPU units = paths of the first d levels (fmm_plan_set_shard_depth); "
                          "0 = auto (2 for 2 or 4 ranks, else 1)")
-    ap.add_argument("--comm", default="reduce", choices=["reduce", "allreduce", "reduce_scatter"],
-                    help="multi-GPU exchange of the partial C (fmm_plan_set_comm_mode)")
+    ap.add_argument("--comm", default="reduce", choices=["reduce", "allreduce", "reduce_scatter", "p2p"],
+                    help="multi-GPU exchange (fmm_plan_set_comm_mode): NCCL on the partial C, or "
+                         "p2p = the fused NVLink W-combination of the peers' top-level products")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-warmup", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")

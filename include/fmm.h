@@ -228,8 +228,35 @@ fmm_status fmm_plan_set_shard_depth(fmm_plan* plan, int depth);
  * 1 = ncclAllReduce(sum) (C valid on every rank);
  * 2 = ncclReduceScatter(sum), in place: rank r's C holds the finished rows
  *     [r M / P, (r + 1) M / P) (M divisible by P, else FMM_E_SHAPE) -- a distributed C at
- *     1 / P of the reduce's per-rank output traffic. */
+ *     1 / P of the reduce's per-rank output traffic;
+ * 3 = fused NVLink combine: each rank writes its owned top-level products
+ *     M_r (r = rank mod P, shard depth 1) into its symmetric buffer (fmm_plan_sym_alloc), and
+ *     after a device-side barrier (1-word ncclAllReduce) rank q computes rows
+ *     [q M / P, (q + 1) M / P) of C = sum_r w_kr M_r (Eq. eqn:recursive_alg) with one
+ *     kernel that loads the peers' products over NVLink (CUDA IPC, fmm_plan_set_peer_handles):
+ *     the W-combination and the exchange in one pass, no partial C, and the same summation
+ *     order as one GPU (bitwise the single-GPU rows).  A second barrier follows.  Needs no
+ *     padding and no scaling (FMM_E_ARG at execute).  Mode 3 recompiles the plan (its schedule
+ *     differs). */
 fmm_status fmm_plan_set_comm_mode(fmm_plan* plan, int mode);
+
+/* Comm mode 3 buffers.  fmm_plan_sym_bytes: size of this rank's symmetric buffer (ceil(R / P)
+ * top-level products of lm[1] x ln[1], slot r / P, plus 256 bytes of barrier scratch).
+ * fmm_plan_sym_alloc: cudaMalloc it on the current device (owned by the plan, freed with it)
+ * and write its 64-byte CUDA IPC handle to `handle`.  fmm_plan_sym_ptr: its device address.
+ * fmm_plan_set_peer_handles: `handles` = n = nranks consecutive 64-byte handles in rank order
+ * (this rank's own is not opened); the plan opens the others (cudaIpcOpenMemHandle) and keeps
+ * the UVA pointer table.  FMM_E_ARG / FMM_E_CUDA on failure. */
+fmm_status fmm_plan_sym_bytes(const fmm_plan* plan, size_t* bytes);
+fmm_status fmm_plan_sym_alloc(fmm_plan* plan, void* handle);
+fmm_status fmm_plan_sym_ptr(const fmm_plan* plan, void** ptr);
+fmm_status fmm_plan_set_peer_handles(fmm_plan* plan, const void* handles, int n);
+
+/* Building block of comm mode 3 (tests, tools): rows [row0, row1) of C (ldc) =
+ * sum_r w_kr M_r with M_r at peer_ptrs[r % n] + (r / n) * lm[1] * ln[1] (device pointers:
+ * host array of n).  Enqueued on `stream`. */
+fmm_status fmm_plan_p2p_combine(fmm_plan* plan, const void* const* peer_ptrs, int n, void* C,
+                                int64_t ldc, int64_t row0, int64_t row1, void* stream);
 
 /* Host-only query: owned[u] = 1 if shard unit u is computed by `rank`; *R receives the number
  * of units (the top-level rank R at shard depth 1). */

@@ -167,6 +167,14 @@ struct fmm_plan {
   mutable std::mutex tmu;
   mutable std::vector<cudaEvent_t> ev_pool;
   mutable std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_used;
+  // comm mode 3 (fused NVLink combine): this rank's symmetric buffer of owned top-level
+  // products (library-allocated, exported by CUDA IPC) and every rank's buffer as a UVA pointer
+  void* sym_own = nullptr;
+  size_t sym_alloc_bytes = 0;
+  std::vector<void*> peers;          // [nranks]; peers[rank] = sym_own, others IPC-opened
+  std::vector<bool> peer_opened;
+  void* dev_peers = nullptr;         // device copy of peers
+  void* dev_tmp_peers = nullptr;     // fmm_plan_p2p_combine's pointer table
   ~fmm_plan();
 };
 
@@ -180,6 +188,11 @@ fmm_plan::~fmm_plan() {
   if (dev_coef) cudaFree(dev_coef);
   if (dev_desc) cudaFree(dev_desc);
   if (comm && nccl() && nccl()->commDestroy) nccl()->commDestroy(comm);
+  for (size_t q = 0; q < peers.size(); ++q)
+    if (q < peer_opened.size() && peer_opened[q] && peers[q]) cudaIpcCloseMemHandle(peers[q]);
+  if (dev_peers) cudaFree(dev_peers);
+  if (dev_tmp_peers) cudaFree(dev_tmp_peers);
+  if (sym_own) cudaFree(sym_own);
 }
 
 namespace {
@@ -767,6 +780,8 @@ struct Builder {
     depth_first(0, root, 0);
   }
 
+  bool p2p_mode() const { return p->comm_mode == 3 && p->nranks > 1 && p->shard_depth == 1; }
+
   static bool hybrid_on() {
     const char* e = getenv("FMM_HYBRID");
     return !e || atoi(e) != 0;
@@ -838,9 +853,16 @@ struct Builder {
       if (!owns_subtree(l + 1, unit)) continue;
       ws_elems = mark;  // subtrees run one after another on one stream: reuse the workspace
       const size_t g0 = p->steps.size();
-      const bool fuse1 = leaf_next && fuse_leaves(1);
-      std::vector<Node> kid = emit_k1(l, {node}, r, !fuse1, fuse1 && opf_on());
-      if (fuse1) {
+      // comm mode 3: the top-level product M_r goes to this rank's symmetric buffer (slot
+      // r / nranks) for the fused NVLink combine; no ACC into a partial C
+      const bool p2p = l == 0 && p2p_mode();
+      const bool fuse1 = leaf_next && !p2p && fuse_leaves(1);
+      std::vector<Node> kid = emit_k1(l, {node}, r, !fuse1 && !p2p, fuse1 && opf_on());
+      if (p2p) {
+        kid[0].c = Op{BASE_SYM, 0, (int64_t)(r / p->nranks) * p->lm[1], 0, p->ln[1]};
+        if (leaf_next) emit_k2(kid);
+        else breadth_first(1, kid);
+      } else if (fuse1) {
         emit_k2f(l, {node}, kid, r, &started);
       } else {
         if (leaf_next) emit_k2(kid);
@@ -864,7 +886,7 @@ struct Builder {
       if (l == 0) p->groups.push_back({r, g0, p->steps.size()});
     }
     const uint32_t all = (ru.m0 * ru.n0 >= 32) ? 0xffffffffu : ((1u << (ru.m0 * ru.n0)) - 1u);
-    if ((started & all) != all) {
+    if ((started & all) != all && !(l == 0 && p2p_mode())) {
       std::vector<ZeroNode> z{ZeroNode{node.c, all & ~started, 0}};
       Step st{};
       st.kind = STEP_ZERO; st.count = 1; st.dev_off = push(z);
@@ -1369,9 +1391,109 @@ fmm_status fmm_plan_fused_launches(const fmm_plan* p, int64_t* n) {
 }
 
 fmm_status fmm_plan_set_comm_mode(fmm_plan* p, int mode) {
-  if (!p || mode < 0 || mode > 2) { set_error("fmm_plan_set_comm_mode: mode must be 0, 1 or 2"); return FMM_E_ARG; }
+  if (!p || mode < 0 || mode > 3) { set_error("fmm_plan_set_comm_mode: mode must be 0, 1, 2 or 3"); return FMM_E_ARG; }
+  const bool recompile = (mode == 3) != (p->comm_mode == 3);  // mode 3 changes the schedule
   p->comm_mode = mode;
+  return recompile ? compile_plan(p) : FMM_OK;
+}
+
+static size_t sym_bytes_of(const fmm_plan* p) {
+  if (p->L == 0 || p->nranks < 1) return 0;
+  const int R = p->rules[p->node_rule[0][0]].R;
+  const int64_t slots = (R + p->nranks - 1) / p->nranks;
+  return (size_t)slots * p->lm[1] * p->ln[1] * elem_size(p->dtype) + 256;  // + barrier scratch
+}
+
+fmm_status fmm_plan_sym_bytes(const fmm_plan* p, size_t* bytes) {
+  if (!p || !bytes) { set_error("fmm_plan_sym_bytes: null"); return FMM_E_ARG; }
+  *bytes = sym_bytes_of(p);
   return FMM_OK;
+}
+
+fmm_status fmm_plan_sym_alloc(fmm_plan* p, void* handle) {
+  if (!p || !handle) { set_error("fmm_plan_sym_alloc: null"); return FMM_E_ARG; }
+  const size_t need = sym_bytes_of(p);
+  if (need == 0) { set_error("fmm_plan_sym_alloc: no top-level products"); return FMM_E_ARG; }
+  cudaError_t e = cudaSuccess;
+  if (!p->sym_own || p->sym_alloc_bytes < need) {
+    if (p->sym_own) cudaFree(p->sym_own);
+    p->sym_own = nullptr;
+    e = cudaMalloc(&p->sym_own, need);  // its own allocation: the IPC handle maps exactly it
+    if (e != cudaSuccess) return cuda_status(e, "fmm_plan_sym_alloc");
+    p->sym_alloc_bytes = need;
+  }
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, p->sym_own);
+  if (e != cudaSuccess) return cuda_status(e, "fmm_plan_sym_alloc (IPC handle)");
+  std::memcpy(handle, &h, sizeof h);
+  return FMM_OK;
+}
+
+fmm_status fmm_plan_sym_ptr(const fmm_plan* p, void** ptr) {
+  if (!p || !ptr) { set_error("fmm_plan_sym_ptr: null"); return FMM_E_ARG; }
+  *ptr = p->sym_own;
+  return FMM_OK;
+}
+
+static fmm_status upload_peers(const std::vector<void*>& ptrs, void** dev) {
+  if (!*dev) {
+    cudaError_t e = cudaMalloc(dev, sizeof(void*) * 64);
+    if (e != cudaSuccess) return cuda_status(e, "peer table");
+  }
+  if (ptrs.size() > 64) { set_error("more than 64 ranks"); return FMM_E_ARG; }
+  return cuda_status(cudaMemcpy(*dev, ptrs.data(), sizeof(void*) * ptrs.size(), cudaMemcpyHostToDevice),
+                     "peer table");
+}
+
+fmm_status fmm_plan_set_peer_handles(fmm_plan* p, const void* handles, int n) {
+  if (!p || !handles || n != p->nranks || n < 1) { set_error("fmm_plan_set_peer_handles: bad args (n must equal nranks)"); return FMM_E_ARG; }
+  if (!p->sym_own) { set_error("fmm_plan_set_peer_handles: call fmm_plan_sym_alloc first"); return FMM_E_ARG; }
+  for (size_t q = 0; q < p->peers.size(); ++q)
+    if (q < p->peer_opened.size() && p->peer_opened[q] && p->peers[q]) cudaIpcCloseMemHandle(p->peers[q]);
+  p->peers.assign(n, nullptr);
+  p->peer_opened.assign(n, false);
+  for (int q = 0; q < n; ++q) {
+    if (q == p->rank) { p->peers[q] = p->sym_own; continue; }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, (const uint8_t*)handles + (size_t)q * sizeof h, sizeof h);
+    cudaError_t e = cudaIpcOpenMemHandle(&p->peers[q], h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_status(e, "fmm_plan_set_peer_handles (cudaIpcOpenMemHandle)");
+    p->peer_opened[q] = true;
+  }
+  return upload_peers(p->peers, &p->dev_peers);
+}
+
+}  // extern "C"
+
+template <typename T>
+static fmm_status p2p_combine(const fmm_plan* p, const void* dev_table, int n, void* C, int64_t ldc,
+                              int64_t row0, int64_t row1, cudaStream_t st) {
+  const RuleData& ru = p->rules[p->node_rule[0][0]];
+  const int vecn = 16 / (int)sizeof(T);
+  const bool vec = p->dims_vec_ok && aligned16(C) && ldc % vecn == 0;
+  TimedLaunch tl(p, 7, st);
+  return cuda_status(launch_p2p_combine<T>((const T* const*)dev_table, n, p->dev_coef,
+                                           p->coef_W[p->node_rule[0][0]], ru.R, ru.m0, ru.n0,
+                                           p->lm[1], p->ln[1], (T*)C, ldc, row0, row1, vec, st),
+                     "p2p combine");
+}
+
+extern "C" {
+
+fmm_status fmm_plan_p2p_combine(fmm_plan* p, const void* const* peer_ptrs, int n, void* C,
+                                int64_t ldc, int64_t row0, int64_t row1, void* stream) {
+  if (!p || !peer_ptrs || !C || n < 1 || p->L == 0 || ldc < p->N || row0 < 0 || row1 > p->M || row0 > row1) {
+    set_error("fmm_plan_p2p_combine: bad args");
+    return FMM_E_ARG;
+  }
+  if (p->padded || p->scaling.mode != FMM_SCALE_NONE) { set_error("fmm_plan_p2p_combine: not for padded or scaled plans"); return FMM_E_ARG; }
+  fmm_status fs = ensure_device(p);
+  if (fs != FMM_OK) return fs;
+  std::vector<void*> v(n);
+  for (int q = 0; q < n; ++q) v[q] = const_cast<void*>(peer_ptrs[q]);
+  if ((fs = upload_peers(v, &p->dev_tmp_peers)) != FMM_OK) return fs;
+  return p->dtype == FMM_F64 ? p2p_combine<double>(p, p->dev_tmp_peers, n, C, ldc, row0, row1, (cudaStream_t)stream)
+                             : p2p_combine<float>(p, p->dev_tmp_peers, n, C, ldc, row0, row1, (cudaStream_t)stream);
 }
 
 fmm_status fmm_plan_set_shard_depth(fmm_plan* p, int depth) {
@@ -1484,6 +1606,15 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
   b.p[BASE_A] = A; b.p[BASE_B] = B; b.p[BASE_C] = C;
   b.p[BASE_WS] = wsb + p->scale_bytes + p->pad_bytes;
   b.ld[BASE_A] = lda; b.ld[BASE_B] = ldb; b.ld[BASE_C] = ldc; b.ld[BASE_WS] = 0;
+  b.p[BASE_SYM] = p->sym_own; b.ld[BASE_SYM] = p->L > 0 ? p->ln[1] : 0;
+  const bool p2p = p->comm_mode == 3 && p->nranks > 1 && p->L > 0;
+  if (p2p) {
+    if (p->shard_depth != 1 || p->padded || p->scaling.mode != FMM_SCALE_NONE) {
+      set_error("fmm_execute: comm mode 3 needs shard depth 1, no padding and no scaling");
+      return FMM_E_ARG;
+    }
+    if (!p->sym_own) { set_error("fmm_execute: comm mode 3 needs fmm_plan_sym_alloc"); return FMM_E_ARG; }
+  }
   double *dA = nullptr, *dB = nullptr;
   if (p->scaling.mode != FMM_SCALE_NONE) {
     double* Ap = (double*)wsb;
@@ -1539,7 +1670,26 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
     cudaError_t e = launch_unscale((double*)C, ldc, p->M, p->N, dA, dB, st);
     if (e != cudaSuccess) return cuda_status(e, "fmm_execute unscale");
   }
-  if (p->comm && p->nranks > 1) {
+  if (p2p && p->comm) {
+    // every rank's owned M_r is in its symmetric buffer once all ranks pass this point; a 1-word
+    // all-reduce orders the streams (device-side barrier), then rank q computes rows
+    // [q M/P, (q+1) M/P) of C reading the products over NVLink, then a second barrier keeps the
+    // next call from overwriting products a peer is still reading
+    NcclApi* api = nccl();
+    if (!api || !api->allreduce) { set_error("NCCL not loadable"); return FMM_E_NCCL; }
+    if (p->peers.size() != (size_t)p->nranks || !p->dev_peers) { set_error("fmm_execute: comm mode 3 needs fmm_plan_set_peer_handles"); return FMM_E_ARG; }
+    float* bar = (float*)((uint8_t*)p->sym_own + sym_bytes_of(p) - 256);
+    ncclResult_t r = api->allreduce(bar, bar, 1, ncclFloat32_, ncclSum_, p->comm, st);
+    if (r != 0) { set_error("ncclAllReduce (barrier)"); return FMM_E_NCCL; }
+    const int64_t row0 = p->M * p->rank / p->nranks, row1 = p->M * (p->rank + 1) / p->nranks;
+    fmm_status cs = p->dtype == FMM_F64 ? p2p_combine<double>(p, p->dev_peers, p->nranks, C, ldc, row0, row1, st)
+                                        : p2p_combine<float>(p, p->dev_peers, p->nranks, C, ldc, row0, row1, st);
+    if (cs != FMM_OK) return cs;
+    r = api->allreduce(bar + 1, bar + 1, 1, ncclFloat32_, ncclSum_, p->comm, st);
+    if (r != 0) { set_error("ncclAllReduce (barrier)"); return FMM_E_NCCL; }
+    return FMM_OK;
+  }
+  if (p->comm && p->nranks > 1 && !p2p) {
     NcclApi* api = nccl();
     if (!api) { set_error("NCCL not loadable"); return FMM_E_NCCL; }
     if (ldc != p->N) { set_error("fmm_execute: multi-GPU reduce needs ldc == N"); return FMM_E_ARG; }

@@ -20,7 +20,8 @@ namespace fmm {
 constexpr int kMaxBlk = 16;  // max m0*k0, k0*n0, m0*n0 of a rule
 constexpr int kMaxR = 32;    // max rank R of a rule
 
-enum BaseId : int32_t { BASE_A = 0, BASE_B = 1, BASE_C = 2, BASE_WS = 3 };
+// BASE_SYM: this rank's symmetric (peer-readable) buffer of top-level products (comm mode 3)
+enum BaseId : int32_t { BASE_A = 0, BASE_B = 1, BASE_C = 2, BASE_WS = 3, BASE_SYM = 4 };
 
 struct Op {
   int32_t base;
@@ -29,8 +30,8 @@ struct Op {
 };
 
 struct Bases {
-  const void* p[4];
-  int64_t ld[4];
+  const void* p[5];
+  int64_t ld[5];
 };
 
 // Selects instead of b.p[o.base]: dynamic indexing of a by-value kernel parameter would force
@@ -38,8 +39,8 @@ struct Bases {
 template <typename T>
 __host__ __device__ inline T* op_ptr(const Bases& b, const Op& o, int64_t& ld) {
   const int id = o.base;
-  const void* base = id == 0 ? b.p[0] : id == 1 ? b.p[1] : id == 2 ? b.p[2] : b.p[3];
-  const int64_t bld = id == 0 ? b.ld[0] : id == 1 ? b.ld[1] : id == 2 ? b.ld[2] : b.ld[3];
+  const void* base = id == 0 ? b.p[0] : id == 1 ? b.p[1] : id == 2 ? b.p[2] : id == 3 ? b.p[3] : b.p[4];
+  const int64_t bld = id == 0 ? b.ld[0] : id == 1 ? b.ld[1] : id == 2 ? b.ld[2] : id == 3 ? b.ld[3] : b.ld[4];
   ld = o.ld >= 0 ? o.ld : bld;
   return (T*)base + o.row0 * ld + o.col0;
 }
@@ -224,6 +225,14 @@ cudaError_t launch_acc(const Step& s, const void* dev_nodes, const double* dev_c
                        const Bases& b, bool vec, cudaStream_t st);
 template <typename T>
 cudaError_t launch_zero(const Step& s, const void* dev_nodes, const Bases& b, cudaStream_t st);
+
+// Comm mode 3 (fused NVLink combine): rows [row0, row1) of C (M x N, ldc; blocks k = ia*N0 + jb
+// of mb x nb) = sum_r ascending w_kr M_r, M_r read from peers[r % P] + (r / P) * mb * nb
+// (each rank's symmetric buffer holds its owned products, slot r / P, dense mb x nb).
+template <typename T>
+cudaError_t launch_p2p_combine(const T* const* dev_peers, int P, const double* dev_coef, int coef_off,
+                               int R, int M0, int N0, int64_t mb, int64_t nb, T* C, int64_t ldc,
+                               int64_t row0, int64_t row1, bool vec, cudaStream_t st);
 
 // dst (rows_p x cols_p, ldd) = src (rows x cols, lds) zero-extended (rows <= rows_p, cols <=
 // cols_p): the zero padding / cropping of non-divisible dims

@@ -872,6 +872,49 @@ cudaError_t launch_zero(const Step& s, const void* dev_nodes, const Bases& b, cu
 }
 
 namespace {
+// One thread per VEC-vector of a C row: block k = ia * N0 + jb of the element, then the
+// sequential sum over r ascending of w_kr M_r (first term initialises) -- ACC's order, so the
+// result is bitwise the single-GPU C.  Peer pointers are UVA addresses of the other ranks'
+// symmetric buffers (CUDA IPC), so the loads of non-local products travel over NVLink.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(kThreads) k_p2p_combine(const T* const* __restrict__ peers, int P,
+                                                          const double* __restrict__ coef, int R,
+                                                          int nw, int N0, int64_t mb, int64_t nb,
+                                                          T* C, int64_t ldc, int64_t row0,
+                                                          int64_t row1) {
+  __shared__ double w[kMaxBlk * kMaxR];
+  __shared__ const T* src[kMaxR];
+  for (int t = threadIdx.x; t < nw; t += blockDim.x) w[t] = coef[t];
+  if (threadIdx.x < R) src[threadIdx.x] = peers[threadIdx.x % P] + (int64_t)(threadIdx.x / P) * mb * nb;
+  __syncthreads();
+  const int64_t j = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * VEC;
+  if (j >= (int64_t)N0 * nb) return;
+  const int jb = (int)(j / nb);
+  const int64_t jj = j % nb;
+  for (int64_t i = row0 + blockIdx.y; i < row1; i += gridDim.y) {
+    const int ia = (int)(i / mb);
+    const int64_t ii = i % mb;
+    const int k = ia * N0 + jb;
+    Vec<T, VEC> acc;
+    bool started = false;
+    for (int r = 0; r < R; ++r) {
+      const double wk = w[k * R + r];
+      if (wk == 0.0) continue;
+      const Vec<T, VEC> m = ld_vec<T, VEC>(src[r] + ii * nb + jj);
+      const T wt = (T)wk;
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        acc.v[e] = started ? add_rn<T>(acc.v[e], mul_rn<T>(wt, m.v[e])) : mul_rn<T>(wt, m.v[e]);
+      started = true;
+    }
+    if (!started) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) acc.v[e] = (T)0;
+    }
+    st_vec<T, VEC>(C + i * ldc + j, acc);
+  }
+}
+
 template <typename T>
 __global__ void k_pad_copy(const T* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
                            T* __restrict__ dst, int64_t rows_p, int64_t cols_p, int64_t ldd) {
@@ -891,6 +934,24 @@ cudaError_t launch_pad_copy(const T* src, int64_t rows, int64_t cols, int64_t ld
   return cudaGetLastError();
 }
 
+template <typename T>
+cudaError_t launch_p2p_combine(const T* const* dev_peers, int P, const double* dev_coef, int coef_off,
+                               int R, int M0, int N0, int64_t mb, int64_t nb, T* C, int64_t ldc,
+                               int64_t row0, int64_t row1, bool vec, cudaStream_t st) {
+  if (row1 <= row0 || nb == 0) return cudaSuccess;
+  constexpr int V = 16 / sizeof(T);
+  const int vv = vec ? V : 1;
+  const int64_t cv = (N0 * nb + vv - 1) / vv;
+  dim3 grid((unsigned)((cv + kThreads - 1) / kThreads), (unsigned)std::min<int64_t>(row1 - row0, 65535));
+  if (vec)
+    k_p2p_combine<T, V><<<grid, kThreads, 0, st>>>(dev_peers, P, dev_coef + coef_off, R, M0 * N0 * R, N0, mb, nb, C, ldc, row0, row1);
+  else
+    k_p2p_combine<T, 1><<<grid, kThreads, 0, st>>>(dev_peers, P, dev_coef + coef_off, R, M0 * N0 * R, N0, mb, nb, C, ldc, row0, row1);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_p2p_combine<double>(const double* const*, int, const double*, int, int, int, int, int64_t, int64_t, double*, int64_t, int64_t, int64_t, bool, cudaStream_t);
+template cudaError_t launch_p2p_combine<float>(const float* const*, int, const double*, int, int, int, int, int64_t, int64_t, float*, int64_t, int64_t, int64_t, bool, cudaStream_t);
 template cudaError_t launch_pad_copy<double>(const double*, int64_t, int64_t, int64_t, double*, int64_t, int64_t, int64_t, cudaStream_t);
 template cudaError_t launch_pad_copy<float>(const float*, int64_t, int64_t, int64_t, float*, int64_t, int64_t, int64_t, cudaStream_t);
 template cudaError_t launch_k1<double>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);

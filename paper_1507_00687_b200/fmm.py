@@ -48,6 +48,11 @@ SIGNATURES = {
     "fmm_rule_transform": (_I, [_P, _I, C.POINTER(_P)]),
     "fmm_plan_set_operand_fusion": (_I, [_P, _I]),
     "fmm_plan_set_k1_levels": (_I, [_P, _I]),
+    "fmm_plan_sym_bytes": (_I, [_P, _P]),
+    "fmm_plan_sym_alloc": (_I, [_P, _P]),
+    "fmm_plan_sym_ptr": (_I, [_P, _P]),
+    "fmm_plan_set_peer_handles": (_I, [_P, _P, _I]),
+    "fmm_plan_p2p_combine": (_I, [_P, _P, _I, _P, _I64, _I64, _I64, _P]),
     "fmm_plan_set_k3_levels": (_I, [_P, _I]),
     "fmm_scale_apply": (_I, [_I, _I64, _I64, _I64, _P, _I64, _P, _I64, _P, _P, _P, _P, _I64, _P, _I64, _P]),
     "fmm_rule_quantities": (_I, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_double), C.POINTER(C.c_double), _P, _P]),
@@ -326,8 +331,39 @@ class Plan:
         return n.value
 
     def set_comm_mode(self, mode: str):
-        """Multi-GPU exchange: 'reduce' (C on rank 0), 'allreduce', 'reduce_scatter' (rows)."""
-        _call("fmm_plan_set_comm_mode", self._h, {"reduce": 0, "allreduce": 1, "reduce_scatter": 2}[mode])
+        """Multi-GPU exchange: 'reduce' (C on rank 0), 'allreduce', 'reduce_scatter' (rows), or
+        'p2p' (fused NVLink combine of the peers' top-level products into this rank's rows)."""
+        _call("fmm_plan_set_comm_mode", self._h,
+              {"reduce": 0, "allreduce": 1, "reduce_scatter": 2, "p2p": 3}[mode])
+        self._ws = None
+
+    def sym_bytes(self) -> int:
+        n = C.c_size_t()
+        _call("fmm_plan_sym_bytes", self._h, C.byref(n))
+        return n.value
+
+    def sym_alloc(self) -> bytes:
+        """Allocate this rank's symmetric product buffer; returns its 64-byte CUDA IPC handle."""
+        h = C.create_string_buffer(64)
+        _call("fmm_plan_sym_alloc", self._h, h)
+        return h.raw
+
+    def sym_ptr(self) -> int:
+        v = C.c_void_p()
+        _call("fmm_plan_sym_ptr", self._h, C.byref(v))
+        return v.value or 0
+
+    def set_peer_handles(self, handles):
+        """Every rank's sym_alloc() handle, in rank order."""
+        buf = b"".join(handles)
+        _call("fmm_plan_set_peer_handles", self._h, C.c_char_p(buf), len(handles))
+
+    def p2p_combine(self, peer_ptrs, C_out, row0: int, row1: int, stream=None):
+        """Rows [row0, row1) of C = sum_r w_kr M_r from the products at peer_ptrs (building block)."""
+        arr = (C.c_void_p * len(peer_ptrs))(*peer_ptrs)
+        _call("fmm_plan_p2p_combine", self._h, arr, len(peer_ptrs), C.c_void_p(C_out.data_ptr()),
+              C_out.stride(0), row0, row1, _stream(stream))
+        return C_out
 
     def set_shard_depth(self, depth: int):
         """Multi-GPU units = paths of the first `depth` levels (fmm_plan_set_shard_depth)."""

@@ -213,3 +213,19 @@ def test_hybrid_schedule_structure():
     assert big.launch_count() != 1 + 7 * 2 + 1
     with pytest.raises(fb.FmmError):
         fb.fmm._call("fmm_plan_set_schedule", p._h, 4)
+
+
+def test_p2p_comm_mode_schedule():
+    # comm mode 3: owned top-level products go to the symmetric buffer (no ACC into a partial
+    # C, no zeroing); its size is ceil(R / P) products plus the barrier scratch
+    w = fb.Rule.builtin("winograd")
+    p = fb.Plan([w, w], 512, 512, 512)
+    p.set_partition(0, 2)
+    n_reduce = p.launch_count()
+    p.set_comm_mode("p2p")
+    assert p.launch_count() == n_reduce - 4  # rank 0 owns r = 0, 2, 4, 6: four ACC launches
+    assert p.sym_bytes() == 4 * 256 * 256 * 8 + 256
+    p.set_comm_mode("reduce")
+    assert p.launch_count() == n_reduce
+    with pytest.raises(fb.FmmError):
+        fb.fmm._call("fmm_plan_set_comm_mode", p._h, 4)

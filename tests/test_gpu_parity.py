@@ -410,3 +410,49 @@ def test_execute_host_batch(fb, nbuf, shape, scaling):
         for c, w_ in zip(Ch, want):
             assert np.array_equal(c.numpy(), w_)
     p.execute_host_batch([], [], [], Ad, Bd, Cd)  # empty batch
+
+
+@pytest.mark.parametrize("names", [("winograd",), ("winograd",) * 2, ("strassen",) * 3,
+                                   ("winograd", "classical222")])
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_p2p_combine_virtual_ranks(fb, names, P):
+    # comm mode 3 on virtual ranks: each rank's plan writes its owned top-level products into
+    # its symmetric buffer; the combine over the P buffers (here local pointers standing in for
+    # the IPC-mapped peers) gives, row slice by row slice, exactly the single-GPU C (ascending r)
+    L = len(names)
+    M, K, N = 2 ** L * 40, 2 ** L * 24, 2 ** L * 32
+    A, B = fi.random_pair(M, K, N, seed=50 + L + P)
+    rules = [fb.Rule.builtin(n) for n in names]
+    ref = fb.Plan(rules, M, K, N).execute(dev(A), dev(B)).cpu().numpy()
+    plans, ptrs = [], []
+    for rank in range(P):
+        p = fb.Plan(rules, M, K, N)
+        p.set_partition(rank, P)
+        p.set_comm_mode("p2p")
+        R = rules[0].info()["R"]
+        assert p.sym_bytes() == -(-R // P) * (M >> 1) * (N >> 1) * 8 + 256
+        p.sym_alloc()
+        p.execute(dev(A), dev(B))  # no communicator: only the owned products, into the buffer
+        plans.append(p)
+        ptrs.append(p.sym_ptr())
+    torch.cuda.synchronize()
+    C = torch.full((M, N), float("nan"), dtype=torch.float64, device="cuda")
+    for rank in range(P):
+        plans[rank].p2p_combine(ptrs, C, M * rank // P, M * (rank + 1) // P)
+    torch.cuda.synchronize()
+    assert np.array_equal(C.cpu().numpy(), ref)
+
+
+def test_p2p_mode_errors(fb):
+    w = fb.Rule.builtin("winograd")
+    p = fb.Plan([w, w], 256, 256, 256)
+    p.set_partition(0, 2)
+    p.set_comm_mode("p2p")
+    with pytest.raises(fb.FmmError):  # no symmetric buffer
+        p.execute(dev(np.zeros((256, 256))), dev(np.zeros((256, 256))))
+    q = fb.Plan([w, w], 250, 256, 256)  # padded: not supported in mode 3
+    q.set_partition(0, 2)
+    q.set_comm_mode("p2p")
+    q.sym_alloc()
+    with pytest.raises(fb.FmmError):
+        q.execute(dev(np.zeros((250, 256))), dev(np.zeros((256, 256))))
