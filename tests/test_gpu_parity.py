@@ -383,6 +383,25 @@ def test_deep_recursion_node_chunks(fb, fusion):
     assert np.array_equal(p.execute(dev(Ai), dev(Bi)).cpu().numpy(), Ci)
 
 
+def test_execute_host_batch_f32_hybrid(fb):
+    # FP32 (3xTF32 leaves) through a hybrid-schedule plan (the host path uses its depth-first
+    # twin), a stream of 4 problems over 2 buffer sets
+    M = K = N = 512
+    w = fb.Rule.builtin("winograd")
+    p = fb.Plan([w, w, w], M, K, N, dtype="f32", leaf=fb.fmm.LEAF_3XTF32)
+    p.set_schedule("hybrid")
+    pairs = [fi.random_pair(M, K, N, seed=200 + i, dtype=np.float32) for i in range(4)]
+    want = [p.execute(dev(A), dev(B)).cpu().numpy() for A, B in pairs]
+    Ah = [torch.from_numpy(A).pin_memory() for A, _ in pairs]
+    Bh = [torch.from_numpy(B).pin_memory() for _, B in pairs]
+    Ch = [torch.empty((M, N), dtype=torch.float32).pin_memory() for _ in pairs]
+    dv = lambda r, c: [torch.empty((r, c), dtype=torch.float32, device="cuda") for _ in range(2)]
+    p.execute_host_batch(Ah, Bh, Ch, dv(M, K), dv(K, N), dv(M, N))
+    torch.cuda.synchronize()
+    for c, w_ in zip(Ch, want):
+        assert np.array_equal(c.numpy(), w_)
+
+
 @pytest.mark.parametrize("nbuf", [1, 2, 3])
 @pytest.mark.parametrize("shape,scaling", [((256, 512, 384), None), ((250, 130, 66), None),
                                            ((256, 256, 256), "repeated")])
@@ -412,31 +431,33 @@ def test_execute_host_batch(fb, nbuf, shape, scaling):
     p.execute_host_batch([], [], [], Ad, Bd, Cd)  # empty batch
 
 
-@pytest.mark.parametrize("names", [("winograd",), ("winograd",) * 2, ("strassen",) * 3,
-                                   ("winograd", "classical222")])
+@pytest.mark.parametrize("names,dtype", [(("winograd",), "f64"), (("winograd",) * 2, "f64"),
+                                         (("strassen",) * 3, "f64"), (("winograd", "classical222"), "f64"),
+                                         (("winograd",) * 2, "f32")])
 @pytest.mark.parametrize("P", [2, 3, 4])
-def test_p2p_combine_virtual_ranks(fb, names, P):
+def test_p2p_combine_virtual_ranks(fb, names, dtype, P):
     # comm mode 3 on virtual ranks: each rank's plan writes its owned top-level products into
     # its symmetric buffer; the combine over the P buffers (here local pointers standing in for
     # the IPC-mapped peers) gives, row slice by row slice, exactly the single-GPU C (ascending r)
     L = len(names)
     M, K, N = 2 ** L * 40, 2 ** L * 24, 2 ** L * 32
-    A, B = fi.random_pair(M, K, N, seed=50 + L + P)
+    npdt = np.float64 if dtype == "f64" else np.float32
+    A, B = fi.random_pair(M, K, N, seed=50 + L + P, dtype=npdt)
     rules = [fb.Rule.builtin(n) for n in names]
-    ref = fb.Plan(rules, M, K, N).execute(dev(A), dev(B)).cpu().numpy()
+    ref = fb.Plan(rules, M, K, N, dtype=dtype).execute(dev(A), dev(B)).cpu().numpy()
     plans, ptrs = [], []
     for rank in range(P):
-        p = fb.Plan(rules, M, K, N)
+        p = fb.Plan(rules, M, K, N, dtype=dtype)
         p.set_partition(rank, P)
         p.set_comm_mode("p2p")
         R = rules[0].info()["R"]
-        assert p.sym_bytes() == -(-R // P) * (M >> 1) * (N >> 1) * 8 + 256
+        assert p.sym_bytes() == -(-R // P) * (M >> 1) * (N >> 1) * A.itemsize + 256
         p.sym_alloc()
         p.execute(dev(A), dev(B))  # no communicator: only the owned products, into the buffer
         plans.append(p)
         ptrs.append(p.sym_ptr())
     torch.cuda.synchronize()
-    C = torch.full((M, N), float("nan"), dtype=torch.float64, device="cuda")
+    C = torch.full((M, N), float("nan"), dtype=torch.from_numpy(A).dtype, device="cuda")
     for rank in range(P):
         plans[rank].p2p_combine(ptrs, C, M * rank // P, M * (rank + 1) // P)
     torch.cuda.synchronize()
