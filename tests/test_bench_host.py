@@ -1,0 +1,50 @@
+"""Host logic of bench.py that feeds reported numbers: the algorithmic pass bytes of the
+whole-step pipeline roofline, checked against hand counts for Strassen-Winograd
+(products and combinations in DESIGN.md reading A2; 4 non-trivial U and V columns, all 4 blocks
+read; 3 trivial columns; W row nonzeros 2 + 4 + 4 + 4)."""
+import sys
+
+import pytest
+
+from fmm_testutil import ROOT
+
+sys.path.insert(0, str(ROOT))
+import bench  # noqa: E402
+import paper_1507_00687_b200 as fb  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def sw():
+    return fb.Rule.builtin("winograd").info()
+
+
+def test_one_level_counts(sw):
+    n, e = 1024, 8
+    q = (n // 2) ** 2  # one quarter block
+    # K1: A's 4 blocks read once + 4 formed S, same for B; K3: 7 products read + C written
+    k1 = 2 * (4 * q + 4 * q)
+    assert bench.pass_bytes([sw], n, n, n, e, False, False, False) == (k1 + 7 * q + 4 * q) * e
+    # fused leaf-parent level: the output written once instead of K3
+    assert bench.pass_bytes([sw], n, n, n, e, True, False, False) == (k1 + 4 * q) * e
+
+
+def test_two_level_counts(sw):
+    n, e = 1024, 8
+    s = (n // 4) ** 2  # one level-2 block
+    # K1X2 per operand: the 16 sub-blocks read once, the 49 - 3*3 = 40 formed grandchildren
+    k1x2 = 2 * (16 + 40) * s
+    # K3X2 from the 49 level-2 products into C (16 sub-blocks)
+    k3x2 = (49 + 16) * s
+    assert bench.pass_bytes([sw, sw], n, n, n, e, False, True, True) == (k1x2 + k3x2) * e
+    # one level per pass: level 0 (4 + 4 blocks of 4s per operand) then 7 nodes x (4 + 4) s,
+    # K3 at level 1 (7 nodes x (7 + 4) s) and at level 0 (7 x 4s + 16 s)
+    one = 2 * (4 * 4 * s + 4 * 4 * s) + 2 * 7 * (4 * s + 4 * s) + 7 * (7 * s + 4 * s) + (7 * 4 * s + 16 * s)
+    assert bench.pass_bytes([sw, sw], n, n, n, e, False, False, False) == one * e
+
+
+def test_depth_first_top_level_not_paired(sw):
+    # the per-r depth-first top level combines with ACC, so K3 pairing starts at level 1
+    n, e = 4096, 8
+    paired = bench.pass_bytes([sw] * 3, n, n, n, e, True, True, True, False)
+    unpaired_top = bench.pass_bytes([sw] * 3, n, n, n, e, True, True, True, True)
+    assert paired < unpaired_top
