@@ -177,7 +177,8 @@ def cpu_baseline(A_host, B_host, plan_rules, M, K, N, C_gpu_host=None, target_s=
     A = A_host.numpy() if hasattr(A_host, "numpy") else A_host
     B = B_host.numpy() if hasattr(B_host, "numpy") else B_host
     pm, _, pn = plan.dims_divisor()
-    # calibrate: one leaf row/col first, then scale to ~target_s
+    # calibrate: one leaf row/col first, doubling both (about 4x the work each time) until one
+    # run takes >= target_s / 2: the reported run is then 7.5-30 s of CPU work at target 15 s
     nr = 1
     res = None
     while True:
@@ -189,7 +190,7 @@ def cpu_baseline(A_host, B_host, plan_rules, M, K, N, C_gpu_host=None, target_s=
         Cs = oracle.fmm(Ag, Bh, plan)
         t = time.perf_counter() - t0
         res = (nr, G, H, Cs, t)
-        if t > target_s / 5 or nr * 2 > min(M // pm, N // pn) or nr >= 1024:
+        if t >= target_s / 2 or nr * 2 > min(M // pm, N // pn) or nr >= 1024:
             break
         nr *= 2
     nr, G, H, Cs, t = res
