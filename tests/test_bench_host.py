@@ -48,3 +48,21 @@ def test_depth_first_top_level_not_paired(sw):
     paired = bench.pass_bytes([sw] * 3, n, n, n, e, True, True, True, False)
     unpaired_top = bench.pass_bytes([sw] * 3, n, n, n, e, True, True, True, True)
     assert paired < unpaired_top
+
+
+def test_cpu_baseline_reports_parity_and_dd_errors():
+    # the CPU-baseline leg on a small problem: the sampled parity against the oracle and both
+    # paths' errors against the double-double reference are reported (here "GPU" = the oracle's
+    # own full result, so the parity is 0 and the two errors coincide)
+    import numpy as np
+    import oracle
+    from oracle import rules as OR
+    import fmm_inputs as fi
+    oracle.build()
+    M = K = N = 128
+    A, B = fi.random_pair(M, K, N, seed=5)
+    full = oracle.fmm(A, B, OR.Plan.uniform([OR.builtin("winograd")] * 2))
+    out = bench.cpu_baseline(A, B, ("winograd", "winograd"), M, K, N, C_gpu_host=full, target_s=0.01)
+    assert out["kind"] == "oracle" and out["parity_sampled"] == 0.0
+    e = out["error_vs_dd"]
+    assert e["gpu"] == e["oracle"] and 0.0 < e["gpu"] < 1e-13
