@@ -1,5 +1,6 @@
 """Full-size parity at BASELINE config C5 (32768^3, S-W L=3) in the launch configuration bench.py
-times (depth-first top-level schedule, same plan, same stream usage), against the oracle on a
+times (the hybrid top-level schedule the auto plan picks, same plan, same stream usage; also
+bitwise against the per-r depth-first schedule), against the oracle on a
 row/column sample it computes bitwise-exactly (oracle.fmm_sub on lifted rows / columns), plus a
 whole-matrix property: the FMM result agrees with the library's own classical product within
 the sum of the two Thm 4.3 bounds."""
@@ -28,8 +29,14 @@ def test_c5_f64_sampled_parity_and_bound(c5):
     Ad, Bd = A.cuda(), B.cuda()
     w = fb.Rule.builtin("winograd")
     plan = fb.Plan([w, w, w], N, N, N)
+    assert plan.launch_count() == 1 + 7 * 2 + 1  # hybrid: root K1, 7 x (K1X2 + K2F), K3X2
     Cd = plan.execute(Ad, Bd)
     torch.cuda.synchronize()
+    pdf = fb.Plan([w, w, w], N, N, N)
+    pdf.set_schedule("depth")  # per-r depth-first (the multi-GPU and host-pipeline form)
+    assert torch.equal(pdf.execute(Ad, Bd), Cd)
+    del pdf
+    torch.cuda.empty_cache()
     An, Bn = A.numpy(), B.numpy()
     amax, bmax = float(np.abs(An).max()), float(np.abs(Bn).max())
     op = R.Plan.stationary(R.winograd(), 3)
