@@ -19,6 +19,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named ranges for nsys / ncu --nvtx
+
 #include "fmm_internal.h"
 #include "builtin_tables.h"
 
@@ -1079,6 +1081,24 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
   return cudaSuccess;
 }
 
+// Host-side NVTX range (enqueue span of a launch / phase) for profiler timelines.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
+static const char* step_name(const Step& s) {
+  switch (s.kind) {
+    case STEP_K1: return s.x2 ? "fmm.K1X2" : "fmm.K1";
+    case STEP_K2: return "fmm.K2";
+    case STEP_K3: return s.x2 ? "fmm.K3X2" : "fmm.K3";
+    case STEP_ACC: return "fmm.ACC";
+    case STEP_ZERO: return "fmm.ZERO";
+    case STEP_K2F: return "fmm.K2F";
+  }
+  return "fmm.step";
+}
+
 template <typename T>
 static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStream_t st,
                             size_t i0 = 0, size_t i1 = (size_t)-1) {
@@ -1086,6 +1106,7 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
   if (i1 > p->steps.size()) i1 = p->steps.size();
   for (size_t si = i0; si < i1; ++si) {
     const Step& s = p->steps[si];
+    NvtxRange nv(step_name(s));
     TimedLaunch tl(p, s.kind == STEP_K2F ? STEP_K2 : s.kind, st);
     cudaError_t e = cudaSuccess;
     int64_t maxn = kMaxNodes;
@@ -1471,6 +1492,7 @@ static fmm_status p2p_combine(const fmm_plan* p, const void* dev_table, int n, v
   const RuleData& ru = p->rules[p->node_rule[0][0]];
   const int vecn = 16 / (int)sizeof(T);
   const bool vec = p->dims_vec_ok && aligned16(C) && ldc % vecn == 0;
+  NvtxRange nv("fmm.p2p_combine");
   TimedLaunch tl(p, 7, st);
   return cuda_status(launch_p2p_combine<T>((const T* const*)dev_table, n, p->dev_coef,
                                            p->coef_W[p->node_rule[0][0]], ru.R, ru.m0, ru.n0,
@@ -1539,6 +1561,7 @@ fmm_status fmm_plan_set_graph(fmm_plan* p, int enable) {
 
 fmm_status fmm_execute(const fmm_plan* p, const void* A, int64_t lda, const void* B, int64_t ldb,
                        void* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream) {
+  NvtxRange nv("fmm_execute");
   if (!p || !p->use_graph || p->timing || (p->comm && p->nranks > 1))
     return execute_impl(p, A, lda, B, ldb, C, ldc, ws, ws_bytes, stream);
   cudaStream_t st = (cudaStream_t)stream;
@@ -1626,6 +1649,7 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
     std::string steps;
     double tau;
     scaling_steps(p->scaling, &steps, &tau);
+    NvtxRange nv("fmm.scale");
     TimedLaunch tl(p, 6, st);
     cudaError_t e = run_scaling(p->M, p->K, p->N, (const double*)A, lda, (const double*)B, ldb, Ap,
                                 p->K, Bp, p->N, dA, dB, dI, steps.data(), (int)steps.size(),
@@ -1666,6 +1690,7 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
     if (e != cudaSuccess) return cuda_status(e, "fmm_execute crop");
   }
   if (p->scaling.mode != FMM_SCALE_NONE) {
+    NvtxRange nv("fmm.scale");
     TimedLaunch tl(p, 6, st);
     cudaError_t e = launch_unscale((double*)C, ldc, p->M, p->N, dA, dB, st);
     if (e != cudaSuccess) return cuda_status(e, "fmm_execute unscale");
@@ -1693,6 +1718,7 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
     NcclApi* api = nccl();
     if (!api) { set_error("NCCL not loadable"); return FMM_E_NCCL; }
     if (ldc != p->N) { set_error("fmm_execute: multi-GPU reduce needs ldc == N"); return FMM_E_ARG; }
+    NvtxRange nv("fmm.nccl");
     TimedLaunch tl(p, 7, st);
     const int dt = p->dtype == FMM_F64 ? ncclFloat64_ : ncclFloat32_;
     const size_t total = (size_t)(p->M * p->N);
