@@ -349,6 +349,33 @@ def test_no_out_of_bounds_writes(fb, dtype, leaf, dims):
     assert parity(Cv.cpu().numpy(), Co, A, B) <= (TOL64 if dtype == "f64" else TOL32)
 
 
+@pytest.mark.parametrize("names,sched,fusion", [(("winograd",) * 3, "hybrid", "on"),
+                                                (("winograd",) * 3, "depth", "off"),
+                                                (("strassen",) * 4, "breadth", "on")])
+def test_no_out_of_bounds_writes_deep(fb, names, sched, fusion):
+    # the same guard bands around the two-level passes (K1X2 / K3X2), the fused leaf kernel,
+    # the hybrid and per-r depth-first top levels, with ragged 64 x 64 leaf tiles
+    L = len(names)
+    M, K, N = 2 ** L * 36, 2 ** L * 20, 2 ** L * 28
+    A, B = fi.random_pair(M, K, N, seed=70 + L)
+    p = fb.Plan([fb.Rule.builtin(n) for n in names], M, K, N)
+    p.set_schedule(sched)
+    p.set_fusion(fusion)
+    ldc = N + 6
+    big = torch.full((M + 8, ldc), 12345.0, dtype=torch.float64, device="cuda")
+    Cv = big[4:4 + M, :N]
+    nb = p.workspace_bytes()
+    wsb = torch.full((nb + 4096,), 0xA5, dtype=torch.uint8, device="cuda")
+    p.execute(dev(A), dev(B), Cv, ws=wsb[:nb])
+    torch.cuda.synchronize()
+    g = big.clone()
+    g[4:4 + M, :N] = 12345.0
+    assert torch.all(g == 12345.0), "write outside C[:, :N]"
+    assert torch.all(wsb[nb:] == 0xA5), "write past the workspace"
+    Co = oracle.fmm(A, B, OPlan.uniform([R.builtin(n) for n in names]))
+    assert parity(Cv.cpu().numpy(), Co, A, B) <= TOL64
+
+
 def test_matmul_convenience_api(fb):
     # fb.matmul: cached plans; FP64 parity, FP32 (3xTF32) parity, scaling, padding
     A, B = fi.random_pair(300, 260, 200, seed=61)
