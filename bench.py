@@ -648,7 +648,9 @@ def run_fmm(args):
                        "l2": ("operands %.1f GiB each > 126 MB L2 (no flush needed)" % (M * K * esz / 2**30))
                   if not small else "L2 flushed (256 MB write) between timed steps, outside the events",
                        "leaf": {0: "native", 1: "tf32", 2: "3xtf32"}[leaf],
-                       "k3_fused_in_leaf_epilogue": bool(fused)},
+                       "k3_fused_in_leaf_epilogue": bool(fused),
+                       **({"scaling_steps_taken": plan.last_scaling_steps(ws=wsp, stream=stream)}
+                          if args.scaling != "none" and ws == 1 else {})},
             "parity": ({"metric": "||C_gpu - C_oracle||_max / (||A||_max ||B||_max K) on the "
                                   "cpu_baseline sample (BASELINE north_star tolerance)",
                         "value": cpu["parity_sampled"], "tolerance": 1e-13 if args.dtype == "f64" else 5e-5,
