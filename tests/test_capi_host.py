@@ -229,3 +229,16 @@ def test_p2p_comm_mode_schedule():
     assert p.launch_count() == n_reduce
     with pytest.raises(fb.FmmError):
         fb.fmm._call("fmm_plan_set_comm_mode", p._h, 4)
+
+
+def test_header_is_plain_c():
+    # the boundary header compiles as C99 and as C++ (no torch / C++ types in the signatures)
+    import shutil
+    import subprocess
+    hdr = ROOT / "include" / "fmm.h"
+    for cc, lang, std in (("gcc", "c", "-std=c99"), ("g++", "c++", "-std=c++17")):
+        if shutil.which(cc) is None:
+            pytest.skip(f"{cc} not available")
+        r = subprocess.run([cc, "-x", lang, std, "-fsyntax-only", "-Wall", "-Werror", str(hdr)],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
