@@ -699,6 +699,9 @@ def main():
     if args.impl == "reference":
         run_reference(args)
     else:
+        if args.warmup < 3:  # timing rule: at least 3 untimed warm-up steps (reported as run)
+            log(f"[bench] --warmup {args.warmup} raised to 3")
+            args.warmup = 3
         run_fmm(args)
 
 
