@@ -166,6 +166,24 @@ def make_inputs(cfg, dtype):
 
 
 # ------------------------------------------------------------------------------------------
+def scaling_config(mode: str):
+    """The scaling configuration the bench runs (readings A7 / A10): power-of-two
+    factors, tau = 1, at most 20 steps."""
+    return None if mode == "none" else {"mode": mode, "tau": 1.0, "max_steps": 20, "pow2": 1}
+
+
+def make_plan(fb, cfg: str, dtype: str = "f64", leaf=None, scaling: str = "none"):
+    """The plan bench.py times for BASELINE config `cfg` (also used by the full-size parity
+    tests, so they check exactly this launch configuration)."""
+    import fmm_inputs as fi
+    c = fi.CONFIGS[cfg]
+    if leaf is None:
+        leaf = fb.fmm.LEAF_NATIVE if dtype == "f64" else fb.fmm.LEAF_3XTF32
+    return fb.Plan([fb.Rule.builtin(r) for r in c.rules], c.M, c.K, c.N, dtype=dtype, leaf=leaf,
+                   scaling=scaling_config(scaling))
+
+
+# ------------------------------------------------------------------------------------------
 def cpu_baseline(A_host, B_host, plan_rules, M, K, N, C_gpu_host=None, target_s=15.0):
     """The CPU oracle, as it stands, on a bounded row/column sample of the same workload:
     rows G = lift_rows(leaf rows), columns H = lift_cols(leaf cols) (bitwise the oracle's own
@@ -389,26 +407,28 @@ def run_fmm(args):
         dist.broadcast(B, 0)
     torch.cuda.synchronize()
 
-    scaling = None
-    if args.scaling != "none":
-        scaling = {"mode": args.scaling, "tau": 1.0, "max_steps": 20, "pow2": 1}
-    plan = fb.Plan([fb.Rule.builtin(r) for r in rules], M, K, N, dtype=args.dtype, leaf=leaf,
-                   scaling=scaling)
+    plan = make_plan(fb, args.config, args.dtype, leaf, args.scaling)
     if args.shard_depth <= 0:  # auto: 49 depth-2 units balance 2 and 4 ranks (98 / 94 % vs
         # 87.5 % with the 7 top-level products); 8 ranks gain nothing from depth 2 (7 / 6.125);
         # the fused NVLink combine works on the top-level products (depth 1)
         args.shard_depth = 2 if ws in (2, 4) and args.comm != "p2p" else 1
+    # --comm-one-rank: a one-rank NCCL communicator at N = 1, so the exchange (the collective,
+    # or mode 3's barriers and combine) really runs on a single GPU
+    use_comm = ws > 1 or args.comm_one_rank
     if ws > 1 and args.shard_depth > 1:
         plan.set_shard_depth(args.shard_depth)
-    if ws > 1 and args.comm != "reduce":
+    if use_comm and args.comm != "reduce":
         plan.set_comm_mode(args.comm)
-    if ws > 1:
+    if use_comm:
         uid = [fb.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, 0)
+        if ws > 1:
+            dist.broadcast_object_list(uid, 0)
         plan.set_comm(uid[0], rank, ws)
         if args.comm == "p2p":  # symmetric product buffers, CUDA IPC handles exchanged
-            handles = [None] * ws
-            dist.all_gather_object(handles, plan.sym_alloc())
+            handles = [plan.sym_alloc()]
+            if ws > 1:
+                mine, handles = handles[0], [None] * ws
+                dist.all_gather_object(handles, mine)
             plan.set_peer_handles(handles)
     wsp = plan.workspace(A.device)
     use_graph = args.graph == "on" or (args.graph == "auto" and M * N * K <= 4096 ** 3 and ws == 1)
@@ -644,7 +664,7 @@ def run_fmm(args):
                                    + (f", scaling {args.scaling} (pow2, tau=1)" if args.scaling != "none" else ""),
                        "parallelism": (f"top-level r round-robin over {ws} GPU(s)" if args.shard_depth <= 1
                                        else f"depth-{args.shard_depth} paths round-robin over {ws} GPU(s)")
-                                      + (f", {args.comm} of C" if ws > 1 else ""),
+                                      + (f", {args.comm} of C" if use_comm else ""),
                        "l2": ("operands %.1f GiB each > 126 MB L2 (no flush needed)" % (M * K * esz / 2**30))
                   if not small else "L2 flushed (256 MB write) between timed steps, outside the events",
                        "leaf": {0: "native", 1: "tf32", 2: "3xtf32"}[leaf],
@@ -686,6 +706,8 @@ def main():
     ap.add_argument("--comm", default="reduce", choices=["reduce", "allreduce", "reduce_scatter", "p2p"],
                     help="multi-GPU exchange (fmm_plan_set_comm_mode): NCCL on the partial C, or "
                          "p2p = the fused NVLink W-combination of the peers' top-level products")
+    ap.add_argument("--comm-one-rank", action="store_true",
+                    help="at N = 1, attach a one-rank NCCL communicator so the --comm exchange runs")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-warmup", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -150,20 +150,10 @@ fmm_status fmm_plan_set_schedule(fmm_plan* plan, int schedule);
  * in ascending r and updates C_k after each (c = w*m first, then c = c + w*m), so M_r is never
  * written to memory and the result is bitwise identical to the unfused K2 + K3 path.
  * mode: 0 = off, 1 = on, 2 = automatic (default; on when parents x output tiles fill the GPU
- * several times), 3 = on, run as the persistent hybrid data-parallel / stream-K kernel (one CTA
- * per SM; units split across CTAs are finished by their owner from scratch in ascending r, still
- * bitwise; needs >= 64 inner-dimension elements per leaf, else mode 1).  FP64 only (FP32 plans
- * ignore it).  The environment variables FMM_FUSION (0/1/2) and FMM_K2P (0/1) set the defaults
- * at fmm_plan_create. */
+ * several times, the units' product chains split over CTAs where that balances the waves).
+ * FMM_E_ARG for other modes.  FP64 plans; FP32 tensor-core plans fuse only with mode 1.  The
+ * environment variable FMM_FUSION (0/1/2) sets the default at fmm_plan_create. */
 fmm_status fmm_plan_set_fusion(fmm_plan* plan, int mode);
-
-/* Operand fusion (host-only): in a fused leaf level, every S_r / T_r whose
- * U / V column has at most two nonzero +-1 entries (Strassen, classical: all; S-W: 5 of 7 per
- * operand) is not written by K1: the fused leaf kernel loads the parent blocks' tiles and
- * combines them in shared memory with K1's sequential sum (bitwise identical results).  Saves
- * the leaf level's S / T writes and reads.  FP64, leaf inner dimension >= 48; default off (the
- * environment variable FMM_OPF=1 turns it on at fmm_plan_create). */
-fmm_status fmm_plan_set_operand_fusion(fmm_plan* plan, int enable);
 
 /* S / T formation levels per pass (host-only; north star item 1, P:104-105 applied twice).
  * levels = 2 (default): where two consecutive recursion levels d, d+1 split 2x2-or-smaller
@@ -393,8 +383,23 @@ fmm_status fmm_plan_last_scaling_steps(const fmm_plan* plan, void* ws, int* step
  * ------------------------------------------------------------------------------------- */
 fmm_status fmm_comm_unique_id(void* out128);
 /* ncclCommInitRank on the current device; attaches the communicator and partition
- * (rank, nranks) to the plan.  fmm_execute then ends with ncclReduce(sum, root 0) of C. */
+ * (rank, nranks) to the plan.  fmm_execute then ends with the exchange of
+ * fmm_plan_set_comm_mode (default ncclReduce(sum, root 0) of C).  A one-rank communicator
+ * (nranks = 1) issues the same collectives (a sum over one rank: C is unchanged, bitwise), so
+ * the exchange runs -- and is testable -- on a single GPU.  FMM_E_NCCL if NCCL cannot be
+ * loaded or the init fails. */
 fmm_status fmm_plan_set_comm(fmm_plan* plan, const void* id128, int rank, int nranks);
+
+/* Comm mode 3's barrier, injected (host-only).  fmm_execute calls fn(user, stream) twice per
+ * call -- after this rank's products are enqueued, and after its combine -- instead of the
+ * 1-word ncclAllReduce; fn must return only when every rank has enqueued up to the same point
+ * and the stream's prior work is complete or ordered before any peer's later reads (e.g.
+ * synchronise the stream, then a host barrier).  Nonzero return -> FMM_E_NCCL.  With fn set,
+ * mode 3 needs no communicator: this is how two processes sharing one GPU test the CUDA-IPC
+ * exchange.  fn = NULL restores the NCCL barrier.  Recompiles the plan when it switches mode 3
+ * on or off. */
+typedef int (*fmm_barrier_fn)(void* user, void* stream);
+fmm_status fmm_plan_set_barrier(fmm_plan* plan, fmm_barrier_fn fn, void* user);
 
 /* Thread-local text of the last error (never NULL). */
 const char* fmm_last_error(void);

@@ -294,12 +294,13 @@ SCALE_MODES = ("none", "outside", "inside", "out_in", "in_out", "repeated")
 
 def scaled_fmm(A, B, plan: Plan, mode="none", pow2=False, tau=1.0, max_steps=20):
     """Scaling wrapper + FMM + unscale (Alg. 1-3).  out_in / in_out = one O then one I step (or
-    reverse) = Alg. 3 with max_steps=2 and no stop test reached.  Returns (C, info)."""
+    reverse) = Alg. 3 with max_steps=2 and no stop test reached.  Returns (C, info); info holds
+    the step count, the factors dA, dB and the scaled operands A', B'."""
     A = np.asarray(A, dtype=np.float64)
     B = np.asarray(B, dtype=np.float64)
     M, K = A.shape
     N = B.shape[1]
-    info = {"steps": 0}
+    info = {"steps": 0, "A": A, "B": B, "dA": np.ones(M), "dB": np.ones(N)}
     if mode == "none":
         return fmm(A, B, plan), info
     if mode == "outside":
@@ -317,7 +318,7 @@ def scaled_fmm(A, B, plan: Plan, mode="none", pow2=False, tau=1.0, max_steps=20)
         Ap, Bp, dA, dB = res["A"], res["B"], res["dA"], res["dB"]
         info["steps"] = res["steps"]
     Cp = fmm(Ap, Bp, plan)
-    info.update(dA=dA, dB=dB)
+    info.update(dA=dA, dB=dB, A=Ap, B=Bp)  # the scaled operands A', B' the FMM ran on
     return unscale(Cp, dA, dB), info
 
 

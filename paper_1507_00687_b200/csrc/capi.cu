@@ -124,12 +124,13 @@ struct fmm_plan {
   int fusion = 2;    // W-combination of the leaves' parents in the leaf GEMM epilogue: 0 off, 1 on, 2 auto
   int shard_depth = 1;  // multi-GPU: units = paths of the first shard_depth levels, round-robin
   int comm_mode = 0;    // multi-GPU exchange: 0 reduce to rank 0, 1 all-reduce, 2 reduce-scatter
-  bool persistent = false;  // fused leaves as the persistent stream-K kernel (K2P) where eligible
-  bool operand_fusion = false;  // S_r / T_r with <= 2 +-1 terms formed inside the fused leaf kernel
   bool split_chains = true;     // fused units' product chains split over CTAs (turnstiles)
   bool k1_two_level = true;     // S / T of two recursion levels formed in one pass (K1X2)
   bool k3_two_level = true;     // W-combination of two recursion levels in one pass (K3X2)
   ncclComm_t comm = nullptr;
+  // comm mode 3 barrier (fmm_plan_set_barrier): called instead of the 1-word NCCL all-reduce
+  fmm_barrier_fn barrier_fn = nullptr;
+  void* barrier_user = nullptr;
   // compiled schedule
   std::vector<Step> steps;
   std::vector<int> coef_U, coef_V, coef_W;  // per rule: offset in coef buffer (doubles)
@@ -163,6 +164,12 @@ struct fmm_plan {
     cudaGraphExec_t exec;
   };
   mutable std::vector<GraphEntry> graphs;
+  // comm mode 3 is live: products go to the symmetric buffer and, with a communicator or an
+  // injected barrier, the fused combine runs (a one-rank communicator / barrier exercises the
+  // exchange on one GPU; several ranks without either are the virtual-rank building block)
+  bool p2p_active() const {
+    return comm_mode == 3 && L > 0 && shard_depth == 1 && (nranks > 1 || comm || barrier_fn);
+  }
   mutable std::mutex gmu;
   // optional per-step timing (events recorded on the launch stream)
   bool timing = false;
@@ -199,7 +206,6 @@ fmm_plan::~fmm_plan() {
 
 namespace {
 
-constexpr int kPersistCtas = 148;  // B200 SMs: one persistent K2P CTA per SM
 constexpr size_t kHybridMaxWs = (size_t)64 << 30;  // hybrid top-level schedule: workspace cap
 constexpr int64_t kK2fSmallK = 1024;  // leaf inner dimension up to which K2F uses 64 x 64 tiles
 
@@ -235,10 +241,6 @@ struct Builder {
   struct Node {
     int64_t idx;  // BFS index within level
     Op a, b, c;
-    // operand fusion: S = sa0 a + sa1 a2 (na sources), T = sb0 b + sb1 b2 (nb sources)
-    Op a2{}, b2{};
-    int8_t sa0 = 1, sa1 = 1, sb0 = 1, sb1 = 1;
-    uint8_t na = 1, nb = 1;
   };
 
   const RuleData& rule_at(int l, int64_t idx) { return p->rules[p->node_rule[l][idx]]; }
@@ -253,27 +255,7 @@ struct Builder {
   }
 
   // K1 for the active nodes of level l (columns in `only_r` if >= 0); returns child nodes.
-  // A U / V column with at most two nonzero +-1 entries (operand fusion candidate): rows
-  // (ascending) and signs.
-  static bool small_col(const RuleData& r, const std::vector<int32_t>& X, int rows, int col,
-                        int* i0, int* s0, int* i1, int* s1, int* cnt) {
-    *cnt = 0;
-    const int32_t one = 1 << r.log2den;
-    for (int i = 0; i < rows; ++i) {
-      const int32_t x = X[(size_t)i * r.R + col];
-      if (x == 0) continue;
-      if (x != one && x != -one) return false;
-      if (*cnt == 0) { *i0 = i; *s0 = x > 0 ? 1 : -1; }
-      else if (*cnt == 1) { *i1 = i; *s1 = x > 0 ? 1 : -1; }
-      if (++*cnt > 2) return false;
-    }
-    return *cnt >= 1;
-  }
-
-  // opf: leave S_r / T_r whose column has <= 2 nonzero +-1 entries unformed; the fused leaf
-  // kernel combines the parent's blocks while staging its tiles (same sequential sum).
-  std::vector<Node> emit_k1(int l, const std::vector<Node>& nodes, int only_r, bool alloc_c = true,
-                            bool opf = false) {
+  std::vector<Node> emit_k1(int l, const std::vector<Node>& nodes, int only_r, bool alloc_c = true) {
     const int64_t mb = p->lm[l + 1], kb = p->lk[l + 1], nb = p->ln[l + 1];
     std::vector<K1Node> ks, kt;
     std::vector<Node> kids;
@@ -291,14 +273,9 @@ struct Builder {
         if (only_r >= 0 && r != only_r) continue;
         Node ch;
         ch.idx = nd.idx * ru.R + r;
-        int row, i0 = 0, i1 = 0, s0 = 1, s1 = 1, cnt = 0;
+        int row;
         if (trivial_col(ru, ru.U, ru.m0 * ru.k0, r, &row)) {
           ch.a = sub(nd.a, (row % ru.m0) * mb, (row / ru.m0) * kb);
-        } else if (opf && small_col(ru, ru.U, ru.m0 * ru.k0, r, &i0, &s0, &i1, &s1, &cnt)) {
-          ch.a = sub(nd.a, (i0 % ru.m0) * mb, (i0 / ru.m0) * kb);
-          ch.sa0 = (int8_t)s0;
-          ch.na = (uint8_t)cnt;
-          if (cnt == 2) { ch.a2 = sub(nd.a, (i1 % ru.m0) * mb, (i1 / ru.m0) * kb); ch.sa1 = (int8_t)s1; }
         } else {
           ch.a = ws_op(ws_alloc(mb * kb), kb);
           s.out[r] = ch.a;
@@ -306,11 +283,6 @@ struct Builder {
         }
         if (trivial_col(ru, ru.V, ru.k0 * ru.n0, r, &row)) {
           ch.b = sub(nd.b, (row % ru.k0) * kb, (row / ru.k0) * nb);
-        } else if (opf && small_col(ru, ru.V, ru.k0 * ru.n0, r, &i0, &s0, &i1, &s1, &cnt)) {
-          ch.b = sub(nd.b, (i0 % ru.k0) * kb, (i0 / ru.k0) * nb);
-          ch.sb0 = (int8_t)s0;
-          ch.nb = (uint8_t)cnt;
-          if (cnt == 2) { ch.b2 = sub(nd.b, (i1 % ru.k0) * kb, (i1 / ru.k0) * nb); ch.sb1 = (int8_t)s1; }
         } else {
           ch.b = ws_op(ws_alloc(kb * nb), nb);
           t.out[r] = ch.b;
@@ -328,15 +300,8 @@ struct Builder {
     const RuleData& r0 = rule_at(l, nodes[0].idx);
     std::vector<K1Node> all = ks;
     all.insert(all.end(), kt.begin(), kt.end());
-    int64_t items = 0;  // TMA-staged K1 work items: 4 rows x 4 KB column chunks per node
-    const int64_t cw = 4096 / elem_size(p->dtype);
-    for (K1Node& kn : all) {
-      kn.item0 = items;
-      items += ((kn.rows + 3) / 4) * ((kn.cols + cw - 1) / cw);
-    }
     if (!all.empty()) {
       Step st{};
-      st.items = items;
       st.kind = STEP_K1;
       st.count = (int)all.size();
       st.dev_off = push(all);
@@ -471,8 +436,6 @@ struct Builder {
   // fuses when that grid (parents x 128x128 output tiles of a leaf, one CTA per SM) fills the
   // 148 SMs in >= 4 waves at >= 90 % wave efficiency, or when a chain split brings the
   // simulated efficiency to >= 93 % (measured: profiles/r01_fusion_variants.md).
-  // operand fusion in the fused leaf kernel (FP64, leaf inner dimension >= STAGES k-tiles)
-  bool opf_on() const { return p->operand_fusion && p->dtype == FMM_F64 && (p->lk[p->L] + 15) / 16 >= 3; }
 
   // Simulated makespan (in product durations) of the fused grid when each unit's R-product
   // chain is split into groups of `chunk` products, dispatched group-major onto kSMs SMs in
@@ -498,13 +461,6 @@ struct Builder {
   }
   // best chain split for a fused leaf level (chunk = R: no split); efficiency out
   static int best_chunk(int64_t units, int R, int KT, int slots, double* eff) {
-    if (const char* ce = getenv("FMM_CHUNK")) {  // experiments: force the split
-      const int c = atoi(ce);
-      if (c >= 1 && c <= R) {
-        if (eff) *eff = 1.0;
-        return c;
-      }
-    }
     int best = R;
     double best_span = fused_makespan(units, R, R, KT, slots);
     if (KT >= 4 && units <= (1 << 16)) {
@@ -522,7 +478,6 @@ struct Builder {
   // SM, so one CTA's epilogue overlaps two others' mainloops) for short leaf inner dimensions,
   // the 128 x 128 kernel (v16, one CTA per SM) otherwise (profiles/r01_fusion_variants.md).
   int k2f_cfg() const {
-    if (const char* e = getenv("FMM_K2F_VARIANT")) return atoi(e);
     if (p->lk[p->L] > kK2fSmallK) return 16;
     for (int ri : p->node_rule[p->L - 1]) {  // v13 holds the tables of 2x2 rules with R <= 8
       const RuleData& r = p->rules[ri];
@@ -530,7 +485,7 @@ struct Builder {
     }
     return 13;
   }
-  int k2f_tile() const { return k2f_cfg() == 13 ? 64 : 128; }
+  int k2f_tile() const { return k2f_tile_of(k2f_cfg()); }
   int k2f_slots() const { return k2f_cfg() == 13 ? 3 * 148 : 148;
   }
 
@@ -554,10 +509,6 @@ struct Builder {
     constexpr int64_t kSMs = 148;
     const int64_t tiles = ((p->lm[p->L] + 127) / 128) * ((p->ln[p->L] + 127) / 128);
     const int64_t units = nparents * tiles;
-    // the persistent stream-K form (K2P) balances any unit count: fuse when the product-tiles
-    // fill the SMs at least once
-    if (p->persistent && (p->lk[p->L] + 15) / 16 >= persistent_min_kt())
-      return units * p->rules[p->node_rule[p->L - 1][0]].R >= kSMs;
     const int64_t waves = (units + kSMs - 1) / kSMs;
     return waves >= 4 && units * 10 >= waves * kSMs * 9;
   }
@@ -586,11 +537,6 @@ struct Builder {
         f.first[f.nr] = wm & ~started;
         f.a[f.nr] = ch.a;
         f.b[f.nr] = ch.b;
-        f.a2[f.nr] = ch.a2;
-        f.b2[f.nr] = ch.b2;
-        f.sa[f.nr][0] = ch.sa0; f.sa[f.nr][1] = ch.sa1;
-        f.sb[f.nr][0] = ch.sb0; f.sb[f.nr][1] = ch.sb1;
-        f.na[f.nr] = ch.na; f.nb[f.nr] = ch.nb;
         started |= wm;
         ++f.nr;
       }
@@ -605,7 +551,6 @@ struct Builder {
     st.rows = p->lm[p->L]; st.cols = p->ln[p->L]; st.inner = p->lk[p->L];
     st.P = r0.m0; st.Q = r0.n0; st.R = r0.R;
     st.nr = fz[0].nr;
-    st.opf = opf_on() ? 1 : 0;
     st.arena_off = -1;
     if (p->dtype == FMM_F32) {  // tensor-core FP32 leaves: split list (parent-major) + hi/lo arena
       std::vector<LeafNode> sl;
@@ -621,7 +566,6 @@ struct Builder {
       p->steps.push_back(st);
       return;
     }
-    // persistent hybrid data-parallel / stream-K form (K2P) when the leaf has >= STAGES k-tiles
     // chain split with per-unit turnstiles (breadth-first levels: every parent has all R products)
     st.k2f_cfg = k2f_cfg();
     if (p->split_chains && fz.size() > 0 && fz[0].nr == r0.R && (st.inner + 15) / 16 >= 4) {
@@ -631,12 +575,8 @@ struct Builder {
                                k2f_slots(), nullptr);
       if (c < r0.R) {
         st.chunk = c;
-        st.turn_off = ws_alloc((st.count * tiles + 1) / 2 + 1);  // ints, in 8-byte elements
+        st.turn_off = ws_alloc((st.count * tiles + 2) / 2);  // count*tiles + 1 ints, in 8-byte elements
       }
-    }
-    if (p->persistent && !st.opf && (st.inner + 15) / 16 >= persistent_min_kt()) {
-      st.persist = kPersistCtas;
-      st.arena_off = ws_alloc((int64_t)((persistent_scratch_bytes(kPersistCtas, st.nr) + 7) / 8));
     }
     p->steps.push_back(st);
   }
@@ -711,12 +651,9 @@ struct Builder {
     int64_t npar = (int64_t)nodes.size();  // parents of the leaves (R uniform per level)
     for (int d = l; d < p->L - 1; ++d) npar *= p->rules[p->node_rule[d][0]].R;
     const bool fuse = fuse_leaves(npar);
-    const bool opf = fuse && opf_on();
     // two levels per K1 pass (K1X2), paired from the bottom: (L-2, L-1), (L-4, L-3), ...
-    // (with operand fusion the last level stays a one-level pass)
-    const int ptop = opf ? p->L - 1 : p->L;
     std::vector<bool> pair_at(p->L + 1, false);
-    for (int e = ptop - 2; e >= l; e -= 2) pair_at[e] = true;
+    for (int e = p->L - 2; e >= l; e -= 2) pair_at[e] = true;
     for (int d = l; d < p->L;) {
       const int pr = pair_at[d] && p->k1_two_level ? k1x2_pair(d, lv.back()) : 0;
       if (pr) {
@@ -726,7 +663,7 @@ struct Builder {
         d += 2;
       } else {
         const bool last = d == p->L - 1;
-        lv.push_back(emit_k1(d, lv.back(), -1, !(last && fuse), last && opf));
+        lv.push_back(emit_k1(d, lv.back(), -1, !(last && fuse)));
         d += 1;
       }
       if (kid_c && lv.size() == (pr ? 3u : 2u))  // the first pass created level l + 1
@@ -765,13 +702,14 @@ struct Builder {
                      p->lm[l + 1] * p->ln[l + 1]);
     }
     const int64_t bf_bytes = bf * elem_size(p->dtype);
-    const bool split = p->schedule >= 2 || p->nranks > 1 ||
+    const bool split = p->schedule >= 2 || p->nranks > 1 || p2p_mode() ||
                        (p->schedule == 0 && bf_bytes > (int64_t)24 << 30);
     if (!split) {
       breadth_first(0, {root});
       return;
     }
-    if ((p->schedule == 3 || (p->schedule == 0 && hybrid_on())) && p->nranks == 1 && p->L >= 2) {
+    if ((p->schedule == 3 || (p->schedule == 0 && hybrid_on())) && p->nranks == 1 && !p2p_mode() &&
+        p->L >= 2) {
       const size_t s0 = p->steps.size(), d0 = desc.size();
       hybrid(root);
       if (ws_peak * elem_size(p->dtype) <= kHybridMaxWs) return;
@@ -782,7 +720,7 @@ struct Builder {
     depth_first(0, root, 0);
   }
 
-  bool p2p_mode() const { return p->comm_mode == 3 && p->nranks > 1 && p->shard_depth == 1; }
+  bool p2p_mode() const { return p->p2p_active(); }
 
   static bool hybrid_on() {
     const char* e = getenv("FMM_HYBRID");
@@ -859,7 +797,7 @@ struct Builder {
       // r / nranks) for the fused NVLink combine; no ACC into a partial C
       const bool p2p = l == 0 && p2p_mode();
       const bool fuse1 = leaf_next && !p2p && fuse_leaves(1);
-      std::vector<Node> kid = emit_k1(l, {node}, r, !fuse1 && !p2p, fuse1 && opf_on());
+      std::vector<Node> kid = emit_k1(l, {node}, r, !fuse1 && !p2p);
       if (p2p) {
         kid[0].c = Op{BASE_SYM, 0, (int64_t)(r / p->nranks) * p->lm[1], 0, p->ln[1]};
         if (leaf_next) emit_k2(kid);
@@ -912,6 +850,8 @@ fmm_status compile_plan(fmm_plan* p) {
     std::lock_guard<std::mutex> g(p->dev_mu);
     if (p->dev_desc) { cudaFree(p->dev_desc); p->dev_desc = nullptr; }
     p->dev_id = -1;
+    delete p->df_twin;  // the twin copies the plan's settings: rebuilt on next use
+    p->df_twin = nullptr;
   }
   Builder b(p);
   b.build();
@@ -936,7 +876,7 @@ fmm_status compile_plan(fmm_plan* p) {
   } else {
     p->scale_bytes = 0;
   }
-  if (p->nranks > 1 && p->comm) p->launches += 1;
+  if (p->comm && !p->p2p_active()) p->launches += 1;
   if (p->padded) p->launches += 3;  // pad A, pad B, crop C
   // vector-path feasibility of all plan-internal dims (caller lds / pointers checked at run)
   const int vec = 16 / elem_size(p->dtype);
@@ -966,6 +906,11 @@ static fmm_status ensure_device(const fmm_plan* p) {
   if (e != cudaSuccess) return cuda_status(e, "cudaGetDevice");
   if (p->dev_id == dev && (p->dev_coef || p->coef_host.empty()) && (p->dev_desc || p->desc_host.empty()))
     return FMM_OK;
+  if (p->dev_id != -1 && p->dev_id != dev) {  // captured graphs hold the old tables' pointers
+    std::lock_guard<std::mutex> gg(p->gmu);
+    for (auto& ge : p->graphs) cudaGraphExecDestroy(ge.exec);
+    p->graphs.clear();
+  }
   if (p->dev_coef) { cudaFree(p->dev_coef); p->dev_coef = nullptr; }
   if (p->dev_desc) { cudaFree(p->dev_desc); p->dev_desc = nullptr; }
   if (!p->coef_host.empty()) {
@@ -1016,14 +961,6 @@ struct TimedLaunch {
   }
 };
 
-// SMs of the current device (the persistent kernel needs one co-resident CTA per SM)
-static int device_sms() {
-  int dev = 0, n = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
-  return n;
-}
-
 // Launch one step (or one node-chunk of it: grid.y / grid.z carry the node count, limited to
 // 65535, so steps with more nodes -- deep recursions, 7^6 = 117649 leaves -- run in chunks).
 // `c0` = first node of the chunk: descriptor arrays, the FP32 split list and the turnstiles
@@ -1041,7 +978,7 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
     case STEP_K2F: node_bytes = sizeof(FusedNode); break;
   }
   const void* nd = (const uint8_t*)p->dev_desc + s.dev_off + c0 * node_bytes;
-  const int ts = s.k2f_cfg == 13 ? 64 : 128;
+  const int ts = k2f_tile_of(s.k2f_cfg);
   const int64_t tiles_f = p->dtype == FMM_F32 ? ((s.rows + 127) / 128) * ((s.cols + 255) / 256)
                                               : ((s.rows + ts - 1) / ts) * ((s.cols + ts - 1) / ts);
   switch (s.kind) {
@@ -1058,16 +995,9 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
             s.rows, s.cols, s.inner, p->dev_coef, s.P, s.Q, s.R, b, p->leaf == FMM_LEAF_TF32 ? 1 : 3,
             (float*)b.p[BASE_WS] + s.arena_off, st, s.chunk, turn);
       }
-      if (s.persist && s.persist <= device_sms()) {
-        double* scr = (double*)b.p[BASE_WS] + s.arena_off;
-        int* flg = (int*)(scr + (size_t)persistent_max_tail_units(s.persist) * s.nr * 128 * 128);
-        return launch_gemm_f64_persistent((const FusedNode*)nd, s.count, s.rows, s.cols, s.inner,
-                                          p->dev_coef, s.P, s.Q, s.R, s.nr, s.persist, scr, flg, b,
-                                          vec, st);
-      }
       return launch_gemm_f64_fused(
           (const FusedNode*)nd, s.count, s.rows, s.cols, s.inner, p->dev_coef, s.P, s.Q, s.R, b, vec,
-          st, s.opf != 0, s.nr, s.chunk,
+          st, s.nr, s.chunk,
           s.turn_off >= 0 ? (int*)((double*)b.p[BASE_WS] + s.turn_off) + c0 * tiles_f : nullptr,
           s.k2f_cfg);
     case STEP_K2:
@@ -1115,7 +1045,6 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
     for (int64_t c0 = 0; c0 < s.count && e == cudaSuccess; c0 += maxn) {
       Step sub = s;
       sub.count = (int)std::min<int64_t>(maxn, s.count - c0);
-      if (sub.count != s.count) sub.items = 0;  // item prefixes span the whole step
       e = launch_step<T>(p, sub, c0, b, vec, st);
     }
     if (e != cudaSuccess) return cuda_status(e, "fmm_execute launch");
@@ -1276,8 +1205,6 @@ fmm_status fmm_plan_create(const fmm_rule* const* nodes, int n_nodes, int levels
   }
   auto p = new fmm_plan();
   p->dtype = dtype; p->leaf = leaf; p->L = levels; p->M = M; p->K = K; p->N = N;
-  if (const char* pe = getenv("FMM_K2P")) p->persistent = atoi(pe) != 0;
-  if (const char* oe = getenv("FMM_OPF")) p->operand_fusion = atoi(oe) != 0;
   if (const char* ce = getenv("FMM_SPLIT")) p->split_chains = atoi(ce) != 0;
   if (const char* xe = getenv("FMM_K1X2")) p->k1_two_level = atoi(xe) != 0;
   if (const char* xe = getenv("FMM_K3X2")) p->k3_two_level = atoi(xe) != 0;
@@ -1380,9 +1307,8 @@ fmm_status fmm_plan_set_schedule(fmm_plan* p, int schedule) {
 }
 
 fmm_status fmm_plan_set_fusion(fmm_plan* p, int mode) {
-  if (!p || mode < 0 || mode > 3) { set_error("fmm_plan_set_fusion: bad args"); return FMM_E_ARG; }
-  p->fusion = mode == 3 ? 1 : mode;
-  p->persistent = mode == 3;
+  if (!p || mode < 0 || mode > 2) { set_error("fmm_plan_set_fusion: mode must be 0, 1 or 2"); return FMM_E_ARG; }
+  p->fusion = mode;
   return compile_plan(p);
 }
 
@@ -1395,12 +1321,6 @@ fmm_status fmm_plan_set_k1_levels(fmm_plan* p, int levels) {
 fmm_status fmm_plan_set_k3_levels(fmm_plan* p, int levels) {
   if (!p || levels < 1 || levels > 2) { set_error("fmm_plan_set_k3_levels: levels must be 1 or 2"); return FMM_E_ARG; }
   p->k3_two_level = levels == 2;
-  return compile_plan(p);
-}
-
-fmm_status fmm_plan_set_operand_fusion(fmm_plan* p, int enable) {
-  if (!p) { set_error("fmm_plan_set_operand_fusion: null"); return FMM_E_ARG; }
-  p->operand_fusion = enable != 0;
   return compile_plan(p);
 }
 
@@ -1562,7 +1482,7 @@ fmm_status fmm_plan_set_graph(fmm_plan* p, int enable) {
 fmm_status fmm_execute(const fmm_plan* p, const void* A, int64_t lda, const void* B, int64_t ldb,
                        void* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream) {
   NvtxRange nv("fmm_execute");
-  if (!p || !p->use_graph || p->timing || (p->comm && p->nranks > 1))
+  if (!p || !p->use_graph || p->timing || p->comm || p->barrier_fn)
     return execute_impl(p, A, lda, B, ldb, C, ldc, ws, ws_bytes, stream);
   cudaStream_t st = (cudaStream_t)stream;
   {
@@ -1630,7 +1550,7 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
   b.p[BASE_WS] = wsb + p->scale_bytes + p->pad_bytes;
   b.ld[BASE_A] = lda; b.ld[BASE_B] = ldb; b.ld[BASE_C] = ldc; b.ld[BASE_WS] = 0;
   b.p[BASE_SYM] = p->sym_own; b.ld[BASE_SYM] = p->L > 0 ? p->ln[1] : 0;
-  const bool p2p = p->comm_mode == 3 && p->nranks > 1 && p->L > 0;
+  const bool p2p = p->p2p_active();
   if (p2p) {
     if (p->shard_depth != 1 || p->padded || p->scaling.mode != FMM_SCALE_NONE) {
       set_error("fmm_execute: comm mode 3 needs shard depth 1, no padding and no scaling");
@@ -1695,26 +1615,34 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
     cudaError_t e = launch_unscale((double*)C, ldc, p->M, p->N, dA, dB, st);
     if (e != cudaSuccess) return cuda_status(e, "fmm_execute unscale");
   }
-  if (p2p && p->comm) {
+  if (p2p && (p->comm || p->barrier_fn)) {
     // every rank's owned M_r is in its symmetric buffer once all ranks pass this point; a 1-word
-    // all-reduce orders the streams (device-side barrier), then rank q computes rows
-    // [q M/P, (q+1) M/P) of C reading the products over NVLink, then a second barrier keeps the
-    // next call from overwriting products a peer is still reading
-    NcclApi* api = nccl();
-    if (!api || !api->allreduce) { set_error("NCCL not loadable"); return FMM_E_NCCL; }
+    // all-reduce orders the streams (device-side barrier; or the injected barrier), then rank q
+    // computes rows [q M/P, (q+1) M/P) of C reading the products over NVLink, then a second
+    // barrier keeps the next call from overwriting products a peer is still reading
     if (p->peers.size() != (size_t)p->nranks || !p->dev_peers) { set_error("fmm_execute: comm mode 3 needs fmm_plan_set_peer_handles"); return FMM_E_ARG; }
+    NcclApi* api = p->barrier_fn ? nullptr : nccl();
+    if (!p->barrier_fn && (!api || !api->allreduce)) { set_error("NCCL not loadable"); return FMM_E_NCCL; }
     float* bar = (float*)((uint8_t*)p->sym_own + sym_bytes_of(p) - 256);
-    ncclResult_t r = api->allreduce(bar, bar, 1, ncclFloat32_, ncclSum_, p->comm, st);
-    if (r != 0) { set_error("ncclAllReduce (barrier)"); return FMM_E_NCCL; }
-    const int64_t row0 = p->M * p->rank / p->nranks, row1 = p->M * (p->rank + 1) / p->nranks;
-    fmm_status cs = p->dtype == FMM_F64 ? p2p_combine<double>(p, p->dev_peers, p->nranks, C, ldc, row0, row1, st)
-                                        : p2p_combine<float>(p, p->dev_peers, p->nranks, C, ldc, row0, row1, st);
+    auto barrier = [&](float* word) -> fmm_status {
+      NvtxRange nv("fmm.p2p_barrier");
+      if (p->barrier_fn) {
+        if (p->barrier_fn(p->barrier_user, (void*)st) != 0) { set_error("fmm_execute: injected barrier failed"); return FMM_E_NCCL; }
+        return FMM_OK;
+      }
+      ncclResult_t r = api->allreduce(word, word, 1, ncclFloat32_, ncclSum_, p->comm, st);
+      if (r != 0) { set_error(std::string("ncclAllReduce (barrier): ") + (api->getErrorString ? api->getErrorString(r) : "?")); return FMM_E_NCCL; }
+      return FMM_OK;
+    };
+    fmm_status cs = barrier(bar);
     if (cs != FMM_OK) return cs;
-    r = api->allreduce(bar + 1, bar + 1, 1, ncclFloat32_, ncclSum_, p->comm, st);
-    if (r != 0) { set_error("ncclAllReduce (barrier)"); return FMM_E_NCCL; }
-    return FMM_OK;
+    const int64_t row0 = p->M * p->rank / p->nranks, row1 = p->M * (p->rank + 1) / p->nranks;
+    cs = p->dtype == FMM_F64 ? p2p_combine<double>(p, p->dev_peers, p->nranks, C, ldc, row0, row1, st)
+                             : p2p_combine<float>(p, p->dev_peers, p->nranks, C, ldc, row0, row1, st);
+    if (cs != FMM_OK) return cs;
+    return barrier(bar + 1);
   }
-  if (p->comm && p->nranks > 1 && !p2p) {
+  if (p->comm && !p2p) {  // a one-rank communicator issues the collective too (identity)
     NcclApi* api = nccl();
     if (!api) { set_error("NCCL not loadable"); return FMM_E_NCCL; }
     if (ldc != p->N) { set_error("fmm_execute: multi-GPU reduce needs ldc == N"); return FMM_E_ARG; }
@@ -1739,6 +1667,14 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
     if (r != 0) { set_error(std::string(what) + ": " + (api->getErrorString ? api->getErrorString(r) : "?")); return FMM_E_NCCL; }
   }
   return FMM_OK;
+}
+
+fmm_status fmm_plan_set_barrier(fmm_plan* p, fmm_barrier_fn fn, void* user) {
+  if (!p) { set_error("fmm_plan_set_barrier: null plan"); return FMM_E_ARG; }
+  const bool recompile = (fn != nullptr) != (p->barrier_fn != nullptr);
+  p->barrier_fn = fn;
+  p->barrier_user = user;
+  return recompile ? compile_plan(p) : FMM_OK;
 }
 
 fmm_status fmm_plan_set_timing(fmm_plan* p, int enable) {
@@ -1920,8 +1856,6 @@ static const fmm_plan* depth_first_twin(const fmm_plan* p) {
     t->rules = p->rules; t->node_rule = p->node_rule; t->lm = p->lm; t->lk = p->lk; t->ln = p->ln;
     t->scaling = p->scaling; t->coef_U = p->coef_U; t->coef_V = p->coef_V; t->coef_W = p->coef_W;
     t->coef_host = p->coef_host; t->schedule = 2; t->fusion = p->fusion; t->shard_depth = p->shard_depth;
-    t->persistent = p->persistent;
-    t->operand_fusion = p->operand_fusion;
     t->split_chains = p->split_chains;
     t->k1_two_level = p->k1_two_level;
     t->k3_two_level = p->k3_two_level;
@@ -1934,9 +1868,12 @@ static const fmm_plan* depth_first_twin(const fmm_plan* p) {
 // The plan whose top-level groups drive the host-copy pipeline (the plan itself if depth-first
 // at the top, else its depth-first twin), or null where the pipeline does not apply.
 static const fmm_plan* host_pipeline_plan(const fmm_plan* p, const void* ws, size_t ws_bytes) {
-  if (!(p->L > 0 && p->scaling.mode == FMM_SCALE_NONE && !(p->comm && p->nranks > 1) &&
-        !p->padded && p->M > 0 && p->N > 0 && p->K > 0))
+  if (!(p->L > 0 && p->scaling.mode == FMM_SCALE_NONE && !p->comm && !p->padded && p->M > 0 &&
+        p->N > 0 && p->K > 0))
     return nullptr;
+  // a partitioned plan runs its own (depth-first) schedule; with no owned product it has no
+  // groups and fmm_execute's zeroing of C is the whole job -- never the full-product twin
+  if (p->nranks > 1 && p->groups.empty()) return nullptr;
   const fmm_plan* q = p->groups.empty() ? depth_first_twin(p) : p;
   size_t need = 0;
   if (q) fmm_plan_workspace_bytes(q, &need);

@@ -72,7 +72,6 @@ RuleQuantities rule_quantities(const RuleData& d);
 // a 2-bit code per input block (0 absent, 1 +1, 2 -1, 3 general coefficient from the table).
 struct K1Node {
   Op in;
-  int64_t item0;       // TMA-staged K1: first work item of this node (prefix over the launch)
   int64_t rows, cols;  // sub-block dims of this node's split (S: mb x kb, T: kb x nb)
   int32_t P, Q;        // split P x Q (S: m0 x k0, T: k0 x n0)
   int32_t coef_off;  // offset (in doubles) of the table in the plan's coefficient buffer
@@ -182,11 +181,6 @@ struct FusedNode {
   uint32_t wmask[kMaxR];  // bit k: w_kr != 0
   uint32_t first[kMaxR];  // bit k: this product initialises C_k
   Op a[kMaxR], b[kMaxR];  // leaf operands S_r, T_r (index i, not r)
-  // operand fusion (fmm_plan_set_operand_fusion): S_i = sa[i][0] a[i] + sa[i][1] a2[i] formed
-  // while staging tiles (na[i] = 1 or 2 sources, signs +-1), likewise T_i from b / b2
-  Op a2[kMaxR], b2[kMaxR];
-  int8_t sa[kMaxR][2], sb[kMaxR][2];
-  uint8_t na[kMaxR], nb[kMaxR];
 };
 
 enum StepKind { STEP_K1 = 1, STEP_K2 = 2, STEP_K3 = 3, STEP_ACC = 4, STEP_ZERO = 5, STEP_K2F = 8 };
@@ -197,18 +191,15 @@ struct Step {
   int64_t dev_off;   // byte offset of the node array in the plan's device descriptor buffer
   int64_t rows, cols, inner;  // sub-block dims (K1/K3/ACC/ZERO) or m, n, k (K2)
   int P, Q, R;       // K1: split P x Q, rank R.  K3/ACC/ZERO: P = M0, Q = N0, R
-  int64_t arena_off; // K2 FP32 tensor-core leaves: offset (elements) of the hi/lo arena in ws;
-                     // K2F persistent (K2P): offset of the scratch tiles + flags in ws
+  int64_t arena_off; // K2 FP32 tensor-core leaves: offset (elements) of the hi/lo arena in ws
   bool vec_ok;       // all ws offsets / dims allow 16-byte vectors (caller bases checked later)
   int nr = 0;        // K2F: products per node (uniform)
   int64_t dev_off2 = -1;  // K2F FP32: LeafNode list (parent-major) for the hi / lo split
-  int64_t items = 0;      // K1 TMA-staged variant: work items (4 rows x 4 KB) of the launch
-  int opf = 0;       // K2F: operands formed in the kernel from up to two sources (na / nb)
   int k2f_cfg = 16;  // K2F tile configuration (16: 128 x 128 / 1 CTA per SM, 13: 64 x 64 / 3)
   int chunk = 0;     // K2F: products per CTA when a unit's chain is split (0: whole chain);
-                     // turnstiles (one int per unit) at ws offset turn_off (bytes)
+                     // turnstiles (one int per unit) + a ticket counter at ws offset turn_off
+                     // (in elements of the plan's dtype)
   int64_t turn_off = -1;
-  int persist = 0;   // K2F: run as the persistent stream-K kernel with this many CTAs (0: grid)
   int x2 = 0;        // K1 / K3: 0 one level (K1Node / K3Node); else K1x2Node / K3x2Node with
                      // rule pair (x2 - 1) / 3, (x2 - 1) % 3 (builtin_tables.h ids)
 };
@@ -244,24 +235,16 @@ cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, in
                             int64_t k, const Bases& b, bool vec, cudaStream_t st);
 cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                   int64_t k, const double* dev_coef, int P, int Q, int R,
-                                  const Bases& b, bool vec, cudaStream_t st, bool opf = false,
-                                  int nr = 0, int chunk = 0, int* turn = nullptr, int cfg = 16);
-// K2P: persistent hybrid data-parallel / stream-K form of K2F (one CTA per SM, `ctas` CTAs;
-// every node has NR products).  scratch / flags: persistent_scratch_bytes(ctas, NR) of
-// workspace (flags zeroed by the launcher).  Needs ceil(k / BK) >= persistent_min_kt().
-cudaError_t launch_gemm_f64_persistent(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
-                                       int64_t k, const double* dev_coef, int P, int Q, int R,
-                                       int NR, int ctas, double* scratch, int* flags,
-                                       const Bases& b, bool vec, cudaStream_t st);
-size_t persistent_scratch_bytes(int ctas, int NR);
+                                  const Bases& b, bool vec, cudaStream_t st, int nr, int chunk,
+                                  int* turn, int cfg);
+// output tile edge (BM = BN) of K2F tile configuration cfg (13: 64, 16: 128)
+int k2f_tile_of(int cfg);
 // K2F for the FP32 tensor-core leaves (3xTF32 / TF32 on tcgen05, TMEM double-buffered)
 cudaError_t launch_gemm_tf32_fused(const FusedNode* dev_nodes, const LeafNode* dev_split_leaves,
                                    int count, int nr, int64_t m, int64_t n, int64_t k,
                                    const double* dev_coef, int P, int Q, int R, const Bases& b,
                                    int passes, float* arena, cudaStream_t st, int chunk = 0,
                                    int* turn = nullptr);
-int64_t persistent_max_tail_units(int ctas);
-int persistent_min_kt();
 cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, const LeafNode* host_leaves, int count,
                             int64_t m, int64_t n, int64_t k, const Bases& b, bool vec, int leaf,
                             float* arena, cudaStream_t st);

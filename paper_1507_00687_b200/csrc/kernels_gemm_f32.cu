@@ -11,10 +11,6 @@ namespace fmm {
 cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
                              int64_t k, const Bases& b, int passes, float* arena,
                              cudaStream_t st, const LeafNode* host_leaves);
-cudaError_t launch_gemm_tf32_v2(const LeafNode* dev_leaves, const LeafNode* host_leaves,
-                                int count, int64_t m, int64_t n, int64_t k, const Bases& b,
-                                int passes, float* arena, cudaStream_t st);
-
 namespace {
 
 constexpr int BM = 128, BN = 128, BK = 8, THREADS = 256;
@@ -102,19 +98,6 @@ __global__ void __launch_bounds__(THREADS)
 
 }  // namespace
 
-// The v2 tensor-core path reads the leaf operands in place through TMA: every operand base must
-// be 16-byte aligned and every leading dimension a multiple of 4 floats.
-static bool tma_ok(const LeafNode* host_leaves, int count, const Bases& b) {
-  if (!host_leaves) return false;
-  for (int i = 0; i < count; ++i) {
-    int64_t lda, ldb;
-    const float* A = op_ptr<const float>(b, host_leaves[i].a, lda);
-    const float* B = op_ptr<const float>(b, host_leaves[i].b, ldb);
-    if ((((uintptr_t)A) & 15u) || (((uintptr_t)B) & 15u) || (lda & 3) || (ldb & 3)) return false;
-  }
-  return true;
-}
-
 cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, const LeafNode* host_leaves, int count,
                             int64_t m, int64_t n, int64_t k, const Bases& b, bool vec, int leaf,
                             float* arena, cudaStream_t st) {
@@ -122,11 +105,6 @@ cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, const LeafNode* host_lea
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
   if (leaf == FMM_LEAF_TF32 || leaf == FMM_LEAF_3XTF32) {
     const int passes = leaf == FMM_LEAF_TF32 ? 1 : 3;
-    // v2 (raw operands in place, MN-major B, lo-only split) is correct but measured slower at
-    // C5 than v1 (324 vs 289 ms per step; profiles/r01_tf32_variants.md): opt-in only.
-    static const bool use_v2 = getenv("FMM_TF32_V2") != nullptr;
-    if (use_v2 && tma_ok(host_leaves, count, b))
-      return launch_gemm_tf32_v2(dev_leaves, host_leaves, count, m, n, k, b, passes, arena, st);
     return launch_gemm_tf32(dev_leaves, count, m, n, k, b, passes, arena, st, host_leaves);
   }
   const int tiles_m = (int)((m + BM - 1) / BM), tiles_n = (int)((n + BN - 1) / BN);

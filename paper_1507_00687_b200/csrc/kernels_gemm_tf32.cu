@@ -96,24 +96,16 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
                : "memory");
 }
 
-__device__ int g_split_mode = 0;  // experiment: 0 rn hi; 1 raw hi + trunc lo; 2 raw hi + rn lo
-
 __device__ __forceinline__ float tf32_hi(float x) {
   uint32_t u = __float_as_uint(x);
   u = (u + 0x1000u) & 0xFFFFE000u;  // round to nearest (ties away) at 10 mantissa bits
   return __uint_as_float(u);
 }
 
+// x = hi + lo exactly: hi = x rounded to TF32, lo = x - hi (exact in FP32)
 __device__ __forceinline__ void split2(float x, float& h, float& l) {
-  const int mode = g_split_mode;
-  if (mode == 0) {
-    h = tf32_hi(x);
-    l = x - h;
-  } else {
-    h = x;
-    const float t = mode == 1 ? __uint_as_float(__float_as_uint(x) & 0xFFFFE000u) : tf32_hi(x);
-    l = x - t;
-  }
+  h = tf32_hi(x);
+  l = x - h;
 }
 
 // K-major UMMA descriptor for a BK-float-wide swizzled tile (BK = 32: SW128, BK = 16: SW64).
@@ -308,15 +300,27 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_slot = (uint32_t*)(bars + 2 * TSTAGES + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // chain split (chunk < nr, turnstiles as in k2f_gemm_f64): grid.y = group * count + parent;
-  // chunk = 1 keeps the unfused kernel's order (all CTAs of one product first: the L2 reuse of
-  // that leaf's panels) while the epilogue still applies the W-combination in place
-  const int parent = blockIdx.y % count, grp = blockIdx.y / count;
+  // chain split (chunk < nr; turnstiles and dispatch-order tickets as in k2f_gemm_f64: the work
+  // item (group, parent, tile), group-major, comes from an atomicAdd ticket taken at CTA start,
+  // so the group a CTA waits for has always started).  chunk = 1 keeps the unfused kernel's
+  // order (all CTAs of one product first: the L2 reuse of that leaf's panels) while the
+  // epilogue still applies the W-combination in place.
+  const int tiles = gridDim.x;
+  int parent = blockIdx.y, grp = 0, tile = blockIdx.x;
+  if (turn) {
+    __shared__ int s_ticket;
+    if (threadIdx.x == 0) s_ticket = atomicAdd(turn + (int64_t)count * tiles, 1);
+    __syncthreads();
+    const int tk = s_ticket, per_grp = count * tiles;
+    grp = tk / per_grp;
+    parent = (tk % per_grp) / tiles;
+    tile = tk % tiles;
+  }
   const FusedNode& nd = nodes[parent];
   const int r_begin = grp * chunk;
   const int r_end = min(nd.nr, r_begin + chunk);
   const int nr_all = nd.nr;
-  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
+  const int tm = tile / tiles_n, tn = tile % tiles_n;
   const int m0 = tm * TBM, n0 = tn * TBN;
   const int KT = (int)(kp / TBK);
 
@@ -410,7 +414,7 @@ __global__ void __launch_bounds__(256, 1)
     const int64_t row = m0 + q * 32 + lane;
     int64_t ldo;
     float* out = op_ptr<float>(bases, nd.out, ldo);
-    int* my_turn = turn ? turn + (int64_t)parent * gridDim.x + blockIdx.x : nullptr;
+    int* my_turn = turn ? turn + (int64_t)parent * tiles + tile : nullptr;
     for (int ri = r_begin; ri < r_end; ++ri) {
       const int j = ri - r_begin;
       const int buf = j & 1;
@@ -419,11 +423,9 @@ __global__ void __launch_bounds__(256, 1)
       if (j == 0 && grp > 0 && my_turn) {  // group grp-1 released this unit
         if (threadIdx.x == 128) {
           unsigned ns = 64;
-          long long spins = 0;
-          while (atomicAdd(my_turn, 0) < grp) {
+          while (atomicAdd(my_turn, 0) < grp) {  // grp-1 holds an earlier ticket: it is running
             __nanosleep(ns);
             if (ns < 2048) ns *= 2;
-            if (++spins > (1ll << 24)) __trap();
           }
           __threadfence();
         }
@@ -541,203 +543,6 @@ __global__ void k_split_tf32(const LeafNode* __restrict__ leaves, Bases bases, i
       split2(x, h, l);
       b_hi[base + nn * kp + kk] = h;
       b_lo[base + nn * kp + kk] = l;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
-// v2: the TF32 "hi" operand is the raw FP32 data itself -- the tensor core truncates the low 13
-// mantissa bits of kind::tf32 inputs (measured: tools/tf32_semantics.py; x = 1 + 0.75 ulp_tf32
-// multiplies as 1) -- so only lo = x - trunc13(x) is materialised, in natural layouts (no
-// transpose): A_lo (m x k4), B_lo (k x n4).  A (raw and lo) is loaded K-major; B (raw and lo) is
-// loaded MN-major straight from the row-major k x n operand (UMMA MN-major SW128 layout: 32-float
-// chunks along N, 4 KB apart (LBO); 8 k-rows of 128 B per core group (SBO = 1024 B)).  One 2-D
-// tensor map per operand per leaf, passed by value in the kernel parameters (<= 48 leaves per
-// launch; 24.6 KB of parameters).
-// ---------------------------------------------------------------------------------------------
-constexpr int MAXL = 48;
-struct TmaBatch {
-  CUtensorMap m[MAXL][4];  // A raw, A lo, B raw, B lo
-};
-
-constexpr uint32_t IDESC_V2 = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) /*B MN-major*/ |
-                              ((uint32_t)(TBN >> 3) << 17) | ((uint32_t)(TBM >> 4) << 24);
-
-__device__ __forceinline__ void mma_tf32_v2(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(IDESC_V2), "r"(acc));
-}
-
-// MN-major for 32-bit types: the "128-byte swizzle with 32-byte atoms" layout (UMMA layout type
-// SWIZZLE_128B_BASE32B = 1, TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): k-rows of 128 B (32 floats
-// of N), 4-row core groups (SBO = 512 B), 32-float MN chunks 4 KB apart (LBO = 4096 B).
-__device__ int g_mn_lbo = 4096, g_mn_sbo = 512, g_mn_layout = 1;
-__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)(g_mn_lbo >> 4) << 16;
-  d |= (uint64_t)(g_mn_sbo >> 4) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)g_mn_layout << 61;
-  return d;
-}
-
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1,
-                                            uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
-      : "memory");
-}
-
-__global__ void __launch_bounds__(256, 1)
-    k2_tf32_v2(const __grid_constant__ TmaBatch tb, const LeafNode* __restrict__ leaves,
-               Bases bases, int64_t m, int64_t n, int64_t k, int tiles_n, int passes) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* bars = (uint64_t*)(smem + TSTAGES * STAGE_BYTES);
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * TSTAGES + 1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int leaf = blockIdx.y;
-  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
-  const int m0 = tm * TBM, n0 = tn * TBN;
-  const int KT = (int)((k + TBK - 1) / TBK);
-  const CUtensorMap* maps = tb.m[leaf];
-
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < TSTAGES; ++s) {
-      mbar_init(su32(&bars[s]), 1);
-      mbar_init(su32(&bars[TSTAGES + s]), 1);
-    }
-    mbar_init(su32(&bars[2 * TSTAGES]), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                     su32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % TSTAGES;
-        const uint32_t ph = (uint32_t)(kt / TSTAGES) & 1u;
-        mbar_wait(su32(&bars[TSTAGES + s]), ph ^ 1u);
-        uint8_t* st = smem + s * STAGE_BYTES;
-        const uint32_t full = su32(&bars[s]);
-        const int kc = kt * TBK;
-        mbar_expect_tx(full, passes == 3 ? STAGE_BYTES : A_BYTES + B_BYTES);
-        tma_load_2d(su32(st), &maps[0], kc, m0, full);
-        if (passes == 3) tma_load_2d(su32(st + A_BYTES), &maps[1], kc, m0, full);
-#pragma unroll
-        for (int j = 0; j < TBN / 32; ++j) {
-          tma_load_2d(su32(st + 2 * A_BYTES + j * 4096), &maps[2], n0 + 32 * j, kc, full);
-          if (passes == 3) tma_load_2d(su32(st + 2 * A_BYTES + B_BYTES + j * 4096), &maps[3], n0 + 32 * j, kc, full);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % TSTAGES;
-        const uint32_t ph = (uint32_t)(kt / TSTAGES) & 1u;
-        mbar_wait(su32(&bars[s]), ph);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        uint8_t* st = smem + s * STAGE_BYTES;
-        const uint64_t a_hi = desc_sw128(su32(st)), a_lo = desc_sw128(su32(st + A_BYTES));
-        const uint64_t b_hi = desc_mn_sw128(su32(st + 2 * A_BYTES));
-        const uint64_t b_lo = desc_mn_sw128(su32(st + 2 * A_BYTES + B_BYTES));
-#pragma unroll
-        for (int kk = 0; kk < TBK / 8; ++kk) {
-          const uint64_t aoff = (uint64_t)((kk * 32) >> 4);    // K-major: 8 tf32 = 32 B
-          const uint64_t boff = (uint64_t)((kk * 1024) >> 4);  // MN-major: 8 k-rows = 1 KB
-          const uint32_t first = (kt == 0 && kk == 0) ? 0u : 1u;
-          if (passes == 3) {
-            mma_tf32_v2(tmem, a_lo + aoff, b_hi + boff, first);
-            mma_tf32_v2(tmem, a_hi + aoff, b_lo + boff, 1u);
-            mma_tf32_v2(tmem, a_hi + aoff, b_hi + boff, 1u);
-          } else {
-            mma_tf32_v2(tmem, a_hi + aoff, b_hi + boff, first);
-          }
-        }
-        mma_commit(su32(&bars[TSTAGES + s]));
-      }
-      mma_commit(su32(&bars[2 * TSTAGES]));
-    }
-  } else if (warp >= 4) {
-    mbar_wait(su32(&bars[2 * TSTAGES]), 0u);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const LeafNode& lf = leaves[leaf];
-    int64_t ldc;
-    float* Cp = op_ptr<float>(bases, lf.c, ldc);
-    const int q = warp & 3;
-    const int64_t row = m0 + q * 32 + lane;
-#pragma unroll 1
-    for (int cb = 0; cb < TBN / 32; ++cb) {
-      uint32_t v[32];
-      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * 32);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-          "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-            "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-            "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-            "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-            "=r"(v[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-      if (KT == 0) {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = 0u;
-      }
-      if (row < m) {
-        float* crow = Cp + row * ldc + n0 + cb * 32;
-        const int64_t cbase = n0 + cb * 32;
-        const bool vec = ((((uintptr_t)crow) & 15u) == 0) && (cbase + 32 <= n);
-        if (vec) {
-#pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            *reinterpret_cast<float4*>(crow + e) =
-                make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
-                            __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (cbase + e < n) crow[e] = __uint_as_float(v[e]);
-        }
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  if (warp == 2)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                 "r"(TMEM_COLS));
-}
-
-// lo = x - trunc13(x) for the leaves' operands, natural layouts: A_lo (m x k4), B_lo (k x n4).
-// grid: x = ceil(cols / 256) vectors..., simple: one thread per element, y = row, z = leaf.
-__global__ void k_split_lo(const LeafNode* __restrict__ leaves, Bases bases, int64_t rows,
-                           int64_t cols, int64_t ldo, float* __restrict__ lo, int side) {
-  const LeafNode& lf = leaves[blockIdx.z];
-  int64_t ld;
-  const float* X = side == 0 ? op_ptr<const float>(bases, lf.a, ld) : op_ptr<const float>(bases, lf.b, ld);
-  float* out = lo + (size_t)blockIdx.z * (size_t)(rows * ldo);
-  for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
-    for (int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x) {
-      const float x = X[r * ld + c];
-      out[r * ldo + c] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
     }
   }
 }
@@ -873,14 +678,6 @@ cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, i
                              int64_t k, const Bases& b, int passes, float* arena,
                              cudaStream_t st, const LeafNode* host_leaves) {
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
-  {
-    static int mode = -1;
-    if (mode < 0) {
-      const char* e = getenv("FMM_TF32_SPLIT_MODE");
-      mode = e ? atoi(e) : 0;
-      cudaMemcpyToSymbol(g_split_mode, &mode, sizeof(int));
-    }
-  }
   if (!arena) return cudaErrorInvalidValue;
   const int64_t kp = (k + TBK - 1) / TBK * TBK;
   float* a_hi = arena;
@@ -944,78 +741,13 @@ cudaError_t launch_gemm_tf32_fused(const FusedNode* dev_nodes, const LeafNode* d
   if (chunk <= 0 || chunk >= nr || !turn) chunk = nr;
   const int groups = (nr + chunk - 1) / chunk;
   if (groups > 1) {
-    e = cudaMemsetAsync(turn, 0, sizeof(int) * (size_t)count * tiles_m * tiles_n, st);
+    e = cudaMemsetAsync(turn, 0, sizeof(int) * ((size_t)count * tiles_m * tiles_n + 1), st);
     if (e != cudaSuccess) return e;
   }
   k2f_tf32<32, 2><<<dim3((unsigned)(tiles_m * tiles_n), (unsigned)(count * groups)), 256, CF::SMEM, st>>>(
       ma_hi, ma_lo, mb_hi, mb_lo, dev_nodes, dev_coef, b, m, n, kp, tiles_n, passes, P, Q, R, count,
       chunk, groups > 1 ? turn : nullptr);
   return cudaGetLastError();
-}
-
-cudaError_t launch_gemm_tf32_v2(const LeafNode* dev_leaves, const LeafNode* host_leaves,
-                                int count, int64_t m, int64_t n, int64_t k, const Bases& b,
-                                int passes, float* arena, cudaStream_t st) {
-  if (count == 0 || m == 0 || n == 0) return cudaSuccess;
-  if (!arena || !host_leaves) return cudaErrorInvalidValue;
-  const int64_t k4 = (k + 3) / 4 * 4, n4 = (n + 3) / 4 * 4;
-  float* a_lo = arena;
-  float* b_lo = a_lo + (size_t)count * m * k4;
-  if (passes == 3 && k > 0) {
-    const unsigned gy = (unsigned)(m < 4096 ? m : 4096), gy2 = (unsigned)(k < 4096 ? k : 4096);
-    k_split_lo<<<dim3((unsigned)((k + 255) / 256), gy, (unsigned)count), 256, 0, st>>>(
-        dev_leaves, b, m, k, k4, a_lo, 0);
-    k_split_lo<<<dim3((unsigned)((n + 255) / 256), gy2, (unsigned)count), 256, 0, st>>>(
-        dev_leaves, b, k, n, n4, b_lo, 1);
-  }
-  {
-    static bool once = false;
-    if (!once) {
-      once = true;
-      const char* l = getenv("FMM_MN_LBO");
-      const char* s2 = getenv("FMM_MN_SBO");
-      if (l) { int v = atoi(l); cudaMemcpyToSymbol(g_mn_lbo, &v, sizeof(int)); }
-      if (s2) { int v = atoi(s2); cudaMemcpyToSymbol(g_mn_sbo, &v, sizeof(int)); }
-      if (const char* lt = getenv("FMM_MN_LAYOUT")) { int v = atoi(lt); cudaMemcpyToSymbol(g_mn_layout, &v, sizeof(int)); }
-    }
-  }
-  cudaError_t e = cudaFuncSetAttribute(k2_tf32_v2, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  if (e != cudaSuccess) return e;
-  auto fn = encode_fn();
-  if (!fn) return cudaErrorNotSupported;
-  const int tiles_m = (int)((m + TBM - 1) / TBM), tiles_n = (int)((n + TBN - 1) / TBN);
-  for (int c0 = 0; c0 < count; c0 += MAXL) {
-    const int cnt = count - c0 < MAXL ? count - c0 : MAXL;
-    TmaBatch tb;
-    for (int i = 0; i < cnt; ++i) {
-      const LeafNode& lf = host_leaves[c0 + i];
-      int64_t lda, ldb;
-      const float* A = op_ptr<const float>(b, lf.a, lda);
-      const float* B = op_ptr<const float>(b, lf.b, ldb);
-      const size_t li = (size_t)(c0 + i);
-      cuuint32_t estr[2] = {1, 1};
-      auto enc = [&](CUtensorMap* map, const float* base, int64_t inner, int64_t outer, int64_t ld,
-                     int bi, int bo, CUtensorMapSwizzle sw) {
-        cuuint64_t dims[2] = {(cuuint64_t)(inner > 0 ? inner : 1), (cuuint64_t)(outer > 0 ? outer : 1)};
-        cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
-        cuuint32_t box[2] = {(cuuint32_t)bi, (cuuint32_t)bo};
-        return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-      };
-      static const CUtensorMapSwizzle bsw = getenv("FMM_MN_SW128_PLAIN") ? CU_TENSOR_MAP_SWIZZLE_128B
-                                                                         : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
-      bool ok = enc(&tb.m[i][0], A, k, m, lda, TBK, TBM, CU_TENSOR_MAP_SWIZZLE_128B) &&
-                enc(&tb.m[i][1], a_lo + li * m * k4, k, m, k4, TBK, TBM, CU_TENSOR_MAP_SWIZZLE_128B) &&
-                enc(&tb.m[i][2], B, n, k, ldb, 32, TBK, bsw) &&
-                enc(&tb.m[i][3], b_lo + li * k * n4, n, k, n4, 32, TBK, bsw);
-      if (!ok) return cudaErrorInvalidValue;
-    }
-    k2_tf32_v2<<<dim3((unsigned)(tiles_m * tiles_n), (unsigned)cnt), 256, SMEM_BYTES, st>>>(
-        tb, dev_leaves + c0, b, m, n, k, tiles_n, passes);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
-  return cudaSuccess;
 }
 
 }  // namespace fmm

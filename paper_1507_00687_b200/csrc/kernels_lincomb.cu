@@ -598,174 +598,7 @@ inline dim3 grid_for(const Step& s, int vec) {
 
 }  // namespace
 
-// ---- K1, TMA-staged persistent variant (opt-in: FMM_K1_TMA=1) ---------------------------------
-// Measured 2.8 TB/s vs the grid kernel's 6.56 (tools/bench_passes.py; one 128 KB double-buffered
-// stage per SM and a single issuing thread keep too few bytes in flight); kept for reference.
-// One CTA per SM loops over work items (node, 4-row group, 4 KB column chunk).  Thread 0 stages
-// every needed input block's row segments into shared memory with 1-D bulk copies
-// (cp.async.bulk, completion counted on an mbarrier) for the NEXT item while all threads form
-// the current item's outputs from shared memory (K1's sequential +-1 sums, bitwise the grid
-// kernel) and store them with coalesced 16-byte writes.  Two stage buffers of 4 blocks x 4 rows
-// x 4 KB.  Needs 16-byte aligned rows / chunks (the vector path).
-constexpr int TK_ROWS = 4, TK_BYTES = 4096, TK_NBLK = 4;
-
-__device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-template <typename T>
-__global__ void __launch_bounds__(kThreads, 1)
-    k1_tma(const K1Node* __restrict__ nodes, int count, int64_t items, const double* __restrict__ coef_all,
-           Bases bases, int R) {
-  constexpr int CW = TK_BYTES / (int)sizeof(T);  // elements per column chunk
-  constexpr int VEC = 16 / (int)sizeof(T);
-  extern __shared__ __align__(128) uint8_t tk_smem[];
-  T* stage = (T*)tk_smem;  // [2][TK_NBLK][TK_ROWS][CW]
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ T* optr[kMaxR];
-  __shared__ int64_t old[kMaxR];
-  __shared__ uint32_t code[kMaxR];
-  __shared__ int rlist[kMaxR];
-  __shared__ int nout_s, node_s;
-  const int tid = threadIdx.x;
-  if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s32(&bar[0])));
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s32(&bar[1])));
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-
-  // last node with item0 <= it: a CTA's items increase, so each stream (the staging issue and
-  // the compute) scans forward from its own last hit
-  int cur_issue = 0, cur_comp = 0;
-  auto find_node = [&](int64_t it, int& cur) {
-    while (cur + 1 < count && nodes[cur + 1].item0 <= it) ++cur;
-    return cur;
-  };
-  // decompose item -> (node, row0, col0, ncols)
-  auto decode = [&](int64_t it, int& cur, int& ni, int64_t& r0, int64_t& c0, int64_t& nc) {
-    ni = find_node(it, cur);
-    const K1Node& nd = nodes[ni];
-    const int64_t local = it - nd.item0;
-    const int64_t chunks = (nd.cols + CW - 1) / CW;
-    r0 = (local / chunks) * TK_ROWS;
-    c0 = (local % chunks) * CW;
-    nc = nd.cols - c0 < CW ? nd.cols - c0 : CW;
-  };
-  // thread 0: stage item `it` into buffer `buf`
-  auto issue = [&](int64_t it, int buf) {
-    int ni;
-    int64_t r0, c0, nc;
-    decode(it, cur_issue, ni, r0, c0, nc);
-    const K1Node& nd = nodes[ni];
-    int64_t ldi;
-    const T* in = op_ptr<const T>(bases, nd.in, ldi);
-    const int P = nd.P, nblk = nd.P * nd.Q;
-    const uint32_t need = nd.need;
-    const int nrow = nd.rows - r0 < TK_ROWS ? (int)(nd.rows - r0) : TK_ROWS;
-    const uint32_t bytes = (uint32_t)(nc * sizeof(T));
-    uint32_t total = 0;
-    for (int b2 = 0; b2 < nblk; ++b2)
-      if ((need >> b2) & 1u) total += bytes * nrow;
-    const uint32_t bb = s32(&bar[buf]);
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bb), "r"(total) : "memory");
-    for (int b2 = 0; b2 < nblk; ++b2) {
-      if (!((need >> b2) & 1u)) continue;
-      const int pp = b2 % P, qq = b2 / P;
-      for (int r = 0; r < nrow; ++r) {
-        const T* src = in + (pp * nd.rows + r0 + r) * ldi + qq * nd.cols + c0;
-        T* dst = stage + (((size_t)buf * TK_NBLK + b2) * TK_ROWS + r) * CW;
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-            ::"r"(s32(dst)), "l"(src), "r"(bytes), "r"(bb) : "memory");
-      }
-    }
-  };
-
-  int64_t it = blockIdx.x;
-  if (it >= items) return;
-  if (tid == 0) issue(it, 0);
-  uint32_t phase[2] = {0u, 0u};
-  for (int buf = 0; it < items; buf ^= 1) {
-    const int64_t nxt = it + gridDim.x;
-    if (tid == 0 && nxt < items) issue(nxt, buf ^ 1);  // buffer buf^1 was released by the last barrier
-    int ni;
-    int64_t r0, c0, nc;
-    decode(it, cur_comp, ni, r0, c0, nc);
-    const K1Node& nd = nodes[ni];
-    if (tid < nd.nout) {
-      const int r = nd.rlist[tid];
-      int64_t ldo;
-      optr[tid] = op_ptr<T>(bases, nd.out[r], ldo);
-      old[tid] = ldo;
-      code[tid] = nd.code[tid];
-      rlist[tid] = r;
-    }
-    if (tid == 0) { nout_s = nd.nout; node_s = ni; }
-    // wait for this item's bytes
-    {
-      const uint32_t bb = s32(&bar[buf]);
-      uint32_t done = 0;
-      while (!done) {
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-                     " selp.u32 %0, 1, 0, p;\n}\n"
-                     : "=r"(done) : "r"(bb), "r"(phase[buf]) : "memory");
-      }
-      phase[buf] ^= 1u;
-    }
-    __syncthreads();
-    const int nout = nout_s;
-    const int nrow = nd.rows - r0 < TK_ROWS ? (int)(nd.rows - r0) : TK_ROWS;
-    const int nblk = nd.P * nd.Q;
-    for (int e0 = tid * VEC; e0 < nc; e0 += kThreads * VEC) {
-      for (int r = 0; r < nrow; ++r) {
-        Vec<T, VEC> x[TK_NBLK];
-#pragma unroll
-        for (int b2 = 0; b2 < TK_NBLK; ++b2)
-          if (b2 < nblk && ((nd.need >> b2) & 1u))
-            x[b2] = ld_vec<T, VEC>(stage + (((size_t)buf * TK_NBLK + b2) * TK_ROWS + r) * CW + e0);
-        for (int o = 0; o < nout; ++o) {
-          const uint32_t c = code[o];
-          Vec<T, VEC> acc;
-          bool started = false;
-#pragma unroll
-          for (int b2 = 0; b2 < TK_NBLK; ++b2) {
-            const uint32_t cb = (c >> (2 * b2)) & 3u;
-            if (cb == 0u) continue;
-            if (cb == 3u) {
-              const T ut = (T)coef_all[nd.coef_off + b2 * R + rlist[o]];
-#pragma unroll
-              for (int e = 0; e < VEC; ++e)
-                acc.v[e] = started ? add_rn<T>(acc.v[e], mul_rn<T>(ut, x[b2].v[e])) : mul_rn<T>(ut, x[b2].v[e]);
-            } else if (cb == 1u) {
-#pragma unroll
-              for (int e = 0; e < VEC; ++e) acc.v[e] = started ? add_rn<T>(acc.v[e], x[b2].v[e]) : x[b2].v[e];
-            } else {
-#pragma unroll
-              for (int e = 0; e < VEC; ++e) acc.v[e] = started ? add_rn<T>(acc.v[e], -x[b2].v[e]) : -x[b2].v[e];
-            }
-            started = true;
-          }
-          if (!started) {
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) acc.v[e] = (T)0;
-          }
-          st_vec<T, VEC>(optr[o] + (r0 + r) * old[o] + c0 + e0, acc);
-        }
-      }
-    }
-    __syncthreads();  // buffer `buf` and the output list are free
-    it = nxt;
-  }
-}
-
 namespace {
-int k1_variant() {
-  static int v = [] {
-    const char* e = getenv("FMM_K1_VARIANT");
-    return e ? atoi(e) : 1;  // 4 rows per block, 2 in flight: 6.58 TB/s (tools/bench_passes.py)
-  }();
-  return v;
-}
-
 template <typename T, int VEC, int NBLK, int RPB, int RIF>
 void k1_go(const Step& s, const K1Node* nd, const double* dev_coef, const Bases& b, cudaStream_t st) {
   const int64_t cv = (s.cols + VEC - 1) / VEC;
@@ -774,26 +607,7 @@ void k1_go(const Step& s, const K1Node* nd, const double* dev_coef, const Bases&
   k1_lincomb<T, VEC, NBLK, RPB, RIF><<<grid, kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
 }
 
-template <typename T, int VEC, int NBLK>
-void k1_pick(const Step& s, const K1Node* nd, const double* dev_coef, const Bases& b, cudaStream_t st) {
-  switch (k1_variant()) {
-    case 2: k1_go<T, VEC, NBLK, 8, 2>(s, nd, dev_coef, b, st); break;
-    case 3: k1_go<T, VEC, NBLK, 16, 2>(s, nd, dev_coef, b, st); break;
-    case 4: k1_go<T, VEC, NBLK, 8, 4>(s, nd, dev_coef, b, st); break;
-    case 5: k1_go<T, VEC, NBLK, 16, 4>(s, nd, dev_coef, b, st); break;
-    case 6: k1_go<T, VEC, NBLK, 32, 2>(s, nd, dev_coef, b, st); break;
-    default: k1_go<T, VEC, NBLK, 4, 2>(s, nd, dev_coef, b, st); break;
-  }
-}
 }  // namespace
-
-int k1_tma_enabled() {
-  static int v = [] {
-    const char* e = getenv("FMM_K1_TMA");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
 
 template <typename T>
 cudaError_t launch_k1(const Step& s, const void* dev_nodes, const double* dev_coef,
@@ -806,17 +620,11 @@ cudaError_t launch_k1(const Step& s, const void* dev_nodes, const double* dev_co
     return cudaGetLastError();
   }
   const K1Node* nd = (const K1Node*)dev_nodes;
-  if (vec && s.P * s.Q <= 4 && s.items > 0 && k1_tma_enabled()) {
-    const size_t smem = (size_t)2 * TK_NBLK * TK_ROWS * TK_BYTES;
-    cudaError_t e = cudaFuncSetAttribute(k1_tma<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const int64_t g = s.items < 148 ? s.items : 148;
-    k1_tma<T><<<(unsigned)g, kThreads, smem, st>>>(nd, s.count, s.items, dev_coef, b, s.R);
-    return cudaGetLastError();
-  }
+  // 4 rows per block, 2 in flight: 6.58 TB/s (tools/bench_passes.py, the fastest of the
+  // round-1 rows-per-block sweep)
   if (s.P * s.Q <= 4) {
-    if (vec) k1_pick<T, V, 4>(s, nd, dev_coef, b, st);
-    else k1_pick<T, 1, 4>(s, nd, dev_coef, b, st);
+    if (vec) k1_go<T, V, 4, 4, 2>(s, nd, dev_coef, b, st);
+    else k1_go<T, 1, 4, 4, 2>(s, nd, dev_coef, b, st);
   } else {
     if (vec) k1_go<T, V, kMaxBlk, 4, 1>(s, nd, dev_coef, b, st);
     else k1_go<T, 1, kMaxBlk, 4, 1>(s, nd, dev_coef, b, st);

@@ -46,7 +46,6 @@ SIGNATURES = {
     "fmm_plan_set_shard_depth": (_I, [_P, _I]),
     "fmm_plan_set_comm_mode": (_I, [_P, _I]),
     "fmm_rule_transform": (_I, [_P, _I, C.POINTER(_P)]),
-    "fmm_plan_set_operand_fusion": (_I, [_P, _I]),
     "fmm_plan_set_k1_levels": (_I, [_P, _I]),
     "fmm_plan_sym_bytes": (_I, [_P, _P]),
     "fmm_plan_sym_alloc": (_I, [_P, _P]),
@@ -79,6 +78,7 @@ SIGNATURES = {
     "fmm_plan_last_scaling_steps": (_I, [_P, _P, C.POINTER(_I), _P]),
     "fmm_comm_unique_id": (_I, [_P]),
     "fmm_plan_set_comm": (_I, [_P, _P, _I, _I]),
+    "fmm_plan_set_barrier": (_I, [_P, _P, _P]),
     "fmm_last_error": (C.c_char_p, []),
     "fmm_version": (C.c_char_p, []),
 }
@@ -305,14 +305,8 @@ class Plan:
         return {"xi": xi.value, "delta": de.value, "uniform_bound": ub.value}
 
     def set_fusion(self, mode):
-        """Leaf-product epilogue fusion of the parents' W-combination:
-        'off' | 'on' | 'auto' | 'persistent' (the stream-K form, K2P)."""
-        _call("fmm_plan_set_fusion", self._h, {"off": 0, "on": 1, "auto": 2, "persistent": 3}[mode])
-        self._ws = None
-
-    def set_operand_fusion(self, enable: bool = True):
-        """Form S_r / T_r with <= 2 +-1 terms inside the fused leaf kernel (no K1 writes)."""
-        _call("fmm_plan_set_operand_fusion", self._h, int(enable))
+        """Leaf-product epilogue fusion of the parents' W-combination: 'off' | 'on' | 'auto'."""
+        _call("fmm_plan_set_fusion", self._h, {"off": 0, "on": 1, "auto": 2}[mode])
         self._ws = None
 
     def set_k1_levels(self, levels: int = 2):
@@ -381,6 +375,25 @@ class Plan:
     def set_comm(self, uid: bytes, rank: int, nranks: int):
         buf = C.create_string_buffer(bytes(uid), 128)
         _call("fmm_plan_set_comm", self._h, buf, rank, nranks)
+        self._ws = None
+
+    BARRIER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p)
+
+    def set_barrier(self, fn):
+        """Comm mode 3's barrier as a Python callable fn(stream_ptr) -> None (raising = failure),
+        or None for the NCCL barrier (fmm_plan_set_barrier)."""
+        if fn is None:
+            self._barrier = None
+            _call("fmm_plan_set_barrier", self._h, None, None)
+        else:
+            def tramp(_user, stream):
+                try:
+                    fn(stream)
+                    return 0
+                except Exception:  # noqa: BLE001 -- reported as FMM_E_NCCL by the library
+                    return 1
+            self._barrier = self.BARRIER_FN(tramp)  # kept alive with the plan
+            _call("fmm_plan_set_barrier", self._h, C.cast(self._barrier, C.c_void_p), None)
         self._ws = None
 
     def workspace(self, device=None):

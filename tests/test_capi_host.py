@@ -155,17 +155,6 @@ def test_shard_depth_units_and_balance():
         p.set_shard_depth(4)
 
 
-def test_operand_fusion_skips_leaf_level_formation():
-    # Strassen: every U / V column has <= 2 +-1 entries, so the leaf level's K1 writes nothing
-    s = fb.Rule.builtin("strassen")
-    p = fb.Plan([s] * 3, 2048, 2048, 2048)
-    p.set_fusion("on")
-    n0, w0 = p.launch_count(), p.workspace_bytes()
-    p.set_operand_fusion(True)
-    assert p.launch_count() == n0 - 1  # no leaf-level K1 (S and T) launch
-    assert p.workspace_bytes() < w0
-
-
 def test_bench_pass_byte_model():
     # bench.py's pipeline roofline counts the algorithmic pass bytes: one S-W
     # level on n^3: K1 reads the 4 quarter blocks of A and B and writes 4 non-trivial S and T;

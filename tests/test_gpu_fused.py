@@ -166,57 +166,6 @@ def test_shard_depth_virtual_ranks(fb, depth, nranks):
     assert oracle.parity_metric(total, ref, np.abs(A).max(), np.abs(B).max(), 256) <= TOL64
 
 
-@pytest.mark.parametrize("dims,names", [((2048, 2048, 2048), ("strassen",) * 3),
-                                        ((1536, 1024, 1280), ("winograd", "classical222")),
-                                        ((2 * 1000, 2 * 200, 2 * 600), ("winograd",))])
-def test_persistent_stream_k_equals_unfused(fb, dims, names):
-    # the persistent hybrid data-parallel / stream-K form (K2P): units split across CTAs are
-    # finished by their owner from the other CTAs' scratch in ascending r -- bitwise the
-    # unfused K2 + K3 (includes ragged tiles: 1000 / 600 are not multiples of 128)
-    M, K, N = dims
-    A, B = fi.random_pair(M, K, N, seed=M // 7)
-    pf = plan(fb, names, M, K, N, "persistent")
-    assert pf.fused_launches() >= 1
-    Cf = exe(pf, A, B)
-    Cu = exe(plan(fb, names, M, K, N, "off"), A, B)
-    assert np.array_equal(Cf, Cu)
-    assert np.array_equal(Cf, exe(pf, A, B))  # deterministic across runs
-    assert np.array_equal(Cf, exe(plan(fb, names, M, K, N, "on"), A, B))
-
-
-@pytest.mark.parametrize("pname", sorted(PLANS))
-def test_persistent_small_problems(fb, pname):
-    # fewer product-tiles than CTAs: most units are split over several CTAs (chains of scratch
-    # products finished by the owner)
-    names = PLANS[pname]
-    A, B = fi.random_pair(512, 384, 256, seed=23)
-    Cp = exe(plan(fb, names, 512, 384, 256, "persistent"), A, B)
-    assert np.array_equal(Cp, exe(plan(fb, names, 512, 384, 256, "off"), A, B))
-
-
-@pytest.mark.parametrize("pname", sorted(PLANS))
-@pytest.mark.parametrize("dims", [(512, 384, 256), (4 * 75, 4 * 33, 4 * 41)])
-def test_operand_fusion_bitwise(fb, pname, dims):
-    # S_r / T_r with <= 2 +-1 terms combined in shared memory while staging (K2O): bitwise the
-    # unfused path (K1's sequential sum); odd leaf dims exercise the 8-byte path
-    names = PLANS[pname]
-    M, K, N = dims
-    A, B = fi.random_pair(M, K, N, seed=M + 3)
-    po = plan(fb, names, M, K, N, "on")
-    po.set_operand_fusion(True)
-    Co = exe(po, A, B)
-    assert np.array_equal(Co, exe(plan(fb, names, M, K, N, "off"), A, B))
-
-
-def test_operand_fusion_C2_full_size(fb):
-    A, B = fi.config_inputs("C2")
-    po = plan(fb, ("strassen",) * 4, 4096, 4096, 4096, "auto")
-    po.set_operand_fusion(True)
-    pu = plan(fb, ("strassen",) * 4, 4096, 4096, 4096, "off")
-    assert po.workspace_bytes() < pu.workspace_bytes()
-    assert np.array_equal(exe(po, A, B), exe(pu, A, B))
-
-
 @pytest.mark.parametrize("dims,names", [((2048, 2048, 2048), ("winograd",) * 3),   # chunks 4 + 3
                                         ((3072, 3072, 3072), ("winograd",) * 2)])  # chunks 3 + 3 + 1
 def test_split_chains_equal_unfused(fb, dims, names):
