@@ -184,16 +184,29 @@ def make_plan(fb, cfg: str, dtype: str = "f64", leaf=None, scaling: str = "none"
 
 
 # ------------------------------------------------------------------------------------------
-def cpu_baseline(A_host, B_host, plan_rules, M, K, N, C_gpu_host=None, target_s=15.0):
+def cpu_baseline(A_host, B_host, plan_rules, M, K, N, C_gpu_host=None, target_s=15.0,
+                 scaling="none"):
     """The CPU oracle, as it stands, on a bounded row/column sample of the same workload:
     rows G = lift_rows(leaf rows), columns H = lift_cols(leaf cols) (bitwise the oracle's own
-    entries of C, oracle.fmm_sub).  Value = 2 |G| |H| K / t."""
+    entries of C, oracle.fmm_sub).  Value = 2 |G| |H| K / t.  With scaling, the oracle first
+    scales the whole operands (Alg. 1-3, O(MK + KN) work, timed separately as
+    `scale_seconds`), runs the sampled FMM on A', B' and unscales the sampled entries -- again
+    bitwise the oracle's own entries."""
     import numpy as np
     import oracle
     from oracle import rules as OR
     plan = OR.Plan.uniform([OR.builtin(n) for n in plan_rules])
     A = A_host.numpy() if hasattr(A_host, "numpy") else A_host
     B = B_host.numpy() if hasattr(B_host, "numpy") else B_host
+    sc = None
+    t_scale = 0.0
+    if scaling != "none":
+        t0 = time.perf_counter()
+        cfg = scaling_config(scaling)
+        sc = oracle.scale_operands(A, B, scaling, pow2=bool(cfg["pow2"]), tau=cfg["tau"],
+                                   max_steps=cfg["max_steps"])
+        t_scale = time.perf_counter() - t0
+    As, Bs = (A, B) if sc is None else (sc["A"], sc["B"])
     pm, _, pn = plan.dims_divisor()
     # calibrate: one leaf row/col first, doubling both (about 4x the work each time) until one
     # run takes >= target_s / 2: the reported run is then 7.5-30 s of CPU work at target 15 s
@@ -202,8 +215,8 @@ def cpu_baseline(A_host, B_host, plan_rules, M, K, N, C_gpu_host=None, target_s=
     while True:
         G = oracle.lift_rows(M, plan, range(nr))
         H = oracle.lift_cols(N, plan, range(nr))
-        Ag = np.ascontiguousarray(A[G, :])
-        Bh = np.ascontiguousarray(B[:, H])
+        Ag = np.ascontiguousarray(As[G, :])
+        Bh = np.ascontiguousarray(Bs[:, H])
         t0 = time.perf_counter()
         Cs = oracle.fmm(Ag, Bh, plan)
         t = time.perf_counter() - t0
@@ -212,11 +225,16 @@ def cpu_baseline(A_host, B_host, plan_rules, M, K, N, C_gpu_host=None, target_s=
             break
         nr *= 2
     nr, G, H, Cs, t = res
+    if sc is not None:
+        Cs = oracle.unscale(Cs, sc["dA"][G], sc["dB"][H])
     flops = 2.0 * len(G) * len(H) * K
     out = {"value": flops / t / 1e9, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
            "sample": f"C[G,H] with |G|={len(G)} rows x |H|={len(H)} cols (leaf rows/cols 0..{nr - 1} "
                      f"lifted through all levels; oracle.fmm_sub, bitwise the full oracle's entries)",
            "seconds": t}
+    if sc is not None:
+        out["scale_seconds"] = t_scale
+        out["scaling_steps"] = int(sc["steps"])
     if C_gpu_host is not None:
         Cg = C_gpu_host[np.ix_(G, H)]
         out["parity_sampled"] = oracle.parity_metric(Cg, Cs, float(np.abs(A).max()),
@@ -226,10 +244,47 @@ def cpu_baseline(A_host, B_host, plan_rules, M, K, N, C_gpu_host=None, target_s=
         g, h = G[:64], H[:64]
         hi, lo = oracle.ref_dd(np.ascontiguousarray(A[g, :]), np.ascontiguousarray(B[:, h]))
         scale = float(np.abs(hi).max()) or 1.0
-        err = lambda X: float(np.max(np.abs((X.astype(np.float64) - hi) - lo)) / scale)
-        out["error_vs_dd"] = {"gpu": err(Cg[:64, :64]), "oracle": err(Cs[:64, :64]),
-                              "measure": "max |C - C_dd| / max |C_dd| over 64 x 64 sampled entries"}
+        nz = hi != 0
+
+        def err(X):
+            d = np.abs((X.astype(np.float64) - hi) - lo)
+            return {"normwise": float(np.max(d) / scale),
+                    "max_rel": float(np.max(d[nz] / np.abs(hi[nz]))) if nz.any() else 0.0}
+
+        eg, eo = err(Cg[:64, :64]), err(Cs[:64, :64])
+        out["error_vs_dd"] = {"gpu": eg["normwise"], "oracle": eo["normwise"],
+                              "gpu_max_rel": eg["max_rel"], "oracle_max_rel": eo["max_rel"],
+                              "measure": "max |C - C_dd| / max |C_dd| (and max |C - C_dd| / |C_dd|) "
+                                         "over 64 x 64 sampled entries"}
+        if sc is not None:
+            # componentwise Thm 4.3 bound through the exact power-of-two unscale (SURVEY §8(c)
+            # C-tol: the normalised metric is vacuous for skewed magnitudes)
+            from oracle import rules as R2
+            f = float(R2.uniform_bound_factor([OR.builtin(n) for n in plan_rules], K))
+            bnd = f * 2.0 ** -53 * float(np.abs(sc["A"]).max()) * float(np.abs(sc["B"]).max()) * \
+                np.outer(sc["dA"][G], sc["dB"][H])
+            d = np.abs(Cg.astype(np.float64) - Cs)
+            nzc = Cs != 0  # exact zeros (cancellation in the unscaled modes) excluded
+            out["componentwise"] = {"max_rel_gpu_vs_oracle": float(np.max(d[nzc] / np.abs(Cs[nzc]))) if nzc.any() else 0.0,
+                                    "max_ratio_to_2x_thm_bound": float(np.max(d / (2 * bnd)))}
     return out
+
+
+def parity_record(cpu, dtype):
+    """The bench line's parity object from the cpu_baseline sample: the north star's metric and
+    tolerance, plus (scaled runs) the componentwise check against twice the Thm 4.3 bound."""
+    if not cpu or "parity_sampled" not in cpu:
+        return None
+    tol = 1e-13 if dtype == "f64" else 5e-5
+    rec = {"metric": "||C_gpu - C_oracle||_max / (||A||_max ||B||_max K) on the cpu_baseline "
+                     "sample (BASELINE north_star tolerance)",
+           "value": cpu["parity_sampled"], "tolerance": tol}
+    ok = cpu["parity_sampled"] <= tol
+    if "componentwise" in cpu:
+        rec["componentwise"] = cpu["componentwise"]
+        ok = ok and cpu["componentwise"]["max_ratio_to_2x_thm_bound"] <= 1.0
+    rec["pass"] = bool(ok)
+    return rec
 
 
 # ------------------------------------------------------------------------------------------
@@ -650,8 +705,8 @@ def run_fmm(args):
         Bn = B_h.numpy() if args.dtype == "f64" else B_h.double().numpy()
         if args.dtype == "f32":
             An, Bn = A_h.numpy(), B_h.numpy()
-        cpu = cpu_baseline(An, Bn, rules, M, K, N, C_gpu_host=Cg if args.scaling == "none" else None,
-                           target_s=args.cpu_seconds)
+        cpu = cpu_baseline(An, Bn, rules, M, K, N, C_gpu_host=Cg, target_s=args.cpu_seconds,
+                           scaling=args.scaling)
 
     if rank == 0:
         line = {
@@ -671,11 +726,7 @@ def run_fmm(args):
                        "k3_fused_in_leaf_epilogue": bool(fused),
                        **({"scaling_steps_taken": plan.last_scaling_steps(ws=wsp, stream=stream)}
                           if args.scaling != "none" and ws == 1 else {})},
-            "parity": ({"metric": "||C_gpu - C_oracle||_max / (||A||_max ||B||_max K) on the "
-                                  "cpu_baseline sample (BASELINE north_star tolerance)",
-                        "value": cpu["parity_sampled"], "tolerance": 1e-13 if args.dtype == "f64" else 5e-5,
-                        "pass": bool(cpu["parity_sampled"] <= (1e-13 if args.dtype == "f64" else 5e-5))}
-                       if cpu and "parity_sampled" in cpu else None),
+            "parity": parity_record(cpu, args.dtype),
             "roofline": roofline, "pipeline_roofline": pipeline, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": clocks,
             "gpu_launches": plan.launch_count() * args.steps,

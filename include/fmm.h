@@ -390,6 +390,17 @@ fmm_status fmm_comm_unique_id(void* out128);
  * loaded or the init fails. */
 fmm_status fmm_plan_set_comm(fmm_plan* plan, const void* id128, int rank, int nranks);
 
+/* Virtual scaling (host-only; default on).  With power-of-two factors (fmm_scaling.pow2 = 1) the
+ * whole scaling run (Alg. 1-3) is one cooperative kernel whose steps read the
+ * ORIGINAL A and B with the factors applied on the fly (exact: multiplication by powers of two),
+ * and the root's S / T formation applies the final factors while it reads A and B, so A' and
+ * B' are never written (the paper's "delay updating actual matrix entries").  Results
+ * are bitwise those of the materialised form (A', B' written, then the recursion), which the
+ * kernel switches to on device whenever an intermediate would not be exact.  enable = 0 forces
+ * the materialised form (same kernel, A', B' written at the end).  Plans without power-of-two
+ * factors, with zero padding, FP32 or L = 0 always materialise. */
+fmm_status fmm_plan_set_virtual_scaling(fmm_plan* plan, int enable);
+
 /* Comm mode 3's barrier, injected (host-only).  fmm_execute calls fn(user, stream) twice per
  * call -- after this rank's products are enqueued, and after its combine -- instead of the
  * 1-word ncclAllReduce; fn must return only when every rank has enqueued up to the same point

@@ -292,34 +292,39 @@ def unscale(Cp, dA, dB):
 SCALE_MODES = ("none", "outside", "inside", "out_in", "in_out", "repeated")
 
 
-def scaled_fmm(A, B, plan: Plan, mode="none", pow2=False, tau=1.0, max_steps=20):
-    """Scaling wrapper + FMM + unscale (Alg. 1-3).  out_in / in_out = one O then one I step (or
-    reverse) = Alg. 3 with max_steps=2 and no stop test reached.  Returns (C, info); info holds
-    the step count, the factors dA, dB and the scaled operands A', B'."""
+def scale_operands(A, B, mode="none", pow2=False, tau=1.0, max_steps=20):
+    """The scaling half of Alg. 1-3: returns dict(A=A', B=B', dA, dB, steps) with
+    A' = D_A^-1 A D, B' = D^-1 B D_B^-1 (D folded into A', B'; P:745-748, P:862-866,
+    P:940-956).  out_in / in_out = one O then one I step (or reverse) = Alg. 3 with
+    max_steps=2 and no stop test reached."""
     A = np.asarray(A, dtype=np.float64)
     B = np.asarray(B, dtype=np.float64)
     M, K = A.shape
     N = B.shape[1]
-    info = {"steps": 0, "A": A, "B": B, "dA": np.ones(M), "dB": np.ones(N)}
     if mode == "none":
-        return fmm(A, B, plan), info
+        return dict(A=A, B=B, dA=np.ones(M), dB=np.ones(N), steps=0)
     if mode == "outside":
         Ap, Bp, dA, dB = scale_outside(A, B, pow2)
-        info["steps"] = 1
-    elif mode == "inside":
+        return dict(A=Ap, B=Bp, dA=dA, dB=dB, steps=1)
+    if mode == "inside":
         Ap, Bp, _ = scale_inside(A, B, pow2)
-        dA, dB = np.ones(M), np.ones(N)
-        info["steps"] = 1
-    else:
-        first_O = mode in ("out_in", "repeated")
-        steps = 2 if mode in ("out_in", "in_out") else max_steps
-        tau_eff = tau if mode == "repeated" else -1.0  # fixed 2-step modes: no stop test
-        res = scale_repeated(A, B, first_O=first_O, tau=tau_eff, max_steps=steps, pow2=pow2)
-        Ap, Bp, dA, dB = res["A"], res["B"], res["dA"], res["dB"]
-        info["steps"] = res["steps"]
-    Cp = fmm(Ap, Bp, plan)
-    info.update(dA=dA, dB=dB, A=Ap, B=Bp)  # the scaled operands A', B' the FMM ran on
-    return unscale(Cp, dA, dB), info
+        return dict(A=Ap, B=Bp, dA=np.ones(M), dB=np.ones(N), steps=1)
+    first_O = mode in ("out_in", "repeated")
+    steps = 2 if mode in ("out_in", "in_out") else max_steps
+    tau_eff = tau if mode == "repeated" else -1.0  # fixed 2-step modes: no stop test
+    res = scale_repeated(A, B, first_O=first_O, tau=tau_eff, max_steps=steps, pow2=pow2)
+    return dict(A=res["A"], B=res["B"], dA=res["dA"], dB=res["dB"], steps=res["steps"])
+
+
+def scaled_fmm(A, B, plan: Plan, mode="none", pow2=False, tau=1.0, max_steps=20):
+    """Scaling wrapper + FMM + unscale (Alg. 1-3; Alg. 1 line 5 read as C' = A'B', DESIGN.md
+    reading A5).  Returns (C, info); info holds the step count, the factors dA, dB and the
+    scaled operands A', B' the FMM ran on."""
+    info = scale_operands(A, B, mode, pow2, tau, max_steps)
+    Cp = fmm(info["A"], info["B"], plan)
+    if mode == "none":
+        return Cp, info
+    return unscale(Cp, info["dA"], info["dB"]), info
 
 
 # ---------------------------------------------------------------------------------------------

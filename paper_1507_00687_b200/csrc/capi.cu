@@ -30,11 +30,14 @@ bool transform_rule(const RuleData& d, int kind, RuleData* out);
 bool builtin_rule(const std::string& name, RuleData* out);
 size_t scale_ws_bytes(int64_t M, int64_t K, int64_t N);
 int* scale_flags_ptr(void* ws, int64_t M, int64_t K, int64_t N);
-cudaError_t run_scaling(int64_t M, int64_t K, int64_t N, const double* A, int64_t lda,
-                        const double* B, int64_t ldb, double* A_out, int64_t lda_out,
-                        double* B_out, int64_t ldb_out, double* dA, double* dB, double* dI,
-                        const char* steps, int nsteps, bool first_O, double tau, int pow2,
-                        void* sws, cudaStream_t st);
+cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, int64_t lda,
+                             const double* B, int64_t ldb, double* A_out, int64_t lda_out,
+                             double* B_out, int64_t ldb_out, double* dA, double* dB, double* dI,
+                             int nsteps, bool first_O, double tau, int pow2, int materialise_end,
+                             void* sws, unsigned int* bar, cudaStream_t st);
+void scale_virtual_view(void* sws, int64_t M, int64_t K, int64_t N, const int32_t** exAr,
+                        const int32_t** exAc, const int32_t** exBr, const int32_t** exBc,
+                        const int** mode_flag);
 cudaError_t launch_unscale(double* C, int64_t ldc, int64_t M, int64_t N, const double* dA,
                            const double* dB, cudaStream_t st);
 cudaError_t launch_scale_apply(int64_t M, int64_t K, int64_t N, const double* A, int64_t lda,
@@ -127,6 +130,10 @@ struct fmm_plan {
   bool split_chains = true;     // fused units' product chains split over CTAs (turnstiles)
   bool k1_two_level = true;     // S / T of two recursion levels formed in one pass (K1X2)
   bool k3_two_level = true;     // W-combination of two recursion levels in one pass (K3X2)
+  // virtual scaling (compile_plan): power-of-two factors applied by the root K1 while it forms
+  // S_r / T_r from the original A, B (the scaled A', B' are not written)
+  bool virt_scale = false;
+  bool virt_scale_enable = true;  // fmm_plan_set_virtual_scaling
   ncclComm_t comm = nullptr;
   // comm mode 3 barrier (fmm_plan_set_barrier): called instead of the 1-word NCCL all-reduce
   fmm_barrier_fn barrier_fn = nullptr;
@@ -257,6 +264,8 @@ struct Builder {
   // K1 for the active nodes of level l (columns in `only_r` if >= 0); returns child nodes.
   std::vector<Node> emit_k1(int l, const std::vector<Node>& nodes, int only_r, bool alloc_c = true) {
     const int64_t mb = p->lm[l + 1], kb = p->lk[l + 1], nb = p->ln[l + 1];
+    // virtual scaling: the root's children are scaled copies, never views of A / B
+    const bool noalias = l == 0 && p->virt_scale;
     std::vector<K1Node> ks, kt;
     std::vector<Node> kids;
     for (const Node& nd : nodes) {
@@ -274,14 +283,14 @@ struct Builder {
         Node ch;
         ch.idx = nd.idx * ru.R + r;
         int row;
-        if (trivial_col(ru, ru.U, ru.m0 * ru.k0, r, &row)) {
+        if (!noalias && trivial_col(ru, ru.U, ru.m0 * ru.k0, r, &row)) {
           ch.a = sub(nd.a, (row % ru.m0) * mb, (row / ru.m0) * kb);
         } else {
           ch.a = ws_op(ws_alloc(mb * kb), kb);
           s.out[r] = ch.a;
           s.out_mask |= 1u << r;
         }
-        if (trivial_col(ru, ru.V, ru.k0 * ru.n0, r, &row)) {
+        if (!noalias && trivial_col(ru, ru.V, ru.k0 * ru.n0, r, &row)) {
           ch.b = sub(nd.b, (row % ru.k0) * kb, (row / ru.k0) * nb);
         } else {
           ch.b = ws_op(ws_alloc(kb * nb), nb);
@@ -309,6 +318,7 @@ struct Builder {
       st.cols = ks.empty() ? nb : kt.empty() ? kb : std::max(kb, nb);
       const int blk = std::max(ks.empty() ? 0 : r0.m0 * r0.k0, kt.empty() ? 0 : r0.k0 * r0.n0);
       st.P = blk; st.Q = 1; st.R = r0.R;  // P * Q: max input sub-blocks of a node
+      st.scaled = noalias ? 1 : 0;
       p->steps.push_back(st);
     }
     return kids;
@@ -653,7 +663,7 @@ struct Builder {
     const bool fuse = fuse_leaves(npar);
     // two levels per K1 pass (K1X2), paired from the bottom: (L-2, L-1), (L-4, L-3), ...
     std::vector<bool> pair_at(p->L + 1, false);
-    for (int e = p->L - 2; e >= l; e -= 2) pair_at[e] = true;
+    for (int e = p->L - 2; e >= l; e -= 2) pair_at[e] = !(e == 0 && p->virt_scale);  // scaled root: one level
     for (int d = l; d < p->L;) {
       const int pr = pair_at[d] && p->k1_two_level ? k1x2_pair(d, lv.back()) : 0;
       if (pr) {
@@ -853,6 +863,10 @@ fmm_status compile_plan(fmm_plan* p) {
     delete p->df_twin;  // the twin copies the plan's settings: rebuilt on next use
     p->df_twin = nullptr;
   }
+  // virtual scaling needs the root to be a K1 pass over the caller's A, B: FP64 power-of-two
+  // factors, no zero padding, at least one recursion level
+  p->virt_scale = p->scaling.mode != FMM_SCALE_NONE && p->scaling.pow2 && !p->padded &&
+                  p->dtype == FMM_F64 && p->L >= 1 && p->virt_scale_enable;
   Builder b(p);
   b.build();
   p->fmm_ws_bytes = (size_t)b.ws_peak * elem_size(p->dtype);
@@ -967,7 +981,7 @@ struct TimedLaunch {
 // are offset accordingly; the FP32 hi / lo arena is reused by consecutive chunks.
 template <typename T>
 static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, const Bases& b,
-                               bool vec, cudaStream_t st) {
+                               bool vec, cudaStream_t st, const ScaleIn* sc) {
   size_t node_bytes = 0;
   switch (s.kind) {
     case STEP_K1: node_bytes = s.x2 ? sizeof(K1x2Node) : sizeof(K1Node); break;
@@ -982,7 +996,7 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
   const int64_t tiles_f = p->dtype == FMM_F32 ? ((s.rows + 127) / 128) * ((s.cols + 255) / 256)
                                               : ((s.rows + ts - 1) / ts) * ((s.cols + ts - 1) / ts);
   switch (s.kind) {
-    case STEP_K1: return launch_k1<T>(s, nd, p->dev_coef, b, vec, st);
+    case STEP_K1: return launch_k1<T>(s, nd, p->dev_coef, b, vec, st, sc);
     case STEP_K3: return launch_k3<T>(s, nd, p->dev_coef, b, vec, st);
     case STEP_ACC: return launch_acc<T>(s, nd, p->dev_coef, b, vec, st);
     case STEP_ZERO: return launch_zero<T>(s, nd, b, st);
@@ -1031,7 +1045,7 @@ static const char* step_name(const Step& s) {
 
 template <typename T>
 static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStream_t st,
-                            size_t i0 = 0, size_t i1 = (size_t)-1) {
+                            size_t i0 = 0, size_t i1 = (size_t)-1, const ScaleIn* sc = nullptr) {
   constexpr int64_t kMaxNodes = 32768;  // per launch (grid.y / grid.z <= 65535)
   if (i1 > p->steps.size()) i1 = p->steps.size();
   for (size_t si = i0; si < i1; ++si) {
@@ -1045,7 +1059,7 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
     for (int64_t c0 = 0; c0 < s.count && e == cudaSuccess; c0 += maxn) {
       Step sub = s;
       sub.count = (int)std::min<int64_t>(maxn, s.count - c0);
-      e = launch_step<T>(p, sub, c0, b, vec, st);
+      e = launch_step<T>(p, sub, c0, b, vec, st, sc);
     }
     if (e != cudaSuccess) return cuda_status(e, "fmm_execute launch");
   }
@@ -1083,20 +1097,22 @@ static fmm_status scale_common(int64_t M, int64_t K, int64_t N, const void* A, i
   void* own = nullptr;
   cudaError_t e = cudaSuccess;
   double *tdA = (double*)dA, *tdB = (double*)dB, *tdI = (double*)dI;
-  size_t need = scale_ws_bytes(M, K, N) + (size_t)(M + N + K) * 8 + 1024;
+  // layout: [scale workspace | grid-barrier word (256 B) | factor vectors the caller omitted]
+  size_t need = scale_ws_bytes(M, K, N) + 256 + (size_t)(M + N + K) * 8 + 1024;
   if (!ws) {
     e = cudaMallocAsync(&own, need, st);
     if (e != cudaSuccess) return cuda_status(e, "fmm_scale alloc");
   }
   uint8_t* w = (uint8_t*)(ws ? ws : own);
   w = (uint8_t*)(((uintptr_t)w + 255) & ~(uintptr_t)255);
-  uint8_t* extra = w + (scale_ws_bytes(M, K, N) + 255) / 256 * 256;
+  unsigned int* bar = (unsigned int*)(w + (scale_ws_bytes(M, K, N) + 255) / 256 * 256);
+  uint8_t* extra = (uint8_t*)bar + 256;
   if (!tdA) { tdA = (double*)extra; }
   if (!tdB) { tdB = (double*)extra + M; }
   if (!tdI) { tdI = (double*)extra + M + N; }
-  e = run_scaling(M, K, N, (const double*)A, lda, (const double*)B, ldb, (double*)A_out, lda_out,
-                  (double*)B_out, ldb_out, tdA, tdB, tdI, steps.data(), (int)steps.size(),
-                  steps[0] == 'O', tau, pow2, w, st);
+  e = run_scaling_coop(M, K, N, (const double*)A, lda, (const double*)B, ldb, (double*)A_out, lda_out,
+                       (double*)B_out, ldb_out, tdA, tdB, tdI, (int)steps.size(), steps[0] == 'O', tau,
+                       pow2, /*materialise_end=*/1, w, bar, st);
   int* flags = scale_flags_ptr(w, M, K, N);
   if (e == cudaSuccess && steps_dev)
     e = cudaMemcpyAsync(steps_dev, flags + 1, sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
@@ -1559,6 +1575,8 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
     if (!p->sym_own) { set_error("fmm_execute: comm mode 3 needs fmm_plan_sym_alloc"); return FMM_E_ARG; }
   }
   double *dA = nullptr, *dB = nullptr;
+  ScaleIn sin{};
+  const ScaleIn* sinp = nullptr;
   if (p->scaling.mode != FMM_SCALE_NONE) {
     double* Ap = (double*)wsb;
     double* Bp = Ap + p->M * p->K;
@@ -1566,17 +1584,30 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
     dB = dA + p->M;
     double* dI = dB + p->N;
     void* sws = (void*)(((uintptr_t)(dI + p->K) + 255) & ~(uintptr_t)255);
+    unsigned int* bar = (unsigned int*)((uint8_t*)sws + (scale_ws_bytes(p->M, p->K, p->N) + 255) / 256 * 256);
     std::string steps;
     double tau;
     scaling_steps(p->scaling, &steps, &tau);
     NvtxRange nv("fmm.scale");
     TimedLaunch tl(p, 6, st);
-    cudaError_t e = run_scaling(p->M, p->K, p->N, (const double*)A, lda, (const double*)B, ldb, Ap,
-                                p->K, Bp, p->N, dA, dB, dI, steps.data(), (int)steps.size(),
-                                steps[0] == 'O', tau, p->scaling.pow2, sws, st);
+    // Alg. 1-3 in one cooperative kernel; with virtual scaling the root K1 reads A, B and the
+    // exponents (or A', B' if the run had to materialise them), else A', B' are written
+    cudaError_t e = run_scaling_coop(p->M, p->K, p->N, (const double*)A, lda, (const double*)B, ldb,
+                                     Ap, p->K, Bp, p->N, dA, dB, dI, (int)steps.size(), steps[0] == 'O',
+                                     tau, p->scaling.pow2, p->virt_scale ? 0 : 1, sws, bar, st);
     if (e != cudaSuccess) return cuda_status(e, "fmm_execute scaling");
-    b.p[BASE_A] = Ap; b.p[BASE_B] = Bp;
-    b.ld[BASE_A] = p->K; b.ld[BASE_B] = p->N;
+    if (p->virt_scale) {
+      const int32_t *ear, *eac, *ebr, *ebc;
+      const int* mode;
+      scale_virtual_view(sws, p->M, p->K, p->N, &ear, &eac, &ebr, &ebc, &mode);
+      sin.er[0] = ear; sin.ec[0] = eac; sin.er[1] = ebr; sin.ec[1] = ebc;
+      sin.mat[0] = Ap; sin.mat[1] = Bp; sin.ldm[0] = p->K; sin.ldm[1] = p->N;
+      sin.mode = mode;
+      sinp = &sin;
+    } else {
+      b.p[BASE_A] = Ap; b.p[BASE_B] = Bp;
+      b.ld[BASE_A] = p->K; b.ld[BASE_B] = p->N;
+    }
   }
   if (p->padded) {  // zero-padded copies of A, B; the recursion writes a padded C
     const size_t es = (size_t)elem_size(p->dtype);
@@ -1600,7 +1631,8 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
   const bool vec = p->dims_vec_ok && aligned16(b.p[BASE_A]) && aligned16(b.p[BASE_B]) &&
                    aligned16(b.p[BASE_C]) && aligned16(b.p[BASE_WS]) && b.ld[BASE_A] % vecn == 0 &&
                    b.ld[BASE_B] % vecn == 0 && b.ld[BASE_C] % vecn == 0;
-  fmm_status s = p->dtype == FMM_F64 ? run_steps<double>(p, b, vec, st) : run_steps<float>(p, b, vec, st);
+  fmm_status s = p->dtype == FMM_F64 ? run_steps<double>(p, b, vec, st, 0, (size_t)-1, sinp)
+                                      : run_steps<float>(p, b, vec, st, 0, (size_t)-1, sinp);
   if (s != FMM_OK) return s;
   if (p->padded) {  // crop
     TimedLaunch tl(p, STEP_K3, st);
@@ -1667,6 +1699,12 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
     if (r != 0) { set_error(std::string(what) + ": " + (api->getErrorString ? api->getErrorString(r) : "?")); return FMM_E_NCCL; }
   }
   return FMM_OK;
+}
+
+fmm_status fmm_plan_set_virtual_scaling(fmm_plan* p, int enable) {
+  if (!p) { set_error("fmm_plan_set_virtual_scaling: null plan"); return FMM_E_ARG; }
+  p->virt_scale_enable = enable != 0;
+  return compile_plan(p);
 }
 
 fmm_status fmm_plan_set_barrier(fmm_plan* p, fmm_barrier_fn fn, void* user) {
@@ -2148,7 +2186,7 @@ fmm_status fmm_gemm(int dtype, int leaf, int64_t M, int64_t K, int64_t N, const 
 
 fmm_status fmm_scale_workspace_bytes(int64_t M, int64_t K, int64_t N, size_t* bytes) {
   if (!bytes) return FMM_E_ARG;
-  *bytes = scale_ws_bytes(M, K, N) + 512;
+  *bytes = scale_ws_bytes(M, K, N) + 1024;  // + alignment + the grid-barrier word
   return FMM_OK;
 }
 

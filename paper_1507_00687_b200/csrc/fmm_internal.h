@@ -34,6 +34,18 @@ struct Bases {
   int64_t ld[5];
 };
 
+// Virtual diagonal scaling (power-of-two factors): the root K1 reads the
+// ORIGINAL A (side 0) / B (side 1) and forms S_r / T_r from a_ij 2^(er_i + ec_j), i.e. from A' /
+// B' without either being written -- unless the one-kernel scaling run switched to its
+// materialised form (*mode != 0), in which case it reads A' / B' from mat[side] (ld ldm[side]).
+struct ScaleIn {
+  const int32_t* er[2];
+  const int32_t* ec[2];
+  const double* mat[2];
+  int64_t ldm[2];
+  const int* mode;
+};
+
 // Selects instead of b.p[o.base]: dynamic indexing of a by-value kernel parameter would force
 // a local-memory copy of Bases.
 template <typename T>
@@ -202,12 +214,13 @@ struct Step {
   int64_t turn_off = -1;
   int x2 = 0;        // K1 / K3: 0 one level (K1Node / K3Node); else K1x2Node / K3x2Node with
                      // rule pair (x2 - 1) / 3, (x2 - 1) % 3 (builtin_tables.h ids)
+  int scaled = 0;    // K1 of the root with virtual scaling (reads A / B through ScaleIn)
 };
 
 // ---- kernel launchers (kernels_*.cu) -----------------------------------------------------------
 template <typename T>
 cudaError_t launch_k1(const Step& s, const void* dev_nodes, const double* dev_coef,
-                      const Bases& b, bool vec, cudaStream_t st);
+                      const Bases& b, bool vec, cudaStream_t st, const ScaleIn* sc = nullptr);
 template <typename T>
 cudaError_t launch_k3(const Step& s, const void* dev_nodes, const double* dev_coef,
                       const Bases& b, bool vec, cudaStream_t st);

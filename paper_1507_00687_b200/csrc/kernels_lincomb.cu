@@ -81,11 +81,20 @@ constexpr int kRowsPerBlock = 4;
 // host into the node descriptor (k1_compile); threads 0..nout-1 resolve the output pointers in
 // parallel, so the per-block setup is one shared-memory round trip.  u*x with u = +-1 is exact,
 // so adding +-x is bitwise the oracle's  s + u*x.
-template <typename T, int VEC, int NBLK, int RPB, int RIF>
+// x 2^e correctly rounded (virtual scaling: one multiplication by an exact power of two)
+__device__ __forceinline__ double scale2(double x, int e) {
+  if (e == 0) return x;
+  if (e >= -1022 && e <= 1023) return __dmul_rn(x, __longlong_as_double((int64_t)(e + 1023) << 52));
+  return ldexp(x, e);
+}
+
+// SC: the root's K1 under virtual scaling (ScaleIn): inputs are the original A / B scaled on
+// load by 2^(er_i + ec_j) -- bitwise the materialised A' / B' -- or the materialised A' / B'.
+template <typename T, int VEC, int NBLK, int RPB, int RIF, bool SC = false>
 __global__ void __launch_bounds__(kThreads) k1_lincomb(const K1Node* __restrict__ nodes,
                                                        const double* __restrict__ coef_all,
                                                        Bases bases, int64_t rows, int64_t cols,
-                                                       int P, int Q, int R) {
+                                                       int P, int Q, int R, ScaleIn sc) {
   __shared__ T* optr[kMaxR];
   __shared__ int64_t old[kMaxR];
   __shared__ uint32_t code[kMaxR];
@@ -115,6 +124,28 @@ __global__ void __launch_bounds__(kThreads) k1_lincomb(const K1Node* __restrict_
   const int64_t jv = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * VEC;
   if (jv >= cols) return;
   const int64_t i0 = (int64_t)blockIdx.y * RPB;
+  // virtual scaling: the exponents of this thread's columns (fixed over its rows)
+  const int side = nd.in.base == BASE_B ? 1 : 0;
+  bool vscale = false;
+  const int32_t* ers = nullptr;
+  int ecv[NBLK][VEC];
+  if constexpr (SC) {
+    if (*sc.mode != 0) {  // the scaling run materialised A' / B'
+      in = (const T*)(side ? sc.mat[1] : sc.mat[0]) + nd.in.row0 * (side ? sc.ldm[1] : sc.ldm[0]) + nd.in.col0;
+      ldi = side ? sc.ldm[1] : sc.ldm[0];
+    } else {
+      vscale = true;
+      ers = (side ? sc.er[1] : sc.er[0]) + nd.in.row0;
+      const int32_t* ecs = (side ? sc.ec[1] : sc.ec[0]) + nd.in.col0;
+#pragma unroll
+      for (int b = 0; b < NBLK; ++b)
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+          const int q = b / P;
+          ecv[b][e] = (b < nblk && jv + e < cols) ? ecs[q * cols + jv + e] : 0;
+        }
+    }
+  }
 #pragma unroll 1
   for (int ii = 0; ii < RPB; ii += RIF) {
     Vec<T, VEC> x[RIF][NBLK];
@@ -126,6 +157,13 @@ __global__ void __launch_bounds__(kThreads) k1_lincomb(const K1Node* __restrict_
         if (b < nblk && ((need >> b) & 1u) && i < rows) {
           const int p = b % P, q = b / P;  // column-major block index
           x[h][b] = ld_vec<T, VEC>(in + (p * rows + i) * ldi + q * cols + jv);
+          if constexpr (SC) {
+            if (vscale) {
+              const int er = ers[p * rows + i];
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) x[h][b].v[e] = (T)scale2((double)x[h][b].v[e], er + ecv[b][e]);
+            }
+          }
         }
       }
     }
@@ -599,21 +637,33 @@ inline dim3 grid_for(const Step& s, int vec) {
 }  // namespace
 
 namespace {
-template <typename T, int VEC, int NBLK, int RPB, int RIF>
-void k1_go(const Step& s, const K1Node* nd, const double* dev_coef, const Bases& b, cudaStream_t st) {
+template <typename T, int VEC, int NBLK, int RPB, int RIF, bool SC = false>
+void k1_go(const Step& s, const K1Node* nd, const double* dev_coef, const Bases& b, cudaStream_t st,
+           const ScaleIn& sc = ScaleIn{}) {
   const int64_t cv = (s.cols + VEC - 1) / VEC;
   dim3 grid((unsigned)((cv + kThreads - 1) / kThreads), (unsigned)((s.rows + RPB - 1) / RPB),
             (unsigned)s.count);
-  k1_lincomb<T, VEC, NBLK, RPB, RIF><<<grid, kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R);
+  k1_lincomb<T, VEC, NBLK, RPB, RIF, SC><<<grid, kThreads, 0, st>>>(nd, dev_coef, b, s.rows, s.cols, s.P, s.Q, s.R, sc);
 }
 
 }  // namespace
 
 template <typename T>
 cudaError_t launch_k1(const Step& s, const void* dev_nodes, const double* dev_coef,
-                      const Bases& b, bool vec, cudaStream_t st) {
+                      const Bases& b, bool vec, cudaStream_t st, const ScaleIn* sc) {
   if (s.count == 0 || s.rows == 0 || s.cols == 0) return cudaSuccess;
   constexpr int V = 16 / sizeof(T);
+  if (sc && s.scaled && !s.x2) {  // the root under virtual scaling (FP64 plans only)
+    const K1Node* nd = (const K1Node*)dev_nodes;
+    if (s.P * s.Q <= 4) {
+      if (vec) k1_go<T, V, 4, 4, 2, true>(s, nd, dev_coef, b, st, *sc);
+      else k1_go<T, 1, 4, 4, 2, true>(s, nd, dev_coef, b, st, *sc);
+    } else {
+      if (vec) k1_go<T, V, kMaxBlk, 4, 1, true>(s, nd, dev_coef, b, st, *sc);
+      else k1_go<T, 1, kMaxBlk, 4, 1, true>(s, nd, dev_coef, b, st, *sc);
+    }
+    return cudaGetLastError();
+  }
   if (s.x2) {
     if (vec) k1x2_pick<T, V>(s, (const K1x2Node*)dev_nodes, b, st);
     else k1x2_pick<T, 1>(s, (const K1x2Node*)dev_nodes, b, st);
@@ -762,8 +812,8 @@ template cudaError_t launch_p2p_combine<double>(const double* const*, int, const
 template cudaError_t launch_p2p_combine<float>(const float* const*, int, const double*, int, int, int, int, int64_t, int64_t, float*, int64_t, int64_t, int64_t, bool, cudaStream_t);
 template cudaError_t launch_pad_copy<double>(const double*, int64_t, int64_t, int64_t, double*, int64_t, int64_t, int64_t, cudaStream_t);
 template cudaError_t launch_pad_copy<float>(const float*, int64_t, int64_t, int64_t, float*, int64_t, int64_t, int64_t, cudaStream_t);
-template cudaError_t launch_k1<double>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);
-template cudaError_t launch_k1<float>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);
+template cudaError_t launch_k1<double>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t, const ScaleIn*);
+template cudaError_t launch_k1<float>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t, const ScaleIn*);
 template cudaError_t launch_k3<double>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);
 template cudaError_t launch_k3<float>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);
 template cudaError_t launch_acc<double>(const Step&, const void*, const double*, const Bases&, bool, cudaStream_t);

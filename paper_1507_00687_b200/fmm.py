@@ -79,6 +79,7 @@ SIGNATURES = {
     "fmm_comm_unique_id": (_I, [_P]),
     "fmm_plan_set_comm": (_I, [_P, _P, _I, _I]),
     "fmm_plan_set_barrier": (_I, [_P, _P, _P]),
+    "fmm_plan_set_virtual_scaling": (_I, [_P, _I]),
     "fmm_last_error": (C.c_char_p, []),
     "fmm_version": (C.c_char_p, []),
 }
@@ -271,6 +272,11 @@ class Plan:
         return n.value
 
     STEP_KINDS = {1: "K1", 2: "K2", 3: "K3", 4: "ACC", 5: "ZERO", 6: "SCALE", 7: "REDUCE"}
+
+    def set_virtual_scaling(self, enable: bool = True):
+        """Power-of-two scaling applied on the fly by the root K1 (default) or materialised."""
+        _call("fmm_plan_set_virtual_scaling", self._h, int(enable))
+        self._ws = None
 
     def set_graph(self, enable: bool = True):
         """Replay fmm_execute as a CUDA graph for repeated calls with the same buffers."""

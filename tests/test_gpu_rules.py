@@ -135,3 +135,27 @@ def test_rotated_323_through_the_abi(fb, kind):
     Cg = p.execute(dev(A2), dev(B2)).cpu().numpy()
     Co = oracle.fmm(A2, B2, OPlan.uniform([orule, R.strassen()]))
     assert oracle.parity_metric(Cg, Co, np.abs(A2).max(), np.abs(B2).max(), 2 * K) <= TOL64
+
+
+def test_three_level_nonuniform_plan(fb):
+    # the 3-level non-uniform plan pinned on the oracle (test_oracle_exec.
+    # test_three_level_nonuniform_node_order): 57 node rules in BFS order through the C ABI,
+    # every schedule and fusion mode -- parity at a generic size, bitwise with leaf inner
+    # dimension 1 (the node -> rule order of the GPU plan must match the oracle's exactly)
+    from test_oracle_exec import _three_level_nonuniform
+    w, lvl1, lvl2 = _three_level_nonuniform()
+    nodes = [to_gpu_rule(fb, w)] + [to_gpu_rule(fb, r) for r in lvl1] + [to_gpu_rule(fb, r) for r in lvl2]
+    oplan = OPlan([[w], lvl1, lvl2])
+    for (M, K, N), check in (((512, 384, 256), "parity"), ((128, 8, 64), "bitwise")):
+        A, B = fi.random_pair(M, K, N, seed=K + 5)
+        Co = oracle.fmm(A, B, oplan)
+        for fusion, sched in (("off", "breadth"), ("on", "breadth"), ("on", "hybrid"), ("off", "depth"),
+                              ("auto", "auto")):
+            p = fb.Plan(nodes, M, K, N, uniform=False, levels=3)
+            p.set_fusion(fusion)
+            p.set_schedule(sched)
+            Cg = p.execute(dev(A), dev(B)).cpu().numpy()
+            if check == "parity":
+                assert oracle.parity_metric(Cg, Co, np.abs(A).max(), np.abs(B).max(), K) <= TOL64
+            else:
+                assert np.array_equal(Cg, Co), (fusion, sched)

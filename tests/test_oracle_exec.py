@@ -209,3 +209,51 @@ def test_dd_row_subset(orc):
     hi, lo = orc.ref_dd(A, B)
     hs, ls = orc.ref_dd(A, B, rows=[3, 11])
     assert np.array_equal(hs, hi[[3, 11]]) and np.array_equal(ls, lo[[3, 11]])
+
+
+def _three_level_nonuniform():
+    """Root S-W; level 1 (7 nodes, BFS index r1) and level 2 (49 nodes, BFS index 7 r1 + r2,
+    P:147-149) draw from ten 7-product 2x2x2 rules -- Strassen, its D'Alberto variant and the
+    eight Castrapel-Gustafson variants of S-W -- by a function of the index that
+    is not symmetric in (r1, r2), so a wrong mixed-radix node order changes which rule runs
+    where."""
+    w = R.winograd()
+    pool = [R.strassen(), R.strassen_dalberto()] + [
+        R.castrapel_gustafson(w, x, y, z) for x in (1, 2) for y in (1, 2) for z in (1, 2)]
+    lvl1 = [pool[(3 * r1 + 1) % 10] for r1 in range(7)]
+    lvl2 = [pool[(idx * idx + 3 * idx) % 10] for idx in range(49)]
+    return w, lvl1, lvl2
+
+
+def test_three_level_nonuniform_node_order(orc):
+    # The oracle's node -> rule mapping (BFS index idx * R + r at every level, P:144-152) at
+    # three levels, where idx = r1 (level 1) and idx = 7 r1 + r2 (level 2) differ from any
+    # other order.  Expectation composed here, level by level, from the oracle's building
+    # blocks (node_st, the classical leaf, node_c) with the BFS index written out explicitly.
+    import oracle
+    w, lvl1, lvl2 = _three_level_nonuniform()
+    A, B = fi.random_pair(64, 64, 64, seed=31)
+
+    def compose(order):
+        S0, T0 = oracle.node_st(w, A, B)
+        M1 = []
+        for r1 in range(7):
+            S1, T1 = oracle.node_st(lvl1[r1], S0[r1], T0[r1])
+            M2 = []
+            for r2 in range(7):
+                rule = lvl2[order(r1, r2)]
+                S2, T2 = oracle.node_st(rule, S1[r2], T1[r2])
+                leaves = np.stack([oracle.fmm(S2[r3], T2[r3], Plan([])) for r3 in range(7)])
+                M2.append(oracle.node_c(rule, leaves))
+            M1.append(oracle.node_c(lvl1[r1], np.stack(M2)))
+        return oracle.node_c(w, np.stack(M1))
+
+    want = compose(lambda r1, r2: 7 * r1 + r2)
+    got = oracle.fmm(A, B, Plan([[w], lvl1, lvl2]))
+    assert np.array_equal(got, want)
+    # the pin is sensitive: the transposed mixed-radix order gives a different rounding
+    assert not np.array_equal(compose(lambda r1, r2: 7 * r2 + r1), want)
+    # and the plan is still a correct product (Brent-exact rules): exact on small integers
+    Ai, Bi = fi.integer_pair(64, 64, 64, seed=9, lo=-4, hi=4)
+    Ci = oracle.fmm(Ai, Bi, Plan([[w], lvl1, lvl2]))
+    assert np.array_equal(Ci, (Ai.astype(np.int64) @ Bi.astype(np.int64)).astype(np.float64))
