@@ -37,7 +37,7 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
                              void* sws, unsigned int* bar, cudaStream_t st);
 void scale_virtual_view(void* sws, int64_t M, int64_t K, int64_t N, const int32_t** exAr,
                         const int32_t** exAc, const int32_t** exBr, const int32_t** exBc,
-                        const int** mode_flag);
+                        const int** mode_flag, const int** ext);
 cudaError_t launch_unscale(double* C, int64_t ldc, int64_t M, int64_t N, const double* dA,
                            const double* dB, cudaStream_t st);
 cudaError_t launch_scale_apply(int64_t M, int64_t K, int64_t N, const double* A, int64_t lda,
@@ -134,6 +134,7 @@ struct fmm_plan {
   // S_r / T_r from the original A, B (the scaled A', B' are not written)
   bool virt_scale = false;
   bool virt_scale_enable = true;  // fmm_plan_set_virtual_scaling
+  bool unscale_fused = false;     // the root K3 / K3X2 applies the unscale
   ncclComm_t comm = nullptr;
   // comm mode 3 barrier (fmm_plan_set_barrier): called instead of the 1-word NCCL all-reduce
   fmm_barrier_fn barrier_fn = nullptr;
@@ -272,11 +273,11 @@ struct Builder {
       const RuleData& ru = rule_at(l, nd.idx);
       K1Node s{};
       s.in = nd.a;
-      s.rows = mb; s.cols = kb; s.P = ru.m0; s.Q = ru.k0;
+      s.rows = mb; s.cols = kb; s.P = ru.m0; s.Q = ru.k0; s.tv = 0;
       s.coef_off = p->coef_U[p->node_rule[l][nd.idx]];
       K1Node t{};
       t.in = nd.b;
-      t.rows = kb; t.cols = nb; t.P = ru.k0; t.Q = ru.n0;
+      t.rows = kb; t.cols = nb; t.P = ru.k0; t.Q = ru.n0; t.tv = 1;
       t.coef_off = p->coef_V[p->node_rule[l][nd.idx]];
       for (int r = 0; r < ru.R; ++r) {
         if (only_r >= 0 && r != only_r) continue;
@@ -319,6 +320,12 @@ struct Builder {
       const int blk = std::max(ks.empty() ? 0 : r0.m0 * r0.k0, kt.empty() ? 0 : r0.k0 * r0.n0);
       st.P = blk; st.Q = 1; st.R = r0.R;  // P * Q: max input sub-blocks of a node
       st.scaled = noalias ? 1 : 0;
+      {  // every node on one built-in rule: the compile-time specialised kernel
+        const int id = builtin_id(r0);
+        bool same = id != kBuiltinNone;
+        for (const Node& nd : nodes) same = same && p->node_rule[l][nd.idx] == p->node_rule[l][nodes[0].idx];
+        st.x1 = same ? 1 + id : 0;
+      }
       p->steps.push_back(st);
     }
     return kids;
@@ -591,6 +598,12 @@ struct Builder {
     p->steps.push_back(st);
   }
 
+  // The root's W-combination writes C once: a scaled plan folds its unscale in there
+  // (C = (d_A,i C'_ij) d_B,j, the same two roundings as the separate pass).
+  bool root_unscale(int l) const {
+    return l == 0 && p->scaling.mode != FMM_SCALE_NONE && !p->padded && p->dtype == FMM_F64;
+  }
+
   // K3 for nodes of level l whose children are `kids` (R per node, in order).
   void emit_k3(int l, const std::vector<Node>& nodes, const std::vector<Node>& kids) {
     std::vector<K3Node> k3;
@@ -609,6 +622,7 @@ struct Builder {
     st.count = (int)k3.size();
     st.dev_off = push(k3);
     st.rows = p->lm[l + 1]; st.cols = p->ln[l + 1]; st.P = r0.m0; st.Q = r0.n0; st.R = r0.R;
+    st.unscale = root_unscale(l) ? 1 : 0;
     p->steps.push_back(st);
   }
 
@@ -632,6 +646,7 @@ struct Builder {
     st.count = (int)k3.size();
     st.dev_off = push(k3);
     st.rows = p->lm[d + 2]; st.cols = p->ln[d + 2]; st.P = 2; st.Q = 2; st.R = builtin_R(ra);
+    st.unscale = root_unscale(d) ? 1 : 0;
     p->steps.push_back(st);
   }
 
@@ -879,6 +894,8 @@ fmm_status compile_plan(fmm_plan* p) {
   }
   p->desc_bytes = b.desc.size();
   p->launches = (int64_t)p->steps.size();
+  p->unscale_fused = false;
+  for (const Step& st : p->steps) p->unscale_fused = p->unscale_fused || st.unscale;
   if (p->scaling.mode != FMM_SCALE_NONE) {
     const size_t vec = (size_t)(p->M + p->N + p->K) * 8;
     const size_t mats = ((size_t)p->M * p->K + (size_t)p->K * p->N) * 8;
@@ -886,7 +903,7 @@ fmm_status compile_plan(fmm_plan* p) {
     std::string stp;
     double tau;
     scaling_steps(p->scaling, &stp, &tau);
-    p->launches += 3 + 2 + 3 * (int64_t)stp.size() + 1;  // fills, reductions, steps, unscale
+    p->launches += 1 + (p->unscale_fused ? 0 : 1);  // the one-kernel scaling run (+ unscale)
   } else {
     p->scale_bytes = 0;
   }
@@ -997,7 +1014,7 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
                                               : ((s.rows + ts - 1) / ts) * ((s.cols + ts - 1) / ts);
   switch (s.kind) {
     case STEP_K1: return launch_k1<T>(s, nd, p->dev_coef, b, vec, st, sc);
-    case STEP_K3: return launch_k3<T>(s, nd, p->dev_coef, b, vec, st);
+    case STEP_K3: return launch_k3<T>(s, nd, p->dev_coef, b, vec, st, sc);
     case STEP_ACC: return launch_acc<T>(s, nd, p->dev_coef, b, vec, st);
     case STEP_ZERO: return launch_zero<T>(s, nd, b, st);
     case STEP_K2F:
@@ -1596,14 +1613,17 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
                                      Ap, p->K, Bp, p->N, dA, dB, dI, (int)steps.size(), steps[0] == 'O',
                                      tau, p->scaling.pow2, p->virt_scale ? 0 : 1, sws, bar, st);
     if (e != cudaSuccess) return cuda_status(e, "fmm_execute scaling");
+    sin.ur = dA;
+    sin.uc = dB;
+    sinp = &sin;
     if (p->virt_scale) {
       const int32_t *ear, *eac, *ebr, *ebc;
-      const int* mode;
-      scale_virtual_view(sws, p->M, p->K, p->N, &ear, &eac, &ebr, &ebc, &mode);
+      const int *mode, *ext;
+      scale_virtual_view(sws, p->M, p->K, p->N, &ear, &eac, &ebr, &ebc, &mode, &ext);
+      sin.ext = ext;
       sin.er[0] = ear; sin.ec[0] = eac; sin.er[1] = ebr; sin.ec[1] = ebc;
       sin.mat[0] = Ap; sin.mat[1] = Bp; sin.ldm[0] = p->K; sin.ldm[1] = p->N;
       sin.mode = mode;
-      sinp = &sin;
     } else {
       b.p[BASE_A] = Ap; b.p[BASE_B] = Bp;
       b.ld[BASE_A] = p->K; b.ld[BASE_B] = p->N;
@@ -1641,7 +1661,7 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
         : launch_pad_copy<float>((const float*)b.p[BASE_C], p->M, p->N, p->Np, (float*)C, p->M, p->N, ldc, st);
     if (e != cudaSuccess) return cuda_status(e, "fmm_execute crop");
   }
-  if (p->scaling.mode != FMM_SCALE_NONE) {
+  if (p->scaling.mode != FMM_SCALE_NONE && !p->unscale_fused) {
     NvtxRange nv("fmm.scale");
     TimedLaunch tl(p, 6, st);
     cudaError_t e = launch_unscale((double*)C, ldc, p->M, p->N, dA, dB, st);

@@ -44,6 +44,9 @@ struct ScaleIn {
   const double* mat[2];
   int64_t ldm[2];
   const int* mode;
+  const int* ext;    // min / max of er[0], ec[0], er[1], ec[1] (8 ints): the two-multiply fast path
+  const double* ur;  // d_A, d_B of the run: the root combination (K3 / K3X2 with Step.unscale)
+  const double* uc;  // writes C = (d_A,i C'_ij) d_B,j directly
 };
 
 // Selects instead of b.p[o.base]: dynamic indexing of a by-value kernel parameter would force
@@ -87,6 +90,7 @@ struct K1Node {
   int64_t rows, cols;  // sub-block dims of this node's split (S: mb x kb, T: kb x nb)
   int32_t P, Q;        // split P x Q (S: m0 x k0, T: k0 x n0)
   int32_t coef_off;  // offset (in doubles) of the table in the plan's coefficient buffer
+  int32_t tv;        // 0: S (U table), 1: T (V table) -- for the compile-time K1 (Step.x1)
   uint32_t out_mask;
   int32_t nout;      // number of outputs written
   uint32_t need;     // bit b: input block b is read
@@ -215,6 +219,9 @@ struct Step {
   int x2 = 0;        // K1 / K3: 0 one level (K1Node / K3Node); else K1x2Node / K3x2Node with
                      // rule pair (x2 - 1) / 3, (x2 - 1) % 3 (builtin_tables.h ids)
   int scaled = 0;    // K1 of the root with virtual scaling (reads A / B through ScaleIn)
+  int x1 = 0;        // one-level K1 whose nodes all use built-in rule x1 - 1 (2x2): the
+                     // compile-time specialised kernel (k1c_lincomb)
+  int unscale = 0;   // K3 / K3X2 of the root of a scaled plan: the unscale folded in
 };
 
 // ---- kernel launchers (kernels_*.cu) -----------------------------------------------------------
@@ -223,7 +230,7 @@ cudaError_t launch_k1(const Step& s, const void* dev_nodes, const double* dev_co
                       const Bases& b, bool vec, cudaStream_t st, const ScaleIn* sc = nullptr);
 template <typename T>
 cudaError_t launch_k3(const Step& s, const void* dev_nodes, const double* dev_coef,
-                      const Bases& b, bool vec, cudaStream_t st);
+                      const Bases& b, bool vec, cudaStream_t st, const ScaleIn* sc = nullptr);
 template <typename T>
 cudaError_t launch_acc(const Step& s, const void* dev_nodes, const double* dev_coef,
                        const Bases& b, bool vec, cudaStream_t st);

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <utility>
 
 #include "fmm_internal.h"
@@ -26,7 +27,9 @@ namespace fmm {
 // reproduce the sequential roundings: switch to materialised), [10], [11] stop-test failure
 // counters of even / odd steps, [12] A' / B' are stored in the materialised buffers
 enum { F_DONE = 0, F_STEPS = 1, F_ERR = 2, F_ERRIDX = 3, F_SKIP = 4, F_INEXACT = 5, F_MODE = 8,
-       F_BAD = 9, F_FAIL = 10, F_STORED = 12, F_COUNT = 16 };
+       F_BAD = 9, F_FAIL = 10, F_STORED = 12, F_EXT = 16, F_COUNT = 24 };
+// [16 .. 23]: min / max of the final net exponents exAr, exAc, exBr, exBc (the root K1's
+// fast path needs every row + column exponent sum to be a normal power of two)
 enum ApplyMode { AP_NONE = 0, AP_ROW_DIV = 1, AP_COL_DIV = 2, AP_COL_MUL = 3 };
 
 namespace {
@@ -598,16 +601,22 @@ struct CoopArgs {
   int* flags;
   int nsteps, first_O, pow2, materialise_end;
   double tau, lo_O, lo_I, hi_I;
-  int64_t chunkA, chunkB;              // rows per tile
+  int64_t chunkA, chunkB;              // rows per tile (materialised passes)
   int stripsA, stripsB, tilesA, tilesB;
+  // reduction-only passes: row tiles (1024-column segments x row chunks) and column tiles
+  // (256-column strips x row chunks), per matrix
+  int64_t rrowsA, rrowsB, crowsA, crowsB;
+  int rsegsA, rsegsB, rtilesA, rtilesB, cstripsA, cstripsB, ctilesA, ctilesB;
+  int skip_passes;  // experiment (FMM_SCALE_SKIP_PASSES=1): barriers and factors only
 };
 
 // x 2^e, correctly rounded (one multiplication by an exact power of two when it is a normal
 // double, else ldexp)
+__device__ __noinline__ double scale2_wide(double x, int e) { return ldexp(x, e); }
 __device__ __forceinline__ double scale2(double x, int e) {
   if (e == 0) return x;
   if (e >= -1022 && e <= 1023) return __dmul_rn(x, __longlong_as_double((int64_t)(e + 1023) << 52));
-  return ldexp(x, e);
+  return scale2_wide(x, e);
 }
 __device__ __forceinline__ bool exact_value(double x, double v) {
   const double a = fabs(v);
@@ -636,8 +645,17 @@ struct MatPass {
   double* rmax; double* cmax;
 };
 
+// The per-element work of the reductions runs on IEEE bit patterns: for non-negative doubles the
+// unsigned order of the bits is the numeric order (so a max is an integer max, combined across
+// blocks with atomicMax), and an exact power-of-two scaling of a normal value is an integer add
+// on the exponent field.  A virtual value a 2^e is exact -- equal to what the sequential
+// divisions store -- iff a = 0 or both a and a 2^e are normal (else F_BAD).
+constexpr uint64_t kAbsMask = 0x7fffffffffffffffULL, kInfBits = 0x7ff0000000000000ULL;
+
+__device__ __forceinline__ uint64_t abs_bits(double x) { return (uint64_t)__double_as_longlong(x) & kAbsMask; }
+
 template <int KIND>
-__device__ void mat_tile(const MatPass& q, int tile, int* flags, double (*cm)[CSTRIP]) {
+__device__ __noinline__ void mat_tile(const MatPass& q, int tile, int* flags, unsigned long long (*cm)[CSTRIP]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int strip = tile % q.strips;
   const int64_t rbeg = (int64_t)(tile / q.strips) * q.chunk;
@@ -647,7 +665,8 @@ __device__ void mat_tile(const MatPass& q, int tile, int* flags, double (*cm)[CS
   const bool vec = ((((uintptr_t)q.src) & 15u) == 0) && (q.lds % 2 == 0) &&
                    (KIND != PK_MAT || (((((uintptr_t)q.dst) & 15u) == 0) && (q.ldd % 2 == 0)));
   int ecl[CCOL];
-  double fcl[CCOL], cmx[CCOL];
+  double fcl[CCOL];
+  uint64_t cmx[CCOL];
   bool bad = false;
 #pragma unroll
   for (int e = 0; e < CCOL; ++e) {
@@ -659,16 +678,22 @@ __device__ void mat_tile(const MatPass& q, int tile, int* flags, double (*cm)[CS
       double inv;
       if (exact_recip(fcl[e], &inv)) ecl[e] += q.cmul ? -log2_pow2(fcl[e]) : log2_pow2(fcl[e]);
     }
-    cmx[e] = 0.0;
+    cmx[e] = 0;
   }
   for (int64_t rb = rbeg + warp; rb < rend; rb += 8 * CRU) {
     double x[CRU][CCOL];
+    int erow[CRU];
+    double frw[CRU];
 #pragma unroll
     for (int u = 0; u < CRU; ++u) {
       const int64_t r = rb + u * 8;
 #pragma unroll
       for (int e = 0; e < CCOL; ++e) x[u][e] = 0.0;
+      erow[u] = 0;
+      frw[u] = 1.0;
       if (r < rend) {
+        if (KIND != PK_RAW && q.er) erow[u] = q.er[r];
+        if (KIND == PK_MAT && q.frow) frw[u] = q.frow[r];
         const double* sp = q.src + r * q.lds + cbase;
 #pragma unroll
         for (int h = 0; h < CCOL / 2; ++h) {
@@ -687,35 +712,24 @@ __device__ void mat_tile(const MatPass& q, int tile, int* flags, double (*cm)[CS
     for (int u = 0; u < CRU; ++u) {
       const int64_t r = rb + u * 8;
       if (r >= rend) continue;  // warp-uniform
-      int erow = (KIND != PK_RAW && q.er) ? q.er[r] : 0;
-      Divisor fdr;
-      if (KIND == PK_MAT && q.frow) {
-        const double f = q.frow[r];
-        fdr = Divisor(f);
-        double inv;
-        if (q.undo && exact_recip(f, &inv)) erow += log2_pow2(f);  // undo this step's row exponent
-      }
-      double rmx = 0.0;
+      uint64_t rmx = 0;
+      if (KIND == PK_MAT) {
+        Divisor fdr;
+        int er = erow[u];
+        if (q.frow) {
+          fdr = Divisor(frw[u]);
+          double inv;
+          if (q.undo && exact_recip(frw[u], &inv)) er += log2_pow2(frw[u]);  // undo this step's row exponent
+        }
+        double* dp = q.dst + r * q.ldd + cbase;
 #pragma unroll
-      for (int e = 0; e < CCOL; ++e) {
-        const int off = (e / 2) * 64 + (e & 1);
-        double v = x[u][e];
-        if (KIND == PK_VIRTUAL) {
-          const double y = scale2(v, erow + ecl[e]);
-          if (off < lim && !exact_value(v, y)) bad = true;
-          v = y;
-        } else if (KIND == PK_MAT) {
-          if (q.undo) v = scale2(v, erow + ecl[e]);  // exact: the values before this step
+        for (int e = 0; e < CCOL; ++e) {
+          double v = x[u][e];
+          if (q.undo) v = scale2(v, er + ecl[e]);  // exact: the values before this step
           if (q.frow) v = fdr.div(v);
           if (q.fcol) v = q.cmul ? __dmul_rn(v, fcl[e]) : Divisor(fcl[e]).div(v);
+          x[u][e] = v;
         }
-        x[u][e] = v;
-        const double a = off < lim ? fabs(v) : 0.0;
-        rmx = fmax(rmx, a);
-        cmx[e] = fmax(cmx[e], a);
-      }
-      if (KIND == PK_MAT) {
-        double* dp = q.dst + r * q.ldd + cbase;
 #pragma unroll
         for (int h = 0; h < CCOL / 2; ++h) {
           const int off = h * 64;
@@ -727,10 +741,27 @@ __device__ void mat_tile(const MatPass& q, int tile, int* flags, double (*cm)[CS
           }
         }
       }
+#pragma unroll
+      for (int e = 0; e < CCOL; ++e) {
+        const int off = (e / 2) * 64 + (e & 1);
+        uint64_t m = abs_bits(x[u][e]);
+        if (KIND == PK_VIRTUAL) {  // |a| 2^e on the exponent field, with the exactness check
+          const int ex = (int)(m >> 52), ee = ex + erow[u] + ecl[e];
+          const bool ok = m == 0 || ((unsigned)(ex - 1) < 2046u && (unsigned)(ee - 1) < 2046u);
+          if (off < lim && !ok) bad = true;
+          m = m == 0 ? 0 : m + ((uint64_t)(int64_t)(erow[u] + ecl[e]) << 52);
+        }
+        if (m > kInfBits || off >= lim) m = 0;  // NaN is ignored by the max (as fmax)
+        rmx = rmx > m ? rmx : m;
+        cmx[e] = cmx[e] > m ? cmx[e] : m;
+      }
       if (q.rmax) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) rmx = fmax(rmx, __shfl_xor_sync(0xffffffffu, rmx, o));
-        if (lane == 0) atomic_max_nonneg(&q.rmax[r], rmx);
+        for (int o = 16; o > 0; o >>= 1) {
+          const uint64_t y = __shfl_xor_sync(0xffffffffu, rmx, o);
+          rmx = rmx > y ? rmx : y;
+        }
+        if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&q.rmax[r]), (unsigned long long)rmx);
       }
     }
   }
@@ -740,14 +771,389 @@ __device__ void mat_tile(const MatPass& q, int tile, int* flags, double (*cm)[CS
     for (int e = 0; e < CCOL; ++e) cm[warp][(e / 2) * 64 + 2 * lane + (e & 1)] = cmx[e];
     __syncthreads();
     for (int c = threadIdx.x; c < CSTRIP; c += CT) {
-      double m = 0.0;
+      unsigned long long m = 0;
 #pragma unroll
-      for (int y = 0; y < 8; ++y) m = fmax(m, cm[y][c]);
+      for (int y = 0; y < 8; ++y) m = m > cm[y][c] ? m : cm[y][c];
       const int64_t cc = (int64_t)strip * CSTRIP + c;
-      if (cc < q.cols) atomic_max_nonneg(&q.cmax[cc], m);
+      if (cc < q.cols) atomicMax(reinterpret_cast<unsigned long long*>(&q.cmax[cc]), m);
     }
     __syncthreads();
   }
+}
+
+
+// ---- reduction-only passes (the original operands, and the virtual form's steps) ------------
+// Row maxima: a tile is a 512-column segment of a row chunk; lane l keeps the 16 column
+// factors 2^ec_j of its columns (j = 64 it + 2 l + {0, 1}) in registers, and each warp walks
+// rows with 8 16-byte loads in flight per lane: per element one multiply, a max and a nonzero
+// min.  Column maxima: a tile is a 256-column strip of a row chunk, lane l owns 8 columns over
+// the chunk's rows (per element: the row factor's multiply, a max, a min); warps combine in
+// shared memory at the end.  Virtual values are exact iff every y = |a| 2^(one exponent) and
+// every v = y 2^(the other) is normal or zero: checked on each row's / column's min and max
+// (scaling is monotone).  RAW (the original values): only a NaN / Inf check (the virtual form
+// cannot carry them: the run then materialises).
+constexpr int RSEG = 512;  // 32 lanes x 16 columns
+constexpr double kDblMin = 2.2250738585072014e-308, kDblMax = 1.7976931348623157e308;
+constexpr double kInf = __builtin_huge_val();
+
+__device__ __forceinline__ double pow2_of(int e, bool* bad) {  // 2^e as a normal double
+  if (e < -1022 || e > 1023) { *bad = true; return 1.0; }
+  return __longlong_as_double((int64_t)(e + 1023) << 52);
+}
+
+template <bool RAW>
+__device__ __noinline__ void row_tile(const MatPass& q, int tile, int* flags, int segs, int64_t rows_per) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int seg = tile % segs;
+  const int64_t r0 = (int64_t)(tile / segs) * rows_per;
+  const int64_t r1 = min(r0 + rows_per, q.rows);
+  const int64_t c0 = (int64_t)seg * RSEG + 2 * lane;
+  const int64_t lim = q.cols - c0;  // lane column offset o is valid iff o < lim
+  bool bad = false;
+  double fc[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int o = (e / 2) * 64 + (e & 1);
+    fc[e] = (!RAW && o < lim) ? pow2_of(q.ec[c0 + o], &bad) : 1.0;
+  }
+  const bool vec = ((((uintptr_t)q.src) & 15u) == 0) && (q.lds % 2 == 0);
+  // software pipeline: the next row's 8 16-byte loads (and its exponent) are in flight while
+  // this row is reduced
+  auto load = [&](int64_t r, double (&x)[16], int& er) {
+    const double* sp = q.src + r * q.lds + c0;
+    er = 0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) x[e] = 0.0;
+    if (r >= r1) return;
+    if (!RAW) er = q.er[r];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      if (vec && h * 64 + 1 < lim) {
+        const double2 v = *reinterpret_cast<const double2*>(sp + h * 64);
+        x[2 * h] = v.x; x[2 * h + 1] = v.y;
+      } else {
+        if (h * 64 < lim) x[2 * h] = sp[h * 64];
+        if (h * 64 + 1 < lim) x[2 * h + 1] = sp[h * 64 + 1];
+      }
+    }
+  };
+  double x[16], xn[16];
+  int er, ern;
+  load(r0 + warp, x, er);
+  for (int64_t r = r0 + warp; r < r1; r += 8) {
+    load(r + 8, xn, ern);
+    double mx = 0.0, mn = kInf;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const double y = __dmul_rn(fabs(x[e]), fc[e]);
+      if (RAW) bad = bad || !(y <= kDblMax);  // NaN or Inf
+      mx = fmax(mx, y);
+      mn = fmin(mn, y > 0.0 ? y : kInf);
+    }
+    if (!RAW && mn != kInf && (mn < kDblMin || scale2(mn, er) < kDblMin)) bad = true;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) {
+      const double v = RAW ? mx : scale2(mx, er);
+      if (!RAW && !(v <= kDblMax)) bad = true;
+      atomicMax(reinterpret_cast<unsigned long long*>(&q.rmax[r]), (unsigned long long)abs_bits(v));
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) x[e] = xn[e];
+    er = ern;
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(&flags[F_BAD], 1);
+}
+
+template <bool RAW>
+__device__ __noinline__ void col_tile(const MatPass& q, int tile, int* flags, int strips, int64_t rows_per,
+                                      double (*cm)[256]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int strip = tile % strips;
+  const int64_t r0 = (int64_t)(tile / strips) * rows_per;
+  const int64_t r1 = min(r0 + rows_per, q.rows);
+  const int64_t c0 = (int64_t)strip * 256 + 2 * lane;
+  const int64_t lim = q.cols - c0;
+  bool bad = false;
+  bool okc[8];
+  double cmx[8], cmn[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    okc[e] = (e / 2) * 64 + (e & 1) < lim;
+    cmx[e] = 0.0;
+    cmn[e] = kInf;
+  }
+  const bool vec = ((((uintptr_t)q.src) & 15u) == 0) && (q.lds % 2 == 0);
+  // software pipeline: the next 2 rows' loads (and row exponents) in flight during this pair
+  auto load = [&](int64_t rb, double (&x)[2][8], int (&er)[2]) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t r = rb + 8 * u;
+      er[u] = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[u][e] = 0.0;
+      if (r < r1) {
+        if (!RAW) er[u] = q.er[r];
+        const double* sp = q.src + r * q.lds + c0;
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          if (vec && okc[2 * h + 1]) {
+            const double2 v = *reinterpret_cast<const double2*>(sp + h * 64);
+            x[u][2 * h] = v.x; x[u][2 * h + 1] = v.y;
+          } else {
+            if (okc[2 * h]) x[u][2 * h] = sp[h * 64];
+            if (okc[2 * h + 1]) x[u][2 * h + 1] = sp[h * 64 + 1];
+          }
+        }
+      }
+    }
+  };
+  double x[2][8], xn[2][8];
+  int er[2], ern[2];
+  load(r0 + warp, x, er);
+  for (int64_t rb = r0 + warp; rb < r1; rb += 16) {
+    load(rb + 16, xn, ern);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double fr = RAW ? 1.0 : pow2_of(er[u], &bad);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const double y = __dmul_rn(fabs(x[u][e]), fr);
+        if (RAW) bad = bad || !(y <= kDblMax);
+        cmx[e] = fmax(cmx[e], y);
+        cmn[e] = fmin(cmn[e], y > 0.0 ? y : kInf);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      er[u] = ern[u];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[u][e] = xn[u][e];
+    }
+  }
+  // combine the 8 warps: maxima in cm, minima (virtual form only) checked per warp and column
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    cm[warp][(e / 2) * 64 + 2 * lane + (e & 1)] = cmx[e];
+    if (!RAW && okc[e] && cmn[e] != kInf) {
+      const int64_t c = c0 + (e / 2) * 64 + (e & 1);
+      if (cmn[e] < kDblMin || scale2(cmn[e], q.ec[c]) < kDblMin) bad = true;
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 256; c += CT) {
+    double m = 0.0;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) m = fmax(m, cm[y][c]);
+    const int64_t cc = (int64_t)strip * 256 + c;
+    if (cc < q.cols) {
+      const double v = RAW ? m : scale2(m, q.ec[cc]);
+      if (!RAW && !(v <= kDblMax)) bad = true;
+      atomicMax(reinterpret_cast<unsigned long long*>(&q.cmax[cc]), (unsigned long long)abs_bits(v));
+    }
+  }
+  __syncthreads();
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(&flags[F_BAD], 1);
+}
+
+
+// ---- TMA-staged forms of row_tile / col_tile (the default when rows are 16-byte aligned) ----
+// Each warp streams its rows through its own ring of CS = 3 stages of 4 KB in shared memory:
+// lane 0 issues one bulk copy (cp.async.bulk, completion counted on the stage's mbarrier) per
+// 4 KB row segment (row tiles) or two 2 KB segments (column tiles: rows r, r + 8), CS copies
+// ahead of the lanes consuming them -- 12 KB in flight per warp, 192 KB per SM, independent of
+// registers.  The tile's row exponents are staged in shared memory once per tile.
+constexpr int CS = 3;                   // stages per warp
+constexpr int CSTG = 512;               // doubles per stage (4 KB)
+constexpr int kTmaRows = 1024;          // row-exponent staging capacity per tile
+struct TmaSmem {
+  double* stage;                        // [8 warps][CS][CSTG]
+  uint64_t* bar;                        // [8 warps][CS]
+  int32_t* er;                          // [kTmaRows]
+  uint32_t* phase;                      // [8 warps]: per-stage parity bits
+};
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(s_u32(bar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_tx(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+               ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(s_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done) : "r"(s_u32(bar)), "r"(parity) : "memory");
+  } while (!done);
+}
+// stage the tile's row exponents (rows [r0, r1)) in shared memory
+__device__ __forceinline__ void stage_er(const MatPass& q, int64_t r0, int64_t r1, int32_t* sh) {
+  __syncthreads();
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += CT) sh[r - r0] = q.er ? q.er[r] : 0;
+  __syncthreads();
+}
+
+template <bool RAW>
+__device__ __noinline__ void row_tile_tma(const MatPass& q, int tile, int* flags, int segs, int64_t rows_per,
+                                          const TmaSmem& sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int seg = tile % segs;
+  const int64_t r0 = (int64_t)(tile / segs) * rows_per;
+  const int64_t r1 = min(r0 + rows_per, q.rows);
+  const int64_t cs = (int64_t)seg * RSEG;  // segment start column
+  const int64_t len = min((int64_t)RSEG, q.cols - cs);
+  const int64_t lim = len - 2 * lane;
+  if (!RAW) stage_er(q, r0, r1, sm.er);
+  bool bad = false;
+  double fc[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int o = (e / 2) * 64 + (e & 1);
+    fc[e] = (!RAW && o < lim) ? pow2_of(q.ec[cs + 2 * lane + o], &bad) : 1.0;
+  }
+  double* buf = sm.stage + (size_t)warp * CS * CSTG;
+  uint64_t* bar = sm.bar + warp * CS;
+  __syncwarp();
+  uint32_t ph = sm.phase[warp];
+  const int64_t rw = r0 + warp;
+  const int n = rw < r1 ? (int)((r1 - rw + 7) / 8) : 0;
+  const uint32_t bytes = (uint32_t)(len * 8);
+  if (lane == 0)
+    for (int k = 0; k < CS && k < n; ++k) bulk_g2s(buf + k * CSTG, q.src + (rw + 8 * k) * q.lds + cs, bytes, bar + k);
+  for (int k = 0; k < n; ++k) {
+    const int st = k % CS;
+    const int64_t r = rw + 8 * k;
+    bar_wait(bar + st, (ph >> st) & 1u);
+    ph ^= 1u << st;
+    double x[16];
+    const double* sp = buf + st * CSTG + 2 * lane;
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const double2 v = *reinterpret_cast<const double2*>(sp + h * 64);
+      x[2 * h] = v.x; x[2 * h + 1] = v.y;
+    }
+    __syncwarp();
+    if (lane == 0 && k + CS < n) bulk_g2s(buf + st * CSTG, q.src + (r + 8 * CS) * q.lds + cs, bytes, bar + st);
+    const int er = RAW ? 0 : sm.er[r - r0];
+    double mx = 0.0, mn = kInf;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const int o = (e / 2) * 64 + (e & 1);
+      const double y = o < lim ? __dmul_rn(fabs(x[e]), fc[e]) : 0.0;
+      if (RAW) bad = bad || !(y <= kDblMax);
+      mx = fmax(mx, y);
+      mn = fmin(mn, y > 0.0 ? y : kInf);
+    }
+    if (!RAW && mn != kInf && (mn < kDblMin || scale2(mn, er) < kDblMin)) bad = true;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) {
+      const double v = RAW ? mx : scale2(mx, er);
+      if (!RAW && !(v <= kDblMax)) bad = true;
+      atomicMax(reinterpret_cast<unsigned long long*>(&q.rmax[r]), (unsigned long long)abs_bits(v));
+    }
+  }
+  if (lane == 0) sm.phase[warp] = ph;
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(&flags[F_BAD], 1);
+}
+
+template <bool RAW>
+__device__ __noinline__ void col_tile_tma(const MatPass& q, int tile, int* flags, int strips, int64_t rows_per,
+                                          const TmaSmem& sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int strip = tile % strips;
+  const int64_t r0 = (int64_t)(tile / strips) * rows_per;
+  const int64_t r1 = min(r0 + rows_per, q.rows);
+  const int64_t cs = (int64_t)strip * 256;
+  const int64_t len = min((int64_t)256, q.cols - cs);
+  const int64_t lim = len - 2 * lane;
+  if (!RAW) stage_er(q, r0, r1, sm.er);
+  bool bad = false;
+  double cmx[8], cmn[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) { cmx[e] = 0.0; cmn[e] = kInf; }
+  double* buf = sm.stage + (size_t)warp * CS * CSTG;
+  uint64_t* bar = sm.bar + warp * CS;
+  __syncwarp();
+  uint32_t ph = sm.phase[warp];
+  const int64_t rw = r0 + warp;  // this warp's rows: rw + 8 j; a stage holds rows j, j + 1 of them
+  const int nr = rw < r1 ? (int)((r1 - rw + 7) / 8) : 0;
+  const int n = (nr + 1) / 2;
+  const uint32_t bytes = (uint32_t)(len * 8);
+  auto issue = [&](int k, int st) {
+    const int64_t ra = rw + 16 * k, rb = ra + 8;
+    const uint32_t tot = rb < r1 ? 2 * bytes : bytes;
+    expect_tx(bar + st, tot);
+    bulk_g2s_tx(buf + st * CSTG, q.src + ra * q.lds + cs, bytes, bar + st);
+    if (rb < r1) bulk_g2s_tx(buf + st * CSTG + 256, q.src + rb * q.lds + cs, bytes, bar + st);
+  };
+  if (lane == 0)
+    for (int k = 0; k < CS && k < n; ++k) issue(k, k);
+  for (int k = 0; k < n; ++k) {
+    const int st = k % CS;
+    bar_wait(bar + st, (ph >> st) & 1u);
+    ph ^= 1u << st;
+    double x[2][8];
+    const int64_t ra = rw + 16 * k;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const double* sp = buf + st * CSTG + u * 256 + 2 * lane;
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const double2 v = *reinterpret_cast<const double2*>(sp + h * 64);
+        x[u][2 * h] = v.x; x[u][2 * h + 1] = v.y;
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && k + CS < n) issue(k + CS, st);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t r = ra + 8 * u;
+      if (r >= r1) continue;  // warp-uniform
+      const double fr = RAW ? 1.0 : pow2_of(sm.er[r - r0], &bad);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int o = (e / 2) * 64 + (e & 1);
+        const double y = o < lim ? __dmul_rn(fabs(x[u][e]), fr) : 0.0;
+        if (RAW) bad = bad || !(y <= kDblMax);
+        cmx[e] = fmax(cmx[e], y);
+        cmn[e] = fmin(cmn[e], y > 0.0 ? y : kInf);
+      }
+    }
+  }
+  if (lane == 0) sm.phase[warp] = ph;
+  // combine the 8 warps (in the stage buffers, now free)
+  __syncthreads();
+  double (*cm)[256] = reinterpret_cast<double (*)[256]>(sm.stage);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int o = (e / 2) * 64 + (e & 1);
+    cm[warp][o + 2 * lane] = cmx[e];
+    if (!RAW && o < lim && cmn[e] != kInf &&
+        (cmn[e] < kDblMin || scale2(cmn[e], q.ec[cs + 2 * lane + o]) < kDblMin))
+      bad = true;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 256; c += CT) {
+    double m = 0.0;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) m = fmax(m, cm[y][c]);
+    if (c < len) {
+      const double v = RAW ? m : scale2(m, q.ec[cs + c]);
+      if (!RAW && !(v <= kDblMax)) bad = true;
+      atomicMax(reinterpret_cast<unsigned long long*>(&q.cmax[cs + c]), (unsigned long long)abs_bits(v));
+    }
+  }
+  __syncthreads();
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(&flags[F_BAD], 1);
 }
 
 // grid barrier: every block of the cooperative launch arrives, then all proceed
@@ -768,8 +1174,24 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nbl
   __syncthreads();
 }
 
+// dynamic shared memory of k_scale_coop: the TMA stage ring (also the warp-combine buffers),
+// its mbarriers, the row exponents of a tile, the per-warp parities
+constexpr size_t kCoopSmem = (size_t)8 * CS * CSTG * sizeof(double) + 8 * CS * sizeof(uint64_t) +
+                             kTmaRows * sizeof(int32_t) + 8 * sizeof(uint32_t);
+
 __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* bar) {
-  __shared__ double cm[8][CSTRIP];
+  extern __shared__ __align__(128) uint8_t dsm[];
+  TmaSmem tsm;
+  tsm.stage = reinterpret_cast<double*>(dsm);
+  tsm.bar = reinterpret_cast<uint64_t*>(dsm + (size_t)8 * CS * CSTG * sizeof(double));
+  tsm.er = reinterpret_cast<int32_t*>(tsm.bar + 8 * CS);
+  tsm.phase = reinterpret_cast<uint32_t*>(tsm.er + kTmaRows);
+  if (threadIdx.x < 8 * CS) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s_u32(tsm.bar + threadIdx.x)));
+  if (threadIdx.x < 8) tsm.phase[threadIdx.x] = 0;
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+  double (*cmd)[256] = reinterpret_cast<double (*)[256]>(dsm);
+  unsigned long long (*cm)[CSTRIP] = reinterpret_cast<unsigned long long (*)[CSTRIP]>(dsm);
   const unsigned int nb = gridDim.x;
   unsigned int gen = 0;
   int* flags = a.flags;
@@ -781,6 +1203,7 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* 
   for (int64_t k = gtid; k < K; k += gstride) { a.dI[k] = 1.0; a.exAc[k] = 0; a.exBr[k] = 0; }
   for (int64_t i = gtid; i < M + 2 * K + N; i += gstride) { a.mx[0][i] = 0.0; a.mx[1][i] = 0.0; }
   if (gtid == 0) flags[F_MODE] = a.pow2 ? 0 : 1;
+  if (gtid < 8) flags[F_EXT + gtid] = (gtid & 1) ? (-0x7fffffff - 1) : 0x7fffffff;
   grid_barrier(bar, nb, gen);
 
   auto views = [&](int isO, int kind, double* m) {  // (A part, B part) of a pass
@@ -792,21 +1215,60 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* 
     pa.rows = M; pa.cols = K; pa.chunk = a.chunkA; pa.strips = a.stripsA;
     pb.rows = K; pb.cols = N; pb.chunk = a.chunkB; pb.strips = a.stripsB;
     pa.er = a.exAr; pa.ec = a.exAc; pb.er = a.exBr; pb.ec = a.exBc;
-    pa.undo = pb.undo = (kind == PK_MAT && !stored) ? 1 : 0;
+    // the exponents carry the factors applied so far only in the virtual form (pow2); a first
+    // materialised application from A, B undoes this step's exponent to get the values before it
+    pa.undo = pb.undo = (kind == PK_MAT && !stored && a.pow2) ? 1 : 0;
     return std::make_pair(pa, pb);
   };
   // run one pass over A and B (tiles of A, then of B, grid-strided)
+  int npass = 0;
   auto run_pass = [&](int kind, MatPass& pa, MatPass& pb) {
-    for (int t = blockIdx.x; t < a.tilesA + a.tilesB; t += nb) {
-      if (t < a.tilesA) {
-        if (kind == PK_RAW) mat_tile<PK_RAW>(pa, t, flags, cm);
-        else if (kind == PK_VIRTUAL) mat_tile<PK_VIRTUAL>(pa, t, flags, cm);
-        else mat_tile<PK_MAT>(pa, t, flags, cm);
-      } else {
-        if (kind == PK_RAW) mat_tile<PK_RAW>(pb, t - a.tilesA, flags, cm);
-        else if (kind == PK_VIRTUAL) mat_tile<PK_VIRTUAL>(pb, t - a.tilesA, flags, cm);
-        else mat_tile<PK_MAT>(pb, t - a.tilesA, flags, cm);
+    if (kind != PK_MAT && a.skip_passes) {  // experiment: maxima 1, no data read
+      for (int64_t i = gtid; i < M + 2 * K + N; i += gstride) { a.mx[0][i] = 1.0; a.mx[1][i] = 1.0; }
+      return;
+    }
+    if (kind != PK_MAT) {  // reductions only: row or column tiles per matrix
+      const int na = pa.rmax ? a.rtilesA : a.ctilesA, nbt = pb.rmax ? a.rtilesB : a.ctilesB;
+      // alternate passes walk the tiles in reverse: a pass starts on the ~100 MB the previous
+      // one read last, still in the 126 MB L2
+      const bool rev = (npass++ & 1) != 0;
+      for (int t0 = blockIdx.x; t0 < na + nbt; t0 += nb) {
+        const int t = rev ? na + nbt - 1 - t0 : t0;
+        const bool isA = t < na;
+        const MatPass& q = isA ? pa : pb;
+        const int tt = isA ? t : t - na;
+        const int segs = isA ? a.rsegsA : a.rsegsB, strips = isA ? a.cstripsA : a.cstripsB;
+        const int64_t rr = isA ? a.rrowsA : a.rrowsB, cr = isA ? a.crowsA : a.crowsB;
+        // TMA staging needs 16-byte aligned rows (and whole 16-byte row segments)
+        const bool tma = ((((uintptr_t)q.src) & 15u) == 0) && q.lds % 2 == 0 && q.cols % 2 == 0;
+        if (q.rmax) {
+          if (tma && rr <= kTmaRows) {
+            if (kind == PK_RAW) row_tile_tma<true>(q, tt, flags, segs, rr, tsm);
+            else row_tile_tma<false>(q, tt, flags, segs, rr, tsm);
+          } else {
+            if (kind == PK_RAW) row_tile<true>(q, tt, flags, segs, rr);
+            else row_tile<false>(q, tt, flags, segs, rr);
+          }
+        } else {
+          if (tma && cr <= kTmaRows) {
+            if (kind == PK_RAW) col_tile_tma<true>(q, tt, flags, strips, cr, tsm);
+            else col_tile_tma<false>(q, tt, flags, strips, cr, tsm);
+          } else {
+            __syncthreads();  // cmd aliases the stage ring
+            if (kind == PK_RAW) col_tile<true>(q, tt, flags, strips, cr, cmd);
+            else col_tile<false>(q, tt, flags, strips, cr, cmd);
+          }
+        }
       }
+      return;
+    }
+    for (int t = blockIdx.x; t < a.tilesA + a.tilesB; t += nb) {
+      const bool isA = t < a.tilesA;
+      const MatPass& q = isA ? pa : pb;
+      const int tt = isA ? t : t - a.tilesA;
+      if (kind == PK_RAW) mat_tile<PK_RAW>(q, tt, flags, cm);
+      else if (kind == PK_VIRTUAL) mat_tile<PK_VIRTUAL>(q, tt, flags, cm);
+      else mat_tile<PK_MAT>(q, tt, flags, cm);
     }
   };
   // the maxima a step of kind isO needs, into maxima set m
@@ -834,7 +1296,7 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* 
   for (int t = 0; t < a.nsteps; ++t) {
     const int isO = (t % 2 == 0) == (a.first_O != 0);
     if (isO && t0 < 0) t0 = t;
-    const int test = (a.tau >= 0.0 && t0 >= 0 && t > t0) ? 1 : 0;
+    const int test = (a.tau >= 0.0 && t0 >= 0 && t > t0 && !a.skip_passes) ? 1 : 0;
     double* cur = a.mx[t & 1];
     double* nxt = a.mx[(t + 1) & 1];
     int* fail = &flags[F_FAIL + (t & 1)];
@@ -949,6 +1411,25 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* 
       break;
     }
   }
+  // extremes of the final exponents (for the root K1's two-multiply fast path)
+  {
+    const int32_t* ex[4] = {a.exAr, a.exAc, a.exBr, a.exBc};
+    const int64_t len[4] = {M, K, K, N};
+#pragma unroll 1
+    for (int v = 0; v < 4; ++v) {
+      int lo = 0x7fffffff, hi = -0x7fffffff - 1;
+      for (int64_t i = gtid; i < len[v]; i += gstride) { lo = min(lo, ex[v][i]); hi = max(hi, ex[v][i]); }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      }
+      if ((threadIdx.x & 31) == 0) {
+        atomicMin(&flags[F_EXT + 2 * v], lo);
+        atomicMax(&flags[F_EXT + 2 * v + 1], hi);
+      }
+    }
+  }
 }
 
 }  // namespace
@@ -973,8 +1454,9 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_scale_coop, CT, 0);
-    if (blocks_per_sm > 3) blocks_per_sm = 3;
+    cudaFuncSetAttribute(k_scale_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCoopSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_scale_coop, CT, kCoopSmem);
+    if (blocks_per_sm > 2) blocks_per_sm = 2;
     if (blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const int nblocks = sms * blocks_per_sm;
@@ -1000,17 +1482,41 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
   };
   tiles(M, K, &a.chunkA, &a.stripsA, &a.tilesA);
   tiles(K, N, &a.chunkB, &a.stripsB, &a.tilesB);
+  // reduction-only passes: about one tile per block per matrix
+  auto rtiles = [&](int64_t rows, int64_t cols, int64_t* rows_per, int* segs, int* ntiles) {
+    *segs = (int)((cols + RSEG - 1) / RSEG);
+    int64_t nch = std::max<int64_t>(1, nblocks / *segs);
+    int64_t rp = (rows + nch - 1) / nch;
+    rp = std::max<int64_t>(8, (rp + 7) / 8 * 8);
+    *rows_per = rp;
+    *ntiles = (int)(*segs * ((rows + rp - 1) / rp));
+  };
+  auto ctiles = [&](int64_t rows, int64_t cols, int64_t* rows_per, int* strips, int* ntiles) {
+    *strips = (int)((cols + 255) / 256);
+    int64_t nch = std::max<int64_t>(1, nblocks / *strips);
+    int64_t rp = (rows + nch - 1) / nch;
+    rp = std::max<int64_t>(16, (rp + 15) / 16 * 16);
+    *rows_per = rp;
+    *ntiles = (int)(*strips * ((rows + rp - 1) / rp));
+  };
+  rtiles(M, K, &a.rrowsA, &a.rsegsA, &a.rtilesA);
+  rtiles(K, N, &a.rrowsB, &a.rsegsB, &a.rtilesB);
+  ctiles(M, K, &a.crowsA, &a.cstripsA, &a.ctilesA);
+  ctiles(K, N, &a.crowsB, &a.cstripsB, &a.ctilesB);
+  a.skip_passes = getenv("FMM_SCALE_SKIP_PASSES") ? 1 : 0;
   void* args[] = {&a, &bar};
-  return cudaLaunchCooperativeKernel((const void*)k_scale_coop, dim3((unsigned)nblocks), dim3(CT), args, 0, st);
+  return cudaLaunchCooperativeKernel((const void*)k_scale_coop, dim3((unsigned)nblocks), dim3(CT), args,
+                                     kCoopSmem, st);
 }
 
 // Exponent vectors and mode flag of the virtual form (for the plan's root K1).
 void scale_virtual_view(void* sws, int64_t M, int64_t K, int64_t N, const int32_t** exAr,
                         const int32_t** exAc, const int32_t** exBr, const int32_t** exBc,
-                        const int** mode_flag) {
+                        const int** mode_flag, const int** ext) {
   ScaleWsView v = scale_ws_view(sws, M, K, N);
   *exAr = v.ex; *exAc = v.ex + M; *exBr = v.ex + M + K; *exBc = v.ex + M + 2 * K;
   *mode_flag = v.flags + F_MODE;
+  *ext = v.flags + F_EXT;
 }
 
 // Apply given factors: A' = (a_ik / dA_i) * d_k, B' = (b_kj / d_k) / dB_j (each operation

@@ -144,3 +144,118 @@ def test_scale_apply_definition_and_roundtrip(fb):
     r = fb.scale_repeated(dev(A), dev(B), first_O=True, tau=1.0, max_steps=12, pow2=True)
     Ao, Bo = fb.scale_apply(dev(A), dev(B), r["dA"], r["dI"], r["dB"])
     assert np.array_equal(host(Ao), host(r["A"])) and np.array_equal(host(Bo), host(r["B"]))
+
+
+def _extreme_pair():
+    # rows / columns whose power-of-two factors have no normal reciprocal (2^1023, subnormal),
+    # and a row whose scaled entries become subnormal after the first O step (max 2^600, an
+    # entry 2^-430 (1 + 2^-20) -> 2^-1030 (1 + 2^-20): not representable) -- both force the
+    # one-kernel scaling run from its virtual form to the materialised one, on device
+    g = np.random.default_rng(3)
+    A = g.uniform(0.5, 1.0, (64, 96))
+    B = g.uniform(0.5, 1.0, (96, 80))
+    A[5] *= 1.2e308
+    A[7] *= 2.0 ** -1060
+    B[:, 3] *= 1.2e308
+    B[:, 9] *= 2.0 ** -1065
+    return A, B
+
+
+def _subnormal_after_step_pair():
+    g = np.random.default_rng(4)
+    A = g.uniform(0.5, 1.0, (64, 96))
+    B = g.uniform(0.5, 1.0, (96, 80))
+    A[11, :] *= 2.0 ** 600
+    A[11, 17] = 2.0 ** -430 * (1 + 2.0 ** -20)
+    return A, B
+
+
+SCALED_PLANS = {
+    "L1_fused": (("winograd",), "auto", "on"),
+    "L2": (("winograd",) * 2, "auto", "auto"),
+    "L3_breadth": (("winograd",) * 3, "breadth", "auto"),
+    "L3_depth": (("winograd",) * 3, "depth", "off"),
+    "L3_hybrid": (("winograd", "classical222", "strassen"), "hybrid", "on"),
+}
+
+
+@pytest.mark.parametrize("pname", sorted(SCALED_PLANS))
+@pytest.mark.parametrize("mode", ["outside", "inside", "out_in", "in_out", "repeated"])
+def test_virtual_scaling_equals_materialised(fb, pname, mode):
+    # virtual scaling (pow2 factors applied while the root K1 reads A, B; unscale folded into the
+    # root combination) is bitwise the materialised form, on every schedule
+    names, sched, fusion = SCALED_PLANS[pname]
+    L = len(names)
+    M, K, N = 2 ** L * 48, 2 ** L * 40, 2 ** L * 36
+    A, B = fi.draw("skew", M, K, N, 3)
+    rules = [fb.Rule.builtin(n) for n in names]
+    sc = {"mode": mode, "tau": 1.0, "max_steps": 20, "pow2": 1}
+    pv = fb.Plan(rules, M, K, N, scaling=sc)
+    pm = fb.Plan(rules, M, K, N, scaling=sc)
+    pm.set_virtual_scaling(False)
+    for p in (pv, pm):
+        p.set_schedule(sched)
+        p.set_fusion(fusion)
+    Cv = host(pv.execute(dev(A), dev(B)))
+    Cm = host(pm.execute(dev(A), dev(B)))
+    assert np.array_equal(Cv, Cm)
+    assert pv.last_scaling_steps() == pm.last_scaling_steps()
+    Co, info = oracle.scaled_fmm(A, B, OPlan.uniform([R.builtin(n) for n in names]), mode=mode,
+                                 pow2=True, tau=1.0, max_steps=20)
+    assert pv.last_scaling_steps() == info["steps"]
+    assert oracle.parity_metric(Cv, Co, np.abs(A).max(), np.abs(B).max(), K) <= 1e-13
+
+
+@pytest.mark.parametrize("pair", ["extreme", "subnormal_after_step"])
+@pytest.mark.parametrize("mode", ["outside", "out_in", "repeated"])
+def test_virtual_scaling_falls_back_bitwise(fb, pair, mode):
+    # inputs the virtual form cannot carry: the run switches to the materialised form on
+    # device; the entry point's A', B', factors and steps stay bitwise the oracle's, and a
+    # scaled plan's C is bitwise the materialised plan's
+    A, B = _extreme_pair() if pair == "extreme" else _subnormal_after_step_pair()
+    first_O = True
+    steps = {"outside": 1, "out_in": 2, "repeated": 12}[mode]
+    tau = 1.0 if mode == "repeated" else -1.0
+    gg = fb.scale_repeated(dev(A), dev(B), first_O=first_O, tau=tau, max_steps=steps, pow2=True)
+    o = oracle.scale_repeated(A, B, first_O=first_O, tau=tau, max_steps=steps, pow2=True)
+    assert gg["steps"] == o["steps"]
+    for k in ("A", "B", "dA", "dB", "dI"):
+        assert np.array_equal(host(gg[k]), o[k]), k
+    w = fb.Rule.builtin("winograd")
+    sc = {"mode": mode, "tau": 1.0, "max_steps": 12, "pow2": 1}
+    pv = fb.Plan([w, w], 64, 96, 80, scaling=sc)
+    pm = fb.Plan([w, w], 64, 96, 80, scaling=sc)
+    pm.set_virtual_scaling(False)
+    Cv = host(pv.execute(dev(A), dev(B)))
+    Cm = host(pm.execute(dev(A), dev(B)))
+    assert np.array_equal(Cv, Cm, equal_nan=True)
+
+
+def test_virtual_scaling_in_cuda_graph(fb):
+    # the one-kernel scaling run is a cooperative launch: captured and replayed in a graph
+    A, B = fi.draw("skew", 256, 256, 256, 3)
+    w = fb.Rule.builtin("winograd")
+    p = fb.Plan([w, w, w], 256, 256, 256, scaling={"mode": "repeated", "pow2": 1})
+    ref = host(p.execute(dev(A), dev(B)))
+    p.set_graph(True)
+    Ad, Bd = dev(A), dev(B)
+    C = torch.empty((256, 256), dtype=torch.float64, device="cuda")
+    for _ in range(3):
+        C.zero_()
+        p.execute(Ad, Bd, C)
+        torch.cuda.synchronize()
+        assert np.array_equal(host(C), ref)
+
+
+@pytest.mark.parametrize("dims", [(1536, 2200, 700), (600, 4096, 1100)])
+def test_repeated_wide_matrices_bitwise(fb, dims):
+    # rows / columns wider than one reduction tile (512 / 256 columns): factors, steps and the
+    # scaled matrices bitwise the oracle's (a tiling bug that skips columns changes the steps)
+    M, K, N = dims
+    A, B = fi.draw("skew", M, K, N, 3)
+    for first_O in (True, False):
+        g = fb.scale_repeated(dev(A), dev(B), first_O=first_O, tau=1.0, max_steps=20, pow2=True)
+        o = oracle.scale_repeated(A, B, first_O=first_O, tau=1.0, max_steps=20, pow2=True)
+        assert g["steps"] == o["steps"]
+        for k in ("A", "B", "dA", "dB", "dI"):
+            assert np.array_equal(host(g[k]), o[k]), k
