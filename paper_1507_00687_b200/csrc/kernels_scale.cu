@@ -607,7 +607,6 @@ struct CoopArgs {
   // (256-column strips x row chunks), per matrix
   int64_t rrowsA, rrowsB, crowsA, crowsB;
   int rsegsA, rsegsB, rtilesA, rtilesB, cstripsA, cstripsB, ctilesA, ctilesB;
-  int skip_passes;  // experiment (FMM_SCALE_SKIP_PASSES=1): barriers and factors only
 };
 
 // x 2^e, correctly rounded (one multiplication by an exact power of two when it is a normal
@@ -974,6 +973,18 @@ struct TmaSmem {
 };
 
 __device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ double2 lds2(uint32_t a) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(a));
+  return v;
+}
+// smallest nonzero y with y and y 2^e both normal: max(2^-1022, 2^(-1022 - e)); +inf if none
+__device__ __forceinline__ double under_thr(int e) {
+  const int t = -1022 - e;
+  if (t <= -1022) return kDblMin;
+  if (t > 1023) return kInf;
+  return __longlong_as_double((int64_t)(t + 1023) << 52);
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(s_u32(bar)), "r"(bytes) : "memory");
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
@@ -1034,25 +1045,29 @@ __device__ __noinline__ void row_tile_tma(const MatPass& q, int tile, int* flags
     bar_wait(bar + st, (ph >> st) & 1u);
     ph ^= 1u << st;
     double x[16];
-    const double* sp = buf + st * CSTG + 2 * lane;
+    const uint32_t sp = s_u32(buf + st * CSTG + 2 * lane);
 #pragma unroll
     for (int h = 0; h < 8; ++h) {
-      const double2 v = *reinterpret_cast<const double2*>(sp + h * 64);
+      const double2 v = lds2(sp + h * 64 * 8);
       x[2 * h] = v.x; x[2 * h + 1] = v.y;
     }
     __syncwarp();
     if (lane == 0 && k + CS < n) bulk_g2s(buf + st * CSTG, q.src + (r + 8 * CS) * q.lds + cs, bytes, bar + st);
     const int er = RAW ? 0 : sm.er[r - r0];
-    double mx = 0.0, mn = kInf;
+    const double thr = under_thr(er);
+    double mx = 0.0;
+    if (lim < 512) {  // ragged segment: columns past the end read as 0
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if ((e / 2) * 64 + (e & 1) >= lim) x[e] = 0.0;
+    }
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
-      const int o = (e / 2) * 64 + (e & 1);
-      const double y = o < lim ? __dmul_rn(fabs(x[e]), fc[e]) : 0.0;
-      if (RAW) bad = bad || !(y <= kDblMax);
+      const double y = __dmul_rn(fabs(x[e]), fc[e]);
+      if (RAW) bad |= !(y <= kDblMax);          // NaN or Inf
+      else bad |= (y < thr) & (y > 0.0);        // y or y 2^er not normal
       mx = fmax(mx, y);
-      mn = fmin(mn, y > 0.0 ? y : kInf);
     }
-    if (!RAW && mn != kInf && (mn < kDblMin || scale2(mn, er) < kDblMin)) bad = true;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) {
@@ -1077,9 +1092,13 @@ __device__ __noinline__ void col_tile_tma(const MatPass& q, int tile, int* flags
   const int64_t lim = len - 2 * lane;
   if (!RAW) stage_er(q, r0, r1, sm.er);
   bool bad = false;
-  double cmx[8], cmn[8];
+  double cmx[8], cthr[8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) { cmx[e] = 0.0; cmn[e] = kInf; }
+  for (int e = 0; e < 8; ++e) {
+    const int o = (e / 2) * 64 + (e & 1);
+    cmx[e] = 0.0;
+    cthr[e] = (!RAW && o < lim) ? under_thr(q.ec[cs + 2 * lane + o]) : kDblMin;
+  }
   double* buf = sm.stage + (size_t)warp * CS * CSTG;
   uint64_t* bar = sm.bar + warp * CS;
   __syncwarp();
@@ -1105,15 +1124,22 @@ __device__ __noinline__ void col_tile_tma(const MatPass& q, int tile, int* flags
     const int64_t ra = rw + 16 * k;
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      const double* sp = buf + st * CSTG + u * 256 + 2 * lane;
+      const uint32_t sp = s_u32(buf + st * CSTG + u * 256 + 2 * lane);
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
-        const double2 v = *reinterpret_cast<const double2*>(sp + h * 64);
+        const double2 v = lds2(sp + h * 64 * 8);
         x[u][2 * h] = v.x; x[u][2 * h + 1] = v.y;
       }
     }
     __syncwarp();
     if (lane == 0 && k + CS < n) issue(k + CS, st);
+    if (lim < 256) {  // ragged strip: columns past the end read as 0
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if ((e / 2) * 64 + (e & 1) >= lim) x[u][e] = 0.0;
+    }
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int64_t r = ra + 8 * u;
@@ -1121,11 +1147,10 @@ __device__ __noinline__ void col_tile_tma(const MatPass& q, int tile, int* flags
       const double fr = RAW ? 1.0 : pow2_of(sm.er[r - r0], &bad);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const int o = (e / 2) * 64 + (e & 1);
-        const double y = o < lim ? __dmul_rn(fabs(x[u][e]), fr) : 0.0;
-        if (RAW) bad = bad || !(y <= kDblMax);
+        const double y = __dmul_rn(fabs(x[u][e]), fr);
+        if (RAW) bad |= !(y <= kDblMax);          // NaN or Inf
+        else bad |= (y < cthr[e]) & (y > 0.0);    // y or y 2^ec not normal
         cmx[e] = fmax(cmx[e], y);
-        cmn[e] = fmin(cmn[e], y > 0.0 ? y : kInf);
       }
     }
   }
@@ -1134,13 +1159,7 @@ __device__ __noinline__ void col_tile_tma(const MatPass& q, int tile, int* flags
   __syncthreads();
   double (*cm)[256] = reinterpret_cast<double (*)[256]>(sm.stage);
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int o = (e / 2) * 64 + (e & 1);
-    cm[warp][o + 2 * lane] = cmx[e];
-    if (!RAW && o < lim && cmn[e] != kInf &&
-        (cmn[e] < kDblMin || scale2(cmn[e], q.ec[cs + 2 * lane + o]) < kDblMin))
-      bad = true;
-  }
+  for (int e = 0; e < 8; ++e) cm[warp][(e / 2) * 64 + (e & 1) + 2 * lane] = cmx[e];
   __syncthreads();
   for (int c = threadIdx.x; c < 256; c += CT) {
     double m = 0.0;
@@ -1223,10 +1242,6 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* 
   // run one pass over A and B (tiles of A, then of B, grid-strided)
   int npass = 0;
   auto run_pass = [&](int kind, MatPass& pa, MatPass& pb) {
-    if (kind != PK_MAT && a.skip_passes) {  // experiment: maxima 1, no data read
-      for (int64_t i = gtid; i < M + 2 * K + N; i += gstride) { a.mx[0][i] = 1.0; a.mx[1][i] = 1.0; }
-      return;
-    }
     if (kind != PK_MAT) {  // reductions only: row or column tiles per matrix
       const int na = pa.rmax ? a.rtilesA : a.ctilesA, nbt = pb.rmax ? a.rtilesB : a.ctilesB;
       // alternate passes walk the tiles in reverse: a pass starts on the ~100 MB the previous
@@ -1296,7 +1311,7 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* 
   for (int t = 0; t < a.nsteps; ++t) {
     const int isO = (t % 2 == 0) == (a.first_O != 0);
     if (isO && t0 < 0) t0 = t;
-    const int test = (a.tau >= 0.0 && t0 >= 0 && t > t0 && !a.skip_passes) ? 1 : 0;
+    const int test = (a.tau >= 0.0 && t0 >= 0 && t > t0) ? 1 : 0;
     double* cur = a.mx[t & 1];
     double* nxt = a.mx[(t + 1) & 1];
     int* fail = &flags[F_FAIL + (t & 1)];
@@ -1503,7 +1518,6 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
   rtiles(K, N, &a.rrowsB, &a.rsegsB, &a.rtilesB);
   ctiles(M, K, &a.crowsA, &a.cstripsA, &a.ctilesA);
   ctiles(K, N, &a.crowsB, &a.cstripsB, &a.ctilesB);
-  a.skip_passes = getenv("FMM_SCALE_SKIP_PASSES") ? 1 : 0;
   void* args[] = {&a, &bar};
   return cudaLaunchCooperativeKernel((const void*)k_scale_coop, dim3((unsigned)nblocks), dim3(CT), args,
                                      kCoopSmem, st);
