@@ -1,14 +1,10 @@
-// K4: diagonal scaling (Section 6, Alg. 1-3) on device, FP64.
-//
-// One scaling step = one tiny factor kernel + one streaming pass per matrix.  The streaming
-// pass applies the step's factors (a / r'_i, a * p_k, b / s'_j, b / p_k -- true divisions,
-// DESIGN.md reading A9) and, in the same read, accumulates the row and column max-abs of the
-// RESULT, which are exactly the reductions the next step needs; so every step reads and writes
-// each matrix once.  Max-abs is combined across CTAs with atomicMax on the IEEE bit pattern
-// (non-negative doubles order like their bit patterns): exact and order-free.
-// The stopping test of Thm stopping-criterion, from the step after the first O
-// step, runs on device; once it fires, later steps' passes exit immediately, so the
-// host never synchronises inside Alg. 3.
+// K4: diagonal scaling (Section 6, Alg. 1-3) on device, FP64: the whole run -- every
+// step's max-abs reductions, factors, stopping test and applications -- in ONE cooperative
+// kernel (k_scale_coop, below), plus the unscale / given-factor apply building blocks.
+// Max-abs is combined across CTAs with atomicMax on the IEEE bit pattern (non-negative
+// doubles order like their bit patterns): exact and order-free.  The stopping test of Thm
+// stopping-criterion, from the step after the first O step, runs on
+// device; the host never synchronises inside Alg. 3.
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
@@ -20,23 +16,16 @@
 namespace fmm {
 
 // flags layout (int32): [0] done, [1] steps taken, [2] error kind (0 none; 1 zero row of A,
-// 2 zero col of B, 3 zero col of A, 4 zero row of B), [3] error index, [4] skip current step
-// [5] inexact: some factor of the current step has no exactly representable power-of-two
-// reciprocal (the multiply pass then yields to the dividing pass)
+// 2 zero col of B, 3 zero col of A, 4 zero row of B), [3] error index,
 // [8] mode of the one-kernel run (0 virtual, 1 materialised), [9] bad (the virtual form cannot
 // reproduce the sequential roundings: switch to materialised), [10], [11] stop-test failure
 // counters of even / odd steps, [12] A' / B' are stored in the materialised buffers
-enum { F_DONE = 0, F_STEPS = 1, F_ERR = 2, F_ERRIDX = 3, F_SKIP = 4, F_INEXACT = 5, F_MODE = 8,
+enum { F_DONE = 0, F_STEPS = 1, F_ERR = 2, F_ERRIDX = 3, F_MODE = 8,
        F_BAD = 9, F_FAIL = 10, F_STORED = 12, F_EXT = 16, F_COUNT = 24 };
 // [16 .. 23]: min / max of the final net exponents exAr, exAc, exBr, exBc (the root K1's
 // fast path needs every row + column exponent sum to be a normal power of two)
-enum ApplyMode { AP_NONE = 0, AP_ROW_DIV = 1, AP_COL_DIV = 2, AP_COL_MUL = 3 };
 
 namespace {
-
-__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
-  atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
-}
 
 // Nearest power of two in log2 (reading A8): x = m 2^e, m in [0.5, 1);
 // round down to 2^(e-1) iff m*m < 1/2, decided exactly with an error-free square.
@@ -48,11 +37,6 @@ __device__ __forceinline__ double pow2_round(double x) {
   bool below = (h < 0.5) || (h == 0.5 && l < 0.0);
   return ldexp(1.0, below ? e - 1 : e);
 }
-
-constexpr int TX = 32, TY = 8;
-constexpr int CPL = 4;         // columns per lane (two 16-byte accesses)
-constexpr int TC = TX * CPL;   // 128-column strips
-constexpr int RU = 2;          // rows in flight per warp
 
 // x / f, correctly rounded.  When f is an exact power of two whose reciprocal is a normal
 // double (pow2 factors, reading A7), x * (1/f) is the same real number rounded
@@ -70,231 +54,6 @@ struct Divisor {
   __device__ __forceinline__ double div(double x) const { return pow2 ? __dmul_rn(x, inv) : __ddiv_rn(x, f); }
 };
 
-// dst = apply(src); row_max[i] = max_j |dst_ij|, col_max[j] = max_i |dst_ij| (atomic).
-// dst may equal src (in place) or be null (reduce only).  Block (x, y) owns the 128-column strip
-// x and the row chunk y; warp w handles rows w, w + TY, ... of the chunk, RU rows at a time
-// (their loads issued together), lane l owns columns 2l, 2l+1 and 64+2l, 64+2l+1 (16-byte
-// accesses when VEC, each warp instruction covering 512 contiguous bytes).  Column maxima stay
-// in registers over the whole chunk: one shared-memory combine and one atomic per column per
-// block at the end, no block barrier inside the stream.
-template <int MODE, bool VEC>
-__global__ void __launch_bounds__(TX* TY, 4)
-    k_apply_reduce(const double* src, int64_t lds, double* dst, int64_t ldd,
-                   int64_t rows, int64_t cols, int64_t chunk, const double* __restrict__ f,
-                   double* __restrict__ row_max, double* __restrict__ col_max,
-                   const int* __restrict__ flags, int only_if_inexact) {
-  if (flags && (flags[F_SKIP] || (only_if_inexact && !flags[F_INEXACT]))) return;
-  __shared__ double cm[TY][TC];
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  const int64_t cbase = (int64_t)blockIdx.x * TC + 2 * tx;
-  const int64_t rbeg = (int64_t)blockIdx.y * chunk;
-  const int64_t rend = rbeg + chunk < rows ? rbeg + chunk : rows;
-  int64_t cidx[CPL];
-  bool ok[CPL];
-#pragma unroll
-  for (int e = 0; e < CPL; ++e) {
-    cidx[e] = cbase + (e / 2) * (2 * TX) + (e & 1);
-    ok[e] = cidx[e] < cols;
-  }
-  Divisor fcol[CPL];
-  double mcol[CPL];
-#pragma unroll
-  for (int e = 0; e < CPL; ++e) {
-    mcol[e] = 1.0;
-    if (MODE == AP_COL_DIV || MODE == AP_COL_MUL) {
-      const double v = ok[e] ? f[cidx[e]] : 1.0;
-      if (MODE == AP_COL_DIV) fcol[e] = Divisor(v);
-      else mcol[e] = v;
-    }
-  }
-  double cmax[CPL];
-#pragma unroll
-  for (int e = 0; e < CPL; ++e) cmax[e] = 0.0;
-#pragma unroll 1
-  for (int64_t rb = rbeg + ty; rb < rend; rb += TY * RU) {
-    double x[RU][CPL];
-    double frow[RU];
-#pragma unroll
-    for (int u = 0; u < RU; ++u) {
-      const int64_t r = rb + u * TY;
-#pragma unroll
-      for (int e = 0; e < CPL; ++e) x[u][e] = 0.0;
-      frow[u] = 1.0;
-      if (r < rend) {
-        if (MODE == AP_ROW_DIV) frow[u] = f[r];  // issued with the row's data loads
-        const double* sp = src + r * lds;
-#pragma unroll
-        for (int h = 0; h < CPL / 2; ++h) {
-          const int64_t c0 = cidx[2 * h];
-          if (VEC && ok[2 * h + 1]) {
-            const double2 v = *reinterpret_cast<const double2*>(sp + c0);
-            x[u][2 * h] = v.x; x[u][2 * h + 1] = v.y;
-          } else {
-            if (ok[2 * h]) x[u][2 * h] = sp[c0];
-            if (ok[2 * h + 1]) x[u][2 * h + 1] = sp[c0 + 1];
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < RU; ++u) {
-      const int64_t r = rb + u * TY;
-      if (r >= rend) continue;  // warp-uniform
-      Divisor fr;
-      if (MODE == AP_ROW_DIV) fr = Divisor(frow[u]);
-      double rmax = 0.0;
-#pragma unroll
-      for (int e = 0; e < CPL; ++e) {
-        double y = x[u][e];
-        if (MODE == AP_ROW_DIV) y = fr.div(y);
-        else if (MODE == AP_COL_DIV) y = fcol[e].div(y);
-        else if (MODE == AP_COL_MUL) y = __dmul_rn(y, mcol[e]);
-        x[u][e] = y;
-        const double v = ok[e] ? fabs(y) : 0.0;
-        rmax = fmax(rmax, v);
-        cmax[e] = fmax(cmax[e], v);
-      }
-      if (dst) {
-        double* dp = dst + r * ldd;
-#pragma unroll
-        for (int h = 0; h < CPL / 2; ++h) {
-          const int64_t c0 = cidx[2 * h];
-          if (VEC && ok[2 * h + 1]) {
-            *reinterpret_cast<double2*>(dp + c0) = make_double2(x[u][2 * h], x[u][2 * h + 1]);
-          } else {
-            if (ok[2 * h]) dp[c0] = x[u][2 * h];
-            if (ok[2 * h + 1]) dp[c0 + 1] = x[u][2 * h + 1];
-          }
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-      if (tx == 0 && row_max) atomic_max_nonneg(&row_max[r], rmax);
-    }
-  }
-  if (col_max) {
-#pragma unroll
-    for (int e = 0; e < CPL; ++e) cm[ty][(e / 2) * (2 * TX) + 2 * tx + (e & 1)] = cmax[e];
-    __syncthreads();
-    for (int q = ty * TX + tx; q < TC; q += TX * TY) {
-      double mx = 0.0;
-#pragma unroll
-      for (int y = 0; y < TY; ++y) mx = fmax(mx, cm[y][q]);
-      const int64_t cc = (int64_t)blockIdx.x * TC + q;
-      if (cc < cols) atomic_max_nonneg(&col_max[cc], mx);
-    }
-  }
-}
-
-// Multiply-only pass for power-of-two factors (pow2 = 1): the factor kernels store the exact
-// reciprocals 1/r, 1/s, 1/p (a power of two's reciprocal is a power of two, exact whenever it
-// is representable), so x / f = x * (1/f) bitwise and every apply is one multiplication.
-// MODE: AP_NONE (reduce only), AP_ROW_MUL (x * g_i), AP_COL_MUL (x * g_j).  Same block / warp
-// layout as k_apply_reduce with 8 columns per lane (256-column strips): half the per-element
-// cost of the row-max shuffles, 8 16-byte loads in flight per lane.  `need_exact`: return
-// unless every factor of this step had an exact reciprocal (flags[F_INEXACT] == 0).
-constexpr int CPL8 = 8, TC8 = TX * CPL8, RU8 = 2;
-enum { AP_ROW_MUL = 4 };
-
-template <int MODE>
-constexpr int mul_blocks_per_sm() { return MODE == AP_COL_MUL ? 2 : 3; }  // COL: 8 more factor registers
-
-template <int MODE, bool VEC>
-__global__ void __launch_bounds__(TX* TY, mul_blocks_per_sm<MODE>())
-    k_apply_reduce_mul(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
-                       int64_t cols, int64_t chunk, const double* __restrict__ g,
-                       double* __restrict__ row_max, double* __restrict__ col_max,
-                       const int* __restrict__ flags, int need_exact) {
-  if (flags && (flags[F_SKIP] || (need_exact && flags[F_INEXACT]))) return;
-  __shared__ double cm[TY][TC8];
-  const int tx = threadIdx.x, ty = threadIdx.y;
-  // lane columns: cbase + off(e), off(e) = (e / 2) * 64 + (e & 1); valid iff off(e) < lim
-  const int64_t cbase = (int64_t)blockIdx.x * TC8 + 2 * tx;
-  const int64_t lim = cols - cbase;
-  const int64_t rbeg = (int64_t)blockIdx.y * chunk;
-  const int64_t rend = rbeg + chunk < rows ? rbeg + chunk : rows;
-  const bool full = lim >= (CPL8 / 2 - 1) * 2 * TX + 2;  // every lane column valid
-  double gc[CPL8], cmax[CPL8];
-#pragma unroll
-  for (int e = 0; e < CPL8; ++e) {
-    const int off = (e / 2) * (2 * TX) + (e & 1);
-    gc[e] = (MODE == AP_COL_MUL && off < lim) ? g[cbase + off] : 1.0;
-    cmax[e] = 0.0;
-  }
-#pragma unroll 1
-  for (int64_t rb = rbeg + ty; rb < rend; rb += TY * RU8) {
-    double x[RU8][CPL8];
-    double gr[RU8];
-#pragma unroll
-    for (int u = 0; u < RU8; ++u) {
-      const int64_t r = rb + u * TY;
-      gr[u] = 1.0;
-#pragma unroll
-      for (int e = 0; e < CPL8; ++e) x[u][e] = 0.0;
-      if (r < rend) {
-        if (MODE == AP_ROW_MUL) gr[u] = g[r];
-        const double* sp = src + r * lds + cbase;
-#pragma unroll
-        for (int h = 0; h < CPL8 / 2; ++h) {
-          const int off = h * (2 * TX);
-          if (VEC && (full || off + 1 < lim)) {
-            const double2 v = *reinterpret_cast<const double2*>(sp + off);
-            x[u][2 * h] = v.x; x[u][2 * h + 1] = v.y;
-          } else {
-            if (off < lim) x[u][2 * h] = sp[off];
-            if (off + 1 < lim) x[u][2 * h + 1] = sp[off + 1];
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < RU8; ++u) {
-      const int64_t r = rb + u * TY;
-      if (r >= rend) continue;  // warp-uniform
-      double rmax = 0.0;
-#pragma unroll
-      for (int e = 0; e < CPL8; ++e) {
-        const int off = (e / 2) * (2 * TX) + (e & 1);
-        double y = x[u][e];
-        if (MODE == AP_ROW_MUL) y = __dmul_rn(y, gr[u]);
-        else if (MODE == AP_COL_MUL) y = __dmul_rn(y, gc[e]);
-        x[u][e] = y;
-        const double v = (full || off < lim) ? fabs(y) : 0.0;
-        rmax = fmax(rmax, v);
-        cmax[e] = fmax(cmax[e], v);
-      }
-      if (dst) {
-        double* dp = dst + r * ldd + cbase;
-#pragma unroll
-        for (int h = 0; h < CPL8 / 2; ++h) {
-          const int off = h * (2 * TX);
-          if (VEC && (full || off + 1 < lim)) {
-            *reinterpret_cast<double2*>(dp + off) = make_double2(x[u][2 * h], x[u][2 * h + 1]);
-          } else {
-            if (off < lim) dp[off] = x[u][2 * h];
-            if (off + 1 < lim) dp[off + 1] = x[u][2 * h + 1];
-          }
-        }
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-      if (tx == 0 && row_max) atomic_max_nonneg(&row_max[r], rmax);
-    }
-  }
-  if (col_max) {
-#pragma unroll
-    for (int e = 0; e < CPL8; ++e) cm[ty][(e / 2) * (2 * TX) + 2 * tx + (e & 1)] = cmax[e];
-    __syncthreads();
-    for (int q = ty * TX + tx; q < TC8; q += TX * TY) {
-      double mx = 0.0;
-#pragma unroll
-      for (int y = 0; y < TY; ++y) mx = fmax(mx, cm[y][q]);
-      const int64_t cc = (int64_t)blockIdx.x * TC8 + q;
-      if (cc < cols) atomic_max_nonneg(&col_max[cc], mx);
-    }
-  }
-}
-
 // exact reciprocal of a power-of-two factor (false if f is not a power of two whose reciprocal
 // is representable; then the dividing pass runs)
 __device__ __forceinline__ bool exact_recip(double f, double* inv) {
@@ -303,94 +62,6 @@ __device__ __forceinline__ bool exact_recip(double f, double* inv) {
   if ((bits & 0x000fffffffffffffLL) != 0 || ex < 1 || ex > 2045 || !(f > 0.0)) return false;
   *inv = __longlong_as_double((int64_t)(2046 - ex) << 52);
   return true;
-}
-
-__device__ bool block_all(bool v) { return __syncthreads_and(v ? 1 : 0) != 0; }
-
-// O step factors (Alg. 3): r'_i = rowmaxA_i, s'_j = colmaxB_j; dA_i *= r'_i;
-// dB_j = s'_j * dB_j; stop test r', s' >= (1+tau)^(-1/2) when `test`.
-__global__ void k_factor_O(const double* __restrict__ rmA, const double* __restrict__ cmB,
-                           int64_t M, int64_t N, int pow2, double* dA, double* dB, double* r_out,
-                           double* s_out, double* r_inv, double* s_inv, int* flags, int test,
-                           double lo_O, double* next_zero, int64_t next_len) {
-  const bool skip = flags[F_DONE] != 0;
-  __syncthreads();
-  if (threadIdx.x == 0) { flags[F_SKIP] = skip ? 1 : 0; flags[F_INEXACT] = 0; }
-  __syncthreads();
-  for (int64_t i = threadIdx.x; i < next_len; i += blockDim.x) next_zero[i] = 0.0;
-  if (skip) return;
-  bool ok = true;
-  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
-    double r = rmA[i];
-    if (!(r > 0.0)) {
-      if (atomicCAS(&flags[F_ERR], 0, 1) == 0) flags[F_ERRIDX] = (int)i;
-      r = __longlong_as_double(0x7ff8000000000000LL);  // NaN propagates to C
-    } else if (pow2) {
-      r = pow2_round(r);
-    }
-    r_out[i] = r;
-    if (pow2 && !exact_recip(r, &r_inv[i])) flags[F_INEXACT] = 1;
-    dA[i] = __dmul_rn(dA[i], r);
-    ok = ok && (r >= lo_O);
-  }
-  for (int64_t j = threadIdx.x; j < N; j += blockDim.x) {
-    double s = cmB[j];
-    if (!(s > 0.0)) {
-      if (atomicCAS(&flags[F_ERR], 0, 2) == 0) flags[F_ERRIDX] = (int)j;
-      s = __longlong_as_double(0x7ff8000000000000LL);
-    } else if (pow2) {
-      s = pow2_round(s);
-    }
-    s_out[j] = s;
-    if (pow2 && !exact_recip(s, &s_inv[j])) flags[F_INEXACT] = 1;
-    dB[j] = __dmul_rn(s, dB[j]);
-    ok = ok && (s >= lo_O);
-  }
-  const bool all = block_all(ok);
-  if (threadIdx.x == 0) {
-    flags[F_STEPS] += 1;
-    if (test && all) flags[F_DONE] = 1;
-  }
-}
-
-// I step factor (Alg. 3): p_k = sqrt(rowmaxB_k / colmaxA_k); dI_k *= p_k;
-// stop test p_k in [(1+tau)^(-1/4), (1+tau)^(1/4)] when `test`.
-__global__ void k_factor_I(const double* __restrict__ cmA, const double* __restrict__ rmB,
-                           int64_t K, int pow2, double* dI, double* p_out, double* p_inv,
-                           int* flags, int test, double lo_I, double hi_I, double* next_zero,
-                           int64_t next_len) {
-  const bool skip = flags[F_DONE] != 0;
-  __syncthreads();
-  if (threadIdx.x == 0) { flags[F_SKIP] = skip ? 1 : 0; flags[F_INEXACT] = 0; }
-  __syncthreads();
-  for (int64_t i = threadIdx.x; i < next_len; i += blockDim.x) next_zero[i] = 0.0;
-  if (skip) return;
-  bool ok = true;
-  for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
-    const double a = cmA[k], b = rmB[k];
-    double p;
-    if (!(a > 0.0) || !(b > 0.0)) {
-      if (atomicCAS(&flags[F_ERR], 0, !(a > 0.0) ? 3 : 4) == 0) flags[F_ERRIDX] = (int)k;
-      p = __longlong_as_double(0x7ff8000000000000LL);
-    } else {
-      p = __dsqrt_rn(__ddiv_rn(b, a));
-      if (pow2) p = pow2_round(p);
-    }
-    p_out[k] = p;
-    if (pow2 && !exact_recip(p, &p_inv[k])) flags[F_INEXACT] = 1;
-    dI[k] = __dmul_rn(dI[k], p);
-    ok = ok && (p >= lo_I && p <= hi_I);
-  }
-  const bool all = block_all(ok);
-  if (threadIdx.x == 0) {
-    flags[F_STEPS] += 1;
-    if (test && all) flags[F_DONE] = 1;
-  }
-}
-
-__global__ void k_fill(double* p, int64_t n, double v) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = v;
 }
 
 // C_ij = (dA_i C'_ij) dB_j (reading A9); VEC: two columns per thread, 16-byte accesses
@@ -456,110 +127,6 @@ int* scale_flags_ptr(void* ws, int64_t M, int64_t K, int64_t N) {
   return scale_ws_view(ws, M, K, N).flags;
 }
 
-static void grid_dims(int64_t rows, int64_t cols, int tc, int ru, int per_sm, dim3* g, int64_t* chunk) {
-  // column strips x row chunks: one wave of per_sm resident blocks per SM, chunks a multiple
-  // of TY * ru rows
-  const int64_t strips = (cols + tc - 1) / tc;
-  int64_t nchunks = std::max<int64_t>(1, (148 * per_sm) / strips);
-  int64_t ch = (rows + nchunks - 1) / nchunks;
-  ch = (ch + TY * ru - 1) / (TY * ru) * (TY * ru);
-  nchunks = (rows + ch - 1) / ch;
-  *g = dim3((unsigned)strips, (unsigned)nchunks);
-  *chunk = ch;
-}
-
-// one streaming pass: dst = apply(src) with the row / column max-abs of the result.
-// mode AP_ROW_DIV / AP_COL_DIV divide by f; with pow2 factors (finv != null) the multiply pass
-// by the exact reciprocals runs instead, and the dividing pass only if some reciprocal was
-// inexact (both check flags on device).
-static void apply_reduce(cudaStream_t st, int mode, const double* src, int64_t lds, double* dst,
-                         int64_t ldd, int64_t rows, int64_t cols, const double* f,
-                         const double* finv, double* row_max, double* col_max, const int* flags) {
-  if (rows == 0 || cols == 0) return;
-  const bool vec = ((uintptr_t)src % 16 == 0) && lds % 2 == 0 &&
-                   (!dst || (((uintptr_t)dst % 16 == 0) && ldd % 2 == 0));
-  dim3 blk(TX, TY);
-  dim3 g;
-  int64_t chunk;
-  const bool mul = mode == AP_NONE || mode == AP_COL_MUL || finv != nullptr;
-  if (mul) {
-    const int mm = mode == AP_ROW_DIV ? AP_ROW_MUL : mode == AP_COL_DIV ? AP_COL_MUL : mode;
-    const double* gv = (mode == AP_ROW_DIV || mode == AP_COL_DIV) ? finv : f;
-    const int need_exact = (mode == AP_ROW_DIV || mode == AP_COL_DIV) ? 1 : 0;
-    grid_dims(rows, cols, TC8, RU8, mm == AP_COL_MUL ? 2 : 3, &g, &chunk);
-#define FMM_ARM(M, V) k_apply_reduce_mul<M, V><<<g, blk, 0, st>>>(src, lds, dst, ldd, rows, cols, chunk, gv, row_max, col_max, flags, need_exact)
-    switch (mm) {
-      case AP_ROW_MUL: if (vec) FMM_ARM(AP_ROW_MUL, true); else FMM_ARM(AP_ROW_MUL, false); break;
-      case AP_COL_MUL: if (vec) FMM_ARM(AP_COL_MUL, true); else FMM_ARM(AP_COL_MUL, false); break;
-      default: if (vec) FMM_ARM(AP_NONE, true); else FMM_ARM(AP_NONE, false); break;
-    }
-#undef FMM_ARM
-    if (!need_exact) return;
-  }
-  // dividing pass (pow2 = 0, or the fallback when a reciprocal was inexact)
-  const int only_if_inexact = mul ? 1 : 0;
-  grid_dims(rows, cols, TC, RU, 4, &g, &chunk);
-#define FMM_AR(M, V) k_apply_reduce<M, V><<<g, blk, 0, st>>>(src, lds, dst, ldd, rows, cols, chunk, f, row_max, col_max, flags, only_if_inexact)
-  switch (mode) {
-    case AP_ROW_DIV: if (vec) FMM_AR(AP_ROW_DIV, true); else FMM_AR(AP_ROW_DIV, false); break;
-    case AP_COL_DIV: if (vec) FMM_AR(AP_COL_DIV, true); else FMM_AR(AP_COL_DIV, false); break;
-    default: break;
-  }
-#undef FMM_AR
-}
-
-// steps: sequence of 'O'/'I' (length nsteps); test_from: index from which the stop test runs
-// (-1: never).  A_out / B_out may alias? no: they are distinct buffers (ws).
-cudaError_t run_scaling(int64_t M, int64_t K, int64_t N, const double* A, int64_t lda,
-                        const double* B, int64_t ldb, double* A_out, int64_t lda_out,
-                        double* B_out, int64_t ldb_out, double* dA, double* dB, double* dI,
-                        const char* steps, int nsteps, bool first_O, double tau, int pow2,
-                        void* sws, cudaStream_t st) {
-  ScaleWsView v = scale_ws_view(sws, M, K, N);
-  const int64_t set = M + K + K + N;
-  cudaError_t e;
-  if ((e = cudaMemsetAsync(v.mx[0], 0, sizeof(double) * set, st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(v.flags, 0, sizeof(int) * F_COUNT, st)) != cudaSuccess) return e;
-  k_fill<<<64, 256, 0, st>>>(dA, M, 1.0);
-  k_fill<<<64, 256, 0, st>>>(dB, N, 1.0);
-  k_fill<<<64, 256, 0, st>>>(dI, K, 1.0);
-  // initial reductions of A, B
-  {
-    double* m = v.mx[0];
-    apply_reduce(st, AP_NONE, A, lda, nullptr, 0, M, K, nullptr, nullptr, m, m + M, nullptr);
-    apply_reduce(st, AP_NONE, B, ldb, nullptr, 0, K, N, nullptr, nullptr, m + M + K, m + M + 2 * K, nullptr);
-  }
-  const double lo_I = pow(1.0 + tau, -0.25), hi_I = pow(1.0 + tau, 0.25), lo_O = pow(1.0 + tau, -0.5);
-  int t0 = -1;
-  for (int t = 0; t < nsteps; ++t) {
-    const bool isO = steps[t] == 'O';
-    if (isO && t0 < 0) t0 = t;
-    const int test = (tau >= 0.0 && t0 >= 0 && t > t0) ? 1 : 0;
-    double* cur = v.mx[t & 1];
-    double* nxt = v.mx[(t + 1) & 1];
-    const double* srcA = t == 0 ? A : A_out;
-    const double* srcB = t == 0 ? B : B_out;
-    const int64_t lsa = t == 0 ? lda : lda_out, lsb = t == 0 ? ldb : ldb_out;
-    if (isO) {
-      k_factor_O<<<1, 1024, 0, st>>>(cur, cur + M + 2 * K, M, N, pow2, dA, dB, v.r, v.s, v.ri, v.si, v.flags,
-                                     test, lo_O, nxt, set);
-      apply_reduce(st, AP_ROW_DIV, srcA, lsa, A_out, lda_out, M, K, v.r, pow2 ? v.ri : nullptr, nxt, nxt + M, v.flags);
-      apply_reduce(st, AP_COL_DIV, srcB, lsb, B_out, ldb_out, K, N, v.s, pow2 ? v.si : nullptr, nxt + M + K,
-                   nxt + M + 2 * K, v.flags);
-    } else {
-      k_factor_I<<<1, 1024, 0, st>>>(cur + M, cur + M + K, K, pow2, dI, v.p, v.pi, v.flags, test, lo_I,
-                                     hi_I, nxt, set);
-      apply_reduce(st, AP_COL_MUL, srcA, lsa, A_out, lda_out, M, K, v.p, nullptr, nxt, nxt + M, v.flags);
-      apply_reduce(st, AP_ROW_DIV, srcB, lsb, B_out, ldb_out, K, N, v.p, pow2 ? v.pi : nullptr, nxt + M + K,
-                   nxt + M + 2 * K, v.flags);
-    }
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  }
-  (void)first_O;
-  return cudaGetLastError();
-}
-
-
 // =============================================================================================
 // Alg. 1-3 in ONE cooperative kernel.  All steps of a scaling run -- the max
 // reductions, the factor computations with the stopping test, the applications -- run in one
@@ -616,10 +183,6 @@ __device__ __forceinline__ double scale2(double x, int e) {
   if (e == 0) return x;
   if (e >= -1022 && e <= 1023) return __dmul_rn(x, __longlong_as_double((int64_t)(e + 1023) << 52));
   return scale2_wide(x, e);
-}
-__device__ __forceinline__ bool exact_value(double x, double v) {
-  const double a = fabs(v);
-  return (a >= 2.2250738585072014e-308 || x == 0.0) && a <= 1.7976931348623157e308;
 }
 __device__ __forceinline__ int log2_pow2(double f) {  // f an exact normal power of two
   return (int)((__double_as_longlong(f) >> 52) & 0x7ff) - 1023;
