@@ -390,6 +390,14 @@ fmm_status fmm_comm_unique_id(void* out128);
  * loaded or the init fails. */
 fmm_status fmm_plan_set_comm(fmm_plan* plan, const void* id128, int rank, int nranks);
 
+/* Single-launch small plans (host-only; default on).  A two-level FP64 plan (no padding, no
+ * scaling, one rank) that compiles to one two-level S / T pass, the batched leaf products and
+ * one two-level W-combination pass, with at most 4 waves of 32 x 64 leaf tiles (BASELINE C1:
+ * Strassen-Winograd L = 2 at 512^3), runs the three as phases of ONE cooperative kernel with
+ * grid-wide barriers (launch latency dominates three launches at this size).  Results are
+ * bitwise the three-launch schedule's.  enable = 0 keeps three launches. */
+fmm_status fmm_plan_set_single_launch(fmm_plan* plan, int enable);
+
 /* Virtual scaling (host-only; default on).  With power-of-two factors (fmm_scaling.pow2 = 1) the
  * whole scaling run (Alg. 1-3) is one cooperative kernel whose steps read the
  * ORIGINAL A and B with the factors applied on the fly (exact: multiplication by powers of two),

@@ -134,6 +134,7 @@ struct fmm_plan {
   // S_r / T_r from the original A, B (the scaled A', B' are not written)
   bool virt_scale = false;
   bool virt_scale_enable = true;  // fmm_plan_set_virtual_scaling
+  bool single_launch = true;      // fmm_plan_set_single_launch: small two-level plans as one kernel
   bool unscale_fused = false;     // the root K3 / K3X2 applies the unscale
   ncclComm_t comm = nullptr;
   // comm mode 3 barrier (fmm_plan_set_barrier): called instead of the 1-word NCCL all-reduce
@@ -731,6 +732,7 @@ struct Builder {
                        (p->schedule == 0 && bf_bytes > (int64_t)24 << 30);
     if (!split) {
       breadth_first(0, {root});
+      try_single_launch();
       return;
     }
     if ((p->schedule == 3 || (p->schedule == 0 && hybrid_on())) && p->nranks == 1 && !p2p_mode() &&
@@ -746,6 +748,31 @@ struct Builder {
   }
 
   bool p2p_mode() const { return p->p2p_active(); }
+
+  // A two-level plan compiled to K1X2 -> K2 -> K3X2 whose leaf phase is at most a few waves of
+  // 32 x 64 tiles (C1: 784 tiles) runs as one cooperative kernel (kernels_small.cu): the three
+  // launches are launch-bound at this size.  Bitwise the three-launch schedule.
+  void try_single_launch() {
+    if (!p->single_launch || p->dtype != FMM_F64 || p->L != 2 || p->padded ||
+        p->scaling.mode != FMM_SCALE_NONE || p->nranks != 1 || p->steps.size() != 3)
+      return;
+    const Step s1 = p->steps[0], s2 = p->steps[1], s3 = p->steps[2];
+    if (s1.kind != STEP_K1 || !s1.x2 || s1.count > 2 || s2.kind != STEP_K2 || s3.kind != STEP_K3 ||
+        s3.x2 != s1.x2)
+      return;
+    const int64_t tiles = ((s2.rows + small_tile_m() - 1) / small_tile_m()) *
+                          ((s2.cols + small_tile_n() - 1) / small_tile_n());
+    if ((int64_t)s2.count * tiles > 4 * 3 * 148) return;
+    Step st{};
+    st.kind = STEP_SMALL;
+    st.x2 = s1.x2;
+    st.dev_off = s1.dev_off; st.count = s1.count;
+    st.dev_off2 = s2.dev_off; st.count2 = s2.count;
+    st.rows = s2.rows; st.cols = s2.cols; st.inner = s2.inner;
+    st.dev_off3 = s3.dev_off; st.count3 = s3.count;
+    st.bar_off = ws_alloc(1);
+    p->steps.assign(1, st);
+  }
 
   static bool hybrid_on() {
     const char* e = getenv("FMM_HYBRID");
@@ -1007,12 +1034,20 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
     case STEP_ZERO: node_bytes = sizeof(ZeroNode); break;
     case STEP_K2: node_bytes = sizeof(LeafNode); break;
     case STEP_K2F: node_bytes = sizeof(FusedNode); break;
+    case STEP_SMALL: node_bytes = sizeof(K1x2Node); break;
   }
   const void* nd = (const uint8_t*)p->dev_desc + s.dev_off + c0 * node_bytes;
   const int ts = k2f_tile_of(s.k2f_cfg);
   const int64_t tiles_f = p->dtype == FMM_F32 ? ((s.rows + 127) / 128) * ((s.cols + 255) / 256)
                                               : ((s.rows + ts - 1) / ts) * ((s.cols + ts - 1) / ts);
   switch (s.kind) {
+    case STEP_SMALL: {
+      const uint8_t* d = (const uint8_t*)p->dev_desc;
+      return launch_small_plan(s.x2, (const K1x2Node*)(d + s.dev_off), s.count,
+                               (const LeafNode*)(d + s.dev_off2), s.count2, s.rows, s.cols, s.inner,
+                               (const K3x2Node*)(d + s.dev_off3), s.count3, b, vec,
+                               (unsigned int*)((double*)b.p[BASE_WS] + s.bar_off), st);
+    }
     case STEP_K1: return launch_k1<T>(s, nd, p->dev_coef, b, vec, st, sc);
     case STEP_K3: return launch_k3<T>(s, nd, p->dev_coef, b, vec, st, sc);
     case STEP_ACC: return launch_acc<T>(s, nd, p->dev_coef, b, vec, st);
@@ -1056,6 +1091,7 @@ static const char* step_name(const Step& s) {
     case STEP_ACC: return "fmm.ACC";
     case STEP_ZERO: return "fmm.ZERO";
     case STEP_K2F: return "fmm.K2F";
+    case STEP_SMALL: return "fmm.SMALL";
   }
   return "fmm.step";
 }
@@ -1068,7 +1104,7 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
   for (size_t si = i0; si < i1; ++si) {
     const Step& s = p->steps[si];
     NvtxRange nv(step_name(s));
-    TimedLaunch tl(p, s.kind == STEP_K2F ? STEP_K2 : s.kind, st);
+    TimedLaunch tl(p, (s.kind == STEP_K2F || s.kind == STEP_SMALL) ? STEP_K2 : s.kind, st);
     cudaError_t e = cudaSuccess;
     int64_t maxn = kMaxNodes;
     if (s.kind == STEP_K2F && s.chunk > 0 && s.nr > s.chunk)  // grid.y = groups x nodes
@@ -1719,6 +1755,12 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
     if (r != 0) { set_error(std::string(what) + ": " + (api->getErrorString ? api->getErrorString(r) : "?")); return FMM_E_NCCL; }
   }
   return FMM_OK;
+}
+
+fmm_status fmm_plan_set_single_launch(fmm_plan* p, int enable) {
+  if (!p) { set_error("fmm_plan_set_single_launch: null plan"); return FMM_E_ARG; }
+  p->single_launch = enable != 0;
+  return compile_plan(p);
 }
 
 fmm_status fmm_plan_set_virtual_scaling(fmm_plan* p, int enable) {

@@ -199,7 +199,8 @@ struct FusedNode {
   Op a[kMaxR], b[kMaxR];  // leaf operands S_r, T_r (index i, not r)
 };
 
-enum StepKind { STEP_K1 = 1, STEP_K2 = 2, STEP_K3 = 3, STEP_ACC = 4, STEP_ZERO = 5, STEP_K2F = 8 };
+enum StepKind { STEP_K1 = 1, STEP_K2 = 2, STEP_K3 = 3, STEP_ACC = 4, STEP_ZERO = 5, STEP_K2F = 8,
+                STEP_SMALL = 9 };
 
 struct Step {
   int kind;
@@ -222,6 +223,11 @@ struct Step {
   int x1 = 0;        // one-level K1 whose nodes all use built-in rule x1 - 1 (2x2): the
                      // compile-time specialised kernel (k1c_lincomb)
   int unscale = 0;   // K3 / K3X2 of the root of a scaled plan: the unscale folded in
+  // STEP_SMALL (kernels_small.cu): the K1X2 nodes (dev_off, count), the leaves (dev_off2,
+  // count2, rows x cols x inner), the K3X2 nodes (dev_off3, count3), rule pair x2, and the grid
+  // barrier word at ws offset bar_off (elements)
+  int count2 = 0, count3 = 0;
+  int64_t dev_off3 = -1, bar_off = -1;
 };
 
 // ---- kernel launchers (kernels_*.cu) -----------------------------------------------------------
@@ -259,6 +265,13 @@ cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t
                                   int* turn, int cfg);
 // output tile edge (BM = BN) of K2F tile configuration cfg (13: 64, 16: 128)
 int k2f_tile_of(int cfg);
+// The single-launch small plan (K1X2 -> leaf products -> K3X2 in one cooperative kernel); its
+// leaf-phase tile (small_tile_m x small_tile_n)
+cudaError_t launch_small_plan(int pair, const K1x2Node* k1, int nk1, const LeafNode* lf, int nlf,
+                              int64_t m, int64_t n, int64_t k, const K3x2Node* k3, int nk3,
+                              const Bases& b, bool vec, unsigned int* bar, cudaStream_t st);
+int small_tile_m();
+int small_tile_n();
 // K2F for the FP32 tensor-core leaves (3xTF32 / TF32 on tcgen05, TMEM double-buffered)
 cudaError_t launch_gemm_tf32_fused(const FusedNode* dev_nodes, const LeafNode* dev_split_leaves,
                                    int count, int nr, int64_t m, int64_t n, int64_t k,

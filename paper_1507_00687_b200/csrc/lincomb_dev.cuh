@@ -30,9 +30,22 @@ struct Vec {
   T v[VEC];
 };
 
-template <typename T, int VEC>
+// CG: an L2-only load (ld.global.cg) -- for data written earlier in the same kernel by other
+// SMs (the single-launch small plan), which a non-coherent L1 line must not serve
+template <typename T, int VEC, bool CG = false>
 __device__ __forceinline__ Vec<T, VEC> ld_vec(const T* p) {
   Vec<T, VEC> r;
+  if constexpr (CG) {
+    if constexpr (VEC * sizeof(T) == 16 && sizeof(T) == 8) {
+      const double2 x = __ldcg(reinterpret_cast<const double2*>(p));
+      r.v[0] = x.x;
+      r.v[1] = x.y;
+    } else {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) r.v[e] = __ldcg(p + e);
+    }
+    return r;
+  }
   if constexpr (VEC * sizeof(T) == 16) {
     if constexpr (sizeof(T) == 8) {
       double2 x = *reinterpret_cast<const double2*>(p);
@@ -375,7 +388,7 @@ struct W2Pair {
 // One grandchild row position of a K3X2 node: per r1 (ascending) form C_{r1}[k2] from the
 // M_{r1 r2} (level d+1, ascending r2) and accumulate w1_{k1 r1} C_{r1}[k2] into the 16 outputs
 // (level d); then store them.
-template <typename T, int VEC, int RA, int RB, bool US = false>
+template <typename T, int VEC, int RA, int RB, bool US = false, bool CG = false>
 __device__ __forceinline__ void k3x2_row(const T* const* iptr, T* __restrict__ out, int64_t ldo,
                                          int64_t rows, int64_t cols, int64_t i, int64_t jv,
                                          const double* ur = nullptr, const double* uc = nullptr) {
@@ -387,7 +400,7 @@ __device__ __forceinline__ void k3x2_row(const T* const* iptr, T* __restrict__ o
       Vec<T, VEC> y[4];
       static_for<X::R2>([&](auto r2) {
         if constexpr (X::used(RB, r2)) {
-          const Vec<T, VEC> m = ld_vec<T, VEC>(iptr[r1 * X::R2 + r2] + off);
+          const Vec<T, VEC> m = ld_vec<T, VEC, CG>(iptr[r1 * X::R2 + r2] + off);
           static_for<4>([&](auto k2) {
             if constexpr (X::code(RB, k2, r2) != 0u)
               lc_fixed<X::code(RB, k2, r2)>(y[k2], X::first(RB, k2, r2), m);

@@ -80,6 +80,7 @@ SIGNATURES = {
     "fmm_plan_set_comm": (_I, [_P, _P, _I, _I]),
     "fmm_plan_set_barrier": (_I, [_P, _P, _P]),
     "fmm_plan_set_virtual_scaling": (_I, [_P, _I]),
+    "fmm_plan_set_single_launch": (_I, [_P, _I]),
     "fmm_last_error": (C.c_char_p, []),
     "fmm_version": (C.c_char_p, []),
 }
@@ -271,7 +272,12 @@ class Plan:
         _call("fmm_plan_launch_count", self._h, C.byref(n))
         return n.value
 
-    STEP_KINDS = {1: "K1", 2: "K2", 3: "K3", 4: "ACC", 5: "ZERO", 6: "SCALE", 7: "REDUCE"}
+    STEP_KINDS = {1: "K1", 2: "K2", 3: "K3", 4: "ACC", 5: "ZERO", 6: "SCALE", 7: "REDUCE"}  # K2 includes K2F / the single-launch kernel
+
+    def set_single_launch(self, enable: bool = True):
+        """Small two-level plans as one cooperative kernel (default) or three launches."""
+        _call("fmm_plan_set_single_launch", self._h, int(enable))
+        self._ws = None
 
     def set_virtual_scaling(self, enable: bool = True):
         """Power-of-two scaling applied on the fly by the root K1 (default) or materialised."""

@@ -74,7 +74,9 @@ def test_plan_shape_errors_and_workspace():
     # non-divisible dims are zero-padded: 510 -> 512 costs the padded copies
     pp = fb.Plan([w, w], 510, 512, 512)
     p = fb.Plan([w, w], 512, 512, 512)
-    assert pp.launch_count() == p.launch_count() + 3  # pad A, pad B, crop C
+    assert p.launch_count() == 1  # the single-launch small plan (K1X2, leaves, K3X2 in one kernel)
+    p.set_single_launch(False)
+    assert pp.launch_count() == p.launch_count() + 3 == 6  # pad A, pad B, crop C
     assert pp.workspace_bytes() == p.workspace_bytes() + 3 * 512 * 512 * 8
     ws = p.workspace_bytes()
     # breadth-first, two levels per K1 pass (default): level 1: 7 M blocks of 256^2 (its S / T
