@@ -58,50 +58,90 @@ def log(*a):
 
 # ------------------------------------------------------------------------------------------
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms while active."""
+    """SM clock and clock-event (throttle) reasons sampled in-process through NVML every 2 ms by a
+    background thread while active, plus one synchronous sample each at the start and the end of
+    the timed region (`point()`), so even a sub-millisecond timed region has samples taken while
+    its kernels run.  Falls back to nvidia-smi (200 ms) when NVML is unavailable."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_s: float = 0.002):
         self.index = index
-        self.proc = None
-        self.lines = []
-        self.stamps = []
-        self.first = 0
+        self.period = period_s
+        self.samples = []  # (sm_mhz, reason bitmask)
+        self.sm_max = None
+        self.on = False
+        self.nv = None
+        self.h = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.sm_max = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception:  # noqa: BLE001 -- NVML missing: nvidia-smi fallback below
+            self.nv = None
+
+    def _one(self):
+        if self.nv is None:
+            return
+        try:
+            sm = float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            rs = int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            self.samples.append((sm, rs))
+        except Exception:  # noqa: BLE001
+            pass
+
+    def _loop(self):
+        while self.on:
+            self._one()
+            time.sleep(self.period)
+
+    def point(self):
+        """A synchronous sample (call right after enqueueing / before synchronising)."""
+        self._one()
 
     def start(self):
+        self.samples = []
+        if self.nv is None:
+            return self._smi_start()
+        self.on = True
+        self.t = threading.Thread(target=self._loop, daemon=True)
+        self.t.start()
+
+    def stop(self):
+        if self.nv is None:
+            return self._smi_stop()
+        self.on = False
+        self.t.join(timeout=1.0)
+        if not self.samples:
+            return None
+        reasons = sorted({n for _, rs in self.samples for n, bit in self.REASONS if rs & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.sm_max,
+                "reasons": reasons, "samples": len(self.samples), "source": "NVML in-process, 2 ms"}
+
+    # -- nvidia-smi fallback (200 ms period) --
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def _smi_start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            self.lines = []
+            self.t = threading.Thread(target=lambda: [self.lines.append(x.strip()) for x in self.proc.stdout],
+                                      daemon=True)
             self.t.start()
         except OSError:
             self.proc = None
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-            self.stamps.append(time.monotonic())
-
-    def wait_first(self, timeout=3.0):
-        """Block until nvidia-smi has produced its first line (it takes ~0.1-0.3 s to start)."""
-        t = time.monotonic()
-        while self.proc is not None and not self.lines and time.monotonic() - t < timeout:
-            time.sleep(0.01)
-
-    def mark(self):
-        """Index of the next sample: samples from here on were taken after this call."""
-        return len(self.lines)
-
-    def stop(self, first=None):
-        if self.proc is None:
+    def _smi_stop(self):
+        if getattr(self, "proc", None) is None:
             return None
-        if first is not None:
-            self.first = first
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -109,22 +149,22 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines[self.first:]:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 8:
+        for ln in self.lines:
+            parts = [q.strip() for q in ln.split(",")]
+            if len(parts) < 6:
                 continue
             try:
                 sm.append(float(parts[0]))
                 mx = float(parts[1])
             except ValueError:
                 continue
-            for n, v in zip(names, parts[4:8]):
+            for n, v in zip(names, parts[2:6]):
                 if v.lower() == "active":
                     reasons.add(n)
         if not sm:
             return None
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": "nvidia-smi, 200 ms"}
 
 
 # ------------------------------------------------------------------------------------------
@@ -511,14 +551,13 @@ def run_fmm(args):
     small = (M * K + K * N + M * N) * esz < (512 << 20)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda") if small else None
     sampler.start()
-    sampler.wait_first()
-    first = sampler.mark()
     if not small:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
+        sampler.point()  # while the enqueued steps run
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
     else:  # operands fit in L2: flush L2 (256 MB write) between steps, outside the events
@@ -531,33 +570,14 @@ def run_fmm(args):
             step()
             b2.record(stream)
             evs.append((a, b2))
+        sampler.point()
         torch.cuda.synchronize()
         ms = sum(a.elapsed_time(b2) for a, b2 in evs)
+    clocks = sampler.stop()
     kinds = plan.step_times()
     plan.set_timing(False)
-    # A timed region shorter than the 200 ms sampling period may see no sample: keep the GPU on
-    # the same (untimed) steps until one arrives, and say so in the clocks record.
-    extra = 0
-    t_ext = time.monotonic()
-    while True:
-        need = sampler.proc is not None and sampler.mark() == first and time.monotonic() - t_ext < 2.0
-        if ws > 1:  # the step may hold a collective: every rank runs the same number of extras
-            f = torch.tensor([1.0 if need else 0.0], device="cuda")
-            dist.all_reduce(f, op=dist.ReduceOp.MAX)
-            need = f.item() > 0
-        if not need:
-            break
-        with torch.cuda.stream(stream):
-            if flush is not None:
-                flush.fill_(1)
-            step()
-        torch.cuda.synchronize()
-        extra += 1
     if ws > 1:
         dist.barrier()
-    clocks = sampler.stop(first)
-    if clocks is not None:
-        clocks["untimed_steps_after"] = extra
     if ws > 1:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -590,7 +610,11 @@ def run_fmm(args):
     workload = f"{args.config}-{args.dtype}-n{M}-L{L}-p{ws}" if args.config == "C5" else \
         f"{args.config}-{args.dtype}-p{ws}"
     fused = plan.fused_launches() > 0
-    k2_name = ("k2f_gemm_f64 (leaf products on DMMA mma.sync f64 + the parents' W-combination "
+    single = (plan.launch_count() == 1 and len(rules) == 2 and args.scaling == "none"
+              and args.dtype == "f64")
+    k2_name = ("k_small_plan (the whole step in one cooperative kernel: K1X2, the leaf products on "
+               "DMMA mma.sync f64, K3X2; achieved = leaf flops / kernel time)" if single else
+               "k2f_gemm_f64 (leaf products on DMMA mma.sync f64 + the parents' W-combination "
                "fused in the epilogue)" if fused else "k2_gemm_f64 (leaf products, DMMA mma.sync f64)")
     k2_name32 = ("k2f_tf32 (3xTF32 leaf products on tcgen05 + the parents' W-combination in a TMEM "
                  "double-buffered epilogue)" if fused else "k2_tf32 (3xTF32 leaf products on tcgen05)")

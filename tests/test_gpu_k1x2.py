@@ -159,6 +159,7 @@ def test_ineligible_rules_fall_back(fb):
     assert np.array_equal(outs[0], outs[1])
     # and an eligible pair drops one launch
     p = fb.Plan([w, w], 256, 256, 256)
+    p.set_single_launch(False)  # (else the whole plan is one kernel)
     n2 = p.launch_count()
     p.set_k1_levels(1)
     assert p.launch_count() == n2 + 1
