@@ -34,7 +34,7 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
                              const double* B, int64_t ldb, double* A_out, int64_t lda_out,
                              double* B_out, int64_t ldb_out, double* dA, double* dB, double* dI,
                              int nsteps, bool first_O, double tau, int pow2, int materialise_end,
-                             void* sws, unsigned int* bar, cudaStream_t st);
+                             void* sws, cudaStream_t st);
 void scale_virtual_view(void* sws, int64_t M, int64_t K, int64_t N, const int32_t** exAr,
                         const int32_t** exAc, const int32_t** exBr, const int32_t** exBc,
                         const int** mode_flag, const int** ext);
@@ -770,7 +770,6 @@ struct Builder {
     st.dev_off2 = s2.dev_off; st.count2 = s2.count;
     st.rows = s2.rows; st.cols = s2.cols; st.inner = s2.inner;
     st.dev_off3 = s3.dev_off; st.count3 = s3.count;
-    st.bar_off = ws_alloc(1);
     p->steps.assign(1, st);
   }
 
@@ -1045,8 +1044,7 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
       const uint8_t* d = (const uint8_t*)p->dev_desc;
       return launch_small_plan(s.x2, (const K1x2Node*)(d + s.dev_off), s.count,
                                (const LeafNode*)(d + s.dev_off2), s.count2, s.rows, s.cols, s.inner,
-                               (const K3x2Node*)(d + s.dev_off3), s.count3, b, vec,
-                               (unsigned int*)((double*)b.p[BASE_WS] + s.bar_off), st);
+                               (const K3x2Node*)(d + s.dev_off3), s.count3, b, vec, st);
     }
     case STEP_K1: return launch_k1<T>(s, nd, p->dev_coef, b, vec, st, sc);
     case STEP_K3: return launch_k3<T>(s, nd, p->dev_coef, b, vec, st, sc);
@@ -1150,7 +1148,7 @@ static fmm_status scale_common(int64_t M, int64_t K, int64_t N, const void* A, i
   void* own = nullptr;
   cudaError_t e = cudaSuccess;
   double *tdA = (double*)dA, *tdB = (double*)dB, *tdI = (double*)dI;
-  // layout: [scale workspace | grid-barrier word (256 B) | factor vectors the caller omitted]
+  // layout: [scale workspace | 256 B | factor vectors the caller omitted]
   size_t need = scale_ws_bytes(M, K, N) + 256 + (size_t)(M + N + K) * 8 + 1024;
   if (!ws) {
     e = cudaMallocAsync(&own, need, st);
@@ -1158,14 +1156,13 @@ static fmm_status scale_common(int64_t M, int64_t K, int64_t N, const void* A, i
   }
   uint8_t* w = (uint8_t*)(ws ? ws : own);
   w = (uint8_t*)(((uintptr_t)w + 255) & ~(uintptr_t)255);
-  unsigned int* bar = (unsigned int*)(w + (scale_ws_bytes(M, K, N) + 255) / 256 * 256);
-  uint8_t* extra = (uint8_t*)bar + 256;
+  uint8_t* extra = w + (scale_ws_bytes(M, K, N) + 255) / 256 * 256 + 256;
   if (!tdA) { tdA = (double*)extra; }
   if (!tdB) { tdB = (double*)extra + M; }
   if (!tdI) { tdI = (double*)extra + M + N; }
   e = run_scaling_coop(M, K, N, (const double*)A, lda, (const double*)B, ldb, (double*)A_out, lda_out,
                        (double*)B_out, ldb_out, tdA, tdB, tdI, (int)steps.size(), steps[0] == 'O', tau,
-                       pow2, /*materialise_end=*/1, w, bar, st);
+                       pow2, /*materialise_end=*/1, w, st);
   int* flags = scale_flags_ptr(w, M, K, N);
   if (e == cudaSuccess && steps_dev)
     e = cudaMemcpyAsync(steps_dev, flags + 1, sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
@@ -1637,7 +1634,6 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
     dB = dA + p->M;
     double* dI = dB + p->N;
     void* sws = (void*)(((uintptr_t)(dI + p->K) + 255) & ~(uintptr_t)255);
-    unsigned int* bar = (unsigned int*)((uint8_t*)sws + (scale_ws_bytes(p->M, p->K, p->N) + 255) / 256 * 256);
     std::string steps;
     double tau;
     scaling_steps(p->scaling, &steps, &tau);
@@ -1647,7 +1643,7 @@ static fmm_status execute_impl(const fmm_plan* p, const void* A, int64_t lda, co
     // exponents (or A', B' if the run had to materialise them), else A', B' are written
     cudaError_t e = run_scaling_coop(p->M, p->K, p->N, (const double*)A, lda, (const double*)B, ldb,
                                      Ap, p->K, Bp, p->N, dA, dB, dI, (int)steps.size(), steps[0] == 'O',
-                                     tau, p->scaling.pow2, p->virt_scale ? 0 : 1, sws, bar, st);
+                                     tau, p->scaling.pow2, p->virt_scale ? 0 : 1, sws, st);
     if (e != cudaSuccess) return cuda_status(e, "fmm_execute scaling");
     sin.ur = dA;
     sin.uc = dB;

@@ -224,10 +224,9 @@ struct Step {
                      // compile-time specialised kernel (k1c_lincomb)
   int unscale = 0;   // K3 / K3X2 of the root of a scaled plan: the unscale folded in
   // STEP_SMALL (kernels_small.cu): the K1X2 nodes (dev_off, count), the leaves (dev_off2,
-  // count2, rows x cols x inner), the K3X2 nodes (dev_off3, count3), rule pair x2, and the grid
-  // barrier word at ws offset bar_off (elements)
+  // count2, rows x cols x inner), the K3X2 nodes (dev_off3, count3), rule pair x2
   int count2 = 0, count3 = 0;
-  int64_t dev_off3 = -1, bar_off = -1;
+  int64_t dev_off3 = -1;
 };
 
 // ---- kernel launchers (kernels_*.cu) -----------------------------------------------------------
@@ -269,7 +268,7 @@ int k2f_tile_of(int cfg);
 // leaf-phase tile (small_tile_m x small_tile_n)
 cudaError_t launch_small_plan(int pair, const K1x2Node* k1, int nk1, const LeafNode* lf, int nlf,
                               int64_t m, int64_t n, int64_t k, const K3x2Node* k3, int nk3,
-                              const Bases& b, bool vec, unsigned int* bar, cudaStream_t st);
+                              const Bases& b, bool vec, cudaStream_t st);
 int small_tile_m();
 int small_tile_n();
 // K2F for the FP32 tensor-core leaves (3xTF32 / TF32 on tcgen05, TMEM double-buffered)

@@ -11,9 +11,13 @@
 #include <cstdlib>
 #include <utility>
 
+#include <cooperative_groups.h>
+
 #include "fmm_internal.h"
 
 namespace fmm {
+
+namespace cg = cooperative_groups;
 
 // flags layout (int32): [0] done, [1] steps taken, [2] error kind (0 none; 1 zero row of A,
 // 2 zero col of B, 3 zero col of A, 4 zero row of B), [3] error index,
@@ -738,30 +742,12 @@ __device__ __noinline__ void col_tile_tma(const MatPass& q, int tile, int* flags
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(&flags[F_BAD], 1);
 }
 
-// grid barrier: every block of the cooperative launch arrives, then all proceed
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks, unsigned int& gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    ++gen;
-    __threadfence();
-    const unsigned int target = gen * nblocks;
-    atomicAdd(bar, 1u);
-    while (true) {
-      const unsigned int v = *(volatile unsigned int*)bar;
-      if (v >= target) break;
-      __nanosleep(32);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 // dynamic shared memory of k_scale_coop: the TMA stage ring (also the warp-combine buffers),
 // its mbarriers, the row exponents of a tile, the per-warp parities
 constexpr size_t kCoopSmem = (size_t)8 * CS * CSTG * sizeof(double) + 8 * CS * sizeof(uint64_t) +
                              kTmaRows * sizeof(int32_t) + 8 * sizeof(uint32_t);
 
-__global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* bar) {
+__global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
   extern __shared__ __align__(128) uint8_t dsm[];
   TmaSmem tsm;
   tsm.stage = reinterpret_cast<double*>(dsm);
@@ -775,7 +761,9 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* 
   double (*cmd)[256] = reinterpret_cast<double (*)[256]>(dsm);
   unsigned long long (*cm)[CSTRIP] = reinterpret_cast<unsigned long long (*)[CSTRIP]>(dsm);
   const unsigned int nb = gridDim.x;
-  unsigned int gen = 0;
+  // grid-wide barrier of the cooperative launch (orders global memory and invalidates L1, so
+  // the factors / exponents / maxima written before it are what every block reads after it)
+  cg::grid_group grid = cg::this_grid();
   int* flags = a.flags;
   const int64_t M = a.M, K = a.K, N = a.N;
   const int64_t gtid = (int64_t)blockIdx.x * CT + threadIdx.x, gstride = (int64_t)nb * CT;
@@ -786,7 +774,7 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* 
   for (int64_t i = gtid; i < M + 2 * K + N; i += gstride) { a.mx[0][i] = 0.0; a.mx[1][i] = 0.0; }
   if (gtid == 0) flags[F_MODE] = a.pow2 ? 0 : 1;
   if (gtid < 8) flags[F_EXT + gtid] = (gtid & 1) ? (-0x7fffffff - 1) : 0x7fffffff;
-  grid_barrier(bar, nb, gen);
+  grid.sync();
 
   auto views = [&](int isO, int kind, double* m) {  // (A part, B part) of a pass
     MatPass pa{}, pb{};
@@ -869,7 +857,7 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* 
     set_max(pp.first, pp.second, isO, a.mx[0]);
     run_pass(PK_RAW, pp.first, pp.second);
   }
-  grid_barrier(bar, nb, gen);
+  grid.sync();
   int t0 = -1;
   for (int t = 0; t < a.nsteps; ++t) {
     const int isO = (t % 2 == 0) == (a.first_O != 0);
@@ -940,7 +928,7 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* 
     if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) atomicAdd(fail, 1);
     if (__any_sync(0xffffffffu, badf) && (threadIdx.x & 31) == 0 && flags[F_MODE] == 0)
       atomicExch(&flags[F_BAD], 1);
-    grid_barrier(bar, nb, gen);
+    grid.sync();
     if (gtid == 0) flags[F_STEPS] += 1;
     const bool done = (test && *(volatile int*)fail == 0) || t == a.nsteps - 1;
     const bool need_next = !done;  // the values after this step feed another step
@@ -952,29 +940,29 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* 
       if (need_next) set_max(pp.first, pp.second, !isO, nxt);
       run_pass(PK_MAT, pp.first, pp.second);
       if (gtid == 0) { flags[F_MODE] = 1; flags[F_STORED] = 1; }
-      grid_barrier(bar, nb, gen);
+      grid.sync();
     } else if (*(volatile int*)&flags[F_MODE] == 0) {
       if (need_next) {  // virtual: the next step's reductions of the values after this step
         auto pp = views(!isO, PK_VIRTUAL, nxt);
         set_max(pp.first, pp.second, !isO, nxt);
         run_pass(PK_VIRTUAL, pp.first, pp.second);
-        grid_barrier(bar, nb, gen);
+        grid.sync();
         if (*(volatile int*)&flags[F_BAD]) {  // inexact intermediates: redo, materialised
           for (int64_t i = gtid; i < set; i += gstride) nxt[i] = 0.0;
-          grid_barrier(bar, nb, gen);
+          grid.sync();
           auto pm = views(isO, PK_MAT, nxt);
           set_factors(pm.first, pm.second, isO);
           set_max(pm.first, pm.second, !isO, nxt);
           run_pass(PK_MAT, pm.first, pm.second);
           if (gtid == 0) { flags[F_MODE] = 1; flags[F_STORED] = 1; }
-          grid_barrier(bar, nb, gen);
+          grid.sync();
         }
       } else if (a.materialise_end) {  // the caller needs A', B' in memory
         auto pp = views(isO, PK_MAT, nxt);
         set_factors(pp.first, pp.second, isO);
         run_pass(PK_MAT, pp.first, pp.second);
         if (gtid == 0) { flags[F_MODE] = 1; flags[F_STORED] = 1; }
-        grid_barrier(bar, nb, gen);
+        grid.sync();
       }
     } else {  // materialised: apply in place (from A, B at the first application)
       auto pp = views(isO, PK_MAT, nxt);
@@ -982,7 +970,7 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* 
       if (need_next) set_max(pp.first, pp.second, !isO, nxt);
       run_pass(PK_MAT, pp.first, pp.second);
       if (gtid == 0) flags[F_STORED] = 1;
-      grid_barrier(bar, nb, gen);
+      grid.sync();
     }
     if (done) {
       if (gtid == 0 && t < a.nsteps - 1) flags[F_DONE] = 1;
@@ -1012,8 +1000,6 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a, unsigned int* 
 
 }  // namespace
 
-size_t coop_scale_ws_extra() { return 64; }  // the grid barrier word (+ padding)
-
 // Launch Alg. 1-3 as one cooperative kernel.  Writes dA, dB, dI, the flags, and either the
 // virtual form's exponents (flags[F_MODE] = 0 at the end: the plan's root K1 applies them) or
 // A', B' into A_out / B_out (flags[F_STORED] = 1).  materialise_end = 1 forces A', B' into
@@ -1022,11 +1008,10 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
                              const double* B, int64_t ldb, double* A_out, int64_t lda_out,
                              double* B_out, int64_t ldb_out, double* dA, double* dB, double* dI,
                              int nsteps, bool first_O, double tau, int pow2, int materialise_end,
-                             void* sws, unsigned int* bar, cudaStream_t st) {
+                             void* sws, cudaStream_t st) {
   ScaleWsView v = scale_ws_view(sws, M, K, N);
   cudaError_t e;
   if ((e = cudaMemsetAsync(v.flags, 0, sizeof(int) * F_COUNT, st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(bar, 0, sizeof(unsigned int), st)) != cudaSuccess) return e;
   static int blocks_per_sm = -1, sms = 0;
   if (blocks_per_sm < 0) {
     int dev = 0;
@@ -1081,7 +1066,7 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
   rtiles(K, N, &a.rrowsB, &a.rsegsB, &a.rtilesB);
   ctiles(M, K, &a.crowsA, &a.cstripsA, &a.ctilesA);
   ctiles(K, N, &a.crowsB, &a.cstripsB, &a.ctilesB);
-  void* args[] = {&a, &bar};
+  void* args[] = {&a};
   return cudaLaunchCooperativeKernel((const void*)k_scale_coop, dim3((unsigned)nblocks), dim3(CT), args,
                                      kCoopSmem, st);
 }

@@ -18,11 +18,15 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "fmm_internal.h"
 #include "gemm_f64_dev.cuh"
 #include "lincomb_dev.cuh"
 
 namespace fmm {
+
+namespace cg = cooperative_groups;
 
 namespace {
 
@@ -48,18 +52,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-__device__ __forceinline__ void small_barrier(unsigned int* bar, unsigned int nblocks, unsigned int& gen) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    ++gen;
-    __threadfence();
-    const unsigned int target = gen * nblocks;
-    atomicAdd(bar, 1u);
-    while (*(volatile unsigned int*)bar < target) __nanosleep(32);
-    __threadfence();
-  }
-  __syncthreads();
-}
 
 // One 32 x 64 tile of M = S T (m x k by k x n), full k, the PIPE mainloop of k2_gemm_f64.
 template <bool VEC>
@@ -158,12 +150,13 @@ __device__ __forceinline__ void leaf_tile(double* As, double* Bs, const double* 
 }
 
 template <int RA, int RB, bool VEC>
-__global__ void __launch_bounds__(kSmallThreads, 3) k_small_plan(SmallArgs a, unsigned int* bar) {
+__global__ void __launch_bounds__(kSmallThreads, 3) k_small_plan(SmallArgs a) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double* optr[2][kMaxX2];
   constexpr int V = VEC ? 2 : 1;
   const unsigned int nb = gridDim.x;
-  unsigned int gen = 0;
+  // grid-wide barrier of the cooperative launch (orders global memory and invalidates L1)
+  cg::grid_group grid = cg::this_grid();
   // phases 1 and 3 are few, long items (a row position of a two-level pass): warps are striped
   // across the blocks first so the items spread over every SM
   const int64_t gt = ((int64_t)(threadIdx.x >> 5) * nb + blockIdx.x) * 32 + (threadIdx.x & 31);
@@ -191,7 +184,7 @@ __global__ void __launch_bounds__(kSmallThreads, 3) k_small_plan(SmallArgs a, un
     }
   }
   if (a.trace && threadIdx.x == 0) atomicMax(&a.trace[1], gtimer());
-  small_barrier(bar, nb, gen);
+  grid.sync();
   if (a.trace && gt == 0) a.trace[2] = gtimer();
   // ---- phase 2: every leaf product M = S T, 32 x 64 tiles ----------------------------------
   {
@@ -210,7 +203,7 @@ __global__ void __launch_bounds__(kSmallThreads, 3) k_small_plan(SmallArgs a, un
     }
   }
   if (a.trace && threadIdx.x == 0) atomicMax(&a.trace[3], gtimer());
-  small_barrier(bar, nb, gen);
+  grid.sync();
   if (a.trace && gt == 0) a.trace[4] = gtimer();
   // ---- phase 3: the W-combination of levels 1 and 0 (K3X2) ---------------------------------
   for (int q = 0; q < a.nk3; ++q) {
@@ -238,7 +231,7 @@ __global__ void __launch_bounds__(kSmallThreads, 3) k_small_plan(SmallArgs a, un
 }
 
 template <int RA, int RB, bool VEC>
-cudaError_t go_small(const SmallArgs& a, unsigned int* bar, cudaStream_t st) {
+cudaError_t go_small(const SmallArgs& a, cudaStream_t st) {
   constexpr int smem = SCfg::SMEM_BYTES;
   auto kern = k_small_plan<RA, RB, VEC>;
   static int blocks = -1;
@@ -254,8 +247,7 @@ cudaError_t go_small(const SmallArgs& a, unsigned int* bar, cudaStream_t st) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, kSmallThreads, smem);
     blocks = sms * std::max(1, std::min(per, 3));
   }
-  cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned int), st);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
   SmallArgs args = a;
   static unsigned long long* trace = nullptr;
   static const bool tracing = getenv("FMM_SMALL_TRACE") != nullptr;
@@ -264,7 +256,7 @@ cudaError_t go_small(const SmallArgs& a, unsigned int* bar, cudaStream_t st) {
     cudaMemsetAsync(trace, 0, 8 * sizeof(unsigned long long), st);
     args.trace = trace;
   }
-  void* p[] = {&args, &bar};
+  void* p[] = {&args};
   e = cudaLaunchCooperativeKernel((const void*)kern, dim3((unsigned)blocks), dim3(kSmallThreads), p,
                                   smem, st);
   if (tracing && e == cudaSuccess) {
@@ -285,13 +277,13 @@ int small_tile_n() { return SCfg::BN; }
 
 cudaError_t launch_small_plan(int pair, const K1x2Node* k1, int nk1, const LeafNode* lf, int nlf,
                               int64_t m, int64_t n, int64_t k, const K3x2Node* k3, int nk3,
-                              const Bases& b, bool vec, unsigned int* bar, cudaStream_t st) {
+                              const Bases& b, bool vec, cudaStream_t st) {
   SmallArgs a{};
   a.k1 = k1; a.nk1 = nk1; a.lf = lf; a.nlf = nlf; a.m = m; a.n = n; a.k = k;
   a.tiles_m = (int)((m + SCfg::BM - 1) / SCfg::BM);
   a.tiles_n = (int)((n + SCfg::BN - 1) / SCfg::BN);
   a.k3 = k3; a.nk3 = nk3; a.b = b;
-#define FMM_SMALL(RA, RB) return vec ? go_small<RA, RB, true>(a, bar, st) : go_small<RA, RB, false>(a, bar, st)
+#define FMM_SMALL(RA, RB) return vec ? go_small<RA, RB, true>(a, st) : go_small<RA, RB, false>(a, st)
   switch (pair - 1) {
     case 0: FMM_SMALL(0, 0);
     case 1: FMM_SMALL(0, 1);
