@@ -202,7 +202,7 @@ template <typename C, bool VEC, bool FLAT>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
     k2f_gemm_f64(const FusedNode* __restrict__ nodes, const double* __restrict__ coef_all,
                  Bases bases, int64_t m, int64_t n, int64_t k, int tiles_m, int tiles_n, int P,
-                 int Q, int R, int count, int chunk, int* __restrict__ turn) {
+                 int Q, int R, int count, int chunk, int* __restrict__ turn, int n_tickets) {
   static_assert(C::PIPE, "the fused kernel uses the PIPE mainloop");
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
@@ -218,25 +218,36 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   __shared__ int r_s[CAPR];
   __shared__ double wcf[CAPW];
 
-  // Product chain split (chunk < nr; `turn` non-null): the work item -- (group, parent, tile),
-  // group-major -- comes from a ticket taken with atomicAdd when the CTA starts, not from
-  // blockIdx, so tickets follow the actual dispatch order.  Group g runs products
-  // [g*chunk, (g+1)*chunk) of its unit after group g-1 released the unit's turnstile (so every
-  // C_k element still sees ascending r); group g-1 of the unit holds an earlier ticket, i.e. it
-  // is already running, so the wait always ends (no assumption on CTA dispatch order).
-  // turn[0 .. count*tiles) are the turnstiles, turn[count*tiles] the ticket counter (zeroed by
-  // the launcher).
+  // Product chain split (chunk < nr; `turn` non-null): persistent CTAs take work items --
+  // (group, parent, tile), group-major -- as tickets from an atomic counter, the next ticket
+  // requested while the current item runs (its round trip hidden), not from blockIdx.  Group g
+  // runs products [g*chunk, (g+1)*chunk) of its unit after group g-1 released the unit's
+  // turnstile (so every C_k element still sees ascending r).  Group g-1 of the unit holds an
+  // earlier ticket; a CTA finishes its current item before the one it prefetched, so the
+  // smallest unfinished ticket always progresses: no deadlock, whatever the CTA dispatch order
+  // or residency.  turn[0 .. count*tiles) are the turnstiles, turn[count*tiles] the ticket
+  // counter (zeroed by the launcher).  Without a split, one CTA per (tile, parent) of the grid.
   const int tid = threadIdx.x;
   const int tiles = tiles_m * tiles_n;
   __shared__ int s_ticket;
+  int tk_next = 0;
+  if (turn && tid == 0) tk_next = atomicAdd(turn + (int64_t)count * tiles, 1);
+  for (int iter = 0;; ++iter) {
   int parent = blockIdx.y, grp = 0, tile = blockIdx.x;
   if (turn) {
-    if (tid == 0) s_ticket = atomicAdd(turn + (int64_t)count * tiles, 1);
+    __syncthreads();  // the previous item is done with the product tables
+    if (tid == 0) {
+      s_ticket = tk_next;
+      tk_next = atomicAdd(turn + (int64_t)count * tiles, 1);  // in flight during this item
+    }
     __syncthreads();
     const int tk = s_ticket, per_grp = count * tiles;
+    if (tk >= n_tickets) break;
     grp = tk / per_grp;
     parent = (tk % per_grp) / tiles;
     tile = tk % tiles;
+  } else if (iter > 0) {
+    break;
   }
   const FusedNode& nd = nodes[parent];
   const int nr_all = nd.nr;
@@ -472,6 +483,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     }
   }
   cp_wait<0>();
+  }  // work items
 }
 
 template <typename C, bool VEC>
@@ -486,12 +498,25 @@ cudaError_t launch_fused_kernel(const FusedNode* dev_nodes, int count, int64_t m
     cudaError_t e = cudaMemsetAsync(turn, 0, sizeof(int) * ((size_t)count * tiles_m * tiles_n + 1), st);
     if (e != cudaSuccess) return e;
   }
-  dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)(count * groups));
+  const int n_tickets = tiles_m * tiles_n * count * groups;
   auto go = [&](auto kern) {
     cudaError_t e = set_smem(kern, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)(count * groups));
+    if (groups > 1) {  // persistent: at most one wave of resident CTAs takes the tickets
+      static int resident = 0;
+      if (!resident) {
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, C::THREADS, C::SMEM_BYTES);
+        resident = sms * std::max(per, 1);
+      }
+      grid = dim3((unsigned)std::min(n_tickets, resident), 1);
+    }
     kern<<<grid, C::THREADS, C::SMEM_BYTES, st>>>(dev_nodes, coef, b, m, n, k, tiles_m, tiles_n, P,
-                                                  Q, R, count, chunk, groups > 1 ? turn : nullptr);
+                                                  Q, R, count, chunk, groups > 1 ? turn : nullptr,
+                                                  n_tickets);
     return cudaGetLastError();
   };
   if (KT >= C::STAGES) return go(k2f_gemm_f64<C, VEC, false>);
