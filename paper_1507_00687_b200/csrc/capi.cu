@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <queue>
 #include <string>
 #include <vector>
 
@@ -456,40 +457,58 @@ struct Builder {
   // simulated efficiency to >= 93 % (measured: profiles/r01_fusion_variants.md).
 
   // Simulated makespan (in product durations) of the fused grid when each unit's R-product
-  // chain is split into groups of `chunk` products, dispatched group-major onto kSMs SMs in
-  // order (one CTA per SM), each item costing its products plus a pipeline fill of
+  // chain is split into consecutive groups of products, dispatched group-major onto kSMs
+  // slots as they free up (the tickets), each item costing its products plus a pipeline fill of
   // STAGES / KT products; group g of a unit cannot finish before group g-1 of that unit.
-  static double fused_makespan(int64_t units, int R, int chunk, int KT, int kSMs) {
-    const int groups = (R + chunk - 1) / chunk;
+  // `ends` = the groups' product ends (ascending, the last = R).
+  static double fused_makespan(int64_t units, const std::vector<int>& ends, int KT, int kSMs) {
     const double fill = 4.0 / std::max(KT, 1);
-    std::vector<double> sm(kSMs, 0.0), prev(units, 0.0);
+    std::priority_queue<double, std::vector<double>, std::greater<double>> sm;
+    for (int i = 0; i < kSMs; ++i) sm.push(0.0);
+    std::vector<double> prev(units, 0.0);
     double span = 0;
-    for (int g = 0; g < groups; ++g) {
-      const int np = std::min(R, (g + 1) * chunk) - g * chunk;
+    for (size_t g = 0; g < ends.size(); ++g) {
+      const int np = ends[g] - (g ? ends[g - 1] : 0);
       for (int64_t u = 0; u < units; ++u) {
-        auto it = std::min_element(sm.begin(), sm.end());
-        const double start = *it;
+        const double start = sm.top();
+        sm.pop();
         const double fin = std::max(start + np + fill, g ? prev[u] + 0.1 : 0.0);
-        *it = fin;
+        sm.push(fin);
         prev[u] = fin;
         span = std::max(span, fin);
       }
     }
     return span;
   }
-  // best chain split for a fused leaf level (chunk = R: no split); efficiency out
-  static int best_chunk(int64_t units, int R, int KT, int slots, double* eff) {
-    int best = R;
-    double best_span = fused_makespan(units, R, R, KT, slots);
-    if (KT >= 4 && units <= (1 << 16)) {
-      for (int groups = 2; groups <= 3; ++groups) {
-        const int c = (R + groups - 1) / groups;
-        const double sp = fused_makespan(units, R, c, KT, slots);
+  static uint32_t pack_split(const std::vector<int>& ends) {
+    if (ends.size() <= 1) return 0u;
+    uint32_t s = 0;
+    for (size_t g = 0; g < ends.size(); ++g) s |= (uint32_t)ends[g] << (8 * g);
+    return s;
+  }
+  // best chain split for a fused leaf level (0: none) among 2 and 3 groups (any cut points for
+  // R <= 8, else near-equal groups); the simulated efficiency out
+  static uint32_t best_split(int64_t units, int R, int KT, int slots, double* eff) {
+    std::vector<int> best{R};
+    double best_span = fused_makespan(units, best, KT, slots);
+    if (KT >= 4 && units <= (1 << 16) && R <= 255) {
+      std::vector<std::vector<int>> cand;
+      if (R <= 8) {
+        for (int a = 1; a < R; ++a) {
+          cand.push_back({a, R});
+          for (int b2 = a + 1; b2 < R; ++b2) cand.push_back({a, b2, R});
+        }
+      } else {
+        cand.push_back({(R + 1) / 2, R});
+        cand.push_back({(R + 2) / 3, 2 * ((R + 2) / 3), R});
+      }
+      for (const auto& c : cand) {
+        const double sp = fused_makespan(units, c, KT, slots);
         if (sp < best_span * 0.995) { best_span = sp; best = c; }
       }
     }
     if (eff) *eff = (double)units * R / ((double)slots * best_span);
-    return best;
+    return pack_split(best);
   }
 
   // K2F tile configuration for this plan's leaves: the 64 x 64 tile kernel (v13, 3 CTAs per
@@ -520,7 +539,7 @@ struct Builder {
       const int slots = k2f_slots();
       double eff = 0;
       if (p->split_chains && KT >= 4 && nparents * tiles >= slots && nparents * tiles * R >= 4 * slots) {
-        best_chunk(nparents * tiles, R, KT, slots, &eff);
+        best_split(nparents * tiles, R, KT, slots, &eff);
         if (eff >= 0.93) return true;
       }
     }
@@ -589,10 +608,11 @@ struct Builder {
     if (p->split_chains && fz.size() > 0 && fz[0].nr == r0.R && (st.inner + 15) / 16 >= 4) {
       const int ts = k2f_tile();
       const int64_t tiles = ((st.rows + ts - 1) / ts) * ((st.cols + ts - 1) / ts);
-      const int c = best_chunk((int64_t)st.count * tiles, r0.R, (int)((st.inner + 15) / 16),
+      uint32_t sp = best_split((int64_t)st.count * tiles, r0.R, (int)((st.inner + 15) / 16),
                                k2f_slots(), nullptr);
-      if (c < r0.R) {
-        st.chunk = c;
+      if (const char* e = getenv("FMM_K2F_SPLIT")) sp = (uint32_t)strtoul(e, nullptr, 0);  // tuning
+      if (split_groups(sp, r0.R) > 1) {
+        st.split = sp;
         st.turn_off = ws_alloc((st.count * tiles + 2) / 2);  // count*tiles + 1 ints, in 8-byte elements
       }
     }
@@ -1061,7 +1081,7 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
       }
       return launch_gemm_f64_fused(
           (const FusedNode*)nd, s.count, s.rows, s.cols, s.inner, p->dev_coef, s.P, s.Q, s.R, b, vec,
-          st, s.nr, s.chunk,
+          st, s.nr, s.split,
           s.turn_off >= 0 ? (int*)((double*)b.p[BASE_WS] + s.turn_off) + c0 * tiles_f : nullptr,
           s.k2f_cfg);
     case STEP_K2:
@@ -1107,6 +1127,8 @@ static fmm_status run_steps(const fmm_plan* p, const Bases& b, bool vec, cudaStr
     int64_t maxn = kMaxNodes;
     if (s.kind == STEP_K2F && s.chunk > 0 && s.nr > s.chunk)  // grid.y = groups x nodes
       maxn = std::min<int64_t>(maxn, 65535 / ((s.nr + s.chunk - 1) / s.chunk));
+    if (s.kind == STEP_K2F && s.split)
+      maxn = std::min<int64_t>(maxn, 65535 / std::max(1, split_groups(s.split, s.nr)));
     for (int64_t c0 = 0; c0 < s.count && e == cudaSuccess; c0 += maxn) {
       Step sub = s;
       sub.count = (int)std::min<int64_t>(maxn, s.count - c0);

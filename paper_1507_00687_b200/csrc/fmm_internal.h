@@ -213,9 +213,10 @@ struct Step {
   int nr = 0;        // K2F: products per node (uniform)
   int64_t dev_off2 = -1;  // K2F FP32: LeafNode list (parent-major) for the hi / lo split
   int k2f_cfg = 16;  // K2F tile configuration (16: 128 x 128 / 1 CTA per SM, 13: 64 x 64 / 3)
-  int chunk = 0;     // K2F: products per CTA when a unit's chain is split (0: whole chain);
-                     // turnstiles (one int per unit) + a ticket counter at ws offset turn_off
-                     // (in elements of the plan's dtype)
+  int chunk = 0;     // K2F FP32: products per CTA when a unit's chain is split (0: whole chain)
+  uint32_t split = 0;  // K2F FP64: chain split, byte g = end of group g's products (0: none);
+                     // both: turnstiles (one int per unit) + a ticket counter at ws offset
+                     // turn_off (in elements of the plan's dtype)
   int64_t turn_off = -1;
   int x2 = 0;        // K1 / K3: 0 one level (K1Node / K3Node); else K1x2Node / K3x2Node with
                      // rule pair (x2 - 1) / 3, (x2 - 1) % 3 (builtin_tables.h ids)
@@ -260,8 +261,10 @@ cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, in
                             int64_t k, const Bases& b, bool vec, cudaStream_t st);
 cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                   int64_t k, const double* dev_coef, int P, int Q, int R,
-                                  const Bases& b, bool vec, cudaStream_t st, int nr, int chunk,
+                                  const Bases& b, bool vec, cudaStream_t st, int nr, uint32_t split,
                                   int* turn, int cfg);
+// groups (1..4) of a K2F chain split for chains of nr products; -1 when malformed
+int split_groups(uint32_t split, int nr);
 // output tile edge (BM = BN) of K2F tile configuration cfg (13: 64, 16: 128)
 int k2f_tile_of(int cfg);
 // The single-launch small plan (K1X2 -> leaf products -> K3X2 in one cooperative kernel); its

@@ -202,7 +202,7 @@ template <typename C, bool VEC, bool FLAT>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
     k2f_gemm_f64(const FusedNode* __restrict__ nodes, const double* __restrict__ coef_all,
                  Bases bases, int64_t m, int64_t n, int64_t k, int tiles_m, int tiles_n, int P,
-                 int Q, int R, int count, int chunk, int* __restrict__ turn, int n_tickets) {
+                 int Q, int R, int count, uint32_t split, int* __restrict__ turn, int n_tickets) {
   static_assert(C::PIPE, "the fused kernel uses the PIPE mainloop");
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
@@ -218,11 +218,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   __shared__ int r_s[CAPR];
   __shared__ double wcf[CAPW];
 
-  // Product chain split (chunk < nr; `turn` non-null): persistent CTAs take work items --
-  // (group, parent, tile), group-major -- as tickets from an atomic counter, the next ticket
-  // requested while the current item runs (its round trip hidden), not from blockIdx.  Group g
-  // runs products [g*chunk, (g+1)*chunk) of its unit after group g-1 released the unit's
-  // turnstile (so every C_k element still sees ascending r).  Group g-1 of the unit holds an
+  // Product chain split (`turn` non-null; byte g of `split` = end of group g's products):
+  // persistent CTAs take work items -- (group, parent, tile), group-major -- as tickets from an
+  // atomic counter, the next ticket requested while the current item runs (its round trip
+  // hidden), not from blockIdx.  Group g runs products [end(g-1), end(g)) of its unit after
+  // group g-1 released the unit's turnstile (so every C_k element still sees ascending r).  Group g-1 of the unit holds an
   // earlier ticket; a CTA finishes its current item before the one it prefetched, so the
   // smallest unfinished ticket always progresses: no deadlock, whatever the CTA dispatch order
   // or residency.  turn[0 .. count*tiles) are the turnstiles, turn[count*tiles] the ticket
@@ -251,8 +251,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   }
   const FusedNode& nd = nodes[parent];
   const int nr_all = nd.nr;
-  const int r_begin = grp * chunk;
-  const int nr = min(nr_all, r_begin + chunk) - r_begin;  // products of this CTA
+  const int r_begin = grp ? (int)((split >> (8 * (grp - 1))) & 0xffu) : 0;
+  const int nr = (turn ? (int)((split >> (8 * grp)) & 0xffu) : nr_all) - r_begin;  // this CTA's
   if (tid < nr) {
     const int q = r_begin + tid;
     int64_t l;
@@ -326,6 +326,36 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     __syncthreads();
     if (tid == 0) atomicExch(my_turn, grp + 1);
   };
+  // first contribution: c = w*m (plain store); later ones: c = c + w*m as L2 reductions
+  // (RED.ADD.F64, round to nearest) with no load round trip.  Only this thread updates these
+  // elements, and same-address operations of one thread are applied in program order, so the
+  // per-element sequence is K3's.
+  auto store_block = [&](double* ob, int64_t ldo, bool first, auto&& wmul) {
+#pragma unroll
+    for (int i = 0; i < C::MI; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t row = m0 + wm * C::WTM + i * 16 + g + h * 8;
+        if (row >= m) continue;
+#pragma unroll
+        for (int j = 0; j < C::NI; ++j) {
+          const int64_t col = n0 + wn * C::WTN + j * 8 + 2 * t;
+          double* cp = ob + row * ldo + col;
+          const double v0 = wmul(acc[i][j][2 * h]), v1 = wmul(acc[i][j][2 * h + 1]);
+          if (first) {
+            if (VEC && col + 1 < n) {
+              *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
+            } else {
+              if (col < n) cp[0] = v0;
+              if (col + 1 < n) cp[1] = v1;
+            }
+          } else {
+            if (col < n) red_add(cp, v0);
+            if (col + 1 < n) red_add(cp + 1, v1);
+          }
+        }
+      }
+  };
   auto epilogue = [&](int ri) {
     const uint32_t wmask = wm_s[ri], fmask = fm_s[ri];
     const int r = r_s[ri];
@@ -336,34 +366,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       const double w = wcf[kk * R + r];
       const bool first = (fmask >> kk) & 1u;
       double* ob = out + (int64_t)(kk / Q) * m * ldo + (int64_t)(kk % Q) * n;
-      // first contribution: c = w*m (plain store); later ones: c = c + w*m as L2 reductions
-      // (RED.ADD.F64, round to nearest) with no load round trip.  Only this thread updates
-      // these elements, and same-address operations of one thread are applied in program
-      // order, so the per-element sequence is K3's.
-#pragma unroll
-      for (int i = 0; i < C::MI; ++i)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int64_t row = m0 + wm * C::WTM + i * 16 + g + h * 8;
-          if (row >= m) continue;
-#pragma unroll
-          for (int j = 0; j < C::NI; ++j) {
-            const int64_t col = n0 + wn * C::WTN + j * 8 + 2 * t;
-            double* cp = ob + row * ldo + col;
-            const double v0 = __dmul_rn(w, acc[i][j][2 * h]), v1 = __dmul_rn(w, acc[i][j][2 * h + 1]);
-            if (first) {
-              if (VEC && col + 1 < n) {
-                *reinterpret_cast<double2*>(cp) = make_double2(v0, v1);
-              } else {
-                if (col < n) cp[0] = v0;
-                if (col + 1 < n) cp[1] = v1;
-              }
-            } else {
-              if (col < n) red_add(cp, v0);
-              if (col + 1 < n) red_add(cp + 1, v1);
-            }
-          }
-        }
+      if (fabs(w) == 1.0)  // w*m is exact: a sign flip on the integer pipe, off the FP64 pipe
+        store_block(ob, ldo, first, [&](double x) {
+          return __longlong_as_double(__double_as_longlong(x) ^ (w < 0 ? INT64_MIN : 0));
+        });
+      else
+        store_block(ob, ldo, first, [&](double x) { return __dmul_rn(w, x); });
     }
   };
 
@@ -489,11 +497,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
 template <typename C, bool VEC>
 cudaError_t launch_fused_kernel(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                 int64_t k, const double* coef, int P, int Q, int R,
-                                const Bases& b, cudaStream_t st, int nr, int chunk, int* turn) {
+                                const Bases& b, cudaStream_t st, int nr, uint32_t split, int* turn) {
   const int tiles_m = (int)((m + C::BM - 1) / C::BM), tiles_n = (int)((n + C::BN - 1) / C::BN);
   const int KT = (int)std::max<int64_t>(1, (k + C::BK - 1) / C::BK);
-  if (chunk <= 0 || chunk >= nr || KT < C::STAGES || !turn) chunk = nr;  // no split
-  const int groups = (nr + chunk - 1) / chunk;
+  int groups = split_groups(split, nr);
+  if (groups <= 0) return cudaErrorInvalidValue;
+  if (KT < C::STAGES || !turn) groups = 1;  // no split
   if (groups > 1) {  // turnstiles + the ticket counter
     cudaError_t e = cudaMemsetAsync(turn, 0, sizeof(int) * ((size_t)count * tiles_m * tiles_n + 1), st);
     if (e != cudaSuccess) return e;
@@ -515,7 +524,7 @@ cudaError_t launch_fused_kernel(const FusedNode* dev_nodes, int count, int64_t m
       grid = dim3((unsigned)std::min(n_tickets, resident), 1);
     }
     kern<<<grid, C::THREADS, C::SMEM_BYTES, st>>>(dev_nodes, coef, b, m, n, k, tiles_m, tiles_n, P,
-                                                  Q, R, count, chunk, groups > 1 ? turn : nullptr,
+                                                  Q, R, count, split, groups > 1 ? turn : nullptr,
                                                   n_tickets);
     return cudaGetLastError();
   };
@@ -546,6 +555,20 @@ using V16 = Cfg<128, 128, 16, 4, 2, 4, 1, true>;
 
 }  // namespace
 
+// Groups of a chain split `split` (byte g = end of group g's products, ascending, the last one
+// = nr; 0 = no split) for chains of nr products: 1..4, or -1 when malformed.
+int split_groups(uint32_t split, int nr) {
+  if (split == 0) return 1;
+  int prev = 0;
+  for (int g = 0; g < 4; ++g) {
+    const int e = (int)((split >> (8 * g)) & 0xffu);
+    if (e <= prev || e > nr) return -1;
+    if (e == nr) return (g + 1 < 4 && (split >> (8 * (g + 1))) != 0u) ? -1 : g + 1;
+    prev = e;
+  }
+  return -1;
+}
+
 int k2f_tile_of(int cfg) { return cfg == 13 ? V13::BM : V16::BM; }
 
 cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
@@ -561,15 +584,15 @@ cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, in
 
 cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                   int64_t k, const double* dev_coef, int P, int Q, int R,
-                                  const Bases& b, bool vec, cudaStream_t st, int nr, int chunk,
+                                  const Bases& b, bool vec, cudaStream_t st, int nr, uint32_t split,
                                   int* turn, int cfg) {
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
   if (cfg == 13 && (R > 8 || P * Q > 4)) return cudaErrorInvalidValue;  // v13's tables: 2x2, R <= 8
   if (cfg == 13)
-    return vec ? launch_fused_kernel<V13, true>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, chunk, turn)
-               : launch_fused_kernel<V13, false>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, chunk, turn);
-  return vec ? launch_fused_kernel<V16, true>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, chunk, turn)
-             : launch_fused_kernel<V16, false>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, chunk, turn);
+    return vec ? launch_fused_kernel<V13, true>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, split, turn)
+               : launch_fused_kernel<V13, false>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, split, turn);
+  return vec ? launch_fused_kernel<V16, true>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, split, turn)
+             : launch_fused_kernel<V16, false>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, split, turn);
 }
 
 }  // namespace fmm

@@ -166,8 +166,8 @@ def test_shard_depth_virtual_ranks(fb, depth, nranks):
     assert oracle.parity_metric(total, ref, np.abs(A).max(), np.abs(B).max(), 256) <= TOL64
 
 
-@pytest.mark.parametrize("dims,names", [((2048, 2048, 2048), ("winograd",) * 3),   # chunks 4 + 3
-                                        ((3072, 3072, 3072), ("winograd",) * 2)])  # chunks 3 + 3 + 1
+@pytest.mark.parametrize("dims,names", [((2048, 2048, 2048), ("winograd",) * 3),
+                                        ((3072, 3072, 3072), ("winograd",) * 2)])
 def test_split_chains_equal_unfused(fb, dims, names):
     # units whose R-product chain is split over 2-3 CTAs ordered by per-unit turnstiles (the
     # split is chosen by the plan's makespan model): bitwise the unfused K2 + K3, deterministic
@@ -175,6 +175,21 @@ def test_split_chains_equal_unfused(fb, dims, names):
     A, B = fi.random_pair(M, K, N, seed=K // 64)
     pa = plan(fb, names, M, K, N, "on")
     assert pa.fused_launches() == 1
+    Cf = exe(pa, A, B)
+    assert np.array_equal(Cf, exe(plan(fb, names, M, K, N, "off"), A, B))
+    assert np.array_equal(Cf, exe(pa, A, B))
+
+
+@pytest.mark.parametrize("split", [0x0706, 0x0701, 0x070301, 0x070502, 0x07060504])
+def test_forced_split_equal_unfused(fb, monkeypatch, split):
+    # non-uniform chain splits (byte g = end of group g's products, FMM_K2F_SPLIT tuning knob):
+    # every grouping keeps each C element's ascending-r sum, so bitwise the unfused K2 + K3
+    M = K = N = 1024
+    names = ("strassen",) * 3
+    A, B = fi.random_pair(M, K, N, seed=split % 97)
+    monkeypatch.setenv("FMM_K2F_SPLIT", str(split))
+    pa = plan(fb, names, M, K, N, "on")
+    assert pa.fused_launches() == 1  # compiles the plan with the forced split
     Cf = exe(pa, A, B)
     assert np.array_equal(Cf, exe(plan(fb, names, M, K, N, "off"), A, B))
     assert np.array_equal(Cf, exe(pa, A, B))
