@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 
@@ -178,6 +179,7 @@ struct CoopArgs {
   // (256-column strips x row chunks), per matrix
   int64_t rrowsA, rrowsB, crowsA, crowsB;
   int rsegsA, rsegsB, rtilesA, rtilesB, cstripsA, cstripsB, ctilesA, ctilesB;
+  unsigned long long* trace;  // FMM_SCALE_TRACE: %globaltimer after every grid barrier
 };
 
 // x 2^e, correctly rounded (one multiplication by an exact power of two when it is a normal
@@ -572,6 +574,12 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
                  : "=r"(done) : "r"(s_u32(bar)), "r"(parity) : "memory");
   } while (!done);
 }
+// stage the tile's row exponents (rows [r0, r1)) in shared memory, the caller having synchronised
+// the block before (nobody reads the previous tile's exponents any more)
+__device__ __forceinline__ void stage_er_nosync(const MatPass& q, int64_t r0, int64_t r1, int32_t* sh) {
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += CT) sh[r - r0] = q.er ? q.er[r] : 0;
+  __syncthreads();
+}
 // stage the tile's row exponents (rows [r0, r1)) in shared memory
 __device__ __forceinline__ void stage_er(const MatPass& q, int64_t r0, int64_t r1, int32_t* sh) {
   __syncthreads();
@@ -589,7 +597,16 @@ __device__ __noinline__ void row_tile_tma(const MatPass& q, int tile, int* flags
   const int64_t cs = (int64_t)seg * RSEG;  // segment start column
   const int64_t len = min((int64_t)RSEG, q.cols - cs);
   const int64_t lim = len - 2 * lane;
-  if (!RAW) stage_er(q, r0, r1, sm.er);
+  double* buf = sm.stage + (size_t)warp * CS * CSTG;
+  uint64_t* bar = sm.bar + warp * CS;
+  const int64_t rw = r0 + warp;
+  const int n = rw < r1 ? (int)((r1 - rw + 7) / 8) : 0;
+  const uint32_t bytes = (uint32_t)(len * 8);
+  // the ring's first stages are requested before the exponent loads, so their latencies overlap
+  __syncthreads();  // every warp is done with the previous tile's ring and exponents
+  if (lane == 0)
+    for (int k = 0; k < CS && k < n; ++k) bulk_g2s(buf + k * CSTG, q.src + (rw + 8 * k) * q.lds + cs, bytes, bar + k);
+  if (!RAW) stage_er_nosync(q, r0, r1, sm.er);
   bool bad = false;
   double fc[16];
 #pragma unroll
@@ -597,15 +614,8 @@ __device__ __noinline__ void row_tile_tma(const MatPass& q, int tile, int* flags
     const int o = (e / 2) * 64 + (e & 1);
     fc[e] = (!RAW && o < lim) ? pow2_of(q.ec[cs + 2 * lane + o], &bad) : 1.0;
   }
-  double* buf = sm.stage + (size_t)warp * CS * CSTG;
-  uint64_t* bar = sm.bar + warp * CS;
   __syncwarp();
   uint32_t ph = sm.phase[warp];
-  const int64_t rw = r0 + warp;
-  const int n = rw < r1 ? (int)((r1 - rw + 7) / 8) : 0;
-  const uint32_t bytes = (uint32_t)(len * 8);
-  if (lane == 0)
-    for (int k = 0; k < CS && k < n; ++k) bulk_g2s(buf + k * CSTG, q.src + (rw + 8 * k) * q.lds + cs, bytes, bar + k);
   for (int k = 0; k < n; ++k) {
     const int st = k % CS;
     const int64_t r = rw + 8 * k;
@@ -657,19 +667,8 @@ __device__ __noinline__ void col_tile_tma(const MatPass& q, int tile, int* flags
   const int64_t cs = (int64_t)strip * 256;
   const int64_t len = min((int64_t)256, q.cols - cs);
   const int64_t lim = len - 2 * lane;
-  if (!RAW) stage_er(q, r0, r1, sm.er);
-  bool bad = false;
-  double cmx[8], cthr[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int o = (e / 2) * 64 + (e & 1);
-    cmx[e] = 0.0;
-    cthr[e] = (!RAW && o < lim) ? under_thr(q.ec[cs + 2 * lane + o]) : kDblMin;
-  }
   double* buf = sm.stage + (size_t)warp * CS * CSTG;
   uint64_t* bar = sm.bar + warp * CS;
-  __syncwarp();
-  uint32_t ph = sm.phase[warp];
   const int64_t rw = r0 + warp;  // this warp's rows: rw + 8 j; a stage holds rows j, j + 1 of them
   const int nr = rw < r1 ? (int)((r1 - rw + 7) / 8) : 0;
   const int n = (nr + 1) / 2;
@@ -681,8 +680,21 @@ __device__ __noinline__ void col_tile_tma(const MatPass& q, int tile, int* flags
     bulk_g2s_tx(buf + st * CSTG, q.src + ra * q.lds + cs, bytes, bar + st);
     if (rb < r1) bulk_g2s_tx(buf + st * CSTG + 256, q.src + rb * q.lds + cs, bytes, bar + st);
   };
+  // the ring's first stages are requested before the exponent loads, so their latencies overlap
+  __syncthreads();  // every warp is done with the previous tile's ring and exponents
   if (lane == 0)
     for (int k = 0; k < CS && k < n; ++k) issue(k, k);
+  if (!RAW) stage_er_nosync(q, r0, r1, sm.er);
+  bool bad = false;
+  double cmx[8], cthr[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int o = (e / 2) * 64 + (e & 1);
+    cmx[e] = 0.0;
+    cthr[e] = (!RAW && o < lim) ? under_thr(q.ec[cs + 2 * lane + o]) : kDblMin;
+  }
+  __syncwarp();
+  uint32_t ph = sm.phase[warp];
   for (int k = 0; k < n; ++k) {
     const int st = k % CS;
     bar_wait(bar + st, (ph >> st) & 1u);
@@ -764,6 +776,20 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
   // grid-wide barrier of the cooperative launch (orders global memory and invalidates L1, so
   // the factors / exponents / maxima written before it are what every block reads after it)
   cg::grid_group grid = cg::this_grid();
+  int nmark = 0;
+  auto gsync = [&]() {
+    grid.sync();
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && nmark < 63) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      a.trace[++nmark] = t;
+    }
+  };
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    a.trace[0] = t;
+  }
   int* flags = a.flags;
   const int64_t M = a.M, K = a.K, N = a.N;
   const int64_t gtid = (int64_t)blockIdx.x * CT + threadIdx.x, gstride = (int64_t)nb * CT;
@@ -774,7 +800,7 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
   for (int64_t i = gtid; i < M + 2 * K + N; i += gstride) { a.mx[0][i] = 0.0; a.mx[1][i] = 0.0; }
   if (gtid == 0) flags[F_MODE] = a.pow2 ? 0 : 1;
   if (gtid < 8) flags[F_EXT + gtid] = (gtid & 1) ? (-0x7fffffff - 1) : 0x7fffffff;
-  grid.sync();
+  gsync();
 
   auto views = [&](int isO, int kind, double* m) {  // (A part, B part) of a pass
     MatPass pa{}, pb{};
@@ -857,7 +883,7 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
     set_max(pp.first, pp.second, isO, a.mx[0]);
     run_pass(PK_RAW, pp.first, pp.second);
   }
-  grid.sync();
+  gsync();
   int t0 = -1;
   for (int t = 0; t < a.nsteps; ++t) {
     const int isO = (t % 2 == 0) == (a.first_O != 0);
@@ -928,7 +954,7 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
     if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) atomicAdd(fail, 1);
     if (__any_sync(0xffffffffu, badf) && (threadIdx.x & 31) == 0 && flags[F_MODE] == 0)
       atomicExch(&flags[F_BAD], 1);
-    grid.sync();
+    gsync();
     if (gtid == 0) flags[F_STEPS] += 1;
     const bool done = (test && *(volatile int*)fail == 0) || t == a.nsteps - 1;
     const bool need_next = !done;  // the values after this step feed another step
@@ -940,29 +966,29 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
       if (need_next) set_max(pp.first, pp.second, !isO, nxt);
       run_pass(PK_MAT, pp.first, pp.second);
       if (gtid == 0) { flags[F_MODE] = 1; flags[F_STORED] = 1; }
-      grid.sync();
+      gsync();
     } else if (*(volatile int*)&flags[F_MODE] == 0) {
       if (need_next) {  // virtual: the next step's reductions of the values after this step
         auto pp = views(!isO, PK_VIRTUAL, nxt);
         set_max(pp.first, pp.second, !isO, nxt);
         run_pass(PK_VIRTUAL, pp.first, pp.second);
-        grid.sync();
+        gsync();
         if (*(volatile int*)&flags[F_BAD]) {  // inexact intermediates: redo, materialised
           for (int64_t i = gtid; i < set; i += gstride) nxt[i] = 0.0;
-          grid.sync();
+          gsync();
           auto pm = views(isO, PK_MAT, nxt);
           set_factors(pm.first, pm.second, isO);
           set_max(pm.first, pm.second, !isO, nxt);
           run_pass(PK_MAT, pm.first, pm.second);
           if (gtid == 0) { flags[F_MODE] = 1; flags[F_STORED] = 1; }
-          grid.sync();
+          gsync();
         }
       } else if (a.materialise_end) {  // the caller needs A', B' in memory
         auto pp = views(isO, PK_MAT, nxt);
         set_factors(pp.first, pp.second, isO);
         run_pass(PK_MAT, pp.first, pp.second);
         if (gtid == 0) { flags[F_MODE] = 1; flags[F_STORED] = 1; }
-        grid.sync();
+        gsync();
       }
     } else {  // materialised: apply in place (from A, B at the first application)
       auto pp = views(isO, PK_MAT, nxt);
@@ -970,7 +996,7 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
       if (need_next) set_max(pp.first, pp.second, !isO, nxt);
       run_pass(PK_MAT, pp.first, pp.second);
       if (gtid == 0) flags[F_STORED] = 1;
-      grid.sync();
+      gsync();
     }
     if (done) {
       if (gtid == 0 && t < a.nsteps - 1) flags[F_DONE] = 1;
@@ -1066,9 +1092,26 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
   rtiles(K, N, &a.rrowsB, &a.rsegsB, &a.rtilesB);
   ctiles(M, K, &a.crowsA, &a.cstripsA, &a.ctilesA);
   ctiles(K, N, &a.crowsB, &a.cstripsB, &a.ctilesB);
+  static unsigned long long* trace = nullptr;
+  static const bool tracing = getenv("FMM_SCALE_TRACE") != nullptr;
+  a.trace = nullptr;
+  if (tracing) {  // barrier timing (development; synchronises)
+    if (!trace) cudaMalloc(&trace, 64 * sizeof(unsigned long long));
+    cudaMemsetAsync(trace, 0, 64 * sizeof(unsigned long long), st);
+    a.trace = trace;
+  }
   void* args[] = {&a};
-  return cudaLaunchCooperativeKernel((const void*)k_scale_coop, dim3((unsigned)nblocks), dim3(CT), args,
-                                     kCoopSmem, st);
+  e = cudaLaunchCooperativeKernel((const void*)k_scale_coop, dim3((unsigned)nblocks), dim3(CT), args,
+                                  kCoopSmem, st);
+  if (tracing && e == cudaSuccess) {
+    unsigned long long h[64];
+    cudaMemcpyAsync(h, trace, sizeof h, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    fprintf(stderr, "[scale] barriers (us from start):");
+    for (int i = 1; i < 64 && h[i]; ++i) fprintf(stderr, " %.1f", (h[i] - h[0]) * 1e-3);
+    fprintf(stderr, "\n");
+  }
+  return e;
 }
 
 // Exponent vectors and mode flag of the virtual form (for the plan's root K1).
