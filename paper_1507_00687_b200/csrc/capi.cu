@@ -605,6 +605,15 @@ struct Builder {
     }
     // chain split with per-unit turnstiles (breadth-first levels: every parent has all R products)
     st.k2f_cfg = k2f_cfg();
+    st.unitw = true;
+    for (const Node& nd : parents) {
+      const RuleData& ru = rule_at(l, nd.idx);
+      for (int kk = 0; kk < ru.m0 * ru.n0; ++kk)
+        for (int r = 0; r < ru.R; ++r) {
+          const double w = ru.coef(ru.W, kk, r);
+          if (w != 0.0 && w != 1.0 && w != -1.0) st.unitw = false;
+        }
+    }
     if (p->split_chains && fz.size() > 0 && fz[0].nr == r0.R && (st.inner + 15) / 16 >= 4) {
       const int ts = k2f_tile();
       const int64_t tiles = ((st.rows + ts - 1) / ts) * ((st.cols + ts - 1) / ts);
@@ -1083,7 +1092,7 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
           (const FusedNode*)nd, s.count, s.rows, s.cols, s.inner, p->dev_coef, s.P, s.Q, s.R, b, vec,
           st, s.nr, s.split,
           s.turn_off >= 0 ? (int*)((double*)b.p[BASE_WS] + s.turn_off) + c0 * tiles_f : nullptr,
-          s.k2f_cfg);
+          s.k2f_cfg, s.unitw);
     case STEP_K2:
       if (p->dtype == FMM_F64)
         return launch_gemm_f64((const LeafNode*)nd, s.count, s.rows, s.cols, s.inner, b, vec, st);

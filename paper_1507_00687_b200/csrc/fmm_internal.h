@@ -212,6 +212,7 @@ struct Step {
   bool vec_ok;       // all ws offsets / dims allow 16-byte vectors (caller bases checked later)
   int nr = 0;        // K2F: products per node (uniform)
   int64_t dev_off2 = -1;  // K2F FP32: LeafNode list (parent-major) for the hi / lo split
+  bool unitw = false;  // K2F: every W coefficient of the level is 0 or +-1 (sign-flip epilogue)
   int k2f_cfg = 16;  // K2F tile configuration (16: 128 x 128 / 1 CTA per SM, 13: 64 x 64 / 3)
   int chunk = 0;     // K2F FP32: products per CTA when a unit's chain is split (0: whole chain)
   uint32_t split = 0;  // K2F FP64: chain split, byte g = end of group g's products (0: none);
@@ -262,7 +263,7 @@ cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, in
 cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                   int64_t k, const double* dev_coef, int P, int Q, int R,
                                   const Bases& b, bool vec, cudaStream_t st, int nr, uint32_t split,
-                                  int* turn, int cfg);
+                                  int* turn, int cfg, bool unitw);
 // groups (1..4) of a K2F chain split for chains of nr products; -1 when malformed
 int split_groups(uint32_t split, int nr);
 // output tile edge (BM = BN) of K2F tile configuration cfg (13: 64, 16: 128)

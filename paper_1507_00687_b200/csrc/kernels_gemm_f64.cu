@@ -16,7 +16,6 @@
 // sequential order, covered by the parity tolerance.
 #include <algorithm>
 #include <cstdint>
-#include <cstdlib>
 
 #include "fmm_internal.h"
 #include "gemm_f64_dev.cuh"
@@ -198,11 +197,11 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
 //   c = w*m (first contribution)  |  c = c + w*m        (both rounded to nearest, no FMA)
 // exactly K3's sequence (k3_combine / k_acc), with M_r never written to memory.
 
-template <typename C, bool VEC, bool FLAT>
+template <typename C, bool VEC, bool FLAT, bool UNITW>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
     k2f_gemm_f64(const FusedNode* __restrict__ nodes, const double* __restrict__ coef_all,
                  Bases bases, int64_t m, int64_t n, int64_t k, int tiles_m, int tiles_n, int P,
-                 int Q, int R, int count, uint32_t split, int* __restrict__ turn, int n_tickets) {
+                 int Q, int R, int count, uint32_t split, int* __restrict__ turn) {
   static_assert(C::PIPE, "the fused kernel uses the PIPE mainloop");
   extern __shared__ __align__(16) double smem[];
   double* As = smem;
@@ -218,36 +217,26 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   __shared__ int r_s[CAPR];
   __shared__ double wcf[CAPW];
 
-  // Product chain split (`turn` non-null; byte g of `split` = end of group g's products):
-  // persistent CTAs take work items -- (group, parent, tile), group-major -- as tickets from an
-  // atomic counter, the next ticket requested while the current item runs (its round trip
-  // hidden), not from blockIdx.  Group g runs products [end(g-1), end(g)) of its unit after
-  // group g-1 released the unit's turnstile (so every C_k element still sees ascending r).  Group g-1 of the unit holds an
-  // earlier ticket; a CTA finishes its current item before the one it prefetched, so the
-  // smallest unfinished ticket always progresses: no deadlock, whatever the CTA dispatch order
-  // or residency.  turn[0 .. count*tiles) are the turnstiles, turn[count*tiles] the ticket
-  // counter (zeroed by the launcher).  Without a split, one CTA per (tile, parent) of the grid.
+  // Product chain split (`turn` non-null; byte g of `split` = end of group g's products): the
+  // work item -- (group, parent, tile), group-major -- comes from a ticket taken with atomicAdd
+  // when the CTA starts, not from blockIdx, so tickets follow the actual dispatch order.  Group
+  // g runs products [end(g-1), end(g)) of its unit after group g-1 released the unit's
+  // turnstile (so every C_k element still sees ascending r); group g-1 of the unit holds an
+  // earlier ticket, i.e. its CTA is already running, so the wait always ends (no assumption on
+  // the CTA dispatch order).  turn[0 .. count*tiles) are the turnstiles, turn[count*tiles] the
+  // ticket counter (zeroed by the launcher).  A persistent form (CTAs looping over tickets, the
+  // next one prefetched) measured slower at C2, C4 and C5 and was dropped.
   const int tid = threadIdx.x;
   const int tiles = tiles_m * tiles_n;
   __shared__ int s_ticket;
-  int tk_next = 0;
-  if (turn && tid == 0) tk_next = atomicAdd(turn + (int64_t)count * tiles, 1);
-  for (int iter = 0;; ++iter) {
   int parent = blockIdx.y, grp = 0, tile = blockIdx.x;
   if (turn) {
-    __syncthreads();  // the previous item is done with the product tables
-    if (tid == 0) {
-      s_ticket = tk_next;
-      tk_next = atomicAdd(turn + (int64_t)count * tiles, 1);  // in flight during this item
-    }
+    if (tid == 0) s_ticket = atomicAdd(turn + (int64_t)count * tiles, 1);
     __syncthreads();
     const int tk = s_ticket, per_grp = count * tiles;
-    if (tk >= n_tickets) break;
     grp = tk / per_grp;
     parent = (tk % per_grp) / tiles;
     tile = tk % tiles;
-  } else if (iter > 0) {
-    break;
   }
   const FusedNode& nd = nodes[parent];
   const int nr_all = nd.nr;
@@ -366,7 +355,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       const double w = wcf[kk * R + r];
       const bool first = (fmask >> kk) & 1u;
       double* ob = out + (int64_t)(kk / Q) * m * ldo + (int64_t)(kk % Q) * n;
-      if (fabs(w) == 1.0)  // w*m is exact: a sign flip on the integer pipe, off the FP64 pipe
+      if constexpr (UNITW)  // every w is +-1: w*m is exact, a sign flip on the integer pipe
         store_block(ob, ldo, first, [&](double x) {
           return __longlong_as_double(__double_as_longlong(x) ^ (w < 0 ? INT64_MIN : 0));
         });
@@ -491,13 +480,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     }
   }
   cp_wait<0>();
-  }  // work items
 }
 
 template <typename C, bool VEC>
 cudaError_t launch_fused_kernel(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                 int64_t k, const double* coef, int P, int Q, int R,
-                                const Bases& b, cudaStream_t st, int nr, uint32_t split, int* turn) {
+                                const Bases& b, cudaStream_t st, int nr, uint32_t split, int* turn,
+                                bool unitw) {
   const int tiles_m = (int)((m + C::BM - 1) / C::BM), tiles_n = (int)((n + C::BN - 1) / C::BN);
   const int KT = (int)std::max<int64_t>(1, (k + C::BK - 1) / C::BK);
   int groups = split_groups(split, nr);
@@ -507,29 +496,17 @@ cudaError_t launch_fused_kernel(const FusedNode* dev_nodes, int count, int64_t m
     cudaError_t e = cudaMemsetAsync(turn, 0, sizeof(int) * ((size_t)count * tiles_m * tiles_n + 1), st);
     if (e != cudaSuccess) return e;
   }
-  const int n_tickets = tiles_m * tiles_n * count * groups;
   auto go = [&](auto kern) {
     cudaError_t e = set_smem(kern, C::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)(count * groups));
-    if (groups > 1) {  // persistent: at most one wave of resident CTAs takes the tickets
-      static int resident = 0;
-      if (!resident) {
-        int dev = 0, sms = 0, per = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, C::THREADS, C::SMEM_BYTES);
-        resident = sms * std::max(per, 1);
-      }
-      grid = dim3((unsigned)std::min(n_tickets, resident), 1);
-    }
+    const dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)(count * groups));
     kern<<<grid, C::THREADS, C::SMEM_BYTES, st>>>(dev_nodes, coef, b, m, n, k, tiles_m, tiles_n, P,
-                                                  Q, R, count, split, groups > 1 ? turn : nullptr,
-                                                  n_tickets);
+                                                  Q, R, count, split, groups > 1 ? turn : nullptr);
     return cudaGetLastError();
   };
-  if (KT >= C::STAGES) return go(k2f_gemm_f64<C, VEC, false>);
-  return go(k2f_gemm_f64<C, VEC, true>);
+  if (KT >= C::STAGES)
+    return unitw ? go(k2f_gemm_f64<C, VEC, false, true>) : go(k2f_gemm_f64<C, VEC, false, false>);
+  return unitw ? go(k2f_gemm_f64<C, VEC, true, true>) : go(k2f_gemm_f64<C, VEC, true, false>);
 }
 
 template <typename C>
@@ -585,14 +562,16 @@ cudaError_t launch_gemm_f64(const LeafNode* dev_leaves, int count, int64_t m, in
 cudaError_t launch_gemm_f64_fused(const FusedNode* dev_nodes, int count, int64_t m, int64_t n,
                                   int64_t k, const double* dev_coef, int P, int Q, int R,
                                   const Bases& b, bool vec, cudaStream_t st, int nr, uint32_t split,
-                                  int* turn, int cfg) {
+                                  int* turn, int cfg, bool unitw) {
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
   if (cfg == 13 && (R > 8 || P * Q > 4)) return cudaErrorInvalidValue;  // v13's tables: 2x2, R <= 8
   if (cfg == 13)
-    return vec ? launch_fused_kernel<V13, true>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, split, turn)
-               : launch_fused_kernel<V13, false>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, split, turn);
-  return vec ? launch_fused_kernel<V16, true>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, split, turn)
-             : launch_fused_kernel<V16, false>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, split, turn);
+    return vec ? launch_fused_kernel<V13, true>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, split, turn, unitw)
+               : launch_fused_kernel<V13, false>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, split, turn, unitw);
+  // the 128 x 128 kernel keeps the DMUL epilogue: its leaves are long (the epilogue is rare)
+  // and the sign-flip variant's main loop schedules worse at 255 registers (C5 +0.9 %)
+  return vec ? launch_fused_kernel<V16, true>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, split, turn, false)
+             : launch_fused_kernel<V16, false>(dev_nodes, count, m, n, k, dev_coef, P, Q, R, b, st, nr, split, turn, false);
 }
 
 }  // namespace fmm
