@@ -527,10 +527,11 @@ struct Builder {
   }
 
   bool fuse_leaves(int64_t nparents) const {
-    const bool tc32 = p->dtype == FMM_F32 && p->leaf != FMM_LEAF_NATIVE;  // tcgen05 FP32 leaves
-    if ((p->dtype != FMM_F64 && !tc32) || p->fusion == 0) return false;
+    // FP64 only: the FP32 tensor-core leaves keep their products in TMEM chunk buffers and
+    // register totals (k2p_tf32) and are combined by K3 (a fused FP32 epilogue,
+    // k2f_tf32, measured slower at C5 in round 1 -- 310 vs 287 ms -- and was removed in round 2)
+    if (p->dtype != FMM_F64 || p->fusion == 0) return false;
     if (p->fusion == 1) return true;
-    if (tc32) return false;  // k2f_tf32 measured slower than k2_tf32 + K3 at C5 (310 vs 287 ms): opt-in
     {  // chain splitting (turnstiles) smooths the wave quantisation of R-product units
       const int ts = k2f_tile();
       const int64_t tiles = ((p->lm[p->L] + ts - 1) / ts) * ((p->ln[p->L] + ts - 1) / ts);
@@ -589,20 +590,6 @@ struct Builder {
     st.P = r0.m0; st.Q = r0.n0; st.R = r0.R;
     st.nr = fz[0].nr;
     st.arena_off = -1;
-    if (p->dtype == FMM_F32) {  // tensor-core FP32 leaves: split list (parent-major) + hi/lo arena
-      std::vector<LeafNode> sl;
-      for (const FusedNode& f : fz)
-        for (int i = 0; i < f.nr; ++i) sl.push_back(LeafNode{f.a[i], f.b[i], Op{}});
-      st.dev_off2 = push(sl);
-      st.arena_off = ws_alloc((int64_t)tf32_arena_floats((int64_t)sl.size(), st.rows, st.cols, st.inner));
-      if (p->split_chains && st.nr > 1) {  // one product per CTA, in product-major order
-        st.chunk = 1;
-        const int64_t tiles = ((st.rows + 127) / 128) * ((st.cols + 255) / 256);
-        st.turn_off = ws_alloc(st.count * tiles + 1);  // ints (in 4-byte elements)
-      }
-      p->steps.push_back(st);
-      return;
-    }
     // chain split with per-unit turnstiles (breadth-first levels: every parent has all R products)
     st.k2f_cfg = k2f_cfg();
     st.unitw = true;
@@ -1066,8 +1053,7 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
   }
   const void* nd = (const uint8_t*)p->dev_desc + s.dev_off + c0 * node_bytes;
   const int ts = k2f_tile_of(s.k2f_cfg);
-  const int64_t tiles_f = p->dtype == FMM_F32 ? ((s.rows + 127) / 128) * ((s.cols + 255) / 256)
-                                              : ((s.rows + ts - 1) / ts) * ((s.cols + ts - 1) / ts);
+  const int64_t tiles_f = ((s.rows + ts - 1) / ts) * ((s.cols + ts - 1) / ts);
   switch (s.kind) {
     case STEP_SMALL: {
       const uint8_t* d = (const uint8_t*)p->dev_desc;
@@ -1080,14 +1066,6 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
     case STEP_ACC: return launch_acc<T>(s, nd, p->dev_coef, b, vec, st);
     case STEP_ZERO: return launch_zero<T>(s, nd, b, st);
     case STEP_K2F:
-      if (p->dtype == FMM_F32) {
-        int* turn = s.turn_off >= 0 ? (int*)((float*)b.p[BASE_WS] + s.turn_off) + c0 * tiles_f : nullptr;
-        return launch_gemm_tf32_fused(
-            (const FusedNode*)nd,
-            (const LeafNode*)((const uint8_t*)p->dev_desc + s.dev_off2) + c0 * s.nr, s.count, s.nr,
-            s.rows, s.cols, s.inner, p->dev_coef, s.P, s.Q, s.R, b, p->leaf == FMM_LEAF_TF32 ? 1 : 3,
-            (float*)b.p[BASE_WS] + s.arena_off, st, s.chunk, turn);
-      }
       return launch_gemm_f64_fused(
           (const FusedNode*)nd, s.count, s.rows, s.cols, s.inner, p->dev_coef, s.P, s.Q, s.R, b, vec,
           st, s.nr, s.split,

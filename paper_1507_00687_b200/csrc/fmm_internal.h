@@ -275,12 +275,6 @@ cudaError_t launch_small_plan(int pair, const K1x2Node* k1, int nk1, const LeafN
                               const Bases& b, bool vec, cudaStream_t st);
 int small_tile_m();
 int small_tile_n();
-// K2F for the FP32 tensor-core leaves (3xTF32 / TF32 on tcgen05, TMEM double-buffered)
-cudaError_t launch_gemm_tf32_fused(const FusedNode* dev_nodes, const LeafNode* dev_split_leaves,
-                                   int count, int nr, int64_t m, int64_t n, int64_t k,
-                                   const double* dev_coef, int P, int Q, int R, const Bases& b,
-                                   int passes, float* arena, cudaStream_t st, int chunk = 0,
-                                   int* turn = nullptr);
 cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, const LeafNode* host_leaves, int count,
                             int64_t m, int64_t n, int64_t k, const Bases& b, bool vec, int leaf,
                             float* arena, cudaStream_t st);

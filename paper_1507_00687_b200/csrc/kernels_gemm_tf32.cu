@@ -7,19 +7,23 @@
 // FP32 parity tolerance at C5; 3xTF32 passes with a wide margin.
 //
 // Two kernels per leaf batch:
-//   k_split_tf32  S (m x k) -> S_hi, S_lo (m x kp, K-major);  T (k x n) -> T_hi^T, T_lo^T
+//   k_split_*     S (m x k) -> S_hi, S_lo (m x kp, K-major);  T (k x n) -> T_hi^T, T_lo^T
 //                 (n x kp, K-major, transposed through shared memory), kp = k rounded up to 32
 //                 with zero padding -- into a per-launch arena in the workspace;
-//   k2_tf32       one CTA per 128 x 256 output tile: warp 0 = TMA producer (3-D tensor maps
-//                 over the whole arena, 128-byte swizzle), warp 1 = MMA issuer (one thread,
-//                 tcgen05.mma.cta_group::1.kind::tf32, M = 128, N = 256, K = 8 per instruction),
-//                 warp 2 = TMEM allocator, warps 4-7 = epilogue (tcgen05.ld 32x32b -> registers
-//                 -> global).  2-stage smem ring with full / empty mbarriers; tcgen05.commit
-//                 releases a stage and finally signals the epilogue.
+//   k2p_tf32      persistent (one CTA per SM, static round-robin over (leaf, 128 x 256 tile)
+//                 items): warp 0 = TMA producer (3-D tensor maps over the arena, 128-byte
+//                 swizzle), warp 1 = MMA issuer (one thread, tcgen05.mma.cta_group::1.kind::tf32,
+//                 M = 128, N = 256, K = 8), warp 2 = TMEM owner, 8 epilogue warps.  The K range is
+//                 accumulated in chunks (default 128): the tensor core's FP32 adds truncate, so
+//                 each chunk's TMEM accumulator is drained into register totals with
+//                 round-to-nearest adds while the next chunk runs in the other TMEM buffer
+//                 (round 1 accumulated all of K in TMEM: 22x the FP32 oracle's
+//                 error against double-double at C5, now below it).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
 #include <mutex>
 
@@ -128,210 +132,67 @@ struct TCfg {
   static_assert(SMEM <= 227 * 1024, "smem");
 };
 
-template <int BK, int STAGES>
-__global__ void __launch_bounds__(256, 1)
-    k2_tf32(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
-            const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
-            const LeafNode* __restrict__ leaves, Bases bases, int64_t m, int64_t n, int64_t kp,
-            int tiles_n, int passes) {
-  using CF = TCfg<BK, STAGES>;
-  constexpr int TSTAGES = STAGES, TBK = BK, A_BYTES = CF::A_B, B_BYTES = CF::B_B,
-                STAGE_BYTES = CF::STAGE;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* bars = (uint64_t*)(smem + TSTAGES * STAGE_BYTES);
-  // bars[0..S) full, [S..2S) empty, [2S] tmem_full; then the TMEM base address
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * TSTAGES + 1);
+// EW epilogue warps: EW / 4 per TMEM lane quadrant, each owning ECOLS = 1024 / EW columns
+template <int EW>
+struct EpiCfg {
+  static constexpr int THREADS = 32 * (4 + EW), ECOLS = 1024 / EW;
+  static_assert(EW == 8 || EW == 16, "epilogue warps");
+};
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int leaf = blockIdx.y;
-  const int tm = blockIdx.x / tiles_n, tn = blockIdx.x % tiles_n;
-  const int m0 = tm * TBM, n0 = tn * TBN;
-  const int KT = (int)(kp / TBK);
-
-  if (warp == 0 && lane == 0) {
-    for (int s = 0; s < TSTAGES; ++s) {
-      mbar_init(su32(&bars[s]), 1);
-      mbar_init(su32(&bars[TSTAGES + s]), 1);
-    }
-    mbar_init(su32(&bars[2 * TSTAGES]), 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                     su32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // ---- TMA producer ----
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % TSTAGES;
-        const uint32_t ph = (uint32_t)(kt / TSTAGES) & 1u;
-        mbar_wait(su32(&bars[TSTAGES + s]), ph ^ 1u);
-        uint8_t* st = smem + s * STAGE_BYTES;
-        const uint32_t full = su32(&bars[s]);
-        const int kc = kt * TBK;
-        if (passes == 3) {
-          mbar_expect_tx(full, STAGE_BYTES);
-          tma_load_3d(su32(st), &ta_hi, kc, m0, leaf, full);
-          tma_load_3d(su32(st + A_BYTES), &ta_lo, kc, m0, leaf, full);
-          tma_load_3d(su32(st + 2 * A_BYTES), &tb_hi, kc, n0, leaf, full);
-          tma_load_3d(su32(st + 2 * A_BYTES + B_BYTES), &tb_lo, kc, n0, leaf, full);
-        } else {
-          mbar_expect_tx(full, A_BYTES + B_BYTES);
-          tma_load_3d(su32(st), &ta_hi, kc, m0, leaf, full);
-          tma_load_3d(su32(st + 2 * A_BYTES), &tb_hi, kc, n0, leaf, full);
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      // ---- MMA issuer (single thread) ----
-      for (int kt = 0; kt < KT; ++kt) {
-        const int s = kt % TSTAGES;
-        const uint32_t ph = (uint32_t)(kt / TSTAGES) & 1u;
-        mbar_wait(su32(&bars[s]), ph);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        uint8_t* st = smem + s * STAGE_BYTES;
-        const uint64_t a_hi = desc_k<BK>(su32(st)), a_lo = desc_k<BK>(su32(st + A_BYTES));
-        const uint64_t b_hi = desc_k<BK>(su32(st + 2 * A_BYTES));
-        const uint64_t b_lo = desc_k<BK>(su32(st + 2 * A_BYTES + B_BYTES));
-#pragma unroll
-        for (int kk = 0; kk < TBK / 8; ++kk) {
-          const uint64_t off = (uint64_t)((kk * 32) >> 4);  // 8 tf32 = 32 bytes along K
-          const uint32_t first = (kt == 0 && kk == 0) ? 0u : 1u;
-          if (passes == 3) {
-            mma_tf32(tmem, a_lo + off, b_hi + off, first);
-            mma_tf32(tmem, a_hi + off, b_lo + off, 1u);
-            mma_tf32(tmem, a_hi + off, b_hi + off, 1u);
-          } else {
-            mma_tf32(tmem, a_hi + off, b_hi + off, first);
-          }
-        }
-        mma_commit(su32(&bars[TSTAGES + s]));  // stage s free once these MMAs complete
-      }
-      mma_commit(su32(&bars[2 * TSTAGES]));    // accumulator complete
-    }
-  } else if (warp >= 4) {
-    // ---- epilogue: TMEM -> registers -> global ----
-    mbar_wait(su32(&bars[2 * TSTAGES]), 0u);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const LeafNode& lf = leaves[leaf];
-    int64_t ldc;
-    float* Cp = op_ptr<float>(bases, lf.c, ldc);
-    const int q = warp & 3;
-    const int64_t row = m0 + q * 32 + lane;
-#pragma unroll 1
-    for (int cb = 0; cb < TBN / 32; ++cb) {
-      uint32_t v[32];
-      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(cb * 32);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-          "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-            "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-            "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-            "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-            "=r"(v[31])
-          : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-      if (KT == 0) {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] = 0u;  // empty inner dimension: C = 0
-      }
-      if (row < m) {
-        float* crow = Cp + row * ldc + n0 + cb * 32;
-        const int64_t cbase = n0 + cb * 32;
-        const bool vec = ((((uintptr_t)crow) & 15u) == 0) && (cbase + 32 <= n);
-        if (vec) {
-#pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            *reinterpret_cast<float4*>(crow + e) =
-                make_float4(__uint_as_float(v[e]), __uint_as_float(v[e + 1]),
-                            __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; ++e)
-            if (cbase + e < n) crow[e] = __uint_as_float(v[e]);
-        }
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  if (warp == 2)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                 "r"(TMEM_COLS));
+// Persistent leaf-product kernel with chunked round-to-nearest accumulation.  Work items are the
+// (leaf, 128 x 256 tile) pairs, leaf-major; CTA b runs items b, b + G, b + 2G, ... (G = grid =
+// min(items, SMs), one CTA per SM).  Roles: warp 0 lane 0 = TMA producer over the flattened
+// (item, k-tile) sequence through a STAGES-deep ring of hi / lo A and B stages; warp 1 lane 0 =
+// the MMA issuer; warp 2 = TMEM owner (512 columns: two 128 x 256 FP32 chunk accumulators);
+// warps 4 .. 4 + EW - 1 = epilogue.  The K range of an item is cut into chunks of chunk_kt k-tiles; the
+// tensor core accumulates one chunk into TMEM buffer (chunk# & 1) -- its FP32 adds truncate
+// -- and the epilogue drains that buffer into per-thread register totals with
+// round-to-nearest adds (tot = c_0, tot = tot + c_1, ...) while the MMAs of the next chunk run in
+// the other buffer.  So the truncation error grows only within a chunk, and both the drain and
+// an item's final stores overlap the next chunk's / item's MMAs.  Epilogue warp w owns TMEM lanes
+// 32 (w % 4) .. +31 (tile rows) and columns ECOLS ((w - 4) / 4) .. +ECOLS-1.
+// Item t -> (leaf, tile origin): leaf-major; inside a leaf, tiles run in groups of group_m tile
+// rows, column-major within a group, so the ~one wave of co-resident CTAs shares group_m A panels
+// and about SMs / group_m B panels (L2 reuse of the hi / lo operand panels).
+__device__ __forceinline__ void item_coords(int t, int tiles, int tiles_m, int tiles_n, int group_m,
+                                            int& leaf, int& m0, int& n0) {
+  leaf = t / tiles;
+  const int tt = t % tiles;
+  const int per_group = group_m * tiles_n;
+  const int g0 = (tt / per_group) * group_m;
+  const int gsz = min(tiles_m - g0, group_m);
+  const int w = tt % per_group;
+  m0 = (g0 + w % gsz) * TBM;
+  n0 = (w / gsz) * TBN;
 }
 
-// K2F for the FP32 tensor-core leaves: one CTA per (128 x 256 output tile, parent node) runs the
-// parent's nr leaf products in ascending r.  TMEM holds TWO 128 x 256 FP32 accumulators (512
-// columns): the single MMA-issuing thread writes product r into buffer r & 1 while warps 4-7
-// drain product r-1 from the other buffer and apply the parent's W-combination -- C_k = w*m for
-// the first contribution, else C_k = C_k + w*m (FP32, round to nearest, plain load / store by
-// the thread owning the row) -- K3's per-element sequence, bitwise, with M_r never written and
-// the epilogue overlapped with the next product's MMAs.  Barriers: full / empty per smem stage
-// (TMA <-> MMA, as in k2_tf32), acc_full / acc_empty per TMEM buffer (MMA <-> epilogue; the
-// epilogue's 128 threads arrive on acc_empty).  Operands: the per-launch hi / lo arena of
-// k_split_tf32 with leaf index parent * nr + r.
-template <int BK, int STAGES>
-__global__ void __launch_bounds__(256, 1)
-    k2f_tf32(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
+template <int BK, int STAGES, int EW>
+__global__ void __launch_bounds__(EpiCfg<EW>::THREADS, 1)
+    k2p_tf32(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
              const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
-             const FusedNode* __restrict__ nodes, const double* __restrict__ coef_all, Bases bases,
-             int64_t m, int64_t n, int64_t kp, int tiles_n, int passes, int P, int Q, int R,
-             int count, int chunk, int* __restrict__ turn) {
+             const LeafNode* __restrict__ leaves, Bases bases, int64_t m, int64_t n, int64_t kp,
+             int tiles_m, int tiles_n, int group_m, int total, int passes, int chunk_kt) {
   using CF = TCfg<BK, STAGES>;
-  constexpr int TSTAGES = STAGES, TBK = BK, A_BYTES = CF::A_B, B_BYTES = CF::B_B,
-                STAGE_BYTES = CF::STAGE;
+  constexpr int A_BYTES = CF::A_B, B_BYTES = CF::B_B, STAGE_BYTES = CF::STAGE;
+  const int tiles = tiles_m * tiles_n;
+  constexpr int ECOLS = EpiCfg<EW>::ECOLS, EPI_WARPS = EW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* bars = (uint64_t*)(smem + TSTAGES * STAGE_BYTES);
+  uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
   // bars: [0,S) full, [S,2S) empty, [2S,2S+2) acc_full, [2S+2,2S+4) acc_empty; then TMEM base
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * TSTAGES + 4);
-
+  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // chain split (chunk < nr; turnstiles and dispatch-order tickets as in k2f_gemm_f64: the work
-  // item (group, parent, tile), group-major, comes from an atomicAdd ticket taken at CTA start,
-  // so the group a CTA waits for has always started).  chunk = 1 keeps the unfused kernel's
-  // order (all CTAs of one product first: the L2 reuse of that leaf's panels) while the
-  // epilogue still applies the W-combination in place.
-  const int tiles = gridDim.x;
-  int parent = blockIdx.y, grp = 0, tile = blockIdx.x;
-  if (turn) {
-    __shared__ int s_ticket;
-    if (threadIdx.x == 0) s_ticket = atomicAdd(turn + (int64_t)count * tiles, 1);
-    __syncthreads();
-    const int tk = s_ticket, per_grp = count * tiles;
-    grp = tk / per_grp;
-    parent = (tk % per_grp) / tiles;
-    tile = tk % tiles;
-  }
-  const FusedNode& nd = nodes[parent];
-  const int r_begin = grp * chunk;
-  const int r_end = min(nd.nr, r_begin + chunk);
-  const int nr_all = nd.nr;
-  const int tm = tile / tiles_n, tn = tile % tiles_n;
-  const int m0 = tm * TBM, n0 = tn * TBN;
-  const int KT = (int)(kp / TBK);
+  const int KT = (int)(kp / BK);
+  const int nch = (KT + chunk_kt - 1) / chunk_kt;
 
   if (warp == 0 && lane == 0) {
-    for (int s2 = 0; s2 < TSTAGES; ++s2) {
-      mbar_init(su32(&bars[s2]), 1);
-      mbar_init(su32(&bars[TSTAGES + s2]), 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(su32(&bars[s]), 1);
+      mbar_init(su32(&bars[STAGES + s]), 1);
     }
     for (int b2 = 0; b2 < 2; ++b2) {
-      mbar_init(su32(&bars[2 * TSTAGES + b2]), 1);        // acc_full: one tcgen05.commit
-      mbar_init(su32(&bars[2 * TSTAGES + 2 + b2]), 128);  // acc_empty: the 128 epilogue threads
+      mbar_init(su32(&bars[2 * STAGES + b2]), 1);                  // acc_full: tcgen05.commit
+      mbar_init(su32(&bars[2 * STAGES + 2 + b2]), EPI_WARPS * 32);  // acc_empty: epilogue threads
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -347,17 +208,18 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer over all (product, k-tile) ----
+    if (lane == 0) {  // ---- TMA producer ----
       int it = 0;
-      for (int ri = r_begin; ri < r_end; ++ri) {
-        const int leaf = parent * nr_all + ri;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        int leaf, m0, n0;
+        item_coords(t, tiles, tiles_m, tiles_n, group_m, leaf, m0, n0);
         for (int kt = 0; kt < KT; ++kt, ++it) {
-          const int s2 = it % TSTAGES;
-          const uint32_t ph = (uint32_t)(it / TSTAGES) & 1u;
-          mbar_wait(su32(&bars[TSTAGES + s2]), ph ^ 1u);
-          uint8_t* st = smem + s2 * STAGE_BYTES;
-          const uint32_t full = su32(&bars[s2]);
-          const int kc = kt * TBK;
+          const int s = it % STAGES;
+          const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+          mbar_wait(su32(&bars[STAGES + s]), ph ^ 1u);
+          uint8_t* st = smem + s * STAGE_BYTES;
+          const uint32_t full = su32(&bars[s]);
+          const int kc = kt * BK;
           if (passes == 3) {
             mbar_expect_tx(full, STAGE_BYTES);
             tma_load_3d(su32(st), &ta_hi, kc, m0, leaf, full);
@@ -374,125 +236,95 @@ __global__ void __launch_bounds__(256, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer ----
-      int it = 0;
-      for (int ri = r_begin; ri < r_end; ++ri) {
-        const int j = ri - r_begin;
-        const int buf = j & 1;
-        if (j >= 2) {  // the epilogue has drained this buffer (product ri - 2)
-          mbar_wait(su32(&bars[2 * TSTAGES + 2 + buf]), (uint32_t)((j / 2 - 1) & 1));
+      int it = 0, g = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        for (int c = 0; c < nch; ++c, ++g) {
+          const int buf = g & 1;
+          mbar_wait(su32(&bars[2 * STAGES + 2 + buf]), (uint32_t)((g >> 1) & 1) ^ 1u);
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        }
-        const uint32_t acc = tmem + (uint32_t)(buf * TMEM_COLS);
-        for (int kt = 0; kt < KT; ++kt, ++it) {
-          const int s2 = it % TSTAGES;
-          const uint32_t ph = (uint32_t)(it / TSTAGES) & 1u;
-          mbar_wait(su32(&bars[s2]), ph);
-          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-          uint8_t* st = smem + s2 * STAGE_BYTES;
-          const uint64_t a_hi = desc_k<BK>(su32(st)), a_lo = desc_k<BK>(su32(st + A_BYTES));
-          const uint64_t b_hi = desc_k<BK>(su32(st + 2 * A_BYTES));
-          const uint64_t b_lo = desc_k<BK>(su32(st + 2 * A_BYTES + B_BYTES));
+          const uint32_t acc = tmem + (uint32_t)(buf * TMEM_COLS);
+          const int kt0 = c * chunk_kt, kt1 = min(KT, kt0 + chunk_kt);
+          for (int kt = kt0; kt < kt1; ++kt, ++it) {
+            const int s = it % STAGES;
+            mbar_wait(su32(&bars[s]), (uint32_t)(it / STAGES) & 1u);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            uint8_t* st = smem + s * STAGE_BYTES;
+            const uint64_t a_hi = desc_k<BK>(su32(st)), a_lo = desc_k<BK>(su32(st + A_BYTES));
+            const uint64_t b_hi = desc_k<BK>(su32(st + 2 * A_BYTES));
+            const uint64_t b_lo = desc_k<BK>(su32(st + 2 * A_BYTES + B_BYTES));
 #pragma unroll
-          for (int kk = 0; kk < TBK / 8; ++kk) {
-            const uint64_t off = (uint64_t)((kk * 32) >> 4);
-            const uint32_t first = (kt == 0 && kk == 0) ? 0u : 1u;
-            if (passes == 3) {
-              mma_tf32(acc, a_lo + off, b_hi + off, first);
-              mma_tf32(acc, a_hi + off, b_lo + off, 1u);
-              mma_tf32(acc, a_hi + off, b_hi + off, 1u);
-            } else {
-              mma_tf32(acc, a_hi + off, b_hi + off, first);
-            }
-          }
-          mma_commit(su32(&bars[TSTAGES + s2]));
-        }
-        mma_commit(su32(&bars[2 * TSTAGES + buf]));  // product ri complete in buffer buf
-      }
-    }
-  } else if (warp >= 4) {  // ---- epilogue: TMEM -> registers -> W-combination ----
-    const int q = warp & 3;
-    const int64_t row = m0 + q * 32 + lane;
-    int64_t ldo;
-    float* out = op_ptr<float>(bases, nd.out, ldo);
-    int* my_turn = turn ? turn + (int64_t)parent * tiles + tile : nullptr;
-    for (int ri = r_begin; ri < r_end; ++ri) {
-      const int j = ri - r_begin;
-      const int buf = j & 1;
-      mbar_wait(su32(&bars[2 * TSTAGES + buf]), (uint32_t)((j / 2) & 1));
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      if (j == 0 && grp > 0 && my_turn) {  // group grp-1 released this unit
-        if (threadIdx.x == 128) {
-          unsigned ns = 64;
-          while (atomicAdd(my_turn, 0) < grp) {  // grp-1 holds an earlier ticket: it is running
-            __nanosleep(ns);
-            if (ns < 2048) ns *= 2;
-          }
-          __threadfence();
-        }
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      }
-      const uint32_t wmask = nd.wmask[ri], fmask = nd.first[ri];
-      const int r = nd.rlist[ri];
-#pragma unroll 1
-      for (int cb = 0; cb < TBN / 32; ++cb) {
-        uint32_t v[32];
-        const uint32_t taddr =
-            tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * TMEM_COLS + cb * 32);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-            "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-              "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-              "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-              "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-              "=r"(v[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        if (KT == 0) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = 0u;
-        }
-        if (row >= m) continue;
-        const int64_t cbase = n0 + cb * 32;
-        for (int kk = 0; kk < P * Q; ++kk) {  // kk = ia*Q + jb (row-major C blocks)
-          if (!((wmask >> kk) & 1u)) continue;
-          const float w = (float)coef_all[nd.coef_off + kk * R + r];
-          const bool first = (fmask >> kk) & 1u;
-          float* crow = out + ((int64_t)(kk / Q) * m + row) * ldo + (int64_t)(kk % Q) * n + cbase;
-          const bool vec = ((((uintptr_t)crow) & 15u) == 0) && (cbase + 32 <= n);
-          if (vec) {
-#pragma unroll
-            for (int e = 0; e < 32; e += 4) {
-              float4 c4;
-              const float y0 = __fmul_rn(w, __uint_as_float(v[e])), y1 = __fmul_rn(w, __uint_as_float(v[e + 1]));
-              const float y2 = __fmul_rn(w, __uint_as_float(v[e + 2])), y3 = __fmul_rn(w, __uint_as_float(v[e + 3]));
-              if (first) {
-                c4 = make_float4(y0, y1, y2, y3);
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint64_t off = (uint64_t)((kk * 32) >> 4);  // 8 tf32 = 32 bytes along K
+              const uint32_t first = (kt == kt0 && kk == 0) ? 0u : 1u;
+              if (passes == 3) {  // small terms first
+                mma_tf32(acc, a_lo + off, b_hi + off, first);
+                mma_tf32(acc, a_hi + off, b_lo + off, 1u);
+                mma_tf32(acc, a_hi + off, b_hi + off, 1u);
               } else {
-                c4 = *reinterpret_cast<const float4*>(crow + e);
-                c4.x = __fadd_rn(c4.x, y0); c4.y = __fadd_rn(c4.y, y1);
-                c4.z = __fadd_rn(c4.z, y2); c4.w = __fadd_rn(c4.w, y3);
+                mma_tf32(acc, a_hi + off, b_hi + off, first);
               }
-              *reinterpret_cast<float4*>(crow + e) = c4;
             }
-          } else {
-            for (int e = 0; e < 32; ++e) {
-              if (cbase + e >= n) break;
-              const float y = __fmul_rn(w, __uint_as_float(v[e]));
-              crow[e] = first ? y : __fadd_rn(crow[e], y);
-            }
+            mma_commit(su32(&bars[STAGES + s]));  // stage s free once these MMAs complete
           }
+          mma_commit(su32(&bars[2 * STAGES + buf]));  // chunk complete in buffer buf
         }
       }
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&bars[2 * TSTAGES + 2 + buf]))
-                   : "memory");
     }
-    if (my_turn && r_end < nr_all) {  // hand the unit to group grp+1
-      __threadfence();
-      asm volatile("bar.sync 1, 128;\n" ::: "memory");
-      if (threadIdx.x == 128) atomicExch(my_turn, grp + 1);
+  } else if (warp >= 4) {  // ---- epilogue: chunk drains into RN register totals, then stores ----
+    const int q = warp & 3, h = (warp - 4) >> 2;
+    int g = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      int leaf, m0, n0;
+      item_coords(t, tiles, tiles_m, tiles_n, group_m, leaf, m0, n0);
+      float tot[ECOLS];
+#pragma unroll
+      for (int e = 0; e < ECOLS; ++e) tot[e] = 0.f;
+      for (int c = 0; c < nch; ++c, ++g) {
+        const int buf = g & 1;
+        mbar_wait(su32(&bars[2 * STAGES + buf]), (uint32_t)((g >> 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t tbase =
+            tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * TMEM_COLS + h * ECOLS);
+#pragma unroll
+        for (int cb = 0; cb < ECOLS / 16; ++cb) {  // x16 loads keep the totals in registers
+          uint32_t v[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+              "%13,%14,%15}, [%16];\n"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(tbase + (uint32_t)(cb * 16)));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          if (c == 0) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) tot[cb * 16 + e] = __uint_as_float(v[e]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) tot[cb * 16 + e] = __fadd_rn(tot[cb * 16 + e], __uint_as_float(v[e]));
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&bars[2 * STAGES + 2 + buf]))
+                     : "memory");
+      }
+      const int64_t row = m0 + q * 32 + lane;
+      if (row < m) {
+        const LeafNode& lf = leaves[leaf];
+        int64_t ldc;
+        float* Cp = op_ptr<float>(bases, lf.c, ldc);
+        const int64_t cbase = n0 + h * ECOLS;
+        float* crow = Cp + row * ldc + cbase;
+        if (((((uintptr_t)crow) & 15u) == 0) && (cbase + ECOLS <= n)) {
+#pragma unroll
+          for (int e = 0; e < ECOLS; e += 4)
+            *reinterpret_cast<float4*>(crow + e) = make_float4(tot[e], tot[e + 1], tot[e + 2], tot[e + 3]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < ECOLS; ++e)
+            if (cbase + e < n) crow[e] = tot[e];
+        }
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -667,11 +499,57 @@ bool make_map(CUtensorMap* map, float* base, int64_t kp, int64_t rows, int64_t l
   return r == CUDA_SUCCESS;
 }
 
+int num_sms() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 148;
+}
+
+template <int BK, int STAGES, int EW>
+cudaError_t launch_k2p(float* a_hi, float* a_lo, float* b_hi, float* b_lo, const LeafNode* dev_leaves,
+                       int count, int64_t m, int64_t n, int64_t kp, const Bases& b, int passes,
+                       int chunk_k, cudaStream_t st) {
+  using CF = TCfg<BK, STAGES>;
+  CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
+  const int64_t kpe = kp > 0 ? kp : TBK;
+  if (!make_map(&ma_hi, a_hi, kpe, m, count, TBM, BK) || !make_map(&ma_lo, a_lo, kpe, m, count, TBM, BK) ||
+      !make_map(&mb_hi, b_hi, kpe, n, count, TBN, BK) || !make_map(&mb_lo, b_lo, kpe, n, count, TBN, BK))
+    return cudaErrorInvalidValue;
+  const int tiles_m = (int)((m + TBM - 1) / TBM), tiles_n = (int)((n + TBN - 1) / TBN);
+  const int tiles = tiles_m * tiles_n;
+  const int64_t total = (int64_t)tiles * count;
+  if (total > INT32_MAX) return cudaErrorInvalidValue;
+  const int grid = (int)std::min<int64_t>(total, num_sms());
+  const int chunk_kt = std::max(1, chunk_k / BK);
+  cudaError_t e = cudaFuncSetAttribute(k2p_tf32<BK, STAGES, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
+  if (e != cudaSuccess) return e;
+  static const int group_m = [] {
+    const char* e = getenv("FMM_TF32_GROUP_M");  // tile rows per rasterisation group
+    const int v = e ? atoi(e) : 16;
+    return v >= 1 ? v : 16;
+  }();
+  k2p_tf32<BK, STAGES, EW><<<grid, EpiCfg<EW>::THREADS, CF::SMEM, st>>>(
+      ma_hi, ma_lo, mb_hi, mb_lo, dev_leaves, b, m, n, kp, tiles_m, tiles_n, group_m, (int)total, passes,
+      chunk_kt);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 size_t tf32_arena_floats(int64_t count, int64_t m, int64_t n, int64_t k) {
   const int64_t kp = (k + TBK - 1) / TBK * TBK;
   return (size_t)count * (size_t)(2 * m * kp + 2 * n * kp);
+}
+
+// Chunk length (k elements) of the round-to-nearest accumulation: FMM_TF32_CHUNK, default 128
+// (the truncating TMEM adds then span at most 128 products per element).
+int tf32_chunk_k() {
+  static const int ck = [] {
+    const char* e = getenv("FMM_TF32_CHUNK");
+    const int v = e ? atoi(e) : 128;
+    return v >= 16 ? v : 128;
+  }();
+  return ck;
 }
 
 cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
@@ -686,68 +564,20 @@ cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, i
   float* b_lo = b_hi + (size_t)count * n * kp;
   if (kp > 0) launch_split(dev_leaves, host_leaves, count, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, st);
   static const int cfg = [] {
-    const char* e = getenv("FMM_TF32_CFG");  // 0: BK 32 / 2 stages (default), 1: BK 16 / 4 stages
+    // 0: BK 32 / 2 stages (default), 1: BK 16 / 4 stages; +2: 16 epilogue warps instead of 8.
+    // Measured at C5 FP32 (sw_power_cap): cfg 0 255.9 ms at 1537 MHz, cfg 1 296.8 ms at 1372,
+    // cfg 3 312.7 ms at 1290 (its tensor pipe is busier per cycle, 84.9 vs 76.9 %, but the
+    // power cap takes it back in clock)
+    const char* e = getenv("FMM_TF32_CFG");
     return e ? atoi(e) : 0;
   }();
-  const int bk = cfg == 0 ? 32 : 16;
-  CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
-  const int64_t kpe = kp > 0 ? kp : TBK;
-  if (!make_map(&ma_hi, a_hi, kpe, m, count, TBM, bk) || !make_map(&ma_lo, a_lo, kpe, m, count, TBM, bk) ||
-      !make_map(&mb_hi, b_hi, kpe, n, count, TBN, bk) || !make_map(&mb_lo, b_lo, kpe, n, count, TBN, bk))
-    return cudaErrorInvalidValue;
-  const int tiles_m = (int)((m + TBM - 1) / TBM), tiles_n = (int)((n + TBN - 1) / TBN);
-  const dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)count);
-  cudaError_t e;
-  if (cfg == 0) {
-    using CF = TCfg<32, 2>;
-    e = cudaFuncSetAttribute(k2_tf32<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
-    if (e != cudaSuccess) return e;
-    k2_tf32<32, 2><<<grid, 256, CF::SMEM, st>>>(ma_hi, ma_lo, mb_hi, mb_lo, dev_leaves, b, m, n, kp,
-                                                 tiles_n, passes);
-  } else {
-    using CF = TCfg<16, 4>;
-    e = cudaFuncSetAttribute(k2_tf32<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
-    if (e != cudaSuccess) return e;
-    k2_tf32<16, 4><<<grid, 256, CF::SMEM, st>>>(ma_hi, ma_lo, mb_hi, mb_lo, dev_leaves, b, m, n, kp,
-                                                 tiles_n, passes);
+  const int ck = tf32_chunk_k();
+  switch (cfg) {
+    case 1: return launch_k2p<16, 4, 8>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st);
+    case 2: return launch_k2p<32, 2, 16>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st);
+    case 3: return launch_k2p<16, 4, 16>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st);
+    default: return launch_k2p<32, 2, 8>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st);
   }
-  return cudaGetLastError();
-}
-
-// Fused FP32 tensor-core leaves: split every (parent, product) leaf of the launch into the hi /
-// lo arena (leaf index parent * nr + r), then k2f_tf32.
-cudaError_t launch_gemm_tf32_fused(const FusedNode* dev_nodes, const LeafNode* dev_split_leaves,
-                                   int count, int nr, int64_t m, int64_t n, int64_t k,
-                                   const double* dev_coef, int P, int Q, int R, const Bases& b,
-                                   int passes, float* arena, cudaStream_t st, int chunk, int* turn) {
-  if (count == 0 || m == 0 || n == 0) return cudaSuccess;
-  if (!arena) return cudaErrorInvalidValue;
-  const int leaves = count * nr;
-  const int64_t kp = (k + TBK - 1) / TBK * TBK;
-  float* a_hi = arena;
-  float* a_lo = a_hi + (size_t)leaves * m * kp;
-  float* b_hi = a_lo + (size_t)leaves * m * kp;
-  float* b_lo = b_hi + (size_t)leaves * n * kp;
-  if (kp > 0) launch_split(dev_split_leaves, nullptr, leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, st);
-  CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
-  const int64_t kpe = kp > 0 ? kp : TBK;
-  if (!make_map(&ma_hi, a_hi, kpe, m, leaves, TBM, 32) || !make_map(&ma_lo, a_lo, kpe, m, leaves, TBM, 32) ||
-      !make_map(&mb_hi, b_hi, kpe, n, leaves, TBN, 32) || !make_map(&mb_lo, b_lo, kpe, n, leaves, TBN, 32))
-    return cudaErrorInvalidValue;
-  const int tiles_m = (int)((m + TBM - 1) / TBM), tiles_n = (int)((n + TBN - 1) / TBN);
-  using CF = TCfg<32, 2>;
-  cudaError_t e = cudaFuncSetAttribute(k2f_tf32<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
-  if (e != cudaSuccess) return e;
-  if (chunk <= 0 || chunk >= nr || !turn) chunk = nr;
-  const int groups = (nr + chunk - 1) / chunk;
-  if (groups > 1) {
-    e = cudaMemsetAsync(turn, 0, sizeof(int) * ((size_t)count * tiles_m * tiles_n + 1), st);
-    if (e != cudaSuccess) return e;
-  }
-  k2f_tf32<32, 2><<<dim3((unsigned)(tiles_m * tiles_n), (unsigned)(count * groups)), 256, CF::SMEM, st>>>(
-      ma_hi, ma_lo, mb_hi, mb_lo, dev_nodes, dev_coef, b, m, n, kp, tiles_n, passes, P, Q, R, count,
-      chunk, groups > 1 ? turn : nullptr);
-  return cudaGetLastError();
 }
 
 }  // namespace fmm

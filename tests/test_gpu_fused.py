@@ -196,38 +196,19 @@ def test_forced_split_equal_unfused(fb, monkeypatch, split):
 
 
 @pytest.mark.parametrize("leaf", ["3xtf32", "tf32"])
-@pytest.mark.parametrize("pname", ["winograd_L2", "strassen_L3", "C3_mix", "winograd_L1"])
-@pytest.mark.parametrize("dims", [(512, 384, 512), (4 * 100, 4 * 72, 4 * 90)])
-def test_fused_tf32_equals_unfused(fb, leaf, pname, dims):
-    # FP32 tensor-core leaves with the W-combination in a TMEM double-buffered epilogue
-    # (k2f_tf32): bitwise the unfused k2_tf32 + K3 (same MMAs, K3's FP32 sequence)
+@pytest.mark.parametrize("pname", ["winograd_L2", "C3_mix"])
+def test_tf32_leaves_never_fuse(fb, leaf, pname):
+    # the FP32 tensor-core leaves keep their products in TMEM chunk buffers + register totals
+    # (k2p_tf32) and are combined by K3: fusion "on" compiles no fused launch and gives the
+    # unfused result (the fused FP32 epilogue of round 1 was removed in round 2)
     names = PLANS[pname]
-    M, K, N = dims
+    M, K, N = 512, 384, 512
     A, B = fi.random_pair(M, K, N, seed=K, dtype=np.float32)
     lf = {"3xtf32": fb.fmm.LEAF_3XTF32, "tf32": fb.fmm.LEAF_TF32}[leaf]
     out = []
     for fusion in ("on", "off"):
         p = fb.Plan([fb.Rule.builtin(n) for n in names], M, K, N, dtype="f32", leaf=lf)
         p.set_fusion(fusion)
-        assert p.fused_launches() == (1 if fusion == "on" else 0)
+        assert p.fused_launches() == 0
         out.append(exe(p, A, B))
     assert np.array_equal(out[0], out[1])
-    if leaf == "3xtf32":
-        Co = oracle.fmm(A, B, OPlan.uniform([R.builtin(n) for n in names]))
-        assert oracle.parity_metric(out[0], Co, np.abs(A).max(), np.abs(B).max(), K) <= 5e-5
-
-
-def test_fused_tf32_depth_first_and_partition(fb):
-    A, B = fi.random_pair(512, 512, 512, seed=7, dtype=np.float32)
-    ref = None
-    for sched, part in (("breadth", None), ("depth", None), ("hybrid", None), ("auto", (0, 2)),
-                        ("auto", (1, 2))):
-        p = fb.Plan([fb.Rule.builtin("winograd")] * 2, 512, 512, 512, dtype="f32",
-                    leaf=fb.fmm.LEAF_3XTF32)
-        p.set_fusion("on")
-        p.set_schedule(sched)
-        if part:
-            p.set_partition(*part)
-        C = exe(p, A, B)
-        p.set_fusion("off")
-        assert np.array_equal(C, exe(p, A, B))
