@@ -616,8 +616,8 @@ def run_fmm(args):
                "DMMA mma.sync f64, K3X2; achieved = leaf flops / kernel time)" if single else
                "k2f_gemm_f64 (leaf products on DMMA mma.sync f64 + the parents' W-combination "
                "fused in the epilogue)" if fused else "k2_gemm_f64 (leaf products, DMMA mma.sync f64)")
-    k2_name32 = ("k2f_tf32 (3xTF32 leaf products on tcgen05 + the parents' W-combination in a TMEM "
-                 "double-buffered epilogue)" if fused else "k2_tf32 (3xTF32 leaf products on tcgen05)")
+    k2_name32 = ("k_split + k2p_tf32 (3xTF32 leaf products on tcgen05, persistent, 128-deep TMEM chunks "
+                 "drained into round-to-nearest register totals)")
     roofline = {"kernel": k2_name if args.dtype == "f64" else k2_name32,
                 "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None,

@@ -100,6 +100,23 @@ def test_leaf_gemm_tf32_tensor_core(fb, shape):
     assert np.all(np.abs(C1 - exact) <= K * 2.0 ** -9 * absab + 1e-30)
 
 
+@pytest.mark.parametrize("K", [4096, 4096 + 96])
+def test_tf32_chunked_accumulation_accuracy(fb, K):
+    # k2p_tf32 drains 128-deep TMEM chunks into round-to-nearest register totals (DESIGN.md
+    # §6.3): against the exact product its error must stay within 2x that of the FP32 oracle's
+    # leaf (the paper's classical base case, in FP32: sequential round-to-nearest dot
+    # products).  Accumulating all of K in the truncating TMEM adds fails this (~13x at K=4096).
+    M = N = 256
+    A, B = fi.random_pair(M, K, N, seed=5, dtype=np.float32)
+    C3 = fb.gemm(dev(A), dev(B), leaf=fb.fmm.LEAF_3XTF32).cpu().numpy().astype(np.float64)
+    exact = A.astype(np.float64) @ B.astype(np.float64)
+    Co = oracle.fmm(A, B, OPlan([])).astype(np.float64)
+    den = np.abs(exact).max()
+    e_gpu = np.abs(C3 - exact).max() / den
+    e_oracle = np.abs(Co - exact).max() / den
+    assert e_gpu <= 2.0 * e_oracle, (e_gpu, e_oracle)
+
+
 @pytest.mark.parametrize("names", [("winograd", "winograd"), ("strassen",) * 3])
 def test_f32_recursion_3xtf32(fb, names):
     A, B = fi.random_pair(512, 512, 512, seed=14, dtype=np.float32)
