@@ -52,6 +52,17 @@ def tf32_peak():
         return TF32_PEAK_TFLOPS_NOMINAL, "B200_PROFILING.md nominal dense TF32 (fallback)"
 
 
+def tf32_burst(achieved, three):
+    """The same kernel against MEASURED_PEAKS.json's burst bf16 figure (the sustained one, the
+    rule for a kernel inside a long step, was measured on cuBLAS at a power-capped 1320 MHz)."""
+    try:
+        v = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["bf16_tflops"])
+    except (OSError, KeyError, ValueError):
+        return {}
+    pk = v * TF32_PEAK_TFLOPS_NOMINAL / BF16_PEAK_TFLOPS_NOMINAL / (3 if three else 1)
+    return {"peak_burst": pk, "frac_burst": (achieved / pk) if achieved else None}
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -329,14 +340,16 @@ def parity_record(cpu, dtype):
 
 # ------------------------------------------------------------------------------------------
 def pass_bytes(rule_infos, M, K, N, esz, fused_leaf_level, two_level=True, two_level_k3=True,
-               depth_first_top=False):
+               depth_first_top=False, tf32_split=None):
     """Algorithmic HBM bytes of the add passes of a uniform plan: per level, K1
     reads each node's A / B block once and writes the non-trivial S_r / T_r (a column with a
     single +1 is an alias); with two levels per pass (K1X2, levels paired from the bottom where
     both split <= 4 blocks) a pass reads the sub-blocks its formed grandchildren use once and
     writes only the grandchildren (all but the products trivial at both levels); K3 reads the R
     child products and writes the node's output; with the leaf-parent level fused, that level
-    only writes its output once."""
+    only writes its output once.  tf32_split (FP32 tensor-core leaves): "pass" -- the leaf
+    level's K1X2 forms every leaf operand (views too) and writes its TF32 hi and lo parts (DESIGN.md
+    §6.3); "kernel" -- a split pass reads every leaf operand and writes hi and lo."""
     def col(X, r):
         return [i for i in range(len(X)) if X[i][r] != 0]
 
@@ -386,6 +399,15 @@ def pass_bytes(rule_infos, M, K, N, esz, fused_leaf_level, two_level=True, two_l
         if pair[l]:
             r2 = rule_infos[l + 1]
             mb, kb, nb = dims[l + 2]
+            if tf32_split == "pass" and l + 2 == L:
+                allf = ri["R"] * r2["R"]  # every grandchild formed, hi + lo written
+                na = len({(i1, i2) for r1 in range(ri["R"]) for i1 in col(ri["U"], r1)
+                          for q in range(r2["R"]) for i2 in col(r2["U"], q)})
+                nb_ = len({(i1, i2) for r1 in range(ri["R"]) for i1 in col(ri["V"], r1)
+                           for q in range(r2["R"]) for i2 in col(r2["V"], q)})
+                total += nodes[l] * ((na + 2 * allf) * mb * kb + (nb_ + 2 * allf) * kb * nb) * esz
+                l += 2
+                continue
             fa, na = two_levels(ri["U"], ri["R"], r2["U"], r2["R"])
             fb_, nb_ = two_levels(ri["V"], ri["R"], r2["V"], r2["R"])
             total += nodes[l] * ((na + fa) * mb * kb + (nb_ + fb_) * kb * nb) * esz
@@ -395,6 +417,9 @@ def pass_bytes(rule_infos, M, K, N, esz, fused_leaf_level, two_level=True, two_l
             (nsa, ua), (nsb, ub) = one_level(ri["U"], ri["R"]), one_level(ri["V"], ri["R"])
             total += nodes[l] * ((ua + nsa) * mb * kb + (ub + nsb) * kb * nb) * esz
             l += 1
+    if tf32_split == "kernel":  # read every leaf operand, write its hi and lo
+        mb, kb, nb = dims[L]
+        total += nodes[L] * 3 * (mb * kb + kb * nb) * esz
     # K3 / fused epilogue; two levels per K3 pass (K3X2) paired from the bottom of the unfused
     # levels (not the depth-first top level, whose W-combination is the per-r ACC pass)
     top = L - 2 if fused_leaf_level else L - 1
@@ -616,8 +641,10 @@ def run_fmm(args):
                "DMMA mma.sync f64, K3X2; achieved = leaf flops / kernel time)" if single else
                "k2f_gemm_f64 (leaf products on DMMA mma.sync f64 + the parents' W-combination "
                "fused in the epilogue)" if fused else "k2_gemm_f64 (leaf products, DMMA mma.sync f64)")
-    k2_name32 = ("k_split + k2p_tf32 (3xTF32 leaf products on tcgen05, persistent, 128-deep TMEM chunks "
-                 "drained into round-to-nearest register totals)")
+    k2_name32 = ("k2p_tf32 (3xTF32 leaf products on tcgen05, persistent, 128-deep TMEM chunks drained "
+                 "into round-to-nearest register totals; hi / lo operands written by the leaf "
+                 "level's K1X2" + (", a split kernel in the launch)" if os.environ.get(
+                     "FMM_TF32_PRESPLIT", "1") == "0" else ")"))
     roofline = {"kernel": k2_name if args.dtype == "f64" else k2_name32,
                 "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None,
@@ -626,6 +653,7 @@ def run_fmm(args):
                                "MEASURED_PEAKS.json has no FP64 entry" if args.dtype == "f64" else
                                tf32_src + (" / 3 (3xTF32: three MMA passes)"
                                            if leaf == fb.fmm.LEAF_3XTF32 else ""),
+                **({} if args.dtype == "f64" else tf32_burst(achieved, leaf == fb.fmm.LEAF_3XTF32)),
                 "flops_per_launch": per_launch_flops, "launch_ms": (k2_ms / k2_n) if k2_n else None,
                 "step_share": {k: v[0] / max(sum(x[0] for x in kinds.values()), 1e-9)
                                for k, v in kinds.items()},
@@ -639,9 +667,16 @@ def run_fmm(args):
         hbm = float(json.loads((ROOT / "MEASURED_PEAKS.json").read_text())["hbm_gbs"])
     except (OSError, KeyError, ValueError):
         pass
+    tf32_split = None
+    if args.dtype == "f32" and leaf != fb.fmm.LEAF_NATIVE:
+        lk = K >> len(rules) if all(r in ("winograd", "strassen", "classical222") for r in rules) else 0
+        ln = N >> len(rules) if lk else 0
+        presplit = (os.environ.get("FMM_TF32_PRESPLIT", "1") != "0" and lk % 32 == 0 and ln % 32 == 0
+                    and os.environ.get("FMM_K1X2", "1") != "0" and len(rules) >= 2)
+        tf32_split = "pass" if presplit else "kernel"
     pbytes = (pass_bytes([fb.Rule.builtin(r).info() for r in rules], M, K, N, esz, fused,
                          os.environ.get("FMM_K1X2", "1") != "0", os.environ.get("FMM_K3X2", "1") != "0",
-                         "ACC" in kinds) if ws == 1 else None)
+                         "ACC" in kinds, tf32_split) if ws == 1 else None)
     pipeline = None
     if pbytes is not None and args.scaling == "none":
         t_roof = leaf_flops_step / (peak * 1e12) + pbytes / (hbm * 1e9)

@@ -167,6 +167,18 @@ fmm_status fmm_plan_set_fusion(fmm_plan* plan, int mode);
  * fmm_plan_create. */
 fmm_status fmm_plan_set_k1_levels(fmm_plan* plan, int levels);
 
+/* Where the FP32 tensor-core leaves' operands are split (host-only; FMM_F32 plans with leaf
+ * FMM_LEAF_3XTF32 / FMM_LEAF_TF32; north star item 2, the leaf products M_r = S_r T_r of P:125).
+ * The tensor-core leaf multiplies TF32 hi / lo parts (x = hi + lo, hi = x rounded to 10 mantissa
+ * bits, lo = x - hi exact) read from an operand arena in the workspace.  in_pass = 1 (default):
+ * where the leaf level's S / T are formed by a two-level K1X2 pass and the leaf k and n are
+ * multiples of 32, that pass writes the hi / lo pairs of every leaf operand straight into the
+ * arena (views included) -- no separate split pass, and the leaf-level S_r / T_r themselves are
+ * never written.  in_pass = 0: the pass writes S_r / T_r and a split kernel fills the arena.
+ * Both give bitwise the same C.  FMM_E_ARG for other values.  The environment variable
+ * FMM_TF32_PRESPLIT=0 sets 0 at fmm_plan_create. */
+fmm_status fmm_plan_set_leaf_split(fmm_plan* plan, int in_pass);
+
 /* W-combination levels per pass (host-only; north star item 3, P:119 applied twice).
  * levels = 2 (default): where a level d and its children use built-in 2x2x2 rules (Strassen,
  * Strassen-Winograd, classical: U, V and W tables equal to the built-in ones), one K3X2 launch

@@ -130,6 +130,8 @@ struct fmm_plan {
   int comm_mode = 0;    // multi-GPU exchange: 0 reduce to rank 0, 1 all-reduce, 2 reduce-scatter
   bool split_chains = true;     // fused units' product chains split over CTAs (turnstiles)
   bool k1_two_level = true;     // S / T of two recursion levels formed in one pass (K1X2)
+  bool tf32_presplit = true;    // FP32 tensor-core leaves: the leaf level's K1X2 writes the
+                                // hi / lo operand arena (no separate split pass)
   bool k3_two_level = true;     // W-combination of two recursion levels in one pass (K3X2)
   // virtual scaling (compile_plan): power-of-two factors applied by the root K1 while it forms
   // S_r / T_r from the original A, B (the scaled A', B' are not written)
@@ -373,18 +375,54 @@ struct Builder {
   // products M_{r1}, only c allocated -- their S / T are never formed) and the grandchildren
   // (level d+2, operands formed or views, c allocated if alloc_c), both in BFS order.  The
   // formed outputs are listed r1-major, r2 ascending: the kernel's compile-time order.
+  // split: the grandchildren are the leaves of an FP32 tensor-core K2 step; every S / T of them
+  // (views too) is written as its TF32 hi / lo pair straight into that step's operand arena
+  // (allocated here, leaf index = BFS position; A side m x k K-major, B side k x n MN-major:
+  // exactly the K1X2 output layout when k and n are multiples of 32), which emit_k2 picks up.
   std::pair<std::vector<Node>, std::vector<Node>> emit_k1x2(int d, const std::vector<Node>& nodes,
-                                                            int pair, bool alloc_c) {
+                                                            int pair, bool alloc_c, bool split = false) {
     const int ra = (pair - 1) / 3, rb = (pair - 1) % 3;
     const int64_t mb1 = p->lm[d + 1], kb1 = p->lk[d + 1], nb1 = p->ln[d + 1];
     const int64_t mb = p->lm[d + 2], kb = p->lk[d + 2], nb = p->ln[d + 2];
     const int R1 = builtin_R(ra), R2 = builtin_R(rb);
     std::vector<K1x2Node> ks, kt;
     std::vector<Node> kids, grand;
+    const int64_t nleaves = (int64_t)nodes.size() * R1 * R2;
+    int64_t arena = -1, slab_a = mb * kb, slab_b = kb * nb;
+    if (split) {
+      arena = ws_alloc((int64_t)tf32_arena_floats(nleaves, mb, nb, kb));
+      pending_arena = arena;
+      pending_leaves = nleaves;
+    }
+    int64_t leaf = 0;
     for (const Node& nd : nodes) {
       K1x2Node s{}, t{};
       s.in = nd.a; s.rows = mb; s.cols = kb; s.tv = 0;
       t.in = nd.b; t.rows = kb; t.cols = nb; t.tv = 1;
+      if (split) {
+        s.lo_off = nleaves * slab_a;
+        t.lo_off = nleaves * slab_b;
+        for (int r1 = 0; r1 < R1; ++r1) {
+          Node ch;
+          ch.idx = nd.idx * R1 + r1;
+          ch.a = Op{}; ch.b = Op{};
+          ch.c = ws_op(ws_alloc(mb1 * nb1), nb1);
+          kids.push_back(ch);
+          for (int r2 = 0; r2 < R2; ++r2, ++leaf) {
+            Node g;
+            g.idx = ch.idx * R2 + r2;
+            g.a = ws_op(arena + leaf * slab_a, kb);                           // S hi (m x k)
+            g.b = ws_op(arena + 2 * nleaves * slab_a + leaf * slab_b, nb);    // T hi (k x n)
+            s.out[s.nout++] = g.a;
+            t.out[t.nout++] = g.b;
+            if (alloc_c) g.c = ws_op(ws_alloc(mb * nb), nb);
+            grand.push_back(g);
+          }
+        }
+        ks.push_back(s);
+        kt.push_back(t);
+        continue;
+      }
       for (int r1 = 0; r1 < R1; ++r1) {
         Node ch;
         ch.idx = nd.idx * R1 + r1;
@@ -430,10 +468,20 @@ struct Builder {
       st.rows = ks.empty() ? kb : kt.empty() ? mb : std::max(mb, kb);
       st.cols = ks.empty() ? nb : kt.empty() ? kb : std::max(kb, nb);
       st.P = 4; st.Q = 1; st.R = R1;
+      st.tf32_split = split ? 1 : 0;
       p->steps.push_back(st);
     }
     return {kids, grand};
   }
+
+  // FP32 tensor-core leaves of dims m x k x n can take their hi / lo operands from the leaf
+  // level's K1X2 (emit_k1x2 split mode)
+  bool presplit_ok() const {
+    const int64_t m = p->lm[p->L], k = p->lk[p->L], n = p->ln[p->L];
+    return p->dtype == FMM_F32 && p->leaf != FMM_LEAF_NATIVE && p->tf32_presplit && tf32_bmn() &&
+           m > 0 && k > 0 && n > 0 && k % 32 == 0 && n % 32 == 0;
+  }
+  int64_t pending_arena = -1, pending_leaves = 0;  // a K1X2 split-mode arena for the next K2
 
   void emit_k2(const std::vector<Node>& leaves) {
     std::vector<LeafNode> lf;
@@ -444,8 +492,16 @@ struct Builder {
     st.dev_off = push(lf);
     st.rows = p->lm[p->L]; st.cols = p->ln[p->L]; st.inner = p->lk[p->L];
     st.arena_off = -1;
-    if (p->dtype == FMM_F32 && p->leaf != FMM_LEAF_NATIVE)
-      st.arena_off = ws_alloc((int64_t)tf32_arena_floats(st.count, st.rows, st.cols, st.inner));
+    if (p->dtype == FMM_F32 && p->leaf != FMM_LEAF_NATIVE) {
+      if (pending_arena >= 0 && pending_leaves == (int64_t)lf.size()) {  // filled by the K1X2
+        st.arena_off = pending_arena;
+        st.tf32_split = 1;
+      } else {
+        st.arena_off = ws_alloc((int64_t)tf32_arena_floats(st.count, st.rows, st.cols, st.inner));
+      }
+    }
+    pending_arena = -1;
+    pending_leaves = 0;
     p->steps.push_back(st);
   }
 
@@ -699,7 +755,8 @@ struct Builder {
     for (int d = l; d < p->L;) {
       const int pr = pair_at[d] && p->k1_two_level ? k1x2_pair(d, lv.back()) : 0;
       if (pr) {
-        auto kg = emit_k1x2(d, lv.back(), pr, !(d + 2 == p->L && fuse));
+        auto kg = emit_k1x2(d, lv.back(), pr, !(d + 2 == p->L && fuse),
+                            d + 2 == p->L && !fuse && presplit_ok());
         lv.push_back(kg.first);
         lv.push_back(kg.second);
         d += 2;
@@ -1077,7 +1134,8 @@ static cudaError_t launch_step(const fmm_plan* p, const Step& s, int64_t c0, con
       return launch_gemm_f32((const LeafNode*)nd,
                              (const LeafNode*)(p->desc_host.data() + s.dev_off) + c0, s.count,
                              s.rows, s.cols, s.inner, b, vec, p->leaf,
-                             s.arena_off >= 0 ? (float*)b.p[BASE_WS] + s.arena_off : nullptr, st);
+                             s.arena_off >= 0 ? (float*)b.p[BASE_WS] + s.arena_off : nullptr, st,
+                             s.tf32_split != 0);
   }
   return cudaSuccess;
 }
@@ -1282,6 +1340,7 @@ fmm_status fmm_plan_create(const fmm_rule* const* nodes, int n_nodes, int levels
   p->dtype = dtype; p->leaf = leaf; p->L = levels; p->M = M; p->K = K; p->N = N;
   if (const char* ce = getenv("FMM_SPLIT")) p->split_chains = atoi(ce) != 0;
   if (const char* xe = getenv("FMM_K1X2")) p->k1_two_level = atoi(xe) != 0;
+  if (const char* xe = getenv("FMM_TF32_PRESPLIT")) p->tf32_presplit = atoi(xe) != 0;
   if (const char* xe = getenv("FMM_K3X2")) p->k3_two_level = atoi(xe) != 0;
   if (const char* fe = getenv("FMM_FUSION")) {
     const int f = atoi(fe);
@@ -1390,6 +1449,12 @@ fmm_status fmm_plan_set_fusion(fmm_plan* p, int mode) {
 fmm_status fmm_plan_set_k1_levels(fmm_plan* p, int levels) {
   if (!p || levels < 1 || levels > 2) { set_error("fmm_plan_set_k1_levels: levels must be 1 or 2"); return FMM_E_ARG; }
   p->k1_two_level = levels == 2;
+  return compile_plan(p);
+}
+
+fmm_status fmm_plan_set_leaf_split(fmm_plan* p, int in_pass) {
+  if (!p || in_pass < 0 || in_pass > 1) { set_error("fmm_plan_set_leaf_split: mode must be 0 or 1"); return FMM_E_ARG; }
+  p->tf32_presplit = in_pass == 1;
   return compile_plan(p);
 }
 
@@ -1963,6 +2028,7 @@ static const fmm_plan* depth_first_twin(const fmm_plan* p) {
     t->coef_host = p->coef_host; t->schedule = 2; t->fusion = p->fusion; t->shard_depth = p->shard_depth;
     t->split_chains = p->split_chains;
     t->k1_two_level = p->k1_two_level;
+    t->tf32_presplit = p->tf32_presplit;
     t->k3_two_level = p->k3_two_level;
     if (compile_plan(t) != FMM_OK) { delete t; return nullptr; }
     p->df_twin = t;

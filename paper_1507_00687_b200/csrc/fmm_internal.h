@@ -137,6 +137,10 @@ struct K1x2Node {
   int64_t rows, cols;  // grandchild block dims (outputs are workspace blocks with ld = cols)
   int32_t tv;          // 0: S (U tables, A side), 1: T (V tables, B side)
   int32_t nout;        // formed grandchildren (checked against the kernel's list)
+  // FP32 tensor-core leaves, split mode (lo_off > 0): EVERY (r1, r2) is formed (views too) and
+  // written as its TF32 hi / lo pair -- hi at out[idx], lo lo_off elements further -- straight
+  // into the leaf GEMM's operand arena
+  int64_t lo_off;
   Op out[kMaxX2];
 };
 
@@ -229,6 +233,8 @@ struct Step {
   // count2, rows x cols x inner), the K3X2 nodes (dev_off3, count3), rule pair x2
   int count2 = 0, count3 = 0;
   int64_t dev_off3 = -1;
+  int tf32_split = 0;  // K1 (x2): split mode (K1x2Node.lo_off); K2 FP32: the arena is already
+                       // filled by that pass (no split kernel)
 };
 
 // ---- kernel launchers (kernels_*.cu) -----------------------------------------------------------
@@ -277,9 +283,21 @@ int small_tile_m();
 int small_tile_n();
 cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, const LeafNode* host_leaves, int count,
                             int64_t m, int64_t n, int64_t k, const Bases& b, bool vec, int leaf,
-                            float* arena, cudaStream_t st);
+                            float* arena, cudaStream_t st, bool presplit = false);
 // floats of workspace the tensor-core FP32 leaf needs for a batch (hi / lo operand arena)
 size_t tf32_arena_floats(int64_t count, int64_t m, int64_t n, int64_t k);
+// the FP32 tensor-core leaf reads B MN-major (T as stored; FMM_TF32_BMN, default on)
+bool tf32_bmn();
+
+// TF32 hi / lo split of an FP32 value: hi = x rounded to 10 mantissa bits (nearest, ties away),
+// lo = x - hi (exact); the split every producer of the tensor-core leaf operands uses
+#ifdef __CUDACC__
+__device__ __forceinline__ void tf32_split(float x, float& h, float& l) {
+  const uint32_t u = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+  h = __uint_as_float(u);
+  l = x - h;
+}
+#endif
 
 // ---- error reporting ------------------------------------------------------------------------
 void set_error(const std::string& msg);

@@ -10,7 +10,7 @@ namespace fmm {
 
 cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
                              int64_t k, const Bases& b, int passes, float* arena,
-                             cudaStream_t st, const LeafNode* host_leaves);
+                             cudaStream_t st, const LeafNode* host_leaves, bool presplit);
 namespace {
 
 constexpr int BM = 128, BN = 128, BK = 8, THREADS = 256;
@@ -100,12 +100,12 @@ __global__ void __launch_bounds__(THREADS)
 
 cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, const LeafNode* host_leaves, int count,
                             int64_t m, int64_t n, int64_t k, const Bases& b, bool vec, int leaf,
-                            float* arena, cudaStream_t st) {
+                            float* arena, cudaStream_t st, bool presplit) {
   (void)vec;
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
   if (leaf == FMM_LEAF_TF32 || leaf == FMM_LEAF_3XTF32) {
     const int passes = leaf == FMM_LEAF_TF32 ? 1 : 3;
-    return launch_gemm_tf32(dev_leaves, count, m, n, k, b, passes, arena, st, host_leaves);
+    return launch_gemm_tf32(dev_leaves, count, m, n, k, b, passes, arena, st, host_leaves, presplit);
   }
   const int tiles_m = (int)((m + BM - 1) / BM), tiles_n = (int)((n + BN - 1) / BN);
   dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)count);

@@ -100,17 +100,8 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
                : "memory");
 }
 
-__device__ __forceinline__ float tf32_hi(float x) {
-  uint32_t u = __float_as_uint(x);
-  u = (u + 0x1000u) & 0xFFFFE000u;  // round to nearest (ties away) at 10 mantissa bits
-  return __uint_as_float(u);
-}
-
-// x = hi + lo exactly: hi = x rounded to TF32, lo = x - hi (exact in FP32)
-__device__ __forceinline__ void split2(float x, float& h, float& l) {
-  h = tf32_hi(x);
-  l = x - h;
-}
+// x = hi + lo exactly: hi = x rounded to TF32 (nearest, ties away), lo = x - hi (exact in FP32)
+__device__ __forceinline__ void split2(float x, float& h, float& l) { tf32_split(x, h, l); }
 
 // K-major UMMA descriptor for a BK-float-wide swizzled tile (BK = 32: SW128, BK = 16: SW64).
 template <int BK>
@@ -122,6 +113,31 @@ __device__ __forceinline__ uint64_t desc_k(uint32_t saddr) {
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)(BK == 32 ? 2 : 4) << 61;  // SWIZZLE_128B / SWIZZLE_64B
   return d;
+}
+
+// MN-major UMMA descriptor for a B tile stored as BK k-rows of 128 bytes (32 n) per 32-column
+// atom, atoms 128 * BK bytes apart along n: the tf32 MN-major layout SWIZZLE_128B_BASE32B (32-byte
+// chunks XOR-ed with the k-row index mod 4, what TMA's SWIZZLE_128B_ATOM_32B writes); LBO = the
+// n-atom stride, SBO = 4 k-rows (512 bytes)
+template <int BK>
+__device__ __forceinline__ uint64_t desc_mn(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)((128 * BK) >> 4) << 16;  // leading byte offset: next 32-column atom
+  d |= (uint64_t)(512 >> 4) << 32;         // stride byte offset: next 4 k-rows
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;                  // SWIZZLE_128B_BASE32B
+  return d;
+}
+
+// instruction descriptor with B MN-major (bit 16: transpose B)
+constexpr uint32_t IDESC_BMN = IDESC | (1u << 16);
+
+__device__ __forceinline__ void mma_tf32_bmn(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(IDESC_BMN), "r"(acc));
 }
 
 template <int BK, int STAGES>
@@ -166,7 +182,7 @@ __device__ __forceinline__ void item_coords(int t, int tiles, int tiles_m, int t
   n0 = (w / gsz) * TBN;
 }
 
-template <int BK, int STAGES, int EW>
+template <int BK, int STAGES, int EW, bool BMN>
 __global__ void __launch_bounds__(EpiCfg<EW>::THREADS, 1)
     k2p_tf32(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
              const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
@@ -207,6 +223,16 @@ __global__ void __launch_bounds__(EpiCfg<EW>::THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  // B tile: K-major (one box of BK x 256 rows of n) or MN-major (eight boxes of 32 n x BK k-rows,
+  // 128 * BK bytes apart)
+  auto load_b = [&](uint8_t* dst, const CUtensorMap* map, int kc, int n0, int leaf, uint32_t full) {
+    if constexpr (BMN) {
+#pragma unroll
+      for (int j = 0; j < TBN / 32; ++j) tma_load_3d(su32(dst + j * 128 * BK), map, n0 + 32 * j, kc, leaf, full);
+    } else {
+      tma_load_3d(su32(dst), map, kc, n0, leaf, full);
+    }
+  };
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer ----
       int it = 0;
@@ -224,12 +250,12 @@ __global__ void __launch_bounds__(EpiCfg<EW>::THREADS, 1)
             mbar_expect_tx(full, STAGE_BYTES);
             tma_load_3d(su32(st), &ta_hi, kc, m0, leaf, full);
             tma_load_3d(su32(st + A_BYTES), &ta_lo, kc, m0, leaf, full);
-            tma_load_3d(su32(st + 2 * A_BYTES), &tb_hi, kc, n0, leaf, full);
-            tma_load_3d(su32(st + 2 * A_BYTES + B_BYTES), &tb_lo, kc, n0, leaf, full);
+            load_b(st + 2 * A_BYTES, &tb_hi, kc, n0, leaf, full);
+            load_b(st + 2 * A_BYTES + B_BYTES, &tb_lo, kc, n0, leaf, full);
           } else {
             mbar_expect_tx(full, A_BYTES + B_BYTES);
             tma_load_3d(su32(st), &ta_hi, kc, m0, leaf, full);
-            tma_load_3d(su32(st + 2 * A_BYTES), &tb_hi, kc, n0, leaf, full);
+            load_b(st + 2 * A_BYTES, &tb_hi, kc, n0, leaf, full);
           }
         }
       }
@@ -250,18 +276,31 @@ __global__ void __launch_bounds__(EpiCfg<EW>::THREADS, 1)
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             uint8_t* st = smem + s * STAGE_BYTES;
             const uint64_t a_hi = desc_k<BK>(su32(st)), a_lo = desc_k<BK>(su32(st + A_BYTES));
-            const uint64_t b_hi = desc_k<BK>(su32(st + 2 * A_BYTES));
-            const uint64_t b_lo = desc_k<BK>(su32(st + 2 * A_BYTES + B_BYTES));
+            const uint64_t b_hi = BMN ? desc_mn<BK>(su32(st + 2 * A_BYTES)) : desc_k<BK>(su32(st + 2 * A_BYTES));
+            const uint64_t b_lo = BMN ? desc_mn<BK>(su32(st + 2 * A_BYTES + B_BYTES))
+                                      : desc_k<BK>(su32(st + 2 * A_BYTES + B_BYTES));
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
               const uint64_t off = (uint64_t)((kk * 32) >> 4);  // 8 tf32 = 32 bytes along K
+              // MN-major B: 8 k-rows of 128 bytes
+              const uint64_t offb = BMN ? (uint64_t)((kk * 8 * 128) >> 4) : off;
               const uint32_t first = (kt == kt0 && kk == 0) ? 0u : 1u;
-              if (passes == 3) {  // small terms first
-                mma_tf32(acc, a_lo + off, b_hi + off, first);
-                mma_tf32(acc, a_hi + off, b_lo + off, 1u);
-                mma_tf32(acc, a_hi + off, b_hi + off, 1u);
+              if constexpr (BMN) {
+                if (passes == 3) {  // small terms first
+                  mma_tf32_bmn(acc, a_lo + off, b_hi + offb, first);
+                  mma_tf32_bmn(acc, a_hi + off, b_lo + offb, 1u);
+                  mma_tf32_bmn(acc, a_hi + off, b_hi + offb, 1u);
+                } else {
+                  mma_tf32_bmn(acc, a_hi + off, b_hi + offb, first);
+                }
               } else {
-                mma_tf32(acc, a_hi + off, b_hi + off, first);
+                if (passes == 3) {  // small terms first
+                  mma_tf32(acc, a_lo + off, b_hi + off, first);
+                  mma_tf32(acc, a_hi + off, b_lo + off, 1u);
+                  mma_tf32(acc, a_hi + off, b_hi + off, 1u);
+                } else {
+                  mma_tf32(acc, a_hi + off, b_hi + off, first);
+                }
               }
             }
             mma_commit(su32(&bars[STAGES + s]));  // stage s free once these MMAs complete
@@ -446,10 +485,48 @@ __global__ void __launch_bounds__(256) k_split_b_vec(const LeafNode* __restrict_
   }
 }
 
+// B side for the MN-major B operand: T (k x n) -> hi, lo (kp x np, rows = k, np = n rounded up
+// to 32, pad rows / columns zero): elementwise, no transpose.  grid: x = np / 4 / 256 chunks,
+// y = row stride, z = leaf.
+__global__ void k_split_bn_vec(const LeafNode* __restrict__ leaves, Bases bases, int64_t n, int64_t k,
+                               int64_t kp, int64_t np, float* __restrict__ b_hi, float* __restrict__ b_lo) {
+  const LeafNode& lf = leaves[blockIdx.z];
+  int64_t ldb;
+  const float* B = op_ptr<const float>(bases, lf.b, ldb);
+  const size_t base = (size_t)blockIdx.z * (size_t)(kp * np);
+  const int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (c >= np) return;
+  for (int64_t r = blockIdx.y; r < kp; r += gridDim.y) {
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (r < k && c < n) x = *reinterpret_cast<const float4*>(B + r * ldb + c);
+    float4 h, l;
+    split2(x.x, h.x, l.x); split2(x.y, h.y, l.y); split2(x.z, h.z, l.z); split2(x.w, h.w, l.w);
+    *reinterpret_cast<float4*>(b_hi + base + r * np + c) = h;
+    *reinterpret_cast<float4*>(b_lo + base + r * np + c) = l;
+  }
+}
+
+__global__ void k_split_bn(const LeafNode* __restrict__ leaves, Bases bases, int64_t n, int64_t k,
+                           int64_t kp, int64_t np, float* __restrict__ b_hi, float* __restrict__ b_lo) {
+  const LeafNode& lf = leaves[blockIdx.z];
+  int64_t ldb;
+  const float* B = op_ptr<const float>(bases, lf.b, ldb);
+  const size_t base = (size_t)blockIdx.z * (size_t)(kp * np);
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= np) return;
+  for (int64_t r = blockIdx.y; r < kp; r += gridDim.y) {
+    const float x = (r < k && c < n) ? B[r * ldb + c] : 0.f;
+    float h, l;
+    split2(x, h, l);
+    b_hi[base + r * np + c] = h;
+    b_lo[base + r * np + c] = l;
+  }
+}
+
 // Split launcher: vectorised kernels when every leaf operand allows 16-byte access.
 void launch_split(const LeafNode* dev_leaves, const LeafNode* host_leaves, int count, const Bases& b,
                   int64_t m, int64_t n, int64_t k, int64_t kp, float* a_hi, float* a_lo, float* b_hi,
-                  float* b_lo, cudaStream_t st) {
+                  float* b_lo, cudaStream_t st, bool bmn) {
   bool vec = host_leaves != nullptr && k % 4 == 0 && n % 4 == 0;
   for (int i = 0; vec && i < count; ++i) {
     int64_t lda, ldb;
@@ -457,18 +534,28 @@ void launch_split(const LeafNode* dev_leaves, const LeafNode* host_leaves, int c
     const float* B = op_ptr<const float>(b, host_leaves[i].b, ldb);
     vec = !((((uintptr_t)A) & 15u) || (((uintptr_t)B) & 15u) || (lda & 3) || (ldb & 3));
   }
+  const int64_t np = (n + 31) / 32 * 32;
+  const unsigned ry = (unsigned)(kp < 8192 ? kp : 8192);
   if (vec) {
     k_split_a_vec<<<dim3((unsigned)((kp / 4 + 255) / 256), (unsigned)(m < 8192 ? m : 8192), (unsigned)count), 256, 0, st>>>(
         dev_leaves, b, m, k, kp, a_hi, a_lo);
-    k_split_b_vec<<<dim3((unsigned)((kp + 63) / 64), (unsigned)((n + 63) / 64), (unsigned)count), 256, 0, st>>>(
-        dev_leaves, b, n, k, kp, b_hi, b_lo);
+    if (bmn)
+      k_split_bn_vec<<<dim3((unsigned)((np / 4 + 255) / 256), ry, (unsigned)count), 256, 0, st>>>(
+          dev_leaves, b, n, k, kp, np, b_hi, b_lo);
+    else
+      k_split_b_vec<<<dim3((unsigned)((kp + 63) / 64), (unsigned)((n + 63) / 64), (unsigned)count), 256, 0, st>>>(
+          dev_leaves, b, n, k, kp, b_hi, b_lo);
     return;
   }
   dim3 blk(32, 8);
   k_split_tf32<<<dim3((unsigned)(kp / 32), (unsigned)((m + 31) / 32), (unsigned)count), blk, 0, st>>>(
       dev_leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, 0);
-  k_split_tf32<<<dim3((unsigned)(kp / 32), (unsigned)((n + 31) / 32), (unsigned)count), blk, 0, st>>>(
-      dev_leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, 1);
+  if (bmn)
+    k_split_bn<<<dim3((unsigned)((np + 255) / 256), ry, (unsigned)count), 256, 0, st>>>(
+        dev_leaves, b, n, k, kp, np, b_hi, b_lo);
+  else
+    k_split_tf32<<<dim3((unsigned)(kp / 32), (unsigned)((n + 31) / 32), (unsigned)count), blk, 0, st>>>(
+        dev_leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, 1);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -499,21 +586,39 @@ bool make_map(CUtensorMap* map, float* base, int64_t kp, int64_t rows, int64_t l
   return r == CUDA_SUCCESS;
 }
 
+// MN-major B: T hi / lo (kp x np per leaf, rows = k), boxes of 32 n x box_k k-rows, 128-byte
+// swizzle with 32-byte atoms (the UMMA SWIZZLE_128B_BASE32B layout)
+bool make_map_mn(CUtensorMap* map, float* base, int64_t np, int64_t kp, int64_t leaves, int box_k) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)np, (cuuint64_t)kp, (cuuint64_t)leaves};
+  cuuint64_t strides[2] = {(cuuint64_t)(np * 4), (cuuint64_t)(np * kp * 4)};
+  cuuint32_t box[3] = {32, (cuuint32_t)box_k, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 int num_sms() {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   return sms > 0 ? sms : 148;
 }
 
-template <int BK, int STAGES, int EW>
+template <int BK, int STAGES, int EW, bool BMN>
 cudaError_t launch_k2p(float* a_hi, float* a_lo, float* b_hi, float* b_lo, const LeafNode* dev_leaves,
                        int count, int64_t m, int64_t n, int64_t kp, const Bases& b, int passes,
                        int chunk_k, cudaStream_t st) {
   using CF = TCfg<BK, STAGES>;
   CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
   const int64_t kpe = kp > 0 ? kp : TBK;
-  if (!make_map(&ma_hi, a_hi, kpe, m, count, TBM, BK) || !make_map(&ma_lo, a_lo, kpe, m, count, TBM, BK) ||
-      !make_map(&mb_hi, b_hi, kpe, n, count, TBN, BK) || !make_map(&mb_lo, b_lo, kpe, n, count, TBN, BK))
+  const int64_t np = (n + 31) / 32 * 32;
+  if (!make_map(&ma_hi, a_hi, kpe, m, count, TBM, BK) || !make_map(&ma_lo, a_lo, kpe, m, count, TBM, BK))
+    return cudaErrorInvalidValue;
+  if (BMN ? (!make_map_mn(&mb_hi, b_hi, np, kpe, count, BK) || !make_map_mn(&mb_lo, b_lo, np, kpe, count, BK))
+          : (!make_map(&mb_hi, b_hi, kpe, n, count, TBN, BK) || !make_map(&mb_lo, b_lo, kpe, n, count, TBN, BK)))
     return cudaErrorInvalidValue;
   const int tiles_m = (int)((m + TBM - 1) / TBM), tiles_n = (int)((n + TBN - 1) / TBN);
   const int tiles = tiles_m * tiles_n;
@@ -521,14 +626,14 @@ cudaError_t launch_k2p(float* a_hi, float* a_lo, float* b_hi, float* b_lo, const
   if (total > INT32_MAX) return cudaErrorInvalidValue;
   const int grid = (int)std::min<int64_t>(total, num_sms());
   const int chunk_kt = std::max(1, chunk_k / BK);
-  cudaError_t e = cudaFuncSetAttribute(k2p_tf32<BK, STAGES, EW>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
+  cudaError_t e = cudaFuncSetAttribute(k2p_tf32<BK, STAGES, EW, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
   if (e != cudaSuccess) return e;
   static const int group_m = [] {
     const char* e = getenv("FMM_TF32_GROUP_M");  // tile rows per rasterisation group
     const int v = e ? atoi(e) : 16;
     return v >= 1 ? v : 16;
   }();
-  k2p_tf32<BK, STAGES, EW><<<grid, EpiCfg<EW>::THREADS, CF::SMEM, st>>>(
+  k2p_tf32<BK, STAGES, EW, BMN><<<grid, EpiCfg<EW>::THREADS, CF::SMEM, st>>>(
       ma_hi, ma_lo, mb_hi, mb_lo, dev_leaves, b, m, n, kp, tiles_m, tiles_n, group_m, (int)total, passes,
       chunk_kt);
   return cudaGetLastError();
@@ -536,9 +641,21 @@ cudaError_t launch_k2p(float* a_hi, float* a_lo, float* b_hi, float* b_lo, const
 
 }  // namespace
 
+// hi / lo arena: A side m x kp (K-major), B side kp x np (MN-major, np = n rounded up to 32) or
+// n x kp (K-major); kp = k rounded up to 32
 size_t tf32_arena_floats(int64_t count, int64_t m, int64_t n, int64_t k) {
-  const int64_t kp = (k + TBK - 1) / TBK * TBK;
-  return (size_t)count * (size_t)(2 * m * kp + 2 * n * kp);
+  const int64_t kp = (k + TBK - 1) / TBK * TBK, np = (n + 31) / 32 * 32;
+  return (size_t)count * (size_t)(2 * m * kp + 2 * np * kp);
+}
+
+// B operand layout of the FP32 tensor-core leaf: FMM_TF32_BMN = 1 (default) MN-major (T as
+// stored, split elementwise), 0 K-major (T transposed by the split)
+bool tf32_bmn() {
+  static const bool v = [] {
+    const char* e = getenv("FMM_TF32_BMN");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return v;
 }
 
 // Chunk length (k elements) of the round-to-nearest accumulation: FMM_TF32_CHUNK, default 128
@@ -554,30 +671,32 @@ int tf32_chunk_k() {
 
 cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, int64_t n,
                              int64_t k, const Bases& b, int passes, float* arena,
-                             cudaStream_t st, const LeafNode* host_leaves) {
+                             cudaStream_t st, const LeafNode* host_leaves, bool presplit) {
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
   if (!arena) return cudaErrorInvalidValue;
+  // presplit: the leaf level's K1X2 wrote the arena (k, n multiples of 32, B MN-major)
+  if (presplit && (k % TBK != 0 || n % 32 != 0 || !tf32_bmn())) return cudaErrorInvalidValue;
   const int64_t kp = (k + TBK - 1) / TBK * TBK;
   float* a_hi = arena;
   float* a_lo = a_hi + (size_t)count * m * kp;
   float* b_hi = a_lo + (size_t)count * m * kp;
-  float* b_lo = b_hi + (size_t)count * n * kp;
-  if (kp > 0) launch_split(dev_leaves, host_leaves, count, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, st);
+  float* b_lo = b_hi + (size_t)count * ((n + 31) / 32 * 32) * kp;
+  const bool bmn = tf32_bmn();
+  if (kp > 0 && !presplit) launch_split(dev_leaves, host_leaves, count, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, st, bmn);
   static const int cfg = [] {
-    // 0: BK 32 / 2 stages (default), 1: BK 16 / 4 stages; +2: 16 epilogue warps instead of 8.
-    // Measured at C5 FP32 (sw_power_cap): cfg 0 255.9 ms at 1537 MHz, cfg 1 296.8 ms at 1372,
-    // cfg 3 312.7 ms at 1290 (its tensor pipe is busier per cycle, 84.9 vs 76.9 %, but the
-    // power cap takes it back in clock)
+    // 0: BK 32 / 2 stages (default), 1: BK 16 / 4 stages.  Measured at C5 FP32 (sw_power_cap):
+    // cfg 0 255.9 ms at 1537 MHz, cfg 1 296.8 ms at 1372 (its tensor pipe is busier per cycle but
+    // the power cap takes it back in clock); 16 instead of 8 epilogue warps: 312.7 ms at 1290
+    // (profiles/r02_tf32_persistent.md)
     const char* e = getenv("FMM_TF32_CFG");
     return e ? atoi(e) : 0;
   }();
   const int ck = tf32_chunk_k();
-  switch (cfg) {
-    case 1: return launch_k2p<16, 4, 8>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st);
-    case 2: return launch_k2p<32, 2, 16>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st);
-    case 3: return launch_k2p<16, 4, 16>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st);
-    default: return launch_k2p<32, 2, 8>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st);
-  }
+  if (cfg == 1)
+    return bmn ? launch_k2p<16, 4, 8, true>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st)
+               : launch_k2p<16, 4, 8, false>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st);
+  return bmn ? launch_k2p<32, 2, 8, true>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st)
+             : launch_k2p<32, 2, 8, false>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st);
 }
 
 }  // namespace fmm

@@ -21,7 +21,7 @@ namespace fmm {
 namespace {
 // K1X2 launch: grid x = column chunks of kThreadsX2 vectors, y = row groups of RPB grandchild
 // rows, z = node (S nodes use the U tables, T nodes the V tables).
-template <typename T, int VEC, int RPB, int RA, int RB>
+template <typename T, int VEC, int RPB, int RA, int RB, bool SPLIT = false>
 __global__ void __launch_bounds__(kThreadsX2) k1x2_lincomb(const K1x2Node* __restrict__ nodes,
                                                             Bases bases) {
   __shared__ T* optr[kMaxX2];
@@ -43,8 +43,8 @@ __global__ void __launch_bounds__(kThreadsX2) k1x2_lincomb(const K1x2Node* __res
   for (int ii = 0; ii < RPB; ++ii) {
     const int64_t i = i0 + ii;
     if (i >= rows) break;
-    if (tv) k1x2_row<T, VEC, RA, RB, 1>(in, ldi, rows, cols, i, jv, optr);
-    else k1x2_row<T, VEC, RA, RB, 0>(in, ldi, rows, cols, i, jv, optr);
+    if (tv) k1x2_row<T, VEC, RA, RB, 1, SPLIT>(in, ldi, rows, cols, i, jv, optr, nd.lo_off);
+    else k1x2_row<T, VEC, RA, RB, 0, SPLIT>(in, ldi, rows, cols, i, jv, optr, nd.lo_off);
   }
 }
 
@@ -70,6 +70,12 @@ void k1x2_go_rpb(const Step& s, const K1x2Node* nd, const Bases& b, cudaStream_t
   const int64_t cv = (s.cols + VEC - 1) / VEC;
   dim3 grid((unsigned)((cv + kThreadsX2 - 1) / kThreadsX2), (unsigned)((s.rows + RPB - 1) / RPB),
             (unsigned)s.count);
+  if constexpr (sizeof(T) == 4) {
+    if (s.tf32_split) {
+      k1x2_lincomb<T, VEC, RPB, RA, RB, true><<<grid, kThreadsX2, 0, st>>>(nd, b);
+      return;
+    }
+  }
   k1x2_lincomb<T, VEC, RPB, RA, RB><<<grid, kThreadsX2, 0, st>>>(nd, b);
 }
 

@@ -262,11 +262,12 @@ __device__ __forceinline__ void lc_term(Vec<T, VEC>& acc, bool& started, uint32_
 constexpr int kThreadsX2 = 128;
 
 // Compile-time output structure of a K1X2 rule pair (RA at level d, RB at level d+1, table TV).
-template <int RA, int RB, int TV>
+// SPLIT: every (r1, r2) is formed (the tensor-core FP32 leaves' operand arena holds views too).
+template <int RA, int RB, int TV, bool SPLIT = false>
 struct X2Pair {
   static constexpr int R1 = builtin_R(RA), R2 = builtin_R(RB);
   static constexpr bool formed(int r1, int r2) {
-    return !(builtin_trivial(RA, TV, r1) && builtin_trivial(RB, TV, r2));
+    return SPLIT || !(builtin_trivial(RA, TV, r1) && builtin_trivial(RB, TV, r2));
   }
   static constexpr bool need2(int r1, int b2) {  // S_{r1}[b2] used by a formed output
     for (int r2 = 0; r2 < R2; ++r2)
@@ -329,10 +330,13 @@ __device__ __forceinline__ void lc_fixed(Vec<T, VEC>& acc, bool first, const Vec
 // form S_{r1}[i2] (level d) and every formed S_{r1 r2} (level d+1) from them, ascending
 // block order in both sums (the one-level K1's order).  All codes are constants, so the body is
 // only the loads, the adds and the stores.
-template <typename T, int VEC, int RA, int RB, int TV>
+// SPLIT (FP32 only): each output is written as its TF32 hi / lo pair (tf32_split), hi at
+// optr[idx] and lo lo_off elements further -- the leaf GEMM's operand arena.
+template <typename T, int VEC, int RA, int RB, int TV, bool SPLIT = false>
 __device__ __forceinline__ void k1x2_row(const T* __restrict__ in, int64_t ldi, int64_t rows,
-                                         int64_t cols, int64_t i, int64_t jv, T* const* optr) {
-  using X = X2Pair<RA, RB, TV>;
+                                         int64_t cols, int64_t i, int64_t jv, T* const* optr,
+                                         int64_t lo_off = 0) {
+  using X = X2Pair<RA, RB, TV, SPLIT>;
   Vec<T, VEC> x[4][4];  // x[i2][i1]
   static_for<4>([&](auto b1) {
     static_for<4>([&](auto b2) {
@@ -360,7 +364,16 @@ __device__ __forceinline__ void k1x2_row(const T* __restrict__ in, int64_t ldi, 
           if constexpr (X::code(RB, b2, r2) != 0u)
             lc_fixed<X::code(RB, b2, r2)>(acc, X::first(RB, b2, r2), y[b2]);
         });
-        st_vec<T, VEC>(optr[X::oidx(r1, r2)] + off, acc);
+        if constexpr (SPLIT) {
+          static_assert(sizeof(T) == 4, "the TF32 split is FP32-only");
+          Vec<T, VEC> hi, lo;
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) tf32_split(acc.v[e], hi.v[e], lo.v[e]);
+          st_vec<T, VEC>(optr[X::oidx(r1, r2)] + off, hi);
+          st_vec<T, VEC>(optr[X::oidx(r1, r2)] + lo_off + off, lo);
+        } else {
+          st_vec<T, VEC>(optr[X::oidx(r1, r2)] + off, acc);
+        }
       }
     });
   });

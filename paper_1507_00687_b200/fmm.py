@@ -47,6 +47,7 @@ SIGNATURES = {
     "fmm_plan_set_comm_mode": (_I, [_P, _I]),
     "fmm_rule_transform": (_I, [_P, _I, C.POINTER(_P)]),
     "fmm_plan_set_k1_levels": (_I, [_P, _I]),
+    "fmm_plan_set_leaf_split": (_I, [_P, _I]),
     "fmm_plan_sym_bytes": (_I, [_P, _P]),
     "fmm_plan_sym_alloc": (_I, [_P, _P]),
     "fmm_plan_sym_ptr": (_I, [_P, _P]),
@@ -324,6 +325,12 @@ class Plan:
     def set_k1_levels(self, levels: int = 2):
         """S / T formation: 2 = two recursion levels per K1 pass (K1X2, default), 1 = one."""
         _call("fmm_plan_set_k1_levels", self._h, int(levels))
+        self._ws = None
+
+    def set_leaf_split(self, in_pass: bool = True):
+        """FP32 tensor-core leaves: hi / lo operand split written by the leaf level's K1X2
+        (True, default where it applies) or by a separate split pass (False)."""
+        _call("fmm_plan_set_leaf_split", self._h, int(bool(in_pass)))
         self._ws = None
 
     def set_k3_levels(self, levels: int = 2):

@@ -66,3 +66,18 @@ def test_cpu_baseline_reports_parity_and_dd_errors():
     assert out["kind"] == "oracle" and out["parity_sampled"] == 0.0
     e = out["error_vs_dd"]
     assert e["gpu"] == e["oracle"] and 0.0 < e["gpu"] < 1e-13
+
+
+def test_tf32_split_counts(sw):
+    # FP32 tensor-core leaves, two levels, 4-byte elements
+    n, e = 1024, 4
+    s = (n // 4) ** 2
+    k3x2 = (49 + 16) * s
+    # split in the leaf level's K1X2: all 49 grandchildren formed (views too), hi + lo written,
+    # the 16 sub-blocks read once, per operand
+    in_pass = 2 * (16 + 2 * 49) * s
+    assert bench.pass_bytes([sw, sw], n, n, n, e, False, True, True, False, "pass") == (in_pass + k3x2) * e
+    # split kernel: the 40 formed grandchildren written by K1X2, then all 49 leaf operands read
+    # and their hi + lo written, per operand
+    kernel = 2 * (16 + 40) * s + 2 * 3 * 49 * s
+    assert bench.pass_bytes([sw, sw], n, n, n, e, False, True, True, False, "kernel") == (kernel + k3x2) * e

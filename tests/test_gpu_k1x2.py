@@ -185,3 +185,46 @@ def test_workspace_smaller(fb):
     ws2 = p.workspace_bytes()
     p.set_k1_levels(1)
     assert ws2 < p.workspace_bytes()
+
+
+@pytest.mark.parametrize("leaf", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("names,dims,sched", [
+    (("winograd",) * 2, (512, 512, 512), "auto"),
+    (("winograd",) * 3, (1024, 512, 768), "hybrid"),     # C5's schedule in miniature
+    (("winograd",) * 3, (1024, 512, 768), "depth"),
+    (("strassen",) * 4, (1024, 1024, 1024), "breadth"),
+    (("winograd", "classical222", "strassen"), (1024, 512, 1024), "auto"),  # C3's rules
+    (("winograd",) * 2, (512, 4 * 72, 4 * 90), "auto"),  # leaf k, n not multiples of 32
+])
+def test_leaf_split_in_pass(fb, leaf, names, dims, sched):
+    # FP32 tensor-core leaves: the leaf level's K1X2 writes every leaf
+    # operand's TF32 hi / lo pair straight into the GEMM's arena (views included) instead of
+    # S_r / T_r + a split kernel: the same elementwise split of the same sums, so bitwise the
+    # split-kernel path; and within the FP32 tolerance of the oracle
+    M, K, N = dims
+    lf = {"3xtf32": fb.fmm.LEAF_3XTF32, "tf32": fb.fmm.LEAF_TF32}[leaf]
+    A, B = fi.random_pair(M, K, N, seed=M + K, dtype=np.float32)
+    outs = []
+    for in_pass in (True, False):
+        p = fb.Plan([fb.Rule.builtin(n) for n in names], M, K, N, dtype="f32", leaf=lf)
+        p.set_schedule(sched)
+        p.set_leaf_split(in_pass)
+        outs.append(p.execute(dev(A), dev(B)).cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+    if leaf == "3xtf32":
+        Co = oracle.fmm(A, B, OPlan.uniform([R.builtin(n) for n in names]))
+        assert oracle.parity_metric(outs[0], Co, np.abs(A).max(), np.abs(B).max(), K) <= TOL32
+
+
+def test_leaf_split_in_pass_partition(fb):
+    # virtual ranks of a multi-GPU partition: each rank's partial is the split-kernel path's
+    A, B = fi.random_pair(1024, 512, 512, seed=9, dtype=np.float32)
+    for rank in range(3):
+        outs = []
+        for in_pass in (True, False):
+            p = fb.Plan([fb.Rule.builtin("winograd")] * 3, 1024, 512, 512, dtype="f32",
+                        leaf=fb.fmm.LEAF_3XTF32)
+            p.set_partition(rank, 3)
+            p.set_leaf_split(in_pass)
+            outs.append(p.execute(dev(A), dev(B)).cpu().numpy())
+        assert np.array_equal(outs[0], outs[1])
