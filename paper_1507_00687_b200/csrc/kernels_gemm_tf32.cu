@@ -374,251 +374,6 @@ __global__ void __launch_bounds__(EpiCfg<EW>::THREADS, 1)
                  "r"(2 * TMEM_COLS));
 }
 
-// ---- the CTA-pair form (cta_group::2) ---------------------------------------------------------
-// One cluster of 2 CTAs on the two SMs of a TPC owns a 256 x 256 output tile: CTA c holds rows
-// 128 c .. +127 of A (hi / lo) and columns 128 c .. +127 of B (hi / lo, MN-major) in its shared
-// memory, and rows 128 c .. +127 of the accumulator in its TMEM; the leader (rank 0) issues
-// tcgen05.mma.cta_group::2 (M = 256, N = 256, K = 8), which reads the A halves and both B halves
-// across the pair.  Per SM that is 64 KB of operand stage per 32-deep k-tile instead of 96 KB
-// (B is shared), so 3 stages fit.  Both producers load into their own shared memory and signal
-// the leader's `full` barrier (.cta_group::2 TMA; the leader expects both CTAs' bytes); the
-// leader's commits arrive on both CTAs' `empty` / `acc_full` barriers (multicast); both
-// epilogues drain their own TMEM rows into register totals exactly as k2p_tf32 does and arrive
-// on the leader's `acc_empty`.
-constexpr uint32_t IDESC_BMN_M256 =
-    (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-// shared::cluster address of the same shared-memory offset in CTA `rank` of the cluster
-__device__ __forceinline__ uint32_t peer_addr(uint32_t a, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(a), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1,
-                                                 int c2, uint32_t bar_leader) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_leader)
-      : "memory");
-}
-__device__ __forceinline__ void mma_tf32_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(IDESC_BMN_M256), "r"(acc));
-}
-__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {  // arrive on bar in both CTAs
-  asm volatile(
-      "{\n .reg .b16 msk;\n mov.b16 msk, 3;\n"
-      " tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], msk;\n}\n" ::"r"(bar)
-      : "memory");
-}
-
-template <int BK, int STAGES>
-struct PairCfg {
-  static constexpr int A_B = 128 * BK * 4, B_B = 128 * BK * 4;  // per CTA: 128 rows, 128 columns
-  static constexpr int STAGE = 2 * A_B + 2 * B_B;
-  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
-  static_assert(SMEM <= 227 * 1024, "smem");
-};
-
-template <int BK, int STAGES>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<8>::THREADS, 1)
-    k2p2_tf32(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
-              const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
-              const LeafNode* __restrict__ leaves, Bases bases, int64_t m, int64_t n, int64_t kp,
-              int tiles_m, int tiles_n, int group_m, int total, int passes, int chunk_kt) {
-  using CF = PairCfg<BK, STAGES>;
-  constexpr int A_BYTES = CF::A_B, B_BYTES = CF::B_B, STAGE_BYTES = CF::STAGE;
-  constexpr int EW = 8, ECOLS = EpiCfg<EW>::ECOLS;
-  constexpr int PM = 256, PN = 256;  // pair tile
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
-  // bars: [0,S) full (leader's counts), [S,2S) empty, [2S,2S+2) acc_full, [2S+2,2S+4) acc_empty
-  // (leader's counts); then the TMEM base
-  uint32_t* tmem_slot = (uint32_t*)(bars + 2 * STAGES + 4);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int tiles = tiles_m * tiles_n;
-  const int KT = (int)(kp / BK);
-  const int nch = (KT + chunk_kt - 1) / chunk_kt;
-
-  if (warp == 0 && lane == 0) {
-    for (int s2 = 0; s2 < STAGES; ++s2) {
-      mbar_init(su32(&bars[s2]), 1);            // the leader's expect_tx arrival
-      mbar_init(su32(&bars[STAGES + s2]), 1);   // the leader's multicast commit
-    }
-    for (int b2 = 0; b2 < 2; ++b2) {
-      mbar_init(su32(&bars[2 * STAGES + b2]), 1);           // multicast commit
-      mbar_init(su32(&bars[2 * STAGES + 2 + b2]), 2 * EW);  // one lane per epilogue warp, both CTAs
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                     su32(tmem_slot)),
-                 "r"(2 * TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  cluster_sync_all();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t tmem = *tmem_slot;
-
-  auto coords = [&](int t, int& leaf, int& m0, int& n0) {  // pair tile origin
-    leaf = t / tiles;
-    const int tt = t % tiles;
-    const int per_group = group_m * tiles_n;
-    const int g0 = (tt / per_group) * group_m;
-    const int gsz = min(tiles_m - g0, group_m);
-    const int w = tt % per_group;
-    m0 = (g0 + w % gsz) * PM;
-    n0 = (w / gsz) * PN;
-  };
-
-  if (warp == 0) {
-    if (lane == 0) {  // ---- TMA producer (both CTAs: own halves, the leader's full barrier) ----
-      const uint32_t full0 = su32(&bars[0]) & 0xFEFFFFFFu;  // the leader's barrier array
-      int it = 0;
-      for (int t = pair; t < total; t += npairs) {
-        int leaf, m0, n0;
-        coords(t, leaf, m0, n0);
-        const int ma = m0 + 128 * (int)rank, nb = n0 + 128 * (int)rank;
-        for (int kt = 0; kt < KT; ++kt, ++it) {
-          const int s2 = it % STAGES;
-          mbar_wait(su32(&bars[STAGES + s2]), ((uint32_t)(it / STAGES) & 1u) ^ 1u);
-          uint8_t* st = smem + s2 * STAGE_BYTES;
-          const uint32_t full = full0 + (uint32_t)(s2 * 8);
-          const int kc = kt * BK;
-          if (rank == 0) mbar_expect_tx(su32(&bars[s2]), 2u * (passes == 3 ? STAGE_BYTES : A_BYTES + B_BYTES));
-          tma_load_3d_pair(su32(st), &ta_hi, kc, ma, leaf, full);
-          if (passes == 3) tma_load_3d_pair(su32(st + A_BYTES), &ta_lo, kc, ma, leaf, full);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            tma_load_3d_pair(su32(st + 2 * A_BYTES + j * 128 * BK), &tb_hi, nb + 32 * j, kc, leaf, full);
-            if (passes == 3)
-              tma_load_3d_pair(su32(st + 2 * A_BYTES + B_BYTES + j * 128 * BK), &tb_lo, nb + 32 * j, kc, leaf, full);
-          }
-        }
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {  // ---- MMA issuer: the leader only ----
-      int it = 0, g = 0;
-      for (int t = pair; t < total; t += npairs) {
-        for (int c = 0; c < nch; ++c, ++g) {
-          const int buf = g & 1;
-          mbar_wait(su32(&bars[2 * STAGES + 2 + buf]), (uint32_t)((g >> 1) & 1) ^ 1u);
-          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-          const uint32_t acc = tmem + (uint32_t)(buf * TMEM_COLS);
-          const int kt0 = c * chunk_kt, kt1 = min(KT, kt0 + chunk_kt);
-          for (int kt = kt0; kt < kt1; ++kt, ++it) {
-            const int s2 = it % STAGES;
-            mbar_wait(su32(&bars[s2]), (uint32_t)(it / STAGES) & 1u);
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            uint8_t* st = smem + s2 * STAGE_BYTES;
-            const uint64_t a_hi = desc_k<BK>(su32(st)), a_lo = desc_k<BK>(su32(st + A_BYTES));
-            const uint64_t b_hi = desc_mn<BK>(su32(st + 2 * A_BYTES));
-            const uint64_t b_lo = desc_mn<BK>(su32(st + 2 * A_BYTES + B_BYTES));
-#pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint64_t off = (uint64_t)((kk * 32) >> 4);
-              const uint64_t offb = (uint64_t)((kk * 8 * 128) >> 4);
-              const uint32_t first = (kt == kt0 && kk == 0) ? 0u : 1u;
-              if (passes == 3) {  // small terms first
-                mma_tf32_pair(acc, a_lo + off, b_hi + offb, first);
-                mma_tf32_pair(acc, a_hi + off, b_lo + offb, 1u);
-                mma_tf32_pair(acc, a_hi + off, b_hi + offb, 1u);
-              } else {
-                mma_tf32_pair(acc, a_hi + off, b_hi + offb, first);
-              }
-            }
-            mma_commit_pair(su32(&bars[STAGES + s2]));  // both CTAs' stage s2 free
-          }
-          mma_commit_pair(su32(&bars[2 * STAGES + buf]));  // chunk complete in both TMEMs
-        }
-      }
-    }
-  } else if (warp >= 4) {  // ---- epilogue (both CTAs): own TMEM rows -> register totals ----
-    const int q = warp & 3, h = (warp - 4) >> 2;
-    const uint32_t empty_leader = peer_addr(su32(&bars[2 * STAGES + 2]), 0);
-    int g = 0;
-    for (int t = pair; t < total; t += npairs) {
-      int leaf, m0, n0;
-      coords(t, leaf, m0, n0);
-      float tot[ECOLS];
-#pragma unroll
-      for (int e = 0; e < ECOLS; ++e) tot[e] = 0.f;
-      for (int c = 0; c < nch; ++c, ++g) {
-        const int buf = g & 1;
-        mbar_wait(su32(&bars[2 * STAGES + buf]), (uint32_t)((g >> 1) & 1));
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint32_t tbase =
-            tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * TMEM_COLS + h * ECOLS);
-#pragma unroll
-        for (int cb = 0; cb < ECOLS / 16; ++cb) {
-          uint32_t v[16];
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-              "%13,%14,%15}, [%16];\n"
-              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
-                "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-              : "r"(tbase + (uint32_t)(cb * 16)));
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-          if (c == 0) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) tot[cb * 16 + e] = __uint_as_float(v[e]);
-          } else {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) tot[cb * 16 + e] = __fadd_rn(tot[cb * 16 + e], __uint_as_float(v[e]));
-          }
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-        __syncwarp();
-        if (lane == 0)
-          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(
-                           empty_leader + (uint32_t)(buf * 8))
-                       : "memory");
-      }
-      const int64_t row = m0 + 128 * (int)rank + q * 32 + lane;
-      if (row < m) {
-        const LeafNode& lf = leaves[leaf];
-        int64_t ldc;
-        float* Cp = op_ptr<float>(bases, lf.c, ldc);
-        const int64_t cbase = n0 + h * ECOLS;
-        float* crow = Cp + row * ldc + cbase;
-        if (((((uintptr_t)crow) & 15u) == 0) && (cbase + ECOLS <= n)) {
-#pragma unroll
-          for (int e = 0; e < ECOLS; e += 4)
-            *reinterpret_cast<float4*>(crow + e) = make_float4(tot[e], tot[e + 1], tot[e + 2], tot[e + 3]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < ECOLS; ++e)
-            if (cbase + e < n) crow[e] = tot[e];
-        }
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-  cluster_sync_all();
-  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  if (warp == 2)
-    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
-                 "r"(2 * TMEM_COLS));
-}
-
 // S (m x k, via the leaf's a operand) -> hi, lo (m x kp); T (k x n) -> hi^T, lo^T (n x kp).
 // grid: x = kp / 32, y = ceil(rows / 32), z = leaf; block 32 x 8.
 __global__ void k_split_tf32(const LeafNode* __restrict__ leaves, Bases bases, int64_t m,
@@ -884,35 +639,6 @@ cudaError_t launch_k2p(float* a_hi, float* a_lo, float* b_hi, float* b_lo, const
   return cudaGetLastError();
 }
 
-template <int BK, int STAGES>
-cudaError_t launch_k2p2(float* a_hi, float* a_lo, float* b_hi, float* b_lo, const LeafNode* dev_leaves,
-                        int count, int64_t m, int64_t n, int64_t kp, const Bases& b, int passes,
-                        int chunk_k, cudaStream_t st) {
-  using CF = PairCfg<BK, STAGES>;
-  CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
-  const int64_t kpe = kp > 0 ? kp : TBK;
-  const int64_t np = (n + 31) / 32 * 32;
-  if (!make_map(&ma_hi, a_hi, kpe, m, count, 128, BK) || !make_map(&ma_lo, a_lo, kpe, m, count, 128, BK) ||
-      !make_map_mn(&mb_hi, b_hi, np, kpe, count, BK) || !make_map_mn(&mb_lo, b_lo, np, kpe, count, BK))
-    return cudaErrorInvalidValue;
-  const int tiles_m = (int)((m + 255) / 256), tiles_n = (int)((n + 255) / 256);
-  const int64_t total = (int64_t)tiles_m * tiles_n * count;
-  if (total > INT32_MAX) return cudaErrorInvalidValue;
-  const int pairs = (int)std::min<int64_t>(total, num_sms() / 2);
-  const int chunk_kt = std::max(1, chunk_k / BK);
-  static const int group_m = [] {
-    const char* e = getenv("FMM_TF32_GROUP_M");
-    const int v = e ? atoi(e) : 8;
-    return v >= 1 ? v : 8;
-  }();
-  cudaError_t e = cudaFuncSetAttribute(k2p2_tf32<BK, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
-  if (e != cudaSuccess) return e;
-  k2p2_tf32<BK, STAGES><<<2 * pairs, EpiCfg<8>::THREADS, CF::SMEM, st>>>(
-      ma_hi, ma_lo, mb_hi, mb_lo, dev_leaves, b, m, n, kp, tiles_m, tiles_n, group_m, (int)total, passes,
-      chunk_kt);
-  return cudaGetLastError();
-}
-
 }  // namespace
 
 // hi / lo arena: A side m x kp (K-major), B side kp x np (MN-major, np = n rounded up to 32) or
@@ -966,12 +692,8 @@ cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, i
     return e ? atoi(e) : 0;
   }();
   const int ck = tf32_chunk_k();
-  static const bool pair = [] {  // FMM_TF32_PAIR=1: the CTA-pair (cta_group::2) kernel
-    const char* e = getenv("FMM_TF32_PAIR");
-    return e ? atoi(e) != 0 : false;
-  }();
-  if (pair && bmn)
-    return launch_k2p2<32, 3>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st);
+  // a CTA-pair form (tcgen05.mma.cta_group::2, 256 x 256 tiles over a TPC, 3 stages) was built
+  // and measured 7 % slower under the power cap (profiles/r02_tf32_persistent.md); removed
   if (cfg == 1)
     return bmn ? launch_k2p<16, 4, 8, true>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st)
                : launch_k2p<16, 4, 8, false>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st);
