@@ -645,7 +645,8 @@ cudaError_t launch_k2p(float* a_hi, float* a_lo, float* b_hi, float* b_lo, const
 // n x kp (K-major); kp = k rounded up to 32
 size_t tf32_arena_floats(int64_t count, int64_t m, int64_t n, int64_t k) {
   const int64_t kp = (k + TBK - 1) / TBK * TBK, np = (n + 31) / 32 * 32;
-  return (size_t)count * (size_t)(2 * m * kp + 2 * np * kp);
+  // k = 0: no operand is read, but the kernel's tensor maps still need a (tiny) valid base
+  return std::max<size_t>((size_t)count * (size_t)(2 * m * kp + 2 * np * kp), 1024);
 }
 
 // B operand layout of the FP32 tensor-core leaf: FMM_TF32_BMN = 1 (default) MN-major (T as

@@ -292,6 +292,38 @@ def test_empty_and_degenerate(fb):
     assert np.array_equal(run(fb, ("strassen",) * 3, I, I), I)
 
 
+@pytest.mark.parametrize("leaf", ["3xtf32", "tf32"])
+def test_tf32_empty_and_degenerate(fb, leaf):
+    # FP32 tensor-core leaves: an empty inner dimension gives C = 0 (no chunk reaches TMEM, the
+    # epilogue stores zeros); an empty plan is a no-op; a leaf GEMM of one row / one column and
+    # identity operands are exact (products of TF32-exact values, sums of zeros)
+    lf = {"3xtf32": fb.fmm.LEAF_3XTF32, "tf32": fb.fmm.LEAF_TF32}[leaf]
+    w = fb.Rule.builtin("winograd")
+    p = fb.Plan([w, w], 64, 0, 96, dtype="f32", leaf=lf)
+    Cg = p.execute(torch.empty((64, 0), dtype=torch.float32, device="cuda"),
+                   torch.empty((0, 96), dtype=torch.float32, device="cuda"))
+    assert Cg.shape == (64, 96) and torch.all(Cg == 0)
+    Cg = fb.gemm(torch.empty((5, 0), dtype=torch.float32, device="cuda"),
+                 torch.empty((0, 7), dtype=torch.float32, device="cuda"), leaf=lf)
+    assert torch.all(Cg == 0)
+    p = fb.Plan([w], 0, 8, 8, dtype="f32", leaf=lf)
+    p.execute(torch.empty((0, 8), dtype=torch.float32, device="cuda"),
+              torch.zeros((8, 8), dtype=torch.float32, device="cuda"))
+    I = np.eye(256, dtype=np.float32)
+    X = fi.random_pair(256, 256, 256, seed=3, dtype=np.float32)[0]
+    # multiples of 1/8 in [-1, 1]: every S / T sum (<= 16 terms) and product stays TF32-exact
+    X = (np.round(X * 8) / 8).astype(np.float32)
+    for names in (("winograd",) * 2, ("strassen",) * 3):
+        p = fb.Plan([fb.Rule.builtin(n) for n in names], 256, 256, 256, dtype="f32", leaf=lf)
+        assert np.array_equal(p.execute(dev(I), dev(X)).cpu().numpy(), run_exact_ref(I, X))
+    row = fb.gemm(dev(X[:1]), dev(I), leaf=lf).cpu().numpy()
+    assert np.array_equal(row, X[:1])
+
+
+def run_exact_ref(A, B):
+    return (A.astype(np.float64) @ B.astype(np.float64)).astype(np.float32)
+
+
 @pytest.mark.parametrize("schedule", ["breadth", "depth", "hybrid"])
 @pytest.mark.parametrize("dtype", ["f64", "f32"])
 def test_execute_host_overlapped(fb, schedule, dtype):
