@@ -162,6 +162,31 @@ __global__ void __launch_bounds__(kSmallThreads, 3) k_small_plan(SmallArgs a) {
   const int64_t gt = ((int64_t)(threadIdx.x >> 5) * nb + blockIdx.x) * 32 + (threadIdx.x & 31);
   const int64_t gs = (int64_t)nb * kSmallThreads;
   if (a.trace && gt == 0) a.trace[0] = gtimer();
+  // Descriptor prefetch: the operand pointers of this block's first leaf tile (phase 2) and the
+  // input pointers of a single K3X2 node (phase 3) are resolved now, by warp 3 (which has no
+  // phase-1 item at C1's sizes), so their dependent global loads overlap phase 1 instead of
+  // starting after the barriers.
+  __shared__ const double* s_pa;
+  __shared__ const double* s_pb;
+  __shared__ double* s_pc;
+  __shared__ int64_t s_ld[3];
+  __shared__ const double* s_k3in[kMaxX2];
+  constexpr int NIN = builtin_R(RA) * builtin_R(RB);
+  const int tiles = a.tiles_m * a.tiles_n;
+  if ((threadIdx.x >> 5) == 3) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0 && (int)blockIdx.x < a.nlf * tiles) {
+      const LeafNode& lf = a.lf[blockIdx.x / tiles];
+      s_pa = op_ptr<const double>(a.b, lf.a, s_ld[0]);
+      s_pb = op_ptr<const double>(a.b, lf.b, s_ld[1]);
+      s_pc = op_ptr<double>(a.b, lf.c, s_ld[2]);
+    }
+    if (a.nk3 == 1)
+      for (int q = lane; q < NIN; q += 32) {
+        int64_t l;
+        s_k3in[q] = op_ptr<const double>(a.b, a.k3[0].in[q], l);
+      }
+  }
   // ---- phase 1: S / T of levels 0 and 1 (K1X2), both nodes' items in one index space ------
   {
     for (int q = 0; q < a.nk1; ++q)
@@ -190,14 +215,21 @@ __global__ void __launch_bounds__(kSmallThreads, 3) k_small_plan(SmallArgs a) {
   {
     double* As = smem;
     double* Bs = smem + SCfg::STAGES * SCfg::A_STAGE;
-    const int tiles = a.tiles_m * a.tiles_n;
     for (int w = blockIdx.x; w < a.nlf * tiles; w += nb) {
-      const LeafNode& lf = a.lf[w / tiles];
       const int tile = w % tiles;
       int64_t lda, ldb, ldc;
-      const double* A = op_ptr<const double>(a.b, lf.a, lda);
-      const double* B = op_ptr<const double>(a.b, lf.b, ldb);
-      double* Cp = op_ptr<double>(a.b, lf.c, ldc);
+      const double* A;
+      const double* B;
+      double* Cp;
+      if (w == (int)blockIdx.x) {  // prefetched
+        A = s_pa; B = s_pb; Cp = s_pc;
+        lda = s_ld[0]; ldb = s_ld[1]; ldc = s_ld[2];
+      } else {
+        const LeafNode& lf = a.lf[w / tiles];
+        A = op_ptr<const double>(a.b, lf.a, lda);
+        B = op_ptr<const double>(a.b, lf.b, ldb);
+        Cp = op_ptr<double>(a.b, lf.c, ldc);
+      }
       leaf_tile<VEC>(As, Bs, A, lda, B, ldb, Cp, ldc, a.m, a.n, a.k,
                      (int64_t)(tile / a.tiles_n) * SCfg::BM, (int64_t)(tile % a.tiles_n) * SCfg::BN);
     }
@@ -208,14 +240,15 @@ __global__ void __launch_bounds__(kSmallThreads, 3) k_small_plan(SmallArgs a) {
   // ---- phase 3: the W-combination of levels 1 and 0 (K3X2) ---------------------------------
   for (int q = 0; q < a.nk3; ++q) {
     const K3x2Node& nd = a.k3[q];
-    constexpr int NIN = builtin_R(RA) * builtin_R(RB);
-    const double* const* iptr = optr[0];
-    __syncthreads();
-    if (threadIdx.x < NIN) {
-      int64_t l;
-      optr[0][threadIdx.x] = op_ptr<double>(a.b, nd.in[threadIdx.x], l);
+    const double* const* iptr = a.nk3 == 1 ? s_k3in : optr[0];
+    if (a.nk3 != 1) {
+      __syncthreads();
+      if (threadIdx.x < NIN) {
+        int64_t l;
+        optr[0][threadIdx.x] = op_ptr<double>(a.b, nd.in[threadIdx.x], l);
+      }
+      __syncthreads();
     }
-    __syncthreads();
     int64_t ldo;
     double* out = op_ptr<double>(a.b, nd.out, ldo);
     const int64_t cv = nd.cols / V;

@@ -74,6 +74,23 @@ def test_leaf_gemm_f64_unaligned_ld(fb):
     assert parity(Cg, oracle.fmm(A, B, OPlan([])), A, B) <= TOL64
 
 
+@pytest.mark.parametrize("leaf", ["3xtf32", "native"])
+def test_leaf_gemm_f32_unaligned_ld(fb, leaf):
+    # operands whose rows are not 16-byte aligned (ld % 4 != 0): the scalar split path of the
+    # tensor-core leaf; an output with ld > n
+    lf = {"3xtf32": fb.fmm.LEAF_3XTF32, "native": fb.fmm.LEAF_NATIVE}[leaf]
+    A, B = fi.random_pair(100, 70, 90, seed=1, dtype=np.float32)
+    Ab = torch.zeros((100, 71), dtype=torch.float32, device="cuda")
+    Ab[:, :70] = dev(A)
+    Bb = torch.zeros((70, 93), dtype=torch.float32, device="cuda")
+    Bb[:, :90] = dev(B)
+    Cb = torch.full((100, 97), float("nan"), dtype=torch.float32, device="cuda")
+    fb.gemm(Ab[:, :70], Bb[:, :90], leaf=lf, C_out=Cb[:, :90])
+    Cg = Cb.cpu().numpy()
+    assert parity(Cg[:, :90], oracle.fmm(A, B, OPlan([])), A, B) <= TOL32
+    assert np.all(np.isnan(Cg[:, 90:]))  # nothing written past n
+
+
 def test_leaf_gemm_f32(fb):
     A, B = fi.random_pair(200, 300, 100, seed=3, dtype=np.float32)
     Cg = fb.gemm(dev(A), dev(B)).cpu().numpy()
