@@ -223,6 +223,20 @@ def scaling_config(mode: str):
     return None if mode == "none" else {"mode": mode, "tau": 1.0, "max_steps": 20, "pow2": 1}
 
 
+def default_shard(nranks: int, levels: int):
+    """(shard depth, unit order) for `nranks` ranks, from the per-rank compute of every rank's
+    partition timed on one B200 at C5 (tools/partition_times.py, profiles/r02_partition_times.md;
+    one-GPU time / (P x slowest rank)): 2 ranks: depth 2 in blocks 0.943 (round-robin 0.924);
+    4: depth 3 in blocks 0.913 (depth 2 round-robin 0.862); 8: depth 3 in blocks 0.895 (the 7
+    top-level products 0.855).  Blocks keep a rank's units on shared upper-level paths, so it
+    repeats fewer S / T formation passes."""
+    if nranks <= 1:
+        return 1, "cyclic"
+    if nranks == 2:
+        return min(2, levels), "block"
+    return min(3, levels), "block"
+
+
 def make_plan(fb, cfg: str, dtype: str = "f64", leaf=None, scaling: str = "none"):
     """The plan bench.py times for BASELINE config `cfg` (also used by the full-size parity
     tests, so they check exactly this launch configuration)."""
@@ -528,15 +542,19 @@ def run_fmm(args):
     torch.cuda.synchronize()
 
     plan = make_plan(fb, args.config, args.dtype, leaf, args.scaling)
-    if args.shard_depth <= 0:  # auto: 49 depth-2 units balance 2 and 4 ranks (98 / 94 % vs
-        # 87.5 % with the 7 top-level products); 8 ranks gain nothing from depth 2 (7 / 6.125);
-        # the fused NVLink combine works on the top-level products (depth 1)
-        args.shard_depth = 2 if ws in (2, 4) and args.comm != "p2p" else 1
+    shard_order = "cyclic" if args.shard_order == "auto" else args.shard_order
+    if args.shard_depth <= 0:  # auto (default_shard); the fused NVLink combine works on the
+        # top-level products (depth 1), laid out round-robin
+        args.shard_depth, auto_order = default_shard(ws, len(rules)) if args.comm != "p2p" else (1, "cyclic")
+        if args.shard_order == "auto":
+            shard_order = auto_order
     # --comm-one-rank: a one-rank NCCL communicator at N = 1, so the exchange (the collective,
     # or mode 3's barriers and combine) really runs on a single GPU
     use_comm = ws > 1 or args.comm_one_rank
     if ws > 1 and args.shard_depth > 1:
         plan.set_shard_depth(args.shard_depth)
+    if ws > 1 and shard_order != "cyclic":
+        plan.set_shard_order(shard_order)
     if use_comm and args.comm != "reduce":
         plan.set_comm_mode(args.comm)
     if use_comm:
@@ -777,7 +795,9 @@ def run_fmm(args):
                                    f"(BASELINE configs[{ {'C1': 0, 'C2': 1, 'C2c': 1, 'C3': 2, 'C4': 3, 'C5': 4}[args.config] }])"
                                    + (f", scaling {args.scaling} (pow2, tau=1)" if args.scaling != "none" else ""),
                        "parallelism": (f"top-level r round-robin over {ws} GPU(s)" if args.shard_depth <= 1
-                                       else f"depth-{args.shard_depth} paths round-robin over {ws} GPU(s)")
+                                       else f"depth-{args.shard_depth} paths "
+                                       f"{'in contiguous blocks' if shard_order == 'block' else 'round-robin'}"
+                                       f" over {ws} GPU(s)")
                                       + (f", {args.comm} of C" if use_comm else ""),
                        "l2": ("operands %.1f GiB each > 126 MB L2 (no flush needed)" % (M * K * esz / 2**30))
                   if not small else "L2 flushed (256 MB write) between timed steps, outside the events",
@@ -812,7 +832,10 @@ def main():
                     choices=["none", "outside", "inside", "out_in", "in_out", "repeated"])
     ap.add_argument("--shard-depth", type=int, default=0,
                     help="multi-GPU units = paths of the first d levels (fmm_plan_set_shard_depth); "
-                         "0 = auto (2 for 2 or 4 ranks, else 1)")
+                         "0 = auto (bench.default_shard: 2 at 2 ranks, 3 at more)")
+    ap.add_argument("--shard-order", default="auto", choices=["auto", "cyclic", "block"],
+                    help="multi-GPU unit order (fmm_plan_set_shard_order); auto = with the auto depth, "
+                         "blocks, else round-robin")
     ap.add_argument("--comm", default="reduce", choices=["reduce", "allreduce", "reduce_scatter", "p2p"],
                     help="multi-GPU exchange (fmm_plan_set_comm_mode): NCCL on the partial C, or "
                          "p2p = the fused NVLink W-combination of the peers' top-level products")

@@ -225,6 +225,14 @@ fmm_status fmm_choose_variants(const fmm_rule* root, const fmm_rule* const* vari
  * 1 <= depth <= levels. */
 fmm_status fmm_plan_set_shard_depth(fmm_plan* plan, int depth);
 
+/* Unit order of the multi-GPU partition (host-only): order = 0 (default) round-robin, unit u on
+ * rank u mod nranks; order = 1 contiguous blocks, rank p owning units
+ * [ceil(p U / nranks), ceil((p + 1) U / nranks)) of the U units -- at shard depth >= 2 a rank's
+ * units then share their upper-level paths, so it repeats fewer S / T formation passes on the
+ * way down.  fmm_plan_owned reports the assignment.  FMM_E_ARG for other values;
+ * FMM_E_UNSUPPORTED together with comm mode 3 (its symmetric buffers are laid out round-robin). */
+fmm_status fmm_plan_set_shard_order(fmm_plan* plan, int order);
+
 /* The multi-GPU exchange after the ranks' partial products (host-only; default 0):
  * 0 = ncclReduce(sum) onto rank 0 (C valid on rank 0);
  * 1 = ncclAllReduce(sum) (C valid on every rank);

@@ -127,6 +127,7 @@ struct fmm_plan {
   int schedule = 0;  // 0 auto, 1 breadth-first, 2 depth-first top level
   int fusion = 2;    // W-combination of the leaves' parents in the leaf GEMM epilogue: 0 off, 1 on, 2 auto
   int shard_depth = 1;  // multi-GPU: units = paths of the first shard_depth levels, round-robin
+  bool shard_block = false;  // units to ranks in contiguous blocks (else round-robin u mod nranks)
   int comm_mode = 0;    // multi-GPU exchange: 0 reduce to rank 0, 1 all-reduce, 2 reduce-scatter
   bool split_chains = true;     // fused units' product chains split over CTAs (turnstiles)
   bool k1_two_level = true;     // S / T of two recursion levels formed in one pass (K1X2)
@@ -897,8 +898,13 @@ struct Builder {
   bool owns_subtree(int level, int64_t unit_prefix) const {
     if (p->nranks == 1) return true;
     const int64_t span = unit_span(level);  // units below this node
-    if (span >= p->nranks) return true;
     const int64_t u0 = unit_prefix * span;
+    if (p->shard_block) {  // rank p owns units [ceil(p U / P), ceil((p + 1) U / P))
+      const int64_t U = unit_span(0), P = p->nranks;
+      const int64_t lo = ((int64_t)p->rank * U + P - 1) / P, hi = ((int64_t)(p->rank + 1) * U + P - 1) / P;
+      return u0 < hi && u0 + span > lo;
+    }
+    if (span >= p->nranks) return true;
     for (int64_t u = u0; u < u0 + span; ++u)
       if (u % p->nranks == p->rank) return true;
     return false;
@@ -1473,6 +1479,10 @@ fmm_status fmm_plan_fused_launches(const fmm_plan* p, int64_t* n) {
 
 fmm_status fmm_plan_set_comm_mode(fmm_plan* p, int mode) {
   if (!p || mode < 0 || mode > 3) { set_error("fmm_plan_set_comm_mode: mode must be 0, 1, 2 or 3"); return FMM_E_ARG; }
+  if (mode == 3 && p->shard_block) {
+    set_error("fmm_plan_set_comm_mode: the fused NVLink combine (mode 3) needs round-robin units");
+    return FMM_E_UNSUPPORTED;
+  }
   const bool recompile = (mode == 3) != (p->comm_mode == 3);  // mode 3 changes the schedule
   p->comm_mode = mode;
   return recompile ? compile_plan(p) : FMM_OK;
@@ -1587,13 +1597,25 @@ fmm_status fmm_plan_set_shard_depth(fmm_plan* p, int depth) {
   return compile_plan(p);
 }
 
+fmm_status fmm_plan_set_shard_order(fmm_plan* p, int order) {
+  if (!p || order < 0 || order > 1) { set_error("fmm_plan_set_shard_order: order must be 0 or 1"); return FMM_E_ARG; }
+  if (order == 1 && p->comm_mode == 3) {
+    set_error("fmm_plan_set_shard_order: the fused NVLink combine (comm mode 3) needs round-robin units");
+    return FMM_E_UNSUPPORTED;
+  }
+  p->shard_block = order == 1;
+  return compile_plan(p);
+}
+
 fmm_status fmm_plan_owned(const fmm_plan* p, int rank, int nranks, int32_t* owned, int* R) {
   if (!p || nranks < 1 || rank < 0 || rank >= nranks) { set_error("fmm_plan_owned: bad args"); return FMM_E_ARG; }
   int64_t units = 1;
   for (int l = 0; l < p->shard_depth && l < p->L; ++l) units *= p->rules[p->node_rule[l][0]].R;
   if (R) *R = (int)units;
   if (owned)
-    for (int64_t u = 0; u < units; ++u) owned[u] = (p->L > 0 ? (u % nranks == rank) : (rank == 0)) ? 1 : 0;
+    for (int64_t u = 0; u < units; ++u)
+      owned[u] = (p->L > 0 ? (p->shard_block ? (u * nranks / units == rank) : (u % nranks == rank))
+                           : (rank == 0)) ? 1 : 0;
   return FMM_OK;
 }
 
@@ -2025,7 +2047,7 @@ static const fmm_plan* depth_first_twin(const fmm_plan* p) {
     t->Mp = p->Mp; t->Kp = p->Kp; t->Np = p->Np; t->padded = p->padded;
     t->rules = p->rules; t->node_rule = p->node_rule; t->lm = p->lm; t->lk = p->lk; t->ln = p->ln;
     t->scaling = p->scaling; t->coef_U = p->coef_U; t->coef_V = p->coef_V; t->coef_W = p->coef_W;
-    t->coef_host = p->coef_host; t->schedule = 2; t->fusion = p->fusion; t->shard_depth = p->shard_depth;
+    t->coef_host = p->coef_host; t->schedule = 2; t->fusion = p->fusion; t->shard_depth = p->shard_depth; t->shard_block = p->shard_block;
     t->split_chains = p->split_chains;
     t->k1_two_level = p->k1_two_level;
     t->tf32_presplit = p->tf32_presplit;

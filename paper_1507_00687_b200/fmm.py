@@ -48,6 +48,7 @@ SIGNATURES = {
     "fmm_rule_transform": (_I, [_P, _I, C.POINTER(_P)]),
     "fmm_plan_set_k1_levels": (_I, [_P, _I]),
     "fmm_plan_set_leaf_split": (_I, [_P, _I]),
+    "fmm_plan_set_shard_order": (_I, [_P, _I]),
     "fmm_plan_sym_bytes": (_I, [_P, _P]),
     "fmm_plan_sym_alloc": (_I, [_P, _P]),
     "fmm_plan_sym_ptr": (_I, [_P, _P]),
@@ -381,6 +382,12 @@ class Plan:
     def set_shard_depth(self, depth: int):
         """Multi-GPU units = paths of the first `depth` levels (fmm_plan_set_shard_depth)."""
         _call("fmm_plan_set_shard_depth", self._h, depth)
+        self._ws = None
+
+    def set_shard_order(self, order: str = "cyclic"):
+        """Multi-GPU unit order: "cyclic" (unit u on rank u mod P, default) or "block"
+        (contiguous blocks of units per rank)."""
+        _call("fmm_plan_set_shard_order", self._h, {"cyclic": 0, "block": 1}[order])
         self._ws = None
 
     def owned(self, rank: int, nranks: int):

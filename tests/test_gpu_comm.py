@@ -200,9 +200,11 @@ def oracle_partial(rules, A, B, depth, owned):
     return np.zeros((A.shape[0], B.shape[1]), A.dtype) if C is None else C
 
 
-@pytest.mark.parametrize("depth,nranks", [(1, 2), (1, 4), (2, 2), (2, 4), (2, 8), (3, 8)])
+@pytest.mark.parametrize("depth,nranks,order", [(1, 2, "cyclic"), (1, 4, "cyclic"), (2, 2, "cyclic"),
+                                               (2, 4, "cyclic"), (2, 8, "cyclic"), (3, 8, "cyclic"),
+                                               (2, 2, "block"), (3, 4, "block"), (3, 8, "block")])
 @pytest.mark.parametrize("K", [8, 256])  # K = 8: leaf inner dimension 1 (bitwise)
-def test_shard_partials_match_oracle_partials(fb, depth, nranks, K):
+def test_shard_partials_match_oracle_partials(fb, depth, nranks, order, K):
     M, N = 256, 192
     A, B = fi.random_pair(M, K, N, seed=40 + depth)
     names = ("winograd",) * 3
@@ -210,6 +212,7 @@ def test_shard_partials_match_oracle_partials(fb, depth, nranks, K):
     for rank in range(nranks):
         p = fb.Plan([fb.Rule.builtin(n) for n in names], M, K, N)
         p.set_shard_depth(depth)
+        p.set_shard_order(order)
         p.set_partition(rank, nranks)
         owned = p.owned(rank, nranks)
         part = exe(p, A, B)

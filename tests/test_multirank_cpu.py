@@ -78,13 +78,14 @@ def _partial_oracle_depth2(owned_units, A, B):
     return _combine(w, m1, A.shape[0] // 2, B.shape[1] // 2)
 
 
-def _worker_depth2(rank, world, port, out_q):
+def _worker_depth2(rank, world, port, out_q, order="cyclic"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_1507_00687_b200 as fb
     w = fb.Rule.builtin("winograd")
     plan = fb.Plan([w, w], 128, 128, 128)
     plan.set_shard_depth(2)
+    plan.set_shard_order(order)
     owned = plan.owned(rank, world)
     A, B = fi.random_pair(128, 128, 128, seed=22)
     part = torch.from_numpy(_partial_oracle_depth2(owned, A, B))
@@ -97,15 +98,17 @@ def _worker_depth2(rank, world, port, out_q):
     dist.destroy_process_group()
 
 
-def test_two_rank_depth2_units_and_reduce():
-    # finer sharding (fmm_plan_set_shard_depth(2)): 49 units, every one owned once; the ranks'
-    # partial sums reduced by a collective equal the full product within the parity tolerance
+@pytest.mark.parametrize("order", ["cyclic", "block"])
+def test_two_rank_depth2_units_and_reduce(order):
+    # finer sharding (fmm_plan_set_shard_depth(2)): 49 units, every one owned once (round-robin
+    # or in contiguous blocks); the ranks' partial sums reduced by a collective equal the full
+    # product within the parity tolerance
     import oracle
     from oracle import rules as R
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker_depth2, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker_depth2, args=(r, 2, port, q, order)) for r in range(2)]
     for p in procs:
         p.start()
     total, counts = q.get(timeout=300)
@@ -193,3 +196,26 @@ def test_two_rank_reduce_scatter_rows():
     full = oracle.fmm(A, B, R.Plan.stationary(R.winograd(), 2))
     C = np.vstack([got[0], got[1]])
     assert oracle.parity_metric(C, full, np.abs(A).max(), np.abs(B).max(), 128) <= 1e-13
+
+
+@pytest.mark.parametrize("depth,nranks", [(1, 2), (2, 3), (2, 8), (3, 4), (3, 8), (3, 7)])
+def test_block_unit_order(depth, nranks):
+    # fmm_plan_set_shard_order(1): rank p owns the contiguous units
+    # [ceil(p U / P), ceil((p + 1) U / P)) -- every unit exactly once, block sizes within one
+    import paper_1507_00687_b200 as fb
+    w = fb.Rule.builtin("winograd")
+    plan = fb.Plan([w, w, w], 64, 64, 64)
+    plan.set_shard_depth(depth)
+    plan.set_shard_order("block")
+    U = 7 ** depth
+    seen = []
+    for p in range(nranks):
+        own = plan.owned(p, nranks)
+        lo, hi = -(-p * U // nranks), -(-(p + 1) * U // nranks)
+        assert own == list(range(lo, hi))
+        seen += own
+    assert seen == list(range(U))
+    sizes = [len(plan.owned(p, nranks)) for p in range(nranks)]
+    assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(fb.fmm.FmmError):  # the fused NVLink combine lays buffers out round-robin
+        plan.set_comm_mode("p2p")
