@@ -479,7 +479,7 @@ struct Builder {
   // level's K1X2 (emit_k1x2 split mode)
   bool presplit_ok() const {
     const int64_t m = p->lm[p->L], k = p->lk[p->L], n = p->ln[p->L];
-    return p->dtype == FMM_F32 && p->leaf != FMM_LEAF_NATIVE && p->tf32_presplit && tf32_bmn() &&
+    return p->dtype == FMM_F32 && p->leaf != FMM_LEAF_NATIVE && p->tf32_presplit &&
            m > 0 && k > 0 && n > 0 && k % 32 == 0 && n % 32 == 0;
   }
   int64_t pending_arena = -1, pending_leaves = 0;  // a K1X2 split-mode arena for the next K2

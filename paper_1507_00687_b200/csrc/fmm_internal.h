@@ -286,8 +286,6 @@ cudaError_t launch_gemm_f32(const LeafNode* dev_leaves, const LeafNode* host_lea
                             float* arena, cudaStream_t st, bool presplit = false);
 // floats of workspace the tensor-core FP32 leaf needs for a batch (hi / lo operand arena)
 size_t tf32_arena_floats(int64_t count, int64_t m, int64_t n, int64_t k);
-// the FP32 tensor-core leaf reads B MN-major (T as stored; FMM_TF32_BMN, default on)
-bool tf32_bmn();
 
 // TF32 hi / lo split of an FP32 value: hi = x rounded to 10 mantissa bits (nearest, ties away),
 // lo = x - hi (exact); the split every producer of the tensor-core leaf operands uses

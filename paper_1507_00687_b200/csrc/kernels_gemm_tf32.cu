@@ -6,13 +6,16 @@
 // TMEM as lo_A.hi_B + hi_A.lo_B + hi_A.hi_B (small terms first).  A TF32-only leaf fails the
 // FP32 parity tolerance at C5; 3xTF32 passes with a wide margin.
 //
-// Two kernels per leaf batch:
-//   k_split_*     S (m x k) -> S_hi, S_lo (m x kp, K-major);  T (k x n) -> T_hi^T, T_lo^T
-//                 (n x kp, K-major, transposed through shared memory), kp = k rounded up to 32
-//                 with zero padding -- into a per-launch arena in the workspace;
+// Per leaf batch:
+//   k_split_*     S (m x k) -> S_hi, S_lo (m x kp, K-major);  T (k x n) -> T_hi, T_lo (kp x np,
+//                 as stored: the MMA reads B MN-major), kp / np = k / n rounded up to 32 with
+//                 zero padding -- into a per-launch arena in the workspace.  Where the leaf
+//                 level's S / T come from a two-level K1X2 pass and k, n are multiples of 32,
+//                 that pass writes the arena itself (fmm_plan_set_leaf_split) and no split runs;
 //   k2p_tf32      persistent (one CTA per SM, static round-robin over (leaf, 128 x 256 tile)
-//                 items): warp 0 = TMA producer (3-D tensor maps over the arena, 128-byte
-//                 swizzle), warp 1 = MMA issuer (one thread, tcgen05.mma.cta_group::1.kind::tf32,
+//                 items): warp 0 = TMA producer (3-D tensor maps over the arena: A 128-byte
+//                 swizzle, B 128-byte swizzle with 32-byte atoms), warp 1 = MMA issuer (one
+//                 thread, tcgen05.mma.cta_group::1.kind::tf32,
 //                 M = 128, N = 256, K = 8), warp 2 = TMEM owner, 8 epilogue warps.  The K range is
 //                 accumulated in chunks (default 128): the tensor core's FP32 adds truncate, so
 //                 each chunk's TMEM accumulator is drained into register totals with
@@ -33,12 +36,8 @@ namespace fmm {
 
 namespace {
 
-constexpr int TBM = 128, TBN = 256, TBK = 32, TSTAGES = 2;
-constexpr int A_BYTES = TBM * TBK * 4;  // 16 KB
-constexpr int B_BYTES = TBN * TBK * 4;  // 32 KB
-constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
-constexpr int SMEM_BYTES = TSTAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int TMEM_COLS = 256;
+constexpr int TBM = 128, TBN = 256, TBK = 32, TSTAGES = 2;  // tile, k-tile, smem stages
+constexpr int TMEM_COLS = 256;                                 // one 128 x 256 FP32 accumulator
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -72,20 +71,9 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       : "memory");
 }
 
-// UMMA shared-memory descriptor, K-major, 128-byte swizzle (8-row x 128-byte atoms, SBO = 1024)
-__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);  // start address [0,14)
-  d |= (uint64_t)1 << 16;                    // leading byte offset (unused for swizzled K-major)
-  d |= (uint64_t)(1024 >> 4) << 32;          // stride byte offset [32,46)
-  d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
-  d |= (uint64_t)2 << 61;                    // layout: SWIZZLE_128B
-  return d;
-}
-
-// instruction descriptor: D F32, A/B TF32, both K-major, N = TBN, M = TBM
-constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TBN >> 3) << 17) |
-                           ((uint32_t)(TBM >> 4) << 24);
+// instruction descriptor: D F32, A / B TF32, A K-major, B MN-major (bit 16), N = TBN, M = TBM
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 16) |
+                           ((uint32_t)(TBN >> 3) << 17) | ((uint32_t)(TBM >> 4) << 24);
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
@@ -103,64 +91,45 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
 // x = hi + lo exactly: hi = x rounded to TF32 (nearest, ties away), lo = x - hi (exact in FP32)
 __device__ __forceinline__ void split2(float x, float& h, float& l) { tf32_split(x, h, l); }
 
-// K-major UMMA descriptor for a BK-float-wide swizzled tile (BK = 32: SW128, BK = 16: SW64).
-template <int BK>
+// K-major UMMA descriptor for the A tile: rows of TBK = 32 floats (128 bytes), 128-byte swizzle
+// (8-row x 128-byte atoms, SBO = 1024 bytes)
 __device__ __forceinline__ uint64_t desc_k(uint32_t saddr) {
   uint64_t d = 0;
-  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)1 << 16;
-  d |= (uint64_t)((8 * BK * 4) >> 4) << 32;  // 8 rows x row bytes
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)(BK == 32 ? 2 : 4) << 61;  // SWIZZLE_128B / SWIZZLE_64B
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);  // start address
+  d |= (uint64_t)1 << 16;                    // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;          // stride byte offset: next 8 rows
+  d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                    // SWIZZLE_128B
   return d;
 }
 
-// MN-major UMMA descriptor for a B tile stored as BK k-rows of 128 bytes (32 n) per 32-column
-// atom, atoms 128 * BK bytes apart along n: the tf32 MN-major layout SWIZZLE_128B_BASE32B (32-byte
-// chunks XOR-ed with the k-row index mod 4, what TMA's SWIZZLE_128B_ATOM_32B writes); LBO = the
-// n-atom stride, SBO = 4 k-rows (512 bytes)
-template <int BK>
+// MN-major UMMA descriptor for the B tile, stored as TBK k-rows of 128 bytes (32 n) per
+// 32-column atom, atoms 128 * TBK bytes apart along n: the tf32 MN-major layout
+// SWIZZLE_128B_BASE32B (32-byte chunks XOR-ed with the k-row index mod 4, what TMA's
+// SWIZZLE_128B_ATOM_32B writes); LBO = the n-atom stride, SBO = 4 k-rows (512 bytes)
 __device__ __forceinline__ uint64_t desc_mn(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
-  d |= (uint64_t)((128 * BK) >> 4) << 16;  // leading byte offset: next 32-column atom
+  d |= (uint64_t)((128 * TBK) >> 4) << 16;  // leading byte offset: next 32-column atom
   d |= (uint64_t)(512 >> 4) << 32;         // stride byte offset: next 4 k-rows
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)1 << 61;                  // SWIZZLE_128B_BASE32B
   return d;
 }
 
-// instruction descriptor with B MN-major (bit 16: transpose B)
-constexpr uint32_t IDESC_BMN = IDESC | (1u << 16);
-
-__device__ __forceinline__ void mma_tf32_bmn(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t acc) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(a), "l"(b), "r"(IDESC_BMN), "r"(acc));
-}
-
-template <int BK, int STAGES>
-struct TCfg {
-  static constexpr int A_B = TBM * BK * 4, B_B = TBN * BK * 4;
-  static constexpr int STAGE = 2 * A_B + 2 * B_B;
-  static constexpr int SMEM = STAGES * STAGE + 1024 + 256;
-  static_assert(SMEM <= 227 * 1024, "smem");
-};
-
-// EW epilogue warps: EW / 4 per TMEM lane quadrant, each owning ECOLS = 1024 / EW columns
-template <int EW>
-struct EpiCfg {
-  static constexpr int THREADS = 32 * (4 + EW), ECOLS = 1024 / EW;
-  static_assert(EW == 8 || EW == 16, "epilogue warps");
-};
+constexpr int A_BYTES = TBM * TBK * 4, B_BYTES = TBN * TBK * 4;  // 16 KB, 32 KB (hi or lo)
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;
+constexpr int SMEM_BYTES = TSTAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+static_assert(SMEM_BYTES <= 227 * 1024, "smem");
+// 8 epilogue warps: two per TMEM lane quadrant, each owning ECOLS = 128 columns
+constexpr int EPI_WARPS = 8, K2P_THREADS = 32 * (4 + EPI_WARPS), ECOLS = 1024 / EPI_WARPS;
 
 // Persistent leaf-product kernel with chunked round-to-nearest accumulation.  Work items are the
 // (leaf, 128 x 256 tile) pairs, leaf-major; CTA b runs items b, b + G, b + 2G, ... (G = grid =
 // min(items, SMs), one CTA per SM).  Roles: warp 0 lane 0 = TMA producer over the flattened
 // (item, k-tile) sequence through a STAGES-deep ring of hi / lo A and B stages; warp 1 lane 0 =
 // the MMA issuer; warp 2 = TMEM owner (512 columns: two 128 x 256 FP32 chunk accumulators);
-// warps 4 .. 4 + EW - 1 = epilogue.  The K range of an item is cut into chunks of chunk_kt k-tiles; the
+// warps 4 .. 11 = epilogue.  The K range of an item is cut into chunks of chunk_kt k-tiles; the
 // tensor core accumulates one chunk into TMEM buffer (chunk# & 1) -- its FP32 adds truncate
 // -- and the epilogue drains that buffer into per-thread register totals with
 // round-to-nearest adds (tot = c_0, tot = tot + c_1, ...) while the MMAs of the next chunk run in
@@ -182,16 +151,13 @@ __device__ __forceinline__ void item_coords(int t, int tiles, int tiles_m, int t
   n0 = (w / gsz) * TBN;
 }
 
-template <int BK, int STAGES, int EW, bool BMN>
-__global__ void __launch_bounds__(EpiCfg<EW>::THREADS, 1)
+__global__ void __launch_bounds__(K2P_THREADS, 1)
     k2p_tf32(const __grid_constant__ CUtensorMap ta_hi, const __grid_constant__ CUtensorMap ta_lo,
              const __grid_constant__ CUtensorMap tb_hi, const __grid_constant__ CUtensorMap tb_lo,
              const LeafNode* __restrict__ leaves, Bases bases, int64_t m, int64_t n, int64_t kp,
              int tiles_m, int tiles_n, int group_m, int total, int passes, int chunk_kt) {
-  using CF = TCfg<BK, STAGES>;
-  constexpr int A_BYTES = CF::A_B, B_BYTES = CF::B_B, STAGE_BYTES = CF::STAGE;
+  constexpr int BK = TBK, STAGES = TSTAGES;
   const int tiles = tiles_m * tiles_n;
-  constexpr int ECOLS = EpiCfg<EW>::ECOLS, EPI_WARPS = EW;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE_BYTES);
@@ -223,15 +189,10 @@ __global__ void __launch_bounds__(EpiCfg<EW>::THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
-  // B tile: K-major (one box of BK x 256 rows of n) or MN-major (eight boxes of 32 n x BK k-rows,
-  // 128 * BK bytes apart)
+  // B tile, MN-major: eight boxes of 32 n x BK k-rows, 128 * BK bytes apart
   auto load_b = [&](uint8_t* dst, const CUtensorMap* map, int kc, int n0, int leaf, uint32_t full) {
-    if constexpr (BMN) {
 #pragma unroll
-      for (int j = 0; j < TBN / 32; ++j) tma_load_3d(su32(dst + j * 128 * BK), map, n0 + 32 * j, kc, leaf, full);
-    } else {
-      tma_load_3d(su32(dst), map, kc, n0, leaf, full);
-    }
+    for (int j = 0; j < TBN / 32; ++j) tma_load_3d(su32(dst + j * 128 * BK), map, n0 + 32 * j, kc, leaf, full);
   };
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer ----
@@ -275,32 +236,20 @@ __global__ void __launch_bounds__(EpiCfg<EW>::THREADS, 1)
             mbar_wait(su32(&bars[s]), (uint32_t)(it / STAGES) & 1u);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             uint8_t* st = smem + s * STAGE_BYTES;
-            const uint64_t a_hi = desc_k<BK>(su32(st)), a_lo = desc_k<BK>(su32(st + A_BYTES));
-            const uint64_t b_hi = BMN ? desc_mn<BK>(su32(st + 2 * A_BYTES)) : desc_k<BK>(su32(st + 2 * A_BYTES));
-            const uint64_t b_lo = BMN ? desc_mn<BK>(su32(st + 2 * A_BYTES + B_BYTES))
-                                      : desc_k<BK>(su32(st + 2 * A_BYTES + B_BYTES));
+            const uint64_t a_hi = desc_k(su32(st)), a_lo = desc_k(su32(st + A_BYTES));
+            const uint64_t b_hi = desc_mn(su32(st + 2 * A_BYTES));
+            const uint64_t b_lo = desc_mn(su32(st + 2 * A_BYTES + B_BYTES));
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint64_t off = (uint64_t)((kk * 32) >> 4);  // 8 tf32 = 32 bytes along K
-              // MN-major B: 8 k-rows of 128 bytes
-              const uint64_t offb = BMN ? (uint64_t)((kk * 8 * 128) >> 4) : off;
+              const uint64_t off = (uint64_t)((kk * 32) >> 4);        // A: 8 tf32 = 32 bytes along K
+              const uint64_t offb = (uint64_t)((kk * 8 * 128) >> 4);  // B: 8 k-rows of 128 bytes
               const uint32_t first = (kt == kt0 && kk == 0) ? 0u : 1u;
-              if constexpr (BMN) {
-                if (passes == 3) {  // small terms first
-                  mma_tf32_bmn(acc, a_lo + off, b_hi + offb, first);
-                  mma_tf32_bmn(acc, a_hi + off, b_lo + offb, 1u);
-                  mma_tf32_bmn(acc, a_hi + off, b_hi + offb, 1u);
-                } else {
-                  mma_tf32_bmn(acc, a_hi + off, b_hi + offb, first);
-                }
+              if (passes == 3) {  // small terms first
+                mma_tf32(acc, a_lo + off, b_hi + offb, first);
+                mma_tf32(acc, a_hi + off, b_lo + offb, 1u);
+                mma_tf32(acc, a_hi + off, b_hi + offb, 1u);
               } else {
-                if (passes == 3) {  // small terms first
-                  mma_tf32(acc, a_lo + off, b_hi + off, first);
-                  mma_tf32(acc, a_hi + off, b_lo + off, 1u);
-                  mma_tf32(acc, a_hi + off, b_hi + off, 1u);
-                } else {
-                  mma_tf32(acc, a_hi + off, b_hi + off, first);
-                }
+                mma_tf32(acc, a_hi + off, b_hi + offb, first);
               }
             }
             mma_commit(su32(&bars[STAGES + s]));  // stage s free once these MMAs complete
@@ -374,55 +323,30 @@ __global__ void __launch_bounds__(EpiCfg<EW>::THREADS, 1)
                  "r"(2 * TMEM_COLS));
 }
 
-// S (m x k, via the leaf's a operand) -> hi, lo (m x kp); T (k x n) -> hi^T, lo^T (n x kp).
-// grid: x = kp / 32, y = ceil(rows / 32), z = leaf; block 32 x 8.
-__global__ void k_split_tf32(const LeafNode* __restrict__ leaves, Bases bases, int64_t m,
-                             int64_t n, int64_t k, int64_t kp, float* __restrict__ a_hi,
-                             float* __restrict__ a_lo, float* __restrict__ b_hi,
-                             float* __restrict__ b_lo, int side) {
-  __shared__ float tile[32][33];
+// S (m x k, via the leaf's a operand) -> hi, lo (m x kp, zero columns k .. kp).
+// grid: x = kp / 32, y = ceil(m / 32), z = leaf; block 32 x 8.
+__global__ void k_split_a(const LeafNode* __restrict__ leaves, Bases bases, int64_t m, int64_t k,
+                          int64_t kp, float* __restrict__ a_hi, float* __restrict__ a_lo) {
   const LeafNode& lf = leaves[blockIdx.z];
   const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  if (side == 0) {  // A side: no transpose
-    int64_t lda;
-    const float* A = op_ptr<const float>(bases, lf.a, lda);
-    const size_t base = (size_t)blockIdx.z * (size_t)(m * kp);
-    for (int rr = ty; rr < 32; rr += 8) {
-      const int64_t r = r0 + rr, c = c0 + tx;
-      if (r >= m) continue;
-      const float x = (c < k) ? A[r * lda + c] : 0.f;
-      float h, l;
-      split2(x, h, l);
-      a_hi[base + r * kp + c] = h;
-      a_lo[base + r * kp + c] = l;
-    }
-  } else {  // B side: T (k x n) -> (n x kp); tile rows = n index, cols = k index
-    int64_t ldb;
-    const float* B = op_ptr<const float>(bases, lf.b, ldb);
-    const size_t base = (size_t)blockIdx.z * (size_t)(n * kp);
-    for (int rr = ty; rr < 32; rr += 8) {  // read T[c0 + rr][r0 + tx]
-      const int64_t kk = c0 + rr, nn = r0 + tx;
-      tile[rr][tx] = (kk < k && nn < n) ? B[kk * ldb + nn] : 0.f;
-    }
-    __syncthreads();
-    for (int rr = ty; rr < 32; rr += 8) {  // write out[r0 + rr][c0 + tx] = T[c0 + tx][r0 + rr]
-      const int64_t nn = r0 + rr, kk = c0 + tx;
-      if (nn >= n) continue;
-      const float x = tile[tx][rr];
-      float h, l;
-      split2(x, h, l);
-      b_hi[base + nn * kp + kk] = h;
-      b_lo[base + nn * kp + kk] = l;
-    }
+  int64_t lda;
+  const float* A = op_ptr<const float>(bases, lf.a, lda);
+  const size_t base = (size_t)blockIdx.z * (size_t)(m * kp);
+  for (int rr = ty; rr < 32; rr += 8) {
+    const int64_t r = r0 + rr, c = c0 + tx;
+    if (r >= m) continue;
+    const float x = (c < k) ? A[r * lda + c] : 0.f;
+    float h, l;
+    split2(x, h, l);
+    a_hi[base + r * kp + c] = h;
+    a_lo[base + r * kp + c] = l;
   }
 }
 
-// Vectorised hi / lo split (same elementwise split2 as k_split_tf32, so bitwise the same arena):
-// A side: 16-byte loads / stores, one float4 per thread, rows grid-strided.
-// B side: 64 x 64 tiles of T (k x n) staged through shared memory, 16-byte loads along n and
-// 16-byte stores along k of the transposed (n x kp) outputs.
-// Requires: leaf operands 16-byte aligned with ld % 4 == 0, k % 4 == 0 (checked by the caller).
+// Vectorised hi / lo split (the same elementwise split2, so bitwise the same arena): 16-byte loads
+// / stores, one float4 per thread, rows grid-strided.  Requires leaf operands 16-byte aligned with
+// ld % 4 == 0, k % 4 == 0, n % 4 == 0 (checked by the caller).
 __global__ void k_split_a_vec(const LeafNode* __restrict__ leaves, Bases bases, int64_t m,
                               int64_t k, int64_t kp, float* __restrict__ a_hi,
                               float* __restrict__ a_lo) {
@@ -439,49 +363,6 @@ __global__ void k_split_a_vec(const LeafNode* __restrict__ leaves, Bases bases, 
     split2(x.x, h.x, l.x); split2(x.y, h.y, l.y); split2(x.z, h.z, l.z); split2(x.w, h.w, l.w);
     *reinterpret_cast<float4*>(a_hi + base + r * kp + c) = h;
     *reinterpret_cast<float4*>(a_lo + base + r * kp + c) = l;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_split_b_vec(const LeafNode* __restrict__ leaves, Bases bases,
-                                                     int64_t n, int64_t k, int64_t kp,
-                                                     float* __restrict__ b_hi, float* __restrict__ b_lo) {
-  __shared__ float tile[64][65];
-  const LeafNode& lf = leaves[blockIdx.z];
-  int64_t ldb;
-  const float* B = op_ptr<const float>(bases, lf.b, ldb);
-  const size_t base = (size_t)blockIdx.z * (size_t)(n * kp);
-  const int64_t k0 = (int64_t)blockIdx.x * 64, n0 = (int64_t)blockIdx.y * 64;
-  const int tid = threadIdx.x;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {  // 64 rows (k) x 16 float4 (n)
-    const int idx = tid + q * 256;
-    const int rr = idx >> 4, cc = (idx & 15) * 4;
-    const int64_t kk = k0 + rr, nn = n0 + cc;
-    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (kk < k) {
-      if (nn + 3 < n) x = *reinterpret_cast<const float4*>(B + kk * ldb + nn);
-      else {
-        if (nn < n) x.x = B[kk * ldb + nn];
-        if (nn + 1 < n) x.y = B[kk * ldb + nn + 1];
-        if (nn + 2 < n) x.z = B[kk * ldb + nn + 2];
-      }
-    }
-    tile[rr][cc] = x.x; tile[rr][cc + 1] = x.y; tile[rr][cc + 2] = x.z; tile[rr][cc + 3] = x.w;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {  // 64 rows (n) x 16 float4 (k) of the transposed tile
-    const int idx = tid + q * 256;
-    const int rr = idx >> 4, cc = (idx & 15) * 4;
-    const int64_t nn = n0 + rr, kk = k0 + cc;
-    if (nn >= n || kk >= kp) continue;
-    float4 h, l;
-    split2(tile[cc][rr], h.x, l.x);
-    split2(tile[cc + 1][rr], h.y, l.y);
-    split2(tile[cc + 2][rr], h.z, l.z);
-    split2(tile[cc + 3][rr], h.w, l.w);
-    *reinterpret_cast<float4*>(b_hi + base + nn * kp + kk) = h;
-    *reinterpret_cast<float4*>(b_lo + base + nn * kp + kk) = l;
   }
 }
 
@@ -526,7 +407,7 @@ __global__ void k_split_bn(const LeafNode* __restrict__ leaves, Bases bases, int
 // Split launcher: vectorised kernels when every leaf operand allows 16-byte access.
 void launch_split(const LeafNode* dev_leaves, const LeafNode* host_leaves, int count, const Bases& b,
                   int64_t m, int64_t n, int64_t k, int64_t kp, float* a_hi, float* a_lo, float* b_hi,
-                  float* b_lo, cudaStream_t st, bool bmn) {
+                  float* b_lo, cudaStream_t st) {
   bool vec = host_leaves != nullptr && k % 4 == 0 && n % 4 == 0;
   for (int i = 0; vec && i < count; ++i) {
     int64_t lda, ldb;
@@ -539,23 +420,14 @@ void launch_split(const LeafNode* dev_leaves, const LeafNode* host_leaves, int c
   if (vec) {
     k_split_a_vec<<<dim3((unsigned)((kp / 4 + 255) / 256), (unsigned)(m < 8192 ? m : 8192), (unsigned)count), 256, 0, st>>>(
         dev_leaves, b, m, k, kp, a_hi, a_lo);
-    if (bmn)
-      k_split_bn_vec<<<dim3((unsigned)((np / 4 + 255) / 256), ry, (unsigned)count), 256, 0, st>>>(
-          dev_leaves, b, n, k, kp, np, b_hi, b_lo);
-    else
-      k_split_b_vec<<<dim3((unsigned)((kp + 63) / 64), (unsigned)((n + 63) / 64), (unsigned)count), 256, 0, st>>>(
-          dev_leaves, b, n, k, kp, b_hi, b_lo);
+    k_split_bn_vec<<<dim3((unsigned)((np / 4 + 255) / 256), ry, (unsigned)count), 256, 0, st>>>(
+        dev_leaves, b, n, k, kp, np, b_hi, b_lo);
     return;
   }
-  dim3 blk(32, 8);
-  k_split_tf32<<<dim3((unsigned)(kp / 32), (unsigned)((m + 31) / 32), (unsigned)count), blk, 0, st>>>(
-      dev_leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, 0);
-  if (bmn)
-    k_split_bn<<<dim3((unsigned)((np + 255) / 256), ry, (unsigned)count), 256, 0, st>>>(
-        dev_leaves, b, n, k, kp, np, b_hi, b_lo);
-  else
-    k_split_tf32<<<dim3((unsigned)(kp / 32), (unsigned)((n + 31) / 32), (unsigned)count), blk, 0, st>>>(
-        dev_leaves, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, 1);
+  k_split_a<<<dim3((unsigned)(kp / 32), (unsigned)((m + 31) / 32), (unsigned)count), dim3(32, 8), 0, st>>>(
+      dev_leaves, b, m, k, kp, a_hi, a_lo);
+  k_split_bn<<<dim3((unsigned)((np + 255) / 256), ry, (unsigned)count), 256, 0, st>>>(
+      dev_leaves, b, n, k, kp, np, b_hi, b_lo);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -571,8 +443,9 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-bool make_map(CUtensorMap* map, float* base, int64_t kp, int64_t rows, int64_t leaves,
-              int box_rows, int box_k = TBK) {
+// K-major A: S hi / lo (m x kp per leaf), boxes of TBK k x box_rows rows, 128-byte swizzle
+bool make_map(CUtensorMap* map, float* base, int64_t kp, int64_t rows, int64_t leaves, int box_rows) {
+  constexpr int box_k = TBK;
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {(cuuint64_t)kp, (cuuint64_t)rows, (cuuint64_t)leaves};
@@ -580,8 +453,7 @@ bool make_map(CUtensorMap* map, float* base, int64_t kp, int64_t rows, int64_t l
   cuuint32_t box[3] = {(cuuint32_t)box_k, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  box_k == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -607,56 +479,41 @@ int num_sms() {
   return sms > 0 ? sms : 148;
 }
 
-template <int BK, int STAGES, int EW, bool BMN>
 cudaError_t launch_k2p(float* a_hi, float* a_lo, float* b_hi, float* b_lo, const LeafNode* dev_leaves,
                        int count, int64_t m, int64_t n, int64_t kp, const Bases& b, int passes,
                        int chunk_k, cudaStream_t st) {
-  using CF = TCfg<BK, STAGES>;
   CUtensorMap ma_hi, ma_lo, mb_hi, mb_lo;
   const int64_t kpe = kp > 0 ? kp : TBK;
   const int64_t np = (n + 31) / 32 * 32;
-  if (!make_map(&ma_hi, a_hi, kpe, m, count, TBM, BK) || !make_map(&ma_lo, a_lo, kpe, m, count, TBM, BK))
-    return cudaErrorInvalidValue;
-  if (BMN ? (!make_map_mn(&mb_hi, b_hi, np, kpe, count, BK) || !make_map_mn(&mb_lo, b_lo, np, kpe, count, BK))
-          : (!make_map(&mb_hi, b_hi, kpe, n, count, TBN, BK) || !make_map(&mb_lo, b_lo, kpe, n, count, TBN, BK)))
+  if (!make_map(&ma_hi, a_hi, kpe, m, count, TBM) || !make_map(&ma_lo, a_lo, kpe, m, count, TBM) ||
+      !make_map_mn(&mb_hi, b_hi, np, kpe, count, TBK) || !make_map_mn(&mb_lo, b_lo, np, kpe, count, TBK))
     return cudaErrorInvalidValue;
   const int tiles_m = (int)((m + TBM - 1) / TBM), tiles_n = (int)((n + TBN - 1) / TBN);
   const int tiles = tiles_m * tiles_n;
   const int64_t total = (int64_t)tiles * count;
   if (total > INT32_MAX) return cudaErrorInvalidValue;
   const int grid = (int)std::min<int64_t>(total, num_sms());
-  const int chunk_kt = std::max(1, chunk_k / BK);
-  cudaError_t e = cudaFuncSetAttribute(k2p_tf32<BK, STAGES, EW, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM);
-  if (e != cudaSuccess) return e;
+  const int chunk_kt = std::max(1, chunk_k / TBK);
   static const int group_m = [] {
     const char* e = getenv("FMM_TF32_GROUP_M");  // tile rows per rasterisation group
     const int v = e ? atoi(e) : 16;
     return v >= 1 ? v : 16;
   }();
-  k2p_tf32<BK, STAGES, EW, BMN><<<grid, EpiCfg<EW>::THREADS, CF::SMEM, st>>>(
-      ma_hi, ma_lo, mb_hi, mb_lo, dev_leaves, b, m, n, kp, tiles_m, tiles_n, group_m, (int)total, passes,
-      chunk_kt);
+  cudaError_t e = cudaFuncSetAttribute(k2p_tf32, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  k2p_tf32<<<grid, K2P_THREADS, SMEM_BYTES, st>>>(ma_hi, ma_lo, mb_hi, mb_lo, dev_leaves, b, m, n, kp,
+                                                 tiles_m, tiles_n, group_m, (int)total, passes, chunk_kt);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-// hi / lo arena: A side m x kp (K-major), B side kp x np (MN-major, np = n rounded up to 32) or
-// n x kp (K-major); kp = k rounded up to 32
+// hi / lo arena: A side m x kp (K-major), B side kp x np (MN-major, np = n rounded up to 32);
+// kp = k rounded up to 32
 size_t tf32_arena_floats(int64_t count, int64_t m, int64_t n, int64_t k) {
   const int64_t kp = (k + TBK - 1) / TBK * TBK, np = (n + 31) / 32 * 32;
   // k = 0: no operand is read, but the kernel's tensor maps still need a (tiny) valid base
   return std::max<size_t>((size_t)count * (size_t)(2 * m * kp + 2 * np * kp), 1024);
-}
-
-// B operand layout of the FP32 tensor-core leaf: FMM_TF32_BMN = 1 (default) MN-major (T as
-// stored, split elementwise), 0 K-major (T transposed by the split)
-bool tf32_bmn() {
-  static const bool v = [] {
-    const char* e = getenv("FMM_TF32_BMN");
-    return e ? atoi(e) != 0 : true;
-  }();
-  return v;
 }
 
 // Chunk length (k elements) of the round-to-nearest accumulation: FMM_TF32_CHUNK, default 128
@@ -676,30 +533,18 @@ cudaError_t launch_gemm_tf32(const LeafNode* dev_leaves, int count, int64_t m, i
   if (count == 0 || m == 0 || n == 0) return cudaSuccess;
   if (!arena) return cudaErrorInvalidValue;
   // presplit: the leaf level's K1X2 wrote the arena (k, n multiples of 32, B MN-major)
-  if (presplit && (k % TBK != 0 || n % 32 != 0 || !tf32_bmn())) return cudaErrorInvalidValue;
+  if (presplit && (k % TBK != 0 || n % 32 != 0)) return cudaErrorInvalidValue;
   const int64_t kp = (k + TBK - 1) / TBK * TBK;
   float* a_hi = arena;
   float* a_lo = a_hi + (size_t)count * m * kp;
   float* b_hi = a_lo + (size_t)count * m * kp;
   float* b_lo = b_hi + (size_t)count * ((n + 31) / 32 * 32) * kp;
-  const bool bmn = tf32_bmn();
-  if (kp > 0 && !presplit) launch_split(dev_leaves, host_leaves, count, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, st, bmn);
-  static const int cfg = [] {
-    // 0: BK 32 / 2 stages (default), 1: BK 16 / 4 stages.  Measured at C5 FP32 (sw_power_cap):
-    // cfg 0 255.9 ms at 1537 MHz, cfg 1 296.8 ms at 1372 (its tensor pipe is busier per cycle but
-    // the power cap takes it back in clock); 16 instead of 8 epilogue warps: 312.7 ms at 1290
-    // (profiles/r02_tf32_persistent.md)
-    const char* e = getenv("FMM_TF32_CFG");
-    return e ? atoi(e) : 0;
-  }();
-  const int ck = tf32_chunk_k();
-  // a CTA-pair form (tcgen05.mma.cta_group::2, 256 x 256 tiles over a TPC, 3 stages) was built
-  // and measured 7 % slower under the power cap (profiles/r02_tf32_persistent.md); removed
-  if (cfg == 1)
-    return bmn ? launch_k2p<16, 4, 8, true>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st)
-               : launch_k2p<16, 4, 8, false>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st);
-  return bmn ? launch_k2p<32, 2, 8, true>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st)
-             : launch_k2p<32, 2, 8, false>(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, ck, st);
+  if (kp > 0 && !presplit) launch_split(dev_leaves, host_leaves, count, b, m, n, k, kp, a_hi, a_lo, b_hi, b_lo, st);
+  // round 2 measured a 4-stage BK = 16 ring (busier tensor pipe, lower clock under the power cap:
+  // 296.8 vs 255.9 ms at C5 FP32), 16 epilogue warps (312.7 ms), a K-major B operand transposed by
+  // the split (same speed, but no in-pass split) and a CTA-pair form (7 % slower): this single
+  // configuration remains (profiles/r02_tf32_persistent.md)
+  return launch_k2p(a_hi, a_lo, b_hi, b_lo, dev_leaves, count, m, n, kp, b, passes, tf32_chunk_k(), st);
 }
 
 }  // namespace fmm
