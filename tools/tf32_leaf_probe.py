@@ -1,6 +1,6 @@
 """FP32 tensor-core leaf probe: time and accuracy of one 3xTF32 leaf GEMM through fmm_gemm
-(k2p_tf32) for the kernel configuration / chunk length in the environment (FMM_TF32_CFG,
-FMM_TF32_CHUNK are read once per process, so run one process per setting).
+(k2p_tf32) for the chunk length in the environment (FMM_TF32_CHUNK is read once per process,
+so run one process per setting).
 
 Accuracy: max |C - C_ref| / max |C_ref| over a 64 x 64 sample, C_ref the exact (fp64) product of
 the FP32 inputs; beside it the same figure for a sequential round-to-nearest FP32 dot product
@@ -46,7 +46,7 @@ def main():
         prod = (a32 * b32[:, j][None, :]).astype(np.float32)  # exact products rounded to FP32
         seq[:, j] = np.cumsum(prod, axis=1, dtype=np.float32)[:, -1]
     den = np.abs(ref).max()
-    print(json.dumps({"n": n, "cfg": os.environ.get("FMM_TF32_CFG", "default"),
+    print(json.dumps({"n": n,
                       "chunk": os.environ.get("FMM_TF32_CHUNK", "default"), "ms": round(ms, 3),
                       "tflops_3x": round(2 * n ** 3 / ms / 1e9, 1),
                       "err_gpu": float(np.abs(got - ref).max() / den),
