@@ -91,6 +91,29 @@ def test_one_rank_communicator_scaled_and_padded(fb):
     assert np.array_equal(exe(p, A, B), ref)
 
 
+@pytest.mark.parametrize("mode", ["outside", "repeated"])
+@pytest.mark.parametrize("nranks,depth,order", [(2, 1, "cyclic"), (3, 2, "block"), (4, 3, "block")])
+def test_scaled_partitions_sum_to_scaled_product(fb, mode, nranks, depth, order):
+    # multi-GPU partitions of a scaled plan: every rank runs the scaling (Alg. 1 / 3)
+    # on the whole A, B, forms its units from the scaled operands and unscales its partial
+    # (C = D_A C' D_B is linear in C'), so the partials sum to the one-rank scaled product --
+    # within the rounding of the different summation order (componentwise: the C4 magnitudes
+    # make the normalised metric vacuous)
+    A, B = fi.draw("skew", 256, 256, 256, 3)
+    w = fb.Rule.builtin("winograd")
+    sc = {"mode": mode, "pow2": 1}
+    ref = exe(fb.Plan([w, w, w], 256, 256, 256, scaling=sc), A, B)
+    tot = np.zeros_like(ref)
+    for rank in range(nranks):
+        p = fb.Plan([w, w, w], 256, 256, 256, scaling=sc)
+        p.set_shard_depth(depth)
+        p.set_shard_order(order)
+        p.set_partition(rank, nranks)
+        tot += exe(p, A, B)
+    absab = np.abs(A) @ np.abs(B)
+    assert np.all(np.abs(tot - ref) <= 1e-12 * absab + 1e-300)
+
+
 # ---- two processes on one GPU: comm mode 3 over CUDA IPC ------------------------------------------
 
 def _free_port():
