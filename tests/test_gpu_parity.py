@@ -366,14 +366,17 @@ def test_execute_host_overlapped(fb, schedule, dtype):
     assert parity(Ch.numpy(), Co, A, B) <= (TOL64 if dtype == "f64" else TOL32)
 
 
-def test_cuda_graph_replay(fb):
-    A, B = fi.random_pair(512, 512, 512, seed=40)
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+def test_cuda_graph_replay(fb, dtype):
+    # FP32: the tensor-core leaf (tensor maps encoded at capture, the in-pass split) replayed
+    npdt = np.float64 if dtype == "f64" else np.float32
+    A, B = fi.random_pair(512, 512, 512, seed=40, dtype=npdt)
     w = fb.Rule.builtin("winograd")
-    p = fb.Plan([w, w], 512, 512, 512)
+    p = fb.Plan([w, w], 512, 512, 512, dtype=dtype)
     ref = p.execute(dev(A), dev(B)).cpu().numpy()
     p.set_graph(True)
     Ad, Bd = dev(A), dev(B)
-    C1 = torch.empty((512, 512), dtype=torch.float64, device="cuda")
+    C1 = torch.empty((512, 512), dtype=Ad.dtype, device="cuda")
     for _ in range(3):
         C1.zero_()
         p.execute(Ad, Bd, C1)
