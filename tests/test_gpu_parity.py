@@ -272,11 +272,16 @@ def test_deterministic(fb):
     assert np.array_equal(c1, c2)
 
 
-def test_split_schedule_matches_breadth_first(fb):
+@pytest.mark.parametrize("dtype,fusion", [("f64", "auto"), ("f64", "off"), ("f32", "auto")])
+def test_split_schedule_matches_breadth_first(fb, dtype, fusion):
     # depth-first top level (used for big problems and sharding) with nranks = 1 is bitwise
-    # equal to the breadth-first schedule: same kernels, same per-element orders.
-    A, B = fi.random_pair(256, 256, 256, seed=8)
-    p = gpu_plan(fb, ("winograd",) * 3, 256, 256, 256)
+    # equal to the breadth-first schedule: same kernels, same per-element orders.  The hybrid
+    # top level combines levels 0-1 in one pass after fused leaf parents, else levels 1-2 per
+    # subtree and the root alone (FP32 tensor-core leaves, unfused FP64): same sums, same order.
+    npdt = np.float64 if dtype == "f64" else np.float32
+    A, B = fi.random_pair(256, 256, 256, seed=8, dtype=npdt)
+    p = gpu_plan(fb, ("winograd",) * 3, 256, 256, 256, dtype=dtype)
+    p.set_fusion(fusion)
     bf = p.execute(dev(A), dev(B)).cpu().numpy()
     p.set_schedule("depth")
     assert np.array_equal(p.execute(dev(A), dev(B)).cpu().numpy(), bf)
@@ -290,7 +295,7 @@ def test_split_schedule_matches_breadth_first(fb):
     # virtual ranks: the partial sums add up to the product (parity), each rank's set of blocks
     # is exact w.r.t. its own owned products
     total = parts[0] + parts[1] + parts[2]
-    assert parity(total, bf, A, B) <= TOL64
+    assert parity(total, bf, A, B) <= (TOL64 if dtype == "f64" else TOL32)
     p.set_partition(0, 1)
     assert np.array_equal(p.execute(dev(A), dev(B)).cpu().numpy(), bf)
 
