@@ -226,14 +226,12 @@ def scaling_config(mode: str):
 def default_shard(nranks: int, levels: int):
     """(shard depth, unit order) for `nranks` ranks, from the per-rank compute of every rank's
     partition timed on one B200 at C5 (tools/partition_times.py, profiles/r02_partition_times.md;
-    one-GPU time / (P x slowest rank)): 2 ranks: depth 2 in blocks 0.943 (round-robin 0.924);
-    4: depth 3 in blocks 0.913 (depth 2 round-robin 0.862); 8: depth 3 in blocks 0.895 (the 7
-    top-level products 0.855).  Blocks keep a rank's units on shared upper-level paths, so it
-    repeats fewer S / T formation passes."""
+    one-GPU time / (P x slowest rank)): depth 3 in contiguous blocks gives 0.974 / 0.948 / 0.909
+    at 2 / 4 / 8 ranks (round 1's choice -- depth 2 round-robin at 2 and 4 ranks, the 7
+    top-level products at 8 -- 0.924 / 0.865 / 0.855).  Blocks keep a rank's units on shared
+    upper-level paths, and a subtree the rank owns entirely runs breadth-first like one unit."""
     if nranks <= 1:
         return 1, "cyclic"
-    if nranks == 2:
-        return min(2, levels), "block"
     return min(3, levels), "block"
 
 
@@ -832,7 +830,7 @@ def main():
                     choices=["none", "outside", "inside", "out_in", "in_out", "repeated"])
     ap.add_argument("--shard-depth", type=int, default=0,
                     help="multi-GPU units = paths of the first d levels (fmm_plan_set_shard_depth); "
-                         "0 = auto (bench.default_shard: 2 at 2 ranks, 3 at more)")
+                         "0 = auto (bench.default_shard: 3 in blocks)")
     ap.add_argument("--shard-order", default="auto", choices=["auto", "cyclic", "block"],
                     help="multi-GPU unit order (fmm_plan_set_shard_order); auto = with the auto depth, "
                          "blocks, else round-robin")

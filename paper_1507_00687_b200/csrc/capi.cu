@@ -918,6 +918,19 @@ struct Builder {
     return false;
   }
 
+  // Does this rank own every unit below a node of `level` (unit_prefix as in owns_subtree)?
+  // Then the subtree runs breadth-first like a unit: one S / T pass for all its products, the
+  // leaf parents fused over whole R-product chains (bitwise the unit-by-unit schedule).
+  bool owns_all(int level, int64_t unit_prefix) const {
+    if (p->nranks == 1) return true;
+    const int64_t span = unit_span(level);
+    if (span == 1) return owns_subtree(level, unit_prefix);
+    if (!p->shard_block) return false;  // round-robin spreads every subtree over the ranks
+    const int64_t U = unit_span(0), P = p->nranks, u0 = unit_prefix * span;
+    const int64_t lo = ((int64_t)p->rank * U + P - 1) / P, hi = ((int64_t)(p->rank + 1) * U + P - 1) / P;
+    return u0 >= lo && u0 + span <= hi;
+  }
+
   // Depth-first over the products r of `node` (level l), accumulating C_k (+)= w_kr M_r into
   // node.c in ascending r; recursion continues depth-first down to the shard depth, then each
   // owned subtree runs breadth-first.  Children's workspace is reused across r (one stream).
@@ -944,7 +957,8 @@ struct Builder {
         emit_k2f(l, {node}, kid, r, &started);
       } else {
         if (leaf_next) emit_k2(kid);
-        else if (l + 1 < p->shard_depth && p->nranks > 1) depth_first(l + 1, kid[0], unit);
+        else if (l + 1 < p->shard_depth && p->nranks > 1 && !owns_all(l + 1, unit))
+          depth_first(l + 1, kid[0], unit);
         else breadth_first(l + 1, kid);
         AccNode a{};
         a.out = node.c;
