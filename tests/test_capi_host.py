@@ -222,6 +222,32 @@ def test_p2p_comm_mode_schedule():
         fb.fmm._call("fmm_plan_set_comm_mode", p._h, 4)
 
 
+def test_leaf_split_and_shard_order_host():
+    # host-only plan structure of the round-2 options (no GPU needed to compile a plan)
+    w = fb.Rule.builtin("winograd")
+    # FP32 tensor-core leaves: the in-pass split removes no launch (the split kernel runs inside
+    # the leaf step) but the plan compiles both ways; other values are argument errors
+    p = fb.Plan([w, w], 512, 512, 512, dtype="f32", leaf=fb.fmm.LEAF_3XTF32)
+    n1 = p.launch_count()
+    p.set_leaf_split(False)
+    assert p.launch_count() == n1
+    with pytest.raises(fb.FmmError):
+        fb.fmm._call("fmm_plan_set_leaf_split", p._h, 2)
+    with pytest.raises(fb.FmmError):
+        fb.fmm._call("fmm_plan_set_shard_order", p._h, 2)
+    # block units at depth 3 over 8 ranks: rank 0 owns units 0..42 = six whole level-2 subtrees
+    # (each run breadth-first: one S / T pass + one fused leaf launch) and one single unit
+    q = fb.Plan([w] * 3, 1024, 1024, 1024)
+    q.set_fusion("on")
+    q.set_shard_depth(3)
+    q.set_shard_order("block")
+    assert q.owned(0, 8) == list(range(43))
+    q.set_partition(0, 8)
+    blocks = q.launch_count()
+    q.set_shard_order("cyclic")
+    assert q.launch_count() > blocks  # round-robin: every unit formed and combined on its own
+
+
 def test_header_is_plain_c():
     # the boundary header compiles as C99 and as C++ (no torch / C++ types in the signatures)
     import shutil
