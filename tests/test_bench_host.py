@@ -81,3 +81,12 @@ def test_tf32_split_counts(sw):
     # and their hi + lo written, per operand
     kernel = 2 * (16 + 40) * s + 2 * 3 * 49 * s
     assert bench.pass_bytes([sw, sw], n, n, n, e, False, True, True, False, "kernel") == (kernel + k3x2) * e
+
+
+def test_default_shard():
+    # bench.py's multi-GPU partition (profiles/r02_partition_times.md): one rank unsharded;
+    # otherwise depth-3 units (or the plan's depth) in contiguous blocks
+    assert bench.default_shard(1, 3) == (1, "cyclic")
+    assert bench.default_shard(2, 3) == (3, "block")
+    assert bench.default_shard(8, 3) == (3, "block")
+    assert bench.default_shard(4, 2) == (2, "block")
