@@ -26,7 +26,9 @@ namespace cg = cooperative_groups;
 // reproduce the sequential roundings: switch to materialised), [10], [11] stop-test failure
 // counters of even / odd steps, [12] A' / B' are stored in the materialised buffers
 enum { F_DONE = 0, F_STEPS = 1, F_ERR = 2, F_ERRIDX = 3, F_MODE = 8,
-       F_BAD = 9, F_FAIL = 10, F_STORED = 12, F_EXT = 16, F_COUNT = 24 };
+       F_BAD = 9, F_FAIL = 10, F_STORED = 12, F_BADX = 13, F_EXT = 16, F_COUNT = 24 };
+// [13] the fused A pass (row_fused_tma) found a value after the O step the virtual form cannot
+// carry (it counts only if that step's I reductions are needed)
 // [16 .. 23]: min / max of the final net exponents exAr, exAc, exBr, exBc (the root K1's
 // fast path needs every row + column exponent sum to be a normal power of two)
 
@@ -96,15 +98,16 @@ __global__ void k_unscale(double* C, int64_t ldc, int64_t M, int64_t N, const do
 // of scale_ws_bytes(M, K, N).  Writes A' / B' (A_out / B_out), dA, dB, dI and flags.
 // ---------------------------------------------------------------------------------------------
 size_t scale_ws_bytes(int64_t M, int64_t K, int64_t N) {
-  // 2 sets of maxima (rowA M, colA K, rowB K, colB N) + factor vectors (r M, s N, p K) + flags
+  // 3 sets of maxima (rowA M, colA K, rowB K, colB N; step t reads set t mod 3, the fused
+  // A pass before an O step also writes set t + 1) + factor vectors (r M, s N, p K) + flags
   // (16 doubles) + exact reciprocals (r M, s N, p K) of power-of-two factors + the net
   // exponents of the virtual form (int32: rowA M, colA K, rowB K, colB N)
-  return (size_t)(2 * (M + K + K + N) + 2 * (M + N + K) + 16) * sizeof(double) +
+  return (size_t)(3 * (M + K + K + N) + 2 * (M + N + K) + 16) * sizeof(double) +
          (size_t)(M + K + K + N) * sizeof(int32_t) + 256;
 }
 
 struct ScaleWsView {
-  double* mx[2];  // each: rowA (M) | colA (K) | rowB (K) | colB (N)
+  double* mx[3];  // each: rowA (M) | colA (K) | rowB (K) | colB (N)
   double *r, *s, *p;
   double *ri, *si, *pi;
   int* flags;
@@ -117,7 +120,8 @@ static ScaleWsView scale_ws_view(void* ws, int64_t M, int64_t K, int64_t N) {
   const int64_t set = M + K + K + N;
   v.mx[0] = w;
   v.mx[1] = w + set;
-  v.r = w + 2 * set;
+  v.mx[2] = w + 2 * set;
+  v.r = w + 3 * set;
   v.s = v.r + M;
   v.p = v.s + N;
   v.ri = v.p + K;
@@ -168,7 +172,7 @@ struct CoopArgs {
   int64_t M, K, N;
   double *dA, *dB, *dI;
   int32_t *exAr, *exAc, *exBr, *exBc;  // net exponents of the virtual form
-  double* mx[2];                       // rowA (M) | colA (K) | rowB (K) | colB (N)
+  double* mx[3];                       // rowA (M) | colA (K) | rowB (K) | colB (N)
   double *fr, *fs, *fp;                // factors of the current step (r M, s N, p K)
   int* flags;
   int nsteps, first_O, pow2, materialise_end;
@@ -179,6 +183,9 @@ struct CoopArgs {
   // (256-column strips x row chunks), per matrix
   int64_t rrowsA, rrowsB, crowsA, crowsB;
   int rsegsA, rsegsB, rtilesA, rtilesB, cstripsA, cstripsB, ctilesA, ctilesB;
+  // the fused A pass before an O step (row_fused_tma): whole-row tiles of frowsA rows
+  int fuseA, ftilesA;
+  int64_t frowsA;
   unsigned long long* trace;  // FMM_SCALE_TRACE: %globaltimer after every grid barrier
 };
 
@@ -754,10 +761,123 @@ __device__ __noinline__ void col_tile_tma(const MatPass& q, int tile, int* flags
   if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(&flags[F_BAD], 1);
 }
 
-// dynamic shared memory of k_scale_coop: the TMA stage ring (also the warp-combine buffers),
-// its mbarriers, the row exponents of a tile, the per-warp parities
+// ---- the fused A pass before an O step ------------------------------------
+// The O step's row factor r_i depends on row i of A alone, so a block that holds whole
+// rows can finish the O reduction of a row, form r_i, and feed the row's values AFTER the step
+// into the next (I) step's column maxima of A while the row is still on chip: one read
+// of A serves two steps.  A tile is a chunk of whole rows (K <= 4096: warp w owns columns
+// [512 w, 512 w + 512), 16 per lane in registers); the rows stream through a ring of CS row-size
+// stages (32 KB each, the per-warp rings' memory) filled by one bulk copy per row.  Per row: the
+// O row maximum exactly as row_tile_tma forms it (written to rowA), r_i as the factor phase will
+// recompute it from that maximum (pow2_round; the factor phase stays the only writer of r, D_A
+// and the exponents, so a redo leaves nothing half-applied), then z = y 2^(er_i - log2 r_i) with
+// y = |a| 2^(ec) into the lane's column maxima, which go to the next step's colA with atomicMax
+// at the end of the tile.  Exactness of z (y 2^e normal or zero, the exponent in range) is
+// flagged in F_BADX, which only matters when the I step's reductions are needed; the row part
+// flags F_BAD exactly as row_tile_tma does.  Virtual form only (pow2, nothing materialised).
+constexpr int FRK = 4096;  // longest fused row (doubles): 8 warps x 512 columns
+template <bool RAW>
+__device__ __noinline__ void row_fused_tma(const MatPass& q, double* colmax_next, int tile, int* flags,
+                                           int64_t rows_per, const TmaSmem& sm, uint64_t* fbar,
+                                           uint32_t* fphase, double (*red)[8]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)tile * rows_per;
+  const int64_t r1 = min(r0 + rows_per, q.rows);
+  const int n = r0 < r1 ? (int)(r1 - r0) : 0;
+  const int64_t cw = (int64_t)warp * 512;
+  const int64_t lim = q.cols - cw - 2 * lane;  // lane column offset o valid iff o < lim
+  const uint32_t bytes = (uint32_t)(q.cols * 8);
+  double* ring = sm.stage;  // CS stages of FRK doubles
+  __syncthreads();  // every warp is done with the previous tile's ring, exponents and red
+  if (threadIdx.x == 0)
+    for (int k = 0; k < CS && k < n; ++k) bulk_g2s(ring + k * FRK, q.src + (r0 + k) * q.lds, bytes, fbar + k);
+  if (!RAW) stage_er_nosync(q, r0, r1, sm.er);
+  bool bad = false, badx = false;
+  double fc[16], cmx[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int o = (e / 2) * 64 + (e & 1);
+    fc[e] = (!RAW && o < lim) ? pow2_of(q.ec[cw + 2 * lane + o], &bad) : 1.0;
+    cmx[e] = 0.0;
+  }
+  uint32_t ph = *fphase;
+  for (int k = 0; k < n; ++k) {
+    const int st = k % CS;
+    const int64_t r = r0 + k;
+    bar_wait(fbar + st, (ph >> st) & 1u);
+    ph ^= 1u << st;
+    double y[16];
+    const uint32_t sp = s_u32(ring + st * FRK + cw + 2 * lane);
+    if (lim > 0) {
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        if (h * 64 < lim) {
+          const double2 v = lds2(sp + h * 64 * 8);
+          y[2 * h] = v.x; y[2 * h + 1] = v.y;
+        } else {
+          y[2 * h] = 0.0; y[2 * h + 1] = 0.0;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) y[e] = 0.0;
+    }
+    const int er = RAW ? 0 : sm.er[r - r0];
+    const double thr = under_thr(er);
+    double mx = 0.0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      y[e] = __dmul_rn(fabs(y[e]), fc[e]);
+      if (RAW) bad |= !(y[e] <= kDblMax);          // NaN or Inf
+      else bad |= (y[e] < thr) & (y[e] > 0.0);     // y or y 2^er not normal
+      mx = fmax(mx, y[e]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) red[k & 1][warp] = mx;
+    __syncthreads();  // row k's maxima are in red; every warp has its values out of the stage
+    if (threadIdx.x == 0 && k + CS < n) bulk_g2s(ring + st * FRK, q.src + (r + CS) * q.lds, bytes, fbar + st);
+    double m = red[k & 1][0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) m = fmax(m, red[k & 1][w]);
+    const double v = RAW ? m : scale2(m, er);  // the O row maximum (row_tile_tma's value)
+    if (!RAW && !(v <= kDblMax)) bad = true;
+    if (threadIdx.x == 0) q.rmax[r] = __longlong_as_double((int64_t)abs_bits(v));
+    // r_i as the factor phase forms it (reading A8), and the row's values after the step
+    int ern = er;
+    double rf = 0.0, inv;
+    if (v > 0.0) rf = pow2_round(v);
+    if (v > 0.0 && exact_recip(rf, &inv)) ern = er - log2_pow2(rf);
+    else badx = true;
+    const double pf = pow2_of(ern, &badx);
+    const double thr2 = under_thr(ern);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      badx |= (y[e] < thr2) & (y[e] > 0.0);      // z = y 2^ern not normal
+      cmx[e] = fmax(cmx[e], __dmul_rn(y[e], pf));
+    }
+  }
+  if (threadIdx.x == 0) *fphase = ph;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const int o = (e / 2) * 64 + (e & 1);
+    if (o < lim && n > 0) {
+      if (!(cmx[e] <= kDblMax)) badx = true;
+      atomicMax(reinterpret_cast<unsigned long long*>(&colmax_next[cw + 2 * lane + o]),
+                (unsigned long long)abs_bits(cmx[e]));
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicExch(&flags[F_BAD], 1);
+  if (__any_sync(0xffffffffu, badx) && lane == 0) atomicExch(&flags[F_BADX], 1);
+}
+
+// dynamic shared memory of k_scale_coop: the TMA stage ring (also the warp-combine buffers and
+// the fused pass's row ring), its mbarriers, the row exponents of a tile, the per-warp parities,
+// the fused pass's row-ring mbarriers, parity word and per-warp row maxima
+static_assert(CS * FRK <= 8 * CS * CSTG, "fused row ring fits the per-warp rings");
 constexpr size_t kCoopSmem = (size_t)8 * CS * CSTG * sizeof(double) + 8 * CS * sizeof(uint64_t) +
-                             kTmaRows * sizeof(int32_t) + 8 * sizeof(uint32_t);
+                             kTmaRows * sizeof(int32_t) + 8 * sizeof(uint32_t) +
+                             CS * sizeof(uint64_t) + 8 + 2 * 8 * sizeof(double);
 
 __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
   extern __shared__ __align__(128) uint8_t dsm[];
@@ -766,8 +886,13 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
   tsm.bar = reinterpret_cast<uint64_t*>(dsm + (size_t)8 * CS * CSTG * sizeof(double));
   tsm.er = reinterpret_cast<int32_t*>(tsm.bar + 8 * CS);
   tsm.phase = reinterpret_cast<uint32_t*>(tsm.er + kTmaRows);
+  uint64_t* fbar = reinterpret_cast<uint64_t*>(tsm.phase + 8);  // fused row ring: CS mbarriers
+  uint32_t* fphase = reinterpret_cast<uint32_t*>(fbar + CS);
+  double (*red)[8] = reinterpret_cast<double (*)[8]>(fphase + 2);
   if (threadIdx.x < 8 * CS) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s_u32(tsm.bar + threadIdx.x)));
+  if (threadIdx.x < CS) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s_u32(fbar + threadIdx.x)));
   if (threadIdx.x < 8) tsm.phase[threadIdx.x] = 0;
+  if (threadIdx.x == 0) *fphase = 0;
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
   double (*cmd)[256] = reinterpret_cast<double (*)[256]>(dsm);
@@ -797,7 +922,7 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
   for (int64_t i = gtid; i < M; i += gstride) { a.dA[i] = 1.0; a.exAr[i] = 0; }
   for (int64_t j = gtid; j < N; j += gstride) { a.dB[j] = 1.0; a.exBc[j] = 0; }
   for (int64_t k = gtid; k < K; k += gstride) { a.dI[k] = 1.0; a.exAc[k] = 0; a.exBr[k] = 0; }
-  for (int64_t i = gtid; i < M + 2 * K + N; i += gstride) { a.mx[0][i] = 0.0; a.mx[1][i] = 0.0; }
+  for (int64_t i = gtid; i < M + 2 * K + N; i += gstride) { a.mx[0][i] = 0.0; a.mx[1][i] = 0.0; a.mx[2][i] = 0.0; }
   if (gtid == 0) flags[F_MODE] = a.pow2 ? 0 : 1;
   if (gtid < 8) flags[F_EXT + gtid] = (gtid & 1) ? (-0x7fffffff - 1) : 0x7fffffff;
   gsync();
@@ -818,9 +943,14 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
   };
   // run one pass over A and B (tiles of A, then of B, grid-strided)
   int npass = 0;
-  auto run_pass = [&](int kind, MatPass& pa, MatPass& pb) {
+  bool fusedQ = false;  // the pass just run was the fused A pass before an O step
+  // amode (reduction passes): 0 A's reductions as set in pa; 1 no A part; 2 the fused A pass
+  // before an O step (row maxima into pa.rmax, the values after the step's column maxima into
+  // colA_next)
+  auto run_pass = [&](int kind, MatPass& pa, MatPass& pb, int amode = 0, double* colA_next = nullptr) {
     if (kind != PK_MAT) {  // reductions only: row or column tiles per matrix
-      const int na = pa.rmax ? a.rtilesA : a.ctilesA, nbt = pb.rmax ? a.rtilesB : a.ctilesB;
+      const int na = amode == 1 ? 0 : amode == 2 ? a.ftilesA : pa.rmax ? a.rtilesA : a.ctilesA;
+      const int nbt = pb.rmax ? a.rtilesB : a.ctilesB;
       // alternate passes walk the tiles in reverse: a pass starts on the ~100 MB the previous
       // one read last, still in the 126 MB L2
       const bool rev = (npass++ & 1) != 0;
@@ -833,7 +963,10 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
         const int64_t rr = isA ? a.rrowsA : a.rrowsB, cr = isA ? a.crowsA : a.crowsB;
         // TMA staging needs 16-byte aligned rows (and whole 16-byte row segments)
         const bool tma = ((((uintptr_t)q.src) & 15u) == 0) && q.lds % 2 == 0 && q.cols % 2 == 0;
-        if (q.rmax) {
+        if (isA && amode == 2) {
+          if (kind == PK_RAW) row_fused_tma<true>(q, colA_next, tt, flags, a.frowsA, tsm, fbar, fphase, red);
+          else row_fused_tma<false>(q, colA_next, tt, flags, a.frowsA, tsm, fbar, fphase, red);
+        } else if (q.rmax) {
           if (tma && rr <= kTmaRows) {
             if (kind == PK_RAW) row_tile_tma<true>(q, tt, flags, segs, rr, tsm);
             else row_tile_tma<false>(q, tt, flags, segs, rr, tsm);
@@ -881,7 +1014,8 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
     const int isO = a.first_O;
     auto pp = views(isO, PK_RAW, a.mx[0]);
     set_max(pp.first, pp.second, isO, a.mx[0]);
-    run_pass(PK_RAW, pp.first, pp.second);
+    fusedQ = isO && a.fuseA && a.nsteps > 1;
+    run_pass(PK_RAW, pp.first, pp.second, fusedQ ? 2 : 0, a.mx[1] + M);
   }
   gsync();
   int t0 = -1;
@@ -889,11 +1023,14 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
     const int isO = (t % 2 == 0) == (a.first_O != 0);
     if (isO && t0 < 0) t0 = t;
     const int test = (a.tau >= 0.0 && t0 >= 0 && t > t0) ? 1 : 0;
-    double* cur = a.mx[t & 1];
-    double* nxt = a.mx[(t + 1) & 1];
+    double* cur = a.mx[t % 3];
+    double* nxt = a.mx[(t + 1) % 3];
+    double* nxt2 = a.mx[(t + 2) % 3];
     int* fail = &flags[F_FAIL + (t & 1)];
-    // ---- factors of step t (Alg. 3) from the maxima in `cur`; zero `nxt`
-    for (int64_t i = gtid; i < set; i += gstride) nxt[i] = 0.0;
+    // ---- factors of step t (Alg. 3) from the maxima in `cur`; zero the set step
+    // t + 2 reads (nxt was zeroed at step t - 1: the fused A pass before an O step t + 1 writes
+    // into it and into nxt2 during step t's application)
+    for (int64_t i = gtid; i < set; i += gstride) nxt2[i] = 0.0;
     if (gtid == 0) flags[F_FAIL + ((t + 1) & 1)] = 0;
     bool ok = true, badf = false;
     if (isO) {
@@ -959,8 +1096,14 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
     const bool done = (test && *(volatile int*)fail == 0) || t == a.nsteps - 1;
     const bool need_next = !done;  // the values after this step feed another step
     // ---- application of step t
+    const bool fusedT = fusedQ;  // step t's maxima came from a fused A pass (nxt holds colA)
+    fusedQ = false;
     if (*(volatile int*)&flags[F_MODE] == 0 && *(volatile int*)&flags[F_BAD]) {
       // a factor the virtual form cannot carry: materialise from the exact values before it
+      if (fusedT && need_next) {  // drop the fused pass's speculative colA
+        for (int64_t i = gtid; i < set; i += gstride) nxt[i] = 0.0;
+        gsync();
+      }
       auto pp = views(isO, PK_MAT, nxt);
       set_factors(pp.first, pp.second, isO);
       if (need_next) set_max(pp.first, pp.second, !isO, nxt);
@@ -971,10 +1114,16 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
       if (need_next) {  // virtual: the next step's reductions of the values after this step
         auto pp = views(!isO, PK_VIRTUAL, nxt);
         set_max(pp.first, pp.second, !isO, nxt);
-        run_pass(PK_VIRTUAL, pp.first, pp.second);
+        // after an I step whose next (O) step is not the last: the fused A pass (it also
+        // forms step t + 2's colA); after an O step whose A side the fused pass did: B only
+        const int amode = fusedT ? 1 : (!isO && a.fuseA && t + 1 < a.nsteps - 1) ? 2 : 0;
+        run_pass(PK_VIRTUAL, pp.first, pp.second, amode, nxt2 + M);
         gsync();
-        if (*(volatile int*)&flags[F_BAD]) {  // inexact intermediates: redo, materialised
+        const bool redo = *(volatile int*)&flags[F_BAD] || (fusedT && *(volatile int*)&flags[F_BADX]);
+        if (!redo && amode == 2) fusedQ = true;
+        if (redo) {  // inexact intermediates: redo, materialised
           for (int64_t i = gtid; i < set; i += gstride) nxt[i] = 0.0;
+          if (amode == 2) for (int64_t i = gtid; i < set; i += gstride) nxt2[i] = 0.0;
           gsync();
           auto pm = views(isO, PK_MAT, nxt);
           set_factors(pm.first, pm.second, isO);
@@ -1055,7 +1204,7 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
   a.M = M; a.K = K; a.N = N;
   a.dA = dA; a.dB = dB; a.dI = dI;
   a.exAr = v.ex; a.exAc = v.ex + M; a.exBr = v.ex + M + K; a.exBc = v.ex + M + 2 * K;
-  a.mx[0] = v.mx[0]; a.mx[1] = v.mx[1];
+  a.mx[0] = v.mx[0]; a.mx[1] = v.mx[1]; a.mx[2] = v.mx[2];
   a.fr = v.r; a.fs = v.s; a.fp = v.p;
   a.flags = v.flags;
   a.nsteps = nsteps; a.first_O = first_O ? 1 : 0; a.pow2 = pow2; a.materialise_end = materialise_end;
@@ -1092,6 +1241,12 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
   rtiles(K, N, &a.rrowsB, &a.rsegsB, &a.rtilesB);
   ctiles(M, K, &a.crowsA, &a.cstripsA, &a.ctilesA);
   ctiles(K, N, &a.crowsB, &a.cstripsB, &a.ctilesB);
+  // fused A pass: whole rows (K <= FRK, 16-byte aligned) in about one tile per block
+  a.frowsA = std::max<int64_t>(1, (M + nblocks - 1) / nblocks);
+  a.ftilesA = M > 0 ? (int)((M + a.frowsA - 1) / a.frowsA) : 0;
+  static const bool no_fuse = getenv("FMM_SCALE_FUSE") && atoi(getenv("FMM_SCALE_FUSE")) == 0;
+  a.fuseA = (!no_fuse && pow2 && M > 0 && K > 0 && K <= FRK && K % 2 == 0 && lda % 2 == 0 &&
+             ((uintptr_t)A & 15u) == 0 && a.frowsA <= kTmaRows) ? 1 : 0;
   static unsigned long long* trace = nullptr;
   static const bool tracing = getenv("FMM_SCALE_TRACE") != nullptr;
   a.trace = nullptr;

@@ -259,3 +259,32 @@ def test_repeated_wide_matrices_bitwise(fb, dims):
         assert g["steps"] == o["steps"]
         for k in ("A", "B", "dA", "dB", "dI"):
             assert np.array_equal(host(g[k]), o[k]), k
+
+
+@pytest.mark.parametrize("dims", [(300, 4094, 500), (257, 4097, 300), (96, 2, 64), (40, 3, 50),
+                                  (5000, 512, 64)])
+def test_repeated_fused_pass_edges_bitwise(fb, dims):
+    # the fused A pass before an O step (whole rows, K <= 4096 even) at its
+    # edges: a ragged last 512-column segment, K past the limit or odd (the unfused passes run),
+    # tiny K, and more rows than blocks x 16 (several rows per tile)
+    M, K, N = dims
+    A, B = fi.draw("skew", M, K, N, 5)
+    for first_O in (True, False):
+        g = fb.scale_repeated(dev(A), dev(B), first_O=first_O, tau=0.0, max_steps=7, pow2=True)
+        o = oracle.scale_repeated(A, B, first_O=first_O, tau=0.0, max_steps=7, pow2=True)
+        assert g["steps"] == o["steps"]
+        for k in ("A", "B", "dA", "dB", "dI"):
+            assert np.array_equal(host(g[k]), o[k]), k
+
+
+@pytest.mark.parametrize("first_O", [True, False])
+def test_fused_pass_fallback_at_later_step(fb, first_O):
+    # a value that turns subnormal only after a later O step: with first_O = False the first
+    # fused pass is the one before step 1, so its speculative column maxima (F_BADX) are what
+    # sends the run to the materialised form there; bitwise the oracle either way
+    A, B = _subnormal_after_step_pair()
+    gg = fb.scale_repeated(dev(A), dev(B), first_O=first_O, tau=0.0, max_steps=6, pow2=True)
+    o = oracle.scale_repeated(A, B, first_O=first_O, tau=0.0, max_steps=6, pow2=True)
+    assert gg["steps"] == o["steps"]
+    for k in ("A", "B", "dA", "dB", "dI"):
+        assert np.array_equal(host(gg[k]), o[k]), k
