@@ -587,12 +587,6 @@ __device__ __forceinline__ void stage_er_nosync(const MatPass& q, int64_t r0, in
   for (int64_t r = r0 + threadIdx.x; r < r1; r += CT) sh[r - r0] = q.er ? q.er[r] : 0;
   __syncthreads();
 }
-// stage the tile's row exponents (rows [r0, r1)) in shared memory
-__device__ __forceinline__ void stage_er(const MatPass& q, int64_t r0, int64_t r1, int32_t* sh) {
-  __syncthreads();
-  for (int64_t r = r0 + threadIdx.x; r < r1; r += CT) sh[r - r0] = q.er ? q.er[r] : 0;
-  __syncthreads();
-}
 
 template <bool RAW>
 __device__ __noinline__ void row_tile_tma(const MatPass& q, int tile, int* flags, int segs, int64_t rows_per,
@@ -628,6 +622,11 @@ __device__ __noinline__ void row_tile_tma(const MatPass& q, int tile, int* flags
     const int64_t r = rw + 8 * k;
     bar_wait(bar + st, (ph >> st) & 1u);
     ph ^= 1u << st;
+#ifdef FMM_SCALE_EXP  // development: the data movement alone (results invalid)
+    __syncwarp();
+    if (lane == 0 && k + CS < n) bulk_g2s(buf + st * CSTG, q.src + (r + 8 * CS) * q.lds + cs, bytes, bar + st);
+    continue;
+#endif
     double x[16];
     const uint32_t sp = s_u32(buf + st * CSTG + 2 * lane);
 #pragma unroll
@@ -706,6 +705,11 @@ __device__ __noinline__ void col_tile_tma(const MatPass& q, int tile, int* flags
     const int st = k % CS;
     bar_wait(bar + st, (ph >> st) & 1u);
     ph ^= 1u << st;
+#ifdef FMM_SCALE_EXP
+    __syncwarp();
+    if (lane == 0 && k + CS < n) issue(k + CS, st);
+    continue;
+#endif
     double x[2][8];
     const int64_t ra = rw + 16 * k;
 #pragma unroll
@@ -806,6 +810,11 @@ __device__ __noinline__ void row_fused_tma(const MatPass& q, double* colmax_next
     const int64_t r = r0 + k;
     bar_wait(fbar + st, (ph >> st) & 1u);
     ph ^= 1u << st;
+#ifdef FMM_SCALE_EXP
+    __syncthreads();
+    if (threadIdx.x == 0 && k + CS < n) bulk_g2s(ring + st * FRK, q.src + (r + CS) * q.lds, bytes, fbar + st);
+    continue;
+#endif
     double y[16];
     const uint32_t sp = s_u32(ring + st * FRK + cw + 2 * lane);
     if (lim > 0) {
