@@ -229,6 +229,11 @@ constexpr uint64_t kAbsMask = 0x7fffffffffffffffULL, kInfBits = 0x7ff00000000000
 
 __device__ __forceinline__ uint64_t abs_bits(double x) { return (uint64_t)__double_as_longlong(x) & kAbsMask; }
 
+// max(m, y) for a running maximum m that is never NaN (it starts at 0 and only takes values that
+// compared greater): exactly fmax(m, y) -- a NaN y is ignored -- in one compare and two selects;
+// sm_100 has no FP64 min / max instruction and fmax's NaN handling costs twice that
+__device__ __forceinline__ double max_nn(double m, double y) { return y > m ? y : m; }
+
 template <int KIND>
 __device__ __noinline__ void mat_tile(const MatPass& q, int tile, int* flags, unsigned long long (*cm)[CSTRIP]) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -649,10 +654,10 @@ __device__ __noinline__ void row_tile_tma(const MatPass& q, int tile, int* flags
       const double y = __dmul_rn(fabs(x[e]), fc[e]);
       if (RAW) bad |= !(y <= kDblMax);          // NaN or Inf
       else bad |= (y < thr) & (y > 0.0);        // y or y 2^er not normal
-      mx = fmax(mx, y);
+      mx = max_nn(mx, y);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = 16; o > 0; o >>= 1) mx = max_nn(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) {
       const double v = RAW ? mx : scale2(mx, er);
       if (!RAW && !(v <= kDblMax)) bad = true;
@@ -740,7 +745,7 @@ __device__ __noinline__ void col_tile_tma(const MatPass& q, int tile, int* flags
         const double y = __dmul_rn(fabs(x[u][e]), fr);
         if (RAW) bad |= !(y <= kDblMax);          // NaN or Inf
         else bad |= (y < cthr[e]) & (y > 0.0);    // y or y 2^ec not normal
-        cmx[e] = fmax(cmx[e], y);
+        cmx[e] = max_nn(cmx[e], y);
       }
     }
   }
@@ -754,7 +759,7 @@ __device__ __noinline__ void col_tile_tma(const MatPass& q, int tile, int* flags
   for (int c = threadIdx.x; c < 256; c += CT) {
     double m = 0.0;
 #pragma unroll
-    for (int y = 0; y < 8; ++y) m = fmax(m, cm[y][c]);
+    for (int y = 0; y < 8; ++y) m = max_nn(m, cm[y][c]);
     if (c < len) {
       const double v = RAW ? m : scale2(m, q.ec[cs + c]);
       if (!RAW && !(v <= kDblMax)) bad = true;
@@ -839,16 +844,16 @@ __device__ __noinline__ void row_fused_tma(const MatPass& q, double* colmax_next
       y[e] = __dmul_rn(fabs(y[e]), fc[e]);
       if (RAW) bad |= !(y[e] <= kDblMax);          // NaN or Inf
       else bad |= (y[e] < thr) & (y[e] > 0.0);     // y or y 2^er not normal
-      mx = fmax(mx, y[e]);
+      mx = max_nn(mx, y[e]);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = 16; o > 0; o >>= 1) mx = max_nn(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) red[k & 1][warp] = mx;
     __syncthreads();  // row k's maxima are in red; every warp has its values out of the stage
     if (threadIdx.x == 0 && k + CS < n) bulk_g2s(ring + st * FRK, q.src + (r + CS) * q.lds, bytes, fbar + st);
     double m = red[k & 1][0];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) m = fmax(m, red[k & 1][w]);
+    for (int w = 1; w < 8; ++w) m = max_nn(m, red[k & 1][w]);
     const double v = RAW ? m : scale2(m, er);  // the O row maximum (row_tile_tma's value)
     if (!RAW && !(v <= kDblMax)) bad = true;
     if (threadIdx.x == 0) q.rmax[r] = __longlong_as_double((int64_t)abs_bits(v));
@@ -863,7 +868,7 @@ __device__ __noinline__ void row_fused_tma(const MatPass& q, double* colmax_next
 #pragma unroll
     for (int e = 0; e < 16; ++e) {
       badx |= (y[e] < thr2) & (y[e] > 0.0);      // z = y 2^ern not normal
-      cmx[e] = fmax(cmx[e], __dmul_rn(y[e], pf));
+      cmx[e] = max_nn(cmx[e], __dmul_rn(y[e], pf));
     }
   }
   if (threadIdx.x == 0) *fphase = ph;
