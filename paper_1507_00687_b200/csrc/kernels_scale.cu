@@ -185,6 +185,7 @@ struct CoopArgs {
   int rsegsA, rsegsB, rtilesA, rtilesB, cstripsA, cstripsB, ctilesA, ctilesB;
   // the fused A pass before an O step (row_fused_tma): whole-row tiles of frowsA rows
   int fuseA, ftilesA;
+  int l2hint;  // L2 eviction-priority hints on the fused schedule's bulk copies
   int64_t frowsA;
   unsigned long long* trace;  // FMM_SCALE_TRACE: %globaltimer after every grid barrier
 };
@@ -218,6 +219,7 @@ struct MatPass {
   int cmul;                                // column factor multiplies (A at an I step)
   int undo;                                // PK_MAT from the original: exponents include this step
   double* rmax; double* cmax;
+  int l2pol;                               // bulk-copy L2 policy: 0 normal, 1 evict_first, 2 evict_last
 };
 
 // The per-element work of the reductions runs on IEEE bit patterns: for non-negative doubles the
@@ -566,14 +568,24 @@ __device__ __forceinline__ double under_thr(int e) {
   if (t > 1023) return kInf;
   return __longlong_as_double((int64_t)(t + 1023) << 52);
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(s_u32(bar)), "r"(bytes) : "memory");
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-               ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(bar)) : "memory");
+// bulk copy global -> shared, completion counted on `bar`; pol: the L2 eviction priority of the
+// lines it reads (0 normal, 1 evict_first: not read again soon, 2 evict_last: the next pass reads
+// them again -- DESIGN.md §6.4)
+__device__ __forceinline__ void bulk_g2s_tx(void* dst, const void* src, uint32_t bytes, uint64_t* bar, int pol = 0) {
+  if (pol == 0) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                 ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(bar)) : "memory");
+    return;
+  }
+  uint64_t cp;
+  if (pol == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(cp));
+  else asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(cp));
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n"
+               ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(bar)), "l"(cp) : "memory");
 }
-__device__ __forceinline__ void bulk_g2s_tx(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-               ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(bar)) : "memory");
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, int pol = 0) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(s_u32(bar)), "r"(bytes) : "memory");
+  bulk_g2s_tx(dst, src, bytes, bar, pol);
 }
 __device__ __forceinline__ void expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(s_u32(bar)), "r"(bytes) : "memory");
@@ -611,7 +623,7 @@ __device__ __noinline__ void row_tile_tma(const MatPass& q, int tile, int* flags
   // the ring's first stages are requested before the exponent loads, so their latencies overlap
   __syncthreads();  // every warp is done with the previous tile's ring and exponents
   if (lane == 0)
-    for (int k = 0; k < CS && k < n; ++k) bulk_g2s(buf + k * CSTG, q.src + (rw + 8 * k) * q.lds + cs, bytes, bar + k);
+    for (int k = 0; k < CS && k < n; ++k) bulk_g2s(buf + k * CSTG, q.src + (rw + 8 * k) * q.lds + cs, bytes, bar + k, q.l2pol);
   if (!RAW) stage_er_nosync(q, r0, r1, sm.er);
   bool bad = false;
   double fc[16];
@@ -629,7 +641,7 @@ __device__ __noinline__ void row_tile_tma(const MatPass& q, int tile, int* flags
     ph ^= 1u << st;
 #ifdef FMM_SCALE_EXP  // development: the data movement alone (results invalid)
     __syncwarp();
-    if (lane == 0 && k + CS < n) bulk_g2s(buf + st * CSTG, q.src + (r + 8 * CS) * q.lds + cs, bytes, bar + st);
+    if (lane == 0 && k + CS < n) bulk_g2s(buf + st * CSTG, q.src + (r + 8 * CS) * q.lds + cs, bytes, bar + st, q.l2pol);
     continue;
 #endif
     double x[16];
@@ -640,7 +652,7 @@ __device__ __noinline__ void row_tile_tma(const MatPass& q, int tile, int* flags
       x[2 * h] = v.x; x[2 * h + 1] = v.y;
     }
     __syncwarp();
-    if (lane == 0 && k + CS < n) bulk_g2s(buf + st * CSTG, q.src + (r + 8 * CS) * q.lds + cs, bytes, bar + st);
+    if (lane == 0 && k + CS < n) bulk_g2s(buf + st * CSTG, q.src + (r + 8 * CS) * q.lds + cs, bytes, bar + st, q.l2pol);
     const int er = RAW ? 0 : sm.er[r - r0];
     const double thr = under_thr(er);
     double mx = 0.0;
@@ -688,8 +700,8 @@ __device__ __noinline__ void col_tile_tma(const MatPass& q, int tile, int* flags
     const int64_t ra = rw + 16 * k, rb = ra + 8;
     const uint32_t tot = rb < r1 ? 2 * bytes : bytes;
     expect_tx(bar + st, tot);
-    bulk_g2s_tx(buf + st * CSTG, q.src + ra * q.lds + cs, bytes, bar + st);
-    if (rb < r1) bulk_g2s_tx(buf + st * CSTG + 256, q.src + rb * q.lds + cs, bytes, bar + st);
+    bulk_g2s_tx(buf + st * CSTG, q.src + ra * q.lds + cs, bytes, bar + st, q.l2pol);
+    if (rb < r1) bulk_g2s_tx(buf + st * CSTG + 256, q.src + rb * q.lds + cs, bytes, bar + st, q.l2pol);
   };
   // the ring's first stages are requested before the exponent loads, so their latencies overlap
   __syncthreads();  // every warp is done with the previous tile's ring and exponents
@@ -799,7 +811,7 @@ __device__ __noinline__ void row_fused_tma(const MatPass& q, double* colmax_next
   double* ring = sm.stage;  // CS stages of FRK doubles
   __syncthreads();  // every warp is done with the previous tile's ring, exponents and red
   if (threadIdx.x == 0)
-    for (int k = 0; k < CS && k < n; ++k) bulk_g2s(ring + k * FRK, q.src + (r0 + k) * q.lds, bytes, fbar + k);
+    for (int k = 0; k < CS && k < n; ++k) bulk_g2s(ring + k * FRK, q.src + (r0 + k) * q.lds, bytes, fbar + k, q.l2pol);
   if (!RAW) stage_er_nosync(q, r0, r1, sm.er);
   bool bad = false, badx = false;
   double fc[16], cmx[16];
@@ -817,7 +829,7 @@ __device__ __noinline__ void row_fused_tma(const MatPass& q, double* colmax_next
     ph ^= 1u << st;
 #ifdef FMM_SCALE_EXP
     __syncthreads();
-    if (threadIdx.x == 0 && k + CS < n) bulk_g2s(ring + st * FRK, q.src + (r + CS) * q.lds, bytes, fbar + st);
+    if (threadIdx.x == 0 && k + CS < n) bulk_g2s(ring + st * FRK, q.src + (r + CS) * q.lds, bytes, fbar + st, q.l2pol);
     continue;
 #endif
     double y[16];
@@ -850,7 +862,7 @@ __device__ __noinline__ void row_fused_tma(const MatPass& q, double* colmax_next
     for (int o = 16; o > 0; o >>= 1) mx = max_nn(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0) red[k & 1][warp] = mx;
     __syncthreads();  // row k's maxima are in red; every warp has its values out of the stage
-    if (threadIdx.x == 0 && k + CS < n) bulk_g2s(ring + st * FRK, q.src + (r + CS) * q.lds, bytes, fbar + st);
+    if (threadIdx.x == 0 && k + CS < n) bulk_g2s(ring + st * FRK, q.src + (r + CS) * q.lds, bytes, fbar + st, q.l2pol);
     double m = red[k & 1][0];
 #pragma unroll
     for (int w = 1; w < 8; ++w) m = max_nn(m, red[k & 1][w]);
@@ -962,6 +974,10 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
   // before an O step (row maxima into pa.rmax, the values after the step's column maxima into
   // colA_next)
   auto run_pass = [&](int kind, MatPass& pa, MatPass& pb, int amode = 0, double* colA_next = nullptr) {
+    if (kind != PK_MAT && a.l2hint) {  // a fused pass keeps B in L2 for the B-only pass after it
+      pa.l2pol = amode == 2 ? 1 : 0;
+      pb.l2pol = amode == 2 ? 2 : amode == 1 ? 1 : 0;
+    }
     if (kind != PK_MAT) {  // reductions only: row or column tiles per matrix
       const int na = amode == 1 ? 0 : amode == 2 ? a.ftilesA : pa.rmax ? a.rtilesA : a.ctilesA;
       const int nbt = pb.rmax ? a.rtilesB : a.ctilesB;
@@ -1243,9 +1259,9 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
     *rows_per = rp;
     *ntiles = (int)(*segs * ((rows + rp - 1) / rp));
   };
-  auto ctiles = [&](int64_t rows, int64_t cols, int64_t* rows_per, int* strips, int* ntiles) {
+  auto ctiles = [&](int64_t rows, int64_t cols, int64_t* rows_per, int* strips, int* ntiles, int tgt) {
     *strips = (int)((cols + 255) / 256);
-    int64_t nch = std::max<int64_t>(1, nblocks / *strips);
+    int64_t nch = std::max<int64_t>(1, tgt / *strips);
     int64_t rp = (rows + nch - 1) / nch;
     rp = std::max<int64_t>(16, (rp + 15) / 16 * 16);
     *rows_per = rp;
@@ -1253,14 +1269,21 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
   };
   rtiles(M, K, &a.rrowsA, &a.rsegsA, &a.rtilesA);
   rtiles(K, N, &a.rrowsB, &a.rsegsB, &a.rtilesB);
-  ctiles(M, K, &a.crowsA, &a.cstripsA, &a.ctilesA);
-  ctiles(K, N, &a.crowsB, &a.cstripsB, &a.ctilesB);
-  // fused A pass: whole rows (K <= FRK, 16-byte aligned) in about one tile per block
-  a.frowsA = std::max<int64_t>(1, (M + nblocks - 1) / nblocks);
-  a.ftilesA = M > 0 ? (int)((M + a.frowsA - 1) / a.frowsA) : 0;
+  // fused A pass: whole rows (K <= FRK, 16-byte aligned).  In the fused schedule the A and the
+  // B column tiles of an O-reduction pass are sized for half the blocks each, so a block streams
+  // one tile per pass (one ring fill and drain) instead of two half-size ones
+  static const bool small_tiles = getenv("FMM_SCALE_BIG") && atoi(getenv("FMM_SCALE_BIG")) == 0;
+  const bool fuse_shape = pow2 && M > 0 && K > 0 && K <= FRK && K % 2 == 0 && lda % 2 == 0 &&
+                          ((uintptr_t)A & 15u) == 0;
   static const bool no_fuse = getenv("FMM_SCALE_FUSE") && atoi(getenv("FMM_SCALE_FUSE")) == 0;
-  a.fuseA = (!no_fuse && pow2 && M > 0 && K > 0 && K <= FRK && K % 2 == 0 && lda % 2 == 0 &&
-             ((uintptr_t)A & 15u) == 0 && a.frowsA <= kTmaRows) ? 1 : 0;
+  const int half = (fuse_shape && !no_fuse && !small_tiles) ? std::max(1, nblocks / 2) : nblocks;
+  ctiles(M, K, &a.crowsA, &a.cstripsA, &a.ctilesA, nblocks);
+  ctiles(K, N, &a.crowsB, &a.cstripsB, &a.ctilesB, half);
+  a.frowsA = std::max<int64_t>(1, (M + half - 1) / half);
+  a.ftilesA = M > 0 ? (int)((M + a.frowsA - 1) / a.frowsA) : 0;
+  static const bool no_hint = getenv("FMM_SCALE_L2HINT") && atoi(getenv("FMM_SCALE_L2HINT")) == 0;
+  a.l2hint = no_hint ? 0 : 1;
+  a.fuseA = (!no_fuse && fuse_shape && a.frowsA <= kTmaRows) ? 1 : 0;
   static unsigned long long* trace = nullptr;
   static const bool tracing = getenv("FMM_SCALE_TRACE") != nullptr;
   a.trace = nullptr;
