@@ -1251,9 +1251,9 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
   tiles(M, K, &a.chunkA, &a.stripsA, &a.tilesA);
   tiles(K, N, &a.chunkB, &a.stripsB, &a.tilesB);
   // reduction-only passes: about one tile per block per matrix
-  auto rtiles = [&](int64_t rows, int64_t cols, int64_t* rows_per, int* segs, int* ntiles) {
+  auto rtiles = [&](int64_t rows, int64_t cols, int64_t* rows_per, int* segs, int* ntiles, int tgt) {
     *segs = (int)((cols + RSEG - 1) / RSEG);
-    int64_t nch = std::max<int64_t>(1, nblocks / *segs);
+    int64_t nch = std::max<int64_t>(1, tgt / *segs);
     int64_t rp = (rows + nch - 1) / nch;
     rp = std::max<int64_t>(8, (rp + 7) / 8 * 8);
     *rows_per = rp;
@@ -1267,8 +1267,6 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
     *rows_per = rp;
     *ntiles = (int)(*strips * ((rows + rp - 1) / rp));
   };
-  rtiles(M, K, &a.rrowsA, &a.rsegsA, &a.rtilesA);
-  rtiles(K, N, &a.rrowsB, &a.rsegsB, &a.rtilesB);
   // fused A pass: whole rows (K <= FRK, 16-byte aligned).  In the fused schedule the A and the
   // B column tiles of an O-reduction pass are sized for half the blocks each, so a block streams
   // one tile per pass (one ring fill and drain) instead of two half-size ones
@@ -1277,6 +1275,11 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
                           ((uintptr_t)A & 15u) == 0;
   static const bool no_fuse = getenv("FMM_SCALE_FUSE") && atoi(getenv("FMM_SCALE_FUSE")) == 0;
   const int half = (fuse_shape && !no_fuse && !small_tiles) ? std::max(1, nblocks / 2) : nblocks;
+  // (an O-reduction pass the schedule does not fuse -- one-step runs, the last step -- pairs A's
+  // row tiles with the same B column tiles, so they are sized alike; B's row tiles run alone in
+  // the B-only passes)
+  rtiles(M, K, &a.rrowsA, &a.rsegsA, &a.rtilesA, half);
+  rtiles(K, N, &a.rrowsB, &a.rsegsB, &a.rtilesB, nblocks);
   ctiles(M, K, &a.crowsA, &a.cstripsA, &a.ctilesA, nblocks);
   ctiles(K, N, &a.crowsB, &a.cstripsB, &a.ctilesB, half);
   a.frowsA = std::max<int64_t>(1, (M + half - 1) / half);
