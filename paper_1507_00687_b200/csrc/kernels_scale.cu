@@ -1063,40 +1063,40 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
     for (int64_t i = gtid; i < set; i += gstride) nxt2[i] = 0.0;
     if (gtid == 0) flags[F_FAIL + ((t + 1) & 1)] = 0;
     bool ok = true, badf = false;
+    // one element per thread over rows then columns (O) or k (I); every input is loaded before
+    // the first store, so each element costs one L2 round trip, not three
     if (isO) {
-      for (int64_t i = gtid; i < M; i += gstride) {
-        double r = cur[i];
-        if (!(r > 0.0)) {
-          if (atomicCAS(&flags[F_ERR], 0, 1) == 0) flags[F_ERRIDX] = (int)i;
-          r = __longlong_as_double(0x7ff8000000000000LL);
+      for (int64_t idx = gtid; idx < M + N; idx += gstride) {
+        const bool row = idx < M;                 // r_i of A's row, else s'_j of B's column
+        const int64_t i = row ? idx : idx - M;
+        double f = row ? cur[i] : cur[M + 2 * K + i];
+        const double dold = row ? a.dA[i] : a.dB[i];
+        const int32_t eold = row ? a.exAr[i] : a.exBc[i];
+        if (!(f > 0.0)) {
+          if (atomicCAS(&flags[F_ERR], 0, row ? 1 : 2) == 0) flags[F_ERRIDX] = (int)i;
+          f = __longlong_as_double(0x7ff8000000000000LL);
         } else if (a.pow2) {
-          r = pow2_round(r);
+          f = pow2_round(f);
         }
-        a.fr[i] = r;
-        a.dA[i] = __dmul_rn(a.dA[i], r);
         double inv;
-        if (a.pow2 && exact_recip(r, &inv)) a.exAr[i] -= log2_pow2(r);
-        else badf = true;
-        ok = ok && (r >= a.lo_O);
-      }
-      for (int64_t j = gtid; j < N; j += gstride) {
-        double sv = cur[M + 2 * K + j];
-        if (!(sv > 0.0)) {
-          if (atomicCAS(&flags[F_ERR], 0, 2) == 0) flags[F_ERRIDX] = (int)j;
-          sv = __longlong_as_double(0x7ff8000000000000LL);
-        } else if (a.pow2) {
-          sv = pow2_round(sv);
+        const bool ex = a.pow2 && exact_recip(f, &inv);
+        if (!ex) badf = true;
+        if (row) {
+          a.fr[i] = f;
+          a.dA[i] = __dmul_rn(dold, f);           // D_A <- D_A r'
+          if (ex) a.exAr[i] = eold - log2_pow2(f);
+        } else {
+          a.fs[i] = f;
+          a.dB[i] = __dmul_rn(f, dold);           // D_B <- s' D_B
+          if (ex) a.exBc[i] = eold - log2_pow2(f);
         }
-        a.fs[j] = sv;
-        a.dB[j] = __dmul_rn(sv, a.dB[j]);
-        double inv;
-        if (a.pow2 && exact_recip(sv, &inv)) a.exBc[j] -= log2_pow2(sv);
-        else badf = true;
-        ok = ok && (sv >= a.lo_O);
+        ok = ok && (f >= a.lo_O);
       }
     } else {
       for (int64_t k = gtid; k < K; k += gstride) {
         const double ca = cur[M + k], rb = cur[M + K + k];
+        const double dold = a.dI[k];
+        const int32_t eac = a.exAc[k], ebr = a.exBr[k];
         double pv;
         if (!(ca > 0.0) || !(rb > 0.0)) {
           if (atomicCAS(&flags[F_ERR], 0, !(ca > 0.0) ? 3 : 4) == 0) flags[F_ERRIDX] = (int)k;
@@ -1106,12 +1106,12 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
           if (a.pow2) pv = pow2_round(pv);
         }
         a.fp[k] = pv;
-        a.dI[k] = __dmul_rn(a.dI[k], pv);
+        a.dI[k] = __dmul_rn(dold, pv);
         double inv;
         if (a.pow2 && exact_recip(pv, &inv)) {
           const int e = log2_pow2(pv);
-          a.exAc[k] += e;
-          a.exBr[k] -= e;
+          a.exAc[k] = eac + e;
+          a.exBr[k] = ebr - e;
         } else {
           badf = true;
         }
