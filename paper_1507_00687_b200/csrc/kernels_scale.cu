@@ -903,7 +903,7 @@ __device__ __noinline__ void row_fused_tma(const MatPass& q, double* colmax_next
 static_assert(CS * FRK <= 8 * CS * CSTG, "fused row ring fits the per-warp rings");
 constexpr size_t kCoopSmem = (size_t)8 * CS * CSTG * sizeof(double) + 8 * CS * sizeof(uint64_t) +
                              kTmaRows * sizeof(int32_t) + 8 * sizeof(uint32_t) +
-                             CS * sizeof(uint64_t) + 8 + 2 * 8 * sizeof(double);
+                             CS * sizeof(uint64_t) + 8 + 2 * 8 * sizeof(double) + 8 * sizeof(int);
 
 __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
   extern __shared__ __align__(128) uint8_t dsm[];
@@ -915,6 +915,7 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
   uint64_t* fbar = reinterpret_cast<uint64_t*>(tsm.phase + 8);  // fused row ring: CS mbarriers
   uint32_t* fphase = reinterpret_cast<uint32_t*>(fbar + CS);
   double (*red)[8] = reinterpret_cast<double (*)[8]>(fphase + 2);
+  int* shflags = reinterpret_cast<int*>(red + 2);  // the run's flags, as thread 0 read them
   if (threadIdx.x < 8 * CS) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s_u32(tsm.bar + threadIdx.x)));
   if (threadIdx.x < CS) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s_u32(fbar + threadIdx.x)));
   if (threadIdx.x < 8) tsm.phase[threadIdx.x] = 0;
@@ -953,9 +954,25 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
   if (gtid < 8) flags[F_EXT + gtid] = (gtid & 1) ? (-0x7fffffff - 1) : 0x7fffffff;
   gsync();
 
+  // The run's control flags after a grid barrier: thread 0 of each block reads them once (one
+  // round trip, one request per block instead of every warp's chain of dependent loads on the
+  // same words) and the block reads its copy in shared memory.
+  struct FlagView { int mode, bad, badx, stored, fail; };
+  auto read_flags = [&](const int* failp) {
+    __syncthreads();  // nobody still reads the previous copy
+    if (threadIdx.x == 0) {
+      const int m = *(volatile int*)&flags[F_MODE], b = *(volatile int*)&flags[F_BAD];
+      const int bx = *(volatile int*)&flags[F_BADX], st = *(volatile int*)&flags[F_STORED];
+      const int f = failp ? *(volatile const int*)failp : 0;
+      shflags[0] = m; shflags[1] = b; shflags[2] = bx; shflags[3] = st; shflags[4] = f;
+    }
+    __syncthreads();
+    return FlagView{shflags[0], shflags[1], shflags[2], shflags[3], shflags[4]};
+  };
+  int stored_now = 0;  // F_STORED as of the last read_flags
   auto views = [&](int isO, int kind, double* m) {  // (A part, B part) of a pass
     MatPass pa{}, pb{};
-    const bool stored = flags[F_STORED] != 0;
+    const bool stored = stored_now != 0;
     pa.src = (kind == PK_MAT && stored) ? a.Aw : a.A; pa.lds = (kind == PK_MAT && stored) ? a.ldaw : a.lda;
     pb.src = (kind == PK_MAT && stored) ? a.Bw : a.B; pb.lds = (kind == PK_MAT && stored) ? a.ldbw : a.ldb;
     pa.dst = a.Aw; pa.ldd = a.ldaw; pb.dst = a.Bw; pb.ldd = a.ldbw;
@@ -1123,12 +1140,14 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
       atomicExch(&flags[F_BAD], 1);
     gsync();
     if (gtid == 0) flags[F_STEPS] += 1;
-    const bool done = (test && *(volatile int*)fail == 0) || t == a.nsteps - 1;
+    const FlagView fv = read_flags(fail);
+    stored_now = fv.stored;
+    const bool done = (test && fv.fail == 0) || t == a.nsteps - 1;
     const bool need_next = !done;  // the values after this step feed another step
     // ---- application of step t
     const bool fusedT = fusedQ;  // step t's maxima came from a fused A pass (nxt holds colA)
     fusedQ = false;
-    if (*(volatile int*)&flags[F_MODE] == 0 && *(volatile int*)&flags[F_BAD]) {
+    if (fv.mode == 0 && fv.bad) {
       // a factor the virtual form cannot carry: materialise from the exact values before it
       if (fusedT && need_next) {  // drop the fused pass's speculative colA
         for (int64_t i = gtid; i < set; i += gstride) nxt[i] = 0.0;
@@ -1140,7 +1159,7 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
       run_pass(PK_MAT, pp.first, pp.second);
       if (gtid == 0) { flags[F_MODE] = 1; flags[F_STORED] = 1; }
       gsync();
-    } else if (*(volatile int*)&flags[F_MODE] == 0) {
+    } else if (fv.mode == 0) {
       if (need_next) {  // virtual: the next step's reductions of the values after this step
         auto pp = views(!isO, PK_VIRTUAL, nxt);
         set_max(pp.first, pp.second, !isO, nxt);
@@ -1149,7 +1168,8 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
         const int amode = fusedT ? 1 : (!isO && a.fuseA && t + 1 < a.nsteps - 1) ? 2 : 0;
         run_pass(PK_VIRTUAL, pp.first, pp.second, amode, nxt2 + M);
         gsync();
-        const bool redo = *(volatile int*)&flags[F_BAD] || (fusedT && *(volatile int*)&flags[F_BADX]);
+        const FlagView fp = read_flags(nullptr);
+        const bool redo = fp.bad || (fusedT && fp.badx);
         if (!redo && amode == 2) fusedQ = true;
         if (redo) {  // inexact intermediates: redo, materialised
           for (int64_t i = gtid; i < set; i += gstride) nxt[i] = 0.0;
