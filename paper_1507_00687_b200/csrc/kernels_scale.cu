@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <utility>
+#include <vector>
 
 #include <cooperative_groups.h>
 
@@ -930,11 +931,22 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
   cg::grid_group grid = cg::this_grid();
   int nmark = 0;
   auto gsync = [&]() {
+    if (a.trace) {  // arrival per block (a.trace is uniform over the grid)
+      __syncthreads();
+      if (threadIdx.x == 0 && nmark < 63 && blockIdx.x < 512) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[64 + nmark * 512 + blockIdx.x] = t;
+      }
+    }
     grid.sync();
-    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && nmark < 63) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-      a.trace[++nmark] = t;
+    if (a.trace && nmark < 63) {
+      ++nmark;  // every thread counts the barriers; block 0 records the release time
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        a.trace[nmark] = t;
+      }
     }
   };
   if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1298,11 +1310,17 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
   // (an O-reduction pass the schedule does not fuse -- one-step runs, the last step -- pairs A's
   // row tiles with the same B column tiles, so they are sized alike; B's row tiles run alone in
   // the B-only passes)
-  rtiles(M, K, &a.rrowsA, &a.rsegsA, &a.rtilesA, half);
-  rtiles(K, N, &a.rrowsB, &a.rsegsB, &a.rtilesB, nblocks);
+  // (the B column tiles get a share bfrac of the blocks and A's tiles exactly the blocks left:
+  // a fused A tile streams more slowly per byte -- one CTA barrier per row -- so an even split
+  // leaves the B blocks waiting at the pass's end; FMM_SCALE_TRACE=2 shows the arrivals)
+  static const double bfrac = getenv("FMM_SCALE_BFRAC") ? atof(getenv("FMM_SCALE_BFRAC")) : 0.45;
+  const int btgt = half < nblocks ? std::max(1, (int)(nblocks * bfrac)) : nblocks;
   ctiles(M, K, &a.crowsA, &a.cstripsA, &a.ctilesA, nblocks);
-  ctiles(K, N, &a.crowsB, &a.cstripsB, &a.ctilesB, half);
-  a.frowsA = std::max<int64_t>(1, (M + half - 1) / half);
+  ctiles(K, N, &a.crowsB, &a.cstripsB, &a.ctilesB, btgt);
+  const int atgt = half < nblocks ? std::max(1, nblocks - a.ctilesB) : nblocks;
+  rtiles(M, K, &a.rrowsA, &a.rsegsA, &a.rtilesA, atgt);
+  rtiles(K, N, &a.rrowsB, &a.rsegsB, &a.rtilesB, nblocks);
+  a.frowsA = std::max<int64_t>(1, (M + atgt - 1) / atgt);
   a.ftilesA = M > 0 ? (int)((M + a.frowsA - 1) / a.frowsA) : 0;
   static const bool no_hint = getenv("FMM_SCALE_L2HINT") && atoi(getenv("FMM_SCALE_L2HINT")) == 0;
   a.l2hint = no_hint ? 0 : 1;
@@ -1311,20 +1329,36 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
   static const bool tracing = getenv("FMM_SCALE_TRACE") != nullptr;
   a.trace = nullptr;
   if (tracing) {  // barrier timing (development; synchronises)
-    if (!trace) cudaMalloc(&trace, 64 * sizeof(unsigned long long));
-    cudaMemsetAsync(trace, 0, 64 * sizeof(unsigned long long), st);
+    if (!trace) cudaMalloc(&trace, (64 + 64 * 512) * sizeof(unsigned long long));
+    cudaMemsetAsync(trace, 0, (64 + 64 * 512) * sizeof(unsigned long long), st);
     a.trace = trace;
   }
   void* args[] = {&a};
   e = cudaLaunchCooperativeKernel((const void*)k_scale_coop, dim3((unsigned)nblocks), dim3(CT), args,
                                   kCoopSmem, st);
   if (tracing && e == cudaSuccess) {
-    unsigned long long h[64];
-    cudaMemcpyAsync(h, trace, sizeof h, cudaMemcpyDeviceToHost, st);
+    std::vector<unsigned long long> h(64 + 64 * 512);
+    cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     fprintf(stderr, "[scale] barriers (us from start):");
     for (int i = 1; i < 64 && h[i]; ++i) fprintf(stderr, " %.1f", (h[i] - h[0]) * 1e-3);
     fprintf(stderr, "\n");
+    if (atoi(getenv("FMM_SCALE_TRACE")) >= 2) {  // per-block arrival at each barrier
+      const int nbk = std::min(nblocks, 512);
+      for (int i = 0; i < 63 && h[i + 1]; ++i) {
+        std::vector<double> v;
+        double lo = 0, hi = 0;
+        for (int b = 0; b < nbk; ++b) {
+          const double x = (h[64 + i * 512 + b] - h[0]) * 1e-3;
+          v.push_back(x);
+          (b < nbk / 2 ? lo : hi) += x;
+        }
+        std::sort(v.begin(), v.end());
+        fprintf(stderr, "[scale]  barrier %2d arrivals: min %.1f p10 %.1f p50 %.1f p90 %.1f max %.1f | "
+                "mean blocks < %d: %.1f, >= : %.1f\n", i + 1, v[0], v[nbk / 10], v[nbk / 2],
+                v[nbk * 9 / 10], v[nbk - 1], nbk / 2, lo / (nbk / 2), hi / (nbk - nbk / 2));
+      }
+    }
   }
   return e;
 }
