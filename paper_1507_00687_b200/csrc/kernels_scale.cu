@@ -133,6 +133,12 @@ static ScaleWsView scale_ws_view(void* ws, int64_t M, int64_t K, int64_t N) {
   return v;
 }
 
+// [mx[0], flags + F_COUNT): the maxima sets, factor vectors, reciprocals and flags (contiguous)
+static void* ws_zero_begin(const ScaleWsView& v) { return v.mx[0]; }
+static size_t ws_zero_bytes(const ScaleWsView& v) {
+  return (size_t)((const char*)(v.flags + F_COUNT) - (const char*)v.mx[0]);
+}
+
 int* scale_flags_ptr(void* ws, int64_t M, int64_t K, int64_t N) {
   return scale_ws_view(ws, M, K, N).flags;
 }
@@ -957,14 +963,14 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
   int* flags = a.flags;
   const int64_t M = a.M, K = a.K, N = a.N;
   const int64_t gtid = (int64_t)blockIdx.x * CT + threadIdx.x, gstride = (int64_t)nb * CT;
-  // ---- init: factors, exponents, maxima set 0 (the launcher zeroed flags and the barrier)
+  // ---- init: factors and exponents (the launcher zeroed the three maxima sets and the flags).
+  // No barrier: the first pass (raw values) reads none of these, and the first reads of them
+  // come after that pass's barrier
   for (int64_t i = gtid; i < M; i += gstride) { a.dA[i] = 1.0; a.exAr[i] = 0; }
   for (int64_t j = gtid; j < N; j += gstride) { a.dB[j] = 1.0; a.exBc[j] = 0; }
   for (int64_t k = gtid; k < K; k += gstride) { a.dI[k] = 1.0; a.exAc[k] = 0; a.exBr[k] = 0; }
-  for (int64_t i = gtid; i < M + 2 * K + N; i += gstride) { a.mx[0][i] = 0.0; a.mx[1][i] = 0.0; a.mx[2][i] = 0.0; }
   if (gtid == 0) flags[F_MODE] = a.pow2 ? 0 : 1;
   if (gtid < 8) flags[F_EXT + gtid] = (gtid & 1) ? (-0x7fffffff - 1) : 0x7fffffff;
-  gsync();
 
   // The run's control flags after a grid barrier: thread 0 of each block reads them once (one
   // round trip, one request per block instead of every warp's chain of dependent loads on the
@@ -1147,9 +1153,13 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
         ok = ok && (pv >= a.lo_I && pv <= a.hi_I);
       }
     }
-    if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) atomicAdd(fail, 1);
-    if (__any_sync(0xffffffffu, badf) && (threadIdx.x & 31) == 0 && flags[F_MODE] == 0)
-      atomicExch(&flags[F_BAD], 1);
+    // one atomic per block, not per warp: up to 256 warps would serialise on the same word
+    // right before the barrier
+    const int blk_fail = __syncthreads_or(!ok), blk_bad = __syncthreads_or(badf);
+    if (threadIdx.x == 0) {
+      if (blk_fail) atomicAdd(fail, 1);
+      if (blk_bad && *(volatile int*)&flags[F_MODE] == 0) atomicExch(&flags[F_BAD], 1);
+    }
     gsync();
     if (gtid == 0) flags[F_STEPS] += 1;
     const FlagView fv = read_flags(fail);
@@ -1248,7 +1258,9 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
                              void* sws, cudaStream_t st) {
   ScaleWsView v = scale_ws_view(sws, M, K, N);
   cudaError_t e;
-  if ((e = cudaMemsetAsync(v.flags, 0, sizeof(int) * F_COUNT, st)) != cudaSuccess) return e;
+  // one memset zeroes the three maxima sets (the first pass combines into sets 0 and 1 with
+  // atomicMax from its first instruction on), the factor vectors and the flags
+  if ((e = cudaMemsetAsync(ws_zero_begin(v), 0, ws_zero_bytes(v), st)) != cudaSuccess) return e;
   static int blocks_per_sm = -1, sms = 0;
   if (blocks_per_sm < 0) {
     int dev = 0;
