@@ -84,6 +84,42 @@ __global__ void warp_ring(const double* x, int64_t nchunks) {
   fold(m);
 }
 
+// per-warp rings over the scaling kernel's row tiles: the buffer as 4096 rows x 8 segments of
+// 4 KB; tile = (row chunk, segment), CTA b takes tile b, warp w rows r0 + w + 8 k of it
+template <int CS>
+__global__ void warp_ring_rowtiles(const double* x, int rows, int segs, int rows_per) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* buf = reinterpret_cast<double*>(sm) + (size_t)warp * CS * 512;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + (size_t)nw * CS * 4096) + warp * CS;
+  if (lane < CS) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(s32(bar + lane)));
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncwarp();
+  const int seg = blockIdx.x % segs, r0 = (blockIdx.x / segs) * rows_per;
+  const int r1 = min(r0 + rows_per, rows);
+  const int rw = r0 + warp;
+  const int n = rw < r1 ? (r1 - rw + nw - 1) / nw : 0;
+  auto src = [&](int k) { return x + (size_t)(rw + nw * k) * segs * 512 + seg * 512; };
+  if (lane == 0)
+    for (int k = 0; k < CS && k < n; ++k) bulk(buf + k * 512, src(k), 4096, bar + k);
+  double m = 0.0;
+  uint32_t ph = 0;
+  for (int k = 0; k < n; ++k) {
+    const int st = k % CS;
+    wait(bar + st, (ph >> st) & 1u);
+    ph ^= 1u << st;
+    const double* b = buf + st * 512;
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const double2 v = *reinterpret_cast<const double2*>(b + h * 64 + 2 * lane);
+      m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+    }
+    __syncwarp();
+    if (lane == 0 && k + CS < n) bulk(buf + st * 512, src(k + CS), 4096, bar + st);
+  }
+  fold(m);
+}
+
 // CTA rings: the buffer as rows of RB bytes; CTA b takes rows b, b + G, ...
 template <int CS>
 __global__ void cta_ring(const double* x, int64_t nrows, int rb) {
@@ -165,6 +201,12 @@ int main() {
     const int smem3b = 4 * 3 * 4096 + 4 * 3 * 8;
     cudaFuncSetAttribute(warp_ring<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
     timeit("warp_ring CS3 (4 x 4 warps / SM)", [&] { warp_ring<3><<<sms * 4, 128, smem3b>>>(x, nd / 512); });
+  }
+  {
+    const int smem3 = 8 * 3 * 4096 + 8 * 3 * 8;
+    cudaFuncSetAttribute(warp_ring_rowtiles<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3);
+    // 4096 rows x 8 segments: rows_per 112 -> 37 chunks x 8 = 296 tiles (the kernel's B row tiles)
+    timeit("warp_ring row tiles (4 KB @ 32 KB)", [&] { warp_ring_rowtiles<3><<<37 * 8, 256, smem3>>>(x, 4096, 8, 112); });
   }
   for (int rb : {8192, 16384, 32768}) {
     const int smem = 3 * rb + 64;
