@@ -288,3 +288,18 @@ def test_fused_pass_fallback_at_later_step(fb, first_O):
     assert gg["steps"] == o["steps"]
     for k in ("A", "B", "dA", "dB", "dI"):
         assert np.array_equal(host(gg[k]), o[k]), k
+
+
+@pytest.mark.parametrize("M", [160000, 180000])
+def test_repeated_fused_pass_tall_bitwise(fb, M):
+    # tall A: about 1000 rows per fused tile at 160000 rows (the tile's exponents staged in
+    # shared memory hold 1024), past that the run falls back to the unfused passes; bitwise the
+    # oracle either way
+    K, N = 64, 48
+    A, B = fi.draw("skew", M, K, N, 6)
+    for first_O in (True, False):
+        g = fb.scale_repeated(dev(A), dev(B), first_O=first_O, tau=0.0, max_steps=5, pow2=True)
+        o = oracle.scale_repeated(A, B, first_O=first_O, tau=0.0, max_steps=5, pow2=True)
+        assert g["steps"] == o["steps"]
+        for k in ("A", "B", "dA", "dB", "dI"):
+            assert np.array_equal(host(g[k]), o[k]), k
