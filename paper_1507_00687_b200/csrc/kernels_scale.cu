@@ -190,6 +190,8 @@ struct CoopArgs {
   // (256-column strips x row chunks), per matrix
   int64_t rrowsA, rrowsB, crowsA, crowsB;
   int rsegsA, rsegsB, rtilesA, rtilesB, cstripsA, cstripsB, ctilesA, ctilesB;
+  // B's row tiles when they share a pass with A's column tiles (an unfused I-reduction pass)
+  int64_t rrowsBp; int rsegsBp, rtilesBp;
   // the fused A pass before an O step (row_fused_tma): whole-row tiles of frowsA rows
   int fuseA, ftilesA;
   int l2hint;  // L2 eviction-priority hints on the fused schedule's bulk copies
@@ -1015,7 +1017,8 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
     }
     if (kind != PK_MAT) {  // reductions only: row or column tiles per matrix
       const int na = amode == 1 ? 0 : amode == 2 ? a.ftilesA : pa.rmax ? a.rtilesA : a.ctilesA;
-      const int nbt = pb.rmax ? a.rtilesB : a.ctilesB;
+      const bool pairedB = na > 0 && pb.rmax != nullptr;  // B rows alongside A columns
+      const int nbt = pb.rmax ? (pairedB ? a.rtilesBp : a.rtilesB) : a.ctilesB;
       // alternate passes walk the tiles in reverse: a pass starts on the ~100 MB the previous
       // one read last, still in the 126 MB L2
       const bool rev = (npass++ & 1) != 0;
@@ -1024,8 +1027,9 @@ __global__ void __launch_bounds__(CT, 2) k_scale_coop(CoopArgs a) {
         const bool isA = t < na;
         const MatPass& q = isA ? pa : pb;
         const int tt = isA ? t : t - na;
-        const int segs = isA ? a.rsegsA : a.rsegsB, strips = isA ? a.cstripsA : a.cstripsB;
-        const int64_t rr = isA ? a.rrowsA : a.rrowsB, cr = isA ? a.crowsA : a.crowsB;
+        const int segs = isA ? a.rsegsA : pairedB ? a.rsegsBp : a.rsegsB;
+        const int strips = isA ? a.cstripsA : a.cstripsB;
+        const int64_t rr = isA ? a.rrowsA : pairedB ? a.rrowsBp : a.rrowsB, cr = isA ? a.crowsA : a.crowsB;
         // TMA staging needs 16-byte aligned rows (and whole 16-byte row segments)
         const bool tma = ((((uintptr_t)q.src) & 15u) == 0) && q.lds % 2 == 0 && q.cols % 2 == 0;
         if (isA && amode == 2) {
@@ -1327,11 +1331,12 @@ cudaError_t run_scaling_coop(int64_t M, int64_t K, int64_t N, const double* A, i
   // leaves the B blocks waiting at the pass's end; FMM_SCALE_TRACE=2 shows the arrivals)
   static const double bfrac = getenv("FMM_SCALE_BFRAC") ? atof(getenv("FMM_SCALE_BFRAC")) : 0.45;
   const int btgt = half < nblocks ? std::max(1, (int)(nblocks * bfrac)) : nblocks;
-  ctiles(M, K, &a.crowsA, &a.cstripsA, &a.ctilesA, nblocks);
+  ctiles(M, K, &a.crowsA, &a.cstripsA, &a.ctilesA, half);
   ctiles(K, N, &a.crowsB, &a.cstripsB, &a.ctilesB, btgt);
   const int atgt = half < nblocks ? std::max(1, nblocks - a.ctilesB) : nblocks;
   rtiles(M, K, &a.rrowsA, &a.rsegsA, &a.rtilesA, atgt);
   rtiles(K, N, &a.rrowsB, &a.rsegsB, &a.rtilesB, nblocks);
+  rtiles(K, N, &a.rrowsBp, &a.rsegsBp, &a.rtilesBp, half < nblocks ? std::max(1, nblocks - a.ctilesA) : nblocks);
   a.frowsA = std::max<int64_t>(1, (M + atgt - 1) / atgt);
   a.ftilesA = M > 0 ? (int)((M + a.frowsA - 1) / a.frowsA) : 0;
   static const bool no_hint = getenv("FMM_SCALE_L2HINT") && atoi(getenv("FMM_SCALE_L2HINT")) == 0;
