@@ -303,3 +303,25 @@ def test_repeated_fused_pass_tall_bitwise(fb, M):
         assert g["steps"] == o["steps"]
         for k in ("A", "B", "dA", "dB", "dI"):
             assert np.array_equal(host(g[k]), o[k]), k
+
+
+@pytest.mark.parametrize("dims", [(300, 4094, 200), (96, 2, 64), (257, 600, 300), (1100, 4096, 520)])
+def test_repeated_guard_band_bitwise(fb, dims):
+    # A and B as views into larger buffers whose padding (columns past K / N and rows past
+    # M / K) holds a huge finite sentinel: a pass that read past a row's end or the last row
+    # would change a maximum, hence the factors and the steps.  Row pitches stay even (the
+    # fused pass and the TMA rings need 16-byte aligned rows).
+    M, K, N = dims
+    A, B = fi.draw("skew", M, K, N, 7)
+    Ab = torch.full((M + 3, K + 6), 1e300, dtype=torch.float64, device="cuda")
+    Bb = torch.full((K + 3, N + 6), 1e300, dtype=torch.float64, device="cuda")
+    Ab[:M, :K] = dev(A)
+    Bb[:K, :N] = dev(B)
+    for first_O in (True, False):
+        g = fb.scale_repeated(Ab[:M, :K], Bb[:K, :N], first_O=first_O, tau=0.0, max_steps=6, pow2=True)
+        o = oracle.scale_repeated(A, B, first_O=first_O, tau=0.0, max_steps=6, pow2=True)
+        assert g["steps"] == o["steps"]
+        for k in ("A", "B", "dA", "dB", "dI"):
+            assert np.array_equal(host(g[k]), o[k]), k
+    assert bool((Ab[M:, :] == 1e300).all()) and bool((Ab[:, K:] == 1e300).all())  # inputs untouched
+    assert bool((Bb[K:, :] == 1e300).all()) and bool((Bb[:, N:] == 1e300).all())
